@@ -1,0 +1,176 @@
+"""Seeded synthetic inputs and workload descriptions shared by tests, smoke() and bench.py.
+
+This module holds NO arithmetic of the method (no layout evaluation, storage
+indexing, swizzling or copying).  It only provides
+
+  * the value generator v(x) (splitmix64, SURVEY.md §8(c) "Data generator"),
+  * the untouched-cell sentinel generator,
+  * the BASELINE.json workload descriptions as plain data: every layout is a
+    dict {"D": [(extent, stride, axis)], "R": [...], "O": {axis: value}} and
+    every storage descriptor is a dict {"digits": [(axis, extent, divisor)],
+    "swizzle": (B, M, S)}.
+
+Both the oracle (oracle/) and the product binding (paper_2601_19092_b200/)
+consume these plain tuples; neither imports the other.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+SEED_BASE = 2601190920  # seed = SEED_BASE + config number
+
+_DT = {1: np.uint8, 2: np.uint16, 4: np.uint32, 8: np.uint64}
+
+
+def _splitmix64(z: np.ndarray) -> np.ndarray:
+    z = z.astype(np.uint64, copy=True)
+    with np.errstate(over="ignore"):
+        z += GOLDEN
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return z
+
+
+def values(n: int, es: int, seed: int) -> np.ndarray:
+    """Logical tensor values v(x), x in [0, n): low 8*es bits of splitmix64(seed ^ x*phi).
+
+    Returned as a flat uint8 array of n*es bytes (raw bit patterns: random bf16/fp32
+    words include NaN/Inf/denormal encodings, so compare as integers, never floats).
+    """
+    out = np.empty(n * es, dtype=np.uint8)
+    chunk = 1 << 24
+    words = max(1, es // 8)
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        x = np.arange(s, e, dtype=np.uint64)
+        if es <= 8:
+            with np.errstate(over="ignore"):
+                h = _splitmix64(np.uint64(seed) ^ (x * GOLDEN))
+            out[s * es:e * es] = h.astype(_DT[es]).view(np.uint8)
+        else:  # 16-byte elements: two consecutive 64-bit draws
+            parts = []
+            for w in range(words):
+                with np.errstate(over="ignore"):
+                    parts.append(_splitmix64(np.uint64(seed) ^ ((x * np.uint64(words) + np.uint64(w)) * GOLDEN)))
+            out[s * es:e * es] = np.stack(parts, axis=1).reshape(-1).view(np.uint8)
+    return out
+
+
+def sentinel(nbytes: int, seed: int) -> np.ndarray:
+    """Untouched-cell sentinel bytes s(i) = splitmix64(~seed ^ i)."""
+    n8 = (nbytes + 7) // 8
+    with np.errstate(over="ignore"):
+        h = _splitmix64(np.uint64(~np.uint64(seed)) ^ (np.arange(n8, dtype=np.uint64) * GOLDEN))
+    return h.view(np.uint8)[:nbytes].copy()
+
+
+# ----------------------------------------------------------------------------
+# Plain-data helpers
+# ----------------------------------------------------------------------------
+
+def layout(D, R=(), O=None):
+    """A layout as plain data. Iters are (extent, stride, axis); axis None means "m"."""
+    fix = lambda it: (int(it[0]), int(it[1]), it[2] if len(it) > 2 and it[2] is not None else "m")
+    return {"D": [fix(i) for i in D], "R": [fix(i) for i in R], "O": dict(O or {})}
+
+
+def storage(digits, swizzle=(0, 0, 0)):
+    fix = lambda d: (d[0], int(d[1]), int(d[2]) if len(d) > 2 else 1)
+    return {"digits": [fix(d) for d in digits], "swizzle": tuple(int(v) for v in swizzle)}
+
+
+def linear_storage(n: int, swizzle=(0, 0, 0), axis="m"):
+    return storage([(axis, n, 1)], swizzle)
+
+
+def storage_cells(st) -> int:
+    n = 1
+    for _, e, _ in st["digits"]:
+        n *= e
+    return n
+
+
+SW128 = (3, 4, 3)
+SW64 = (2, 4, 3)
+SW32 = (1, 4, 3)
+
+# ----------------------------------------------------------------------------
+# BASELINE.json configs; sizes are parameters so tests can
+# scale them down while keeping their structure.
+# ----------------------------------------------------------------------------
+
+
+def config1():
+    """8x8 fp32 row-major -> (lane, warp, m) layout with replica + offset."""
+    src = layout([(8, 8), (8, 1)])
+    dst = layout([(8, 4, "lane"), (2, 1, "warp"), (2, 1, "lane"), (2, 1, "m")],
+                 [(2, 4, "warp")], {"warp": 5})
+    return dict(name="config1", es=4, src=src, src_st=linear_storage(64),
+                dst=dst, dst_st=storage([("warp", 11), ("lane", 32), ("m", 2)]), seed=SEED_BASE + 1)
+
+
+def config1_tc():
+    """The exact §2.2 tensor-core tile layout on an 8x16 fp32 tile."""
+    src = layout([(8, 16), (16, 1)])
+    dst = layout([(8, 4, "lane"), (2, 1, "warp"), (4, 1, "lane"), (2, 1, "reg")],
+                 [(2, 4, "warp")], {"warp": 5})
+    return dict(name="config1_tc", es=4, src=src, src_st=linear_storage(128),
+                dst=dst, dst_st=storage([("warp", 11), ("lane", 32), ("reg", 2)]), seed=SEED_BASE + 1)
+
+
+def config2(n: int = 4096, tile: int = 64, es: int = 2, swizzle=SW128, reverse: bool = False):
+    """n x n row-major -> (n/t, t, n/t, t):(t*n, t, t*t, 1) tiles, 128B swizzle."""
+    b = n // tile
+    rm = layout([(n, n), (n, 1)])
+    tl = layout([(b, tile * n), (tile, tile), (b, tile * tile), (tile, 1)])
+    st_rm = linear_storage(n * n)
+    st_tl = linear_storage(n * n, swizzle)
+    if reverse:
+        return dict(name="config2r", es=es, src=tl, src_st=st_tl, dst=rm, dst_st=st_rm, seed=SEED_BASE + 2)
+    return dict(name="config2", es=es, src=rm, src_st=st_rm, dst=tl, dst_st=st_tl, seed=SEED_BASE + 2)
+
+
+def _regdump_storage(tiles: int):
+    return storage([("cta", tiles), ("warp", 8), ("reg", 16, 8), ("lane", 32), ("reg", 8)])
+
+
+def config3_src(tiles: int):
+    """mma.sync m16n8k16 C-fragments of a 128x256 tile over 8 warps (2x4), warp tile 64x64."""
+    return layout([(tiles, 1, "cta"), (2, 4, "warp"), (4, 32, "reg"), (2, 2, "reg"), (8, 4, "lane"),
+                   (4, 1, "warp"), (8, 4, "reg"), (4, 1, "lane"), (2, 1, "reg")])
+
+
+def config3a_dst(tiles: int):
+    """tcgen05.ld 32x32b row-per-thread: warp = 4*wg + wq, lane = row mod 32, reg = column."""
+    return layout([(tiles, 1, "cta"), (4, 1, "warp"), (32, 1, "lane"), (2, 4, "warp"), (128, 1, "reg")])
+
+
+def config3b_dst(tiles: int):
+    """Per-8x8 transposed fragment (movmatrix.trans of every 32-bit register)."""
+    return layout([(tiles, 1, "cta"), (2, 4, "warp"), (4, 32, "reg"), (2, 2, "reg"), (4, 1, "lane"),
+                   (2, 1, "reg"), (4, 1, "warp"), (8, 4, "reg"), (4, 8, "lane"), (2, 4, "lane")])
+
+
+def config3(tiles: int = 65536, variant: str = "a"):
+    dst = config3a_dst(tiles) if variant == "a" else config3b_dst(tiles)
+    st = _regdump_storage(tiles)
+    return dict(name="config3" + variant, es=2, src=config3_src(tiles), src_st=st, dst=dst, dst_st=st,
+                seed=SEED_BASE + 3)
+
+
+def config4(P: int, n: int = 16384):
+    """n x n on a 1-D mesh: shard(dim0) -> replicate (all-gather)."""
+    src = layout([(P, 1, "gpuid"), (n // P, n), (n, 1)])
+    dst = layout([(n, n), (n, 1)], [(P, 1, "gpuid")])
+    return dict(name="config4", es=2, nranks=P, src=src, src_st=linear_storage(n // P * n),
+                dst=dst, dst_st=linear_storage(n * n), seed=SEED_BASE + 4)
+
+
+def config5(rows: int = 32768, cols: int = 8192, A: int = 2, B: int = 4):
+    """A x B mesh (gpuid = B*a + b): [S(0)@a, R@b] -> [R@a, S(1)@b]."""
+    src = layout([(A, B, "gpuid"), (rows // A, cols), (cols, 1)], [(B, 1, "gpuid")])
+    dst = layout([(rows, cols // B), (B, 1, "gpuid"), (cols // B, 1)], [(A, B, "gpuid")])
+    return dict(name="config5", es=2, nranks=A * B, src=src, src_st=linear_storage(rows // A * cols),
+                dst=dst, dst_st=linear_storage(rows * cols // B), seed=SEED_BASE + 5)
