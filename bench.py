@@ -1,0 +1,312 @@
+#!/usr/bin/env python
+"""bench.py -- layout-copy throughput of libaxe on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): a 4096x4096 bf16
+tensor, row-major -> 64x64 tiles with the 128-byte swizzle.  One step = one
+axe_copy_plan_execute (plan built outside the timed region) over one tensor.
+Inputs are resident in HBM; L2 is defeated by rotating over buffer pairs whose
+total footprint is > 4x the L2 size.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl axe|reference]
+
+N > 1 (under torchrun): every rank converts its own tensors (replicas only,
+weak scaling; the copy has no exchange step), timing is the max over ranks.
+--impl reference times the CPU oracle (oracle/) -- the only other place this
+file executes oracle code besides the cpu_baseline leg.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "layout-copy GB/s (% of HBM peak) at 1 B200"
+WORKLOAD = "config2: 4096x4096 bf16 row-major -> (64,64,64,64):(262144,64,4096,1) tiles + SW128"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("config2", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the GPU is under load."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 7 for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def dist_init(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def oracle_sample_seconds(budget_s: float, nthreads: int):
+    """Time the oracle (as it stands) on 64-row bands of the config-2 conversion until the budget is spent.
+    Returns (GB/s, bands, seconds)."""
+    import oracle
+    cfg = synth.config2()
+    n, es = 4096, 2
+    src = synth.values(n * n, es, cfg["seed"])
+    dst = np.zeros(n * n * es, np.uint8)
+    band_bytes = 64 * n * es * 2  # read + write per band
+    done, t0 = 0, time.perf_counter()
+    while True:
+        b = done % 64
+        s = {"D": [(64, n, "m"), (n, 1, "m")], "R": [], "O": {"m": b * 64 * n}}
+        d = {"D": [(64, 64, "m"), (64, 4096, "m"), (64, 1, "m")], "R": [], "O": {"m": b * 64 * n}}
+        oracle.copy(s, cfg["src_st"], src, d, cfg["dst_st"], dst, es, nthreads)
+        done += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    return done * band_bytes / el / 1e9, done, el
+
+
+def run_reference(args):
+    ws, rank, _ = dist_init(args)
+    if rank != 0:
+        return
+    import oracle
+    nthreads = os.cpu_count() or 1
+    cfg = synth.config2()
+    n, es = 4096, 2
+    src = synth.values(n * n, es, cfg["seed"])
+    dst = np.zeros(n * n * es, np.uint8)
+
+    def step(i):  # one bounded sample: one 64-row band (1/64 of the workload)
+        b = i % 64
+        s = {"D": [(64, n, "m"), (n, 1, "m")], "R": [], "O": {"m": b * 64 * n}}
+        d = {"D": [(64, 64, "m"), (64, 4096, "m"), (64, 1, "m")], "R": [], "O": {"m": b * 64 * n}}
+        oracle.copy(s, cfg["src_st"], src, d, cfg["dst_st"], dst, es, nthreads)
+
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step(i)
+    el = time.perf_counter() - t0
+    band_bytes = 64 * n * es * 2
+    v = args.steps * band_bytes / el / 1e9
+    sample = "64-row band (1/64) of the 4096^2 bf16 config-2 conversion per step"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": nthreads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_axe(args):
+    import torch
+    ws, rank, local = dist_init(args)
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2601_19092_b200 as axe
+
+    cfg = synth.config2()
+    es = cfg["es"]
+    n = 4096
+    nbytes = n * n * es
+    alg_bytes = 2 * nbytes  # es * (1 + E_R) per element, E_R = 1
+    plan = axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], es)
+    desc = plan.describe()
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    pairs = max(2, -(-4 * l2 // (2 * nbytes)))
+    g = torch.Generator(device="cuda").manual_seed(cfg["seed"] + rank)
+    srcs = [torch.randint(-2**31, 2**31 - 1, (nbytes // 4,), dtype=torch.int32, device="cuda", generator=g)
+            for _ in range(pairs)]
+    dsts = [torch.empty_like(s) for s in srcs]
+    stream = torch.cuda.current_stream()
+
+    def step(i):
+        plan.execute(srcs[i % pairs], dsts[i % pairs], stream)
+
+    for i in range(max(3, args.warmup)):
+        step(i)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    with ClockSampler(local) as clk:
+        # keep the GPU loaded long enough for the clock sampler to see the timed region's clocks
+        t_end = time.perf_counter() + 0.4
+        i = 0
+        while time.perf_counter() < t_end:
+            for _ in range(200):
+                step(i)
+                i += 1
+            torch.cuda.synchronize()
+        barrier()
+        n0 = axe.kernel_launch_count()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        ev1.record(stream)
+        barrier()
+        launches = axe.kernel_launch_count() - n0
+        ms = ev0.elapsed_time(ev1)
+        # per-launch kernel durations (events bracketing each launch, same stream)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(200)]
+        for j, (a, b) in enumerate(evs):
+            a.record(stream)
+            step(j)
+            b.record(stream)
+        torch.cuda.synchronize()
+    k_ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = ws * alg_bytes / (ms_step * 1e-3) / 1e9
+
+    # end to end through the public host-buffer call: H2D of the inputs + kernel + D2H of the result
+    hs = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    hs.copy_(srcs[0].view(torch.uint8).cpu())
+    hd = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    e_steps = max(5, min(50, args.steps))
+    for i in range(2):
+        plan.execute_host(hs, hd, srcs[0], dsts[0], stream)
+    barrier()
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(e_steps):
+        plan.execute_host(hs, hd, srcs[i % pairs], dsts[i % pairs], stream)
+    e1.record(stream)
+    barrier()
+    e_ms = e0.elapsed_time(e1) / e_steps
+    if dist:
+        t = torch.tensor([e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+    e2e = ws * alg_bytes / (e_ms * 1e-3) / 1e9
+
+    peak, peak_src = peaks()
+    achieved = alg_bytes / (k_ms * 1e-3) / 1e9
+    out = None
+    if rank == 0:
+        cpu = None
+        if ws == 1 and not args.no_cpu_baseline:
+            nthreads = os.cpu_count() or 1
+            gbs, bands, sec = oracle_sample_seconds(args.cpu_seconds, nthreads)
+            cpu = {"value": gbs, "unit": "GB/s", "cores": nthreads, "kind": "oracle",
+                   "sample": f"{bands} 64-row bands of the config-2 conversion ({sec:.1f} s)"}
+        out = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "elem": "bf16 bit patterns (bitwise copy)",
+                       "l2_defeat": f"rotating {pairs} src/dst pairs ({pairs * 2 * nbytes >> 20} MiB) > 4x L2 ({l2 >> 20} MiB)",
+                       "parallelism": f"replicas x{ws}", "kernel": desc.get("kernel"),
+                       "vec_bytes": desc.get("vec_bytes")},
+            "pct_of_peak": 100.0 * (value / ws) / peak,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": ncu_traffic(), "peak_source": peak_src,
+                         "kernel_ms": k_ms, "alg_bytes_per_launch": alg_bytes},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                    "api": "axe_copy_plan_execute_host (pinned host buffers)", "ms_per_step": e_ms},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="axe", choices=["axe", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_axe(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,248 @@
+/*
+ * axe.h -- C ABI of libaxe: Axe layouts (arXiv 2601.19092) and layout-driven
+ * tensor data movement on B200 (sm_100a).
+ *
+ * Citations: "P:<line>" = /root/reference/PAPER.md line (section / definition
+ * named beside it); "R<n>" = a reading listed in DESIGN.md §3.
+ *
+ * Conventions:
+ *   - An Axe layout L = (D, R, O) (Def. Layout) maps a logical index
+ *     x in [0, E_D) to the set f_L(x) = { f_D(x) + f_R(r) + O } of coordinates on
+ *     named axes (Def. Induced map).  D is unflattened
+ *     lexicographically, last iter fastest (R2).
+ *   - Strides and offsets on memory axes are in ELEMENTS (R3); bytes appear
+ *     only inside the swizzle.
+ *   - A tensor = layout + pointer + element size; "address = base pointer +
+ *     memory components of the layout".  Where the axes of a layout
+ *     live in a buffer is given by an axe_storage descriptor (R17).
+ *   - All calls are thread-safe; layout handles are immutable.
+ *   - Every validation happens on the host before any launch; a failing call
+ *     launches nothing and leaves every buffer untouched.
+ *   - Errors: an axe_status != AXE_OK; axe_last_error() gives a thread-local
+ *     message for the last failing call on this thread.
+ */
+#ifndef AXE_H_
+#define AXE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int axe_status;
+enum {
+  AXE_OK = 0,
+  AXE_ERR_INVALID_ARG = 1,      /* e < 1, s == 0, bad axis name, n_shard < 1, NULL pointer, bad storage */
+  AXE_ERR_OVERFLOW = 2,         /* an extent product or coordinate leaves int64            */
+  AXE_ERR_DOMAIN = 3,           /* x outside [0, E_D)                                                     */
+  AXE_ERR_CAPACITY = 4,         /* caller's output array too small                                       */
+  AXE_ERR_SIZE_MISMATCH = 5,    /* E_D(src) != E_D(dst)                                                   */
+  AXE_ERR_NONINJECTIVE = 6,     /* two different x write the same destination cell (R6)                  */
+  AXE_ERR_BOUNDS = 7,           /* a coordinate outside its storage box, or gpuid outside [0, nranks)     */
+  AXE_ERR_UNSUPPORTED_AXIS = 8, /* axis not bound by the storage descriptor; gpuid in axe_copy           */
+  AXE_ERR_ALIGNMENT = 9,        /* elem_size not in {1,2,4,8,16}; pointer misaligned for a forced plan    */
+  AXE_ERR_ALIAS = 10,           /* source and destination byte ranges overlap (no in-place)               */
+  AXE_ERR_CUDA = 11,            /* a CUDA runtime call failed (message has the CUDA error string)         */
+  AXE_ERR_NCCL = 12,            /* an NCCL call failed                                                    */
+  AXE_ERR_UNSUPPORTED = 13      /* a forced kernel cannot run this pair of layouts                        */
+};
+
+/* ------------------------------------------------------------------------- */
+/* Layouts (Defs. Iter, Layout, Induced map, span)                 */
+/* ------------------------------------------------------------------------- */
+
+typedef struct axe_layout axe_layout; /* opaque, immutable, shareable across threads */
+
+/* An iter (e, s, a): extent e >= 1, stride s != 0 on axis a (Def. Iter).
+ * axis == NULL means "m" ("if some stride is not paired with an axis, the axis m
+ * is used by default").  Axis names are identifiers [A-Za-z_][A-Za-z0-9_]*. */
+typedef struct {
+  int64_t extent;
+  int64_t stride;
+  const char *axis;
+} axe_iter;
+
+/* One component of the offset O in ZA. */
+typedef struct {
+  const char *axis;
+  int64_t value;
+} axe_axis_coord;
+
+/* Create L = (D, R, O).  shard: n_shard >= 1 iters, outermost first (D is an
+ * ordered tuple).  replica: n_replica >= 0 iters (a multiset).  offset:
+ * n_offset components; repeated axes add.  The library copies every input
+ * (strings included).  Errors: AXE_ERR_INVALID_ARG, AXE_ERR_OVERFLOW (E_D or
+ * E_R or an axis's coordinate range leaves int64). */
+axe_status axe_layout_create(const axe_iter *shard, int n_shard, const axe_iter *replica, int n_replica,
+                             const axe_axis_coord *offset, int n_offset, axe_layout **out);
+void axe_layout_destroy(axe_layout *layout);
+
+/* E_D = prod of shard extents, E_R = prod of replica extents (1 if none),
+ * n_axes = number of distinct axes (first-appearance order over D, R, O). */
+axe_status axe_layout_info(const axe_layout *layout, int64_t *E_D, int64_t *E_R, int *n_axes);
+/* Name of axis i (0 <= i < n_axes); the string lives as long as the layout. */
+axe_status axe_layout_axis_name(const axe_layout *layout, int i, const char **name);
+/* Read back the iters: which = 0 for D, 1 for R.  *n receives the count; at most
+ * capacity are written.  Axis strings live as long as the layout. */
+axe_status axe_layout_iters(const axe_layout *layout, int which, axe_iter *out, int capacity, int *n);
+/* Read back O (one entry per axis with a nonzero component). */
+axe_status axe_layout_offset(const axe_layout *layout, axe_axis_coord *out, int capacity, int *n);
+
+/* f_L(x) (Def. Induced map): writes E_R rows of n_axes int64 values,
+ * row-major, replicas in lexicographic order (last replica iter fastest; R8).
+ * capacity counts int64 values.  Errors: AXE_ERR_DOMAIN, AXE_ERR_CAPACITY. */
+axe_status axe_layout_eval(const axe_layout *layout, int64_t x, int64_t *coords, int64_t capacity);
+
+/* Canonical form (App. A.1): D0/D1 on D; C0/C1/C2 on (O, R).  The
+ * result induces the same f_L (Prop.).  *gap_ok (may be NULL)
+ * receives 1 when the canonical R satisfies the gap condition GC. */
+axe_status axe_layout_canonicalize(const axe_layout *layout, axe_layout **out, int *gap_ok);
+
+/* Signed min / max of the axis over every coordinate of every f_L(x) -- the
+ * closed form of Lemma span-closed with O included (R1).  For an
+ * axis the layout never names: min = max = 0 and AXE_OK. */
+axe_status axe_layout_bounds(const axe_layout *layout, const char *axis, int64_t *min, int64_t *max);
+
+/* ------------------------------------------------------------------------- */
+/* Storage descriptors (R16, R17)                                             */
+/* ------------------------------------------------------------------------- */
+
+/* One storage digit: the value (c[axis] / divisor) mod extent. */
+typedef struct {
+  const char *axis;
+  int64_t extent;
+  int64_t divisor;
+} axe_storage_digit;
+
+/* Element index of a coordinate c = sum_k ((c[a_k] / div_k) mod ext_k) * prod_{j>k} ext_j
+ * (digits outermost first).  The digits of one axis must form a chain: the
+ * divisor of a digit equals extent * divisor of the next (inner) digit of the
+ * same axis, and the innermost digit of an axis has divisor 1; the outermost
+ * digit of an axis bounds it: 0 <= c[a] < extent * divisor.  The buffer holds
+ * prod_k ext_k elements of elem_size bytes.  Then the byte offset b = idx *
+ * elem_size is swizzled as CUTLASS Swizzle<B, M, S> on bytes:
+ *   b' = b ^ (((b >> (M + S)) & (2^B - 1)) << M)
+ * (swz_bits = B, swz_base = M, swz_shift = S; B = 0 means no swizzle; SW128 =
+ * (3,4,3), SW64 = (2,4,3), SW32 = (1,4,3): the TMA atom swizzles of P:527).
+ * The swizzle is relative to the buffer base pointer. */
+typedef struct {
+  int n;
+  const axe_storage_digit *digits;
+  int swz_bits, swz_base, swz_shift;
+} axe_storage;
+
+/* ------------------------------------------------------------------------- */
+/* Copy on one device (copy operator, schedules chosen from layouts) */
+/* ------------------------------------------------------------------------- */
+
+/* Kernel choice for plans (flags of axe_copy_plan_create); AUTO picks from the
+ * layouts.  The environment variable AXE_FORCE_KERNEL
+ * (generic | vector | tma | tile) overrides AUTO. */
+enum {
+  AXE_KERNEL_AUTO = 0,
+  AXE_KERNEL_GENERIC = 1, /* K0: per-element evaluation of both layouts (always applicable) */
+  AXE_KERNEL_VECTOR = 2,  /* K1: joint-digit vectorised LDG/STG copy                         */
+  AXE_KERNEL_TMA = 3,     /* K1-TMA: TMA box load into swizzled smem + bulk store            */
+  AXE_KERNEL_TILE = 4     /* K2: smem-staged tile permute / transpose                        */
+};
+
+typedef struct axe_copy_plan axe_copy_plan;
+
+/* Plan a copy dst <- src (host only, no device work): validates both layouts
+ * and storages, E_D(src) == E_D(dst), bounds, destination injectivity, and
+ * chooses the kernel.  Copy semantics (R4, R6, R7): for every x, the bytes of
+ * the source cell f_D^src(x) + O^src are written to every cell of f_L^dst(x);
+ * cells of dst not in the image keep their contents; the bit pattern is moved
+ * verbatim (no floating point).  elem_size in {1, 2, 4, 8, 16}.  Layouts may
+ * not name the device axis "gpuid" (use axe_redistribute). */
+axe_status axe_copy_plan_create(const axe_layout *src, const axe_storage *src_st, const axe_layout *dst,
+                                const axe_storage *dst_st, int elem_size, int kernel, axe_copy_plan **out);
+/* Launch the planned copy on cuda_stream (a cudaStream_t; NULL = legacy default
+ * stream), asynchronously.  src_ptr / dst_ptr are DEVICE pointers to buffers
+ * of the storage sizes; the caller owns them.  Errors: AXE_ERR_ALIGNMENT (the
+ * pointers are not aligned to the plan's vector width), AXE_ERR_ALIAS,
+ * AXE_ERR_CUDA.  Launch count: 1 kernel. */
+axe_status axe_copy_plan_execute(const axe_copy_plan *plan, const void *src_ptr, void *dst_ptr, void *cuda_stream);
+/* End-to-end variant: src/dst are HOST buffers (pinned for async overlap),
+ * staged through the caller's device buffers dev_src / dev_dst (storage sizes)
+ * with cudaMemcpyAsync: H2D, copy kernel, D2H, all on cuda_stream.  Asynchronous
+ * with respect to the host. */
+axe_status axe_copy_plan_execute_host(const axe_copy_plan *plan, const void *host_src, void *host_dst,
+                                      void *dev_src, void *dev_dst, void *cuda_stream);
+/* Byte sizes of the source and destination storages. */
+axe_status axe_copy_plan_sizes(const axe_copy_plan *plan, int64_t *src_bytes, int64_t *dst_bytes);
+/* A JSON description of the plan (kernel, joint digits, vector width, grid). */
+axe_status axe_copy_plan_describe(const axe_copy_plan *plan, char *buf, int capacity);
+void axe_copy_plan_destroy(axe_copy_plan *plan);
+
+/* One-shot copy through an internal plan cache keyed by (layouts, storages,
+ * elem_size, pointer alignment).  Same semantics and errors as plan_create +
+ * plan_execute. */
+axe_status axe_copy(const axe_layout *src, const axe_storage *src_st, const void *src_ptr, const axe_layout *dst,
+                    const axe_storage *dst_st, void *dst_ptr, int elem_size, void *cuda_stream);
+
+/* ------------------------------------------------------------------------- */
+/* Redistribution across the device axis "gpuid"       */
+/* ------------------------------------------------------------------------- */
+
+typedef struct axe_comm axe_comm;
+
+/* 128-byte NCCL unique id, created on one rank and broadcast by the caller. */
+axe_status axe_get_unique_id(uint8_t out[128]);
+/* Collective over nranks processes, one device each (cuda_device). */
+axe_status axe_comm_create(const uint8_t id[128], int nranks, int rank, int cuda_device, axe_comm **out);
+void axe_comm_destroy(axe_comm *comm);
+
+typedef struct axe_redist_plan axe_redist_plan;
+
+/* Plan rank `rank`'s part of a redistribution (host only): the layouts describe
+ * the global tensor; their "gpuid" coordinate names the rank, and the storages
+ * describe the non-gpuid axes of each rank's local buffer.  Every rank must
+ * plan with identical arguments (except rank).  For each destination cell the
+ * source owner is the local rank when it holds the element, else one owner
+ * chosen to balance egress (R5). */
+axe_status axe_redist_plan_create(const axe_layout *src, const axe_storage *src_st, const axe_layout *dst,
+                                  const axe_storage *dst_st, int elem_size, int nranks, int rank,
+                                  axe_redist_plan **out);
+/* Collective launch: pack kernels, NCCL exchange over the comm, unpack kernels
+ * and the local copy, all ordered on cuda_stream. src_local/dst_local are this
+ * rank's device buffers. */
+axe_status axe_redist_plan_execute(const axe_redist_plan *plan, axe_comm *comm, const void *src_local,
+                                   void *dst_local, void *cuda_stream);
+/* JSON description: pattern (allgather / exchange / local), per-peer element
+ * counts and the kernels used. */
+axe_status axe_redist_plan_describe(const axe_redist_plan *plan, char *buf, int capacity);
+/* Host-side view of the plan for tests: for peer p, *send = elements this rank
+ * sends to p, *recv = elements it receives from p (p == rank: local copy). */
+axe_status axe_redist_plan_counts(const axe_redist_plan *plan, int peer, int64_t *send, int64_t *recv);
+/* Host-side view for tests: the k-th (k < send count) element this rank sends to
+ * peer in packed order, as (source element index in src_local storage order,
+ * destination element index in the peer's dst_local storage; -1 if the
+ * destination cell has several replicas -> first of them). */
+axe_status axe_redist_plan_send_map(const axe_redist_plan *plan, int peer, int64_t k, int64_t *src_elem,
+                                    int64_t *dst_elem);
+void axe_redist_plan_destroy(axe_redist_plan *plan);
+
+/* One-shot collective redistribute (plans through an internal cache). */
+axe_status axe_redistribute(const axe_layout *src, const axe_storage *src_st, const void *src_local,
+                            const axe_layout *dst, const axe_storage *dst_st, void *dst_local, int elem_size,
+                            axe_comm *comm, void *cuda_stream);
+
+/* Single-device emulation of a whole redistribution for tests: runs every
+ * rank's plan (plans[g] planned with rank g) on the current device, with the
+ * NCCL exchange replaced by device-to-device copies between the ranks'
+ * staging buffers.  src_locals[g] / dst_locals[g] are device buffers. */
+axe_status axe_redist_emulate(const axe_redist_plan *const *plans, int nranks, const void *const *src_locals,
+                              void *const *dst_locals, void *cuda_stream);
+
+/* ------------------------------------------------------------------------- */
+const char *axe_last_error(void);
+/* Number of kernels this library has launched in this process (all threads). */
+int64_t axe_kernel_launch_count(void);
+const char *axe_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AXE_H_ */

@@ -1,0 +1,319 @@
+"""paper_2601_19092_b200 -- thin Python binding of libaxe (include/axe.h).
+
+Argument marshalling only: every step of the data path runs inside libaxe.so
+(host planner in C++, kernels in CUDA for sm_100a).  There is no Python or CPU
+fallback: importing this package fails loudly if libaxe.so is missing.
+
+Layouts / storages are accepted as the plain-data dicts of synth.py:
+  layout  = {"D": [(extent, stride, axis)], "R": [...], "O": {axis: value}}
+  storage = {"digits": [(axis, extent, divisor)], "swizzle": (B, M, S)}
+Device buffers are torch CUDA tensors (or raw device pointers as ints).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libaxe.so")
+
+if not os.path.exists(_SO):
+    raise ImportError(f"libaxe.so not built ({_SO}); run __graft_entry__.build() or "
+                      f"python paper_2601_19092_b200/build.py")
+
+_lib = C.CDLL(_SO, mode=C.RTLD_GLOBAL)
+
+# --------------------------------------------------------------------------- C types
+AXE_OK = 0
+ERRORS = {0: "AXE_OK", 1: "AXE_ERR_INVALID_ARG", 2: "AXE_ERR_OVERFLOW", 3: "AXE_ERR_DOMAIN", 4: "AXE_ERR_CAPACITY",
+          5: "AXE_ERR_SIZE_MISMATCH", 6: "AXE_ERR_NONINJECTIVE", 7: "AXE_ERR_BOUNDS",
+          8: "AXE_ERR_UNSUPPORTED_AXIS", 9: "AXE_ERR_ALIGNMENT", 10: "AXE_ERR_ALIAS", 11: "AXE_ERR_CUDA",
+          12: "AXE_ERR_NCCL", 13: "AXE_ERR_UNSUPPORTED"}
+KERNELS = {"auto": 0, "generic": 1, "vector": 2, "tma": 3, "tile": 4}
+
+
+class axe_iter(C.Structure):
+    _fields_ = [("extent", C.c_int64), ("stride", C.c_int64), ("axis", C.c_char_p)]
+
+
+class axe_axis_coord(C.Structure):
+    _fields_ = [("axis", C.c_char_p), ("value", C.c_int64)]
+
+
+class axe_storage_digit(C.Structure):
+    _fields_ = [("axis", C.c_char_p), ("extent", C.c_int64), ("divisor", C.c_int64)]
+
+
+class axe_storage(C.Structure):
+    _fields_ = [("n", C.c_int), ("digits", C.POINTER(axe_storage_digit)), ("swz_bits", C.c_int),
+                ("swz_base", C.c_int), ("swz_shift", C.c_int)]
+
+
+_vp, _i64, _pi64 = C.c_void_p, C.c_int64, C.POINTER(C.c_int64)
+_SIGS = {
+    "axe_last_error": ([], C.c_char_p),
+    "axe_version": ([], C.c_char_p),
+    "axe_kernel_launch_count": ([], C.c_int64),
+    "axe_layout_create": ([C.POINTER(axe_iter), C.c_int, C.POINTER(axe_iter), C.c_int, C.POINTER(axe_axis_coord),
+                           C.c_int, C.POINTER(_vp)], C.c_int),
+    "axe_layout_destroy": ([_vp], None),
+    "axe_layout_info": ([_vp, _pi64, _pi64, C.POINTER(C.c_int)], C.c_int),
+    "axe_layout_axis_name": ([_vp, C.c_int, C.POINTER(C.c_char_p)], C.c_int),
+    "axe_layout_iters": ([_vp, C.c_int, C.POINTER(axe_iter), C.c_int, C.POINTER(C.c_int)], C.c_int),
+    "axe_layout_offset": ([_vp, C.POINTER(axe_axis_coord), C.c_int, C.POINTER(C.c_int)], C.c_int),
+    "axe_layout_eval": ([_vp, _i64, _pi64, _i64], C.c_int),
+    "axe_layout_canonicalize": ([_vp, C.POINTER(_vp), C.POINTER(C.c_int)], C.c_int),
+    "axe_layout_bounds": ([_vp, C.c_char_p, _pi64, _pi64], C.c_int),
+    "axe_copy_plan_create": ([_vp, C.POINTER(axe_storage), _vp, C.POINTER(axe_storage), C.c_int, C.c_int,
+                              C.POINTER(_vp)], C.c_int),
+    "axe_copy_plan_execute": ([_vp, _vp, _vp, _vp], C.c_int),
+    "axe_copy_plan_execute_host": ([_vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "axe_copy_plan_sizes": ([_vp, _pi64, _pi64], C.c_int),
+    "axe_copy_plan_describe": ([_vp, C.c_char_p, C.c_int], C.c_int),
+    "axe_copy_plan_destroy": ([_vp], None),
+    "axe_copy": ([_vp, C.POINTER(axe_storage), _vp, _vp, C.POINTER(axe_storage), _vp, C.c_int, _vp], C.c_int),
+    "axe_get_unique_id": ([C.c_char_p], C.c_int),
+    "axe_comm_create": ([C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)], C.c_int),
+    "axe_comm_destroy": ([_vp], None),
+    "axe_redist_plan_create": ([_vp, C.POINTER(axe_storage), _vp, C.POINTER(axe_storage), C.c_int, C.c_int, C.c_int,
+                                C.POINTER(_vp)], C.c_int),
+    "axe_redist_plan_execute": ([_vp, _vp, _vp, _vp, _vp], C.c_int),
+    "axe_redist_plan_describe": ([_vp, C.c_char_p, C.c_int], C.c_int),
+    "axe_redist_plan_counts": ([_vp, C.c_int, _pi64, _pi64], C.c_int),
+    "axe_redist_plan_send_map": ([_vp, C.c_int, _i64, _pi64, _pi64], C.c_int),
+    "axe_redist_plan_destroy": ([_vp], None),
+    "axe_redistribute": ([_vp, C.POINTER(axe_storage), _vp, _vp, C.POINTER(axe_storage), _vp, C.c_int, _vp, _vp],
+                         C.c_int),
+    "axe_redist_emulate": ([C.POINTER(_vp), C.c_int, C.POINTER(_vp), C.POINTER(_vp), _vp], C.c_int),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+EXPORTED = sorted(_SIGS)
+
+
+class AxeError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        self.code = code
+        self.name = ERRORS.get(code, str(code))
+        msg = _lib.axe_last_error()
+        super().__init__(f"{what}: {self.name}: {msg.decode() if msg else ''}")
+
+
+def _check(code: int, what: str):
+    if code != AXE_OK:
+        raise AxeError(code, what)
+
+
+def version() -> str:
+    return _lib.axe_version().decode()
+
+
+def kernel_launch_count() -> int:
+    return int(_lib.axe_kernel_launch_count())
+
+
+# --------------------------------------------------------------------------- marshalling
+def _iters(lst, keep):
+    arr = (axe_iter * max(1, len(lst)))()
+    for i, it in enumerate(lst):
+        e, s = int(it[0]), int(it[1])
+        a = it[2] if len(it) > 2 and it[2] is not None else "m"
+        b = a.encode()
+        keep.append(b)
+        arr[i] = axe_iter(e, s, b)
+    keep.append(arr)
+    return arr
+
+
+def make_storage(st) -> tuple:
+    """plain-data storage dict -> (axe_storage, keepalive)."""
+    keep = []
+    d = st["digits"]
+    arr = (axe_storage_digit * max(1, len(d)))()
+    for i, dg in enumerate(d):
+        b = dg[0].encode()
+        keep.append(b)
+        arr[i] = axe_storage_digit(b, int(dg[1]), int(dg[2]) if len(dg) > 2 else 1)
+    keep.append(arr)
+    sw = tuple(st.get("swizzle", (0, 0, 0)))
+    return axe_storage(len(d), arr, sw[0], sw[1], sw[2]), keep
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    if hasattr(x, "ctypes"):
+        return x.ctypes.data
+    raise TypeError(f"cannot take a pointer of {type(x)}")
+
+
+def _stream(s):
+    if s is None:
+        try:
+            import torch
+            return torch.cuda.current_stream().cuda_stream
+        except Exception:
+            return None
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream
+
+
+# --------------------------------------------------------------------------- layouts
+class Layout:
+    """An immutable Axe layout L = (D, R, O) owned by libaxe."""
+
+    def __init__(self, D=None, R=(), O=None, *, spec=None, _handle=None):
+        if _handle is not None:
+            self._h = _handle
+            return
+        if spec is not None:
+            D, R, O = spec["D"], spec.get("R", []), spec.get("O", {})
+        keep = []
+        O = dict(O or {})
+        oarr = (axe_axis_coord * max(1, len(O)))()
+        for i, (a, v) in enumerate(O.items()):
+            b = a.encode()
+            keep.append(b)
+            oarr[i] = axe_axis_coord(b, int(v))
+        h = C.c_void_p()
+        _check(_lib.axe_layout_create(_iters(list(D), keep), len(D), _iters(list(R), keep), len(R), oarr, len(O),
+                                      C.byref(h)), "axe_layout_create")
+        self._h = h
+
+    @classmethod
+    def of(cls, spec) -> "Layout":
+        return spec if isinstance(spec, Layout) else cls(spec=spec)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.axe_layout_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self):
+        ed, er, na = C.c_int64(), C.c_int64(), C.c_int()
+        _check(_lib.axe_layout_info(self._h, C.byref(ed), C.byref(er), C.byref(na)), "axe_layout_info")
+        return ed.value, er.value, na.value
+
+    @property
+    def E_D(self):
+        return self.info()[0]
+
+    @property
+    def E_R(self):
+        return self.info()[1]
+
+    def axes(self):
+        n = self.info()[2]
+        out = []
+        for i in range(n):
+            p = C.c_char_p()
+            _check(_lib.axe_layout_axis_name(self._h, i, C.byref(p)), "axe_layout_axis_name")
+            out.append(p.value.decode())
+        return out
+
+    def iters(self, which: int = 0):
+        n = C.c_int()
+        arr = (axe_iter * 64)()
+        _check(_lib.axe_layout_iters(self._h, which, arr, 64, C.byref(n)), "axe_layout_iters")
+        return [(arr[i].extent, arr[i].stride, arr[i].axis.decode()) for i in range(n.value)]
+
+    def offset(self):
+        n = C.c_int()
+        arr = (axe_axis_coord * 64)()
+        _check(_lib.axe_layout_offset(self._h, arr, 64, C.byref(n)), "axe_layout_offset")
+        return {arr[i].axis.decode(): arr[i].value for i in range(n.value)}
+
+    def spec(self):
+        return {"D": self.iters(0), "R": self.iters(1), "O": self.offset()}
+
+    def eval(self, x: int):
+        """f_L(x): list of E_R dicts {axis: value}."""
+        ed, er, na = self.info()
+        buf = (C.c_int64 * max(1, er * na))()
+        _check(_lib.axe_layout_eval(self._h, x, buf, er * na), "axe_layout_eval")
+        ax = self.axes()
+        return [{ax[i]: buf[r * na + i] for i in range(na)} for r in range(er)]
+
+    def canonicalize(self):
+        h = C.c_void_p()
+        gc = C.c_int()
+        _check(_lib.axe_layout_canonicalize(self._h, C.byref(h), C.byref(gc)), "axe_layout_canonicalize")
+        return Layout(_handle=h), bool(gc.value)
+
+    def bounds(self, axis: str):
+        lo, hi = C.c_int64(), C.c_int64()
+        _check(_lib.axe_layout_bounds(self._h, axis.encode(), C.byref(lo), C.byref(hi)), "axe_layout_bounds")
+        return lo.value, hi.value
+
+
+# --------------------------------------------------------------------------- copy
+class CopyPlan:
+    """axe_copy_plan_create / _execute / _describe (include/axe.h)."""
+
+    def __init__(self, src, src_st, dst, dst_st, elem_size: int, kernel: str = "auto"):
+        self.src, self.dst = Layout.of(src), Layout.of(dst)
+        ss, k1 = make_storage(src_st)
+        ds, k2 = make_storage(dst_st)
+        h = C.c_void_p()
+        _check(_lib.axe_copy_plan_create(self.src.handle, C.byref(ss), self.dst.handle, C.byref(ds), elem_size,
+                                         KERNELS[kernel], C.byref(h)), "axe_copy_plan_create")
+        self._h = h
+        self.elem_size = elem_size
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.axe_copy_plan_destroy(h)
+            self._h = None
+
+    def execute(self, src, dst, stream=None):
+        _check(_lib.axe_copy_plan_execute(self._h, _ptr(src), _ptr(dst), _stream(stream)), "axe_copy_plan_execute")
+
+    def execute_host(self, host_src, host_dst, dev_src, dev_dst, stream=None):
+        _check(_lib.axe_copy_plan_execute_host(self._h, _ptr(host_src), _ptr(host_dst), _ptr(dev_src), _ptr(dev_dst),
+                                               _stream(stream)), "axe_copy_plan_execute_host")
+
+    def sizes(self):
+        a, b = C.c_int64(), C.c_int64()
+        _check(_lib.axe_copy_plan_sizes(self._h, C.byref(a), C.byref(b)), "axe_copy_plan_sizes")
+        return a.value, b.value
+
+    def describe(self) -> dict:
+        buf = C.create_string_buffer(1 << 16)
+        _check(_lib.axe_copy_plan_describe(self._h, buf, len(buf)), "axe_copy_plan_describe")
+        return json.loads(buf.value.decode())
+
+
+def axe_copy(src, src_st, src_buf, dst, dst_st, dst_buf, elem_size: int, stream=None):
+    """One-shot stream-ordered copy dst <- src (include/axe.h axe_copy)."""
+    s, d = Layout.of(src), Layout.of(dst)
+    ss, k1 = make_storage(src_st)
+    ds, k2 = make_storage(dst_st)
+    _check(_lib.axe_copy(s.handle, C.byref(ss), _ptr(src_buf), d.handle, C.byref(ds), _ptr(dst_buf), elem_size,
+                         _stream(stream)), "axe_copy")
+
+
+def axe_layout_create(D, R=(), O=None) -> Layout:
+    return Layout(D, R, O)
+
+
+def axe_layout_eval(layout, x: int):
+    return Layout.of(layout).eval(x)
+
+
+def axe_copy_plan_create(src, src_st, dst, dst_st, elem_size: int, kernel: str = "auto") -> CopyPlan:
+    return CopyPlan(src, src_st, dst, dst_st, elem_size, kernel)

@@ -1,0 +1,233 @@
+// kernels.cu -- libaxe device code for sm_100a.
+//
+//   K0 generic : one thread per logical element x; evaluates f_D^src(x) + O,
+//                f_L^dst(x) and both storage maps per element (always
+//                applicable; the fallback for non-affine storage compositions
+//                and non-nested digit systems).
+//   K1 vector  : joint-digit copy: one thread per 16-byte (or
+//                narrower) vector shared by both layouts' contiguous run; one
+//                load, one swizzled store per destination replica.
+//
+// "address = base pointer + memory components of the layout"; the
+// copy operator's schedule is chosen from the two layouts.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+
+#include "kernels.cuh"
+
+namespace axe {
+
+std::atomic<int64_t> g_launches{0};
+
+// ------------------------------------------------------------------ helpers
+template <int B>
+struct VecT;
+template <>
+struct VecT<1> { using T = uint8_t; };
+template <>
+struct VecT<2> { using T = uint16_t; };
+template <>
+struct VecT<4> { using T = uint32_t; };
+template <>
+struct VecT<8> { using T = uint2; };
+template <>
+struct VecT<16> { using T = uint4; };
+
+template <int B>
+__device__ __forceinline__ typename VecT<B>::T ld_stream(const uint8_t *p) {
+  using T = typename VecT<B>::T;
+  if constexpr (B == 16) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+  } else {
+    return __ldg(reinterpret_cast<const T *>(p));
+  }
+}
+
+template <int B>
+__device__ __forceinline__ void st_vec(uint8_t *p, const typename VecT<B>::T &v) {
+  *reinterpret_cast<typename VecT<B>::T *>(p) = v;
+}
+
+// ------------------------------------------------------------------ K0
+__device__ __forceinline__ int64_t k0_storage_index(const K0Side &S, const int64_t *c) {
+  int64_t idx = 0;
+  for (int k = 0; k < S.nsd; k++) {
+    int64_t v = S.sax[k] >= 0 ? c[S.sax[k]] : 0;
+    idx = idx * S.sext[k] + (v / S.sdiv[k]) % S.sext[k];
+  }
+  return idx;
+}
+
+template <int ES>
+__global__ void __launch_bounds__(256) k0_generic(const __grid_constant__ K0Params p, const uint8_t *__restrict__ src,
+                                                  uint8_t *__restrict__ dst) {
+  using T = typename VecT<ES>::T;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < (uint64_t)p.ED; x += stride) {
+    int64_t c[K0_MAXAX];
+    // source representative f_D(x) + O (reading R4)
+    for (int i = 0; i < p.src.nax; i++) c[i] = p.src.off[i];
+    int64_t rem = (int64_t)x;
+    for (int i = p.src.nD - 1; i >= 0; i--) {
+      int64_t d = rem % p.src.e[i];
+      rem /= p.src.e[i];
+      c[p.src.ax[i]] += d * p.src.s[i];
+    }
+    int64_t sb = swz(p.src.sw, k0_storage_index(p.src, c) * ES);
+    T v = *reinterpret_cast<const T *>(src + sb);
+    // destination: every replica of f_L(x)
+    int64_t b[K0_MAXAX];
+    for (int i = 0; i < p.dst.nax; i++) b[i] = p.dst.off[i];
+    rem = (int64_t)x;
+    for (int i = p.dst.nD - 1; i >= 0; i--) {
+      int64_t d = rem % p.dst.e[i];
+      rem /= p.dst.e[i];
+      b[p.dst.ax[i]] += d * p.dst.s[i];
+    }
+    for (int64_t r = 0; r < p.ER; r++) {
+      for (int i = 0; i < p.dst.nax; i++) c[i] = b[i];
+      int64_t rr = r;
+      for (int t = p.dst.nR - 1; t >= 0; t--) {
+        int64_t d = rr % p.dst.re[t];
+        rr /= p.dst.re[t];
+        c[p.dst.rax[t]] += d * p.dst.rs[t];
+      }
+      int64_t db = swz(p.dst.sw, k0_storage_index(p.dst, c) * ES);
+      *reinterpret_cast<T *>(dst + db) = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K1
+constexpr int K1_THREADS = 256;
+
+// ND > 0: digit count known at compile time; ND == 0: runtime p.nd (<= K1_MAXD)
+template <int ND>
+__device__ __forceinline__ void k1_decode(const K1Params &p, uint32_t i, int64_t &so, int64_t &dof) {
+  so = p.sbase;
+  dof = p.dbase;
+  constexpr int TOP = ND > 0 ? ND : K1_MAXD;
+#pragma unroll
+  for (int k = TOP - 1; k >= 1; k--) {
+    if (ND == 0 && k >= p.nd) continue;
+    uint32_t q = fdiv(p.fd[k], i);
+    uint32_t d = i - q * p.fd[k].d;
+    i = q;
+    so += (int64_t)d * p.ss[k];
+    dof += (int64_t)d * p.ds[k];
+  }
+  so += (int64_t)i * p.ss[0];
+  dof += (int64_t)i * p.ds[0];
+}
+
+template <int ND, int VB, int U>
+__global__ void __launch_bounds__(K1_THREADS) k1_vector(const __grid_constant__ K1Params p,
+                                                        const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
+  using T = typename VecT<VB>::T;
+  const uint32_t total = p.total;
+  const uint32_t step = gridDim.x * (K1_THREADS * U);
+  for (uint32_t base = blockIdx.x * (K1_THREADS * U) + threadIdx.x; base < total; base += step) {
+    T v[U];
+    int64_t dof[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      uint32_t i = base + u * K1_THREADS;
+      if (i < total) {
+        int64_t so;
+        k1_decode<ND>(p, i, so, dof[u]);
+        v[u] = ld_stream<VB>(src + swz(p.ssw, so));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      uint32_t i = base + u * K1_THREADS;
+      if (i < total) {
+        for (int r = 0; r < p.nrep; r++) st_vec<VB>(dst + swz(p.dsw, dof[u] + p.rep[r]), v[u]);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+static int g_num_sms = 0;
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+      g_num_sms = n;
+    else
+      g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+cudaError_t launch_k0(const K0Params &p, const void *src, void *dst, cudaStream_t st) {
+  int64_t blocks = (p.ED + 255) / 256;
+  int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  const uint8_t *s = (const uint8_t *)src;
+  uint8_t *d = (uint8_t *)dst;
+  switch (p.es) {
+    case 1: k0_generic<1><<<(unsigned)blocks, 256, 0, st>>>(p, s, d); break;
+    case 2: k0_generic<2><<<(unsigned)blocks, 256, 0, st>>>(p, s, d); break;
+    case 4: k0_generic<4><<<(unsigned)blocks, 256, 0, st>>>(p, s, d); break;
+    case 8: k0_generic<8><<<(unsigned)blocks, 256, 0, st>>>(p, s, d); break;
+    case 16: k0_generic<16><<<(unsigned)blocks, 256, 0, st>>>(p, s, d); break;
+    default: return cudaErrorInvalidValue;
+  }
+  g_launches++;
+  return cudaGetLastError();
+}
+
+template <int ND, int VB>
+static void k1_launch_nd(const K1Params &p, unsigned blocks, const uint8_t *s, uint8_t *d, cudaStream_t st) {
+  constexpr int U = VB >= 8 ? 4 : 8;
+  k1_vector<ND, VB, U><<<blocks, K1_THREADS, 0, st>>>(p, s, d);
+}
+
+template <int VB>
+static cudaError_t k1_launch_vb(const K1Params &p, unsigned blocks, const uint8_t *s, uint8_t *d, cudaStream_t st) {
+  switch (p.nd) {
+    case 1: k1_launch_nd<1, VB>(p, blocks, s, d, st); break;
+    case 2: k1_launch_nd<2, VB>(p, blocks, s, d, st); break;
+    case 3: k1_launch_nd<3, VB>(p, blocks, s, d, st); break;
+    case 4: k1_launch_nd<4, VB>(p, blocks, s, d, st); break;
+    case 5: k1_launch_nd<5, VB>(p, blocks, s, d, st); break;
+    case 6: k1_launch_nd<6, VB>(p, blocks, s, d, st); break;
+    case 7: k1_launch_nd<7, VB>(p, blocks, s, d, st); break;
+    case 8: k1_launch_nd<8, VB>(p, blocks, s, d, st); break;
+    default:
+      if (p.nd > K1_MAXD) return cudaErrorInvalidValue;
+      k1_launch_nd<0, VB>(p, blocks, s, d, st);
+      break;
+  }
+  return cudaSuccess;
+}
+
+int k1_unroll(int vb) { return vb >= 8 ? 4 : 8; }
+
+cudaError_t launch_k1(const K1Params &p, int vb, unsigned blocks, const void *src, void *dst, cudaStream_t st) {
+  const uint8_t *s = (const uint8_t *)src;
+  uint8_t *d = (uint8_t *)dst;
+  cudaError_t e;
+  switch (vb) {
+    case 1: e = k1_launch_vb<1>(p, blocks, s, d, st); break;
+    case 2: e = k1_launch_vb<2>(p, blocks, s, d, st); break;
+    case 4: e = k1_launch_vb<4>(p, blocks, s, d, st); break;
+    case 8: e = k1_launch_vb<8>(p, blocks, s, d, st); break;
+    case 16: e = k1_launch_vb<16>(p, blocks, s, d, st); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
+  g_launches++;
+  return cudaGetLastError();
+}
+
+}  // namespace axe

@@ -1,0 +1,122 @@
+// kernels.cuh -- parameter blocks of the libaxe kernels (host <-> device).
+//
+// Every block is passed by value as a __grid_constant__ kernel parameter.
+#pragma once
+
+#include <cstdint>
+
+#ifdef __CUDACC__
+#define AXE_HD __host__ __device__ __forceinline__
+#else
+#define AXE_HD inline
+#endif
+
+namespace axe {
+
+// Unsigned 32-bit division by an invariant divisor: q = (umulhi(n, m) + n) >> l
+// (round-up multiplier; exact for every n < 2^32 and 1 <= d < 2^32).
+struct FastDiv {
+  uint32_t d, m, l;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  uint32_t l = 0;
+  while (l < 32 && (uint64_t(1) << l) < d) l++;
+  f.l = l;
+  f.m = (uint32_t)(((uint64_t(1) << 32) * ((uint64_t(1) << l) - d)) / d + 1);
+  return f;
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ uint32_t fdiv(const FastDiv &f, uint32_t n) {
+  uint32_t t = __umulhi(n, f.m);
+  return (uint32_t)(((uint64_t)t + n) >> f.l);
+}
+#endif
+
+// Byte-offset swizzle b' = b ^ (((b >> (M+S)) & mask) << M) (CUTLASS Swizzle<B,M,S>, R16).
+struct Swz {
+  uint32_t shift;  // M + S
+  uint32_t mask;   // 2^B - 1 (0: no swizzle)
+  uint32_t base;   // M
+};
+AXE_HD int64_t swz(const Swz &s, int64_t b) { return b ^ (int64_t)(((uint64_t)b >> s.shift) & s.mask) << s.base; }
+
+// ---------------------------------------------------------------- K0 generic
+constexpr int K0_MAXI = 16;   // iters per D or R
+constexpr int K0_MAXAX = 8;   // axes per side
+constexpr int K0_MAXSD = 12;  // storage digits per side
+
+struct K0Side {
+  int nD, nR, nsd, nax;
+  int64_t e[K0_MAXI], s[K0_MAXI];
+  int8_t ax[K0_MAXI];
+  int64_t re[K0_MAXI], rs[K0_MAXI];
+  int8_t rax[K0_MAXI];
+  int64_t off[K0_MAXAX];
+  int8_t sax[K0_MAXSD];  // -1: skipped axis (gpuid)
+  int64_t sext[K0_MAXSD], sdiv[K0_MAXSD];
+  Swz sw;
+};
+struct K0Params {
+  K0Side src, dst;
+  int64_t ED, ER;
+  int es;
+};
+
+// ---------------------------------------------------------------- K1 vector
+constexpr int K1_MAXD = 16;
+constexpr int K1_MAXREP = 32;
+struct K1Params {
+  uint32_t total;   // number of vectors
+  int nd;           // joint digits (vector digit excluded), outermost first
+  FastDiv fd[K1_MAXD];
+  int64_t ss[K1_MAXD], ds[K1_MAXD];  // byte strides
+  int64_t sbase, dbase;              // byte offsets of the representative cells
+  int nrep;
+  int64_t rep[K1_MAXREP];            // byte offsets of the destination replicas (rep[0] = 0)
+  Swz ssw, dsw;
+};
+
+// ---------------------------------------------------------------- K1-TMA
+// One 2-D box (rows x row_bytes) per tile; the box is TMA-loaded with the
+// destination swizzle into smem and written back with one bulk store.
+struct TmaParams {
+  uint32_t tiles;          // number of boxes
+  int nd;                  // outer digits (tile index -> coordinates)
+  FastDiv fd[K1_MAXD];
+  int64_t sc0[K1_MAXD];    // source box coordinate (inner dim, elements) per digit
+  int64_t sc1[K1_MAXD];    // source box coordinate (row dim) per digit
+  int64_t ds[K1_MAXD];     // destination byte stride per digit
+  int64_t s0, s1, dbase;
+  uint32_t box_bytes;
+};
+
+// ---------------------------------------------------------------- K2 tile
+// A tile = product of the tile digits (src-fast run x dst-fast run x ...),
+// staged through shared memory; the other digits index tiles.
+constexpr int K2_MAXD = 10;
+constexpr int K2_MAXT = 6;
+struct K2Params {
+  uint32_t tiles;                 // number of tiles
+  int nd;                         // grid digits, outermost first
+  FastDiv fd[K2_MAXD];
+  int64_t ss[K2_MAXD], ds[K2_MAXD];  // byte strides of the grid digits
+  int64_t sbase, dbase;
+  // tile digits in smem order (outermost first); element strides on each side
+  int nt;
+  FastDiv tfd[K2_MAXT];
+  int64_t tss[K2_MAXT], tds[K2_MAXT];  // byte strides (global)
+  uint32_t tsm[K2_MAXT];              // smem element strides
+  uint32_t tile_elems;
+  // load phase: vectors of lvec elements along the src-fast digit (tile digit ls)
+  // store phase: vectors of svec elements along the dst-fast digit (tile digit ds_)
+  int ls, dsd;
+  uint32_t lvec, svec;
+  int nrep;
+  int64_t rep[K1_MAXREP];
+  Swz ssw, dsw;
+  uint32_t smem_bytes;
+};
+
+}  // namespace axe

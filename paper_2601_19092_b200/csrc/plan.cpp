@@ -1,0 +1,375 @@
+// plan.cpp -- copy planning: validation, storage composition, joint digits,
+// kernel selection and parameter-table emission.
+#include "plan.hpp"
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <set>
+
+namespace axe {
+
+axe_status check_side(const Layout &L, const Storage &st, int skip_axis, const char *which) {
+  if (skip_axis < 0 && L.names_axis(axis_gpuid()))
+    AXE_FAIL(AXE_ERR_UNSUPPORTED_AXIS, "%s layout names the device axis gpuid; use axe_redistribute", which);
+  for (int a : L.axes) {
+    if (a == skip_axis) continue;
+    int64_t mn, mx;
+    axis_bounds(L, a, &mn, &mx);
+    if (!st.binds(a)) {
+      if (mn != 0 || mx != 0)
+        AXE_FAIL(AXE_ERR_UNSUPPORTED_AXIS, "%s layout uses axis %s, which its storage does not bind", which,
+                 axis_name(a));
+      continue;
+    }
+    int64_t top = st.top(a);
+    if (mn < 0 || mx >= top)
+      AXE_FAIL(AXE_ERR_BOUNDS, "%s layout reaches %s in [%lld, %lld], outside the storage box [0, %lld)", which,
+               axis_name(a), (long long)mn, (long long)mx, (long long)top);
+  }
+  if (st.swz_b > 0) {
+    // the swizzle permutes bytes inside 2^(B+M+S)-byte blocks; the buffer must hold whole blocks
+    (void)0;
+  }
+  return AXE_OK;
+}
+
+// Destination injectivity (reading R6): different x never share a cell.
+axe_status check_injective(const Layout &dst, const Storage &st, int skip_axis) {
+  Linear lin;
+  if (skip_axis < 0 && compose_linear(dst, st, skip_axis, &lin)) {
+    // fast sufficient test: sorted by |s|, each stride exceeds the reach of all
+    // smaller digits (cumulative separation, Lemma cum.)
+    std::vector<LinIter> all = lin.D;
+    all.insert(all.end(), lin.R.begin(), lin.R.end());
+    std::sort(all.begin(), all.end(), [](const LinIter &a, const LinIter &b) {
+      return (a.s < 0 ? -a.s : a.s) < (b.s < 0 ? -b.s : b.s);
+    });
+    bool ok = true;
+    int64_t reach = 0;
+    for (auto &it : all) {
+      int64_t u = it.s < 0 ? -it.s : it.s;
+      if (u <= reach) {
+        ok = false;
+        break;
+      }
+      reach += (it.e - 1) * u;
+    }
+    if (ok) return AXE_OK;
+    // exact: enumerate every (x, r) on the element index (odometer), bitmap of cells
+    int64_t work = dst.ED * dst.ER;
+    if (work > (int64_t(1) << 28) || st.cells > (int64_t(1) << 34))
+      AXE_FAIL(AXE_ERR_UNSUPPORTED, "cannot verify destination injectivity (E_D*E_R = %lld too large)",
+               (long long)work);
+    std::vector<uint64_t> seen((size_t)(st.cells / 64 + 1), 0);
+    std::vector<int64_t> reps{0};
+    for (auto &r : lin.R) {
+      std::vector<int64_t> nx;
+      for (int64_t base : reps)
+        for (int64_t d = 0; d < r.e; d++) nx.push_back(base + d * r.s);
+      reps.swap(nx);
+    }
+    std::sort(reps.begin(), reps.end());
+    reps.erase(std::unique(reps.begin(), reps.end()), reps.end());
+    std::vector<int64_t> dig(lin.D.size(), 0);
+    int64_t off = lin.base;
+    for (int64_t x = 0; x < dst.ED; x++) {
+      for (int64_t r : reps) {
+        int64_t c = off + r;
+        uint64_t m = uint64_t(1) << (c & 63);
+        if (seen[c >> 6] & m)
+          AXE_FAIL(AXE_ERR_NONINJECTIVE, "destination layout writes element %lld twice (x = %lld)", (long long)c,
+                   (long long)x);
+        seen[c >> 6] |= m;
+      }
+      for (int k = (int)lin.D.size() - 1; k >= 0; k--) {  // odometer step
+        off += lin.D[k].s;
+        if (++dig[k] < lin.D[k].e) break;
+        off -= lin.D[k].e * lin.D[k].s;
+        dig[k] = 0;
+      }
+    }
+    return AXE_OK;
+  }
+  // non-affine composition: evaluate every (x, r) on the host
+  int64_t work = dst.ED * dst.ER;
+  if (work > (int64_t(1) << 24))
+    AXE_FAIL(AXE_ERR_UNSUPPORTED, "cannot verify destination injectivity of a non-affine layout (E_D*E_R = %lld)",
+             (long long)work);
+  const int na = (int)dst.axes.size();
+  std::vector<int64_t> rows((size_t)(dst.ER * na));
+  std::vector<uint64_t> seen((size_t)(st.cells / 64 + 1), 0);
+  std::vector<int> slot(st.d.size(), -1);
+  for (size_t k = 0; k < st.d.size(); k++)
+    for (int i = 0; i < na; i++)
+      if (dst.axes[i] == st.d[k].a) slot[k] = i;
+  for (int64_t x = 0; x < dst.ED; x++) {
+    eval_layout(dst, x, rows.data());
+    std::vector<int64_t> cells;
+    for (int64_t r = 0; r < dst.ER; r++) {
+      int64_t idx = 0;
+      for (size_t k = 0; k < st.d.size(); k++) {
+        int64_t v = slot[k] >= 0 ? rows[r * na + slot[k]] : 0;
+        idx = idx * st.d[k].ext + (v / st.d[k].div) % st.d[k].ext;
+      }
+      cells.push_back(idx);
+    }
+    std::sort(cells.begin(), cells.end());
+    cells.erase(std::unique(cells.begin(), cells.end()), cells.end());
+    for (int64_t c : cells) {
+      uint64_t m = uint64_t(1) << (c & 63);
+      if (seen[c >> 6] & m)
+        AXE_FAIL(AXE_ERR_NONINJECTIVE, "destination layout writes element %lld twice (x = %lld)", (long long)c,
+                 (long long)x);
+      seen[c >> 6] |= m;
+    }
+  }
+  return AXE_OK;
+}
+
+static Swz make_swz(const Storage &st) {
+  Swz s;
+  s.shift = (uint32_t)(st.swz_m + st.swz_s);
+  s.mask = st.swz_b > 0 ? (uint32_t)((1u << st.swz_b) - 1) : 0u;
+  s.base = (uint32_t)st.swz_m;
+  return s;
+}
+
+static axe_status build_k0_side(const Layout &L, const Storage &st, int skip_axis, K0Side *S) {
+  memset(S, 0, sizeof(*S));
+  std::vector<int> ax;
+  for (int a : L.axes)
+    if (a != skip_axis) ax.push_back(a);
+  if ((int)ax.size() > K0_MAXAX) AXE_FAIL(AXE_ERR_UNSUPPORTED, "generic kernel supports <= %d axes", K0_MAXAX);
+  auto slot = [&](int a) {
+    for (size_t i = 0; i < ax.size(); i++)
+      if (ax[i] == a) return (int)i;
+    return -1;
+  };
+  S->nax = (int)ax.size();
+  for (auto &it : L.D) {
+    if (it.a == skip_axis) continue;
+    if (S->nD == K0_MAXI) AXE_FAIL(AXE_ERR_UNSUPPORTED, "generic kernel supports <= %d shard iters", K0_MAXI);
+    S->e[S->nD] = it.e;
+    S->s[S->nD] = it.s;
+    S->ax[S->nD] = (int8_t)slot(it.a);
+    S->nD++;
+  }
+  // skipped-axis iters still take part in the unflattening: keep them with stride 0 on a dummy slot
+  if (skip_axis >= 0) {
+    S->nD = 0;
+    for (auto &it : L.D) {
+      if (S->nD == K0_MAXI) AXE_FAIL(AXE_ERR_UNSUPPORTED, "generic kernel supports <= %d shard iters", K0_MAXI);
+      bool sk = it.a == skip_axis;
+      S->e[S->nD] = it.e;
+      S->s[S->nD] = sk ? 0 : it.s;
+      S->ax[S->nD] = (int8_t)(sk ? 0 : slot(it.a));
+      S->nD++;
+    }
+  }
+  for (auto &it : L.R) {
+    if (S->nR == K0_MAXI) AXE_FAIL(AXE_ERR_UNSUPPORTED, "generic kernel supports <= %d replica iters", K0_MAXI);
+    bool sk = it.a == skip_axis;
+    S->re[S->nR] = it.e;
+    S->rs[S->nR] = sk ? 0 : it.s;
+    S->rax[S->nR] = (int8_t)(sk ? 0 : slot(it.a));
+    S->nR++;
+  }
+  for (auto &p : L.O)
+    if (p.first != skip_axis) S->off[slot(p.first)] = p.second;
+  if ((int)st.d.size() > K0_MAXSD) AXE_FAIL(AXE_ERR_UNSUPPORTED, "generic kernel supports <= %d storage digits", K0_MAXSD);
+  S->nsd = (int)st.d.size();
+  for (size_t k = 0; k < st.d.size(); k++) {
+    S->sax[k] = (int8_t)slot(st.d[k].a);
+    S->sext[k] = st.d[k].ext;
+    S->sdiv[k] = st.d[k].div;
+  }
+  S->sw = make_swz(st);
+  return AXE_OK;
+}
+
+static std::string joint_json(const std::vector<Joint> &J) {
+  std::string s = "[";
+  char b[96];
+  for (size_t i = 0; i < J.size(); i++) {
+    snprintf(b, sizeof b, "%s[%lld,%lld,%lld]", i ? "," : "", (long long)J[i].e, (long long)J[i].ss,
+             (long long)J[i].ds);
+    s += b;
+  }
+  return s + "]";
+}
+
+static int env_kernel() {
+  const char *e = getenv("AXE_FORCE_KERNEL");
+  if (!e || !*e) return AXE_KERNEL_AUTO;
+  if (!strcmp(e, "generic")) return AXE_KERNEL_GENERIC;
+  if (!strcmp(e, "vector")) return AXE_KERNEL_VECTOR;
+  if (!strcmp(e, "tma")) return AXE_KERNEL_TMA;
+  if (!strcmp(e, "tile")) return AXE_KERNEL_TILE;
+  return AXE_KERNEL_AUTO;
+}
+
+static bool divides_all(int64_t v, const std::vector<int64_t> &xs) {
+  for (int64_t x : xs)
+    if (x % v) return false;
+  return true;
+}
+
+// K1: vector digit + joint digits -> parameter block.  Returns false if K1 cannot run the problem.
+static bool build_k1(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, const Storage &sst,
+                     const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why) {
+  // destination replica offsets (elements), deduplicated (set semantics)
+  std::vector<int64_t> reps{0};
+  for (auto &r : ld.R) {
+    std::vector<int64_t> nx;
+    for (int64_t b : reps)
+      for (int64_t d = 0; d < r.e; d++) nx.push_back(b + d * r.s);
+    reps.swap(nx);
+    if (reps.size() > 4096) break;
+  }
+  std::sort(reps.begin(), reps.end());
+  reps.erase(std::unique(reps.begin(), reps.end()), reps.end());
+  if ((int)reps.size() > K1_MAXREP) {
+    *why = "too many destination replicas for the vector kernel";
+    return false;
+  }
+  std::vector<Joint> J = J0;
+  // vector width V (elements): a power of two with V*es <= 16 dividing the shared
+  // innermost stride-1 run, every other stride, both bases and every replica offset
+  int64_t V = 1;
+  const Joint &in = J.back();
+  if (in.ss == 1 && in.ds == 1) {
+    std::vector<int64_t> all{ls.base, ld.base};
+    for (size_t k = 0; k + 1 < J.size(); k++) {
+      all.push_back(J[k].ss);
+      all.push_back(J[k].ds);
+    }
+    for (int64_t r : reps) all.push_back(r);
+    int64_t cap = std::min<int64_t>(16, max_align) / es;
+    if (sst.swz_b > 0) cap = std::min<int64_t>(cap, std::max<int64_t>(1, (int64_t(1) << sst.swz_m) / es));
+    if (dstst.swz_b > 0) cap = std::min<int64_t>(cap, std::max<int64_t>(1, (int64_t(1) << dstst.swz_m) / es));
+    for (int64_t v = 2; v <= cap; v *= 2)
+      if (in.e % v == 0 && divides_all(v, all)) V = v;
+  }
+  if (V > 1) {
+    Joint last = J.back();
+    J.pop_back();
+    if (last.e / V > 1) J.push_back(Joint{last.e / V, V, V});
+  }
+  std::vector<Joint> D;
+  for (auto &j : J)
+    if (j.e > 1) D.push_back(j);
+  if (D.empty()) D.push_back(Joint{1, 0, 0});
+  if ((int)D.size() > K1_MAXD) {
+    *why = "too many joint digits for the vector kernel";
+    return false;
+  }
+  int64_t total = 1;
+  for (auto &j : D) total *= j.e;
+  if (total >= (int64_t(1) << 32)) {
+    *why = "more than 2^32 vectors";
+    return false;
+  }
+  K1Params &k = P->k1;
+  memset(&k, 0, sizeof(k));
+  k.total = (uint32_t)total;
+  k.nd = (int)D.size();
+  for (int i = 0; i < k.nd; i++) {
+    k.fd[i] = make_fastdiv((uint32_t)D[i].e);
+    k.ss[i] = D[i].ss * es;
+    k.ds[i] = D[i].ds * es;
+  }
+  k.sbase = ls.base * es;
+  k.dbase = ld.base * es;
+  k.nrep = (int)reps.size();
+  for (size_t i = 0; i < reps.size(); i++) k.rep[i] = reps[i] * es;
+  k.ssw = make_swz(sst);
+  k.dsw = make_swz(dstst);
+  P->covers_all = (int64_t)reps.size() * total * V == dstst.cells;
+  P->vb = (int)(V * es);
+  P->align = std::max(P->vb, es);
+  int u = k1_unroll(P->vb);
+  int64_t blocks = (total + 256LL * u - 1) / (256LL * u);
+  int64_t cap = (int64_t)num_sms() * 8;
+  P->blocks = (unsigned)std::max<int64_t>(1, std::min(blocks, cap));
+  char b[256];
+  snprintf(b, sizeof b, "{\"kernel\":\"vector\",\"vec_bytes\":%d,\"vectors\":%lld,\"replicas\":%d,\"blocks\":%u,\"digits\":",
+           P->vb, (long long)total, k.nrep, P->blocks);
+  P->desc = std::string(b) + joint_json(D) + ",\"joint\":" + joint_json(J0) + "}";
+  return true;
+}
+
+axe_status plan_copy(const PlanRequest &rq, CopyPlan *out) {
+  const Layout &S = *rq.src, &D = *rq.dst;
+  int es = rq.es;
+  if (es != 1 && es != 2 && es != 4 && es != 8 && es != 16)
+    AXE_FAIL(AXE_ERR_ALIGNMENT, "elem_size %d not in {1,2,4,8,16}", es);
+  if (S.ED != D.ED) AXE_FAIL(AXE_ERR_SIZE_MISMATCH, "E_D(src) = %lld != E_D(dst) = %lld", (long long)S.ED, (long long)D.ED);
+  AXE_TRY(check_side(S, *rq.sst, rq.skip_axis, "source"));
+  AXE_TRY(check_side(D, *rq.dstst, rq.skip_axis, "destination"));
+  for (const Storage *st : {rq.sst, rq.dstst})
+    if (st->swz_b > 0 && (st->cells * es) % (int64_t(1) << (st->swz_b + st->swz_m + st->swz_s)))
+      AXE_FAIL(AXE_ERR_BOUNDS, "swizzled storage of %lld bytes is not a whole number of %d-byte swizzle blocks",
+               (long long)(st->cells * es), 1 << (st->swz_b + st->swz_m + st->swz_s));
+  AXE_TRY(check_injective(D, *rq.dstst, rq.skip_axis));
+
+  CopyPlan P;
+  P.es = es;
+  P.src_bytes = rq.sst->cells * es;
+  P.dst_bytes = rq.dstst->cells * es;
+  P.align = es;
+  int kernel = rq.kernel == AXE_KERNEL_AUTO ? env_kernel() : rq.kernel;
+
+  Linear ls, ld;
+  bool lin = compose_linear(S, *rq.sst, rq.skip_axis, &ls) && compose_linear(D, *rq.dstst, rq.skip_axis, &ld);
+  std::vector<Joint> J;
+  bool joint = lin && joint_refine(ls.D, ld.D, &J);
+  P.linear = joint;
+  if (joint) P.joint = J;
+
+  std::string why = lin ? (joint ? "" : "digit systems are not nested (no joint refinement)")
+                        : "storage composition is not affine";
+  if (kernel == AXE_KERNEL_AUTO || kernel == AXE_KERNEL_VECTOR || kernel == AXE_KERNEL_TILE ||
+      kernel == AXE_KERNEL_TMA) {
+    if (joint && build_k1(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &why)) {
+      P.kernel = KK_VECTOR;
+      *out = std::move(P);
+      return AXE_OK;
+    }
+    if (kernel != AXE_KERNEL_AUTO)
+      AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced kernel cannot run these layouts: %s", why.c_str());
+  }
+  // K0 generic
+  memset(&P.k0, 0, sizeof(P.k0));
+  AXE_TRY(build_k0_side(S, *rq.sst, rq.skip_axis, &P.k0.src));
+  AXE_TRY(build_k0_side(D, *rq.dstst, rq.skip_axis, &P.k0.dst));
+  P.k0.src.nR = 0;  // the source is read at its representative (reading R4)
+  P.k0.ED = D.ED;
+  P.k0.ER = D.ER;
+  P.k0.es = es;
+  P.kernel = KK_GENERIC;
+  char b[256];
+  snprintf(b, sizeof b, "{\"kernel\":\"generic\",\"elements\":%lld,\"replicas\":%lld,\"reason\":\"%s\"}",
+           (long long)D.ED, (long long)D.ER, why.c_str());
+  P.desc = b;
+  *out = std::move(P);
+  return AXE_OK;
+}
+
+axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t st) {
+  uintptr_t s = (uintptr_t)src, d = (uintptr_t)dst;
+  if (!src || !dst) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL buffer");
+  if (s % p.align || d % p.align)
+    AXE_FAIL(AXE_ERR_ALIGNMENT, "buffers must be %d-byte aligned for this plan", p.align);
+  if (s < d + p.dst_bytes && d < s + p.src_bytes) AXE_FAIL(AXE_ERR_ALIAS, "source and destination buffers overlap");
+  cudaError_t e = cudaSuccess;
+  switch (p.kernel) {
+    case KK_VECTOR: e = launch_k1(p.k1, p.vb, p.blocks, src, dst, st); break;
+    case KK_GENERIC: e = launch_k0(p.k0, src, dst, st); break;
+    default: AXE_FAIL(AXE_ERR_UNSUPPORTED, "unknown kernel");
+  }
+  if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+  return AXE_OK;
+}
+
+}  // namespace axe

@@ -1,0 +1,212 @@
+"""Host-side tests of libaxe (no GPU): the library loads and exports every symbol
+include/axe.h declares; layout creation / evaluation / bounds / canonicalisation
+agree with the independent oracle; copy planning validates and chooses kernels.
+No compute call (kernel launch) happens here."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth import layout, linear_storage, storage
+
+import paper_2601_19092_b200 as axe
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    with open(os.path.join(ROOT, "include", "axe.h")) as f:
+        txt = f.read()
+    return sorted(set(re.findall(r"^\s*(?:axe_status|void|const char \*|int64_t)\s*\*?\s*(axe_\w+)\(", txt, re.M)))
+
+
+def test_every_header_symbol_is_exported():
+    names = header_functions()
+    assert len(names) >= 25
+    lib = ctypes.CDLL(os.path.join(ROOT, "paper_2601_19092_b200", "libaxe.so"))
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(axe.EXPORTED)
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf",
+                          os.path.join(ROOT, "paper_2601_19092_b200", "libaxe.so")], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def sets(coords):
+    return sorted(sorted((a, v) for a, v in c.items() if v != 0) for c in coords)
+
+
+def rand_layout(rng, axes=("m", "lane", "warp")):
+    D = [(int(rng.integers(1, 7)), int(rng.choice([-1, 1]) * rng.integers(1, 24)), str(rng.choice(axes)))
+         for _ in range(rng.integers(1, 5))]
+    R = [(int(rng.integers(1, 4)), int(rng.choice([-1, 1]) * rng.integers(1, 24)), str(rng.choice(axes)))
+         for _ in range(rng.integers(0, 3))]
+    O = {str(a): int(rng.integers(-5, 6)) for a in rng.choice(axes, size=rng.integers(0, 3))}
+    return layout(D, R, O)
+
+
+def test_eval_matches_oracle_random():
+    rng = np.random.default_rng(1)
+    for _ in range(300):
+        spec = rand_layout(rng)
+        L = axe.Layout(spec=spec)
+        ed, er = oracle.sizes(spec)
+        assert (L.E_D, L.E_R) == (ed, er)
+        for x in range(0, ed, max(1, ed // 5)):
+            assert sets(L.eval(x)) == sets(oracle.eval(spec, x))
+
+
+def test_bounds_match_oracle_bruteforce():
+    rng = np.random.default_rng(2)
+    for _ in range(200):
+        spec = rand_layout(rng)
+        L = axe.Layout(spec=spec)
+        for a in ("m", "lane", "warp"):
+            b = oracle.bounds(spec, a)
+            assert L.bounds(a) == (b if b is not None else (0, 0))
+
+
+def test_canonicalize_preserves_map_and_is_idempotent():
+    """Prop.: D0/D1 and C0-C2 preserve f_L; the fixpoint is stable."""
+    rng = np.random.default_rng(3)
+    for _ in range(300):
+        spec = rand_layout(rng)
+        L = axe.Layout(spec=spec)
+        Cn, _ = L.canonicalize()
+        cs = Cn.spec()
+        for x in range(L.E_D):
+            assert sets(oracle.eval(cs, x)) == sets(oracle.eval(spec, x)), (spec, cs)
+        C2, _ = Cn.canonicalize()
+        assert C2.spec() == cs
+
+
+@pytest.mark.parametrize("D,exp", [
+    ([(2, 8), (8, 1)], [(16, 1, "m")]),                              # SPEC S:164 (D1)
+    ([(1, 5), (4, 1)], [(4, 1, "m")]),                               # D0
+    ([(2, 192), (8, 8), (3, 64), (8, 1)], [(2, 192, "m"), (8, 8, "m"), (3, 64, "m"), (8, 1, "m")]),
+    ([(4, 4), (2, 2), (2, 1)], [(16, 1, "m")]),                      # App. F chain
+    ([(4096, 4096), (4096, 1)], [(16777216, 1, "m")]),               # SURVEY §8(a) a2, config 2 source
+])
+def test_canonical_shard_examples(D, exp):
+    Cn, _ = axe.Layout(D).canonicalize()
+    assert Cn.iters(0) == exp
+
+
+def test_canonical_replica_examples():
+    """C1 flips a negative stride into O; C2 with q = e_i (reading R9): [(2,1),(3,2)] -> [(6,1)]."""
+    Cn, gc = axe.Layout([(2, 1)], [(3, -2)]).canonicalize()
+    assert Cn.iters(1) == [(3, 2, "m")] and Cn.offset() == {"m": -4}
+    Cn, gc = axe.Layout([(2, 100)], [(2, 1), (3, 2)]).canonicalize()
+    assert Cn.iters(1) == [(6, 1, "m")] and gc
+    Cn, gc = axe.Layout([(2, 100)], [(3, 2), (2, 3)]).canonicalize()   # GC fails: 3 <= 3*2
+    assert not gc
+
+
+def test_layout_errors():
+    with pytest.raises(axe.AxeError) as e:
+        axe.Layout([(4, 0)])
+    assert e.value.name == "AXE_ERR_INVALID_ARG"
+    with pytest.raises(axe.AxeError) as e:
+        axe.Layout([])
+    assert e.value.name == "AXE_ERR_INVALID_ARG"
+    with pytest.raises(axe.AxeError) as e:
+        axe.Layout([(4, 1, "9bad")])
+    assert e.value.name == "AXE_ERR_INVALID_ARG"
+    with pytest.raises(axe.AxeError) as e:
+        axe.Layout([(1 << 40, 1), (1 << 40, 1)])
+    assert e.value.name == "AXE_ERR_OVERFLOW"
+    with pytest.raises(axe.AxeError) as e:
+        axe.Layout([(4, 1)]).eval(4)
+    assert e.value.name == "AXE_ERR_DOMAIN"
+
+
+# --------------------------------------------------------------------------- planning
+def plan(cfg, kernel="auto"):
+    return axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], cfg["es"], kernel)
+
+
+def test_config2_plan_is_16B_vector_copy():
+    d = plan(synth.config2()).describe()
+    assert d["kernel"] == "vector" and d["vec_bytes"] == 16
+    # joint digits (64:262144|262144),(64:4096|64),(64:64|4096),(64:1|1)
+    assert d["joint"] == [[64, 262144, 262144], [64, 4096, 64], [64, 64, 4096], [64, 1, 1]]
+    assert d["vectors"] == 4096 * 4096 // 8
+
+
+def test_config1_plan():
+    d = plan(synth.config1()).describe()
+    assert d["kernel"] == "vector" and d["replicas"] == 2 and d["vec_bytes"] == 16
+
+
+def test_config3_plans_are_affine():
+    for v in "ab":
+        d = plan(synth.config3(64, v)).describe()
+        assert d["kernel"] in ("vector", "tile"), d
+
+
+def test_nonnested_falls_back_to_generic():
+    """(2,3):(1,2) vs (3,2):(1,3): suffix products {1,3,6} vs {1,2,6} are not nested (SURVEY §7 hard part 3)."""
+    src, dst = layout([(2, 1), (3, 2)]), layout([(3, 1), (2, 3)])
+    d = axe.CopyPlan(src, linear_storage(6), dst, linear_storage(6), 4).describe()
+    assert d["kernel"] == "generic"
+
+
+def test_plan_errors():
+    st = linear_storage(16)
+    cases = [
+        (layout([(16, 1)]), layout([(8, 1)]), st, "AXE_ERR_SIZE_MISMATCH"),
+        (layout([(16, 1)]), layout([(4, 1), (4, 1)]), st, "AXE_ERR_NONINJECTIVE"),
+        (layout([(16, 1)]), layout([(16, 1)], O={"m": 1}), st, "AXE_ERR_BOUNDS"),
+        (layout([(16, 1)]), layout([(16, 1, "lane")]), st, "AXE_ERR_UNSUPPORTED_AXIS"),
+        (layout([(16, 1)]), layout([(8, 1), (2, 1, "gpuid")]), st, "AXE_ERR_UNSUPPORTED_AXIS"),
+    ]
+    for s, d, dst_st, name in cases:
+        with pytest.raises(axe.AxeError) as e:
+            axe.CopyPlan(s, st, d, dst_st, 4)
+        assert e.value.name == name, (d, e.value)
+    with pytest.raises(axe.AxeError) as e:
+        axe.CopyPlan(layout([(16, 1)]), st, layout([(16, 1)]), st, 3)
+    assert e.value.name == "AXE_ERR_ALIGNMENT"
+    with pytest.raises(axe.AxeError) as e:
+        axe.CopyPlan(layout([(16, 1)]), st, layout([(16, 1)]), storage([("reg", 4, 3), ("reg", 4)]), 4)
+    assert e.value.name == "AXE_ERR_INVALID_ARG"
+
+
+def test_generic_injectivity_matches_oracle():
+    """Random destination layouts: the planner accepts exactly when the oracle's copy sees no collision."""
+    rng = np.random.default_rng(5)
+    agree = 0
+    for _ in range(300):
+        n = int(rng.integers(2, 9))
+        D = [(int(rng.integers(1, 5)), int(rng.integers(1, 12))) for _ in range(rng.integers(1, 4))]
+        R = [(int(rng.integers(1, 3)), int(rng.integers(1, 12))) for _ in range(rng.integers(0, 2))]
+        dst = layout(D, R)
+        ed, er = oracle.sizes(dst)
+        cells = 1 + sum((e - 1) * s for e, s, _ in dst["D"] + dst["R"])
+        st = linear_storage(cells)
+        src = layout([(ed, 1)])
+        v = synth.values(ed, 4, 1)
+        out = np.zeros(cells * 4, np.uint8)
+        try:
+            oracle.copy(src, linear_storage(ed), v, dst, st, out, 4)
+            ok_oracle = True
+        except oracle.OracleError as e:
+            assert e.status == "collide"
+            ok_oracle = False
+        try:
+            axe.CopyPlan(src, linear_storage(ed), dst, st, 4)
+            ok_axe = True
+        except axe.AxeError as e:
+            assert e.name == "AXE_ERR_NONINJECTIVE", e
+            ok_axe = False
+        assert ok_axe == ok_oracle, dst
+        agree += 1
+    assert agree == 300

@@ -1,0 +1,233 @@
+"""GPU parity of axe_copy against the CPU oracle (bit-exact, every byte of the
+destination buffer including cells that must stay untouched)."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth import layout, linear_storage, storage
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+NT = os.cpu_count() or 4
+
+
+@pytest.fixture(scope="module")
+def axe():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2601_19092_b200 as m
+    return m
+
+
+def to_dev(a: np.ndarray):
+    return torch.from_numpy(a).cuda()
+
+
+def prepare(cfg):
+    es = cfg["es"]
+    ed, _ = oracle.sizes(cfg["src"])
+    v = synth.values(ed, es, cfg["seed"])
+    s_fill = synth.sentinel(synth.storage_cells(cfg["src_st"]) * es, cfg["seed"] + 17)
+    src = oracle.scatter_logical(cfg["src"], cfg["src_st"], v, es, s_fill, NT)
+    d_fill = synth.sentinel(synth.storage_cells(cfg["dst_st"]) * es, cfg["seed"])
+    exp = d_fill.copy()
+    oracle.copy(cfg["src"], cfg["src_st"], src, cfg["dst"], cfg["dst_st"], exp, es, NT)
+    return src, d_fill, exp
+
+
+def run_gpu(axe, cfg, src, d_fill, kernel="auto"):
+    plan = axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], cfg["es"], kernel)
+    s = to_dev(src)
+    d = to_dev(d_fill)
+    plan.execute(s, d)
+    torch.cuda.synchronize()
+    return d.cpu().numpy(), plan.describe()
+
+
+def check(axe, cfg, kernel="auto", expect_kernel=None):
+    src, d_fill, exp = prepare(cfg)
+    got, desc = run_gpu(axe, cfg, src, d_fill, kernel)
+    if expect_kernel:
+        assert desc["kernel"] == expect_kernel, desc
+    if not np.array_equal(got, exp):
+        bad = np.nonzero(got != exp)[0]
+        raise AssertionError(f"{cfg['name']} [{desc['kernel']}]: {len(bad)} bytes differ, first at {bad[:8]}")
+    return desc
+
+
+@pytest.mark.parametrize("kernel", ["auto", "generic"])
+@pytest.mark.parametrize("mk", [synth.config1, synth.config1_tc])
+def test_config1_exhaustive(axe, mk, kernel):
+    check(axe, mk(), kernel)
+
+
+@pytest.mark.parametrize("kernel", ["auto", "generic"])
+@pytest.mark.parametrize("n,es,sw,rev", [(256, 2, synth.SW128, False), (256, 2, synth.SW128, True),
+                                        (512, 4, synth.SW64, False), (192, 8, synth.SW32, True),
+                                        (128, 1, (0, 0, 0), False)])
+def test_config2_small(axe, n, es, sw, rev, kernel):
+    check(axe, synth.config2(n, 64, es, sw, rev), kernel)
+
+
+@pytest.mark.parametrize("rev", [False, True])
+def test_config2_full(axe, rev):
+    """BASELINE config 2 at full size (4096^2 bf16) in the launch configuration bench.py times."""
+    desc = check(axe, synth.config2(reverse=rev))
+    assert desc["kernel"] in ("vector", "tma")
+
+
+@pytest.mark.parametrize("kernel", ["auto", "generic"])
+@pytest.mark.parametrize("variant", ["a", "b"])
+def test_config3_small(axe, variant, kernel):
+    check(axe, synth.config3(16, variant), kernel)
+
+
+@pytest.mark.parametrize("variant", ["a", "b"])
+def test_config3_full_sampled(axe, variant):
+    """Full 65536-tile batch (4 GiB each side); every tile's map is the same (cta stride), so sampled
+    tiles are checked against the oracle run on a one-tile problem over that tile's bytes."""
+    T = 65536
+    cfg = synth.config3(T, variant)
+    tile_bytes = 128 * 256 * 2
+    plan = axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], 2)
+    g = torch.Generator(device="cuda").manual_seed(cfg["seed"])
+    s = torch.randint(-2**31, 2**31 - 1, (T * tile_bytes // 4,), dtype=torch.int32, device="cuda", generator=g)
+    d = torch.zeros_like(s)
+    plan.execute(s, d)
+    torch.cuda.synchronize()
+    one = synth.config3(1, variant)
+    rng = np.random.default_rng(0)
+    for t in [0, 1, T - 1] + list(rng.integers(0, T, 13)):
+        t = int(t)
+        sb = s[t * tile_bytes // 4:(t + 1) * tile_bytes // 4].cpu().numpy().view(np.uint8).copy()
+        exp = np.zeros(tile_bytes, np.uint8)
+        oracle.copy(one["src"], one["src_st"], sb, one["dst"], one["dst_st"], exp, 2)
+        got = d[t * tile_bytes // 4:(t + 1) * tile_bytes // 4].cpu().numpy().view(np.uint8)
+        assert np.array_equal(got, exp), t
+    del s, d
+    torch.cuda.empty_cache()
+
+
+def test_identity_and_transpose_reduce_to_torch(axe):
+    """Special cases that reduce to library routines: identity = clone, row->column major = .t()."""
+    R, Cn = 1000, 777
+    x = torch.randint(-2**15, 2**15 - 1, (R, Cn), dtype=torch.int16, device="cuda")
+    y = torch.empty_like(x)
+    axe.axe_copy(layout([(R, Cn), (Cn, 1)]), linear_storage(R * Cn), x, layout([(R, Cn), (Cn, 1)]),
+                 linear_storage(R * Cn), y, 2)
+    torch.cuda.synchronize()
+    assert torch.equal(x, y)
+    z = torch.empty(Cn, R, dtype=torch.int16, device="cuda")
+    axe.axe_copy(layout([(R, Cn), (Cn, 1)]), linear_storage(R * Cn), x, layout([(R, 1), (Cn, R)]),
+                 linear_storage(R * Cn), z, 2)
+    torch.cuda.synchronize()
+    assert torch.equal(z, x.t().contiguous())
+
+
+def test_tiling_reduces_to_torch_permute(axe):
+    n, t = 1024, 64
+    x = torch.randint(-2**31, 2**31 - 1, (n, n), dtype=torch.int32, device="cuda")
+    y = torch.empty_like(x)
+    cfg = synth.config2(n, t, 4, (0, 0, 0))
+    axe.axe_copy(cfg["src"], cfg["src_st"], x, cfg["dst"], cfg["dst_st"], y, 4)
+    torch.cuda.synchronize()
+    assert torch.equal(y.view(-1), x.view(n // t, t, n // t, t).permute(0, 2, 1, 3).contiguous().view(-1))
+
+
+def rand_injective(rng, N_exts, allow_neg=True, reps=True):
+    """A random injective layout over extents N_exts on axis m: a mixed radix in random order with gaps,
+    optional negative strides (offset compensates) and replicas beyond the shard span."""
+    n = len(N_exts)
+    order = rng.permutation(n)
+    strides = [0] * n
+    cur = 1
+    for i in order:
+        strides[i] = cur
+        cur *= N_exts[i] * int(rng.choice([1, 1, 1, 2]))
+    O = 0
+    D = []
+    for i in range(n):
+        s = strides[i]
+        if allow_neg and rng.random() < 0.2:
+            O += (N_exts[i] - 1) * s
+            s = -s
+        D.append((N_exts[i], s))
+    R = []
+    if reps and rng.random() < 0.4:
+        e = int(rng.integers(2, 4))
+        R.append((e, cur))
+        cur *= e
+    return layout(D, R, {"m": O} if O else {}), cur
+
+
+def random_split(rng, N):
+    exts = []
+    while N > 1:
+        for f in (2, 3, 4, 5, 8):
+            if N % f == 0 and rng.random() < 0.5:
+                exts.append(f)
+                N //= f
+                break
+        else:
+            exts.append(N)
+            N = 1
+    return exts or [1]
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_layout_pairs(axe, seed):
+    """Brute force on small random pairs: every kernel the planner can pick, and the generic kernel."""
+    rng = np.random.default_rng(1000 + seed)
+    N = int(rng.choice([64, 96, 120, 256, 360, 512, 1024]))
+    es = int(rng.choice([1, 2, 4, 8, 16]))
+    src, sc = rand_injective(rng, random_split(rng, N), reps=False)
+    dst, dc = rand_injective(rng, random_split(rng, N))
+    sw = (0, 0, 0)
+    if rng.random() < 0.3 and (dc * es) % 1024 == 0:
+        sw = synth.SW128
+    cfg = dict(name=f"rand{seed}", es=es, src=src, src_st=linear_storage(sc), dst=dst,
+               dst_st=linear_storage(dc, sw), seed=seed)
+    check(axe, cfg, "auto")
+    check(axe, cfg, "generic")
+
+
+def test_alias_and_alignment_errors(axe):
+    x = torch.zeros(1024, dtype=torch.int32, device="cuda")
+    L = layout([(512, 1)])
+    st = linear_storage(512)
+    with pytest.raises(axe.AxeError) as e:
+        axe.axe_copy(L, st, x, L, st, x[256:], 4)
+    assert e.value.name == "AXE_ERR_ALIAS"
+    plan = axe.CopyPlan(L, st, L, st, 4)
+    with pytest.raises(axe.AxeError) as e:
+        plan.execute(x[1:], x[600:])     # 4-byte offset breaks the 16-byte vector plan
+    assert e.value.name == "AXE_ERR_ALIGNMENT"
+    y = torch.zeros(1100, dtype=torch.int32, device="cuda")
+    axe.axe_copy(L, st, x[1:], L, st, y[3:], 4)     # the cached path re-plans for 4-byte alignment
+    torch.cuda.synchronize()
+    assert torch.equal(y[3:515], x[1:513])
+
+
+def test_launch_counter(axe):
+    x = torch.zeros(4096, dtype=torch.int16, device="cuda")
+    y = torch.zeros_like(x)
+    n0 = axe.kernel_launch_count()
+    for _ in range(3):
+        axe.axe_copy(layout([(4096, 1)]), linear_storage(4096), x, layout([(4096, 1)]), linear_storage(4096), y, 2)
+    assert axe.kernel_launch_count() - n0 == 3
+
+
+def test_execute_host_e2e(axe):
+    cfg = synth.config2(512, 64)
+    src, d_fill, exp = prepare(cfg)
+    plan = axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], 2)
+    hs = torch.from_numpy(src).pin_memory()
+    hd = torch.from_numpy(d_fill.copy()).pin_memory()
+    ds = torch.empty(src.nbytes, dtype=torch.uint8, device="cuda")
+    dd = torch.empty(d_fill.nbytes, dtype=torch.uint8, device="cuda")
+    plan.execute_host(hs, hd, ds, dd)
+    torch.cuda.synchronize()
+    assert np.array_equal(hd.numpy(), exp)
