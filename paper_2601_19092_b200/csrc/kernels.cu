@@ -154,6 +154,53 @@ __global__ void __launch_bounds__(K1_THREADS) k1_vector(const __grid_constant__ 
   }
 }
 
+// Tiled K1: the per-thread part of the digit decode (and the swizzle, when the
+// tile bases are whole swizzle blocks) is done once; each tile then costs one
+// uniform base decode, U loads and U * nrep stores per thread.
+__device__ __forceinline__ void decode_digits(int n, const FastDiv *fd, const int64_t *a, const int64_t *b, uint32_t i,
+                                              int64_t &oa, int64_t &ob) {
+#pragma unroll
+  for (int k = K1_MAXD - 1; k >= 1; k--) {
+    if (k >= n) continue;
+    uint32_t q = fdiv(fd[k], i);
+    uint32_t d = i - q * fd[k].d;
+    i = q;
+    oa += (int64_t)d * a[k];
+    ob += (int64_t)d * b[k];
+  }
+  if (n > 0) {
+    oa += (int64_t)i * a[0];
+    ob += (int64_t)i * b[0];
+  }
+}
+
+template <int VB, int U>
+__global__ void __launch_bounds__(K1_THREADS) k1_tiled(const __grid_constant__ K1Params p, const uint8_t *__restrict__ src,
+                                                       uint8_t *__restrict__ dst) {
+  using T = typename VecT<VB>::T;
+  int64_t so[U], dof[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    so[u] = 0;
+    dof[u] = 0;
+    decode_digits(p.nin, p.ifd, p.iss, p.ids, threadIdx.x + u * K1_THREADS, so[u], dof[u]);
+    if (p.pre_s) so[u] = swz(p.ssw, so[u]);
+    if (p.pre_d) dof[u] = swz(p.dsw, dof[u]);
+  }
+  for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+    int64_t sb = p.sbase, db = p.dbase;
+    decode_digits(p.nout, p.ofd, p.oss, p.ods, t, sb, db);
+    T v[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) v[u] = ld_stream<VB>(src + (p.pre_s ? sb + so[u] : swz(p.ssw, sb + so[u])));
+    for (int r = 0; r < p.nrep; r++) {
+      const int64_t b = db + p.rep[r];
+#pragma unroll
+      for (int u = 0; u < U; u++) st_vec<VB>(dst + (p.pre_d ? b + dof[u] : swz(p.dsw, b + dof[u])), v[u]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ launchers
 static int g_num_sms = 0;
 int num_sms() {
@@ -213,10 +260,28 @@ static cudaError_t k1_launch_vb(const K1Params &p, unsigned blocks, const uint8_
 
 int k1_unroll(int vb) { return vb >= 8 ? 4 : 8; }
 
+template <int VB>
+static void k1_tiled_launch(const K1Params &p, unsigned blocks, const uint8_t *s, uint8_t *d, cudaStream_t st) {
+  constexpr int U = VB >= 8 ? 4 : 8;
+  k1_tiled<VB, U><<<blocks, K1_THREADS, 0, st>>>(p, s, d);
+}
+
 cudaError_t launch_k1(const K1Params &p, int vb, unsigned blocks, const void *src, void *dst, cudaStream_t st) {
   const uint8_t *s = (const uint8_t *)src;
   uint8_t *d = (uint8_t *)dst;
-  cudaError_t e;
+  cudaError_t e = cudaSuccess;
+  if (p.tile_v > 0) {
+    switch (vb) {
+      case 1: k1_tiled_launch<1>(p, blocks, s, d, st); break;
+      case 2: k1_tiled_launch<2>(p, blocks, s, d, st); break;
+      case 4: k1_tiled_launch<4>(p, blocks, s, d, st); break;
+      case 8: k1_tiled_launch<8>(p, blocks, s, d, st); break;
+      case 16: k1_tiled_launch<16>(p, blocks, s, d, st); break;
+      default: return cudaErrorInvalidValue;
+    }
+    g_launches++;
+    return cudaGetLastError();
+  }
   switch (vb) {
     case 1: e = k1_launch_vb<1>(p, blocks, s, d, st); break;
     case 2: e = k1_launch_vb<2>(p, blocks, s, d, st); break;

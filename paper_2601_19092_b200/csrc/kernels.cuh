@@ -69,27 +69,43 @@ constexpr int K1_MAXD = 16;
 constexpr int K1_MAXREP = 32;
 struct K1Params {
   uint32_t total;   // number of vectors
-  int nd;           // joint digits (vector digit excluded), outermost first
+  int nd;           // joint digits (vector digit excluded) in kernel order, outermost first
   FastDiv fd[K1_MAXD];
   int64_t ss[K1_MAXD], ds[K1_MAXD];  // byte strides
   int64_t sbase, dbase;              // byte offsets of the representative cells
   int nrep;
   int64_t rep[K1_MAXREP];            // byte offsets of the destination replicas (rep[0] = 0)
   Swz ssw, dsw;
+  // tiled mode (tile_v > 0): vectors [t*tile_v, (t+1)*tile_v) form tile t; the
+  // inner digits give every thread fixed offsets, the outer digits a tile base.
+  uint32_t tile_v, ntiles;
+  int nin, nout;
+  FastDiv ifd[K1_MAXD], ofd[K1_MAXD];
+  int64_t iss[K1_MAXD], ids[K1_MAXD], oss[K1_MAXD], ods[K1_MAXD];
+  int pre_s, pre_d;  // swizzle folded into the per-thread offsets (tile bases are whole swizzle blocks)
 };
 
 // ---------------------------------------------------------------- K1-TMA
-// One 2-D box (rows x row_bytes) per tile; the box is TMA-loaded with the
-// destination swizzle into smem and written back with one bulk store.
+// The paper's TMA lowering: every box is (rows x row bytes), whole
+// in shared memory; one side is addressed through a CUtensorMap (5-D, byte
+// elements, the other side's swizzle applied in smem), the other side is a
+// contiguous run of box_bytes moved with one bulk copy.
+//   mode 0: TMA tensor load (src)  -> smem -> bulk store (dst, every replica)
+//   mode 1: bulk load (src)        -> smem -> TMA tensor store (dst)
+constexpr int TMA_MAXD = 6;
 struct TmaParams {
-  uint32_t tiles;          // number of boxes
-  int nd;                  // outer digits (tile index -> coordinates)
-  FastDiv fd[K1_MAXD];
-  int64_t sc0[K1_MAXD];    // source box coordinate (inner dim, elements) per digit
-  int64_t sc1[K1_MAXD];    // source box coordinate (row dim) per digit
-  int64_t ds[K1_MAXD];     // destination byte stride per digit
-  int64_t s0, s1, dbase;
+  uint32_t nboxes;
+  int nd;                      // box-index digits, outermost first
+  FastDiv fd[TMA_MAXD];
+  int32_t cdim[TMA_MAXD];      // tensor-map dimension the digit moves along
+  int32_t cmul[TMA_MAXD];      // coordinate step per digit value
+  int64_t bstride[TMA_MAXD];   // byte stride of the digit on the bulk side
+  int64_t bbase;               // byte offset of box 0 on the bulk side
   uint32_t box_bytes;
+  int stages;
+  int mode;
+  int nrep;
+  int64_t rep[K1_MAXREP];      // mode 0: byte offsets of the destination replicas
 };
 
 // ---------------------------------------------------------------- K2 tile

@@ -1,0 +1,213 @@
+// kernels_tma.cu -- K1-TMA: the paper's TMA copy lowering on sm_100a.
+//
+// One elected thread per CTA runs an S-stage ring of shared-memory boxes:
+//   mode 0: cp.async.bulk.tensor (TMA, 5-D map, swizzle in smem) global->smem,
+//           then cp.async.bulk smem->global for every destination replica;
+//   mode 1: cp.async.bulk global->smem, then cp.async.bulk.tensor smem->global.
+// The swizzled smem image of a box is exactly the destination's swizzled bytes
+// (SW128: 16-byte chunk j of row r at j ^ (r mod 8), reading R16), so no thread
+// ever touches the data.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstring>
+#include <mutex>
+
+#include "kernels.cuh"
+
+namespace axe {
+
+extern std::atomic<int64_t> g_launches;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load5(void *dst_smem, const CUtensorMap *map, uint64_t *bar, int c0, int c1, int c2,
+                                          int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, "
+      "%7}], [%2];" ::"r"(smem_u32(dst_smem)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store5(const CUtensorMap *map, const void *src_smem, int c0, int c1, int c2, int c3,
+                                           int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(map),
+      "r"(smem_u32(src_smem)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *dst_smem, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void *dst, const void *src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+struct BoxAddr {
+  int c[5];
+  int64_t boff;
+};
+
+__device__ __forceinline__ BoxAddr box_addr(const TmaParams &p, uint32_t b) {
+  BoxAddr a;
+#pragma unroll
+  for (int i = 0; i < 5; i++) a.c[i] = 0;
+  a.boff = p.bbase;
+#pragma unroll
+  for (int k = TMA_MAXD - 1; k >= 0; k--) {
+    if (k >= p.nd) continue;
+    uint32_t d;
+    if (k > 0) {
+      uint32_t q = fdiv(p.fd[k], b);
+      d = b - q * p.fd[k].d;
+      b = q;
+    } else {
+      d = b;
+    }
+#pragma unroll
+    for (int i = 0; i < 5; i++)
+      if (p.cdim[k] == i) a.c[i] += (int)d * p.cmul[k];
+    a.boff += (int64_t)d * p.bstride[k];
+  }
+  return a;
+}
+
+constexpr int TMA_MAX_STAGES = 16;
+
+__global__ void __launch_bounds__(32) k1_tma(const __grid_constant__ CUtensorMap map, const __grid_constant__ TmaParams p,
+                                             const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full[TMA_MAX_STAGES];
+  if (threadIdx.x != 0) return;
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int S = p.stages;
+  const uint32_t B = p.box_bytes;
+  for (int s = 0; s < S; s++) mbar_init(&full[s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  fence_async_smem();
+
+  const uint32_t nb = p.nboxes;
+  const uint32_t first = blockIdx.x, step = gridDim.x;
+  const uint32_t mine = first < nb ? (nb - first + step - 1) / step : 0;
+
+  auto issue_load = [&](uint32_t k) {
+    const int s = (int)(k % (uint32_t)S);
+    BoxAddr a = box_addr(p, first + k * step);
+    mbar_expect_tx(&full[s], B);
+    if (p.mode == 0)
+      tma_load5(smem + (size_t)s * B, &map, &full[s], a.c[0], a.c[1], a.c[2], a.c[3], a.c[4]);
+    else
+      bulk_load(smem + (size_t)s * B, src + a.boff, B, &full[s]);
+  };
+
+  const uint32_t pre = mine < (uint32_t)S ? mine : (uint32_t)S;
+  for (uint32_t k = 0; k < pre; k++) issue_load(k);
+  for (uint32_t k = 0; k < mine; k++) {
+    const int s = (int)(k % (uint32_t)S);
+    mbar_wait(&full[s], (k / (uint32_t)S) & 1u);
+    BoxAddr a = box_addr(p, first + k * step);
+    if (p.mode == 0) {
+      for (int r = 0; r < p.nrep; r++) bulk_store(dst + a.boff + p.rep[r], smem + (size_t)s * B, B);
+    } else {
+      tma_store5(&map, smem + (size_t)s * B, a.c[0], a.c[1], a.c[2], a.c[3], a.c[4]);
+    }
+    bulk_commit();
+    // the stage of box k-1 is free once its store has read shared memory
+    if (k >= 1 && k - 1 + S < mine) {
+      bulk_wait_read<1>();
+      issue_load(k - 1 + S);
+    }
+  }
+  bulk_wait_all();
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                    const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled encode_fn() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_encodeTiled)p;
+  });
+  return fn;
+}
+
+// dims/strides in bytes (byte elements); rank 5; swizzle_bytes in {0, 32, 64, 128}
+int encode_tensor_map(void *out128, void *gaddr, const uint64_t dims[5], const uint64_t strides[4],
+                      const uint32_t box[5], int swizzle_bytes) {
+  PFN_encodeTiled fn = encode_fn();
+  if (!fn) return -1;
+  CUtensorMapSwizzle sw = swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                          : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                : CU_TENSOR_MAP_SWIZZLE_NONE;
+  cuuint64_t gd[5], gs[4];
+  cuuint32_t bd[5], es[5];
+  for (int i = 0; i < 5; i++) {
+    gd[i] = dims[i];
+    bd[i] = box[i];
+    es[i] = 1;
+  }
+  for (int i = 0; i < 4; i++) gs[i] = strides[i];
+  CUtensorMap m;  // 64-byte aligned
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, gaddr, gd, gs, bd, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  memcpy(out128, &m, sizeof(m));
+  return (int)r;
+}
+
+size_t tma_smem_bytes(const TmaParams &p) { return (size_t)p.stages * p.box_bytes + 1024; }
+
+cudaError_t launch_tma(const void *map128, const TmaParams &p, unsigned blocks, const void *src, void *dst,
+                       cudaStream_t st) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(k1_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  CUtensorMap m;
+  memcpy(&m, map128, sizeof(m));
+  k1_tma<<<blocks, 32, tma_smem_bytes(p), st>>>(m, p, (const uint8_t *)src, (uint8_t *)dst);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+}  // namespace axe

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <numeric>
 #include <set>
 
 namespace axe {
@@ -256,14 +257,18 @@ static bool build_k1(const std::vector<Joint> &J0, const Linear &ls, const Linea
     J.pop_back();
     if (last.e / V > 1) J.push_back(Joint{last.e / V, V, V});
   }
-  std::vector<Joint> D;
+  // kernel order: the traversal order of a copy is free (every digit is an
+  // independent loop), so consecutive threads walk the destination-contiguous
+  // digits first -- every warp writes whole 128-byte lines.
+  std::vector<Joint> D;  // inner (fastest) first
   for (auto &j : J)
     if (j.e > 1) D.push_back(j);
+  std::stable_sort(D.begin(), D.end(), [](const Joint &a, const Joint &b) {
+    int64_t x = a.ds < 0 ? -a.ds : a.ds, y = b.ds < 0 ? -b.ds : b.ds;
+    if (x != y) return x < y;
+    return (a.ss < 0 ? -a.ss : a.ss) < (b.ss < 0 ? -b.ss : b.ss);
+  });
   if (D.empty()) D.push_back(Joint{1, 0, 0});
-  if ((int)D.size() > K1_MAXD) {
-    *why = "too many joint digits for the vector kernel";
-    return false;
-  }
   int64_t total = 1;
   for (auto &j : D) total *= j.e;
   if (total >= (int64_t(1) << 32)) {
@@ -273,12 +278,6 @@ static bool build_k1(const std::vector<Joint> &J0, const Linear &ls, const Linea
   K1Params &k = P->k1;
   memset(&k, 0, sizeof(k));
   k.total = (uint32_t)total;
-  k.nd = (int)D.size();
-  for (int i = 0; i < k.nd; i++) {
-    k.fd[i] = make_fastdiv((uint32_t)D[i].e);
-    k.ss[i] = D[i].ss * es;
-    k.ds[i] = D[i].ds * es;
-  }
   k.sbase = ls.base * es;
   k.dbase = ld.base * es;
   k.nrep = (int)reps.size();
@@ -288,14 +287,221 @@ static bool build_k1(const std::vector<Joint> &J0, const Linear &ls, const Linea
   P->covers_all = (int64_t)reps.size() * total * V == dstst.cells;
   P->vb = (int)(V * es);
   P->align = std::max(P->vb, es);
-  int u = k1_unroll(P->vb);
-  int64_t blocks = (total + 256LL * u - 1) / (256LL * u);
-  int64_t cap = (int64_t)num_sms() * 8;
-  P->blocks = (unsigned)std::max<int64_t>(1, std::min(blocks, cap));
-  char b[256];
-  snprintf(b, sizeof b, "{\"kernel\":\"vector\",\"vec_bytes\":%d,\"vectors\":%lld,\"replicas\":%d,\"blocks\":%u,\"digits\":",
-           P->vb, (long long)total, k.nrep, P->blocks);
+  const int u = k1_unroll(P->vb);
+
+  // tiled form: a digit boundary at tile_v = 256 * u vectors (split by gcd, Lemma split)
+  std::vector<Joint> inner, outer;
+  int64_t tile_v = 256LL * u;
+  bool tiled = total >= tile_v && total % tile_v == 0;
+  if (tiled) {
+    int64_t prefix = 1;
+    size_t k2 = 0;
+    std::vector<Joint> rest = D;
+    while (prefix < tile_v && k2 < rest.size()) {
+      int64_t need = tile_v / prefix;
+      Joint j = rest[k2];
+      int64_t g = std::gcd(j.e, need);
+      if (g == j.e) {
+        inner.push_back(j);
+        prefix *= j.e;
+        k2++;
+      } else if (g > 1) {
+        inner.push_back(Joint{g, j.ss, j.ds});
+        rest[k2] = Joint{j.e / g, j.ss * g, j.ds * g};
+        prefix *= g;
+      } else {
+        break;
+      }
+    }
+    if (prefix != tile_v) tiled = false;
+    for (; tiled && k2 < rest.size(); k2++) outer.push_back(rest[k2]);
+    if ((int)inner.size() > K1_MAXD || (int)outer.size() > K1_MAXD) tiled = false;
+  }
+  auto fill = [&](const std::vector<Joint> &inner_first, FastDiv *fd, int64_t *a, int64_t *b) {
+    int n = (int)inner_first.size();
+    for (int i = 0; i < n; i++) {  // parameter blocks are outermost first
+      const Joint &j = inner_first[n - 1 - i];
+      fd[i] = make_fastdiv((uint32_t)j.e);
+      a[i] = j.ss * es;
+      b[i] = j.ds * es;
+    }
+    return n;
+  };
+  std::string mode;
+  if (tiled) {
+    k.tile_v = (uint32_t)tile_v;
+    k.ntiles = (uint32_t)(total / tile_v);
+    k.nin = fill(inner, k.ifd, k.iss, k.ids);
+    k.nout = fill(outer, k.ofd, k.oss, k.ods);
+    // the swizzle commutes with adding a tile base that is a whole number of swizzle blocks
+    auto whole = [&](const Swz &sw, int64_t base, const std::vector<int64_t> &extra, bool src) {
+      if (!sw.mask) return 1;
+      int64_t blk = int64_t(1) << (sw.shift + ilog2_floor(sw.mask + 1));
+      if (base % blk) return 0;
+      for (auto &j : outer)
+        if ((src ? j.ss : j.ds) * es % blk) return 0;
+      for (int64_t r : extra)
+        if (r % blk) return 0;
+      return 1;
+    };
+    std::vector<int64_t> rb;
+    for (int64_t r : reps) rb.push_back(r * es);
+    k.pre_s = whole(k.ssw, k.sbase, {}, true);
+    k.pre_d = whole(k.dsw, k.dbase, rb, false);
+    int64_t cap = (int64_t)num_sms() * 8;
+    P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(k.ntiles, cap));
+    mode = "tiled";
+  } else {
+    if ((int)D.size() > K1_MAXD) {
+      *why = "too many joint digits for the vector kernel";
+      return false;
+    }
+    k.nd = fill(D, k.fd, k.ss, k.ds);
+    int64_t blocks = (total + 256LL * u - 1) / (256LL * u);
+    int64_t cap = (int64_t)num_sms() * 8;
+    P->blocks = (unsigned)std::max<int64_t>(1, std::min(blocks, cap));
+    mode = "decode";
+  }
+  char b[320];
+  snprintf(b, sizeof b,
+           "{\"kernel\":\"vector\",\"mode\":\"%s\",\"vec_bytes\":%d,\"vectors\":%lld,\"replicas\":%d,\"blocks\":%u,"
+           "\"tile_vectors\":%u,\"pre_swizzle\":[%d,%d],\"digits\":",
+           mode.c_str(), P->vb, (long long)total, k.nrep, P->blocks, k.tile_v, k.pre_s, k.pre_d);
   P->desc = std::string(b) + joint_json(D) + ",\"joint\":" + joint_json(J0) + "}";
+  return true;
+}
+
+// K1-TMA: boxes of (rows x row bytes) contiguous on the "bulk" side
+// and a strided 2-D box (plus up to 3 outer dims) on the "tensor" side.
+// mode 0: tensor side = source (TMA load), bulk side = destination;
+// mode 1: tensor side = destination (TMA store), bulk side = source.
+static bool build_tma(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, const Storage &sst,
+                      const Storage &dstst, int es, int mode, CopyPlan *P, std::string *why) {
+  const Storage &tst = mode == 0 ? sst : dstst;
+  const Storage &bst = mode == 0 ? dstst : sst;
+  const Linear &lt = mode == 0 ? ls : ld;
+  const Linear &lb = mode == 0 ? ld : ls;
+  auto fail = [&](const char *m) {
+    *why = m;
+    return false;
+  };
+  if (tst.swz_b) return fail("tma: the tensor-map side is swizzled in global memory");
+  int span = 0;
+  if (bst.swz_b) {
+    if (bst.swz_m != 4 || bst.swz_s != 3 || bst.swz_b > 3) return fail("tma: swizzle is not a TMA mode");
+    span = 16 << bst.swz_b;
+  }
+  if (mode == 1 && !ld.R.empty()) return fail("tma: destination replicas need the bulk-store mode");
+  std::vector<int64_t> reps{0};
+  for (auto &r : ld.R) {
+    std::vector<int64_t> nx;
+    for (int64_t b : reps)
+      for (int64_t d = 0; d < r.e; d++) nx.push_back(b + d * r.s);
+    reps.swap(nx);
+  }
+  std::sort(reps.begin(), reps.end());
+  reps.erase(std::unique(reps.begin(), reps.end()), reps.end());
+  if ((int)reps.size() > K1_MAXREP) return fail("tma: too many replicas");
+  struct TB {
+    int64_t e, t, b;
+  };
+  std::vector<TB> d;
+  for (auto &j : J0)
+    if (j.e > 1) d.push_back(TB{j.e, mode == 0 ? j.ss : j.ds, mode == 0 ? j.ds : j.ss});
+  for (auto &x : d)
+    if (x.t <= 0 || x.b <= 0) return fail("tma: negative strides");
+  std::stable_sort(d.begin(), d.end(), [](const TB &a, const TB &b) { return a.b < b.b; });
+  if (d.size() < 2 || d[0].t != 1 || d[0].b != 1) return fail("tma: no shared contiguous run");
+  const int64_t e0 = d[0].e;
+  int64_t R = 0;
+  if (span) {
+    if (span % es || e0 % (span / es)) return fail("tma: run does not fill the swizzle span");
+    R = span / es;
+  } else {
+    for (int64_t r = e0; r >= 1; r--)
+      if (e0 % r == 0 && r * es <= 256 && (r * es) % 16 == 0) {
+        R = r;
+        break;
+      }
+    if (!R) return fail("tma: no 16-byte-multiple row length");
+  }
+  if (e0 > R) {
+    d[0] = TB{R, 1, 1};
+    d.insert(d.begin() + 1, TB{e0 / R, R, R});
+  }
+  if (d[1].b != R) return fail("tma: rows of a box are not contiguous on the bulk side");
+  const int64_t E1 = d[1].e, t1 = d[1].t;
+  if ((t1 * es) % 16) return fail("tma: row stride not a multiple of 16 bytes");
+  const int64_t row_bytes = R * es;
+  int64_t B1 = 0;
+  for (int64_t b = std::min<int64_t>(E1, 256); b >= 1; b--)
+    if (E1 % b == 0 && b * row_bytes <= 16384 && (!span || b % 8 == 0)) {
+      B1 = b;
+      break;
+    }
+  if (!B1) return fail("tma: no legal box height");
+  const int64_t box_bytes = B1 * row_bytes;
+  const int64_t blk = span ? span * 8 : 16;  // the bulk-side box base must be a whole swizzle block
+  TmaParams &k = P->tma;
+  memset(&k, 0, sizeof(k));
+  std::vector<std::array<int64_t, 4>> digs;  // extent, cdim, cmul, bulk stride (bytes), outermost last
+  if (E1 / B1 > 1) digs.push_back({E1 / B1, 1, B1, B1 * d[1].b * es});
+  int dim = 2;
+  P->tm_dims[0] = (uint64_t)row_bytes;
+  P->tm_box[0] = (uint32_t)row_bytes;
+  P->tm_dims[1] = (uint64_t)E1;
+  P->tm_strides[0] = (uint64_t)(t1 * es);
+  P->tm_box[1] = (uint32_t)B1;
+  for (size_t i = 2; i < d.size(); i++) {
+    if (dim > 4) return fail("tma: more than 5 tensor dimensions");
+    if ((d[i].t * es) % 16) return fail("tma: outer stride not a multiple of 16 bytes");
+    P->tm_dims[dim] = (uint64_t)d[i].e;
+    P->tm_strides[dim - 1] = (uint64_t)(d[i].t * es);
+    P->tm_box[dim] = 1;
+    digs.push_back({d[i].e, dim, 1, d[i].b * es});
+    dim++;
+  }
+  for (int i = dim; i < 5; i++) P->tm_strides[i - 1] = P->tm_strides[dim - 2 > 0 ? dim - 2 : 0];
+  if ((int)digs.size() > TMA_MAXD) return fail("tma: too many box digits");
+  int64_t nboxes = 1;
+  for (auto &g : digs) {
+    nboxes *= g[0];
+    if (g[3] % blk) return fail("tma: box bases are not whole swizzle blocks");
+  }
+  if (nboxes >= (int64_t(1) << 31)) return fail("tma: too many boxes");
+  if ((lb.base * es) % blk || (lt.base * es) % 16) return fail("tma: misaligned base offset");
+  for (int64_t r : reps)
+    if ((r * es) % blk) return fail("tma: replica offsets are not whole swizzle blocks");
+  k.nboxes = (uint32_t)nboxes;
+  k.nd = (int)digs.size();
+  for (int i = 0; i < k.nd; i++) {  // params are outermost first; digs is innermost first
+    auto &g = digs[digs.size() - 1 - i];
+    k.fd[i] = make_fastdiv((uint32_t)g[0]);
+    k.cdim[i] = (int32_t)g[1];
+    k.cmul[i] = (int32_t)g[2];
+    k.bstride[i] = g[3];
+  }
+  k.bbase = lb.base * es;
+  k.box_bytes = (uint32_t)box_bytes;
+  k.mode = mode;
+  k.nrep = (int)reps.size();
+  for (size_t i = 0; i < reps.size(); i++) k.rep[i] = reps[i] * es;
+  int stages = (int)std::max<int64_t>(2, std::min<int64_t>(16, 49152 / box_bytes));
+  k.stages = stages;
+  P->tm_swizzle = span;
+  P->tm_base = lt.base * es;
+  P->tm_cache = std::make_shared<TmaCache>();
+  int per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(16, (220 * 1024) / (int64_t)tma_smem_bytes(k)));
+  P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nboxes, (int64_t)num_sms() * per_sm));
+  P->align = 16;
+  P->covers_all = (int64_t)reps.size() * nboxes * box_bytes == dstst.cells * es;
+  char b[320];
+  snprintf(b, sizeof b,
+           "{\"kernel\":\"tma\",\"mode\":\"%s\",\"box\":[%lld,%lld],\"box_bytes\":%lld,\"boxes\":%lld,\"stages\":%d,"
+           "\"blocks\":%u,\"swizzle\":%d,\"replicas\":%d,\"joint\":",
+           mode == 0 ? "tensor-load/bulk-store" : "bulk-load/tensor-store", (long long)B1, (long long)row_bytes,
+           (long long)box_bytes, (long long)nboxes, stages, P->blocks, span, k.nrep);
+  P->desc = std::string(b) + joint_json(J0) + "}";
   return true;
 }
 
@@ -329,6 +535,17 @@ axe_status plan_copy(const PlanRequest &rq, CopyPlan *out) {
 
   std::string why = lin ? (joint ? "" : "digit systems are not nested (no joint refinement)")
                         : "storage composition is not affine";
+  if (joint && rq.max_align >= 16 && (kernel == AXE_KERNEL_AUTO || kernel == AXE_KERNEL_TMA)) {
+    std::string w0, w1;
+    if (build_tma(J, ls, ld, *rq.sst, *rq.dstst, es, 0, &P, &w0) ||
+        build_tma(J, ls, ld, *rq.sst, *rq.dstst, es, 1, &P, &w1)) {
+      P.kernel = KK_TMA;
+      *out = std::move(P);
+      return AXE_OK;
+    }
+    if (kernel == AXE_KERNEL_TMA)
+      AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced TMA kernel cannot run these layouts: %s / %s", w0.c_str(), w1.c_str());
+  }
   if (kernel == AXE_KERNEL_AUTO || kernel == AXE_KERNEL_VECTOR || kernel == AXE_KERNEL_TILE ||
       kernel == AXE_KERNEL_TMA) {
     if (joint && build_k1(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &why)) {
@@ -366,6 +583,30 @@ axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t 
   switch (p.kernel) {
     case KK_VECTOR: e = launch_k1(p.k1, p.vb, p.blocks, src, dst, st); break;
     case KK_GENERIC: e = launch_k0(p.k0, src, dst, st); break;
+    case KK_TMA: {
+      const void *tptr = p.tma.mode == 0 ? src : (const void *)dst;
+      std::array<uint64_t, 16> map;
+      bool hit = false;
+      {
+        std::lock_guard<std::mutex> lk(p.tm_cache->mu);
+        for (auto &m : p.tm_cache->maps)
+          if (m.first == tptr) {
+            map = m.second;
+            hit = true;
+            break;
+          }
+      }
+      if (!hit) {
+        int r = encode_tensor_map(map.data(), (uint8_t *)tptr + p.tm_base, p.tm_dims, p.tm_strides, p.tm_box,
+                                  p.tm_swizzle);
+        if (r != 0) AXE_FAIL(AXE_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", r);
+        std::lock_guard<std::mutex> lk(p.tm_cache->mu);
+        if (p.tm_cache->maps.size() >= 32) p.tm_cache->maps.erase(p.tm_cache->maps.begin());
+        p.tm_cache->maps.push_back({tptr, map});
+      }
+      e = launch_tma(map.data(), p.tma, p.blocks, src, dst, st);
+      break;
+    }
     default: AXE_FAIL(AXE_ERR_UNSUPPORTED, "unknown kernel");
   }
   if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));

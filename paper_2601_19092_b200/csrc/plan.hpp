@@ -3,6 +3,9 @@
 
 #include <cuda_runtime.h>
 
+#include <array>
+#include <memory>
+#include <mutex>
 #include <string>
 
 #include "common.hpp"
@@ -26,6 +29,18 @@ struct CopyPlan {
   std::vector<Joint> joint;
   bool linear = false;
   bool covers_all = false;  // the destination image is every cell of the dst storage
+  // K1-TMA: the tensor-map side (mode 0: src, mode 1: dst), encoded per pointer at execute
+  TmaParams tma;
+  uint64_t tm_dims[5] = {1, 1, 1, 1, 1}, tm_strides[4] = {16, 16, 16, 16};
+  uint32_t tm_box[5] = {1, 1, 1, 1, 1};
+  int tm_swizzle = 0;       // bytes: 0, 32, 64, 128
+  int64_t tm_base = 0;      // byte offset of coordinate 0 from the buffer base
+  std::shared_ptr<struct TmaCache> tm_cache;
+};
+
+struct TmaCache {
+  std::mutex mu;
+  std::vector<std::pair<const void *, std::array<uint64_t, 16>>> maps;  // LRU-ish, small
 };
 
 struct PlanRequest {
@@ -48,6 +63,12 @@ axe_status check_injective(const Layout &dst, const Storage &st, int skip_axis);
 cudaError_t launch_k0(const K0Params &p, const void *src, void *dst, cudaStream_t st);
 cudaError_t launch_k1(const K1Params &p, int vb, unsigned blocks, const void *src, void *dst, cudaStream_t st);
 int k1_unroll(int vb);
+// kernels_tma.cu
+int encode_tensor_map(void *out128, void *gaddr, const uint64_t dims[5], const uint64_t strides[4],
+                      const uint32_t box[5], int swizzle_bytes);
+cudaError_t launch_tma(const void *map128, const TmaParams &p, unsigned blocks, const void *src, void *dst,
+                       cudaStream_t st);
+size_t tma_smem_bytes(const TmaParams &p);
 int num_sms();
 int64_t kernel_launches();
 

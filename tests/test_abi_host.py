@@ -133,12 +133,19 @@ def plan(cfg, kernel="auto"):
     return axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], cfg["es"], kernel)
 
 
-def test_config2_plan_is_16B_vector_copy():
+def test_config2_plan_is_tma_box_copy():
+    """Config 2 lowers to the paper's TMA recipe: 64x128 B boxes, SW128 in smem."""
     d = plan(synth.config2()).describe()
-    assert d["kernel"] == "vector" and d["vec_bytes"] == 16
+    assert d["kernel"] == "tma" and d["box"] == [64, 128] and d["boxes"] == 4096 and d["swizzle"] == 128
     # SURVEY §8(a) a4: joint digits (64:262144|262144),(64:4096|64),(64:64|4096),(64:1|1)
     assert d["joint"] == [[64, 262144, 262144], [64, 4096, 64], [64, 64, 4096], [64, 1, 1]]
-    assert d["vectors"] == 4096 * 4096 // 8
+    r = plan(synth.config2(reverse=True)).describe()
+    assert r["kernel"] == "tma" and r["mode"] == "bulk-load/tensor-store"
+
+
+def test_config2_vector_plan():
+    d = plan(synth.config2(), "vector").describe()
+    assert d["kernel"] == "vector" and d["vec_bytes"] == 16 and d["vectors"] == 4096 * 4096 // 8
 
 
 def test_config1_plan():

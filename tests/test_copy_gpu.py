@@ -64,7 +64,7 @@ def test_config1_exhaustive(axe, mk, kernel):
     check(axe, mk(), kernel)
 
 
-@pytest.mark.parametrize("kernel", ["auto", "generic"])
+@pytest.mark.parametrize("kernel", ["auto", "generic", "vector"])
 @pytest.mark.parametrize("n,es,sw,rev", [(256, 2, synth.SW128, False), (256, 2, synth.SW128, True),
                                         (512, 4, synth.SW64, False), (192, 8, synth.SW32, True),
                                         (128, 1, (0, 0, 0), False)])
@@ -73,10 +73,11 @@ def test_config2_small(axe, n, es, sw, rev, kernel):
 
 
 @pytest.mark.parametrize("rev", [False, True])
-def test_config2_full(axe, rev):
-    """BASELINE config 2 at full size (4096^2 bf16) in the launch configuration bench.py times."""
-    desc = check(axe, synth.config2(reverse=rev))
-    assert desc["kernel"] in ("vector", "tma")
+@pytest.mark.parametrize("kernel", ["auto", "vector", "tma"])
+def test_config2_full(axe, rev, kernel):
+    """BASELINE config 2 at full size (4096^2 bf16); "auto" is the launch configuration bench.py times."""
+    desc = check(axe, synth.config2(reverse=rev), kernel)
+    assert desc["kernel"] == ("tma" if kernel == "auto" else kernel)
 
 
 @pytest.mark.parametrize("kernel", ["auto", "generic"])
@@ -192,6 +193,7 @@ def test_random_layout_pairs(axe, seed):
                dst_st=linear_storage(dc, sw), seed=seed)
     check(axe, cfg, "auto")
     check(axe, cfg, "generic")
+    check(axe, cfg, "vector") if axe.CopyPlan(src, cfg["src_st"], dst, cfg["dst_st"], es).describe()["kernel"] != "generic" else None
 
 
 def test_alias_and_alignment_errors(axe):

@@ -1,0 +1,92 @@
+#!/usr/bin/env python
+"""Development timing of every single-GPU BASELINE config (not the bench contract line).
+
+For each config: plan once, rotate over buffer pairs whose footprint exceeds
+4x L2, capture G back-to-back executes in a CUDA graph, replay, report
+algorithmic GB/s (es * (1 + E_R) bytes per element) and the
+fraction of the measured HBM copy peak.  Kernels can be forced with
+--kernel (auto|generic|vector|tma|tile).
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+import paper_2601_19092_b200 as axe  # noqa: E402
+
+
+def transpose_cfg(R, C, es):
+    return dict(name=f"transpose{R}x{C}x{es}", es=es, src=synth.layout([(R, C), (C, 1)]),
+                src_st=synth.linear_storage(R * C), dst=synth.layout([(R, 1), (C, R)]),
+                dst_st=synth.linear_storage(R * C), seed=7)
+
+
+CONFIGS = {
+    "config2": lambda: synth.config2(),
+    "config2r": lambda: synth.config2(reverse=True),
+    "config2_16k": lambda: synth.config2(16384),
+    "config3a": lambda: synth.config3(65536, "a"),
+    "config3b": lambda: synth.config3(65536, "b"),
+    "transpose_bf16": lambda: transpose_cfg(8192, 8192, 2),
+    "transpose_f32": lambda: transpose_cfg(8192, 8192, 4),
+}
+
+
+def time_cfg(cfg, kernel, reps=20):
+    es = cfg["es"]
+    plan = axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], es, kernel)
+    sb, db = plan.sizes()
+    ed = plan.src.E_D
+    er = plan.dst.E_R
+    alg = ed * es * (1 + er)
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    pairs = max(1, min(8, -(-4 * l2 // (sb + db))))
+    srcs = [torch.empty(sb, dtype=torch.uint8, device="cuda") for _ in range(pairs)]
+    dsts = [torch.empty(db, dtype=torch.uint8, device="cuda") for _ in range(pairs)]
+    for s in srcs:
+        s.random_()
+    G = pairs * max(1, 64 // pairs) if alg < (1 << 28) else pairs
+    g = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    with torch.cuda.graph(g, stream=cs):
+        for j in range(G):
+            plan.execute(srcs[j % pairs], dsts[j % pairs], torch.cuda.current_stream())
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / (reps * G)
+    gbs = alg / (ms * 1e-3) / 1e9
+    d = plan.describe()
+    del srcs, dsts, g
+    torch.cuda.empty_cache()
+    return {"config": cfg["name"], "kernel": d["kernel"], "mode": d.get("mode"), "us": ms * 1e3, "GB/s": gbs,
+            "frac_measured": gbs / 6547.2, "alg_bytes": alg}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--kernel", default="auto")
+    ap.add_argument("--only", default="")
+    a = ap.parse_args()
+    names = a.only.split(",") if a.only else list(CONFIGS)
+    for n in names:
+        try:
+            print(json.dumps(time_cfg(CONFIGS[n](), a.kernel)), flush=True)
+        except Exception as e:  # report and continue
+            print(json.dumps({"config": n, "error": str(e)}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
