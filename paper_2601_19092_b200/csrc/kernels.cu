@@ -16,6 +16,7 @@
 #include <cstdio>
 
 #include "kernels.cuh"
+#include "launch.cuh"
 
 namespace axe {
 
@@ -68,6 +69,8 @@ template <int ES>
 __global__ void __launch_bounds__(256) k0_generic(const __grid_constant__ K0Params p, const uint8_t *__restrict__ src,
                                                   uint8_t *__restrict__ dst) {
   using T = typename VecT<ES>::T;
+  pdl_wait();
+  pdl_launch_dependents();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < (uint64_t)p.ED; x += stride) {
     int64_t c[K0_MAXAX];
@@ -130,6 +133,8 @@ template <int ND, int VB, int U>
 __global__ void __launch_bounds__(K1_THREADS) k1_vector(const __grid_constant__ K1Params p,
                                                         const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
   using T = typename VecT<VB>::T;
+  pdl_wait();
+  pdl_launch_dependents();
   const uint32_t total = p.total;
   const uint32_t step = gridDim.x * (K1_THREADS * U);
   for (uint32_t base = blockIdx.x * (K1_THREADS * U) + threadIdx.x; base < total; base += step) {
@@ -187,6 +192,8 @@ __global__ void __launch_bounds__(K1_THREADS) k1_tiled(const __grid_constant__ K
     if (p.pre_s) so[u] = swz(p.ssw, so[u]);
     if (p.pre_d) dof[u] = swz(p.dsw, dof[u]);
   }
+  pdl_wait();  // the per-thread decode above overlaps the previous kernel's tail
+  pdl_launch_dependents();
   for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
     int64_t sb = p.sbase, db = p.dbase;
     decode_digits(p.nout, p.ofd, p.oss, p.ods, t, sb, db);
@@ -221,49 +228,49 @@ cudaError_t launch_k0(const K0Params &p, const void *src, void *dst, cudaStream_
   if (blocks < 1) blocks = 1;
   const uint8_t *s = (const uint8_t *)src;
   uint8_t *d = (uint8_t *)dst;
+  cudaError_t e = cudaSuccess;
   switch (p.es) {
-    case 1: k0_generic<1><<<(unsigned)blocks, 256, 0, st>>>(p, s, d); break;
-    case 2: k0_generic<2><<<(unsigned)blocks, 256, 0, st>>>(p, s, d); break;
-    case 4: k0_generic<4><<<(unsigned)blocks, 256, 0, st>>>(p, s, d); break;
-    case 8: k0_generic<8><<<(unsigned)blocks, 256, 0, st>>>(p, s, d); break;
-    case 16: k0_generic<16><<<(unsigned)blocks, 256, 0, st>>>(p, s, d); break;
+    case 1: e = launch_ex(k0_generic<1>, dim3((unsigned)blocks), dim3(256), 0, st, p, s, d); break;
+    case 2: e = launch_ex(k0_generic<2>, dim3((unsigned)blocks), dim3(256), 0, st, p, s, d); break;
+    case 4: e = launch_ex(k0_generic<4>, dim3((unsigned)blocks), dim3(256), 0, st, p, s, d); break;
+    case 8: e = launch_ex(k0_generic<8>, dim3((unsigned)blocks), dim3(256), 0, st, p, s, d); break;
+    case 16: e = launch_ex(k0_generic<16>, dim3((unsigned)blocks), dim3(256), 0, st, p, s, d); break;
     default: return cudaErrorInvalidValue;
   }
+  if (e != cudaSuccess) return e;
   g_launches++;
   return cudaGetLastError();
 }
 
 template <int ND, int VB>
-static void k1_launch_nd(const K1Params &p, unsigned blocks, const uint8_t *s, uint8_t *d, cudaStream_t st) {
+static cudaError_t k1_launch_nd(const K1Params &p, unsigned blocks, const uint8_t *s, uint8_t *d, cudaStream_t st) {
   constexpr int U = VB >= 8 ? 4 : 8;
-  k1_vector<ND, VB, U><<<blocks, K1_THREADS, 0, st>>>(p, s, d);
+  return launch_ex(k1_vector<ND, VB, U>, dim3(blocks), dim3(K1_THREADS), 0, st, p, s, d);
 }
 
 template <int VB>
 static cudaError_t k1_launch_vb(const K1Params &p, unsigned blocks, const uint8_t *s, uint8_t *d, cudaStream_t st) {
   switch (p.nd) {
-    case 1: k1_launch_nd<1, VB>(p, blocks, s, d, st); break;
-    case 2: k1_launch_nd<2, VB>(p, blocks, s, d, st); break;
-    case 3: k1_launch_nd<3, VB>(p, blocks, s, d, st); break;
-    case 4: k1_launch_nd<4, VB>(p, blocks, s, d, st); break;
-    case 5: k1_launch_nd<5, VB>(p, blocks, s, d, st); break;
-    case 6: k1_launch_nd<6, VB>(p, blocks, s, d, st); break;
-    case 7: k1_launch_nd<7, VB>(p, blocks, s, d, st); break;
-    case 8: k1_launch_nd<8, VB>(p, blocks, s, d, st); break;
+    case 1: return k1_launch_nd<1, VB>(p, blocks, s, d, st);
+    case 2: return k1_launch_nd<2, VB>(p, blocks, s, d, st);
+    case 3: return k1_launch_nd<3, VB>(p, blocks, s, d, st);
+    case 4: return k1_launch_nd<4, VB>(p, blocks, s, d, st);
+    case 5: return k1_launch_nd<5, VB>(p, blocks, s, d, st);
+    case 6: return k1_launch_nd<6, VB>(p, blocks, s, d, st);
+    case 7: return k1_launch_nd<7, VB>(p, blocks, s, d, st);
+    case 8: return k1_launch_nd<8, VB>(p, blocks, s, d, st);
     default:
       if (p.nd > K1_MAXD) return cudaErrorInvalidValue;
-      k1_launch_nd<0, VB>(p, blocks, s, d, st);
-      break;
+      return k1_launch_nd<0, VB>(p, blocks, s, d, st);
   }
-  return cudaSuccess;
 }
 
 int k1_unroll(int vb) { return vb >= 8 ? 4 : 8; }
 
 template <int VB>
-static void k1_tiled_launch(const K1Params &p, unsigned blocks, const uint8_t *s, uint8_t *d, cudaStream_t st) {
+static cudaError_t k1_tiled_launch(const K1Params &p, unsigned blocks, const uint8_t *s, uint8_t *d, cudaStream_t st) {
   constexpr int U = VB >= 8 ? 4 : 8;
-  k1_tiled<VB, U><<<blocks, K1_THREADS, 0, st>>>(p, s, d);
+  return launch_ex(k1_tiled<VB, U>, dim3(blocks), dim3(K1_THREADS), 0, st, p, s, d);
 }
 
 cudaError_t launch_k1(const K1Params &p, int vb, unsigned blocks, const void *src, void *dst, cudaStream_t st) {
@@ -272,23 +279,22 @@ cudaError_t launch_k1(const K1Params &p, int vb, unsigned blocks, const void *sr
   cudaError_t e = cudaSuccess;
   if (p.tile_v > 0) {
     switch (vb) {
-      case 1: k1_tiled_launch<1>(p, blocks, s, d, st); break;
-      case 2: k1_tiled_launch<2>(p, blocks, s, d, st); break;
-      case 4: k1_tiled_launch<4>(p, blocks, s, d, st); break;
-      case 8: k1_tiled_launch<8>(p, blocks, s, d, st); break;
-      case 16: k1_tiled_launch<16>(p, blocks, s, d, st); break;
+      case 1: e = k1_tiled_launch<1>(p, blocks, s, d, st); break;
+      case 2: e = k1_tiled_launch<2>(p, blocks, s, d, st); break;
+      case 4: e = k1_tiled_launch<4>(p, blocks, s, d, st); break;
+      case 8: e = k1_tiled_launch<8>(p, blocks, s, d, st); break;
+      case 16: e = k1_tiled_launch<16>(p, blocks, s, d, st); break;
       default: return cudaErrorInvalidValue;
     }
-    g_launches++;
-    return cudaGetLastError();
-  }
-  switch (vb) {
-    case 1: e = k1_launch_vb<1>(p, blocks, s, d, st); break;
-    case 2: e = k1_launch_vb<2>(p, blocks, s, d, st); break;
-    case 4: e = k1_launch_vb<4>(p, blocks, s, d, st); break;
-    case 8: e = k1_launch_vb<8>(p, blocks, s, d, st); break;
-    case 16: e = k1_launch_vb<16>(p, blocks, s, d, st); break;
-    default: return cudaErrorInvalidValue;
+  } else {
+    switch (vb) {
+      case 1: e = k1_launch_vb<1>(p, blocks, s, d, st); break;
+      case 2: e = k1_launch_vb<2>(p, blocks, s, d, st); break;
+      case 4: e = k1_launch_vb<4>(p, blocks, s, d, st); break;
+      case 8: e = k1_launch_vb<8>(p, blocks, s, d, st); break;
+      case 16: e = k1_launch_vb<16>(p, blocks, s, d, st); break;
+      default: return cudaErrorInvalidValue;
+    }
   }
   if (e != cudaSuccess) return e;
   g_launches++;

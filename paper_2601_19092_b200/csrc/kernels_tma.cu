@@ -15,6 +15,7 @@
 #include <mutex>
 
 #include "kernels.cuh"
+#include "launch.cuh"
 
 namespace axe {
 
@@ -109,6 +110,8 @@ __global__ void __launch_bounds__(32) k1_tma(const __grid_constant__ CUtensorMap
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[TMA_MAX_STAGES];
   if (threadIdx.x != 0) return;
+  pdl_wait();
+  pdl_launch_dependents();
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int S = p.stages;
   const uint32_t B = p.box_bytes;
@@ -205,7 +208,9 @@ cudaError_t launch_tma(const void *map128, const TmaParams &p, unsigned blocks, 
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap m;
   memcpy(&m, map128, sizeof(m));
-  k1_tma<<<blocks, 32, tma_smem_bytes(p), st>>>(m, p, (const uint8_t *)src, (uint8_t *)dst);
+  cudaError_t e = launch_ex(k1_tma, dim3(blocks), dim3(32), tma_smem_bytes(p), st, m, p, (const uint8_t *)src,
+                            (uint8_t *)dst);
+  if (e != cudaSuccess) return e;
   g_launches++;
   return cudaGetLastError();
 }

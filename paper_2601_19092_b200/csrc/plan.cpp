@@ -200,6 +200,11 @@ static std::string joint_json(const std::vector<Joint> &J) {
   return s + "]";
 }
 
+static int64_t env_int(const char *name, int64_t dflt) {
+  const char *e = getenv(name);
+  return (e && *e) ? atoll(e) : dflt;
+}
+
 static int env_kernel() {
   const char *e = getenv("AXE_FORCE_KERNEL");
   if (!e || !*e) return AXE_KERNEL_AUTO;
@@ -486,12 +491,14 @@ static bool build_tma(const std::vector<Joint> &J0, const Linear &ls, const Line
   k.mode = mode;
   k.nrep = (int)reps.size();
   for (size_t i = 0; i < reps.size(); i++) k.rep[i] = reps[i] * es;
-  int stages = (int)std::max<int64_t>(2, std::min<int64_t>(16, 49152 / box_bytes));
+  int64_t stage_bytes = env_int("AXE_TMA_STAGE_BYTES", 49152);
+  int stages = (int)std::max<int64_t>(2, std::min<int64_t>(16, stage_bytes / box_bytes));
   k.stages = stages;
   P->tm_swizzle = span;
   P->tm_base = lt.base * es;
   P->tm_cache = std::make_shared<TmaCache>();
   int per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(16, (220 * 1024) / (int64_t)tma_smem_bytes(k)));
+  per_sm = (int)std::min<int64_t>(per_sm, env_int("AXE_TMA_PER_SM", per_sm));
   P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nboxes, (int64_t)num_sms() * per_sm));
   P->align = 16;
   P->covers_all = (int64_t)reps.size() * nboxes * box_bytes == dstst.cells * es;

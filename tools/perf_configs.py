@@ -75,11 +75,40 @@ def time_cfg(cfg, kernel, reps=20):
             "frac_measured": gbs / 6547.2, "alg_bytes": alg}
 
 
+def torch_copy(nbytes, reps=20):
+    """Reference point: torch's own copy_ of nbytes (read + write counted), same rotation and graph."""
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    pairs = max(1, min(8, -(-4 * l2 // (2 * nbytes))))
+    srcs = [torch.empty(nbytes, dtype=torch.uint8, device="cuda") for _ in range(pairs)]
+    dsts = [torch.empty(nbytes, dtype=torch.uint8, device="cuda") for _ in range(pairs)]
+    G = pairs * 8
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=torch.cuda.Stream()):
+        for j in range(G):
+            dsts[j % pairs].copy_(srcs[j % pairs])
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / (reps * G)
+    gbs = 2 * nbytes / (ms * 1e-3) / 1e9
+    return {"config": f"torch_copy_{nbytes >> 20}MiB", "us": ms * 1e3, "GB/s": gbs, "frac_measured": gbs / 6547.2}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--kernel", default="auto")
     ap.add_argument("--only", default="")
+    ap.add_argument("--torch-copy", action="store_true")
     a = ap.parse_args()
+    if a.torch_copy:
+        for nb in (32 << 20, 512 << 20):
+            print(json.dumps(torch_copy(nb)), flush=True)
     names = a.only.split(",") if a.only else list(CONFIGS)
     for n in names:
         try:
