@@ -69,7 +69,7 @@ template <int ES>
 __global__ void __launch_bounds__(256) k0_generic(const __grid_constant__ K0Params p, const uint8_t *__restrict__ src,
                                                   uint8_t *__restrict__ dst) {
   using T = typename VecT<ES>::T;
-  pdl_wait();
+  if (p.dep) pdl_wait();
   pdl_launch_dependents();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < (uint64_t)p.ED; x += stride) {
@@ -133,7 +133,7 @@ template <int ND, int VB, int U>
 __global__ void __launch_bounds__(K1_THREADS) k1_vector(const __grid_constant__ K1Params p,
                                                         const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
   using T = typename VecT<VB>::T;
-  pdl_wait();
+  if (p.dep) pdl_wait();
   pdl_launch_dependents();
   const uint32_t total = p.total;
   const uint32_t step = gridDim.x * (K1_THREADS * U);
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_tiled(const __grid_constant__ K
     if (p.pre_s) so[u] = swz(p.ssw, so[u]);
     if (p.pre_d) dof[u] = swz(p.dsw, dof[u]);
   }
-  pdl_wait();  // the per-thread decode above overlaps the previous kernel's tail
+  if (p.dep) pdl_wait();  // the per-thread decode above overlaps the previous kernel's tail
   pdl_launch_dependents();
   for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
     int64_t sb = p.sbase, db = p.dbase;

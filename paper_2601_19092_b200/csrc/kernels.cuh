@@ -62,6 +62,7 @@ struct K0Params {
   K0Side src, dst;
   int64_t ED, ER;
   int es;
+  int dep;  // 1: wait for the previous kernel in the stream (griddepcontrol.wait)
 };
 
 // ---------------------------------------------------------------- K1 vector
@@ -83,6 +84,7 @@ struct K1Params {
   FastDiv ifd[K1_MAXD], ofd[K1_MAXD];
   int64_t iss[K1_MAXD], ids[K1_MAXD], oss[K1_MAXD], ods[K1_MAXD];
   int pre_s, pre_d;  // swizzle folded into the per-thread offsets (tile bases are whole swizzle blocks)
+  int dep;           // 1: wait for the previous kernel in the stream (griddepcontrol.wait)
 };
 
 // ---------------------------------------------------------------- K1-TMA
@@ -106,6 +108,7 @@ struct TmaParams {
   int mode;
   int nrep;
   int64_t rep[K1_MAXREP];      // mode 0: byte offsets of the destination replicas
+  int dep;                     // 1: wait for the previous kernel in the stream (griddepcontrol.wait)
 };
 
 // ---------------------------------------------------------------- K2 tile

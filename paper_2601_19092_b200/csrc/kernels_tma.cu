@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(32) k1_tma(const __grid_constant__ CUtensorMap
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[TMA_MAX_STAGES];
   if (threadIdx.x != 0) return;
-  pdl_wait();
+  if (p.dep) pdl_wait();
   pdl_launch_dependents();
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int S = p.stages;

@@ -7,6 +7,7 @@
 #include <cstring>
 #include <numeric>
 #include <set>
+#include <unordered_map>
 
 namespace axe {
 
@@ -580,16 +581,59 @@ axe_status plan_copy(const PlanRequest &rq, CopyPlan *out) {
   return AXE_OK;
 }
 
+// Programmatic-dependent-launch bookkeeping: the byte ranges of the last libaxe
+// kernel launched on each stream.  A new kernel that neither reads nor writes
+// what that kernel wrote, and does not write what it read, may run without
+// griddepcontrol.wait and so overlap the previous kernel's tail.  Any kernel
+// the caller put in between is not a PDL primary of ours (it never triggers
+// early), so the new kernel still starts only after it completes.
+namespace {
+struct Ranges {
+  uintptr_t s0, s1, d0, d1;
+};
+std::mutex g_dep_mu;
+std::unordered_map<cudaStream_t, Ranges> g_last;
+}  // namespace
+
+int stream_dependency(cudaStream_t st, uintptr_t s0, uintptr_t s1, uintptr_t d0, uintptr_t d1) {
+  static const int overlap_ok = [] {
+    const char *e = getenv("AXE_PDL_OVERLAP");
+    return (e && *e == '0') ? 0 : 1;
+  }();
+  auto hit = [](uintptr_t a0, uintptr_t a1, uintptr_t b0, uintptr_t b1) { return a0 < b1 && b0 < a1; };
+  std::lock_guard<std::mutex> lk(g_dep_mu);
+  int dep = 1;
+  auto it = g_last.find(st);
+  if (overlap_ok && it != g_last.end()) {
+    const Ranges &L = it->second;
+    dep = (hit(d0, d1, L.d0, L.d1) || hit(d0, d1, L.s0, L.s1) || hit(s0, s1, L.d0, L.d1)) ? 1 : 0;
+  }
+  if (g_last.size() > 256) g_last.clear();
+  g_last[st] = Ranges{s0, s1, d0, d1};
+  return dep;
+}
+
 axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t st) {
   uintptr_t s = (uintptr_t)src, d = (uintptr_t)dst;
   if (!src || !dst) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL buffer");
   if (s % p.align || d % p.align)
     AXE_FAIL(AXE_ERR_ALIGNMENT, "buffers must be %d-byte aligned for this plan", p.align);
   if (s < d + p.dst_bytes && d < s + p.src_bytes) AXE_FAIL(AXE_ERR_ALIAS, "source and destination buffers overlap");
+  const int dep = stream_dependency(st, s, s + p.src_bytes, d, d + p.dst_bytes);
   cudaError_t e = cudaSuccess;
   switch (p.kernel) {
-    case KK_VECTOR: e = launch_k1(p.k1, p.vb, p.blocks, src, dst, st); break;
-    case KK_GENERIC: e = launch_k0(p.k0, src, dst, st); break;
+    case KK_VECTOR: {
+      K1Params k = p.k1;
+      k.dep = dep;
+      e = launch_k1(k, p.vb, p.blocks, src, dst, st);
+      break;
+    }
+    case KK_GENERIC: {
+      K0Params k = p.k0;
+      k.dep = dep;
+      e = launch_k0(k, src, dst, st);
+      break;
+    }
     case KK_TMA: {
       const void *tptr = p.tma.mode == 0 ? src : (const void *)dst;
       std::array<uint64_t, 16> map;
@@ -611,7 +655,9 @@ axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t 
         if (p.tm_cache->maps.size() >= 32) p.tm_cache->maps.erase(p.tm_cache->maps.begin());
         p.tm_cache->maps.push_back({tptr, map});
       }
-      e = launch_tma(map.data(), p.tma, p.blocks, src, dst, st);
+      TmaParams k = p.tma;
+      k.dep = dep;
+      e = launch_tma(map.data(), k, p.blocks, src, dst, st);
       break;
     }
     default: AXE_FAIL(AXE_ERR_UNSUPPORTED, "unknown kernel");

@@ -71,5 +71,8 @@ cudaError_t launch_tma(const void *map128, const TmaParams &p, unsigned blocks, 
 size_t tma_smem_bytes(const TmaParams &p);
 int num_sms();
 int64_t kernel_launches();
+// 1 if a kernel reading [s0,s1) and writing [d0,d1) on stream st must wait for
+// the previous libaxe kernel on st (records the new kernel as the previous one).
+int stream_dependency(cudaStream_t st, uintptr_t s0, uintptr_t s1, uintptr_t d0, uintptr_t d1);
 
 }  // namespace axe
