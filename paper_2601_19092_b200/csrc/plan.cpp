@@ -492,7 +492,9 @@ static bool build_tma(const std::vector<Joint> &J0, const Linear &ls, const Line
   k.mode = mode;
   k.nrep = (int)reps.size();
   for (size_t i = 0; i < reps.size(); i++) k.rep[i] = reps[i] * es;
-  int64_t stage_bytes = env_int("AXE_TMA_STAGE_BYTES", 49152);
+  // 24 KiB of boxes per CTA (3 x 8 KiB for config 2) and ~8 CTAs per SM measured best at
+  // both 64 MiB and 1 GiB (profiles/r01_tuning.md)
+  int64_t stage_bytes = env_int("AXE_TMA_STAGE_BYTES", 24576);
   int stages = (int)std::max<int64_t>(2, std::min<int64_t>(16, stage_bytes / box_bytes));
   k.stages = stages;
   P->tm_swizzle = span;
