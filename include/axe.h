@@ -214,14 +214,18 @@ axe_status axe_redist_plan_execute(const axe_redist_plan *plan, axe_comm *comm, 
  * counts and the kernels used. */
 axe_status axe_redist_plan_describe(const axe_redist_plan *plan, char *buf, int capacity);
 /* Host-side view of the plan for tests: for peer p, *send = elements this rank
- * sends to p, *recv = elements it receives from p (p == rank: local copy). */
+ * sends to p, *recv = elements it receives from p (p == rank: both are the
+ * number of elements copied locally). */
 axe_status axe_redist_plan_counts(const axe_redist_plan *plan, int peer, int64_t *send, int64_t *recv);
-/* Host-side view for tests: the k-th (k < send count) element this rank sends to
- * peer in packed order, as (source element index in src_local storage order,
- * destination element index in the peer's dst_local storage; -1 if the
- * destination cell has several replicas -> first of them). */
-axe_status axe_redist_plan_send_map(const axe_redist_plan *plan, int peer, int64_t k, int64_t *src_elem,
-                                    int64_t *dst_elem);
+/* Host-side view for tests, element k in wire order:
+ *   kind 0 (send to peer, k < send count): *a = source element index in this
+ *          rank's src_local storage (before the storage swizzle), *b = -1;
+ *   kind 1 (receive from peer, k < recv count): *a = destination element index
+ *          in this rank's dst_local (the first destination replica), *b = -1;
+ *   kind 2 (local copy, k < counts(rank)): *a = source element, *b = destination
+ *          element (first replica).
+ * A sender's k-th element to p is the receiver's k-th element from the sender. */
+axe_status axe_redist_plan_map(const axe_redist_plan *plan, int kind, int peer, int64_t k, int64_t *a, int64_t *b);
 void axe_redist_plan_destroy(axe_redist_plan *plan);
 
 /* One-shot collective redistribute (plans through an internal cache). */

@@ -81,7 +81,7 @@ _SIGS = {
     "axe_redist_plan_execute": ([_vp, _vp, _vp, _vp, _vp], C.c_int),
     "axe_redist_plan_describe": ([_vp, C.c_char_p, C.c_int], C.c_int),
     "axe_redist_plan_counts": ([_vp, C.c_int, _pi64, _pi64], C.c_int),
-    "axe_redist_plan_send_map": ([_vp, C.c_int, _i64, _pi64, _pi64], C.c_int),
+    "axe_redist_plan_map": ([_vp, C.c_int, C.c_int, _i64, _pi64, _pi64], C.c_int),
     "axe_redist_plan_destroy": ([_vp], None),
     "axe_redistribute": ([_vp, C.POINTER(axe_storage), _vp, _vp, C.POINTER(axe_storage), _vp, C.c_int, _vp, _vp],
                          C.c_int),
@@ -305,6 +305,101 @@ def axe_copy(src, src_st, src_buf, dst, dst_st, dst_buf, elem_size: int, stream=
     ds, k2 = make_storage(dst_st)
     _check(_lib.axe_copy(s.handle, C.byref(ss), _ptr(src_buf), d.handle, C.byref(ds), _ptr(dst_buf), elem_size,
                          _stream(stream)), "axe_copy")
+
+
+# --------------------------------------------------------------------------- redistribute
+def get_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib.axe_get_unique_id(buf), "axe_get_unique_id")
+    return buf.raw
+
+
+class Comm:
+    """axe_comm_create: an NCCL communicator owned by libaxe.  The 128-byte id is created on rank 0
+    (get_unique_id) and broadcast by the caller, e.g. over a torch.distributed process group."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+        h = C.c_void_p()
+        _check(_lib.axe_comm_create(uid, nranks, rank, device, C.byref(h)), "axe_comm_create")
+        self._h, self.nranks, self.rank = h, nranks, rank
+
+    @classmethod
+    def from_process_group(cls, device: int, group=None) -> "Comm":
+        import torch
+        import torch.distributed as dist
+        rank, ws = dist.get_rank(group), dist.get_world_size(group)
+        obj = [get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(obj[0], ws, rank, device)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.axe_comm_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+
+class RedistPlan:
+    """axe_redist_plan_create / _execute / _describe / _counts / _map (include/axe.h)."""
+
+    def __init__(self, src, src_st, dst, dst_st, elem_size: int, nranks: int, rank: int):
+        self.src, self.dst = Layout.of(src), Layout.of(dst)
+        ss, k1 = make_storage(src_st)
+        ds, k2 = make_storage(dst_st)
+        h = C.c_void_p()
+        _check(_lib.axe_redist_plan_create(self.src.handle, C.byref(ss), self.dst.handle, C.byref(ds), elem_size,
+                                           nranks, rank, C.byref(h)), "axe_redist_plan_create")
+        self._h, self.nranks, self.rank, self.elem_size = h, nranks, rank, elem_size
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.axe_redist_plan_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def execute(self, comm: Comm, src_local, dst_local, stream=None):
+        _check(_lib.axe_redist_plan_execute(self._h, comm.handle, _ptr(src_local), _ptr(dst_local), _stream(stream)),
+               "axe_redist_plan_execute")
+
+    def describe(self) -> dict:
+        buf = C.create_string_buffer(1 << 14)
+        _check(_lib.axe_redist_plan_describe(self._h, buf, len(buf)), "axe_redist_plan_describe")
+        return json.loads(buf.value.decode())
+
+    def counts(self, peer: int):
+        a, b = C.c_int64(), C.c_int64()
+        _check(_lib.axe_redist_plan_counts(self._h, peer, C.byref(a), C.byref(b)), "axe_redist_plan_counts")
+        return a.value, b.value
+
+    def map(self, kind: int, peer: int, k: int):
+        a, b = C.c_int64(), C.c_int64()
+        _check(_lib.axe_redist_plan_map(self._h, kind, peer, k, C.byref(a), C.byref(b)), "axe_redist_plan_map")
+        return a.value, b.value
+
+
+def axe_redistribute(src, src_st, src_local, dst, dst_st, dst_local, elem_size: int, comm: Comm, stream=None):
+    s, d = Layout.of(src), Layout.of(dst)
+    ss, k1 = make_storage(src_st)
+    ds, k2 = make_storage(dst_st)
+    _check(_lib.axe_redistribute(s.handle, C.byref(ss), _ptr(src_local), d.handle, C.byref(ds), _ptr(dst_local),
+                                 elem_size, comm.handle, _stream(stream)), "axe_redistribute")
+
+
+def redist_emulate(plans, src_locals, dst_locals, stream=None):
+    """axe_redist_emulate: every rank's plan on the current device, device-to-device copies as the wire."""
+    n = len(plans)
+    hp = (C.c_void_p * n)(*[p.handle.value for p in plans])
+    sp = (C.c_void_p * n)(*[_ptr(x) for x in src_locals])
+    dp = (C.c_void_p * n)(*[_ptr(x) for x in dst_locals])
+    _check(_lib.axe_redist_emulate(hp, n, sp, dp, _stream(stream)), "axe_redist_emulate")
 
 
 def axe_layout_create(D, R=(), O=None) -> Layout:

@@ -5,16 +5,9 @@
 #include <mutex>
 #include <unordered_map>
 
-#include "plan.hpp"
+#include "handles.hpp"
 
 using namespace axe;
-
-struct axe_layout {
-  Layout L;
-};
-struct axe_copy_plan {
-  CopyPlan P;
-};
 
 namespace axe {
 extern std::atomic<int64_t> g_launches;

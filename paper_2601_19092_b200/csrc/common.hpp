@@ -111,21 +111,25 @@ std::string layout_key(const Layout &L);
 // buffer's element index ("memory components").
 struct LinIter {
   int64_t e;
-  int64_t s;  // element-index stride (may be negative)
+  int64_t s;        // element-index stride (may be negative); rank stride when dev
+  int dev = 0;      // 1: a piece on the device axis (gpuid), kept unsplit
 };
 struct Linear {
   std::vector<LinIter> D;  // outermost first
   std::vector<LinIter> R;
   int64_t base = 0;        // element index of f_D(0) + O (the r = 0 representative)
+  int64_t dev_base = 0;    // device-axis component of O
 };
 // Returns false (no error) when the composition is not affine in the digits;
-// the caller then uses the generic kernel.  skip_axis: axis ignored (gpuid).
-bool compose_linear(const Layout &L, const Storage &st, int skip_axis, Linear *out);
+// the caller then uses the generic kernel.  dev_axis: the device axis, whose
+// iters are emitted as dev pieces (only when keep_dev) or dropped.
+bool compose_linear(const Layout &L, const Storage &st, int dev_axis, Linear *out, bool keep_dev = false);
 
 // Joint digit of a copy: one extent, a source and a destination stride.
 struct Joint {
   int64_t e;
   int64_t ss, ds;
+  int sdev = 0, ddev = 0;  // stride is on the device axis (redistribute)
 };
 // Refine two linear shard lists over the same domain into one joint digit list
 // (innermost-first gcd/divisibility pairing; Alg. 1 generalised, R21).

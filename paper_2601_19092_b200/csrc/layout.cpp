@@ -314,7 +314,7 @@ std::string storage_key(const Storage &s) {
 // is split (Lemma split) so every piece lands in one storage
 // digit of axis a; the result is exact iff, per storage digit, the offset's
 // digit plus every piece's contribution stays inside [0, ext) (no carries).
-bool compose_linear(const Layout &L, const Storage &st, int skip_axis, Linear *out) {
+bool compose_linear(const Layout &L, const Storage &st, int skip_axis, Linear *out, bool keep_dev) {
   Linear lin;
   struct Piece {
     int64_t e, t;  // extent, coefficient in storage-digit units
@@ -350,8 +350,11 @@ bool compose_linear(const Layout &L, const Storage &st, int skip_axis, Linear *o
   };
   auto emit = [&](const std::vector<Iter> &src, std::vector<LinIter> &dst) -> bool {
     for (auto &it : src) {
-      if (it.a == skip_axis) continue;
       if (it.e == 1) continue;
+      if (it.a == skip_axis) {
+        if (keep_dev) dst.push_back(LinIter{it.e, it.s, 1});
+        continue;
+      }
       if (!st.binds(it.a)) return false;
       std::vector<Piece> pcs;
       if (!split(it, pcs)) return false;
@@ -381,6 +384,7 @@ bool compose_linear(const Layout &L, const Storage &st, int skip_axis, Linear *o
   }
   for (auto &p : L.O)
     if (p.first != skip_axis && !st.binds(p.first)) return false;
+  if (skip_axis >= 0) lin.dev_base = L.offset(skip_axis);
   *out = std::move(lin);
   return true;
 }
@@ -393,8 +397,8 @@ static std::vector<LinIter> normalize_lin(const std::vector<LinIter> &D) {
     out.push_back(it);
     while (out.size() >= 2) {
       LinIter &p = out[out.size() - 2], &q = out.back();
-      if (p.s == q.e * q.s) {
-        LinIter m{p.e * q.e, q.s};
+      if (p.dev == q.dev && p.s == q.e * q.s) {
+        LinIter m{p.e * q.e, q.s, q.dev};
         out.pop_back();
         out.back() = m;
       } else {
@@ -416,16 +420,16 @@ bool joint_refine(const std::vector<LinIter> &src_in, const std::vector<LinIter>
   while (!a.empty() && !b.empty()) {
     LinIter &x = a.back(), &y = b.back();
     if (x.e == y.e) {
-      J.push_back(Joint{x.e, x.s, y.s});
+      J.push_back(Joint{x.e, x.s, y.s, x.dev, y.dev});
       a.pop_back();
       b.pop_back();
     } else if (x.e % y.e == 0) {
-      J.push_back(Joint{y.e, x.s, y.s});
-      x = LinIter{x.e / y.e, x.s * y.e};
+      J.push_back(Joint{y.e, x.s, y.s, x.dev, y.dev});
+      x = LinIter{x.e / y.e, x.s * y.e, x.dev};
       b.pop_back();
     } else if (y.e % x.e == 0) {
-      J.push_back(Joint{x.e, x.s, y.s});
-      y = LinIter{y.e / x.e, y.s * x.e};
+      J.push_back(Joint{x.e, x.s, y.s, x.dev, y.dev});
+      y = LinIter{y.e / x.e, y.s * x.e, y.dev};
       a.pop_back();
     } else {
       return false;
@@ -439,8 +443,8 @@ bool joint_refine(const std::vector<LinIter> &src_in, const std::vector<LinIter>
     F.push_back(j);
     while (F.size() >= 2) {
       Joint &p = F[F.size() - 2], &q = F.back();
-      if (p.ss == q.e * q.ss && p.ds == q.e * q.ds) {
-        Joint m{p.e * q.e, q.ss, q.ds};
+      if (p.sdev == q.sdev && p.ddev == q.ddev && p.ss == q.e * q.ss && p.ds == q.e * q.ds) {
+        Joint m{p.e * q.e, q.ss, q.ds, q.sdev, q.ddev};
         F.pop_back();
         F.back() = m;
       } else {

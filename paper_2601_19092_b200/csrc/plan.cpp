@@ -615,6 +615,13 @@ int stream_dependency(cudaStream_t st, uintptr_t s0, uintptr_t s1, uintptr_t d0,
   return dep;
 }
 
+// Work the library does not launch itself (NCCL, memcpy) was enqueued on st:
+// the next libaxe kernel there must wait (full dependency).
+void stream_forget(cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_dep_mu);
+  g_last.erase(st);
+}
+
 axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t st) {
   uintptr_t s = (uintptr_t)src, d = (uintptr_t)dst;
   if (!src || !dst) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL buffer");

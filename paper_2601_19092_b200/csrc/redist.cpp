@@ -1,34 +1,574 @@
-// redist.cpp -- axe_redistribute (placeholder until the NCCL path lands).
-#include "plan.hpp"
+// redist.cpp -- axe_redistribute: layout-driven resharding across the device
+// axis "gpuid" (P:173-199 distributed layouts; P:399-403 DTensor signatures;
+// P:408 "a copy might involve an all-gather ... under the hood").
+//
+// Planning (host, identical on every rank):
+//   1. compose both layouts with their local storages, keeping the gpuid
+//      pieces (compose_linear keep_dev) and refine them jointly;
+//   2. joint digits touching gpuid on either side index "blocks" (one
+//      (source rank, destination rank) pair each); the remaining digits form
+//      one memory-only sub-box shared by every block;
+//   3. every block gets one sender: the destination rank itself when it owns
+//      the element (local copy), else a source replica balanced by egress
+//      (reading R5);
+//   4. per rank: pack plans (src_local -> send staging), NCCL send/recv per
+//      block, unpack plans (recv staging -> dst_local), local copy plans;
+//      pack/unpack are elided when a block is contiguous on that side, and an
+//      all-gather pattern is lowered to ncclAllGather.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <numeric>
+#include <unordered_map>
+
+#include "handles.hpp"
 
 using namespace axe;
 
-extern "C" {
-struct axe_comm { int dummy; };
-struct axe_redist_plan { int dummy; };
+namespace axe {
+void stream_forget(cudaStream_t st);
+}
 
-axe_status axe_get_unique_id(uint8_t out[128]) { (void)out; AXE_FAIL(AXE_ERR_UNSUPPORTED, "not yet implemented"); }
-axe_status axe_comm_create(const uint8_t id[128], int nranks, int rank, int dev, axe_comm **out) {
-  (void)id; (void)nranks; (void)rank; (void)dev; (void)out;
-  AXE_FAIL(AXE_ERR_UNSUPPORTED, "not yet implemented");
+struct axe_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 0, rank = 0, device = 0;
+};
+
+namespace {
+
+struct Xfer {
+  int peer = -1;
+  int64_t ms = 0, md = 0;          // element offsets (source local, destination local)
+  bool elided = false;             // send straight from src / receive straight into dst
+  int64_t stage = 0;               // element offset in the staging buffer when not elided
+  std::shared_ptr<CopyPlan> plan;  // pack (send), unpack (recv) or local copy
+};
+
+}  // namespace
+
+struct axe_redist_plan {
+  int nranks = 0, rank = 0, es = 0;
+  std::vector<Joint> M;            // memory-only digits, packed order (outermost first)
+  std::vector<int64_t> packed;     // packed (compact) element strides of M
+  int64_t n = 1;                   // elements per block
+  std::vector<Xfer> sends, recvs, locals;
+  int64_t send_elems = 0, recv_elems = 0;
+  int64_t src_cells = 0, dst_cells = 0;
+  bool allgather = false;
+  int64_t ag_src = 0, ag_dst = 0;  // element offsets of the all-gather
+  std::string desc;
+  // scratch owned by the plan (allocated on first execute, on the current device)
+  mutable std::mutex mu;
+  mutable void *send_buf = nullptr, *recv_buf = nullptr;
+  mutable cudaStream_t side = nullptr;
+  mutable cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  ~axe_redist_plan() {
+    if (send_buf) cudaFree(send_buf);
+    if (recv_buf) cudaFree(recv_buf);
+    if (side) cudaStreamDestroy(side);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+  }
+};
+
+namespace {
+
+Layout mlayout(const std::vector<std::pair<int64_t, int64_t>> &D, const std::vector<LinIter> &R, int64_t off) {
+  std::vector<Iter> d, r;
+  for (auto &p : D) d.push_back(Iter{p.first, p.second, axis_m()});
+  if (d.empty()) d.push_back(Iter{1, 1, axis_m()});
+  for (auto &q : R) r.push_back(Iter{q.e, q.s, axis_m()});
+  std::vector<std::pair<int, int64_t>> o;
+  if (off) o.push_back({axis_m(), off});
+  Layout L;
+  make_layout(d, r, o, &L);
+  return L;
 }
-void axe_comm_destroy(axe_comm *c) { delete c; }
-axe_status axe_redist_plan_create(const axe_layout *, const axe_storage *, const axe_layout *, const axe_storage *,
-                                  int, int, int, axe_redist_plan **) {
-  AXE_FAIL(AXE_ERR_UNSUPPORTED, "not yet implemented");
+
+Storage mstorage(int64_t cells, const Storage *swz_from) {
+  Storage s;
+  s.d.push_back(SDigit{axis_m(), cells, 1, 1});
+  s.cells = cells;
+  if (swz_from) {
+    s.swz_b = swz_from->swz_b;
+    s.swz_m = swz_from->swz_m;
+    s.swz_s = swz_from->swz_s;
+  }
+  return s;
 }
-axe_status axe_redist_plan_execute(const axe_redist_plan *, axe_comm *, const void *, void *, void *) {
-  AXE_FAIL(AXE_ERR_UNSUPPORTED, "not yet implemented");
+
+axe_status subplan(const Layout &src, const Storage &sst, const Layout &dst, const Storage &dstst, int es,
+                   std::shared_ptr<CopyPlan> *out) {
+  auto p = std::make_shared<CopyPlan>();
+  PlanRequest rq{&src, &dst, &sst, &dstst, es, AXE_KERNEL_AUTO, 16, -1};
+  AXE_TRY(plan_copy(rq, p.get()));
+  *out = p;
+  return AXE_OK;
 }
-axe_status axe_redist_plan_describe(const axe_redist_plan *, char *, int) { AXE_FAIL(AXE_ERR_UNSUPPORTED, "nyi"); }
-axe_status axe_redist_plan_counts(const axe_redist_plan *, int, int64_t *, int64_t *) { AXE_FAIL(AXE_ERR_UNSUPPORTED, "nyi"); }
-axe_status axe_redist_plan_send_map(const axe_redist_plan *, int, int64_t, int64_t *, int64_t *) { AXE_FAIL(AXE_ERR_UNSUPPORTED, "nyi"); }
+
+}  // namespace
+
+static axe_status plan_redist(const Layout &S, const Storage &sst, const Layout &T, const Storage &dstst, int es,
+                              int nranks, int rank, axe_redist_plan *P) {
+  const int g = axis_gpuid();
+  if (es != 1 && es != 2 && es != 4 && es != 8 && es != 16)
+    AXE_FAIL(AXE_ERR_ALIGNMENT, "elem_size %d not in {1,2,4,8,16}", es);
+  if (nranks < 1 || rank < 0 || rank >= nranks) AXE_FAIL(AXE_ERR_INVALID_ARG, "bad rank %d of %d", rank, nranks);
+  if (S.ED != T.ED) AXE_FAIL(AXE_ERR_SIZE_MISMATCH, "E_D(src) = %lld != E_D(dst) = %lld", (long long)S.ED, (long long)T.ED);
+  AXE_TRY(check_side(S, sst, g, "source"));
+  AXE_TRY(check_side(T, dstst, g, "destination"));
+  for (const Layout *L : {&S, &T}) {
+    int64_t mn, mx;
+    axis_bounds(*L, g, &mn, &mx);
+    if (mn < 0 || mx >= nranks)
+      AXE_FAIL(AXE_ERR_BOUNDS, "%s layout reaches gpuid in [%lld, %lld] with %d ranks", L == &S ? "source" : "destination",
+               (long long)mn, (long long)mx, nranks);
+  }
+  Linear ls, ld;
+  if (!compose_linear(S, sst, g, &ls, true) || !compose_linear(T, dstst, g, &ld, true))
+    AXE_FAIL(AXE_ERR_UNSUPPORTED, "redistribute needs affine storage compositions");
+  std::vector<Joint> J;
+  if (!joint_refine(ls.D, ld.D, &J))
+    AXE_FAIL(AXE_ERR_UNSUPPORTED, "redistribute: the two digit systems are not nested");
+
+  // destination injectivity over (rank, cell): cumulative separation on the combined index
+  {
+    std::vector<LinIter> all;
+    for (auto *v : {&ld.D, &ld.R})
+      for (auto &it : *v) all.push_back(LinIter{it.e, it.dev ? it.s * dstst.cells : it.s, 0});
+    std::sort(all.begin(), all.end(), [](const LinIter &a, const LinIter &b) { return std::llabs(a.s) < std::llabs(b.s); });
+    int64_t reach = 0;
+    for (auto &it : all) {
+      if (std::llabs(it.s) <= reach)
+        AXE_FAIL(AXE_ERR_NONINJECTIVE, "redistribute: destination layout is not injective over (rank, cell)");
+      reach += (it.e - 1) * std::llabs(it.s);
+    }
+  }
+
+  // replicas: device-axis replica offsets (owners / receivers) and memory replicas of the destination
+  std::vector<int64_t> own{0}, recvr{0};
+  std::vector<LinIter> dst_mem_R;
+  for (auto &r : ls.R)
+    if (r.dev) {
+      std::vector<int64_t> nx;
+      for (int64_t b : own)
+        for (int64_t d = 0; d < r.e; d++) nx.push_back(b + d * r.s);
+      own.swap(nx);
+    }
+  for (auto &r : ld.R) {
+    if (!r.dev) {
+      dst_mem_R.push_back(r);
+      continue;
+    }
+    std::vector<int64_t> nx;
+    for (int64_t b : recvr)
+      for (int64_t d = 0; d < r.e; d++) nx.push_back(b + d * r.s);
+    recvr.swap(nx);
+  }
+
+  std::vector<Joint> G;
+  for (auto &j : J) (j.sdev || j.ddev ? G : P->M).push_back(j);
+  // packed order: destination order (largest |dst stride| outermost)
+  std::stable_sort(P->M.begin(), P->M.end(), [](const Joint &a, const Joint &b) { return std::llabs(a.ds) > std::llabs(b.ds); });
+  P->n = 1;
+  for (auto &m : P->M) P->n *= m.e;
+  P->packed.assign(P->M.size(), 1);
+  for (int k = (int)P->M.size() - 2; k >= 0; k--) P->packed[k] = P->packed[k + 1] * P->M[k + 1].e;
+
+  int64_t nblk = (int64_t)recvr.size();
+  for (auto &j : G) nblk *= j.e;
+  if (nblk > (1 << 20)) AXE_FAIL(AXE_ERR_UNSUPPORTED, "redistribute: %lld blocks", (long long)nblk);
+
+  struct Blk {
+    int snd, rcv;
+    int64_t ms, md;
+  };
+  std::vector<Blk> blocks;
+  std::vector<int64_t> egress(nranks, 0);
+  std::vector<int64_t> dig(G.size(), 0);
+  for (int64_t b = 0; b < (int64_t)(nblk / recvr.size()); b++) {
+    int64_t rem = b, gs = ls.dev_base, ms = ls.base, gd0 = ld.dev_base, md = ld.base;
+    for (int k = (int)G.size() - 1; k >= 0; k--) {
+      int64_t d = rem % G[k].e;
+      rem /= G[k].e;
+      (G[k].sdev ? gs : ms) += d * G[k].ss;
+      (G[k].ddev ? gd0 : md) += d * G[k].ds;
+    }
+    std::vector<int> owners;
+    for (int64_t o : own) owners.push_back((int)(gs + o));
+    std::sort(owners.begin(), owners.end());
+    owners.erase(std::unique(owners.begin(), owners.end()), owners.end());
+    for (int64_t r : recvr) {
+      int gd = (int)(gd0 + r);
+      int snd;
+      if (std::find(owners.begin(), owners.end(), gd) != owners.end()) {
+        snd = gd;
+      } else {
+        int dflt = owners[(size_t)gd % owners.size()];
+        int best = dflt;
+        for (int o : owners)
+          if (egress[o] < egress[best]) best = o;
+        snd = egress[best] + P->n <= egress[dflt] ? best : dflt;  // keep the default unless clearly unbalanced
+        egress[snd] += P->n;
+      }
+      blocks.push_back(Blk{snd, gd, ms, md});
+    }
+  }
+
+  P->nranks = nranks;
+  P->rank = rank;
+  P->es = es;
+  P->src_cells = sst.cells;
+  P->dst_cells = dstst.cells;
+  // contiguity of a block on each side in packed order
+  bool src_contig = !sst.swz_b, dst_contig = !dstst.swz_b && dst_mem_R.empty();
+  for (size_t k = 0; k < P->M.size(); k++) {
+    if (P->M[k].ss != P->packed[k]) src_contig = false;
+    if (P->M[k].ds != P->packed[k]) dst_contig = false;
+  }
+  std::vector<std::pair<int64_t, int64_t>> Dsrc, Ddst, Dpk;
+  for (size_t k = 0; k < P->M.size(); k++) {
+    Dsrc.push_back({P->M[k].e, P->M[k].ss});
+    Ddst.push_back({P->M[k].e, P->M[k].ds});
+    Dpk.push_back({P->M[k].e, P->packed[k]});
+  }
+  // this rank's lists (block order within each peer is the global block order)
+  for (auto &b : blocks) {
+    Xfer x;
+    x.ms = b.ms;
+    x.md = b.md;
+    if (b.snd == rank && b.rcv == rank) {
+      x.peer = rank;
+      P->locals.push_back(x);
+    } else if (b.snd == rank) {
+      x.peer = b.rcv;
+      x.elided = src_contig;
+      P->sends.push_back(x);
+    } else if (b.rcv == rank) {
+      x.peer = b.snd;
+      x.elided = dst_contig;
+      P->recvs.push_back(x);
+    }
+  }
+  auto by_peer = [](const Xfer &a, const Xfer &b) { return a.peer < b.peer; };
+  std::stable_sort(P->sends.begin(), P->sends.end(), by_peer);
+  std::stable_sort(P->recvs.begin(), P->recvs.end(), by_peer);
+  for (auto &x : P->sends)
+    if (!x.elided) {
+      x.stage = P->send_elems;
+      P->send_elems += P->n;
+    }
+  for (auto &x : P->recvs)
+    if (!x.elided) {
+      x.stage = P->recv_elems;
+      P->recv_elems += P->n;
+    }
+  Storage s_src = mstorage(sst.cells, &sst), s_dst = mstorage(dstst.cells, &dstst);
+  Storage s_send = mstorage(std::max<int64_t>(1, P->send_elems), nullptr);
+  Storage s_recv = mstorage(std::max<int64_t>(1, P->recv_elems), nullptr);
+  for (auto &x : P->sends)
+    if (!x.elided) AXE_TRY(subplan(mlayout(Dsrc, {}, x.ms), s_src, mlayout(Dpk, {}, x.stage), s_send, es, &x.plan));
+  for (auto &x : P->recvs)
+    if (!x.elided)
+      AXE_TRY(subplan(mlayout(Dpk, {}, x.stage), s_recv, mlayout(Ddst, dst_mem_R, x.md), s_dst, es, &x.plan));
+  for (auto &x : P->locals)
+    AXE_TRY(subplan(mlayout(Dsrc, {}, x.ms), s_src, mlayout(Ddst, dst_mem_R, x.md), s_dst, es, &x.plan));
+
+  // all-gather pattern (decided from the global block list, so every rank agrees):
+  // each rank r sends one contiguous block at the same offset to every other rank and
+  // holds it locally; rank r's block lands contiguous at dst offset base + r * n everywhere.
+  {
+    bool ag = nranks > 1 && src_contig && dst_contig && (int64_t)blocks.size() == (int64_t)nranks * nranks;
+    int64_t base = 0, soff = -1;
+    if (ag) {
+      std::map<std::pair<int, int>, const Blk *> m;
+      for (auto &b : blocks) m[{b.snd, b.rcv}] = &b;
+      if ((int)m.size() != nranks * nranks) ag = false;
+      for (int r = 0; ag && r < nranks; r++)
+        for (int q = 0; ag && q < nranks; q++) {
+          const Blk *b = m[{r, q}];
+          if (!b) {
+            ag = false;
+            break;
+          }
+          if (r == 0 && q == 0) {
+            base = b->md;
+            soff = b->ms;
+          }
+          if (b->ms != soff || b->md != base + (int64_t)r * P->n) ag = false;
+        }
+    }
+    if (ag) {
+      P->allgather = true;
+      P->ag_src = soff;
+      P->ag_dst = base;
+    }
+  }
+  char buf[512];
+  int64_t sc = 0, rc = 0;
+  for (auto &x : P->sends) sc += P->n;
+  for (auto &x : P->recvs) rc += P->n;
+  int ps = 0, pu = 0;
+  for (auto &x : P->sends) ps += !x.elided;
+  for (auto &x : P->recvs) pu += !x.elided;
+  snprintf(buf, sizeof buf,
+           "{\"pattern\":\"%s\",\"nranks\":%d,\"rank\":%d,\"block_elems\":%lld,\"blocks\":%lld,\"sends\":%zu,"
+           "\"recvs\":%zu,\"locals\":%zu,\"send_elems\":%lld,\"recv_elems\":%lld,\"packs\":%d,\"unpacks\":%d,"
+           "\"owner_replicas\":%zu,\"receiver_replicas\":%zu}",
+           P->allgather ? "allgather" : (P->sends.empty() && P->recvs.empty() ? "local" : "exchange"), nranks, rank,
+           (long long)P->n, (long long)blocks.size(), P->sends.size(), P->recvs.size(), P->locals.size(), (long long)sc,
+           (long long)rc, ps, pu, own.size(), recvr.size());
+  P->desc = buf;
+  return AXE_OK;
+}
+
+static axe_status ensure_scratch(const axe_redist_plan *P) {
+  std::lock_guard<std::mutex> lk(P->mu);
+  cudaError_t e = cudaSuccess;
+  if (!P->send_buf && P->send_elems) e = cudaMalloc(&P->send_buf, (size_t)(P->send_elems * P->es));
+  if (e == cudaSuccess && !P->recv_buf && P->recv_elems) e = cudaMalloc(&P->recv_buf, (size_t)(P->recv_elems * P->es));
+  if (e == cudaSuccess && !P->side) e = cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess && !P->ev_fork) e = cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess && !P->ev_join) e = cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming);
+  if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "redistribute scratch: %s", cudaGetErrorString(e));
+  return AXE_OK;
+}
+
+#define NCCL_TRY(call)                                                                  \
+  do {                                                                                  \
+    ncclResult_t _r = (call);                                                           \
+    if (_r != ncclSuccess) AXE_FAIL(AXE_ERR_NCCL, "%s: %s", #call, ncclGetErrorString(_r)); \
+  } while (0)
+
+static axe_status exec_redist(const axe_redist_plan *P, axe_comm *C, const void *src, void *dst, cudaStream_t st) {
+  if (!C || !C->comm) AXE_FAIL(AXE_ERR_INVALID_ARG, "no communicator");
+  if (C->nranks != P->nranks || C->rank != P->rank)
+    AXE_FAIL(AXE_ERR_INVALID_ARG, "plan for rank %d/%d used on comm rank %d/%d", P->rank, P->nranks, C->rank, C->nranks);
+  const uint8_t *s = (const uint8_t *)src;
+  uint8_t *d = (uint8_t *)dst;
+  const size_t bytes = (size_t)(P->n * P->es);
+  if (P->allgather) {
+    NCCL_TRY(ncclAllGather(s + P->ag_src * P->es, d + P->ag_dst * P->es, bytes, ncclUint8, C->comm, st));
+    stream_forget(st);
+    return AXE_OK;
+  }
+  AXE_TRY(ensure_scratch(P));
+  // local copies on a side stream, overlapping pack + exchange
+  cudaError_t e = cudaSuccess;
+  if (!P->locals.empty()) {
+    e = cudaEventRecord(P->ev_fork, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(P->side, P->ev_fork, 0);
+    if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "fork: %s", cudaGetErrorString(e));
+    stream_forget(P->side);
+    for (auto &x : P->locals) AXE_TRY(run_copy(*x.plan, src, dst, P->side));
+  }
+  for (auto &x : P->sends)
+    if (!x.elided) AXE_TRY(run_copy(*x.plan, src, P->send_buf, st));
+  NCCL_TRY(ncclGroupStart());
+  for (auto &x : P->sends) {
+    const void *ptr = x.elided ? (const void *)(s + x.ms * P->es) : (const void *)((uint8_t *)P->send_buf + x.stage * P->es);
+    NCCL_TRY(ncclSend(ptr, bytes, ncclUint8, x.peer, C->comm, st));
+  }
+  for (auto &x : P->recvs) {
+    void *ptr = x.elided ? (void *)(d + x.md * P->es) : (void *)((uint8_t *)P->recv_buf + x.stage * P->es);
+    NCCL_TRY(ncclRecv(ptr, bytes, ncclUint8, x.peer, C->comm, st));
+  }
+  NCCL_TRY(ncclGroupEnd());
+  stream_forget(st);  // the next libaxe kernel on st waits for NCCL (full dependency)
+  for (auto &x : P->recvs)
+    if (!x.elided) AXE_TRY(run_copy(*x.plan, P->recv_buf, dst, st));
+  if (!P->locals.empty()) {
+    e = cudaEventRecord(P->ev_join, P->side);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, P->ev_join, 0);
+    if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "join: %s", cudaGetErrorString(e));
+  }
+  return AXE_OK;
+}
+
+extern "C" {
+
+axe_status axe_get_unique_id(uint8_t out[128]) {
+  if (!out) AXE_FAIL(AXE_ERR_INVALID_ARG, "out is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  memcpy(out, &id, 128);
+  return AXE_OK;
+}
+
+axe_status axe_comm_create(const uint8_t id[128], int nranks, int rank, int cuda_device, axe_comm **out) {
+  if (!id || !out) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks) AXE_FAIL(AXE_ERR_INVALID_ARG, "bad rank %d of %d", rank, nranks);
+  cudaError_t e = cudaSetDevice(cuda_device);
+  if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "cudaSetDevice(%d): %s", cuda_device, cudaGetErrorString(e));
+  ncclUniqueId uid;
+  memcpy(&uid, id, 128);
+  auto *c = new axe_comm;
+  ncclResult_t r = ncclCommInitRank(&c->comm, nranks, uid, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    AXE_FAIL(AXE_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = cuda_device;
+  *out = c;
+  return AXE_OK;
+}
+
+void axe_comm_destroy(axe_comm *c) {
+  if (!c) return;
+  if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+}
+
+axe_status axe_redist_plan_create(const axe_layout *src, const axe_storage *src_st, const axe_layout *dst,
+                                  const axe_storage *dst_st, int elem_size, int nranks, int rank,
+                                  axe_redist_plan **out) {
+  if (!src || !dst || !out) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
+  *out = nullptr;
+  Storage ss, ds;
+  AXE_TRY(make_storage(src_st, &ss));
+  AXE_TRY(make_storage(dst_st, &ds));
+  auto *p = new axe_redist_plan;
+  axe_status st = plan_redist(src->L, ss, dst->L, ds, elem_size, nranks, rank, p);
+  if (st != AXE_OK) {
+    delete p;
+    return st;
+  }
+  *out = p;
+  return AXE_OK;
+}
+
+axe_status axe_redist_plan_execute(const axe_redist_plan *plan, axe_comm *comm, const void *src_local, void *dst_local,
+                                   void *stream) {
+  if (!plan) AXE_FAIL(AXE_ERR_INVALID_ARG, "plan is NULL");
+  return exec_redist(plan, comm, src_local, dst_local, (cudaStream_t)stream);
+}
+
+axe_status axe_redist_plan_describe(const axe_redist_plan *plan, char *buf, int capacity) {
+  if (!plan || !buf) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
+  if ((int)plan->desc.size() + 1 > capacity) AXE_FAIL(AXE_ERR_CAPACITY, "need %d bytes", (int)plan->desc.size() + 1);
+  memcpy(buf, plan->desc.c_str(), plan->desc.size() + 1);
+  return AXE_OK;
+}
+
+axe_status axe_redist_plan_counts(const axe_redist_plan *plan, int peer, int64_t *send, int64_t *recv) {
+  if (!plan || !send || !recv) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
+  if (peer < 0 || peer >= plan->nranks) AXE_FAIL(AXE_ERR_DOMAIN, "peer %d out of range", peer);
+  *send = *recv = 0;
+  if (peer == plan->rank) {
+    *send = *recv = (int64_t)plan->locals.size() * plan->n;
+    return AXE_OK;
+  }
+  for (auto &x : plan->sends) *send += x.peer == peer ? plan->n : 0;
+  for (auto &x : plan->recvs) *recv += x.peer == peer ? plan->n : 0;
+  return AXE_OK;
+}
+
+axe_status axe_redist_plan_map(const axe_redist_plan *plan, int kind, int peer, int64_t k, int64_t *a, int64_t *b) {
+  if (!plan || !a || !b) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
+  const std::vector<Xfer> &lst = kind == 0 ? plan->sends : kind == 1 ? plan->recvs : plan->locals;
+  if (kind < 0 || kind > 2) AXE_FAIL(AXE_ERR_INVALID_ARG, "kind must be 0, 1 or 2");
+  int64_t idx = k / plan->n, j = k % plan->n;
+  const Xfer *x = nullptr;
+  for (auto &e : lst)
+    if (kind == 2 || e.peer == peer) {
+      if (idx == 0) {
+        x = &e;
+        break;
+      }
+      idx--;
+    }
+  if (k < 0 || !x) AXE_FAIL(AXE_ERR_DOMAIN, "element %lld out of range", (long long)k);
+  int64_t so = x->ms, dof = x->md;
+  for (int m = (int)plan->M.size() - 1; m >= 0; m--) {
+    int64_t d = j % plan->M[m].e;
+    j /= plan->M[m].e;
+    so += d * plan->M[m].ss;
+    dof += d * plan->M[m].ds;
+  }
+  *a = kind == 1 ? dof : so;
+  *b = kind == 2 ? dof : -1;
+  return AXE_OK;
+}
+
 void axe_redist_plan_destroy(axe_redist_plan *p) { delete p; }
-axe_status axe_redistribute(const axe_layout *, const axe_storage *, const void *, const axe_layout *,
-                            const axe_storage *, void *, int, axe_comm *, void *) {
-  AXE_FAIL(AXE_ERR_UNSUPPORTED, "not yet implemented");
+
+axe_status axe_redistribute(const axe_layout *src, const axe_storage *src_st, const void *src_local,
+                            const axe_layout *dst, const axe_storage *dst_st, void *dst_local, int elem_size,
+                            axe_comm *comm, void *stream) {
+  if (!comm) AXE_FAIL(AXE_ERR_INVALID_ARG, "comm is NULL");
+  static std::mutex mu;
+  static std::unordered_map<std::string, std::shared_ptr<axe_redist_plan>> cache;
+  if (!src || !dst) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL layout");
+  Storage ss, ds;
+  AXE_TRY(make_storage(src_st, &ss));
+  AXE_TRY(make_storage(dst_st, &ds));
+  std::string key = layout_key(src->L) + "#" + storage_key(ss) + "#" + layout_key(dst->L) + "#" + storage_key(ds) +
+                    "#" + std::to_string(elem_size) + "#" + std::to_string(comm->nranks) + "#" +
+                    std::to_string(comm->rank) + "#" + std::to_string((uintptr_t)comm);
+  std::shared_ptr<axe_redist_plan> p;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) p = it->second;
+  }
+  if (!p) {
+    p = std::make_shared<axe_redist_plan>();
+    AXE_TRY(plan_redist(src->L, ss, dst->L, ds, elem_size, comm->nranks, comm->rank, p.get()));
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = p;
+  }
+  return exec_redist(p.get(), comm, src_local, dst_local, (cudaStream_t)stream);
 }
-axe_status axe_redist_emulate(const axe_redist_plan *const *, int, const void *const *, void *const *, void *) {
-  AXE_FAIL(AXE_ERR_UNSUPPORTED, "not yet implemented");
+
+axe_status axe_redist_emulate(const axe_redist_plan *const *plans, int nranks, const void *const *src_locals,
+                              void *const *dst_locals, void *stream) {
+  if (!plans || !src_locals || !dst_locals || nranks < 1) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int r = 0; r < nranks; r++) {
+    if (!plans[r] || plans[r]->rank != r || plans[r]->nranks != nranks)
+      AXE_FAIL(AXE_ERR_INVALID_ARG, "plans[%d] is not rank %d of %d", r, r, nranks);
+    AXE_TRY(ensure_scratch(plans[r]));
+  }
+  for (int r = 0; r < nranks; r++)
+    for (auto &x : plans[r]->sends)
+      if (!x.elided) AXE_TRY(run_copy(*x.plan, src_locals[r], plans[r]->send_buf, st));
+  // the wire: the k-th block rank r sends to p is the k-th block p receives from r
+  for (int r = 0; r < nranks; r++)
+    for (int p = 0; p < nranks; p++) {
+      if (p == r) continue;
+      std::vector<const Xfer *> out, in;
+      for (auto &x : plans[r]->sends)
+        if (x.peer == p) out.push_back(&x);
+      for (auto &x : plans[p]->recvs)
+        if (x.peer == r) in.push_back(&x);
+      if (out.size() != in.size())
+        AXE_FAIL(AXE_ERR_INVALID_ARG, "plans disagree: rank %d sends %zu blocks to %d, which expects %zu", r,
+                 out.size(), p, in.size());
+      const size_t bytes = (size_t)(plans[r]->n * plans[r]->es);
+      for (size_t i = 0; i < out.size(); i++) {
+        const uint8_t *sp = out[i]->elided ? (const uint8_t *)src_locals[r] + out[i]->ms * plans[r]->es
+                                           : (const uint8_t *)plans[r]->send_buf + out[i]->stage * plans[r]->es;
+        uint8_t *dp = in[i]->elided ? (uint8_t *)dst_locals[p] + in[i]->md * plans[p]->es
+                                    : (uint8_t *)plans[p]->recv_buf + in[i]->stage * plans[p]->es;
+        cudaError_t e = cudaMemcpyAsync(dp, sp, bytes, cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "emulated exchange: %s", cudaGetErrorString(e));
+      }
+    }
+  stream_forget(st);
+  for (int r = 0; r < nranks; r++) {
+    for (auto &x : plans[r]->recvs)
+      if (!x.elided) AXE_TRY(run_copy(*x.plan, plans[r]->recv_buf, dst_locals[r], st));
+    for (auto &x : plans[r]->locals) AXE_TRY(run_copy(*x.plan, src_locals[r], dst_locals[r], st));
+  }
+  return AXE_OK;
 }
-}
+
+}  // extern "C"
