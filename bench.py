@@ -165,6 +165,58 @@ def run_reference(args):
     }), flush=True)
 
 
+def measure_reshard(axe, torch, dist, ws, rank, local, stream, iters=20, warm=3):
+    """axe_redistribute over NCCL on all ranks (BASELINE configs 4 and 5).  Bus GB/s = per-GPU NVLink
+    ingress bytes / time (max over ranks), i.e. NCCL's busbw for all-gather / all-to-all."""
+    comm = axe.Comm.from_process_group(local)
+    res = {}
+
+    def timed(fn):
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / iters], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # config 4: 16384^2 bf16, shard(dim0) -> replicate over P = ws
+    c4 = synth.config4(ws)
+    p4 = axe.RedistPlan(c4["src"], c4["src_st"], c4["dst"], c4["dst_st"], 2, ws, rank)
+    src = torch.randint(-2**15, 2**15 - 1, (synth.storage_cells(c4["src_st"]),), dtype=torch.int16, device="cuda")
+    dst = torch.empty(synth.storage_cells(c4["dst_st"]), dtype=torch.int16, device="cuda")
+    ms = timed(lambda: p4.execute(comm, src, dst, stream))
+    ingress = (ws - 1) * src.numel() * 2
+    ref = torch.empty_like(dst)
+    ms_ref = timed(lambda: dist.all_gather_into_tensor(ref, src))
+    res["config4"] = {"P": ws, "pattern": p4.describe()["pattern"], "ms": ms, "ingress_bytes_per_gpu": ingress,
+                      "bus_GBps": ingress / (ms * 1e-3) / 1e9, "frac_of_900": ingress / (ms * 1e-3) / 1e9 / 900,
+                      "frac_of_measured_770": ingress / (ms * 1e-3) / 1e9 / 770,
+                      "torch_all_gather_bus_GBps": ingress / (ms_ref * 1e-3) / 1e9}
+    del src, dst, ref
+    if ws == 8:
+        c5 = synth.config5()
+        p5 = axe.RedistPlan(c5["src"], c5["src_st"], c5["dst"], c5["dst_st"], 2, 8, rank)
+        src = torch.randint(-2**15, 2**15 - 1, (synth.storage_cells(c5["src_st"]),), dtype=torch.int16, device="cuda")
+        dst = torch.empty(synth.storage_cells(c5["dst_st"]), dtype=torch.int16, device="cuda")
+        ms = timed(lambda: p5.execute(comm, src, dst, stream))
+        ingress = max(p5.counts(q)[1] for q in range(8) if q != rank) * 2
+        res["config5"] = {"mesh": "2x4", "pattern": p5.describe()["pattern"], "ms": ms,
+                          "ingress_bytes_per_gpu": ingress, "bus_GBps": ingress / (ms * 1e-3) / 1e9,
+                          "frac_of_900": ingress / (ms * 1e-3) / 1e9 / 900}
+        del src, dst
+    torch.cuda.synchronize()
+    dist.barrier()
+    del comm
+    return res
+
+
 def run_axe(args):
     import torch
     ws, rank, local = dist_init(args)
@@ -283,6 +335,13 @@ def run_axe(args):
         e_ms = float(t.item())
     e2e = ws * alg_bytes / (e_ms * 1e-3) / 1e9
 
+    reshard = None
+    if ws > 1 and not args.no_reshard:
+        try:
+            reshard = measure_reshard(axe, torch, dist, ws, rank, local, stream)
+        except Exception as e:  # keep the contract line even if the reshard leg fails
+            reshard = {"error": f"{type(e).__name__}: {e}"}
+
     peak, peak_src = peaks()
     achieved = alg_bytes / (k_ms * 1e-3) / 1e9
     out = None
@@ -313,6 +372,8 @@ def run_axe(args):
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        if reshard is not None:
+            out["reshard"] = reshard
         print(json.dumps(out), flush=True)
     if dist:
         dist.barrier()
@@ -329,6 +390,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every step directly (no CUDA graph)")
+    ap.add_argument("--no-reshard", action="store_true", help="skip the N>1 axe_redistribute measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

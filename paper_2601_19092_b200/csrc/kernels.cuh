@@ -112,30 +112,31 @@ struct TmaParams {
 };
 
 // ---------------------------------------------------------------- K2 tile
-// A tile = product of the tile digits (src-fast run x dst-fast run x ...),
-// staged through shared memory; the other digits index tiles.
-constexpr int K2_MAXD = 10;
-constexpr int K2_MAXT = 6;
+// A tile = the tile digits (a source-contiguous run x a destination-contiguous
+// run x whatever else they share), staged through shared memory in source
+// order; the other digits index tiles.  Load: every thread moves VS-byte
+// vectors global -> smem; store: every thread gathers granules from smem into
+// VD-byte destination vectors.  All per-thread offsets are tables built on the
+// host: offset(j, t[, k]) = B[j] + A[t] (+ C[k]).
+constexpr int K2_NT = 256;
+constexpr int K2_MAXJ = 16;
+constexpr int K2_MAXK = 16;
 struct K2Params {
-  uint32_t tiles;                 // number of tiles
-  int nd;                         // grid digits, outermost first
-  FastDiv fd[K2_MAXD];
-  int64_t ss[K2_MAXD], ds[K2_MAXD];  // byte strides of the grid digits
-  int64_t sbase, dbase;
-  // tile digits in smem order (outermost first); element strides on each side
-  int nt;
-  FastDiv tfd[K2_MAXT];
-  int64_t tss[K2_MAXT], tds[K2_MAXT];  // byte strides (global)
-  uint32_t tsm[K2_MAXT];              // smem element strides
-  uint32_t tile_elems;
-  // load phase: vectors of lvec elements along the src-fast digit (tile digit ls)
-  // store phase: vectors of svec elements along the dst-fast digit (tile digit ds_)
-  int ls, dsd;
-  uint32_t lvec, svec;
+  uint32_t ntiles;
+  int nout;
+  FastDiv ofd[K1_MAXD];
+  int64_t oss[K1_MAXD], ods[K1_MAXD];  // byte strides of the tile-index digits
+  int64_t sbase, dbase;                // bytes
+  int lj, sj, kg;                      // load iterations, store iterations, granules per store vector
+  int32_t A_l[K2_NT], A_s[K2_NT], A_d[K2_NT];  // bytes: src global, smem (pre-swizzle), dst global
+  int32_t B_l[K2_MAXJ], B_s[K2_MAXJ], B_d[K2_MAXJ];
+  int32_t C_s[K2_MAXK];
+  uint32_t tile_bytes;
+  Swz smsw;                            // shared-memory swizzle chosen by the planner
+  Swz ssw, dsw;                        // global swizzles of the storages
   int nrep;
   int64_t rep[K1_MAXREP];
-  Swz ssw, dsw;
-  uint32_t smem_bytes;
+  int dep;
 };
 
 }  // namespace axe

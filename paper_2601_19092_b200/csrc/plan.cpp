@@ -129,7 +129,7 @@ axe_status check_injective(const Layout &dst, const Storage &st, int skip_axis) 
   return AXE_OK;
 }
 
-static Swz make_swz(const Storage &st) {
+Swz make_swz(const Storage &st) {
   Swz s;
   s.shift = (uint32_t)(st.swz_m + st.swz_s);
   s.mask = st.swz_b > 0 ? (uint32_t)((1u << st.swz_b) - 1) : 0u;
@@ -190,7 +190,7 @@ static axe_status build_k0_side(const Layout &L, const Storage &st, int skip_axi
   return AXE_OK;
 }
 
-static std::string joint_json(const std::vector<Joint> &J) {
+std::string joint_json(const std::vector<Joint> &J) {
   std::string s = "[";
   char b[96];
   for (size_t i = 0; i < J.size(); i++) {
@@ -556,10 +556,27 @@ axe_status plan_copy(const PlanRequest &rq, CopyPlan *out) {
     if (kernel == AXE_KERNEL_TMA)
       AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced TMA kernel cannot run these layouts: %s / %s", w0.c_str(), w1.c_str());
   }
-  if (kernel == AXE_KERNEL_AUTO || kernel == AXE_KERNEL_VECTOR || kernel == AXE_KERNEL_TILE ||
-      kernel == AXE_KERNEL_TMA) {
+  if (joint && kernel == AXE_KERNEL_TILE) {
+    if (build_k2(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &why)) {
+      P.kernel = KK_TILE;
+      *out = std::move(P);
+      return AXE_OK;
+    }
+    AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced tile kernel cannot run these layouts: %s", why.c_str());
+  }
+  if (kernel == AXE_KERNEL_AUTO || kernel == AXE_KERNEL_VECTOR || kernel == AXE_KERNEL_TMA) {
     if (joint && build_k1(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &why)) {
       P.kernel = KK_VECTOR;
+      // narrower than 16-byte vectors on one side: stage through shared memory instead (K2)
+      if (kernel == AXE_KERNEL_AUTO && P.vb < 16) {
+        CopyPlan T = P;
+        std::string w2;
+        if (build_k2(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &T, &w2)) {
+          T.kernel = KK_TILE;
+          *out = std::move(T);
+          return AXE_OK;
+        }
+      }
       *out = std::move(P);
       return AXE_OK;
     }
@@ -641,6 +658,12 @@ axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t 
       K0Params k = p.k0;
       k.dep = dep;
       e = launch_k0(k, src, dst, st);
+      break;
+    }
+    case KK_TILE: {
+      K2Params k = p.k2;
+      k.dep = dep;
+      e = launch_k2(k, p.k2_vs, p.k2_vd, p.k2_gb, p.blocks, src, dst, st);
       break;
     }
     case KK_TMA: {

@@ -36,7 +36,16 @@ struct CopyPlan {
   int tm_swizzle = 0;       // bytes: 0, 32, 64, 128
   int64_t tm_base = 0;      // byte offset of coordinate 0 from the buffer base
   std::shared_ptr<struct TmaCache> tm_cache;
+  // K2 tile
+  K2Params k2;
+  int k2_vs = 0, k2_vd = 0, k2_gb = 0;
 };
+
+bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,
+              const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why);
+cudaError_t launch_k2(const K2Params &p, int vs, int vd, int gb, unsigned blocks, const void *src, void *dst,
+                      cudaStream_t st);
+std::string joint_json(const std::vector<Joint> &J);
 
 struct TmaCache {
   std::mutex mu;

@@ -80,7 +80,7 @@ def test_config2_full(axe, rev, kernel):
     assert desc["kernel"] == ("tma" if kernel == "auto" else kernel)
 
 
-@pytest.mark.parametrize("kernel", ["auto", "generic"])
+@pytest.mark.parametrize("kernel", ["auto", "generic", "vector", "tile"])
 @pytest.mark.parametrize("variant", ["a", "b"])
 def test_config3_small(axe, variant, kernel):
     check(axe, synth.config3(16, variant), kernel)
@@ -193,7 +193,28 @@ def test_random_layout_pairs(axe, seed):
                dst_st=linear_storage(dc, sw), seed=seed)
     check(axe, cfg, "auto")
     check(axe, cfg, "generic")
-    check(axe, cfg, "vector") if axe.CopyPlan(src, cfg["src_st"], dst, cfg["dst_st"], es).describe()["kernel"] != "generic" else None
+    if axe.CopyPlan(src, cfg["src_st"], dst, cfg["dst_st"], es).describe()["kernel"] != "generic":
+        check(axe, cfg, "vector")
+    try:
+        axe.CopyPlan(src, cfg["src_st"], dst, cfg["dst_st"], es, "tile")
+    except axe.AxeError:
+        return
+    check(axe, cfg, "tile")
+
+
+@pytest.mark.parametrize("R,Cn,es", [(256, 512, 2), (512, 256, 4), (128, 384, 8), (256, 256, 1), (64, 96, 16),
+                                     (1024, 64, 2)])
+def test_transposes_all_kernels(axe, R, Cn, es):
+    """Row-major -> column-major at every element size through K2 (smem tile), K1 and the generic kernel."""
+    cfg = dict(name=f"T{R}x{Cn}x{es}", es=es, src=layout([(R, Cn), (Cn, 1)]), src_st=linear_storage(R * Cn),
+               dst=layout([(R, 1), (Cn, R)]), dst_st=linear_storage(R * Cn), seed=R + es)
+    for k in ("auto", "vector", "generic"):
+        check(axe, cfg, k)
+    try:
+        axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], es, "tile")
+    except axe.AxeError:
+        return
+    check(axe, cfg, "tile")
 
 
 def test_alias_and_alignment_errors(axe):

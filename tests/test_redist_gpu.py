@@ -68,6 +68,24 @@ def test_config4_full_p8_sampled_rank(axe):
     run(axe, synth.config4(8), only=[3])
 
 
+def test_nccl_comm_single_rank(axe):
+    """The NCCL path on the one GPU a gpurun box has: a 1-rank communicator, axe_redistribute through
+    the public call (plan cache + execute), checked against the oracle."""
+    comm = axe.Comm(axe.get_unique_id(), 1, 0, torch.cuda.current_device())
+    R, Cn = 64, 48
+    src = layout([(R, Cn), (Cn, 1)])
+    dst = layout([(R, 1), (Cn, R)], [(1, 1, "gpuid")])
+    v = synth.values(R * Cn, 4, 5)
+    x = torch.from_numpy(v.copy()).cuda()
+    y = torch.zeros_like(x)
+    axe.axe_redistribute(src, linear_storage(R * Cn), x, dst, linear_storage(R * Cn), y, 4, comm)
+    torch.cuda.synchronize()
+    exp = np.zeros_like(v)
+    oracle.redistribute(src, linear_storage(R * Cn), [v], dst, linear_storage(R * Cn), [exp], 4)
+    assert np.array_equal(y.cpu().numpy(), exp)
+    del comm
+
+
 @pytest.mark.parametrize("seed", range(8))
 def test_random_meshes(axe, seed):
     """Random 1-D/2-D meshes: the shard axis, the sharded logical dimension and replication are drawn at random."""
