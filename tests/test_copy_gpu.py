@@ -283,3 +283,41 @@ def test_execute_host_e2e(axe):
     plan.execute_host(hs, hd, ds, dd)
     torch.cuda.synchronize()
     assert np.array_equal(hd.numpy(), exp)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_permutes_reduce_to_numpy(axe, seed):
+    """Random N-d permutations (numpy.transpose semantics): src row-major (s0..sn), dst row-major over the
+    permuted dims.  Every kernel that can run the pair must produce numpy's transpose exactly."""
+    rng = np.random.default_rng(77 + seed)
+    nd = int(rng.integers(2, 5))
+    shape = [int(rng.choice([2, 4, 8, 16, 32, 64, 128])) for _ in range(nd)]
+    while np.prod(shape) < 4096:
+        shape[int(rng.integers(0, nd))] *= 2
+    while np.prod(shape) > (1 << 20):
+        i = int(np.argmax(shape))
+        shape[i] //= 2
+    perm = list(rng.permutation(nd))
+    es = int(rng.choice([1, 2, 4, 8]))
+    N = int(np.prod(shape))
+    rs = [int(np.prod(shape[i + 1:])) for i in range(nd)]            # row-major strides of the source
+    pshape = [shape[p] for p in perm]
+    prs = [int(np.prod(pshape[i + 1:])) for i in range(nd)]          # row-major strides of the destination
+    dst_stride = [0] * nd
+    for i, p in enumerate(perm):
+        dst_stride[p] = prs[i]
+    src = layout([(shape[i], rs[i]) for i in range(nd)])
+    dst = layout([(shape[i], dst_stride[i]) for i in range(nd)])
+    dt = {1: np.uint8, 2: np.uint16, 4: np.uint32, 8: np.uint64}[es]
+    v = synth.values(N, es, seed)
+    expect = np.ascontiguousarray(v.view(dt).reshape(shape).transpose(perm)).reshape(-1)
+    for kernel in ("auto", "vector", "tile", "generic"):
+        try:
+            plan = axe.CopyPlan(src, linear_storage(N), dst, linear_storage(N), es, kernel)
+        except axe.AxeError:
+            continue
+        s = torch.from_numpy(v.copy()).cuda()
+        d = torch.zeros_like(s)
+        plan.execute(s, d)
+        torch.cuda.synchronize()
+        assert np.array_equal(d.cpu().numpy().view(dt), expect), (kernel, shape, perm, es, plan.describe())
