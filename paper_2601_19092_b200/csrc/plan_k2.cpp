@@ -8,6 +8,7 @@
 // chosen from the layouts", BASELINE north star; SW-style XOR of 16-byte
 // chunks as in the TMA atoms of P:527).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -157,7 +158,9 @@ bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
     }
     return L;
   };
-  const int64_t budget = 32768 / es;  // tile elements (32 KiB)
+  // tile budget (double-buffered in smem): 16 KiB by default, AXE_K2_TILE_BYTES overrides
+  const char *tb = getenv("AXE_K2_TILE_BYTES");
+  const int64_t budget = ((tb && *tb) ? atoll(tb) : 16384) / es;
   const int NT = K2_NT;
   struct Choice {
     int64_t Ls, Ld, TE, Vs, Vd;
@@ -320,7 +323,7 @@ bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
   P->k2_vd = (int)(Vd * es);
   P->k2_gb = GBB;
   P->align = 16;
-  int per_sm = std::max(1, std::min(8, (int)(200 * 1024 / (TE * es + 1024))));
+  int per_sm = std::max(1, std::min(8, (int)(200 * 1024 / (2 * TE * es + 1024))));
   P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(k.ntiles, (int64_t)num_sms() * per_sm));
   int64_t total = 1;
   for (auto &j : J) total *= j.e;
