@@ -48,7 +48,7 @@ __device__ __forceinline__ typename K2Vec<B>::T ldg(const uint8_t *p) {
     return __ldg(reinterpret_cast<const typename K2Vec<B>::T *>(p));
 }
 
-constexpr int K2_MAXLJ = 8;
+constexpr int K2_MAXLJ = 4;
 
 __device__ __forceinline__ void tile_bases(const K2Params &p, uint32_t i, int64_t &sb, int64_t &db) {
   sb = p.sbase;
@@ -81,38 +81,38 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Two smem buffers: the cp.async loads of tile i+1 run while tile i is gathered and stored.
+// Software pipeline with one smem buffer: the registers hold tile i+1's
+// vectors (loaded while tile i is gathered and stored), so global loads stay in
+// flight across the store phase.
 template <int VS, int VD, int GB>
-__global__ void __launch_bounds__(K2_NT) k2_tile(const __grid_constant__ K2Params p, const uint8_t *__restrict__ src,
-                                                 uint8_t *__restrict__ dst) {
+__global__ void __launch_bounds__(K2_NT, 4) k2_tile(const __grid_constant__ K2Params p, const uint8_t *__restrict__ src,
+                                                    uint8_t *__restrict__ dst) {
   extern __shared__ __align__(128) uint8_t sm[];
+  using TS = typename K2Vec<VS>::T;
   using TD = typename K2Vec<VD>::T;
   using TG = typename K2Vec<GB>::T;
   constexpr int KG = VD / GB;
   const int t = threadIdx.x;
   const int32_t al = p.A_l[t], as = p.A_s[t], ad = p.A_d[t];
-  const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(sm);
   if (p.dep) pdl_wait();
   pdl_launch_dependents();
-  auto issue = [&](uint32_t tile, int buf) {
+  TS v[K2_MAXLJ];
+  auto load = [&](uint32_t tile) {
     int64_t sb, db;
     tile_bases(p, tile, sb, db);
-    const uint32_t b0 = sm0 + (uint32_t)buf * p.tile_bytes;
 #pragma unroll
     for (int j = 0; j < K2_MAXLJ; j++)
-      if (j < p.lj)
-        cp_async<VS>(b0 + swz32(p.smsw, (uint32_t)((j * K2_NT + t) * VS)), src + swz(p.ssw, sb + p.B_l[j] + al));
+      if (j < p.lj) v[j] = ldg<VS>(src + swz(p.ssw, sb + p.B_l[j] + al));
   };
   uint32_t tile = blockIdx.x;
-  if (tile < p.ntiles) issue(tile, 0);
-  cp_async_commit();
-  for (int it = 0; tile < p.ntiles; tile += gridDim.x, it++) {
-    const uint32_t next = tile + gridDim.x;
-    if (next < p.ntiles) issue(next, (it + 1) & 1);
-    cp_async_commit();
-    cp_async_wait<1>();
+  if (tile < p.ntiles) load(tile);
+  while (tile < p.ntiles) {
+#pragma unroll
+    for (int j = 0; j < K2_MAXLJ; j++)
+      if (j < p.lj) *reinterpret_cast<TS *>(sm + swz32(p.smsw, (uint32_t)((j * K2_NT + t) * VS))) = v[j];
     __syncthreads();
-    const uint8_t *buf = sm + (size_t)(it & 1) * p.tile_bytes;
+    const uint32_t next = tile + gridDim.x;
+    if (next < p.ntiles) load(next);
     int64_t sb, db;
     tile_bases(p, tile, sb, db);
 #pragma unroll 4
@@ -121,13 +121,13 @@ __global__ void __launch_bounds__(K2_NT) k2_tile(const __grid_constant__ K2Param
       TG *o = reinterpret_cast<TG *>(&out);
       const uint32_t base = (uint32_t)(as + p.B_s[j]);
 #pragma unroll
-      for (int k = 0; k < KG; k++) o[k] = *reinterpret_cast<const TG *>(buf + swz32(p.smsw, base + p.C_s[k]));
+      for (int k = 0; k < KG; k++) o[k] = *reinterpret_cast<const TG *>(sm + swz32(p.smsw, base + p.C_s[k]));
       const int64_t d = db + p.B_d[j] + ad;
       for (int r = 0; r < p.nrep; r++) *reinterpret_cast<TD *>(dst + swz(p.dsw, d + p.rep[r])) = out;
     }
     __syncthreads();
+    tile = next;
   }
-  cp_async_wait<0>();
 }
 
 template <int VS, int VD, int GB>
@@ -171,7 +171,7 @@ static cudaError_t k2_vd(int vd, int gb, const K2Params &p, unsigned blocks, siz
 
 cudaError_t launch_k2(const K2Params &p, int vs, int vd, int gb, unsigned blocks, const void *src, void *dst,
                       cudaStream_t st) {
-  size_t smem = 2 * (size_t)p.tile_bytes;  // double buffer
+  size_t smem = (size_t)p.tile_bytes;
   cudaError_t e;
   switch (vs) {
     case 4: e = k2_vd<4>(vd, gb, p, blocks, smem, src, dst, st); break;
