@@ -48,45 +48,11 @@ __device__ __forceinline__ typename K2Vec<B>::T ldg(const uint8_t *p) {
     return __ldg(reinterpret_cast<const typename K2Vec<B>::T *>(p));
 }
 
-constexpr int K2_MAXLJ = 4;
+constexpr int K2_MAXLJ = 8;
 
-__device__ __forceinline__ void tile_bases(const K2Params &p, uint32_t i, int64_t &sb, int64_t &db) {
-  sb = p.sbase;
-  db = p.dbase;
-#pragma unroll
-  for (int k = K1_MAXD - 1; k >= 1; k--) {
-    if (k >= p.nout) continue;
-    uint32_t q = fdiv(p.ofd[k], i);
-    uint32_t d = i - q * p.ofd[k].d;
-    i = q;
-    sb += (int64_t)d * p.oss[k];
-    db += (int64_t)d * p.ods[k];
-  }
-  if (p.nout > 0) {
-    sb += (int64_t)i * p.oss[0];
-    db += (int64_t)i * p.ods[0];
-  }
-}
-
-template <int VS>
-__device__ __forceinline__ void cp_async(uint32_t smem_addr, const uint8_t *g) {
-  if constexpr (VS == 16)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(g) : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_addr), "l"(g), "n"(VS) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// Software pipeline with one smem buffer: the registers hold tile i+1's
-// vectors (loaded while tile i is gathered and stored), so global loads stay in
-// flight across the store phase.
 template <int VS, int VD, int GB>
-__global__ void __launch_bounds__(K2_NT, 4) k2_tile(const __grid_constant__ K2Params p, const uint8_t *__restrict__ src,
-                                                    uint8_t *__restrict__ dst) {
+__global__ void __launch_bounds__(K2_NT) k2_tile(const __grid_constant__ K2Params p, const uint8_t *__restrict__ src,
+                                                 uint8_t *__restrict__ dst) {
   extern __shared__ __align__(128) uint8_t sm[];
   using TS = typename K2Vec<VS>::T;
   using TD = typename K2Vec<VD>::T;
@@ -96,26 +62,32 @@ __global__ void __launch_bounds__(K2_NT, 4) k2_tile(const __grid_constant__ K2Pa
   const int32_t al = p.A_l[t], as = p.A_s[t], ad = p.A_d[t];
   if (p.dep) pdl_wait();
   pdl_launch_dependents();
-  TS v[K2_MAXLJ];
-  auto load = [&](uint32_t tile) {
-    int64_t sb, db;
-    tile_bases(p, tile, sb, db);
+  for (uint32_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+    int64_t sb = p.sbase, db = p.dbase;
+    {
+      uint32_t i = tile;
+#pragma unroll
+      for (int k = K1_MAXD - 1; k >= 1; k--) {
+        if (k >= p.nout) continue;
+        uint32_t q = fdiv(p.ofd[k], i);
+        uint32_t d = i - q * p.ofd[k].d;
+        i = q;
+        sb += (int64_t)d * p.oss[k];
+        db += (int64_t)d * p.ods[k];
+      }
+      if (p.nout > 0) {
+        sb += (int64_t)i * p.oss[0];
+        db += (int64_t)i * p.ods[0];
+      }
+    }
+    TS v[K2_MAXLJ];
 #pragma unroll
     for (int j = 0; j < K2_MAXLJ; j++)
       if (j < p.lj) v[j] = ldg<VS>(src + swz(p.ssw, sb + p.B_l[j] + al));
-  };
-  uint32_t tile = blockIdx.x;
-  if (tile < p.ntiles) load(tile);
-  while (tile < p.ntiles) {
 #pragma unroll
     for (int j = 0; j < K2_MAXLJ; j++)
       if (j < p.lj) *reinterpret_cast<TS *>(sm + swz32(p.smsw, (uint32_t)((j * K2_NT + t) * VS))) = v[j];
     __syncthreads();
-    const uint32_t next = tile + gridDim.x;
-    if (next < p.ntiles) load(next);
-    int64_t sb, db;
-    tile_bases(p, tile, sb, db);
-#pragma unroll 4
     for (int j = 0; j < p.sj; j++) {
       TD out;
       TG *o = reinterpret_cast<TG *>(&out);
@@ -126,7 +98,6 @@ __global__ void __launch_bounds__(K2_NT, 4) k2_tile(const __grid_constant__ K2Pa
       for (int r = 0; r < p.nrep; r++) *reinterpret_cast<TD *>(dst + swz(p.dsw, d + p.rep[r])) = out;
     }
     __syncthreads();
-    tile = next;
   }
 }
 
@@ -171,7 +142,7 @@ static cudaError_t k2_vd(int vd, int gb, const K2Params &p, unsigned blocks, siz
 
 cudaError_t launch_k2(const K2Params &p, int vs, int vd, int gb, unsigned blocks, const void *src, void *dst,
                       cudaStream_t st) {
-  size_t smem = (size_t)p.tile_bytes;
+  size_t smem = p.tile_bytes;
   cudaError_t e;
   switch (vs) {
     case 4: e = k2_vd<4>(vd, gb, p, blocks, smem, src, dst, st); break;

@@ -291,6 +291,25 @@ static bool build_k1(const std::vector<Joint> &J0, const Linear &ls, const Linea
   k.ssw = make_swz(sst);
   k.dsw = make_swz(dstst);
   P->covers_all = (int64_t)reps.size() * total * V == dstst.cells;
+  {
+    // sector efficiency of one CTA's worth of vectors (kernel order, dst-contiguous first): a
+    // schedule whose source reads scatter over many 32-byte sectors is better staged through smem
+    const int64_t nv = std::min<int64_t>(total, 1024);
+    std::set<int64_t> ssec, dsec;
+    for (int64_t i = 0; i < nv; i++) {
+      int64_t rem = i, so = 0, dof = 0;
+      for (auto &j : D) {
+        int64_t d = rem % j.e;
+        rem /= j.e;
+        so += d * j.ss;
+        dof += d * j.ds;
+      }
+      for (int64_t b = so * es; b < so * es + (int64_t)(V * es); b += 32) ssec.insert(b >> 5);
+      for (int64_t b = dof * es; b < dof * es + (int64_t)(V * es); b += 32) dsec.insert(b >> 5);
+    }
+    const double useful = (double)nv * V * es;
+    P->k1_sector_eff = std::min(useful / (32.0 * ssec.size()), useful / (32.0 * dsec.size()));
+  }
   P->vb = (int)(V * es);
   P->align = std::max(P->vb, es);
   const int u = k1_unroll(P->vb);
@@ -568,7 +587,7 @@ axe_status plan_copy(const PlanRequest &rq, CopyPlan *out) {
     if (joint && build_k1(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &why)) {
       P.kernel = KK_VECTOR;
       // narrower than 16-byte vectors on one side: stage through shared memory instead (K2)
-      if (kernel == AXE_KERNEL_AUTO && P.vb < 16) {
+      if (kernel == AXE_KERNEL_AUTO && P.vb < 16 && (P.vb <= 2 || P.k1_sector_eff < 0.5)) {
         CopyPlan T = P;
         std::string w2;
         if (build_k2(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &T, &w2)) {

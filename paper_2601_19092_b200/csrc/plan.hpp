@@ -39,6 +39,7 @@ struct CopyPlan {
   // K2 tile
   K2Params k2;
   int k2_vs = 0, k2_vd = 0, k2_gb = 0;
+  double k1_sector_eff = 1.0;  // K1: useful bytes / 32-byte sectors touched by one CTA's vectors (min of both sides)
 };
 
 bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,

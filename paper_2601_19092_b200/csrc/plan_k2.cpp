@@ -8,7 +8,6 @@
 // chosen from the layouts", BASELINE north star; SW-style XOR of 16-byte
 // chunks as in the TMA atoms of P:527).
 #include <algorithm>
-#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -158,9 +157,7 @@ bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
     }
     return L;
   };
-  // tile budget (double-buffered in smem): 16 KiB by default, AXE_K2_TILE_BYTES overrides
-  const char *tb = getenv("AXE_K2_TILE_BYTES");
-  const int64_t budget = ((tb && *tb) ? atoll(tb) : 16384) / es;
+  const int64_t budget = 32768 / es;  // tile elements (32 KiB)
   const int NT = K2_NT;
   struct Choice {
     int64_t Ls, Ld, TE, Vs, Vd;
@@ -185,7 +182,7 @@ bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
       while (Vd * 2 * es <= 16 && Ld % (Vd * 2) == 0) Vd *= 2;
       if (Vs * es < 4 || Vd * es < 4) continue;
       if (TE % (Vs * NT) || TE % (Vd * NT)) continue;
-      if (TE / (Vs * NT) > 4 || TE / (Vd * NT) > K2_MAXJ || Vd / G > K2_MAXK) continue;
+      if (TE / (Vs * NT) > 8 || TE / (Vd * NT) > K2_MAXJ || Vd / G > K2_MAXK) continue;
       int score = (int)(std::min<int64_t>(Ls * es, 256) + std::min<int64_t>(Ld * es, 256));
       score = score * 4 + (int)std::min<int64_t>(TE * es / 4096, 4);  // then prefer tiles up to 16 KiB
       if (score > best.score) best = Choice{Ls, Ld, TE, Vs, Vd, inc, score};
@@ -323,7 +320,7 @@ bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
   P->k2_vd = (int)(Vd * es);
   P->k2_gb = GBB;
   P->align = 16;
-  int per_sm = std::max(1, std::min(4, (int)(200 * 1024 / (TE * es + 1024))));
+  int per_sm = std::max(1, std::min(8, (int)(200 * 1024 / (TE * es + 1024))));
   P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(k.ntiles, (int64_t)num_sms() * per_sm));
   int64_t total = 1;
   for (auto &j : J) total *= j.e;
