@@ -138,13 +138,14 @@ typedef struct {
 
 /* Kernel choice for plans (flags of axe_copy_plan_create); AUTO picks from the
  * layouts.  The environment variable AXE_FORCE_KERNEL
- * (generic | vector | tma | tile) overrides AUTO. */
+ * (generic | vector | tma | tile | register) overrides AUTO. */
 enum {
   AXE_KERNEL_AUTO = 0,
   AXE_KERNEL_GENERIC = 1, /* K0: per-element evaluation of both layouts (always applicable) */
   AXE_KERNEL_VECTOR = 2,  /* K1: joint-digit vectorised LDG/STG copy                         */
   AXE_KERNEL_TMA = 3,     /* K1-TMA: TMA box load into swizzled smem + bulk store            */
-  AXE_KERNEL_TILE = 4     /* K2: smem-staged tile permute / transpose                        */
+  AXE_KERNEL_TILE = 4,    /* K2: smem-staged tile permute / transpose                        */
+  AXE_KERNEL_REGISTER = 5 /* K3: warp-register permute through movmatrix (b16 8x8 atoms)     */
 };
 
 typedef struct axe_copy_plan axe_copy_plan;

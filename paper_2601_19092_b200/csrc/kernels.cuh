@@ -139,4 +139,21 @@ struct K2Params {
   int dep;
 };
 
+// ---------------------------------------------------------------- K3 movmatrix
+// Register-layout permute that is, on every 512-byte "warp row" of a register
+// dump (32 lanes x 8 b16 registers), the per-register 8x8 transpose of
+// movmatrix.sync.aligned.m8n8.trans.b16 (config 3b): one warp moves one block
+// with LDG.128, 4 x MOVM, STG.128 -- no shared memory.
+struct K3Params {
+  uint32_t nblocks;
+  int nd;  // block-index digits, outermost first
+  FastDiv fd[K1_MAXD];
+  int64_t ss[K1_MAXD], ds[K1_MAXD];  // bytes
+  int64_t sbase, dbase;
+  int nrep;
+  int64_t rep[K1_MAXREP];
+  Swz ssw, dsw;
+  int dep;
+};
+
 }  // namespace axe

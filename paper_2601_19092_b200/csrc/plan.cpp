@@ -213,6 +213,7 @@ static int env_kernel() {
   if (!strcmp(e, "vector")) return AXE_KERNEL_VECTOR;
   if (!strcmp(e, "tma")) return AXE_KERNEL_TMA;
   if (!strcmp(e, "tile")) return AXE_KERNEL_TILE;
+  if (!strcmp(e, "register")) return AXE_KERNEL_REGISTER;
   return AXE_KERNEL_AUTO;
 }
 
@@ -575,6 +576,16 @@ axe_status plan_copy(const PlanRequest &rq, CopyPlan *out) {
     if (kernel == AXE_KERNEL_TMA)
       AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced TMA kernel cannot run these layouts: %s / %s", w0.c_str(), w1.c_str());
   }
+  if (joint && (kernel == AXE_KERNEL_AUTO || kernel == AXE_KERNEL_REGISTER)) {
+    std::string w3;
+    if (build_k3(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &w3)) {
+      P.kernel = KK_REGISTER;
+      *out = std::move(P);
+      return AXE_OK;
+    }
+    if (kernel == AXE_KERNEL_REGISTER)
+      AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced register kernel cannot run these layouts: %s", w3.c_str());
+  }
   if (joint && kernel == AXE_KERNEL_TILE) {
     if (build_k2(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &why)) {
       P.kernel = KK_TILE;
@@ -677,6 +688,12 @@ axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t 
       K0Params k = p.k0;
       k.dep = dep;
       e = launch_k0(k, src, dst, st);
+      break;
+    }
+    case KK_REGISTER: {
+      K3Params k = p.k3;
+      k.dep = dep;
+      e = launch_k3(k, p.blocks, src, dst, st);
       break;
     }
     case KK_TILE: {

@@ -13,7 +13,7 @@
 
 namespace axe {
 
-enum KernelKind { KK_GENERIC = 1, KK_VECTOR = 2, KK_TMA = 3, KK_TILE = 4 };
+enum KernelKind { KK_GENERIC = 1, KK_VECTOR = 2, KK_TMA = 3, KK_TILE = 4, KK_REGISTER = 5 };
 
 struct CopyPlan {
   int kernel = KK_GENERIC;
@@ -40,7 +40,13 @@ struct CopyPlan {
   K2Params k2;
   int k2_vs = 0, k2_vd = 0, k2_gb = 0;
   double k1_sector_eff = 1.0;  // K1: useful bytes / 32-byte sectors touched by one CTA's vectors (min of both sides)
+  // K3 movmatrix
+  K3Params k3;
 };
+
+bool build_k3(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,
+              const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why);
+cudaError_t launch_k3(const K3Params &p, unsigned blocks, const void *src, void *dst, cudaStream_t st);
 
 bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,
               const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why);

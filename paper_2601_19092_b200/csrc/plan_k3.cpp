@@ -1,0 +1,110 @@
+// plan_k3.cpp -- planner of K3, the movmatrix register permute.
+//
+// The copy qualifies when (after joint refinement, element strides) its digits
+// split into in-block digits acting inside 256-element (512-byte) blocks and
+// block digits whose strides are whole blocks on both sides, and when the
+// in-block map equals the movmatrix.m8n8.trans.b16 atom applied to every
+// 32-bit register of a 32-lane x 8-register warp row: element (lane, 2q + v)
+// with lane = 4i + j goes to (4 (2j + v) + i/2, 2q + i mod 2).  This is the
+// "tile of an instruction atom" test of the paper's dispatch (P:519-536,
+// App. D) for one concrete atom.
+#include <algorithm>
+#include <cstring>
+
+#include "plan.hpp"
+
+namespace axe {
+
+Swz make_swz(const Storage &st);
+int num_sms();
+
+static int64_t movm_atom(int64_t e) {  // in-block element offset -> destination offset
+  int64_t lane = e / 8, lo = e % 8, q = lo / 2, v = lo % 2;
+  int64_t i = lane / 4, j = lane % 4;
+  return (4 * (2 * j + v) + i / 2) * 8 + 2 * q + (i % 2);
+}
+
+bool build_k3(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,
+              const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why) {
+  auto fail = [&](const char *m) {
+    *why = m;
+    return false;
+  };
+  if (es != 2) return fail("register: movmatrix moves b16 elements");
+  if (max_align < 16) return fail("register: needs 16-byte aligned buffers");
+  if ((sst.swz_b && sst.swz_m < 4) || (dstst.swz_b && dstst.swz_m < 4)) return fail("register: swizzle below 16 bytes");
+  const int64_t BLK = 256;
+  if (ls.base % BLK || ld.base % BLK) return fail("register: bases are not whole blocks");
+  std::vector<int64_t> reps{0};
+  for (auto &r : ld.R) {
+    std::vector<int64_t> nx;
+    for (int64_t b : reps)
+      for (int64_t d = 0; d < r.e; d++) nx.push_back(b + d * r.s);
+    reps.swap(nx);
+  }
+  std::sort(reps.begin(), reps.end());
+  reps.erase(std::unique(reps.begin(), reps.end()), reps.end());
+  if ((int)reps.size() > K1_MAXREP) return fail("register: too many replicas");
+  for (int64_t r : reps)
+    if (r % 8) return fail("register: replica offsets not 16-byte aligned");
+  std::vector<Joint> in, out;
+  int64_t inprod = 1;
+  for (auto &j : J) {
+    if (j.e == 1) continue;
+    if (j.ss > 0 && j.ds > 0 && (j.e - 1) * j.ss < BLK && (j.e - 1) * j.ds < BLK) {
+      in.push_back(j);
+      inprod *= j.e;
+    } else if (j.ss % BLK == 0 && j.ds % BLK == 0) {
+      out.push_back(j);
+    } else {
+      return fail("register: a digit straddles the 512-byte blocks");
+    }
+  }
+  if (inprod != BLK) return fail("register: in-block digits do not cover a warp row");
+  std::vector<int> seen(BLK, 0);
+  for (int64_t x = 0; x < BLK; x++) {
+    int64_t rem = x, s = 0, d = 0;
+    for (int k = (int)in.size() - 1; k >= 0; k--) {
+      int64_t dg = rem % in[k].e;
+      rem /= in[k].e;
+      s += dg * in[k].ss;
+      d += dg * in[k].ds;
+    }
+    if (s < 0 || s >= BLK || seen[s]) return fail("register: in-block map is not a permutation");
+    seen[s] = 1;
+    if (movm_atom(s) != d) return fail("register: in-block map is not the movmatrix atom");
+  }
+  if ((int)out.size() > K1_MAXD) return fail("register: too many block digits");
+  int64_t nb = 1;
+  for (auto &o : out) nb *= o.e;
+  if (nb >= (int64_t(1) << 32)) return fail("register: too many blocks");
+  K3Params &k = P->k3;
+  memset(&k, 0, sizeof(k));
+  std::stable_sort(out.begin(), out.end(), [](const Joint &a, const Joint &b) { return std::llabs(a.ds) > std::llabs(b.ds); });
+  k.nblocks = (uint32_t)nb;
+  k.nd = (int)out.size();
+  for (int i = 0; i < k.nd; i++) {
+    k.fd[i] = make_fastdiv((uint32_t)out[i].e);
+    k.ss[i] = out[i].ss * es;
+    k.ds[i] = out[i].ds * es;
+  }
+  k.sbase = ls.base * es;
+  k.dbase = ld.base * es;
+  k.nrep = (int)reps.size();
+  for (size_t i = 0; i < reps.size(); i++) k.rep[i] = reps[i] * es;
+  k.ssw = make_swz(sst);
+  k.dsw = make_swz(dstst);
+  P->align = 16;
+  const int64_t per_cta = 8 * 4;  // warps x blocks per warp per iteration
+  P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nb + per_cta - 1) / per_cta, (int64_t)num_sms() * 8));
+  P->covers_all = (int64_t)reps.size() * nb * BLK == dstst.cells;
+  char b[256];
+  snprintf(b, sizeof b,
+           "{\"kernel\":\"register\",\"atom\":\"movmatrix.m8n8.trans.b16\",\"blocks_512B\":%lld,\"ctas\":%u,"
+           "\"replicas\":%d,\"joint\":",
+           (long long)nb, P->blocks, k.nrep);
+  P->desc = std::string(b) + joint_json(J) + "}";
+  return true;
+}
+
+}  // namespace axe

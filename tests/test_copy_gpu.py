@@ -80,10 +80,17 @@ def test_config2_full(axe, rev, kernel):
     assert desc["kernel"] == ("tma" if kernel == "auto" else kernel)
 
 
-@pytest.mark.parametrize("kernel", ["auto", "generic", "vector", "tile"])
+@pytest.mark.parametrize("kernel", ["auto", "generic", "vector", "tile", "register"])
 @pytest.mark.parametrize("variant", ["a", "b"])
 def test_config3_small(axe, variant, kernel):
-    check(axe, synth.config3(16, variant), kernel)
+    if kernel == "register" and variant == "a":
+        with pytest.raises(axe.AxeError):   # 3a moves data across warps: not a movmatrix atom
+            axe.CopyPlan(synth.config3(16, "a")["src"], synth.config3(16, "a")["src_st"],
+                         synth.config3(16, "a")["dst"], synth.config3(16, "a")["dst_st"], 2, "register")
+        return
+    d = check(axe, synth.config3(16, variant), kernel)
+    if variant == "b" and kernel == "auto":
+        assert d["kernel"] == "register"
 
 
 @pytest.mark.parametrize("variant", ["a", "b"])
