@@ -156,7 +156,7 @@ def test_config1_plan():
 def test_config3_plans_are_affine():
     for v in "ab":
         d = plan(synth.config3(64, v)).describe()
-        assert d["kernel"] in ("vector", "tile"), d
+        assert d["kernel"] == {"a": "vector", "b": "register"}[v], d
 
 
 def test_nonnested_falls_back_to_generic():
