@@ -11,6 +11,7 @@
 #include <memory>
 #include <string>
 #include <utility>
+#include <algorithm>
 #include <vector>
 
 #include "axe.h"
@@ -134,6 +135,25 @@ struct Joint {
 // Refine two linear shard lists over the same domain into one joint digit list
 // (innermost-first gcd/divisibility pairing; Alg. 1 generalised, R21).
 bool joint_refine(const std::vector<LinIter> &src, const std::vector<LinIter> &dst, std::vector<Joint> *out);
+
+// Order digits by |dst stride| (outermost first) and fuse neighbours that are
+// contiguous on both sides (Cor. fuse): fewer digits to decode.
+inline void sort_fuse_outer(std::vector<Joint> &v) {
+  std::stable_sort(v.begin(), v.end(), [](const Joint &a, const Joint &b) {
+    int64_t x = a.ds < 0 ? -a.ds : a.ds, y = b.ds < 0 ? -b.ds : b.ds;
+    return x > y;
+  });
+  std::vector<Joint> f;
+  for (auto &j : v) {
+    if (!f.empty() && f.back().ss == j.e * j.ss && f.back().ds == j.e * j.ds && f.back().sdev == j.sdev &&
+        f.back().ddev == j.ddev) {
+      f.back() = Joint{f.back().e * j.e, j.ss, j.ds, j.sdev, j.ddev};
+    } else {
+      f.push_back(j);
+    }
+  }
+  v.swap(f);
+}
 
 inline int64_t ilog2_floor(uint64_t v) {
   int64_t r = -1;

@@ -341,6 +341,11 @@ static bool build_k1(const std::vector<Joint> &J0, const Linear &ls, const Linea
     }
     if (prefix != tile_v) tiled = false;
     for (; tiled && k2 < rest.size(); k2++) outer.push_back(rest[k2]);
+    if (tiled) {
+      // fill() below expects inner-first order: fuse outermost-first, then reverse
+      sort_fuse_outer(outer);
+      std::reverse(outer.begin(), outer.end());
+    }
     if ((int)inner.size() > K1_MAXD || (int)outer.size() > K1_MAXD) tiled = false;
   }
   auto fill = [&](const std::vector<Joint> &inner_first, FastDiv *fd, int64_t *a, int64_t *b) {

@@ -303,7 +303,14 @@ bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
   k.ntiles = 1;
   for (auto &o : outer) k.ntiles *= (uint32_t)o.e;
   k.nout = (int)outer.size();
-  std::stable_sort(outer.begin(), outer.end(), [](const Dig &a, const Dig &b) { return a.ds > b.ds; });
+  {
+    std::vector<Joint> oj;
+    for (auto &o : outer) oj.push_back(Joint{o.e, o.ss, o.ds});
+    sort_fuse_outer(oj);
+    outer.clear();
+    for (auto &o : oj) outer.push_back(Dig{o.e, o.ss, o.ds});
+    k.nout = (int)outer.size();
+  }
   for (int i = 0; i < k.nout; i++) {
     k.ofd[i] = make_fastdiv((uint32_t)outer[i].e);
     k.oss[i] = outer[i].ss * es;

@@ -80,7 +80,7 @@ bool build_k3(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
   if (nb >= (int64_t(1) << 32)) return fail("register: too many blocks");
   K3Params &k = P->k3;
   memset(&k, 0, sizeof(k));
-  std::stable_sort(out.begin(), out.end(), [](const Joint &a, const Joint &b) { return std::llabs(a.ds) > std::llabs(b.ds); });
+  sort_fuse_outer(out);
   k.nblocks = (uint32_t)nb;
   k.nd = (int)out.size();
   for (int i = 0; i < k.nd; i++) {

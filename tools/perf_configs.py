@@ -33,6 +33,12 @@ CONFIGS = {
     "config2_16k": lambda: synth.config2(16384),
     "config3a": lambda: synth.config3(65536, "a"),
     "config3b": lambda: synth.config3(65536, "b"),
+    "identity_4g": lambda: dict(name="identity_4g", es=2, src=synth.layout([(1 << 31, 1)]),
+                                src_st=synth.linear_storage(1 << 31), dst=synth.layout([(1 << 31, 1)]),
+                                dst_st=synth.linear_storage(1 << 31), seed=3),
+    "identity_1g": lambda: dict(name="identity_1g", es=2, src=synth.layout([(1 << 29, 1)]),
+                                src_st=synth.linear_storage(1 << 29), dst=synth.layout([(1 << 29, 1)]),
+                                dst_st=synth.linear_storage(1 << 29), seed=3),
     "transpose_bf16": lambda: transpose_cfg(8192, 8192, 2),
     "transpose_f32": lambda: transpose_cfg(8192, 8192, 4),
 }
@@ -79,8 +85,8 @@ def torch_copy(nbytes, reps=20):
     """Reference point: torch's own copy_ of nbytes (read + write counted), same rotation and graph."""
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
     pairs = max(1, min(8, -(-4 * l2 // (2 * nbytes))))
-    srcs = [torch.empty(nbytes, dtype=torch.uint8, device="cuda") for _ in range(pairs)]
-    dsts = [torch.empty(nbytes, dtype=torch.uint8, device="cuda") for _ in range(pairs)]
+    srcs = [torch.empty(nbytes // 2, dtype=torch.bfloat16, device="cuda") for _ in range(pairs)]
+    dsts = [torch.empty(nbytes // 2, dtype=torch.bfloat16, device="cuda") for _ in range(pairs)]
     G = pairs * 8
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=torch.cuda.Stream()):
@@ -107,7 +113,7 @@ def main():
     ap.add_argument("--torch-copy", action="store_true")
     a = ap.parse_args()
     if a.torch_copy:
-        for nb in (32 << 20, 512 << 20):
+        for nb in (32 << 20, 1 << 30, 4 << 30):
             print(json.dumps(torch_copy(nb)), flush=True)
     names = a.only.split(",") if a.only else list(CONFIGS)
     for n in names:
