@@ -161,19 +161,9 @@ axe_status axe_copy_plan_execute_host(const axe_copy_plan *plan, const void *hos
   CHECK_NULL(plan, "plan");
   CHECK_NULL(host_src, "host_src");
   CHECK_NULL(host_dst, "host_dst");
-  cudaStream_t s = (cudaStream_t)stream;
-  const CopyPlan &P = plan->P;
-  cudaError_t e = cudaMemcpyAsync(dev_src, host_src, (size_t)P.src_bytes, cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "H2D copy failed: %s", cudaGetErrorString(e));
-  // cells outside the destination image keep their contents (reading R7): stage them too
-  if (!P.covers_all) {
-    e = cudaMemcpyAsync(dev_dst, host_dst, (size_t)P.dst_bytes, cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "H2D copy failed: %s", cudaGetErrorString(e));
-  }
-  AXE_TRY(run_copy(P, dev_src, dev_dst, s));
-  e = cudaMemcpyAsync(host_dst, dev_dst, (size_t)P.dst_bytes, cudaMemcpyDeviceToHost, s);
-  if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "D2H copy failed: %s", cudaGetErrorString(e));
-  return AXE_OK;
+  CHECK_NULL(dev_src, "dev_src");
+  CHECK_NULL(dev_dst, "dev_dst");
+  return run_copy_host(plan->P, host_src, host_dst, dev_src, dev_dst, (cudaStream_t)stream);
 }
 
 axe_status axe_copy_plan_sizes(const axe_copy_plan *plan, int64_t *src_bytes, int64_t *dst_bytes) {

@@ -540,7 +540,138 @@ static bool build_tma(const std::vector<Joint> &J0, const Linear &ls, const Line
   return true;
 }
 
+static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out);
+
 axe_status plan_copy(const PlanRequest &rq, CopyPlan *out) {
+  AXE_TRY(plan_copy_core(rq, out));
+  if (!rq.no_chunk && rq.skip_axis < 0 && out->linear) {
+    Linear ls, ld;
+    std::vector<Joint> J;
+    if (compose_linear(*rq.src, *rq.sst, -1, &ls) && compose_linear(*rq.dst, *rq.dstst, -1, &ld) &&
+        joint_refine(ls.D, ld.D, &J))
+      plan_chunks(rq, J, ls, ld, out);  // best effort: no chunking on failure
+    if (out->n_chunks && !out->desc.empty() && out->desc.back() == '}')
+      out->desc.insert(out->desc.size() - 1, ",\"host_chunks\":" + std::to_string(out->n_chunks));
+  }
+  return AXE_OK;
+}
+
+HostPipe::~HostPipe() {
+  for (auto e : ev)
+    if (e) cudaEventDestroy(e);
+  for (auto s : {h2d, comp, d2h})
+    if (s) cudaStreamDestroy(s);
+}
+
+// A joint digit that spans both whole buffers (src stride * extent = src cells,
+// dst stride * extent = dst cells) cuts the copy into independent slabs.
+axe_status plan_chunks(const PlanRequest &rq, const std::vector<Joint> &J, const Linear &ls, const Linear &ld,
+                       CopyPlan *P) {
+  if (ls.base || ld.base || !ld.R.empty()) return AXE_OK;
+  const int64_t sc = rq.sst->cells, dc = rq.dstst->cells, es = rq.es;
+  int best = -1;
+  for (size_t i = 0; i < J.size(); i++)
+    if (J[i].ss > 0 && J[i].ds > 0 && J[i].ss * J[i].e == sc && J[i].ds * J[i].e == dc && J[i].e > 1) best = (int)i;
+  if (best < 0) return AXE_OK;
+  const Joint cj = J[best];
+  // about 8 slabs of >= 1 MiB, each a whole number of swizzle blocks on both sides
+  int n = 1;
+  for (int c = 2; c <= 16; c++) {
+    if (cj.e % c) continue;
+    int64_t sb = sc / c * es, db = dc / c * es;
+    if (sb < (1 << 20)) break;
+    auto whole = [&](const Storage *st, int64_t bytes) {
+      return !st->swz_b || bytes % (int64_t(1) << (st->swz_b + st->swz_m + st->swz_s)) == 0;
+    };
+    if (whole(rq.sst, sb) && whole(rq.dstst, db) && sb % 16 == 0 && db % 16 == 0) n = c;
+    if (n >= 8) break;
+  }
+  if (n < 2) return AXE_OK;
+  std::vector<Iter> sD, dD;
+  for (size_t i = 0; i < J.size(); i++) {
+    int64_t e = (int)i == best ? J[i].e / n : J[i].e;
+    sD.push_back(Iter{e, J[i].ss, axis_m()});
+    dD.push_back(Iter{e, J[i].ds, axis_m()});
+  }
+  Layout sL, dL;
+  AXE_TRY(make_layout(sD, {}, {}, &sL));
+  AXE_TRY(make_layout(dD, {}, {}, &dL));
+  Storage sst, dst;
+  sst.d.push_back(SDigit{axis_m(), sc / n, 1, 1});
+  sst.cells = sc / n;
+  sst.swz_b = rq.sst->swz_b, sst.swz_m = rq.sst->swz_m, sst.swz_s = rq.sst->swz_s;
+  dst.d.push_back(SDigit{axis_m(), dc / n, 1, 1});
+  dst.cells = dc / n;
+  dst.swz_b = rq.dstst->swz_b, dst.swz_m = rq.dstst->swz_m, dst.swz_s = rq.dstst->swz_s;
+  auto sub = std::make_shared<CopyPlan>();
+  PlanRequest r2{&sL, &dL, &sst, &dst, rq.es, rq.kernel, rq.max_align, -1};
+  r2.no_chunk = 1;
+  if (plan_copy_core(r2, sub.get()) != AXE_OK) return AXE_OK;
+  P->chunk = sub;
+  P->n_chunks = n;
+  P->pipe = std::make_shared<HostPipe>();
+  return AXE_OK;
+}
+
+axe_status run_copy_host(const CopyPlan &P, const void *host_src, void *host_dst, void *dev_src, void *dev_dst,
+                         cudaStream_t st) {
+  cudaError_t e = cudaSuccess;
+#define CU(x)                                                                              \
+  do {                                                                                     \
+    e = (x);                                                                               \
+    if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "%s: %s", #x, cudaGetErrorString(e));     \
+  } while (0)
+  if (!P.chunk) {
+    CU(cudaMemcpyAsync(dev_src, host_src, (size_t)P.src_bytes, cudaMemcpyHostToDevice, st));
+    // cells outside the destination image keep their contents (reading R7): stage them too
+    if (!P.covers_all) CU(cudaMemcpyAsync(dev_dst, host_dst, (size_t)P.dst_bytes, cudaMemcpyHostToDevice, st));
+    AXE_TRY(run_copy(P, dev_src, dev_dst, st));
+    CU(cudaMemcpyAsync(host_dst, dev_dst, (size_t)P.dst_bytes, cudaMemcpyDeviceToHost, st));
+    return AXE_OK;
+  }
+  HostPipe &H = *P.pipe;
+  std::lock_guard<std::mutex> lk(H.mu);
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  if (H.device != dev) {
+    for (auto ev : H.ev)
+      if (ev) cudaEventDestroy(ev);
+    H.ev.clear();
+    for (cudaStream_t *s : {&H.h2d, &H.comp, &H.d2h}) {
+      if (*s) cudaStreamDestroy(*s);
+      CU(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
+    }
+    H.ev.assign(3 * P.n_chunks + 2, nullptr);
+    for (auto &ev : H.ev) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    H.device = dev;
+  }
+  const int n = P.n_chunks;
+  const int64_t sb = P.src_bytes / n, db = P.dst_bytes / n;
+  cudaEvent_t fork = H.ev[3 * n], join = H.ev[3 * n + 1];
+  CU(cudaEventRecord(fork, st));
+  for (cudaStream_t s : {H.h2d, H.comp, H.d2h}) CU(cudaStreamWaitEvent(s, fork, 0));
+  stream_forget(H.comp);
+  for (int c = 0; c < n; c++) {
+    const uint8_t *hs = (const uint8_t *)host_src + c * sb;
+    uint8_t *hd = (uint8_t *)host_dst + c * db;
+    uint8_t *ds = (uint8_t *)dev_src + c * sb, *dd = (uint8_t *)dev_dst + c * db;
+    CU(cudaMemcpyAsync(ds, hs, (size_t)sb, cudaMemcpyHostToDevice, H.h2d));
+    if (!P.covers_all) CU(cudaMemcpyAsync(dd, hd, (size_t)db, cudaMemcpyHostToDevice, H.h2d));
+    CU(cudaEventRecord(H.ev[3 * c], H.h2d));
+    CU(cudaStreamWaitEvent(H.comp, H.ev[3 * c], 0));
+    stream_forget(H.comp);
+    AXE_TRY(run_copy(*P.chunk, ds, dd, H.comp));
+    CU(cudaEventRecord(H.ev[3 * c + 1], H.comp));
+    CU(cudaStreamWaitEvent(H.d2h, H.ev[3 * c + 1], 0));
+    CU(cudaMemcpyAsync(hd, dd, (size_t)db, cudaMemcpyDeviceToHost, H.d2h));
+  }
+  CU(cudaEventRecord(join, H.d2h));
+  CU(cudaStreamWaitEvent(st, join, 0));
+#undef CU
+  return AXE_OK;
+}
+
+static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
   const Layout &S = *rq.src, &D = *rq.dst;
   int es = rq.es;
   if (es != 1 && es != 2 && es != 4 && es != 8 && es != 16)

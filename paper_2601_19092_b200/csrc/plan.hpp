@@ -42,7 +42,24 @@ struct CopyPlan {
   double k1_sector_eff = 1.0;  // K1: useful bytes / 32-byte sectors touched by one CTA's vectors (min of both sides)
   // K3 movmatrix
   K3Params k3;
+  // host-buffer pipeline (axe_copy_plan_execute_host): the copy splits into n_chunks
+  // independent slabs (a joint digit spanning both whole buffers); each slab's
+  // H2D, kernel and D2H run on three streams so PCIe traffic in both directions overlaps.
+  std::shared_ptr<CopyPlan> chunk;
+  int n_chunks = 0;
+  std::shared_ptr<struct HostPipe> pipe;
 };
+
+struct HostPipe {
+  std::mutex mu;
+  int device = -1;
+  cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> ev;  // 3 per chunk + 2
+  ~HostPipe();
+};
+
+axe_status run_copy_host(const CopyPlan &p, const void *host_src, void *host_dst, void *dev_src, void *dev_dst,
+                         cudaStream_t st);
 
 bool build_k3(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,
               const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why);
@@ -66,7 +83,12 @@ struct PlanRequest {
   int kernel;            // AXE_KERNEL_*
   int max_align;         // pointer alignment known to hold (bytes, power of 2, <= 16)
   int skip_axis;         // -1 for copy; gpuid id for redistribute pieces
+  int no_chunk = 0;      // do not build the host-pipeline slab plan
 };
+
+void stream_forget(cudaStream_t st);
+axe_status plan_chunks(const PlanRequest &rq, const std::vector<Joint> &J, const Linear &ls, const Linear &ld,
+                       CopyPlan *P);
 
 axe_status plan_copy(const PlanRequest &rq, CopyPlan *out);
 axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t st);

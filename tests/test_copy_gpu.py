@@ -328,3 +328,26 @@ def test_random_permutes_reduce_to_numpy(axe, seed):
         plan.execute(s, d)
         torch.cuda.synchronize()
         assert np.array_equal(d.cpu().numpy().view(dt), expect), (kernel, shape, perm, es, plan.describe())
+
+
+@pytest.mark.parametrize("case", ["config2", "config2r", "padded"])
+def test_execute_host_pipelined(axe, case):
+    """axe_copy_plan_execute_host with the slab pipeline (H2D / kernel / D2H on three streams): host-to-host
+    result equals the oracle, including destination cells outside the image (padded rows keep the sentinel)."""
+    if case == "padded":
+        n, pitch = 2048, 2056
+        cfg = dict(name="padded", es=2, src=layout([(n, n), (n, 1)]), src_st=linear_storage(n * n),
+                   dst=layout([(n, pitch), (n, 1)]), dst_st=linear_storage(n * pitch), seed=4)
+    else:
+        cfg = synth.config2(reverse=case == "config2r")
+    src, d_fill, exp = prepare(cfg)
+    plan = axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], 2)
+    assert plan.describe().get("host_chunks", 0) >= 2, plan.describe()
+    hs = torch.from_numpy(src).pin_memory()
+    hd = torch.from_numpy(d_fill.copy()).pin_memory()
+    ds = torch.empty(src.nbytes, dtype=torch.uint8, device="cuda")
+    dd = torch.empty(d_fill.nbytes, dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        plan.execute_host(hs, hd, ds, dd)
+    torch.cuda.synchronize()
+    assert np.array_equal(hd.numpy(), exp)
