@@ -38,13 +38,20 @@ def prepare(cfg):
     return src, d_fill, exp
 
 
+GUARD = 4096  # bytes of sentinel on both sides of every device buffer (compute-sanitizer is closed on this pool)
+
+
 def run_gpu(axe, cfg, src, d_fill, kernel="auto"):
     plan = axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], cfg["es"], kernel)
-    s = to_dev(src)
-    d = to_dev(d_fill)
-    plan.execute(s, d)
+    g = synth.sentinel(2 * GUARD, 99)
+    s = to_dev(np.concatenate([g[:GUARD], src, g[GUARD:]]))
+    d = to_dev(np.concatenate([g[:GUARD], d_fill, g[GUARD:]]))
+    plan.execute(s[GUARD:GUARD + src.nbytes], d[GUARD:GUARD + d_fill.nbytes])
     torch.cuda.synchronize()
-    return d.cpu().numpy(), plan.describe()
+    out = d.cpu().numpy()
+    assert np.array_equal(out[:GUARD], g[:GUARD]) and np.array_equal(out[-GUARD:], g[GUARD:]), \
+        f"{cfg['name']}: write outside the destination buffer"
+    return out[GUARD:GUARD + d_fill.nbytes], plan.describe()
 
 
 def check(axe, cfg, kernel="auto", expect_kernel=None):
