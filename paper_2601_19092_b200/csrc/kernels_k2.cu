@@ -88,14 +88,28 @@ __global__ void __launch_bounds__(K2_NT) k2_tile(const __grid_constant__ K2Param
     for (int j = 0; j < K2_MAXLJ; j++)
       if (j < p.lj) *reinterpret_cast<TS *>(sm + swz32(p.smsw, (uint32_t)((j * K2_NT + t) * VS))) = v[j];
     __syncthreads();
-    for (int j = 0; j < p.sj; j++) {
-      TD out;
-      TG *o = reinterpret_cast<TG *>(&out);
-      const uint32_t base = (uint32_t)(as + p.B_s[j]);
+    if (p.xor_ok && p.nrep == 1 && !p.dsw.mask) {
+      // fast path: 1 LOP3 + 1 LDS per granule, 1 STG per vector
+      uint8_t *dt = dst + db + ad + p.rep[0];
+#pragma unroll 4
+      for (int j = 0; j < p.sj; j++) {
+        TD out;
+        TG *o = reinterpret_cast<TG *>(&out);
+        const uint32_t base = (uint32_t)as ^ (uint32_t)p.B_s[j];
 #pragma unroll
-      for (int k = 0; k < KG; k++) o[k] = *reinterpret_cast<const TG *>(sm + swz32(p.smsw, base + p.C_s[k]));
-      const int64_t d = db + p.B_d[j] + ad;
-      for (int r = 0; r < p.nrep; r++) *reinterpret_cast<TD *>(dst + swz(p.dsw, d + p.rep[r])) = out;
+        for (int k = 0; k < KG; k++) o[k] = *reinterpret_cast<const TG *>(sm + (base ^ (uint32_t)p.C_s[k]));
+        *reinterpret_cast<TD *>(dt + p.B_d[j]) = out;
+      }
+    } else {
+      for (int j = 0; j < p.sj; j++) {
+        TD out;
+        TG *o = reinterpret_cast<TG *>(&out);
+        const uint32_t base = (uint32_t)(as + p.B_s[j]);
+#pragma unroll
+        for (int k = 0; k < KG; k++) o[k] = *reinterpret_cast<const TG *>(sm + swz32(p.smsw, base + p.C_s[k]));
+        const int64_t d = db + p.B_d[j] + ad;
+        for (int r = 0; r < p.nrep; r++) *reinterpret_cast<TD *>(dst + swz(p.dsw, d + p.rep[r])) = out;
+      }
     }
     __syncthreads();
   }
