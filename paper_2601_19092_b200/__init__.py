@@ -16,7 +16,7 @@ import json
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libaxe.so")
+_SO = os.environ.get("AXE_LIBAXE") or os.path.join(_HERE, "libaxe.so")  # AXE_LIBAXE: A/B builds only
 
 if not os.path.exists(_SO):
     raise ImportError(f"libaxe.so not built ({_SO}); run __graft_entry__.build() or "

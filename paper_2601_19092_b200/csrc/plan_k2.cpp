@@ -303,7 +303,8 @@ bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
   {
     // XOR tables: when the three offsets are disjoint bit fields, a + b + c = a ^ b ^ c, and the
     // swizzle (GF(2)-linear) can be applied to each table entry once on the host
-    bool ok = true;
+    const char *xe = getenv("AXE_K2_XOR");
+    bool ok = !(xe && *xe == '0');
     for (int j = 0; j < k.sj && ok; j++)
       for (int t = 0; t < NT && ok; t++)
         for (int q = 0; q < k.kg; q++) {
