@@ -131,9 +131,6 @@ struct K2Params {
   int32_t A_l[K2_NT], A_s[K2_NT], A_d[K2_NT];  // bytes: src global, smem (pre-swizzle), dst global
   int32_t B_l[K2_MAXJ], B_s[K2_MAXJ], B_d[K2_MAXJ];
   int32_t C_s[K2_MAXK];
-  // xor_ok: every gather offset B_s[j] + A_s[t] + C_s[k] adds disjoint bit fields, so (the
-  // swizzle being GF(2)-linear) the tables hold pre-swizzled values combined with XOR
-  int xor_ok;
   uint32_t tile_bytes;
   Swz smsw;                            // shared-memory swizzle chosen by the planner
   Swz ssw, dsw;                        // global swizzles of the storages

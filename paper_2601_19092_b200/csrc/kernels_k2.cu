@@ -50,7 +50,7 @@ __device__ __forceinline__ typename K2Vec<B>::T ldg(const uint8_t *p) {
 
 constexpr int K2_MAXLJ = 8;
 
-template <int VS, int VD, int GB, bool FAST>
+template <int VS, int VD, int GB>
 __global__ void __launch_bounds__(K2_NT) k2_tile(const __grid_constant__ K2Params p, const uint8_t *__restrict__ src,
                                                  uint8_t *__restrict__ dst) {
   extern __shared__ __align__(128) uint8_t sm[];
@@ -88,28 +88,14 @@ __global__ void __launch_bounds__(K2_NT) k2_tile(const __grid_constant__ K2Param
     for (int j = 0; j < K2_MAXLJ; j++)
       if (j < p.lj) *reinterpret_cast<TS *>(sm + swz32(p.smsw, (uint32_t)((j * K2_NT + t) * VS))) = v[j];
     __syncthreads();
-    if constexpr (FAST) {
-      // fast path: 1 LOP3 + 1 LDS per granule, 1 STG per vector
-      uint8_t *dt = dst + db + ad + p.rep[0];
-#pragma unroll 4
-      for (int j = 0; j < p.sj; j++) {
-        TD out;
-        TG *o = reinterpret_cast<TG *>(&out);
-        const uint32_t base = (uint32_t)as ^ (uint32_t)p.B_s[j];
+    for (int j = 0; j < p.sj; j++) {
+      TD out;
+      TG *o = reinterpret_cast<TG *>(&out);
+      const uint32_t base = (uint32_t)(as + p.B_s[j]);
 #pragma unroll
-        for (int k = 0; k < KG; k++) o[k] = *reinterpret_cast<const TG *>(sm + (base ^ (uint32_t)p.C_s[k]));
-        *reinterpret_cast<TD *>(dt + p.B_d[j]) = out;
-      }
-    } else {
-      for (int j = 0; j < p.sj; j++) {
-        TD out;
-        TG *o = reinterpret_cast<TG *>(&out);
-        const uint32_t base = (uint32_t)(as + p.B_s[j]);
-#pragma unroll
-        for (int k = 0; k < KG; k++) o[k] = *reinterpret_cast<const TG *>(sm + swz32(p.smsw, base + p.C_s[k]));
-        const int64_t d = db + p.B_d[j] + ad;
-        for (int r = 0; r < p.nrep; r++) *reinterpret_cast<TD *>(dst + swz(p.dsw, d + p.rep[r])) = out;
-      }
+      for (int k = 0; k < KG; k++) o[k] = *reinterpret_cast<const TG *>(sm + swz32(p.smsw, base + p.C_s[k]));
+      const int64_t d = db + p.B_d[j] + ad;
+      for (int r = 0; r < p.nrep; r++) *reinterpret_cast<TD *>(dst + swz(p.dsw, d + p.rep[r])) = out;
     }
     __syncthreads();
   }
@@ -119,15 +105,11 @@ template <int VS, int VD, int GB>
 static cudaError_t k2_go(const K2Params &p, unsigned blocks, size_t smem, const void *s, void *d, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k2_tile<VS, VD, GB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k2_tile<VS, VD, GB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k2_tile<VS, VD, GB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (p.xor_ok && p.nrep == 1 && !p.dsw.mask)
-    return launch_ex(k2_tile<VS, VD, GB, true>, dim3(blocks), dim3(K2_NT), smem, st, p, (const uint8_t *)s, (uint8_t *)d);
-  return launch_ex(k2_tile<VS, VD, GB, false>, dim3(blocks), dim3(K2_NT), smem, st, p, (const uint8_t *)s, (uint8_t *)d);
+  return launch_ex(k2_tile<VS, VD, GB>, dim3(blocks), dim3(K2_NT), smem, st, p, (const uint8_t *)s, (uint8_t *)d);
 }
 
 template <int VS, int VD>

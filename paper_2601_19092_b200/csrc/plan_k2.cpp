@@ -300,27 +300,6 @@ bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
     }
   }
   k.smsw = bestsw;
-  {
-    // XOR tables: when the three offsets are disjoint bit fields, a + b + c = a ^ b ^ c, and the
-    // swizzle (GF(2)-linear) can be applied to each table entry once on the host
-    const char *xe = getenv("AXE_K2_XOR");
-    bool ok = !(xe && *xe == '0');
-    for (int j = 0; j < k.sj && ok; j++)
-      for (int t = 0; t < NT && ok; t++)
-        for (int q = 0; q < k.kg; q++) {
-          uint32_t a = (uint32_t)k.A_s[t], bb = (uint32_t)k.B_s[j], c = (uint32_t)k.C_s[q];
-          if ((a ^ bb ^ c) != a + bb + c) {
-            ok = false;
-            break;
-          }
-        }
-    if (ok) {
-      for (int t = 0; t < NT; t++) k.A_s[t] = (int32_t)swz_host(bestsw, (uint32_t)k.A_s[t]);
-      for (int j = 0; j < k.sj; j++) k.B_s[j] = (int32_t)swz_host(bestsw, (uint32_t)k.B_s[j]);
-      for (int q = 0; q < k.kg; q++) k.C_s[q] = (int32_t)swz_host(bestsw, (uint32_t)k.C_s[q]);
-      k.xor_ok = 1;
-    }
-  }
   k.ntiles = 1;
   for (auto &o : outer) k.ntiles *= (uint32_t)o.e;
   k.nout = (int)outer.size();
@@ -357,9 +336,9 @@ bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
   snprintf(b, sizeof b,
            "{\"kernel\":\"tile\",\"tile_bytes\":%lld,\"tiles\":%u,\"src_run_bytes\":%lld,\"dst_run_bytes\":%lld,"
            "\"load_vec\":%d,\"store_vec\":%d,\"granule\":%d,\"smem_swizzle\":[%u,%u],\"wavefronts\":[%d,%d],"
-           "\"blocks\":%u,\"replicas\":%d,\"xor_tables\":%d,\"joint\":",
+           "\"blocks\":%u,\"replicas\":%d,\"joint\":",
            (long long)(TE * es), k.ntiles, (long long)(best.Ls * es), (long long)(best.Ld * es), VSB, P->k2_vd, GBB,
-           bestsw.shift, bestsw.mask, nonec, bestc, P->blocks, k.nrep, k.xor_ok);
+           bestsw.shift, bestsw.mask, nonec, bestc, P->blocks, k.nrep);
   P->desc = std::string(b) + joint_json(J) + "}";
   return true;
 }
