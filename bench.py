@@ -217,6 +217,58 @@ def measure_reshard(axe, torch, dist, ws, rank, local, stream, iters=20, warm=3)
     return res
 
 
+def _time_plan(torch, plan, reps=10):
+    """Graph-replayed back-to-back executes over rotating buffers (> 4x L2); returns ms per launch."""
+    sb, db = plan.sizes()
+    l2 = torch.cuda.get_device_properties(torch.cuda.current_device()).L2_cache_size
+    pairs = max(1, min(8, -(-4 * l2 // (sb + db))))
+    srcs = [torch.empty(sb, dtype=torch.uint8, device="cuda").random_() for _ in range(pairs)]
+    dsts = [torch.empty(db, dtype=torch.uint8, device="cuda") for _ in range(pairs)]
+    G = pairs * max(1, 32 // pairs) if sb < (1 << 27) else pairs
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=torch.cuda.Stream()):
+        for j in range(G):
+            plan.execute(srcs[j % pairs], dsts[j % pairs], torch.cuda.current_stream())
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / (reps * G)
+    del srcs, dsts, g
+    torch.cuda.empty_cache()
+    return ms
+
+
+def measure_extras(axe, torch):
+    """The other single-GPU rows of SURVEY §8(a) (a6 reverse direction, a7 register permutes, K2 staging),
+    each timed like the headline; GB/s = es * (1 + E_R) bytes per element / time."""
+    peak, _ = peaks()
+    rows = {}
+    cases = {
+        "config1_8x8_lane_warp_replica": synth.config1(),
+        "config2_reverse_tiles_to_rowmajor": synth.config2(reverse=True),
+        "config3a_mma_c_to_tcgen05_rows": synth.config3(65536, "a"),
+        "config3b_mma_c_8x8_transposed": synth.config3(65536, "b"),
+        "transpose_8192sq_bf16_smem_staged": dict(es=2, src=synth.layout([(8192, 8192), (8192, 1)]),
+                                                 src_st=synth.linear_storage(8192 * 8192),
+                                                 dst=synth.layout([(8192, 1), (8192, 8192)]),
+                                                 dst_st=synth.linear_storage(8192 * 8192)),
+    }
+    for name, cfg in cases.items():
+        plan = axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], cfg["es"])
+        ms = _time_plan(torch, plan)
+        alg = plan.src.E_D * cfg["es"] * (1 + plan.dst.E_R)
+        gbs = alg / (ms * 1e-3) / 1e9
+        rows[name] = {"kernel": plan.describe()["kernel"], "us": ms * 1e3, "GBps": gbs, "frac_of_measured": gbs / peak,
+                      "alg_bytes": alg}
+    return rows
+
+
 def run_axe(args):
     import torch
     ws, rank, local = dist_init(args)
@@ -336,11 +388,20 @@ def run_axe(args):
     e2e = ws * alg_bytes / (e_ms * 1e-3) / 1e9
 
     reshard = None
-    if ws > 1 and not args.no_reshard:
+    if (ws > 1 or args.force_reshard) and not args.no_reshard:
         try:
+            if dist is None:
+                import torch.distributed as dist
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
             reshard = measure_reshard(axe, torch, dist, ws, rank, local, stream)
         except Exception as e:  # keep the contract line even if the reshard leg fails
             reshard = {"error": f"{type(e).__name__}: {e}"}
+    extras = None
+    if ws == 1 and not args.no_extras:
+        try:
+            extras = measure_extras(axe, torch)
+        except Exception as e:
+            extras = {"error": f"{type(e).__name__}: {e}"}
 
     peak, peak_src = peaks()
     achieved = alg_bytes / (k_ms * 1e-3) / 1e9
@@ -374,6 +435,8 @@ def run_axe(args):
         }
         if reshard is not None:
             out["reshard"] = reshard
+        if extras is not None:
+            out["other_rows"] = extras
         print(json.dumps(out), flush=True)
     if dist:
         dist.barrier()
@@ -391,6 +454,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every step directly (no CUDA graph)")
     ap.add_argument("--no-reshard", action="store_true", help="skip the N>1 axe_redistribute measurements")
+    ap.add_argument("--force-reshard", action="store_true", help="run the reshard leg even at N=1 (code-path check)")
+    ap.add_argument("--no-extras", action="store_true", help="skip the other single-GPU SURVEY §8 rows")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
