@@ -194,7 +194,7 @@ def measure_reshard(axe, torch, dist, ws, rank, local, stream, iters=20, warm=3)
     ms = timed(lambda: p4.execute(comm, src, dst, stream))
     ingress = (ws - 1) * src.numel() * 2
     ref = torch.empty_like(dst)
-    ms_ref = timed(lambda: dist.all_gather_into_tensor(ref, src))
+    ms_ref = timed(lambda: dist.all_gather_into_tensor(ref.view(torch.bfloat16), src.view(torch.bfloat16)))
     res["config4"] = {"P": ws, "pattern": p4.describe()["pattern"], "ms": ms, "ingress_bytes_per_gpu": ingress,
                       "bus_GBps": ingress / (ms * 1e-3) / 1e9, "frac_of_900": ingress / (ms * 1e-3) / 1e9 / 900,
                       "frac_of_measured_770": ingress / (ms * 1e-3) / 1e9 / 770,
