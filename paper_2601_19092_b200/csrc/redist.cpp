@@ -19,6 +19,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -45,7 +46,8 @@ struct Xfer {
   int64_t ms = 0, md = 0;          // element offsets (source local, destination local)
   bool elided = false;             // send straight from src / receive straight into dst
   int64_t stage = 0;               // element offset in the staging buffer when not elided
-  std::shared_ptr<CopyPlan> plan;  // pack (send), unpack (recv) or local copy
+  std::shared_ptr<CopyPlan> plan;  // local copy
+  std::vector<std::shared_ptr<CopyPlan>> cp;  // per wire chunk: pack (send) or unpack (recv)
 };
 
 }  // namespace
@@ -55,6 +57,8 @@ struct axe_redist_plan {
   std::vector<Joint> M;            // memory-only digits, packed order (outermost first)
   std::vector<int64_t> packed;     // packed (compact) element strides of M
   int64_t n = 1;                   // elements per block
+  int nchunk = 1;                  // wire chunks per block (cut along the outermost packed digit)
+  int64_t cn = 1;                  // elements per chunk
   std::vector<Xfer> sends, recvs, locals;
   int64_t send_elems = 0, recv_elems = 0;
   int64_t src_cells = 0, dst_cells = 0;
@@ -65,13 +69,19 @@ struct axe_redist_plan {
   mutable std::mutex mu;
   mutable void *send_buf = nullptr, *recv_buf = nullptr;
   mutable cudaStream_t side = nullptr;
-  mutable cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  mutable cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
+  mutable cudaStream_t pk = nullptr, up = nullptr;  // pack / unpack streams
+  mutable std::vector<cudaEvent_t> ev_pack, ev_recv;
   ~axe_redist_plan() {
     if (send_buf) cudaFree(send_buf);
     if (recv_buf) cudaFree(recv_buf);
-    if (side) cudaStreamDestroy(side);
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
+    for (cudaStream_t x : {side, pk, up})
+      if (x) cudaStreamDestroy(x);
+    for (cudaEvent_t x : {ev_fork, ev_join, ev_join2})
+      if (x) cudaEventDestroy(x);
+    for (auto &v : {ev_pack, ev_recv})
+      for (cudaEvent_t x : v)
+        if (x) cudaEventDestroy(x);
   }
 };
 
@@ -178,6 +188,19 @@ static axe_status plan_redist(const Layout &S, const Storage &sst, const Layout 
   for (auto &m : P->M) P->n *= m.e;
   P->packed.assign(P->M.size(), 1);
   for (int k = (int)P->M.size() - 2; k >= 0; k--) P->packed[k] = P->packed[k + 1] * P->M[k + 1].e;
+  // wire chunks: cutting the outermost packed digit lets packing chunk c+1 overlap sending chunk c
+  // (every chunk is a contiguous slice of the packed block on both sides of the wire)
+  P->nchunk = 1;
+  // (AXE_REDIST_CHUNK_BYTES lowers the 8 MiB minimum chunk, for tests)
+  const char *cb = getenv("AXE_REDIST_CHUNK_BYTES");
+  const int64_t min_chunk = (cb && *cb) ? atoll(cb) : (int64_t(8) << 20);
+  if (!P->M.empty() && P->n * es >= 2 * min_chunk)
+    for (int c : {4, 2})
+      if (P->M[0].e % c == 0 && P->n * es / c >= min_chunk) {
+        P->nchunk = c;
+        break;
+      }
+  P->cn = P->n / P->nchunk;
 
   int64_t nblk = (int64_t)recvr.size();
   for (auto &j : G) nblk *= j.e;
@@ -270,11 +293,26 @@ static axe_status plan_redist(const Layout &S, const Storage &sst, const Layout 
   Storage s_src = mstorage(sst.cells, &sst), s_dst = mstorage(dstst.cells, &dstst);
   Storage s_send = mstorage(std::max<int64_t>(1, P->send_elems), nullptr);
   Storage s_recv = mstorage(std::max<int64_t>(1, P->recv_elems), nullptr);
+  // per-chunk pack / unpack plans: the outermost packed digit shrinks to e0 / nchunk
+  std::vector<std::pair<int64_t, int64_t>> cDsrc = Dsrc, cDdst = Ddst, cDpk = Dpk;
+  const int64_t ce0 = P->M.empty() ? 1 : P->M[0].e / P->nchunk;
+  if (!P->M.empty()) cDsrc[0].first = cDdst[0].first = cDpk[0].first = ce0;
   for (auto &x : P->sends)
-    if (!x.elided) AXE_TRY(subplan(mlayout(Dsrc, {}, x.ms), s_src, mlayout(Dpk, {}, x.stage), s_send, es, &x.plan));
+    if (!x.elided)
+      for (int c = 0; c < P->nchunk; c++) {
+        std::shared_ptr<CopyPlan> q;
+        AXE_TRY(subplan(mlayout(cDsrc, {}, x.ms + (P->M.empty() ? 0 : c * ce0 * P->M[0].ss)), s_src,
+                        mlayout(cDpk, {}, x.stage + c * P->cn), s_send, es, &q));
+        x.cp.push_back(q);
+      }
   for (auto &x : P->recvs)
     if (!x.elided)
-      AXE_TRY(subplan(mlayout(Dpk, {}, x.stage), s_recv, mlayout(Ddst, dst_mem_R, x.md), s_dst, es, &x.plan));
+      for (int c = 0; c < P->nchunk; c++) {
+        std::shared_ptr<CopyPlan> q;
+        AXE_TRY(subplan(mlayout(cDpk, {}, x.stage + c * P->cn), s_recv,
+                        mlayout(cDdst, dst_mem_R, x.md + (P->M.empty() ? 0 : c * ce0 * P->M[0].ds)), s_dst, es, &q));
+        x.cp.push_back(q);
+      }
   for (auto &x : P->locals)
     AXE_TRY(subplan(mlayout(Dsrc, {}, x.ms), s_src, mlayout(Ddst, dst_mem_R, x.md), s_dst, es, &x.plan));
 
@@ -318,10 +356,10 @@ static axe_status plan_redist(const Layout &S, const Storage &sst, const Layout 
   snprintf(buf, sizeof buf,
            "{\"pattern\":\"%s\",\"nranks\":%d,\"rank\":%d,\"block_elems\":%lld,\"blocks\":%lld,\"sends\":%zu,"
            "\"recvs\":%zu,\"locals\":%zu,\"send_elems\":%lld,\"recv_elems\":%lld,\"packs\":%d,\"unpacks\":%d,"
-           "\"owner_replicas\":%zu,\"receiver_replicas\":%zu}",
+           "\"owner_replicas\":%zu,\"receiver_replicas\":%zu,\"wire_chunks\":%d}",
            P->allgather ? "allgather" : (P->sends.empty() && P->recvs.empty() ? "local" : "exchange"), nranks, rank,
            (long long)P->n, (long long)blocks.size(), P->sends.size(), P->recvs.size(), P->locals.size(), (long long)sc,
-           (long long)rc, ps, pu, own.size(), recvr.size());
+           (long long)rc, ps, pu, own.size(), recvr.size(), P->nchunk);
   P->desc = buf;
   return AXE_OK;
 }
@@ -334,6 +372,16 @@ static axe_status ensure_scratch(const axe_redist_plan *P) {
   if (e == cudaSuccess && !P->side) e = cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking);
   if (e == cudaSuccess && !P->ev_fork) e = cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess && !P->ev_join) e = cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming);
+  if (e == cudaSuccess && !P->ev_join2) e = cudaEventCreateWithFlags(&P->ev_join2, cudaEventDisableTiming);
+  if (e == cudaSuccess && !P->pk) e = cudaStreamCreateWithFlags(&P->pk, cudaStreamNonBlocking);
+  if (e == cudaSuccess && !P->up) e = cudaStreamCreateWithFlags(&P->up, cudaStreamNonBlocking);
+  while (e == cudaSuccess && (int)P->ev_pack.size() < P->nchunk) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    e = cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
+    P->ev_pack.push_back(a);
+    P->ev_recv.push_back(b);
+  }
   if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "redistribute scratch: %s", cudaGetErrorString(e));
   return AXE_OK;
 }
@@ -357,35 +405,69 @@ static axe_status exec_redist(const axe_redist_plan *P, axe_comm *C, const void 
     return AXE_OK;
   }
   AXE_TRY(ensure_scratch(P));
-  // local copies on a side stream, overlapping pack + exchange
   cudaError_t e = cudaSuccess;
+#define CU_TRY(x)                                                                        \
+  do {                                                                                   \
+    e = (x);                                                                             \
+    if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "%s: %s", #x, cudaGetErrorString(e));   \
+  } while (0)
+  bool packs = false, unpacks = false;
+  for (auto &x : P->sends) packs |= !x.elided;
+  for (auto &x : P->recvs) unpacks |= !x.elided;
+  CU_TRY(cudaEventRecord(P->ev_fork, st));
+  // local copies on a side stream, overlapping pack + exchange
   if (!P->locals.empty()) {
-    e = cudaEventRecord(P->ev_fork, st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(P->side, P->ev_fork, 0);
-    if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "fork: %s", cudaGetErrorString(e));
+    CU_TRY(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
     stream_forget(P->side);
     for (auto &x : P->locals) AXE_TRY(run_copy(*x.plan, src, dst, P->side));
   }
-  for (auto &x : P->sends)
-    if (!x.elided) AXE_TRY(run_copy(*x.plan, src, P->send_buf, st));
-  NCCL_TRY(ncclGroupStart());
-  for (auto &x : P->sends) {
-    const void *ptr = x.elided ? (const void *)(s + x.ms * P->es) : (const void *)((uint8_t *)P->send_buf + x.stage * P->es);
-    NCCL_TRY(ncclSend(ptr, bytes, ncclUint8, x.peer, C->comm, st));
+  // packs, chunk by chunk, on the pack stream
+  if (packs) {
+    CU_TRY(cudaStreamWaitEvent(P->pk, P->ev_fork, 0));
+    stream_forget(P->pk);
+    for (int c = 0; c < P->nchunk; c++) {
+      for (auto &x : P->sends)
+        if (!x.elided) AXE_TRY(run_copy(*x.cp[c], src, P->send_buf, P->pk));
+      CU_TRY(cudaEventRecord(P->ev_pack[c], P->pk));
+    }
   }
-  for (auto &x : P->recvs) {
-    void *ptr = x.elided ? (void *)(d + x.md * P->es) : (void *)((uint8_t *)P->recv_buf + x.stage * P->es);
-    NCCL_TRY(ncclRecv(ptr, bytes, ncclUint8, x.peer, C->comm, st));
+  if (unpacks) {
+    CU_TRY(cudaStreamWaitEvent(P->up, P->ev_fork, 0));
   }
-  NCCL_TRY(ncclGroupEnd());
-  stream_forget(st);  // the next libaxe kernel on st waits for NCCL (full dependency)
-  for (auto &x : P->recvs)
-    if (!x.elided) AXE_TRY(run_copy(*x.plan, P->recv_buf, dst, st));
+  // the wire: one NCCL group per chunk (chunk c of every block), after that chunk is packed
+  const size_t cbytes = (size_t)(P->cn * P->es);
+  for (int c = 0; c < P->nchunk; c++) {
+    if (packs) CU_TRY(cudaStreamWaitEvent(st, P->ev_pack[c], 0));
+    NCCL_TRY(ncclGroupStart());
+    for (auto &x : P->sends) {
+      const uint8_t *ptr = x.elided ? s + (x.ms + (P->M.empty() ? 0 : c * (P->M[0].e / P->nchunk) * P->M[0].ss)) * P->es
+                                    : (const uint8_t *)P->send_buf + (x.stage + c * P->cn) * P->es;
+      NCCL_TRY(ncclSend(ptr, cbytes, ncclUint8, x.peer, C->comm, st));
+    }
+    for (auto &x : P->recvs) {
+      uint8_t *ptr = x.elided ? d + (x.md + (P->M.empty() ? 0 : c * (P->M[0].e / P->nchunk) * P->M[0].ds)) * P->es
+                              : (uint8_t *)P->recv_buf + (x.stage + c * P->cn) * P->es;
+      NCCL_TRY(ncclRecv(ptr, cbytes, ncclUint8, x.peer, C->comm, st));
+    }
+    NCCL_TRY(ncclGroupEnd());
+    if (unpacks) {
+      CU_TRY(cudaEventRecord(P->ev_recv[c], st));
+      CU_TRY(cudaStreamWaitEvent(P->up, P->ev_recv[c], 0));
+      stream_forget(P->up);  // full dependency on the NCCL kernels that filled this chunk
+      for (auto &x : P->recvs)
+        if (!x.elided) AXE_TRY(run_copy(*x.cp[c], P->recv_buf, dst, P->up));
+    }
+  }
+  stream_forget(st);
   if (!P->locals.empty()) {
-    e = cudaEventRecord(P->ev_join, P->side);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, P->ev_join, 0);
-    if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "join: %s", cudaGetErrorString(e));
+    CU_TRY(cudaEventRecord(P->ev_join, P->side));
+    CU_TRY(cudaStreamWaitEvent(st, P->ev_join, 0));
   }
+  if (unpacks) {
+    CU_TRY(cudaEventRecord(P->ev_join2, P->up));
+    CU_TRY(cudaStreamWaitEvent(st, P->ev_join2, 0));
+  }
+#undef CU_TRY
   return AXE_OK;
 }
 
@@ -473,25 +555,29 @@ axe_status axe_redist_plan_counts(const axe_redist_plan *plan, int peer, int64_t
 
 axe_status axe_redist_plan_map(const axe_redist_plan *plan, int kind, int peer, int64_t k, int64_t *a, int64_t *b) {
   if (!plan || !a || !b) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
-  const std::vector<Xfer> &lst = kind == 0 ? plan->sends : kind == 1 ? plan->recvs : plan->locals;
   if (kind < 0 || kind > 2) AXE_FAIL(AXE_ERR_INVALID_ARG, "kind must be 0, 1 or 2");
-  int64_t idx = k / plan->n, j = k % plan->n;
-  const Xfer *x = nullptr;
+  const std::vector<Xfer> &lst = kind == 0 ? plan->sends : kind == 1 ? plan->recvs : plan->locals;
+  std::vector<const Xfer *> mine;
   for (auto &e : lst)
-    if (kind == 2 || e.peer == peer) {
-      if (idx == 0) {
-        x = &e;
-        break;
-      }
-      idx--;
-    }
-  if (k < 0 || !x) AXE_FAIL(AXE_ERR_DOMAIN, "element %lld out of range", (long long)k);
+    if (kind == 2 || e.peer == peer) mine.push_back(&e);
+  const int64_t nb = (int64_t)mine.size();
+  if (k < 0 || k >= nb * plan->n) AXE_FAIL(AXE_ERR_DOMAIN, "element %lld out of range", (long long)k);
+  int64_t bi, j;
+  if (kind == 2) {  // local copies: block-major
+    bi = k / plan->n;
+    j = k % plan->n;
+  } else {          // the wire is chunk-major: chunk c of every block, then chunk c+1
+    const int64_t c = k / (nb * plan->cn), w = k % (nb * plan->cn);
+    bi = w / plan->cn;
+    j = c * plan->cn + w % plan->cn;
+  }
+  const Xfer *x = mine[bi];
   int64_t so = x->ms, dof = x->md;
   for (int m = (int)plan->M.size() - 1; m >= 0; m--) {
-    int64_t d = j % plan->M[m].e;
+    int64_t dg = j % plan->M[m].e;
     j /= plan->M[m].e;
-    so += d * plan->M[m].ss;
-    dof += d * plan->M[m].ds;
+    so += dg * plan->M[m].ss;
+    dof += dg * plan->M[m].ds;
   }
   *a = kind == 1 ? dof : so;
   *b = kind == 2 ? dof : -1;
@@ -537,37 +623,46 @@ axe_status axe_redist_emulate(const axe_redist_plan *const *plans, int nranks, c
       AXE_FAIL(AXE_ERR_INVALID_ARG, "plans[%d] is not rank %d of %d", r, r, nranks);
     AXE_TRY(ensure_scratch(plans[r]));
   }
+  const int nch = plans[0]->nchunk;
   for (int r = 0; r < nranks; r++)
-    for (auto &x : plans[r]->sends)
-      if (!x.elided) AXE_TRY(run_copy(*x.plan, src_locals[r], plans[r]->send_buf, st));
-  // the wire: the k-th block rank r sends to p is the k-th block p receives from r
-  for (int r = 0; r < nranks; r++)
-    for (int p = 0; p < nranks; p++) {
-      if (p == r) continue;
-      std::vector<const Xfer *> out, in;
+    if (plans[r]->nchunk != nch) AXE_FAIL(AXE_ERR_INVALID_ARG, "plans disagree on wire chunks");
+  for (int c = 0; c < nch; c++) {
+    for (int r = 0; r < nranks; r++)
       for (auto &x : plans[r]->sends)
-        if (x.peer == p) out.push_back(&x);
-      for (auto &x : plans[p]->recvs)
-        if (x.peer == r) in.push_back(&x);
-      if (out.size() != in.size())
-        AXE_FAIL(AXE_ERR_INVALID_ARG, "plans disagree: rank %d sends %zu blocks to %d, which expects %zu", r,
-                 out.size(), p, in.size());
-      const size_t bytes = (size_t)(plans[r]->n * plans[r]->es);
-      for (size_t i = 0; i < out.size(); i++) {
-        const uint8_t *sp = out[i]->elided ? (const uint8_t *)src_locals[r] + out[i]->ms * plans[r]->es
-                                           : (const uint8_t *)plans[r]->send_buf + out[i]->stage * plans[r]->es;
-        uint8_t *dp = in[i]->elided ? (uint8_t *)dst_locals[p] + in[i]->md * plans[p]->es
-                                    : (uint8_t *)plans[p]->recv_buf + in[i]->stage * plans[p]->es;
-        cudaError_t e = cudaMemcpyAsync(dp, sp, bytes, cudaMemcpyDeviceToDevice, st);
-        if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "emulated exchange: %s", cudaGetErrorString(e));
+        if (!x.elided) AXE_TRY(run_copy(*x.cp[c], src_locals[r], plans[r]->send_buf, st));
+    // the wire: chunk c of the k-th block rank r sends to p is chunk c of the k-th block p receives from r
+    for (int r = 0; r < nranks; r++)
+      for (int p = 0; p < nranks; p++) {
+        if (p == r) continue;
+        std::vector<const Xfer *> out, in;
+        for (auto &x : plans[r]->sends)
+          if (x.peer == p) out.push_back(&x);
+        for (auto &x : plans[p]->recvs)
+          if (x.peer == r) in.push_back(&x);
+        if (out.size() != in.size())
+          AXE_FAIL(AXE_ERR_INVALID_ARG, "plans disagree: rank %d sends %zu blocks to %d, which expects %zu", r,
+                   out.size(), p, in.size());
+        const axe_redist_plan *R = plans[r], *Q = plans[p];
+        const size_t bytes = (size_t)(R->cn * R->es);
+        const int64_t ce0 = R->M.empty() ? 0 : R->M[0].e / nch;
+        for (size_t i = 0; i < out.size(); i++) {
+          const uint8_t *sp = out[i]->elided
+                                  ? (const uint8_t *)src_locals[r] + (out[i]->ms + (R->M.empty() ? 0 : c * ce0 * R->M[0].ss)) * R->es
+                                  : (const uint8_t *)R->send_buf + (out[i]->stage + c * R->cn) * R->es;
+          uint8_t *dp = in[i]->elided
+                            ? (uint8_t *)dst_locals[p] + (in[i]->md + (Q->M.empty() ? 0 : c * ce0 * Q->M[0].ds)) * Q->es
+                            : (uint8_t *)Q->recv_buf + (in[i]->stage + c * Q->cn) * Q->es;
+          cudaError_t e = cudaMemcpyAsync(dp, sp, bytes, cudaMemcpyDeviceToDevice, st);
+          if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "emulated exchange: %s", cudaGetErrorString(e));
+        }
       }
-    }
-  stream_forget(st);
-  for (int r = 0; r < nranks; r++) {
-    for (auto &x : plans[r]->recvs)
-      if (!x.elided) AXE_TRY(run_copy(*x.plan, plans[r]->recv_buf, dst_locals[r], st));
-    for (auto &x : plans[r]->locals) AXE_TRY(run_copy(*x.plan, src_locals[r], dst_locals[r], st));
+    stream_forget(st);
+    for (int r = 0; r < nranks; r++)
+      for (auto &x : plans[r]->recvs)
+        if (!x.elided) AXE_TRY(run_copy(*x.cp[c], plans[r]->recv_buf, dst_locals[r], st));
   }
+  for (int r = 0; r < nranks; r++)
+    for (auto &x : plans[r]->locals) AXE_TRY(run_copy(*x.plan, src_locals[r], dst_locals[r], st));
   return AXE_OK;
 }
 

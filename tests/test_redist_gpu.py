@@ -106,3 +106,11 @@ def test_random_meshes(axe, seed):
     cfg = dict(name=f"mesh{seed}", es=int(rng.choice([2, 4])), src=src, src_st=linear_storage(sc), dst=dst,
                dst_st=linear_storage(dc), seed=seed, nranks=n)
     run(axe, cfg)
+
+
+@pytest.mark.parametrize("shape", [(256, 128), (64, 32, 2, 2)])
+def test_config5_chunked_emulated(axe, shape, monkeypatch):
+    """Per-chunk pack kernels and wire copies (AXE_REDIST_CHUNK_BYTES forces chunking at small sizes)."""
+    monkeypatch.setenv("AXE_REDIST_CHUNK_BYTES", "1024")
+    d = run(axe, synth.config5(*shape))
+    assert d["wire_chunks"] >= 2
