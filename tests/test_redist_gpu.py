@@ -111,6 +111,6 @@ def test_random_meshes(axe, seed):
 @pytest.mark.parametrize("shape", [(256, 128), (64, 32, 2, 2)])
 def test_config5_chunked_emulated(axe, shape, monkeypatch):
     """Per-chunk pack kernels and wire copies (AXE_REDIST_CHUNK_BYTES forces chunking at small sizes)."""
-    monkeypatch.setenv("AXE_REDIST_CHUNK_BYTES", "1024")
+    monkeypatch.setenv("AXE_REDIST_CHUNK_BYTES", "256")
     d = run(axe, synth.config5(*shape))
     assert d["wire_chunks"] >= 2
