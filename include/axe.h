@@ -105,6 +105,35 @@ axe_status axe_layout_canonicalize(const axe_layout *layout, axe_layout **out, i
 axe_status axe_layout_bounds(const axe_layout *layout, const char *axis, int64_t *min, int64_t *max);
 
 /* ------------------------------------------------------------------------- */
+/* Layout operators (§3.3, Apps. B-F): host-side algebra, the building blocks */
+/* of the paper's TMA lowering.  Shapes are int64 arrays of `rank`  */
+/* dimensions.  Algorithmic failure (the conditions are sufficient only) is   */
+/* AXE_ERR_UNSUPPORTED; shape admission failure is AXE_ERR_SIZE_MISMATCH.     */
+/* ------------------------------------------------------------------------- */
+
+/* Group-By-Shape (Alg. 1): *out has D refined so that consecutive
+ * blocks have extent products shape[i]; bounds (may be NULL, rank+1 ints)
+ * receives the block boundaries into the refined D.  f_L is unchanged. */
+axe_status axe_layout_group(const axe_layout *layout, const int64_t *shape, int rank, axe_layout **out, int *bounds);
+/* span_a(f_L) in closed form (Lemma span-closed); 1 for an axis the layout never names. */
+axe_status axe_layout_span(const axe_layout *layout, const char *axis, int64_t *span);
+/* Tile (Alg. 2): f_T(x||y) = f_A(x) (.) span(f_B) + f_B(y), T grouped by
+ * the interleaved shape (S_A[0], S_B[0], ..., S_A[r-1], S_B[r-1]). */
+axe_status axe_layout_tile(const axe_layout *A, const int64_t *S_A, const axe_layout *B, const int64_t *S_B, int rank,
+                           axe_layout **out);
+/* TileOf_AndRecoverC (Alg. 3, with the offset / replication checks of
+ * P:1332-1380): on success A = C (x) B; S_C (rank int64s) receives S_A / S_B. */
+axe_status axe_layout_tile_of(const axe_layout *A, const int64_t *S_A, const axe_layout *B, const int64_t *S_B,
+                              int rank, axe_layout **C, int64_t *S_C);
+/* Direct sum on the tiling domain (App. F): f(x||y) = f_A(x) + f_B(y). */
+axe_status axe_layout_direct_sum(const axe_layout *A, const int64_t *S_A, const axe_layout *B, const int64_t *S_B,
+                                 int rank, axe_layout **out);
+/* Slice L[R:S] (§3.3, Alg. 4 per block): region [begin, begin+extent) of
+ * shape S; f_{L[R:S]<extent>}(u) = f_{L<S>}(u + begin). */
+axe_status axe_layout_slice(const axe_layout *layout, const int64_t *shape, int rank, const int64_t *begin,
+                            const int64_t *extent, axe_layout **out);
+
+/* ------------------------------------------------------------------------- */
 /* Storage descriptors (R16, R17)                                             */
 /* ------------------------------------------------------------------------- */
 

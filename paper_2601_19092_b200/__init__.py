@@ -65,6 +65,12 @@ _SIGS = {
     "axe_layout_eval": ([_vp, _i64, _pi64, _i64], C.c_int),
     "axe_layout_canonicalize": ([_vp, C.POINTER(_vp), C.POINTER(C.c_int)], C.c_int),
     "axe_layout_bounds": ([_vp, C.c_char_p, _pi64, _pi64], C.c_int),
+    "axe_layout_group": ([_vp, _pi64, C.c_int, C.POINTER(_vp), C.POINTER(C.c_int)], C.c_int),
+    "axe_layout_span": ([_vp, C.c_char_p, _pi64], C.c_int),
+    "axe_layout_tile": ([_vp, _pi64, _vp, _pi64, C.c_int, C.POINTER(_vp)], C.c_int),
+    "axe_layout_tile_of": ([_vp, _pi64, _vp, _pi64, C.c_int, C.POINTER(_vp), _pi64], C.c_int),
+    "axe_layout_direct_sum": ([_vp, _pi64, _vp, _pi64, C.c_int, C.POINTER(_vp)], C.c_int),
+    "axe_layout_slice": ([_vp, _pi64, C.c_int, _pi64, _pi64, C.POINTER(_vp)], C.c_int),
     "axe_copy_plan_create": ([_vp, C.POINTER(axe_storage), _vp, C.POINTER(axe_storage), C.c_int, C.c_int,
                               C.POINTER(_vp)], C.c_int),
     "axe_copy_plan_execute": ([_vp, _vp, _vp, _vp], C.c_int),
@@ -258,6 +264,51 @@ class Layout:
         lo, hi = C.c_int64(), C.c_int64()
         _check(_lib.axe_layout_bounds(self._h, axis.encode(), C.byref(lo), C.byref(hi)), "axe_layout_bounds")
         return lo.value, hi.value
+
+    # ---- layout operators (§3.3, Apps. B-F) ----
+    @staticmethod
+    def _shape(S):
+        return (C.c_int64 * len(S))(*[int(v) for v in S])
+
+    def span(self, axis: str) -> int:
+        v = C.c_int64()
+        _check(_lib.axe_layout_span(self._h, axis.encode(), C.byref(v)), "axe_layout_span")
+        return v.value
+
+    def group(self, S):
+        """Group-By-Shape (Alg. 1): (grouped layout, block boundaries)."""
+        h = C.c_void_p()
+        b = (C.c_int * (len(S) + 1))()
+        _check(_lib.axe_layout_group(self._h, self._shape(S), len(S), C.byref(h), b), "axe_layout_group")
+        return Layout(_handle=h), list(b)
+
+    def tile(self, SA, B, SB):
+        """self (x) B (Alg. 2), grouped by the interleaved shape."""
+        h = C.c_void_p()
+        _check(_lib.axe_layout_tile(self._h, self._shape(SA), Layout.of(B).handle, self._shape(SB), len(SA),
+                                    C.byref(h)), "axe_layout_tile")
+        return Layout(_handle=h)
+
+    def tile_of(self, SA, B, SB):
+        """TileOf_AndRecoverC (Alg. 3): (C, S_C) with self = C (x) B."""
+        h = C.c_void_p()
+        sc = (C.c_int64 * len(SA))()
+        _check(_lib.axe_layout_tile_of(self._h, self._shape(SA), Layout.of(B).handle, self._shape(SB), len(SA),
+                                       C.byref(h), sc), "axe_layout_tile_of")
+        return Layout(_handle=h), list(sc)
+
+    def direct_sum(self, SA, B, SB):
+        h = C.c_void_p()
+        _check(_lib.axe_layout_direct_sum(self._h, self._shape(SA), Layout.of(B).handle, self._shape(SB), len(SA),
+                                          C.byref(h)), "axe_layout_direct_sum")
+        return Layout(_handle=h)
+
+    def slice(self, S, begin, extent):
+        """L[R:S] (Alg. 4 per block) for the region [begin, begin + extent)."""
+        h = C.c_void_p()
+        _check(_lib.axe_layout_slice(self._h, self._shape(S), len(S), self._shape(begin), self._shape(extent),
+                                     C.byref(h)), "axe_layout_slice")
+        return Layout(_handle=h)
 
 
 # --------------------------------------------------------------------------- copy
