@@ -240,6 +240,15 @@ axe_status axe_redist_plan_create(const axe_layout *src, const axe_storage *src_
  * rank's device buffers. */
 axe_status axe_redist_plan_execute(const axe_redist_plan *plan, axe_comm *comm, const void *src_local,
                                    void *dst_local, void *cuda_stream);
+/* One-sided form: every block this rank sends is ONE copy kernel reading
+ * src_local and writing straight into the receiver's destination buffer
+ * dst_peers[receiver] (peer memory mapped into this process, e.g. CUDA IPC or
+ * torch symmetric memory; dst_peers[rank] is this rank's own dst_local) -- the
+ * pack, the NVLink transfer and the unpack fused.  The caller orders it across
+ * ranks: every peer's dst buffer must be ready before (a barrier) and is
+ * complete only after every rank's launches finished (a barrier after). */
+axe_status axe_redist_plan_execute_peers(const axe_redist_plan *plan, const void *src_local, void *const *dst_peers,
+                                         void *cuda_stream);
 /* JSON description: pattern (allgather / exchange / local), per-peer element
  * counts and the kernels used. */
 axe_status axe_redist_plan_describe(const axe_redist_plan *plan, char *buf, int capacity);

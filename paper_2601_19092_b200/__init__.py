@@ -86,6 +86,7 @@ _SIGS = {
                                 C.POINTER(_vp)], C.c_int),
     "axe_redist_plan_execute": ([_vp, _vp, _vp, _vp, _vp], C.c_int),
     "axe_redist_plan_describe": ([_vp, C.c_char_p, C.c_int], C.c_int),
+    "axe_redist_plan_execute_peers": ([_vp, _vp, C.POINTER(_vp), _vp], C.c_int),
     "axe_redist_plan_counts": ([_vp, C.c_int, _pi64, _pi64], C.c_int),
     "axe_redist_plan_map": ([_vp, C.c_int, C.c_int, _i64, _pi64, _pi64], C.c_int),
     "axe_redist_plan_destroy": ([_vp], None),
@@ -424,6 +425,12 @@ class RedistPlan:
         buf = C.create_string_buffer(1 << 14)
         _check(_lib.axe_redist_plan_describe(self._h, buf, len(buf)), "axe_redist_plan_describe")
         return json.loads(buf.value.decode())
+
+    def execute_peers(self, src_local, dst_peers, stream=None):
+        """One-sided: copy kernels from src_local straight into every receiver's dst (peer pointers)."""
+        arr = (C.c_void_p * len(dst_peers))(*[_ptr(d) for d in dst_peers])
+        _check(_lib.axe_redist_plan_execute_peers(self._h, _ptr(src_local), arr, _stream(stream)),
+               "axe_redist_plan_execute_peers")
 
     def counts(self, peer: int):
         a, b = C.c_int64(), C.c_int64()

@@ -315,6 +315,11 @@ static axe_status plan_redist(const Layout &S, const Storage &sst, const Layout 
       }
   for (auto &x : P->locals)
     AXE_TRY(subplan(mlayout(Dsrc, {}, x.ms), s_src, mlayout(Ddst, dst_mem_R, x.md), s_dst, es, &x.plan));
+  // one-sided form (axe_redist_plan_execute_peers): every outgoing block is one copy kernel from
+  // src_local straight into the receiver's dst_local (peer memory over NVLink) -- pack, wire and
+  // unpack fused, no staging
+  for (auto &x : P->sends)
+    AXE_TRY(subplan(mlayout(Dsrc, {}, x.ms), s_src, mlayout(Ddst, dst_mem_R, x.md), s_dst, es, &x.plan));
 
   // all-gather pattern (decided from the global block list, so every rank agrees):
   // each rank r sends one contiguous block at the same offset to every other rank and
@@ -531,6 +536,18 @@ axe_status axe_redist_plan_execute(const axe_redist_plan *plan, axe_comm *comm, 
                                    void *stream) {
   if (!plan) AXE_FAIL(AXE_ERR_INVALID_ARG, "plan is NULL");
   return exec_redist(plan, comm, src_local, dst_local, (cudaStream_t)stream);
+}
+
+axe_status axe_redist_plan_execute_peers(const axe_redist_plan *plan, const void *src_local, void *const *dst_peers,
+                                         void *stream) {
+  if (!plan || !src_local || !dst_peers) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
+  for (int r = 0; r < plan->nranks; r++)
+    if (!dst_peers[r]) AXE_FAIL(AXE_ERR_INVALID_ARG, "dst_peers[%d] is NULL", r);
+  cudaStream_t st = (cudaStream_t)stream;
+  // remote blocks first (they cross NVLink), then the local ones
+  for (auto &x : plan->sends) AXE_TRY(run_copy(*x.plan, src_local, dst_peers[x.peer], st));
+  for (auto &x : plan->locals) AXE_TRY(run_copy(*x.plan, src_local, dst_peers[plan->rank], st));
+  return AXE_OK;
 }
 
 axe_status axe_redist_plan_describe(const axe_redist_plan *plan, char *buf, int capacity) {

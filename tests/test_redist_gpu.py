@@ -114,3 +114,27 @@ def test_config5_chunked_emulated(axe, shape, monkeypatch):
     monkeypatch.setenv("AXE_REDIST_CHUNK_BYTES", "256")
     d = run(axe, synth.config5(*shape))
     assert d["wire_chunks"] >= 2
+
+
+@pytest.mark.parametrize("mk", [lambda: synth.config4(4, 256), lambda: synth.config5(256, 128),
+                                lambda: synth.config5(64, 32, 2, 2)])
+def test_one_sided_peer_stores(axe, mk):
+    """axe_redist_plan_execute_peers: each rank's copy kernels write straight into the receivers' dst
+    buffers (on one GPU the "peer" buffers are ordinary device buffers); result equals the oracle."""
+    cfg = mk()
+    n, es = cfg["nranks"], cfg["es"]
+    ed, _ = oracle.sizes(cfg["src"])
+    v = synth.values(ed, es, cfg["seed"])
+    sfill = synth.sentinel(synth.storage_cells(cfg["src_st"]) * es, cfg["seed"] + 3)
+    src = oracle.scatter_ranks(cfg["src"], cfg["src_st"], v, es, n, sfill, NT)
+    dfill = synth.sentinel(synth.storage_cells(cfg["dst_st"]) * es, cfg["seed"])
+    plans = [axe.RedistPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], es, n, r) for r in range(n)]
+    s_dev = [torch.from_numpy(s).cuda() for s in src]
+    d_dev = [torch.from_numpy(dfill).cuda() for _ in range(n)]
+    for r in range(n):
+        plans[r].execute_peers(s_dev[r], d_dev)
+    torch.cuda.synchronize()
+    exp = [dfill.copy() for _ in range(n)]
+    oracle.redistribute(cfg["src"], cfg["src_st"], src, cfg["dst"], cfg["dst_st"], exp, es, nthreads=NT)
+    for r in range(n):
+        assert np.array_equal(d_dev[r].cpu().numpy(), exp[r]), r
