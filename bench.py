@@ -214,7 +214,42 @@ def measure_reshard(axe, torch, dist, ws, rank, local, stream, iters=20, warm=3)
     torch.cuda.synchronize()
     dist.barrier()
     del comm
+    # one-sided form: copy kernels write straight into the peers' dst buffers (torch symmetric memory)
+    res["one_sided"] = measure_reshard_p2p(axe, torch, dist, ws, rank, local, stream, timed)
     return res
+
+
+def measure_reshard_p2p(axe, torch, dist, ws, rank, local, stream, timed):
+    ok = torch.tensor([1], device="cuda")
+    try:
+        import torch.distributed._symmetric_memory as symm_mem  # noqa: F401
+    except Exception:
+        ok.zero_()
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)      # every rank takes the same branch
+    if not int(ok.item()):
+        return {"skipped": "torch symmetric memory unavailable"}
+    import torch.distributed._symmetric_memory as symm_mem
+    out = {}
+    cases = [("config4", synth.config4(ws))] + ([("config5", synth.config5())] if ws == 8 else [])
+    for name, cfg in cases:
+        plan = axe.RedistPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], 2, ws, rank)
+        buf = symm_mem.empty(synth.storage_cells(cfg["dst_st"]), dtype=torch.bfloat16, device=f"cuda:{local}")
+        hdl = symm_mem.rendezvous(buf, dist.group.WORLD)
+        peers = [int(p) for p in hdl.buffer_ptrs]
+        src = torch.empty(synth.storage_cells(cfg["src_st"]), dtype=torch.bfloat16, device="cuda").normal_()
+
+        def fn():
+            hdl.barrier(channel=0)
+            plan.execute_peers(src, peers, stream)
+            hdl.barrier(channel=0)
+        ms = timed(fn)
+        ingress = max(plan.counts(q)[1] for q in range(ws) if q != rank) * 2 if ws > 1 else 0
+        if name == "config4":
+            ingress = (ws - 1) * src.numel() * 2
+        out[name] = {"ms": ms, "ingress_bytes_per_gpu": ingress, "bus_GBps": ingress / (ms * 1e-3) / 1e9,
+                     "frac_of_900": ingress / (ms * 1e-3) / 1e9 / 900}
+        del buf, hdl, src
+    return out
 
 
 def _time_plan(torch, plan, reps=10):
