@@ -174,7 +174,8 @@ enum {
   AXE_KERNEL_VECTOR = 2,  /* K1: joint-digit vectorised LDG/STG copy                         */
   AXE_KERNEL_TMA = 3,     /* K1-TMA: TMA box load into swizzled smem + bulk store            */
   AXE_KERNEL_TILE = 4,    /* K2: smem-staged tile permute / transpose                        */
-  AXE_KERNEL_REGISTER = 5 /* K3: warp-register permute through movmatrix (b16 8x8 atoms)     */
+  AXE_KERNEL_REGISTER = 5, /* K3: warp-register permute through movmatrix (b16 8x8 atoms)    */
+  AXE_KERNEL_TMA_TILE = 6  /* K2T: TMA SW128 box staging + conflict-free gather (transposes)  */
 };
 
 typedef struct axe_copy_plan axe_copy_plan;

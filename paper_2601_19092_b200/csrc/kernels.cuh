@@ -139,6 +139,30 @@ struct K2Params {
   int dep;
 };
 
+// ---------------------------------------------------------------- K2T: TMA-staged transpose
+// The source box (H rows of 128 bytes along the source-contiguous digit) is
+// TMA-loaded with SWIZZLE_128B into an S-stage smem ring; the 8 warps gather
+// 16-byte destination vectors along the destination-contiguous digit (thread
+// lanes walk the 128-byte row, which the swizzle makes bank-conflict free) and
+// store them with st.global.v4.  Box loads need no registers, so many boxes
+// are in flight per SM.
+struct K2TParams {
+  uint32_t ntiles;
+  int nd;                      // tile-index digits, outermost first
+  FastDiv fd[TMA_MAXD];
+  int32_t cdim[TMA_MAXD];      // tensor-map dimension of the digit (1: rows, 2..4: outer dims)
+  int32_t cmul[TMA_MAXD];
+  int64_t dstride[TMA_MAXD];   // destination byte stride of the digit
+  int64_t dbase;
+  uint32_t W;                  // elements per box row (128 / es)
+  uint32_t H;                  // box rows
+  int64_t dcol;                // destination byte stride of the source-contiguous digit (one column)
+  int stages;
+  int nrep;
+  int64_t rep[K1_MAXREP];
+  int dep;
+};
+
 // ---------------------------------------------------------------- K3 movmatrix
 // Register-layout permute that is, on every 512-byte "warp row" of a register
 // dump (32 lanes x 8 b16 registers), the per-register 8x8 transpose of

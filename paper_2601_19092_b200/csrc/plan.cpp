@@ -214,6 +214,7 @@ static int env_kernel() {
   if (!strcmp(e, "tma")) return AXE_KERNEL_TMA;
   if (!strcmp(e, "tile")) return AXE_KERNEL_TILE;
   if (!strcmp(e, "register")) return AXE_KERNEL_REGISTER;
+  if (!strcmp(e, "tma_tile")) return AXE_KERNEL_TMA_TILE;
   return AXE_KERNEL_AUTO;
 }
 
@@ -722,6 +723,14 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
     if (kernel == AXE_KERNEL_REGISTER)
       AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced register kernel cannot run these layouts: %s", w3.c_str());
   }
+  if (joint && kernel == AXE_KERNEL_TMA_TILE) {
+    if (build_k2t(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &why)) {
+      P.kernel = KK_TMA_TILE;
+      *out = std::move(P);
+      return AXE_OK;
+    }
+    AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced tma_tile kernel cannot run these layouts: %s", why.c_str());
+  }
   if (joint && kernel == AXE_KERNEL_TILE) {
     if (build_k2(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &why)) {
       P.kernel = KK_TILE;
@@ -737,6 +746,12 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
       if (kernel == AXE_KERNEL_AUTO && P.vb < 16 && (P.vb <= 2 || P.k1_sector_eff < 0.5)) {
         CopyPlan T = P;
         std::string w2;
+        if (build_k2t(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &T, &w2)) {
+          T.kernel = KK_TMA_TILE;
+          *out = std::move(T);
+          return AXE_OK;
+        }
+        T = P;
         if (build_k2(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &T, &w2)) {
           T.kernel = KK_TILE;
           *out = std::move(T);
@@ -798,6 +813,24 @@ int stream_dependency(cudaStream_t st, uintptr_t s0, uintptr_t s1, uintptr_t d0,
   return dep;
 }
 
+// The plan's CUtensorMap for a given pointer (encoded once per pointer, small per-plan cache).
+static axe_status tensor_map_for(const CopyPlan &p, const void *tptr, std::array<uint64_t, 16> *map) {
+  {
+    std::lock_guard<std::mutex> lk(p.tm_cache->mu);
+    for (auto &m : p.tm_cache->maps)
+      if (m.first == tptr) {
+        *map = m.second;
+        return AXE_OK;
+      }
+  }
+  int r = encode_tensor_map(map->data(), (uint8_t *)tptr + p.tm_base, p.tm_dims, p.tm_strides, p.tm_box, p.tm_swizzle);
+  if (r != 0) AXE_FAIL(AXE_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", r);
+  std::lock_guard<std::mutex> lk(p.tm_cache->mu);
+  if (p.tm_cache->maps.size() >= 32) p.tm_cache->maps.erase(p.tm_cache->maps.begin());
+  p.tm_cache->maps.push_back({tptr, *map});
+  return AXE_OK;
+}
+
 // Work the library does not launch itself (NCCL, memcpy) was enqueued on st:
 // the next libaxe kernel there must wait (full dependency).
 void stream_forget(cudaStream_t st) {
@@ -838,27 +871,18 @@ axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t 
       e = launch_k2(k, p.k2_vs, p.k2_vd, p.k2_gb, p.blocks, src, dst, st);
       break;
     }
+    case KK_TMA_TILE: {
+      std::array<uint64_t, 16> map;
+      AXE_TRY(tensor_map_for(p, src, &map));
+      K2TParams k = p.k2t;
+      k.dep = dep;
+      e = launch_k2t(map.data(), k, p.es, p.blocks, dst, st);
+      break;
+    }
     case KK_TMA: {
       const void *tptr = p.tma.mode == 0 ? src : (const void *)dst;
       std::array<uint64_t, 16> map;
-      bool hit = false;
-      {
-        std::lock_guard<std::mutex> lk(p.tm_cache->mu);
-        for (auto &m : p.tm_cache->maps)
-          if (m.first == tptr) {
-            map = m.second;
-            hit = true;
-            break;
-          }
-      }
-      if (!hit) {
-        int r = encode_tensor_map(map.data(), (uint8_t *)tptr + p.tm_base, p.tm_dims, p.tm_strides, p.tm_box,
-                                  p.tm_swizzle);
-        if (r != 0) AXE_FAIL(AXE_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", r);
-        std::lock_guard<std::mutex> lk(p.tm_cache->mu);
-        if (p.tm_cache->maps.size() >= 32) p.tm_cache->maps.erase(p.tm_cache->maps.begin());
-        p.tm_cache->maps.push_back({tptr, map});
-      }
+      AXE_TRY(tensor_map_for(p, tptr, &map));
       TmaParams k = p.tma;
       k.dep = dep;
       e = launch_tma(map.data(), k, p.blocks, src, dst, st);

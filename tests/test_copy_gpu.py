@@ -224,11 +224,12 @@ def test_transposes_all_kernels(axe, R, Cn, es):
                dst=layout([(R, 1), (Cn, R)]), dst_st=linear_storage(R * Cn), seed=R + es)
     for k in ("auto", "vector", "generic"):
         check(axe, cfg, k)
-    try:
-        axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], es, "tile")
-    except axe.AxeError:
-        return
-    check(axe, cfg, "tile")
+    for k in ("tile", "tma_tile"):
+        try:
+            axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], es, k)
+        except axe.AxeError:
+            continue
+        check(axe, cfg, k)
 
 
 def test_alias_and_alignment_errors(axe):
@@ -325,7 +326,7 @@ def test_random_permutes_reduce_to_numpy(axe, seed):
     dt = {1: np.uint8, 2: np.uint16, 4: np.uint32, 8: np.uint64}[es]
     v = synth.values(N, es, seed)
     expect = np.ascontiguousarray(v.view(dt).reshape(shape).transpose(perm)).reshape(-1)
-    for kernel in ("auto", "vector", "tile", "generic"):
+    for kernel in ("auto", "vector", "tile", "tma_tile", "generic"):
         try:
             plan = axe.CopyPlan(src, linear_storage(N), dst, linear_storage(N), es, kernel)
         except axe.AxeError:
