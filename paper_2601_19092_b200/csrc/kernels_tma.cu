@@ -222,7 +222,8 @@ __global__ void __launch_bounds__(K2T_THREADS) k2t_transpose(const __grid_consta
     for (uint32_t k = 0; k < pre; k++) issue(k);
   }
   const uint32_t W = p.W;
-  const uint32_t nvec = W * (p.H / VD);
+  const uint32_t QN = p.H / VD;  // destination vectors per column of a box
+  const uint32_t nvec = W * QN;
   for (uint32_t k = 0; k < mine; k++) {
     const int s = (int)(k % (uint32_t)S);
     mbar_wait(&full[s], (k / (uint32_t)S) & 1u);
@@ -231,16 +232,35 @@ __global__ void __launch_bounds__(K2T_THREADS) k2t_transpose(const __grid_consta
     decode(first + k * step, c5, db);
     const uint8_t *box = smem + (size_t)s * B;
     for (uint32_t v = t; v < nvec; v += K2T_THREADS) {
-      const uint32_t col = v % W, q = v / W;
+      // consecutive lanes take consecutive destination vectors of one column (coalesced stores);
+      // lane q reads its rows in an order rotated by q, so in every load instruction the lanes hit
+      // rows with different (r mod 8) -- different 16-byte chunks of the SWIZZLE_128B image
+      const uint32_t q = v % QN, col = v / QN;
       const uint32_t cb = col * ES;
-      uint4 out;
-      T *o = reinterpret_cast<T *>(&out);
+      const uint32_t rot = q % VD;
+      uint4 reg;
+      T *o = reinterpret_cast<T *>(&reg);
 #pragma unroll
       for (int i = 0; i < VD; i++) {
-        const uint32_t r = q * VD + i;
-        // SWIZZLE_128B image of row r: 16-byte chunk j stored at j ^ (r mod 8)
+        const uint32_t j = (i + rot) % VD;
+        const uint32_t r = q * VD + j;
         o[i] = *reinterpret_cast<const T *>(box + r * 128u + ((((cb >> 4) ^ (r & 7u)) << 4) | (cb & 15u)));
       }
+      // reg holds element (i + rot) at slot i: rotate the 16 bytes up by rot * ES bytes
+      const uint32_t b = rot * ES, kw = b >> 2, m = b & 3;
+      const uint32_t w[4] = {reg.x, reg.y, reg.z, reg.w};
+      uint32_t hi[4], lo[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        const uint32_t a = (uint32_t)(i - (int)kw) & 3u, c = (uint32_t)(i - (int)kw - 1) & 3u;
+        hi[i] = a == 0 ? w[0] : a == 1 ? w[1] : a == 2 ? w[2] : w[3];
+        lo[i] = c == 0 ? w[0] : c == 1 ? w[1] : c == 2 ? w[2] : w[3];
+      }
+      uint4 out;
+      out.x = __funnelshift_l(lo[0], hi[0], 8 * m);
+      out.y = __funnelshift_l(lo[1], hi[1], 8 * m);
+      out.z = __funnelshift_l(lo[2], hi[2], 8 * m);
+      out.w = __funnelshift_l(lo[3], hi[3], 8 * m);
       const int64_t d = db + (int64_t)col * p.dcol + (int64_t)q * 16;
       for (int rr = 0; rr < p.nrep; rr++) *reinterpret_cast<uint4 *>(dst + d + p.rep[rr]) = out;
     }
