@@ -744,14 +744,9 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
       P.kernel = KK_VECTOR;
       // narrower than 16-byte vectors on one side: stage through shared memory instead (K2)
       if (kernel == AXE_KERNEL_AUTO && P.vb < 16 && (P.vb <= 2 || P.k1_sector_eff < 0.5)) {
+        // (K2T, the TMA-staged variant, stays opt-in: measured slower than K2 on B200 in round 1)
         CopyPlan T = P;
         std::string w2;
-        if (build_k2t(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &T, &w2)) {
-          T.kernel = KK_TMA_TILE;
-          *out = std::move(T);
-          return AXE_OK;
-        }
-        T = P;
         if (build_k2(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &T, &w2)) {
           T.kernel = KK_TILE;
           *out = std::move(T);
