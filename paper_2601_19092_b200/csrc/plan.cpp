@@ -575,9 +575,10 @@ axe_status plan_chunks(const PlanRequest &rq, const std::vector<Joint> &J, const
     if (J[i].ss > 0 && J[i].ds > 0 && J[i].ss * J[i].e == sc && J[i].ds * J[i].e == dc && J[i].e > 1) best = (int)i;
   if (best < 0) return AXE_OK;
   const Joint cj = J[best];
-  // about 8 slabs of >= 1 MiB, each a whole number of swizzle blocks on both sides
+  // up to AXE_HOST_CHUNKS (16) slabs of >= 1 MiB, each a whole number of swizzle blocks on both sides
   int n = 1;
-  for (int c = 2; c <= 16; c++) {
+  const int64_t max_ch = env_int("AXE_HOST_CHUNKS", 16);
+  for (int c = 2; c <= 32; c++) {
     if (cj.e % c) continue;
     int64_t sb = sc / c * es, db = dc / c * es;
     if (sb < (1 << 20)) break;
@@ -585,7 +586,7 @@ axe_status plan_chunks(const PlanRequest &rq, const std::vector<Joint> &J, const
       return !st->swz_b || bytes % (int64_t(1) << (st->swz_b + st->swz_m + st->swz_s)) == 0;
     };
     if (whole(rq.sst, sb) && whole(rq.dstst, db) && sb % 16 == 0 && db % 16 == 0) n = c;
-    if (n >= 8) break;
+    if (n >= max_ch) break;
   }
   if (n < 2) return AXE_OK;
   std::vector<Iter> sD, dD;
