@@ -575,9 +575,9 @@ axe_status plan_chunks(const PlanRequest &rq, const std::vector<Joint> &J, const
     if (J[i].ss > 0 && J[i].ds > 0 && J[i].ss * J[i].e == sc && J[i].ds * J[i].e == dc && J[i].e > 1) best = (int)i;
   if (best < 0) return AXE_OK;
   const Joint cj = J[best];
-  // up to AXE_HOST_CHUNKS (16) slabs of >= 1 MiB, each a whole number of swizzle blocks on both sides
+  // up to AXE_HOST_CHUNKS (8, measured best of 4..32) slabs of >= 1 MiB, each a whole number of swizzle blocks on both sides
   int n = 1;
-  const int64_t max_ch = env_int("AXE_HOST_CHUNKS", 16);
+  const int64_t max_ch = env_int("AXE_HOST_CHUNKS", 8);
   for (int c = 2; c <= 32; c++) {
     if (cj.e % c) continue;
     int64_t sb = sc / c * es, db = dc / c * es;
