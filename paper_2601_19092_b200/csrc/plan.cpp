@@ -293,14 +293,12 @@ static bool build_k1(const std::vector<Joint> &J0, const Linear &ls, const Linea
   k.ssw = make_swz(sst);
   k.dsw = make_swz(dstst);
   P->covers_all = (int64_t)reps.size() * total * V == dstst.cells;
-  {
-    // sector efficiency of one CTA's worth of vectors (kernel order, dst-contiguous first): a
-    // schedule whose source reads scatter over many 32-byte sectors is better staged through smem
-    const int64_t nv = std::min<int64_t>(total, 1024);
+  // distinct 32-byte sectors (source, destination) touched by the first nv vectors of order D
+  auto sectors = [&](const std::vector<Joint> &order, int64_t nv) {
     std::set<int64_t> ssec, dsec;
     for (int64_t i = 0; i < nv; i++) {
       int64_t rem = i, so = 0, dof = 0;
-      for (auto &j : D) {
+      for (auto &j : order) {
         int64_t d = rem % j.e;
         rem /= j.e;
         so += d * j.ss;
@@ -309,8 +307,57 @@ static bool build_k1(const std::vector<Joint> &J0, const Linear &ls, const Linea
       for (int64_t b = so * es; b < so * es + (int64_t)(V * es); b += 32) ssec.insert(b >> 5);
       for (int64_t b = dof * es; b < dof * es + (int64_t)(V * es); b += 32) dsec.insert(b >> 5);
     }
+    return std::make_pair((int64_t)ssec.size(), (int64_t)dsec.size());
+  };
+  {
+    // sector efficiency of one CTA's worth of vectors (kernel order, dst-contiguous first): a
+    // schedule whose source reads scatter over many 32-byte sectors is better staged through smem
+    const int64_t nv = std::min<int64_t>(total, 1024);
+    auto sd = sectors(D, nv);
     const double useful = (double)nv * V * es;
-    P->k1_sector_eff = std::min(useful / (32.0 * ssec.size()), useful / (32.0 * dsec.size()));
+    P->k1_sector_eff = std::min(useful / (32.0 * sd.first), useful / (32.0 * sd.second));
+  }
+  if (env_int("AXE_K1_WARP_ORDER", 1) && total >= env_int("AXE_K1_WARP_VECTORS", 32)) {
+    // warp-level order: the 32 vectors one warp moves at once are chosen greedily, one prime
+    // factor of a digit at a time, to touch the fewest 32-byte sectors on both sides (ties keep
+    // the destination-contiguous order); the rest stays destination-stride sorted. Any order of
+    // the independent digits is the same copy, so this only changes the schedule.
+    const int64_t wv = env_int("AXE_K1_WARP_VECTORS", 32);
+    std::vector<Joint> rem = D, pre;
+    int64_t pv = 1;
+    while (pv < wv) {
+      int bi = -1;
+      int64_t bc = 0, bf = 0;
+      for (size_t i = 0; i < rem.size(); i++) {
+        int64_t e = rem[i].e, f = 2;
+        if (e <= 1) continue;
+        while (e % f) f++;
+        if (pv * f > wv) continue;
+        std::vector<Joint> t = pre;
+        t.push_back(Joint{f, rem[i].ss, rem[i].ds});
+        auto sd = sectors(t, pv * f);
+        int64_t c = sd.first + sd.second;
+        if (bi < 0 || c < bc) bi = (int)i, bc = c, bf = f;
+      }
+      if (bi < 0) break;
+      pre.push_back(Joint{bf, rem[bi].ss, rem[bi].ds});
+      rem[bi] = Joint{rem[bi].e / bf, rem[bi].ss * bf, rem[bi].ds * bf};
+      pv *= bf;
+    }
+    std::vector<Joint> nd;
+    for (auto &j : pre) nd.push_back(j);
+    for (auto &j : rem)
+      if (j.e > 1) nd.push_back(j);
+    // fuse neighbours that continue one another (inner-first)
+    std::vector<Joint> fz;
+    for (auto &j : nd) {
+      if (!fz.empty() && fz.back().ss * fz.back().e == j.ss && fz.back().ds * fz.back().e == j.ds)
+        fz.back().e *= j.e;
+      else
+        fz.push_back(j);
+    }
+    auto a = sectors(D, wv), b = sectors(fz, wv);
+    if (b.first + b.second < a.first + a.second) D = fz;
   }
   P->vb = (int)(V * es);
   P->align = std::max(P->vb, es);
