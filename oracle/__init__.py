@@ -36,7 +36,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread", "-Wall",
-                               "-o", tmp, _SRC])
+                               "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -86,6 +86,8 @@ def _L():
             lib.ora_redistribute.argtypes = [P(_Layout), P(_Storage), P(C.c_void_p), C.c_int64, P(_Layout),
                                              P(_Storage), P(C.c_void_p), C.c_int64, C.c_int, C.c_int, C.c_int,
                                              C.c_int]
+            lib.ora_reduce.argtypes = [P(_Layout), P(_Storage), P(C.c_void_p), C.c_int64, P(_Layout), P(_Storage),
+                                       P(C.c_void_p), C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int]
             _lib = lib
     return _lib
 
@@ -234,3 +236,27 @@ def scatter_ranks(L, st, values_bytes: np.ndarray, es: int, nranks: int, fill: n
     bufs = [fill.copy() for _ in range(nranks)]
     redistribute(ident, ident_st, [values_bytes] * nranks, L, st, bufs, es, -1, nthreads)
     return bufs
+
+
+# element types of the reduction (the oracle's own codes; ints add modulo 2^bits)
+DTYPES = {"f32": 1, "f64": 2, "f16": 3, "bf16": 4, "i32": 5, "i64": 6}
+DTYPE_SIZE = {"f32": 4, "f64": 8, "f16": 2, "bf16": 2, "i32": 4, "i64": 8}
+
+
+def reduce(src, src_st, sbufs, dst, dst_st, dbufs, dtype: str, nranks: int = 0, only_rank: int = -1,
+           nthreads: int = 1) -> None:
+    """dst(y) = sum_k src(k * E_D(dst) + y) (reading R24): fp64 sum in k order,
+    rounded once to dtype; ints modulo 2^bits.  nranks = 0: sbufs / dbufs are single arrays;
+    else per-rank lists selected by the gpuid coordinate (as redistribute)."""
+    k = _Keep()
+    if nranks == 0:
+        sbufs, dbufs = [sbufs], [dbufs]
+    n = len(sbufs)
+    sp = (C.c_void_p * n)(*[_ptr(b).value for b in sbufs])
+    dp = (C.c_void_p * n)(*[(_ptr(b).value if b is not None else None) for b in dbufs])
+    dbytes = next(b.nbytes for b in dbufs if b is not None)
+    st = _L().ora_reduce(C.byref(_mk_layout(src, k)), C.byref(_mk_storage(src_st, k)), sp, sbufs[0].nbytes,
+                         C.byref(_mk_layout(dst, k)), C.byref(_mk_storage(dst_st, k)), dp, dbytes, DTYPES[dtype],
+                         nranks, only_rank, nthreads)
+    if st:
+        raise OracleError(st, "reduce")

@@ -26,6 +26,8 @@
  *             the r = 0 source replica; P:122 replicas are copies)
  *   redistribute: as copy, the `gpuid` coordinate selecting the rank buffer
  *
+ *   reduce    dst(y) = sum_k src(k E_D(dst) + y), fp64 sum rounded once (reading R24,
+ *             P:399-403; see the reduction section at the end)
  *
  * Parity pins live in tests/test_oracle_pins.py (paper worked examples,
  * library special cases, invariants, TMA hardware for the swizzle).
@@ -454,6 +456,231 @@ int ora_redistribute(const ora_layout *src, const ora_storage *sst, const uint8_
   J.sbytes = sbytes; J.dbytes = dbytes; J.es = es;
   J.nranks = nranks; J.only_rank = only_rank; J.seen = seen; J.cells = cells;
   st = run_all(&J, ED, nthreads);
+  free(seen);
+  return st;
+}
+
+/* ---- reduction: SURVEY §8(f) f3 ----------------------------------------------
+ * P:399-403 (the DTensor reduce-scatter signature: an input of shape (4,64,64)
+ * "sums over 0", producing a (64,64) output) and P:628 ("invokes the sum
+ * operator").  Reading R24 of DESIGN.md: the leading logical dimension of the
+ * source is summed away,
+ *
+ *   K = E_D(src) / E_D(dst),   dst(y) = sum_{k=0}^{K-1} src(k * E_D(dst) + y),
+ *
+ * the source element read for x being the representative f_D(x) + O (R4) and
+ * the sum written to every cell of f_L^dst(y).  Floating point summands are
+ * added in fp64 in k order and the sum is rounded ONCE to the element type
+ * (round to nearest, ties to even); integers add modulo 2^bits.
+ * --------------------------------------------------------------------------- */
+#include <math.h>
+
+#define ORA_DT_F32 1
+#define ORA_DT_F64 2
+#define ORA_DT_F16 3
+#define ORA_DT_BF16 4
+#define ORA_DT_I32 5
+#define ORA_DT_I64 6
+
+static int dt_size(int dt) {
+  switch (dt) {
+    case ORA_DT_F32: case ORA_DT_I32: return 4;
+    case ORA_DT_F64: case ORA_DT_I64: return 8;
+    case ORA_DT_F16: case ORA_DT_BF16: return 2;
+  }
+  return 0;
+}
+
+/* IEEE-754 binary16: 1 sign, 5 exponent (bias 15), 10 fraction bits */
+static double f16_value(uint16_t h) {
+  int s = h >> 15, e = (h >> 10) & 31, f = h & 1023;
+  double v;
+  if (e == 0) v = ldexp((double)f, -24);
+  else if (e == 31) v = f ? NAN : INFINITY;
+  else v = ldexp((double)(1024 + f), e - 25);
+  return s ? -v : v;
+}
+
+/* bfloat16: the upper half of an IEEE-754 binary32 */
+static double bf16_value(uint16_t h) {
+  uint32_t w = (uint32_t)h << 16;
+  float f;
+  memcpy(&f, &w, 4);
+  return (double)f;
+}
+
+/* v rounded to p significant bits (ties to even), exponents below emin kept at
+ * emin (gradual underflow); magnitudes above max_finite become infinite. */
+static double round_sig(double v, int p, int emin, double max_finite) {
+  if (v == 0 || isnan(v) || isinf(v)) return v;
+  int e;
+  frexp(v, &e); /* |v| = m 2^e, 1/2 <= m < 1: leading bit weight 2^(e-1) */
+  int lead = e - 1 < emin ? emin : e - 1;
+  int q = lead - (p - 1); /* weight of the last kept bit */
+  double r = ldexp(nearbyint(ldexp(v, -q)), q);
+  if (fabs(r) > max_finite) r = r > 0 ? INFINITY : -INFINITY;
+  return r;
+}
+
+static void put_f16(uint8_t *p, double v) {
+  uint16_t h;
+  double r = round_sig(v, 11, -14, 65504.0);
+  if (isnan(r)) h = 0x7e00;
+  else {
+    uint16_t s = signbit(r) ? 0x8000 : 0;
+    double a = fabs(r);
+    if (isinf(a)) h = s | 0x7c00;
+    else if (a < ldexp(1.0, -14)) h = s | (uint16_t)ldexp(a, 24); /* subnormal: a = f 2^-24 */
+    else {
+      int e;
+      double m = frexp(a, &e); /* a = (2m) 2^(e-1), 1 <= 2m < 2 */
+      h = s | (uint16_t)((e - 1 + 15) << 10) | (uint16_t)ldexp(2 * m - 1, 10);
+    }
+  }
+  memcpy(p, &h, 2);
+}
+
+static void put_bf16(uint8_t *p, double v) {
+  uint16_t h;
+  double r = round_sig(v, 8, -126, ldexp(255.0, 120)); /* max (2 - 2^-7) 2^127 */
+  if (isnan(r)) h = 0x7fc0;
+  else {
+    float f = (float)r; /* exact: r has <= 8 significant bits */
+    uint32_t w;
+    memcpy(&w, &f, 4);
+    h = (uint16_t)(w >> 16);
+  }
+  memcpy(p, &h, 2);
+}
+
+typedef struct {
+  const ora_layout *src, *dst;
+  const ora_storage *sst, *dstst;
+  const uint8_t *const *sbufs;
+  uint8_t *const *dbufs;
+  int64_t sbytes, dbytes, K, Y;
+  int dt, nranks, only_rank;
+  uint64_t *seen;
+  int64_t cells;
+  int64_t y0, y1;
+  int status;
+} rjob_t;
+
+static void *run_reduce_job(void *arg) {
+  rjob_t *J = (rjob_t *)arg;
+  const char *dev = J->nranks > 0 ? "gpuid" : NULL;
+  const int es = dt_size(J->dt);
+  int64_t ED, ER;
+  check_layout(J->dst, &ED, &ER);
+  int64_t *done = (int64_t *)malloc(sizeof(int64_t) * (size_t)ER * 2);
+  if (!done) { J->status = ORA_ENOMEM; return NULL; }
+  for (int64_t y = J->y0; y < J->y1 && J->status == ORA_OK; y++) {
+    double fsum = 0;
+    uint64_t isum = 0;
+    for (int64_t k = 0; k < J->K; k++) {
+      coord_t c;
+      fD_plus_O(J->src, k * J->Y + y, &c); /* source representative (R4) */
+      int g = 0;
+      if (dev) {
+        int64_t gv = coord_get(&c, dev);
+        if (gv < 0 || gv >= J->nranks) { J->status = ORA_EBOUNDS; break; }
+        g = (int)gv;
+      }
+      int64_t si = storage_index(J->sst, &c, dev);
+      if (si < 0) { J->status = ORA_EBOUNDS; break; }
+      int64_t sb = swizzle_byte(J->sst, si * es);
+      if (sb + es > J->sbytes) { J->status = ORA_EBOUNDS; break; }
+      const uint8_t *p = J->sbufs[g] + sb;
+      switch (J->dt) {
+        case ORA_DT_F32: { float f; memcpy(&f, p, 4); fsum += (double)f; break; }
+        case ORA_DT_F64: { double f; memcpy(&f, p, 8); fsum += f; break; }
+        case ORA_DT_F16: { uint16_t h; memcpy(&h, p, 2); fsum += f16_value(h); break; }
+        case ORA_DT_BF16: { uint16_t h; memcpy(&h, p, 2); fsum += bf16_value(h); break; }
+        case ORA_DT_I32: { uint32_t w; memcpy(&w, p, 4); isum += w; break; }
+        case ORA_DT_I64: { uint64_t w; memcpy(&w, p, 8); isum += w; break; }
+      }
+    }
+    if (J->status) break;
+    uint8_t v[8];
+    switch (J->dt) {
+      case ORA_DT_F32: { float f = (float)fsum; memcpy(v, &f, 4); break; } /* C cast: nearest even */
+      case ORA_DT_F64: memcpy(v, &fsum, 8); break;
+      case ORA_DT_F16: put_f16(v, fsum); break;
+      case ORA_DT_BF16: put_bf16(v, fsum); break;
+      case ORA_DT_I32: { uint32_t w = (uint32_t)isum; memcpy(v, &w, 4); break; }
+      case ORA_DT_I64: memcpy(v, &isum, 8); break;
+    }
+    int64_t ndone = 0;
+    for (int64_t r = 0; r < ER; r++) {
+      coord_t c;
+      fL(J->dst, y, r, &c);
+      int gd = 0;
+      if (dev) {
+        int64_t gv = coord_get(&c, dev);
+        if (gv < 0 || gv >= J->nranks) { J->status = ORA_EBOUNDS; break; }
+        gd = (int)gv;
+      }
+      int64_t di = storage_index(J->dstst, &c, dev);
+      if (di < 0) { J->status = ORA_EBOUNDS; break; }
+      int64_t db = swizzle_byte(J->dstst, di * es);
+      if (db + es > J->dbytes) { J->status = ORA_EBOUNDS; break; }
+      int dup = 0;
+      for (int64_t q = 0; q < ndone; q++)
+        if (done[2 * q] == gd && done[2 * q + 1] == di) dup = 1;
+      if (dup) continue;
+      done[2 * ndone] = gd;
+      done[2 * ndone + 1] = di;
+      ndone++;
+      if (test_and_set(J->seen, (int64_t)gd * J->cells + di)) { J->status = ORA_ECOLLIDE; break; }
+      if (J->only_rank < 0 || J->only_rank == gd) memcpy(J->dbufs[gd] + db, v, (size_t)es);
+    }
+  }
+  free(done);
+  return NULL;
+}
+
+/*
+ * ora_reduce: dst(y) = sum_k src(k * E_D(dst) + y) (reading R24).  nranks = 0: one
+ * buffer per side (no device axis); nranks > 0: the `gpuid` coordinate selects
+ * sbufs[g] / dbufs[g'] as in ora_redistribute (only_rank as there).
+ */
+int ora_reduce(const ora_layout *src, const ora_storage *sst, const uint8_t *const *sbufs, int64_t sbytes,
+               const ora_layout *dst, const ora_storage *dstst, uint8_t *const *dbufs, int64_t dbytes, int dt,
+               int nranks, int only_rank, int nthreads) {
+  int64_t eds, ers, edd, erd;
+  int st;
+  if ((st = check_layout(src, &eds, &ers))) return st;
+  if ((st = check_layout(dst, &edd, &erd))) return st;
+  if ((st = ora_storage_check(sst))) return st;
+  if ((st = ora_storage_check(dstst))) return st;
+  if (!dt_size(dt) || nranks < 0) return ORA_EINVAL;
+  if (eds % edd) return ORA_ESIZE;
+  int64_t cells = ora_storage_cells(dstst);
+  int nr = nranks > 0 ? nranks : 1;
+  uint64_t *seen = (uint64_t *)calloc((size_t)((cells * nr) / 64 + 1), sizeof(uint64_t));
+  if (!seen) return ORA_ENOMEM;
+  if (nthreads < 1) nthreads = 1;
+  if ((int64_t)nthreads > edd) nthreads = (int)edd;
+  rjob_t *jobs = (rjob_t *)calloc((size_t)nthreads, sizeof(rjob_t));
+  pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+  if (!jobs || !th) { free(jobs); free(th); free(seen); return ORA_ENOMEM; }
+  for (int t = 0; t < nthreads; t++) {
+    rjob_t *J = &jobs[t];
+    J->src = src; J->dst = dst; J->sst = sst; J->dstst = dstst;
+    J->sbufs = sbufs; J->dbufs = dbufs; J->sbytes = sbytes; J->dbytes = dbytes;
+    J->K = eds / edd; J->Y = edd; J->dt = dt; J->nranks = nranks; J->only_rank = only_rank;
+    J->seen = seen; J->cells = cells;
+    J->y0 = edd * t / nthreads;
+    J->y1 = edd * (t + 1) / nthreads;
+  }
+  for (int t = 1; t < nthreads; t++) pthread_create(&th[t], NULL, run_reduce_job, &jobs[t]);
+  run_reduce_job(&jobs[0]);
+  for (int t = 1; t < nthreads; t++) pthread_join(th[t], NULL);
+  st = ORA_OK;
+  for (int t = 0; t < nthreads; t++)
+    if (jobs[t].status && !st) st = jobs[t].status;
+  free(jobs);
+  free(th);
   free(seen);
   return st;
 }

@@ -174,3 +174,68 @@ def config5(rows: int = 32768, cols: int = 8192, A: int = 2, B: int = 4):
     dst = layout([(rows, cols // B), (B, 1, "gpuid"), (cols // B, 1)], [(A, B, "gpuid")])
     return dict(name="config5", es=2, nranks=A * B, src=src, src_st=linear_storage(rows // A * cols),
                 dst=dst, dst_st=linear_storage(rows * cols // B), seed=SEED_BASE + 5)
+
+
+# ----------------------------------------------------------------------------
+# Reduction rows.  Summands are finite numbers
+# whose bit patterns are assembled directly from the splitmix64 draws (no
+# rounding, no arithmetic of the method).
+# ----------------------------------------------------------------------------
+
+# name -> (sign bit, exponent shift, exponent bias, fraction bits, storage dtype)
+_FLOAT_FORMATS = {
+    "f16": (15, 10, 15, 10, np.uint16),
+    "bf16": (15, 7, 127, 7, np.uint16),
+    "f32": (31, 23, 127, 23, np.uint32),
+    "f64": (63, 52, 1023, 52, np.uint64),
+}
+DTYPE_SIZE = {"f16": 2, "bf16": 2, "f32": 4, "f64": 8, "i32": 4, "i64": 8}
+
+
+def numbers(n: int, dtype: str, seed: int) -> np.ndarray:
+    """n summands of `dtype` as raw bytes.  Floats: random sign, |v| in [2^-8, 1) (exponent
+    bias-8 .. bias-1 from draw bits 56-58, fraction from the low draw bits).  Integers: the
+    raw draws (sums wrap modulo 2^bits)."""
+    with np.errstate(over="ignore"):
+        h = _splitmix64(np.uint64(seed) ^ (np.arange(n, dtype=np.uint64) * GOLDEN))
+    if dtype == "i32":
+        return h.astype(np.uint32).view(np.uint8)
+    if dtype == "i64":
+        return h.view(np.uint8)
+    sbit, eshift, bias, fbits, st = _FLOAT_FORMATS[dtype]
+    sign = (h >> np.uint64(63)) << np.uint64(sbit)
+    expo = (np.uint64(bias - 8) + ((h >> np.uint64(56)) & np.uint64(7))) << np.uint64(eshift)
+    frac = h & np.uint64((1 << fbits) - 1)
+    return (sign | expo | frac).astype(st).view(np.uint8)
+
+
+def reduce_local(K: int = 8, rows: int = 8192, cols: int = 4096, dtype: str = "bf16", tiled: bool = False):
+    """One-GPU sum over the leading dimension: (K, rows, cols) row-major -> (rows, cols), row-major
+    or (tiled) 64x64 tiles with SW128 (the reduction fused with the re-tiling of config 2)."""
+    src = layout([(K, rows * cols), (rows, cols), (cols, 1)])
+    if tiled:
+        t = 64
+        dst = layout([(rows // t, t * cols), (t, t), (cols // t, t * t), (t, 1)])
+        dst_st = linear_storage(rows * cols, SW128)
+    else:
+        dst = layout([(rows, cols), (cols, 1)])
+        dst_st = linear_storage(rows * cols)
+    return dict(name="reduce_local" + ("_tiled" if tiled else ""), dtype=dtype, K=K, src=src,
+                src_st=linear_storage(K * rows * cols), dst=dst, dst_st=dst_st, seed=SEED_BASE + 6)
+
+
+def reduce_scatter(P: int, rows: int = 64, cols: int = 64, dtype: str = "bf16"):
+    """The DTensor reduce-scatter of P:399-403: a (P, rows, cols) tensor whose dim 0 is sharded over
+    P devices (each holds one partial), summed over dim 0 into (rows, cols) sharded by rows."""
+    src = layout([(P, 1, "gpuid"), (rows, cols), (cols, 1)])
+    dst = layout([(P, 1, "gpuid"), (rows // P, cols), (cols, 1)])
+    return dict(name="reduce_scatter", dtype=dtype, nranks=P, src=src, src_st=linear_storage(rows * cols),
+                dst=dst, dst_st=linear_storage(rows // P * cols), seed=SEED_BASE + 7)
+
+
+def all_reduce(P: int, rows: int = 64, cols: int = 64, dtype: str = "bf16"):
+    """Partial -> Replicate: every device ends with the full sum."""
+    src = layout([(P, 1, "gpuid"), (rows, cols), (cols, 1)])
+    dst = layout([(rows, cols), (cols, 1)], [(P, 1, "gpuid")])
+    return dict(name="all_reduce", dtype=dtype, nranks=P, src=src, src_st=linear_storage(rows * cols),
+                dst=dst, dst_st=linear_storage(rows * cols), seed=SEED_BASE + 8)
