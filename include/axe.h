@@ -281,6 +281,66 @@ axe_status axe_redist_emulate(const axe_redist_plan *const *plans, int nranks, c
                               void *const *dst_locals, void *cuda_stream);
 
 /* ------------------------------------------------------------------------- */
+/* Reduction over the leading logical dimension              */
+/* ------------------------------------------------------------------------- */
+/* a reduce-scatter "accepts a DTensor with shape (4, 64, 64) that
+ * shards over the first dimension, and sums over 0, generating an output
+ * DTensor with shape (64, 64)"; "invokes the sum operator".  Reading R24
+ * (DESIGN.md): with K = E_D(src) / E_D(dst) (an integer, else
+ * AXE_ERR_SIZE_MISMATCH),
+ *     dst(y) = sum_{k=0}^{K-1} src(k * E_D(dst) + y)   for every y in [0, E_D(dst)),
+ * the source element of x read at its representative f_D(x) + O (R4) and the
+ * sum written to every cell of f_L^dst(y); other dst cells are untouched.
+ * Floating point: summed in fp32 (fp64 for AXE_DTYPE_F64) in k order and
+ * rounded once to the element type (round to nearest even); integers add
+ * modulo 2^bits.  Elements are dtype-sized; storages as for copies. */
+enum {
+  AXE_DTYPE_F32 = 1,
+  AXE_DTYPE_F64 = 2,
+  AXE_DTYPE_F16 = 3,
+  AXE_DTYPE_BF16 = 4,
+  AXE_DTYPE_I32 = 5,
+  AXE_DTYPE_I64 = 6
+};
+
+typedef struct axe_reduce_plan axe_reduce_plan;
+
+/* Plan a one-device reduction (host only).  Errors: AXE_ERR_INVALID_ARG (unknown
+ * dtype), AXE_ERR_SIZE_MISMATCH, AXE_ERR_BOUNDS, AXE_ERR_NONINJECTIVE,
+ * AXE_ERR_UNSUPPORTED_AXIS (gpuid: use axe_redist_reduce_plan_create). */
+axe_status axe_reduce_plan_create(const axe_layout *src, const axe_storage *src_st, const axe_layout *dst,
+                                  const axe_storage *dst_st, int dtype, axe_reduce_plan **out);
+/* Launch on cuda_stream (asynchronous, 1 kernel).  src_ptr / dst_ptr: DEVICE
+ * buffers of the storage sizes, owned by the caller, not overlapping
+ * (AXE_ERR_ALIAS); aligned to the plan's vector width (AXE_ERR_ALIGNMENT). */
+axe_status axe_reduce_plan_execute(const axe_reduce_plan *plan, const void *src_ptr, void *dst_ptr, void *cuda_stream);
+axe_status axe_reduce_plan_sizes(const axe_reduce_plan *plan, int64_t *src_bytes, int64_t *dst_bytes);
+/* JSON: kernel (reduce | reduce_generic), K, vector bytes, output / reduction digits. */
+axe_status axe_reduce_plan_describe(const axe_reduce_plan *plan, char *buf, int capacity);
+void axe_reduce_plan_destroy(axe_reduce_plan *plan);
+/* One-shot form through an internal plan cache. */
+axe_status axe_reduce(const axe_layout *src, const axe_storage *src_st, const void *src_ptr, const axe_layout *dst,
+                      const axe_storage *dst_st, void *dst_ptr, int dtype, void *cuda_stream);
+
+/* Distributed form (Partial -> Shard = reduce-scatter, Partial -> Replicate =
+ * all-reduce): the layouts name "gpuid" as for axe_redist_plan_create, and the
+ * source's summed dimension is typically sharded over gpuid (one partial per
+ * rank).  Executed as an exchange of the partials into a library-owned stage
+ * buffer (K slabs shaped like this rank's dst storage; pack / NCCL / unpack as
+ * axe_redist_plan_execute) followed by one K4 sum of the slabs into dst_local.
+ * Every rank's destination image must be its whole dst storage
+ * (AXE_ERR_UNSUPPORTED otherwise).  The returned plan is used with
+ * axe_redist_plan_execute / _describe / _counts / _map (stage element indices)
+ * / _destroy and axe_redist_emulate; not with _execute_peers. */
+axe_status axe_redist_reduce_plan_create(const axe_layout *src, const axe_storage *src_st, const axe_layout *dst,
+                                         const axe_storage *dst_st, int dtype, int nranks, int rank,
+                                         axe_redist_plan **out);
+/* One-shot collective form (plans through an internal cache). */
+axe_status axe_redistribute_reduce(const axe_layout *src, const axe_storage *src_st, const void *src_local,
+                                   const axe_layout *dst, const axe_storage *dst_st, void *dst_local, int dtype,
+                                   axe_comm *comm, void *cuda_stream);
+
+/* ------------------------------------------------------------------------- */
 const char *axe_last_error(void);
 /* Number of kernels this library has launched in this process (all threads). */
 int64_t axe_kernel_launch_count(void);

@@ -93,6 +93,17 @@ _SIGS = {
     "axe_redistribute": ([_vp, C.POINTER(axe_storage), _vp, _vp, C.POINTER(axe_storage), _vp, C.c_int, _vp, _vp],
                          C.c_int),
     "axe_redist_emulate": ([C.POINTER(_vp), C.c_int, C.POINTER(_vp), C.POINTER(_vp), _vp], C.c_int),
+    "axe_reduce_plan_create": ([_vp, C.POINTER(axe_storage), _vp, C.POINTER(axe_storage), C.c_int, C.POINTER(_vp)],
+                               C.c_int),
+    "axe_reduce_plan_execute": ([_vp, _vp, _vp, _vp], C.c_int),
+    "axe_reduce_plan_sizes": ([_vp, _pi64, _pi64], C.c_int),
+    "axe_reduce_plan_describe": ([_vp, C.c_char_p, C.c_int], C.c_int),
+    "axe_reduce_plan_destroy": ([_vp], None),
+    "axe_reduce": ([_vp, C.POINTER(axe_storage), _vp, _vp, C.POINTER(axe_storage), _vp, C.c_int, _vp], C.c_int),
+    "axe_redist_reduce_plan_create": ([_vp, C.POINTER(axe_storage), _vp, C.POINTER(axe_storage), C.c_int, C.c_int,
+                                       C.c_int, C.POINTER(_vp)], C.c_int),
+    "axe_redistribute_reduce": ([_vp, C.POINTER(axe_storage), _vp, _vp, C.POINTER(axe_storage), _vp, C.c_int, _vp,
+                                 _vp], C.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -396,15 +407,23 @@ class Comm:
 
 
 class RedistPlan:
-    """axe_redist_plan_create / _execute / _describe / _counts / _map (include/axe.h)."""
+    """axe_redist_plan_create / _execute / _describe / _counts / _map (include/axe.h).
+    With reduce_dtype set: axe_redist_reduce_plan_create (the source's leading logical dimension
+    is summed away; elem_size is then the dtype's size)."""
 
-    def __init__(self, src, src_st, dst, dst_st, elem_size: int, nranks: int, rank: int):
+    def __init__(self, src, src_st, dst, dst_st, elem_size: int, nranks: int, rank: int, reduce_dtype=None):
         self.src, self.dst = Layout.of(src), Layout.of(dst)
         ss, k1 = make_storage(src_st)
         ds, k2 = make_storage(dst_st)
         h = C.c_void_p()
-        _check(_lib.axe_redist_plan_create(self.src.handle, C.byref(ss), self.dst.handle, C.byref(ds), elem_size,
-                                           nranks, rank, C.byref(h)), "axe_redist_plan_create")
+        if reduce_dtype is None:
+            _check(_lib.axe_redist_plan_create(self.src.handle, C.byref(ss), self.dst.handle, C.byref(ds), elem_size,
+                                               nranks, rank, C.byref(h)), "axe_redist_plan_create")
+        else:
+            _check(_lib.axe_redist_reduce_plan_create(self.src.handle, C.byref(ss), self.dst.handle, C.byref(ds),
+                                                      DTYPES[reduce_dtype], nranks, rank, C.byref(h)),
+                   "axe_redist_reduce_plan_create")
+            elem_size = DTYPE_SIZE[reduce_dtype]
         self._h, self.nranks, self.rank, self.elem_size = h, nranks, rank, elem_size
 
     def __del__(self):
@@ -449,6 +468,61 @@ def axe_redistribute(src, src_st, src_local, dst, dst_st, dst_local, elem_size: 
     ds, k2 = make_storage(dst_st)
     _check(_lib.axe_redistribute(s.handle, C.byref(ss), _ptr(src_local), d.handle, C.byref(ds), _ptr(dst_local),
                                  elem_size, comm.handle, _stream(stream)), "axe_redistribute")
+
+
+# --------------------------------------------------------------------------- reduction (§8(f) f3)
+DTYPES = {"f32": 1, "f64": 2, "f16": 3, "bf16": 4, "i32": 5, "i64": 6}
+DTYPE_SIZE = {"f32": 4, "f64": 8, "f16": 2, "bf16": 2, "i32": 4, "i64": 8}
+
+
+class ReducePlan:
+    """axe_reduce_plan_create / _execute / _sizes / _describe: dst(y) = sum_k src(k * E_D(dst) + y)."""
+
+    def __init__(self, src, src_st, dst, dst_st, dtype: str):
+        self.src, self.dst = Layout.of(src), Layout.of(dst)
+        ss, k1 = make_storage(src_st)
+        ds, k2 = make_storage(dst_st)
+        h = C.c_void_p()
+        _check(_lib.axe_reduce_plan_create(self.src.handle, C.byref(ss), self.dst.handle, C.byref(ds), DTYPES[dtype],
+                                           C.byref(h)), "axe_reduce_plan_create")
+        self._h, self.dtype = h, dtype
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.axe_reduce_plan_destroy(h)
+            self._h = None
+
+    def execute(self, src, dst, stream=None):
+        _check(_lib.axe_reduce_plan_execute(self._h, _ptr(src), _ptr(dst), _stream(stream)), "axe_reduce_plan_execute")
+
+    def sizes(self):
+        a, b = C.c_int64(), C.c_int64()
+        _check(_lib.axe_reduce_plan_sizes(self._h, C.byref(a), C.byref(b)), "axe_reduce_plan_sizes")
+        return a.value, b.value
+
+    def describe(self) -> dict:
+        buf = C.create_string_buffer(1 << 14)
+        _check(_lib.axe_reduce_plan_describe(self._h, buf, len(buf)), "axe_reduce_plan_describe")
+        return json.loads(buf.value.decode())
+
+
+def axe_reduce(src, src_st, src_buf, dst, dst_st, dst_buf, dtype: str, stream=None):
+    """One-shot stream-ordered reduction over the leading logical dimension (include/axe.h axe_reduce)."""
+    s, d = Layout.of(src), Layout.of(dst)
+    ss, k1 = make_storage(src_st)
+    ds, k2 = make_storage(dst_st)
+    _check(_lib.axe_reduce(s.handle, C.byref(ss), _ptr(src_buf), d.handle, C.byref(ds), _ptr(dst_buf), DTYPES[dtype],
+                           _stream(stream)), "axe_reduce")
+
+
+def axe_redistribute_reduce(src, src_st, src_local, dst, dst_st, dst_local, dtype: str, comm: Comm, stream=None):
+    s, d = Layout.of(src), Layout.of(dst)
+    ss, k1 = make_storage(src_st)
+    ds, k2 = make_storage(dst_st)
+    _check(_lib.axe_redistribute_reduce(s.handle, C.byref(ss), _ptr(src_local), d.handle, C.byref(ds),
+                                        _ptr(dst_local), DTYPES[dtype], comm.handle, _stream(stream)),
+           "axe_redistribute_reduce")
 
 
 def redist_emulate(plans, src_locals, dst_locals, stream=None):

@@ -180,4 +180,33 @@ struct K3Params {
   int dep;
 };
 
+// ------------------------------------------------------- K4 reduce (§8(f) f3)
+// dst(y) = sum_k src(k * E_D(dst) + y) (reading R24).  Element types:
+enum DType { DT_F32 = 1, DT_F64 = 2, DT_F16 = 3, DT_BF16 = 4, DT_I32 = 5, DT_I64 = 6 };
+constexpr int K4_MAXD = 12;
+constexpr int K4_MAXK = 256;  // summand offsets kept as a table up to this K
+struct K4Params {
+  uint32_t total;                      // output vectors
+  int nd;                              // output digits, outermost first
+  FastDiv fd[K4_MAXD];
+  int64_t ss[K4_MAXD], ds[K4_MAXD];    // byte strides (source, destination)
+  int nk;                              // > 0: koff[0..nk) are the summands' byte offsets, k ascending
+  int64_t koff[K4_MAXK];
+  uint32_t ktotal;                     // nk == 0: decode k over the reduction digits
+  int nkd;
+  FastDiv kfd[K4_MAXD];
+  int64_t kss[K4_MAXD];
+  int64_t sbase, dbase;
+  int nrep;
+  int64_t rep[K1_MAXREP];
+  Swz ssw, dsw;
+  int dep;
+};
+// generic form: both layouts evaluated per element (K0 sides; the source side spans K * Y)
+struct K4GParams {
+  K0Side src, dst;
+  int64_t Y, K, ER;
+  int dep;
+};
+
 }  // namespace axe

@@ -137,7 +137,7 @@ Swz make_swz(const Storage &st) {
   return s;
 }
 
-static axe_status build_k0_side(const Layout &L, const Storage &st, int skip_axis, K0Side *S) {
+axe_status build_k0_side(const Layout &L, const Storage &st, int skip_axis, K0Side *S) {
   memset(S, 0, sizeof(*S));
   std::vector<int> ax;
   for (int a : L.axes)

@@ -118,5 +118,27 @@ int64_t kernel_launches();
 // 1 if a kernel reading [s0,s1) and writing [d0,d1) on stream st must wait for
 // the previous libaxe kernel on st (records the new kernel as the previous one).
 int stream_dependency(cudaStream_t st, uintptr_t s0, uintptr_t s1, uintptr_t d0, uintptr_t d1);
+axe_status build_k0_side(const Layout &L, const Storage &st, int skip_axis, K0Side *S);
+Swz make_swz(const Storage &st);
+
+// ---- K4 reduction over the leading logical dimension (plan_reduce.cpp, kernels_reduce.cu)
+struct ReducePlan {
+  int kind = 0;          // 1: generic (k4_generic), 2: vector (k4_reduce)
+  int dtype = 0, es = 0;
+  int64_t K = 1;         // summands per output element
+  int64_t src_bytes = 0, dst_bytes = 0;
+  int align = 1, vb = 0;
+  unsigned blocks = 1;
+  K4Params k4;
+  K4GParams k4g;
+  std::string desc;
+};
+int dtype_size(int dtype);
+axe_status plan_reduce(const Layout &src, const Storage &sst, const Layout &dst, const Storage &dstst, int dtype,
+                       int max_align, ReducePlan *out);
+axe_status run_reduce(const ReducePlan &p, const void *src, void *dst, cudaStream_t st);
+cudaError_t launch_k4(const K4Params &p, int dtype, int vb, unsigned blocks, const void *src, void *dst,
+                      cudaStream_t st);
+cudaError_t launch_k4g(const K4GParams &p, int dtype, const void *src, void *dst, cudaStream_t st);
 
 }  // namespace axe

@@ -65,9 +65,15 @@ struct axe_redist_plan {
   bool allgather = false;
   int64_t ag_src = 0, ag_dst = 0;  // element offsets of the all-gather
   std::string desc;
+  int64_t dst_rep = 1;             // destination memory replicas per element (distinct cells)
+  // reduction (axe_redist_reduce_plan_create): `inner` moves the partials into the stage
+  // buffer (K slabs shaped like this rank's dst storage), `red` sums the slabs into dst_local
+  std::shared_ptr<axe_redist_plan> inner;
+  ReducePlan red;
+  int64_t stage_bytes = 0;
   // scratch owned by the plan (allocated on first execute, on the current device)
   mutable std::mutex mu;
-  mutable void *send_buf = nullptr, *recv_buf = nullptr;
+  mutable void *send_buf = nullptr, *recv_buf = nullptr, *stage = nullptr;
   mutable cudaStream_t side = nullptr;
   mutable cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
   mutable cudaStream_t pk = nullptr, up = nullptr;  // pack / unpack streams
@@ -75,6 +81,7 @@ struct axe_redist_plan {
   ~axe_redist_plan() {
     if (send_buf) cudaFree(send_buf);
     if (recv_buf) cudaFree(recv_buf);
+    if (stage) cudaFree(stage);
     for (cudaStream_t x : {side, pk, up})
       if (x) cudaStreamDestroy(x);
     for (cudaEvent_t x : {ev_fork, ev_join, ev_join2})
@@ -245,6 +252,7 @@ static axe_status plan_redist(const Layout &S, const Storage &sst, const Layout 
   P->nranks = nranks;
   P->rank = rank;
   P->es = es;
+  for (auto &r : dst_mem_R) P->dst_rep *= r.e;
   P->src_cells = sst.cells;
   P->dst_cells = dstst.cells;
   // contiguity of a block on each side in packed order
@@ -369,6 +377,68 @@ static axe_status plan_redist(const Layout &S, const Storage &sst, const Layout 
   return AXE_OK;
 }
 
+// Reduce-redistribute (reading R24): dst(y) = sum_k src(k E_D(dst) + y).
+// Phase 1 redistributes the source (its K partials) into a stage layout -- the destination
+// layout with the summed dimension prepended on a private storage axis, so rank g's stage
+// buffer holds K slabs shaped exactly like its dst storage.  Phase 2 sums the slabs cell by
+// cell in k order (K4).  A swizzle permutes every slab identically (the slab is a whole number
+// of swizzle blocks), so phase 2 is a flat elementwise sum.  Every rank's destination image
+// must be its whole dst storage (checked), or phase 2 would write cells outside the image.
+static axe_status plan_redist_reduce(const Layout &S, const Storage &sst, const Layout &T, const Storage &dstst,
+                                     int dtype, int nranks, int rank, axe_redist_plan *P) {
+  const int es = dtype_size(dtype);
+  if (!es) AXE_FAIL(AXE_ERR_INVALID_ARG, "unknown dtype %d", dtype);
+  if (S.ED % T.ED)
+    AXE_FAIL(AXE_ERR_SIZE_MISMATCH, "E_D(src) = %lld is not a multiple of E_D(dst) = %lld", (long long)S.ED,
+             (long long)T.ED);
+  const int64_t K = S.ED / T.ED;
+  const int ak = intern_axis("axe_reduce_k");
+  if (T.names_axis(ak) || S.names_axis(ak)) AXE_FAIL(AXE_ERR_INVALID_ARG, "axis name axe_reduce_k is reserved");
+  if (dstst.swz_b > 0 && (dstst.cells * es) % (int64_t(1) << (dstst.swz_b + dstst.swz_m + dstst.swz_s)))
+    AXE_FAIL(AXE_ERR_BOUNDS, "swizzled destination storage is not a whole number of swizzle blocks");
+  Layout T2;
+  std::vector<Iter> d2 = T.D;
+  d2.insert(d2.begin(), Iter{K, 1, ak});
+  AXE_TRY(make_layout(d2, T.R, T.O, &T2));
+  Storage st2 = dstst;
+  st2.d.insert(st2.d.begin(), SDigit{ak, K, 1, dstst.cells});
+  st2.cells = K * dstst.cells;
+  auto in = std::make_shared<axe_redist_plan>();
+  AXE_TRY(plan_redist(S, sst, T2, st2, es, nranks, rank, in.get()));
+  const int64_t covered = (int64_t)(in->locals.size() + in->recvs.size()) * in->n * in->dst_rep;
+  if (covered != st2.cells)
+    AXE_FAIL(AXE_ERR_UNSUPPORTED,
+             "reduce-redistribute: rank %d's destination image (%lld of %lld cells) must be its whole storage", rank,
+             (long long)(covered / std::max<int64_t>(1, K)), (long long)dstst.cells);
+  // phase 2: (K, C):(C, 1) -> (C):(1) on flat storages
+  const int64_t C = dstst.cells;
+  Layout a, b;
+  std::vector<Iter> da{Iter{C, 1, axis_m()}};
+  if (K > 1) da.insert(da.begin(), Iter{K, C, axis_m()});
+  AXE_TRY(make_layout(da, {}, {}, &a));
+  AXE_TRY(make_layout({Iter{C, 1, axis_m()}}, {}, {}, &b));
+  AXE_TRY(plan_reduce(a, mstorage(K * C, nullptr), b, mstorage(C, nullptr), dtype, 16, &P->red));
+  P->inner = in;
+  P->nranks = nranks;
+  P->rank = rank;
+  P->es = es;
+  P->src_cells = sst.cells;
+  P->dst_cells = dstst.cells;
+  P->stage_bytes = K * C * es;
+  P->desc = "{\"pattern\":\"reduce\",\"K\":" + std::to_string(K) + ",\"exchange\":" + in->desc +
+            ",\"reduce\":" + P->red.desc + "}";
+  return AXE_OK;
+}
+
+static axe_status ensure_stage(const axe_redist_plan *P) {
+  std::lock_guard<std::mutex> lk(P->mu);
+  if (!P->stage && P->stage_bytes) {
+    cudaError_t e = cudaMalloc(&P->stage, (size_t)P->stage_bytes);
+    if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "reduce stage: %s", cudaGetErrorString(e));
+  }
+  return AXE_OK;
+}
+
 static axe_status ensure_scratch(const axe_redist_plan *P) {
   std::lock_guard<std::mutex> lk(P->mu);
   cudaError_t e = cudaSuccess;
@@ -399,6 +469,11 @@ static axe_status ensure_scratch(const axe_redist_plan *P) {
 
 static axe_status exec_redist(const axe_redist_plan *P, axe_comm *C, const void *src, void *dst, cudaStream_t st) {
   if (!C || !C->comm) AXE_FAIL(AXE_ERR_INVALID_ARG, "no communicator");
+  if (P->inner) {  // reduce-redistribute: partials -> stage (exchange), then the slab sum
+    AXE_TRY(ensure_stage(P));
+    AXE_TRY(exec_redist(P->inner.get(), C, src, P->stage, st));
+    return run_reduce(P->red, P->stage, dst, st);
+  }
   if (C->nranks != P->nranks || C->rank != P->rank)
     AXE_FAIL(AXE_ERR_INVALID_ARG, "plan for rank %d/%d used on comm rank %d/%d", P->rank, P->nranks, C->rank, C->nranks);
   const uint8_t *s = (const uint8_t *)src;
@@ -532,6 +607,52 @@ axe_status axe_redist_plan_create(const axe_layout *src, const axe_storage *src_
   return AXE_OK;
 }
 
+axe_status axe_redist_reduce_plan_create(const axe_layout *src, const axe_storage *src_st, const axe_layout *dst,
+                                         const axe_storage *dst_st, int dtype, int nranks, int rank,
+                                         axe_redist_plan **out) {
+  if (!src || !dst || !out) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
+  *out = nullptr;
+  Storage ss, ds;
+  AXE_TRY(make_storage(src_st, &ss));
+  AXE_TRY(make_storage(dst_st, &ds));
+  auto *p = new axe_redist_plan;
+  axe_status st = plan_redist_reduce(src->L, ss, dst->L, ds, dtype, nranks, rank, p);
+  if (st != AXE_OK) {
+    delete p;
+    return st;
+  }
+  *out = p;
+  return AXE_OK;
+}
+
+axe_status axe_redistribute_reduce(const axe_layout *src, const axe_storage *src_st, const void *src_local,
+                                   const axe_layout *dst, const axe_storage *dst_st, void *dst_local, int dtype,
+                                   axe_comm *comm, void *stream) {
+  if (!comm) AXE_FAIL(AXE_ERR_INVALID_ARG, "comm is NULL");
+  if (!src || !dst) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL layout");
+  static std::mutex mu;
+  static std::unordered_map<std::string, std::shared_ptr<axe_redist_plan>> cache;
+  Storage ss, ds;
+  AXE_TRY(make_storage(src_st, &ss));
+  AXE_TRY(make_storage(dst_st, &ds));
+  const std::string key = layout_key(src->L) + "#" + storage_key(ss) + "#" + layout_key(dst->L) + "#" +
+                          storage_key(ds) + "#" + std::to_string(dtype) + "#" + std::to_string(comm->nranks) + "#" +
+                          std::to_string(comm->rank) + "#" + std::to_string((uintptr_t)comm);
+  std::shared_ptr<axe_redist_plan> p;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) p = it->second;
+  }
+  if (!p) {
+    p = std::make_shared<axe_redist_plan>();
+    AXE_TRY(plan_redist_reduce(src->L, ss, dst->L, ds, dtype, comm->nranks, comm->rank, p.get()));
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = p;
+  }
+  return exec_redist(p.get(), comm, src_local, dst_local, (cudaStream_t)stream);
+}
+
 axe_status axe_redist_plan_execute(const axe_redist_plan *plan, axe_comm *comm, const void *src_local, void *dst_local,
                                    void *stream) {
   if (!plan) AXE_FAIL(AXE_ERR_INVALID_ARG, "plan is NULL");
@@ -541,6 +662,7 @@ axe_status axe_redist_plan_execute(const axe_redist_plan *plan, axe_comm *comm, 
 axe_status axe_redist_plan_execute_peers(const axe_redist_plan *plan, const void *src_local, void *const *dst_peers,
                                          void *stream) {
   if (!plan || !src_local || !dst_peers) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
+  if (plan->inner) AXE_FAIL(AXE_ERR_UNSUPPORTED, "execute_peers: reduce plans stage through library memory");
   for (int r = 0; r < plan->nranks; r++)
     if (!dst_peers[r]) AXE_FAIL(AXE_ERR_INVALID_ARG, "dst_peers[%d] is NULL", r);
   cudaStream_t st = (cudaStream_t)stream;
@@ -560,6 +682,7 @@ axe_status axe_redist_plan_describe(const axe_redist_plan *plan, char *buf, int 
 axe_status axe_redist_plan_counts(const axe_redist_plan *plan, int peer, int64_t *send, int64_t *recv) {
   if (!plan || !send || !recv) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
   if (peer < 0 || peer >= plan->nranks) AXE_FAIL(AXE_ERR_DOMAIN, "peer %d out of range", peer);
+  if (plan->inner) return axe_redist_plan_counts(plan->inner.get(), peer, send, recv);
   *send = *recv = 0;
   if (peer == plan->rank) {
     *send = *recv = (int64_t)plan->locals.size() * plan->n;
@@ -573,6 +696,7 @@ axe_status axe_redist_plan_counts(const axe_redist_plan *plan, int peer, int64_t
 axe_status axe_redist_plan_map(const axe_redist_plan *plan, int kind, int peer, int64_t k, int64_t *a, int64_t *b) {
   if (!plan || !a || !b) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
   if (kind < 0 || kind > 2) AXE_FAIL(AXE_ERR_INVALID_ARG, "kind must be 0, 1 or 2");
+  if (plan->inner) return axe_redist_plan_map(plan->inner.get(), kind, peer, k, a, b);
   const std::vector<Xfer> &lst = kind == 0 ? plan->sends : kind == 1 ? plan->recvs : plan->locals;
   std::vector<const Xfer *> mine;
   for (auto &e : lst)
@@ -635,11 +759,23 @@ axe_status axe_redist_emulate(const axe_redist_plan *const *plans, int nranks, c
                               void *const *dst_locals, void *stream) {
   if (!plans || !src_locals || !dst_locals || nranks < 1) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
   cudaStream_t st = (cudaStream_t)stream;
-  for (int r = 0; r < nranks; r++) {
+  for (int r = 0; r < nranks; r++)
     if (!plans[r] || plans[r]->rank != r || plans[r]->nranks != nranks)
       AXE_FAIL(AXE_ERR_INVALID_ARG, "plans[%d] is not rank %d of %d", r, r, nranks);
-    AXE_TRY(ensure_scratch(plans[r]));
+  if (plans[0]->inner) {  // reduce plans: emulate the exchange into the stages, then sum per rank
+    std::vector<const axe_redist_plan *> in(nranks);
+    std::vector<void *> stages(nranks);
+    for (int r = 0; r < nranks; r++) {
+      if (!plans[r]->inner) AXE_FAIL(AXE_ERR_INVALID_ARG, "plans mix reduce and plain redistribution");
+      AXE_TRY(ensure_stage(plans[r]));
+      in[r] = plans[r]->inner.get();
+      stages[r] = plans[r]->stage;
+    }
+    AXE_TRY(axe_redist_emulate(in.data(), nranks, src_locals, stages.data(), stream));
+    for (int r = 0; r < nranks; r++) AXE_TRY(run_reduce(plans[r]->red, plans[r]->stage, dst_locals[r], st));
+    return AXE_OK;
   }
+  for (int r = 0; r < nranks; r++) AXE_TRY(ensure_scratch(plans[r]));
   const int nch = plans[0]->nchunk;
   for (int r = 0; r < nranks; r++)
     if (plans[r]->nchunk != nch) AXE_FAIL(AXE_ERR_INVALID_ARG, "plans disagree on wire chunks");

@@ -1,0 +1,241 @@
+"""GPU parity of the reduction row (reading R24): K4 on one device
+(axe_reduce / ReducePlan) and the distributed reduce-redistribute (emulated on one
+B200, and through a 1-rank NCCL communicator), against oracle.reduce.
+
+Tolerance (DESIGN.md §3 R24): bf16 / f16 / integer results are compared
+bit-exactly -- the summands of synth.numbers are multiples of 2^-15 (bf16) or
+2^-18 (f16) below 1 in magnitude, so every partial sum of K <= 32 of them is exact
+in fp32 and both sides round the same exact value once.  f32 / f64 sums are not
+exact: the kernel adds in k order in fp32 / fp64, the oracle in fp64, so each
+output may differ by the accumulated rounding, at most K * sum|x_k| * u <= K^2 u
+(|x| < 1, u = 2^-24 / 2^-53), plus one output rounding."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth import layout, linear_storage, storage
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+NT = os.cpu_count() or 4
+FLOAT = {"f32": (np.float32, np.uint32, 2.0 ** -24), "f64": (np.float64, np.uint64, 2.0 ** -53)}
+
+
+@pytest.fixture(scope="module")
+def axe():
+    assert torch.cuda.is_available()
+    import paper_2601_19092_b200 as m
+    return m
+
+
+def guard(nbytes, seed):
+    """Device buffer with 4 KiB sentinel guards on both sides (compute-sanitizer is closed on the pool)."""
+    g = 4096
+    buf = torch.from_numpy(synth.sentinel(nbytes + 2 * g, seed)).cuda()
+    return buf, buf[g:g + nbytes]
+
+
+def check_guards(buf, nbytes, seed):
+    g = 4096
+    ref = synth.sentinel(nbytes + 2 * g, seed)
+    h = buf.cpu().numpy()
+    assert np.array_equal(h[:g], ref[:g]) and np.array_equal(h[g + nbytes:], ref[g + nbytes:]), "guard overwritten"
+
+
+def compare(got, exp, fill, dtype, K):
+    if dtype not in FLOAT:
+        assert np.array_equal(got, exp)
+        return
+    ft, ut, u = FLOAT[dtype]
+    untouched = exp.view(ut) == fill.view(ut)
+    assert np.array_equal(got.view(ut)[untouched], exp.view(ut)[untouched]), "cells outside the image changed"
+    g, e = got.view(ft)[~untouched].astype(np.float64), exp.view(ft)[~untouched].astype(np.float64)
+    tol = K * K * u + np.abs(e) * u
+    bad = np.abs(g - e) > tol
+    assert not bad.any(), f"{bad.sum()} elements outside the bound, worst {np.abs(g - e).max()}"
+
+
+def run_local(axe, cfg, dtype, seed=7, one_shot=False):
+    es = synth.DTYPE_SIZE[dtype]
+    ed, _ = oracle.sizes(cfg["src"])
+    edd, _ = oracle.sizes(cfg["dst"])
+    K = ed // edd
+    vals = synth.numbers(ed, dtype, seed)
+    sfill = synth.sentinel(synth.storage_cells(cfg["src_st"]) * es, seed + 1)
+    sbuf = oracle.scatter_logical(cfg["src"], cfg["src_st"], vals, es, sfill, NT)
+    dbytes = synth.storage_cells(cfg["dst_st"]) * es
+    dfill = synth.sentinel(dbytes, seed + 2)
+    exp = dfill.copy()
+    oracle.reduce(cfg["src"], cfg["src_st"], sbuf, cfg["dst"], cfg["dst_st"], exp, dtype, nthreads=NT)
+    s_dev = torch.from_numpy(sbuf).cuda()
+    gbuf, d_dev = guard(dbytes, seed + 2 - 1)
+    d_dev.copy_(torch.from_numpy(dfill))
+    n0 = axe.kernel_launch_count()
+    if one_shot:
+        axe.axe_reduce(cfg["src"], cfg["src_st"], s_dev, cfg["dst"], cfg["dst_st"], d_dev, dtype)
+        desc = None
+    else:
+        plan = axe.ReducePlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], dtype)
+        assert plan.sizes() == (sbuf.nbytes, dbytes)
+        plan.execute(s_dev, d_dev)
+        desc = plan.describe()
+    torch.cuda.synchronize()
+    assert axe.kernel_launch_count() - n0 == 1
+    check_guards(gbuf, dbytes, seed + 1)
+    compare(d_dev.cpu().numpy(), exp, dfill, dtype, K)
+    return desc
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f16", "f32", "f64", "i32", "i64"])
+def test_leading_dim_sum_row_major(axe, dtype):
+    d = run_local(axe, synth.reduce_local(8, 96, 200, dtype), dtype)
+    assert d["kernel"] == "reduce" and d["K"] == 8
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_sum_into_swizzled_tiles(axe, dtype):
+    """The reduction fused with config 2's re-tiling: 64x64 tiles + SW128 destination."""
+    d = run_local(axe, synth.reduce_local(4, 256, 512, dtype, tiled=True), dtype)
+    assert d["kernel"] == "reduce" and d["vec_bytes"] == 16
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 17, 300])
+def test_k_values(axe, K):
+    """K = 1 (a copy), odd K (tail of the 8-wide load batch), K > 256 (decoded summand offsets)."""
+    dtype = "f16" if K <= 32 else "i32"
+    d = run_local(axe, synth.reduce_local(K, 8, 96, dtype), dtype)
+    assert d["table"] == (K <= 256)
+
+
+def test_interleaved_summands_and_transposed_destination(axe):
+    """Summands innermost in memory (src (Y, K) storage order) into a column-major padded destination."""
+    K, R, C, ld = 6, 40, 24, 48
+    src = layout([(K, 1), (R, C * K), (C, K)])
+    dst = layout([(R, 1), (C, ld)])
+    cfg = dict(src=src, src_st=linear_storage(K * R * C), dst=dst, dst_st=linear_storage(C * ld))
+    run_local(axe, cfg, "bf16")
+
+
+def test_replicas_and_offsets(axe):
+    """Source replicas (read at the representative) and destination replicas + offset on named axes."""
+    K, N = 4, 256
+    src = layout([(K, N), (N, 1)], [(2, K * N)])
+    dst = layout([(N // 32, 1, "warp"), (32, 1, "lane")], [(2, 8, "warp")], {"warp": 1})
+    cfg = dict(src=src, src_st=linear_storage(2 * K * N), dst=dst, dst_st=storage([("warp", 17), ("lane", 32)]))
+    d = run_local(axe, cfg, "f32")
+    assert d["replicas"] == 2
+
+
+def test_generic_fallback(axe):
+    """Digit systems that do not nest: the source is a column-major 30x7 matrix (K = 6 blocks of 35), the
+    destination a 7x5 matrix with rows padded to 8 -- innermost extents 7 and 5 share no divisor -> k4_generic."""
+    src = layout([(30, 1), (7, 30)])
+    dst = layout([(7, 8), (5, 1)])
+    cfg = dict(src=src, src_st=linear_storage(210), dst=dst, dst_st=linear_storage(56))
+    d = run_local(axe, cfg, "f32")
+    assert d["kernel"] == "reduce_generic"
+
+
+def test_one_shot_cached(axe):
+    cfg = synth.reduce_local(3, 32, 64, "bf16")
+    run_local(axe, cfg, "bf16", one_shot=True)
+    run_local(axe, cfg, "bf16", seed=9, one_shot=True)
+
+
+def test_bench_workload_full_size(axe):
+    """bench.py's reduce row at full size: (8, 8192, 4096) bf16 -> (8192, 4096), every element."""
+    d = run_local(axe, synth.reduce_local(8, 8192, 4096, "bf16"), "bf16")
+    assert d["vec_bytes"] == 16
+
+
+def test_errors(axe):
+    with pytest.raises(axe.AxeError) as e:
+        axe.ReducePlan(layout([(30, 1)]), linear_storage(30), layout([(7, 1)]), linear_storage(7), "f32")
+    assert e.value.name == "AXE_ERR_SIZE_MISMATCH"
+    x = torch.zeros(64, dtype=torch.float32, device="cuda")
+    plan = axe.ReducePlan(layout([(2, 32), (32, 1)]), linear_storage(64), layout([(32, 1)]), linear_storage(32), "f32")
+    with pytest.raises(axe.AxeError) as e:
+        plan.execute(x, x[8:])
+    assert e.value.name == "AXE_ERR_ALIAS"
+
+
+# ------------------------------------------------------------------ distributed
+
+
+def run_dist(axe, cfg, dtype, seed=21):
+    n, es = cfg["nranks"], synth.DTYPE_SIZE[dtype]
+    ed, _ = oracle.sizes(cfg["src"])
+    edd, _ = oracle.sizes(cfg["dst"])
+    K = ed // edd
+    vals = synth.numbers(ed, dtype, seed)
+    sfill = synth.sentinel(synth.storage_cells(cfg["src_st"]) * es, seed + 1)
+    src = oracle.scatter_ranks(cfg["src"], cfg["src_st"], vals, es, n, sfill, NT)
+    dfill = synth.sentinel(synth.storage_cells(cfg["dst_st"]) * es, seed + 2)
+    exp = [dfill.copy() for _ in range(n)]
+    oracle.reduce(cfg["src"], cfg["src_st"], src, cfg["dst"], cfg["dst_st"], exp, dtype, nranks=n, nthreads=NT)
+    plans = [axe.RedistPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], es, n, r, reduce_dtype=dtype)
+             for r in range(n)]
+    s_dev = [torch.from_numpy(s).cuda() for s in src]
+    d_dev = [torch.from_numpy(dfill).cuda() for _ in range(n)]
+    axe.redist_emulate(plans, s_dev, d_dev)
+    torch.cuda.synchronize()
+    for r in range(n):
+        compare(d_dev[r].cpu().numpy(), exp[r], dfill, dtype, K)
+    return plans[0].describe()
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_reduce_scatter_emulated(axe, P, dtype):
+    """The DTensor reduce-scatter of P:399-403 ((P, 64, 64) partials summed over dim 0, rows sharded)."""
+    d = run_dist(axe, synth.reduce_scatter(P, 64, 64, dtype), dtype)
+    assert d["pattern"] == "reduce" and d["K"] == P
+
+
+def test_reduce_scatter_emulated_large(axe):
+    d = run_dist(axe, synth.reduce_scatter(8, 1024, 2048, "bf16"), "bf16")
+    assert d["exchange"]["packs"] == 0
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_all_reduce_emulated(axe, P):
+    run_dist(axe, synth.all_reduce(P, 32, 128, "bf16"), "bf16")
+
+
+def test_mesh_partial_over_one_axis(axe):
+    """2x2 mesh (gpuid = 2a + b): partials over a, replicated over b -> summed, sharded by rows over b,
+    replicated over a."""
+    R, C = 64, 32
+    src = layout([(2, 2, "gpuid"), (R, C), (C, 1)], [(2, 1, "gpuid")])
+    dst = layout([(2, 1, "gpuid"), (R // 2, C), (C, 1)], [(2, 2, "gpuid")])
+    cfg = dict(nranks=4, src=src, src_st=linear_storage(R * C), dst=dst, dst_st=linear_storage(R // 2 * C))
+    run_dist(axe, cfg, "f32")
+
+
+def test_transposed_shard_emulated(axe):
+    """Partials row-major, destination column shards stored column-major (pack + unpack kernels)."""
+    P, R, C = 4, 32, 64
+    src = layout([(P, 1, "gpuid"), (R, C), (C, 1)])
+    dst = layout([(R, 1), (P, 1, "gpuid"), (C // P, R)])
+    cfg = dict(nranks=P, src=src, src_st=linear_storage(R * C), dst=dst, dst_st=linear_storage(R * C // P))
+    run_dist(axe, cfg, "bf16")
+
+
+def test_nccl_single_rank_reduce(axe):
+    """The NCCL path on one GPU: both partials on rank 0 (K = 2), axe_redistribute_reduce through a 1-rank
+    communicator, against the oracle."""
+    comm = axe.Comm(axe.get_unique_id(), 1, 0, torch.cuda.current_device())
+    K, R, C = 2, 64, 96
+    src = layout([(K, R * C), (R, C), (C, 1)])
+    dst = layout([(R, C), (C, 1)], [(1, 1, "gpuid")])
+    vals = synth.numbers(K * R * C, "bf16", 3)
+    x = torch.from_numpy(vals.copy()).cuda()
+    y = torch.zeros(R * C * 2, dtype=torch.uint8, device="cuda")
+    axe.axe_redistribute_reduce(src, linear_storage(K * R * C), x, dst, linear_storage(R * C), y, "bf16", comm)
+    torch.cuda.synchronize()
+    exp = np.zeros(R * C * 2, np.uint8)
+    oracle.reduce(src, linear_storage(K * R * C), [vals], dst, linear_storage(R * C), [exp], "bf16", nranks=1)
+    assert np.array_equal(y.cpu().numpy(), exp)
