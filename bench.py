@@ -211,6 +211,19 @@ def measure_reshard(axe, torch, dist, ws, rank, local, stream, iters=20, warm=3)
                           "ingress_bytes_per_gpu": ingress, "bus_GBps": ingress / (ms * 1e-3) / 1e9,
                           "frac_of_900": ingress / (ms * 1e-3) / 1e9 / 900}
         del src, dst
+    # §8(f) f3: reduce-scatter of (ws, 16384, 8192) bf16 partials (P:399-403 at scale); NCCL busbw
+    # convention: (P-1)/P * partial bytes per GPU
+    rs = synth.reduce_scatter(ws, 16384, 8192, "bf16")
+    prs = axe.RedistPlan(rs["src"], rs["src_st"], rs["dst"], rs["dst_st"], 2, ws, rank, reduce_dtype="bf16")
+    src = torch.empty(synth.storage_cells(rs["src_st"]), dtype=torch.bfloat16, device="cuda").normal_()
+    dst = torch.empty(synth.storage_cells(rs["dst_st"]), dtype=torch.bfloat16, device="cuda")
+    ms = timed(lambda: prs.execute(comm, src, dst, stream))
+    ref = torch.empty_like(dst)
+    ms_ref = timed(lambda: dist.reduce_scatter_tensor(ref, src))
+    bus = (ws - 1) / ws * src.numel() * 2
+    res["reduce_scatter"] = {"P": ws, "ms": ms, "bus_bytes_per_gpu": bus, "bus_GBps": bus / (ms * 1e-3) / 1e9,
+                             "torch_reduce_scatter_bus_GBps": bus / (ms_ref * 1e-3) / 1e9}
+    del src, dst, ref
     torch.cuda.synchronize()
     dist.barrier()
     del comm
@@ -298,6 +311,15 @@ def measure_extras(axe, torch):
         plan = axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], cfg["es"])
         ms = _time_plan(torch, plan)
         alg = plan.src.E_D * cfg["es"] * (1 + plan.dst.E_R)
+        gbs = alg / (ms * 1e-3) / 1e9
+        rows[name] = {"kernel": plan.describe()["kernel"], "us": ms * 1e3, "GBps": gbs, "frac_of_measured": gbs / peak,
+                      "alg_bytes": alg}
+    # §8(f) f3: the K4 sum over the leading dimension (K partials read once, the sum written once)
+    for name, cfg in {"reduce_k8_bf16_8192x4096": synth.reduce_local(8, 8192, 4096, "bf16"),
+                      "reduce_k8_bf16_into_sw128_tiles": synth.reduce_local(8, 8192, 4096, "bf16", tiled=True)}.items():
+        plan = axe.ReducePlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], cfg["dtype"])
+        ms = _time_plan(torch, plan)
+        alg = sum(plan.sizes())
         gbs = alg / (ms * 1e-3) / 1e9
         rows[name] = {"kernel": plan.describe()["kernel"], "us": ms * 1e3, "GBps": gbs, "frac_of_measured": gbs / peak,
                       "alg_bytes": alg}

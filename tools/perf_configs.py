@@ -81,6 +81,59 @@ def time_cfg(cfg, kernel, reps=20):
             "frac_measured": gbs / 6547.2, "alg_bytes": alg}
 
 
+REDUCE = {
+    "reduce_bf16_k8": lambda: synth.reduce_local(8, 8192, 4096, "bf16"),
+    "reduce_bf16_k8_tiled": lambda: synth.reduce_local(8, 8192, 4096, "bf16", tiled=True),
+    "reduce_f32_k8": lambda: synth.reduce_local(8, 8192, 2048, "f32"),
+    "reduce_bf16_k2": lambda: synth.reduce_local(2, 16384, 8192, "bf16"),
+}
+
+
+def _graph_time(fn, G, reps):
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=torch.cuda.Stream()):
+        for j in range(G):
+            fn(j)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / (reps * G)
+
+
+def time_reduce(name, reps=20):
+    """K4 sum over the leading dimension; algorithmic bytes = K*Y*es read + Y*es written.  Also torch's
+    own x.view(K, -1).sum(0) on the same bytes (library reference point, row-major case)."""
+    cfg = REDUCE[name]()
+    dt = cfg["dtype"]
+    plan = axe.ReducePlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], dt)
+    sb, db = plan.sizes()
+    K = cfg["K"]
+    alg = sb + db
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    pairs = max(1, min(4, -(-4 * l2 // (sb + db))))
+    tdt = {"bf16": torch.bfloat16, "f32": torch.float32}[dt]
+    es = synth.DTYPE_SIZE[dt]
+    srcs = [torch.randn(sb // es, device="cuda").to(tdt) for _ in range(pairs)]
+    dsts = [torch.empty(db // es, dtype=tdt, device="cuda") for _ in range(pairs)]
+    ms = _graph_time(lambda j: plan.execute(srcs[j % pairs], dsts[j % pairs], torch.cuda.current_stream()),
+                     pairs * 4, reps)
+    out = {"config": name, "kernel": plan.describe()["kernel"], "us": ms * 1e3, "GB/s": alg / (ms * 1e-3) / 1e9,
+           "frac_measured": alg / (ms * 1e-3) / 1e9 / 6547.2, "alg_bytes": alg}
+    if "tiled" not in name:
+        tms = _graph_time(lambda j: torch.sum(srcs[j % pairs].view(K, -1), dim=0, out=dsts[j % pairs]), pairs * 4, reps)
+        out["torch_sum_us"] = tms * 1e3
+        out["torch_sum_GB/s"] = alg / (tms * 1e-3) / 1e9
+    del srcs, dsts
+    torch.cuda.empty_cache()
+    return out
+
+
 def torch_copy(nbytes, reps=20):
     """Reference point: torch's own copy_ of nbytes (read + write counted), same rotation and graph."""
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
@@ -111,7 +164,12 @@ def main():
     ap.add_argument("--kernel", default="auto")
     ap.add_argument("--only", default="")
     ap.add_argument("--torch-copy", action="store_true")
+    ap.add_argument("--reduce", action="store_true", help="time the K4 reduction rows instead")
     a = ap.parse_args()
+    if a.reduce:
+        for n in (a.only.split(",") if a.only else list(REDUCE)):
+            print(json.dumps(time_reduce(n)), flush=True)
+        return
     if a.torch_copy:
         for nb in (32 << 20, 1 << 30, 4 << 30):
             print(json.dumps(torch_copy(nb)), flush=True)
