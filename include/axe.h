@@ -329,12 +329,22 @@ axe_status axe_reduce(const axe_layout *src, const axe_storage *src_st, const vo
  * buffer (K slabs shaped like this rank's dst storage; pack / NCCL / unpack as
  * axe_redist_plan_execute) followed by one K4 sum of the slabs into dst_local.
  * Every rank's destination image must be its whole dst storage
- * (AXE_ERR_UNSUPPORTED otherwise).  The returned plan is used with
- * axe_redist_plan_execute / _describe / _counts / _map (stage element indices)
- * / _destroy and axe_redist_emulate; not with _execute_peers. */
+ * (AXE_ERR_UNSUPPORTED otherwise).  A destination replicated over >= 3 ranks
+ * is planned in two phases instead: a reduce-scatter (as above) into an even
+ * shard (nranks, E_D(dst)/nranks):(1@gpuid, 1@m), then a plain redistribution
+ * of that shard into the destination (an all-gather for a row-major replicated
+ * destination) -- describe() says "reduce_scatter_allgather" and
+ * axe_redist_plan_phase returns the two sub-plans.  The returned plan is used
+ * with axe_redist_plan_execute / _describe / _counts / _map (stage element
+ * indices; two-phase plans: query the phases) / _destroy and
+ * axe_redist_emulate; not with _execute_peers. */
 axe_status axe_redist_reduce_plan_create(const axe_layout *src, const axe_storage *src_st, const axe_layout *dst,
                                          const axe_storage *dst_st, int dtype, int nranks, int rank,
                                          axe_redist_plan **out);
+/* Phase i (0: reduce-scatter, 1: gather) of a two-phase reduction plan; the
+ * sub-plan is owned by `plan` (do not destroy it).  AXE_ERR_UNSUPPORTED for
+ * any other plan. */
+axe_status axe_redist_plan_phase(const axe_redist_plan *plan, int i, const axe_redist_plan **out);
 /* One-shot collective form (plans through an internal cache). */
 axe_status axe_redistribute_reduce(const axe_layout *src, const axe_storage *src_st, const void *src_local,
                                    const axe_layout *dst, const axe_storage *dst_st, void *dst_local, int dtype,

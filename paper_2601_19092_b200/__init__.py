@@ -102,6 +102,7 @@ _SIGS = {
     "axe_reduce": ([_vp, C.POINTER(axe_storage), _vp, _vp, C.POINTER(axe_storage), _vp, C.c_int, _vp], C.c_int),
     "axe_redist_reduce_plan_create": ([_vp, C.POINTER(axe_storage), _vp, C.POINTER(axe_storage), C.c_int, C.c_int,
                                        C.c_int, C.POINTER(_vp)], C.c_int),
+    "axe_redist_plan_phase": ([_vp, C.c_int, C.POINTER(_vp)], C.c_int),
     "axe_redistribute_reduce": ([_vp, C.POINTER(axe_storage), _vp, _vp, C.POINTER(axe_storage), _vp, C.c_int, _vp,
                                  _vp], C.c_int),
 }
@@ -428,9 +429,18 @@ class RedistPlan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and getattr(self, "_owned", True):
             _lib.axe_redist_plan_destroy(h)
-            self._h = None
+        self._h = None
+
+    def phase(self, i: int) -> "RedistPlan":
+        """Sub-plan i (0: reduce-scatter, 1: gather) of a two-phase reduction plan (owned by this plan)."""
+        h = C.c_void_p()
+        _check(_lib.axe_redist_plan_phase(self._h, i, C.byref(h)), "axe_redist_plan_phase")
+        sub = RedistPlan.__new__(RedistPlan)
+        sub._h, sub._owned, sub._parent = h, False, self
+        sub.nranks, sub.rank, sub.elem_size = self.nranks, self.rank, self.elem_size
+        return sub
 
     @property
     def handle(self):

@@ -71,9 +71,13 @@ struct axe_redist_plan {
   std::shared_ptr<axe_redist_plan> inner;
   ReducePlan red;
   int64_t stage_bytes = 0;
+  // two-phase reduction (destination replicated over >= 3 ranks): phase_a reduce-scatters into an
+  // evenly sharded temporary, phase_b redistributes (all-gathers) it into the destination
+  std::shared_ptr<axe_redist_plan> phase_a, phase_b;
+  int64_t tmp_bytes = 0;
   // scratch owned by the plan (allocated on first execute, on the current device)
   mutable std::mutex mu;
-  mutable void *send_buf = nullptr, *recv_buf = nullptr, *stage = nullptr;
+  mutable void *send_buf = nullptr, *recv_buf = nullptr, *stage = nullptr, *tmp = nullptr;
   mutable cudaStream_t side = nullptr;
   mutable cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
   mutable cudaStream_t pk = nullptr, up = nullptr;  // pack / unpack streams
@@ -82,6 +86,7 @@ struct axe_redist_plan {
     if (send_buf) cudaFree(send_buf);
     if (recv_buf) cudaFree(recv_buf);
     if (stage) cudaFree(stage);
+    if (tmp) cudaFree(tmp);
     for (cudaStream_t x : {side, pk, up})
       if (x) cudaStreamDestroy(x);
     for (cudaEvent_t x : {ev_fork, ev_join, ev_join2})
@@ -384,8 +389,8 @@ static axe_status plan_redist(const Layout &S, const Storage &sst, const Layout 
 // cell in k order (K4).  A swizzle permutes every slab identically (the slab is a whole number
 // of swizzle blocks), so phase 2 is a flat elementwise sum.  Every rank's destination image
 // must be its whole dst storage (checked), or phase 2 would write cells outside the image.
-static axe_status plan_redist_reduce(const Layout &S, const Storage &sst, const Layout &T, const Storage &dstst,
-                                     int dtype, int nranks, int rank, axe_redist_plan *P) {
+static axe_status plan_redist_reduce_1(const Layout &S, const Storage &sst, const Layout &T, const Storage &dstst,
+                                       int dtype, int nranks, int rank, axe_redist_plan *P) {
   const int es = dtype_size(dtype);
   if (!es) AXE_FAIL(AXE_ERR_INVALID_ARG, "unknown dtype %d", dtype);
   if (S.ED % T.ED)
@@ -430,12 +435,44 @@ static axe_status plan_redist_reduce(const Layout &S, const Storage &sst, const 
   return AXE_OK;
 }
 
+// A destination replicated over R >= 3 ranks would receive every partial on every replica
+// ((P-1) partials of wire per GPU); instead reduce-scatter into an even shard of the logical
+// range, (P, E_D/P):(1@gpuid, 1@m), and redistribute that (an all-gather for a row-major
+// replicated destination): 2(P-1)/P of a partial per GPU, as a ring all-reduce.
+static axe_status plan_redist_reduce(const Layout &S, const Storage &sst, const Layout &T, const Storage &dstst,
+                                     int dtype, int nranks, int rank, axe_redist_plan *P) {
+  const int g = axis_gpuid();
+  int64_t reps = 1;
+  for (auto &it : T.R)
+    if (it.a == g) reps *= it.e;
+  const int es = dtype_size(dtype);
+  if (reps < 3 || nranks < 3 || T.ED % nranks || !es)
+    return plan_redist_reduce_1(S, sst, T, dstst, dtype, nranks, rank, P);
+  Layout Tt;
+  AXE_TRY(make_layout({Iter{nranks, 1, g}, Iter{T.ED / nranks, 1, axis_m()}}, {}, {}, &Tt));
+  const Storage tst = mstorage(T.ED / nranks, nullptr);
+  auto A = std::make_shared<axe_redist_plan>(), B = std::make_shared<axe_redist_plan>();
+  AXE_TRY(plan_redist_reduce_1(S, sst, Tt, tst, dtype, nranks, rank, A.get()));
+  AXE_TRY(plan_redist(Tt, tst, T, dstst, es, nranks, rank, B.get()));
+  P->phase_a = A;
+  P->phase_b = B;
+  P->nranks = nranks;
+  P->rank = rank;
+  P->es = es;
+  P->src_cells = sst.cells;
+  P->dst_cells = dstst.cells;
+  P->tmp_bytes = tst.cells * es;
+  P->desc = "{\"pattern\":\"reduce_scatter_allgather\",\"K\":" + std::to_string(S.ED / T.ED) +
+            ",\"phase_a\":" + A->desc + ",\"phase_b\":" + B->desc + "}";
+  return AXE_OK;
+}
+
 static axe_status ensure_stage(const axe_redist_plan *P) {
   std::lock_guard<std::mutex> lk(P->mu);
-  if (!P->stage && P->stage_bytes) {
-    cudaError_t e = cudaMalloc(&P->stage, (size_t)P->stage_bytes);
-    if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "reduce stage: %s", cudaGetErrorString(e));
-  }
+  cudaError_t e = cudaSuccess;
+  if (!P->stage && P->stage_bytes) e = cudaMalloc(&P->stage, (size_t)P->stage_bytes);
+  if (e == cudaSuccess && !P->tmp && P->tmp_bytes) e = cudaMalloc(&P->tmp, (size_t)P->tmp_bytes);
+  if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "reduce staging: %s", cudaGetErrorString(e));
   return AXE_OK;
 }
 
@@ -469,6 +506,11 @@ static axe_status ensure_scratch(const axe_redist_plan *P) {
 
 static axe_status exec_redist(const axe_redist_plan *P, axe_comm *C, const void *src, void *dst, cudaStream_t st) {
   if (!C || !C->comm) AXE_FAIL(AXE_ERR_INVALID_ARG, "no communicator");
+  if (P->phase_a) {  // two-phase reduction: reduce-scatter into tmp, then redistribute tmp
+    AXE_TRY(ensure_stage(P));
+    AXE_TRY(exec_redist(P->phase_a.get(), C, src, P->tmp, st));
+    return exec_redist(P->phase_b.get(), C, P->tmp, dst, st);
+  }
   if (P->inner) {  // reduce-redistribute: partials -> stage (exchange), then the slab sum
     AXE_TRY(ensure_stage(P));
     AXE_TRY(exec_redist(P->inner.get(), C, src, P->stage, st));
@@ -662,7 +704,8 @@ axe_status axe_redist_plan_execute(const axe_redist_plan *plan, axe_comm *comm, 
 axe_status axe_redist_plan_execute_peers(const axe_redist_plan *plan, const void *src_local, void *const *dst_peers,
                                          void *stream) {
   if (!plan || !src_local || !dst_peers) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
-  if (plan->inner) AXE_FAIL(AXE_ERR_UNSUPPORTED, "execute_peers: reduce plans stage through library memory");
+  if (plan->inner || plan->phase_a)
+    AXE_FAIL(AXE_ERR_UNSUPPORTED, "execute_peers: reduce plans stage through library memory");
   for (int r = 0; r < plan->nranks; r++)
     if (!dst_peers[r]) AXE_FAIL(AXE_ERR_INVALID_ARG, "dst_peers[%d] is NULL", r);
   cudaStream_t st = (cudaStream_t)stream;
@@ -682,6 +725,7 @@ axe_status axe_redist_plan_describe(const axe_redist_plan *plan, char *buf, int 
 axe_status axe_redist_plan_counts(const axe_redist_plan *plan, int peer, int64_t *send, int64_t *recv) {
   if (!plan || !send || !recv) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
   if (peer < 0 || peer >= plan->nranks) AXE_FAIL(AXE_ERR_DOMAIN, "peer %d out of range", peer);
+  if (plan->phase_a) AXE_FAIL(AXE_ERR_UNSUPPORTED, "two-phase plan: query axe_redist_plan_phase(plan, 0 / 1)");
   if (plan->inner) return axe_redist_plan_counts(plan->inner.get(), peer, send, recv);
   *send = *recv = 0;
   if (peer == plan->rank) {
@@ -696,6 +740,7 @@ axe_status axe_redist_plan_counts(const axe_redist_plan *plan, int peer, int64_t
 axe_status axe_redist_plan_map(const axe_redist_plan *plan, int kind, int peer, int64_t k, int64_t *a, int64_t *b) {
   if (!plan || !a || !b) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
   if (kind < 0 || kind > 2) AXE_FAIL(AXE_ERR_INVALID_ARG, "kind must be 0, 1 or 2");
+  if (plan->phase_a) AXE_FAIL(AXE_ERR_UNSUPPORTED, "two-phase plan: query axe_redist_plan_phase(plan, 0 / 1)");
   if (plan->inner) return axe_redist_plan_map(plan->inner.get(), kind, peer, k, a, b);
   const std::vector<Xfer> &lst = kind == 0 ? plan->sends : kind == 1 ? plan->recvs : plan->locals;
   std::vector<const Xfer *> mine;
@@ -722,6 +767,15 @@ axe_status axe_redist_plan_map(const axe_redist_plan *plan, int kind, int peer, 
   }
   *a = kind == 1 ? dof : so;
   *b = kind == 2 ? dof : -1;
+  return AXE_OK;
+}
+
+axe_status axe_redist_plan_phase(const axe_redist_plan *plan, int i, const axe_redist_plan **out) {
+  if (!plan || !out) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
+  *out = nullptr;
+  if (!plan->phase_a) AXE_FAIL(AXE_ERR_UNSUPPORTED, "not a two-phase plan");
+  if (i != 0 && i != 1) AXE_FAIL(AXE_ERR_DOMAIN, "phase %d: 0 (reduce-scatter) or 1 (gather)", i);
+  *out = i == 0 ? plan->phase_a.get() : plan->phase_b.get();
   return AXE_OK;
 }
 
@@ -762,6 +816,19 @@ axe_status axe_redist_emulate(const axe_redist_plan *const *plans, int nranks, c
   for (int r = 0; r < nranks; r++)
     if (!plans[r] || plans[r]->rank != r || plans[r]->nranks != nranks)
       AXE_FAIL(AXE_ERR_INVALID_ARG, "plans[%d] is not rank %d of %d", r, r, nranks);
+  if (plans[0]->phase_a) {  // two-phase reduction: emulate phase a into the temporaries, then phase b
+    std::vector<const axe_redist_plan *> pa(nranks), pb(nranks);
+    std::vector<void *> tmps(nranks);
+    for (int r = 0; r < nranks; r++) {
+      if (!plans[r]->phase_a) AXE_FAIL(AXE_ERR_INVALID_ARG, "plans mix two-phase and other plans");
+      AXE_TRY(ensure_stage(plans[r]));
+      pa[r] = plans[r]->phase_a.get();
+      pb[r] = plans[r]->phase_b.get();
+      tmps[r] = plans[r]->tmp;
+    }
+    AXE_TRY(axe_redist_emulate(pa.data(), nranks, src_locals, tmps.data(), stream));
+    return axe_redist_emulate(pb.data(), nranks, tmps.data(), dst_locals, stream);
+  }
   if (plans[0]->inner) {  // reduce plans: emulate the exchange into the stages, then sum per rank
     std::vector<const axe_redist_plan *> in(nranks);
     std::vector<void *> stages(nranks);

@@ -200,9 +200,12 @@ def test_reduce_scatter_emulated_large(axe):
     assert d["exchange"]["packs"] == 0
 
 
-@pytest.mark.parametrize("P", [2, 4])
-def test_all_reduce_emulated(axe, P):
-    run_dist(axe, synth.all_reduce(P, 32, 128, "bf16"), "bf16")
+@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_all_reduce_emulated(axe, P, dtype):
+    """Partial -> Replicate: one exchange at P = 2, reduce-scatter + all-gather (two phases) at P >= 3."""
+    d = run_dist(axe, synth.all_reduce(P, 32, 128, dtype), dtype)
+    assert d["pattern"] == ("reduce" if P == 2 else "reduce_scatter_allgather")
 
 
 def test_mesh_partial_over_one_axis(axe):

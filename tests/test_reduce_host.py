@@ -59,6 +59,20 @@ def test_reduce_scatter_plan(P):
         assert d["reduce"]["K"] == P and d["reduce"]["vectors"] * 8 == 64 * 64 // P
 
 
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_all_reduce_plan_phases(P):
+    """Replicated over >= 3 ranks: reduce-scatter into an even shard, then an all-gather (2(P-1)/P of a
+    partial on the wire per GPU, as a ring all-reduce); over 2 ranks one exchange of the partials."""
+    cfg = synth.all_reduce(P, 64, 64, "bf16")
+    d = axe.RedistPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], 2, P, 0, reduce_dtype="bf16").describe()
+    if P == 2:
+        assert d["pattern"] == "reduce" and d["exchange"]["recv_elems"] == 64 * 64
+    else:
+        assert d["pattern"] == "reduce_scatter_allgather"
+        assert d["phase_a"]["exchange"]["recv_elems"] == (P - 1) * 64 * 64 // P
+        assert d["phase_b"]["pattern"] == "allgather" and d["phase_b"]["recv_elems"] == (P - 1) * 64 * 64 // P
+
+
 def test_uncovered_destination_is_rejected():
     """The slab sum writes every cell of the local dst storage; a destination image that misses cells is
     refused instead of overwriting them (R24)."""
@@ -109,6 +123,7 @@ def dist_inputs(cfg, dtype, seed=5):
 
 @pytest.mark.parametrize("mk,dtype", [(lambda: synth.reduce_scatter(4, 16, 8, "f16"), "f16"),
                                       (lambda: synth.all_reduce(3, 8, 8, "bf16"), "bf16"),
+                                      (lambda: synth.all_reduce(4, 8, 16, "f32"), "f32"),
                                       (lambda: synth.reduce_scatter(2, 8, 16, "i32"), "i32")])
 def test_cpu_enactment_matches_oracle(mk, dtype):
     cfg = mk()
@@ -120,15 +135,32 @@ def test_cpu_enactment_matches_oracle(mk, dtype):
     plans = [axe.RedistPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], 0, n, r, reduce_dtype=dtype)
              for r in range(n)]
     et = ELEM[dtype]
+    two_phase = plans[0].describe()["pattern"] == "reduce_scatter_allgather"
+    red = [p.phase(0) for p in plans] if two_phase else plans
+    if two_phase:
+        Cc = edd // n                      # phase a reduces into (n, E_D/n):(1@gpuid, 1@m)
 
     def wire(sender, receiver):
-        p = plans[sender]
+        p = red[sender]
         s = src[sender].view(et)
         return np.array([s[p.map(0, receiver, k)[0]] for k in range(p.counts(receiver)[0])], et)
 
+    got = [enact_rank(red[r], r, n, K, Cc, dtype, lambda g: src[g], lambda q: wire(q, r)) for r in range(n)]
+    if two_phase:                          # phase b: a plain redistribution of the reduced shards
+        gat = [p.phase(1) for p in plans]
+        tmp = got
+        got = [synth.sentinel(synth.storage_cells(cfg["dst_st"]) * synth.DTYPE_SIZE[dtype], 5 + 2) for _ in range(n)]
+        for r in range(n):
+            d = got[r].view(et)
+            for k in range(gat[r].counts(r)[0]):
+                a, b = gat[r].map(2, r, k)
+                d[b] = tmp[r].view(et)[a]
+            for q in range(n):
+                if q != r:
+                    for k in range(gat[r].counts(q)[1]):
+                        d[gat[r].map(1, q, k)[0]] = tmp[q].view(et)[gat[q].map(0, r, k)[0]]
     for r in range(n):
-        got = enact_rank(plans[r], r, n, K, Cc, dtype, lambda g: src[g], lambda q: wire(q, r))
-        assert np.array_equal(got, exp[r]), r
+        assert np.array_equal(got[r], exp[r]), r
 
 
 # ------------------------------------------------------------------ world_size 2, gloo
