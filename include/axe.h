@@ -133,6 +133,30 @@ axe_status axe_layout_direct_sum(const axe_layout *A, const int64_t *S_A, const 
 axe_status axe_layout_slice(const axe_layout *layout, const int64_t *shape, int rank, const int64_t *begin,
                             const int64_t *extent, axe_layout **out);
 
+/* Textual form of the paper's matrix notation (Figures 2 and 5):
+ *   layout  := shard ( "+" replica )? ( "+" offset )*
+ *   shard   := "(" INT ("," INT)* "):(" stride ("," stride)* ")"
+ *   stride  := INT ("@" AXIS)?          (axis m by default)
+ *   replica := "[" shard "]"
+ *   offset  := INT "@" AXIS             (repeated axes add)
+ * Whitespace is insignificant.  Errors: AXE_ERR_INVALID_ARG with *error_pos (may
+ * be NULL) = the byte offset of the syntax error, or -1 for a semantic error
+ * (extent < 1, zero stride: Def. Iter); AXE_ERR_OVERFLOW. */
+axe_status axe_layout_parse(const char *text, axe_layout **out, int *error_pos);
+/* The layout in that grammar ("@m" omitted); parse(format(L)) is structurally L. */
+axe_status axe_layout_format(const axe_layout *layout, char *buf, int capacity);
+/* {"schema_version":1,"shard":[[e,s,"axis"],...],"replica":[...],"offset":{"axis":v},
+ *  "E_D":..,"E_R":..,"text":"<format>"} */
+axe_status axe_layout_to_json(const axe_layout *layout, char *buf, int capacity);
+/* Do a and b induce the same map (§3.3 "verify if they represent the same induced
+ * function")?  Both are canonicalized (App. A.1); when both canonical replica
+ * sets satisfy the gap condition the canonical form is unique and
+ * the answer is structural (D element-wise, R per axis as a multiset, O);
+ * otherwise f_a(x) and f_b(x) are compared as sets for every x when E_D * E_R
+ * <= threshold (< 0: 65536), else *result = -1 (undecidable).  *result = 1
+ * equivalent, 0 not (different E_D is never equivalent). */
+axe_status axe_layout_equivalent(const axe_layout *a, const axe_layout *b, int64_t threshold, int *result);
+
 /* ------------------------------------------------------------------------- */
 /* Storage descriptors (R16, R17)                                             */
 /* ------------------------------------------------------------------------- */

@@ -71,6 +71,10 @@ _SIGS = {
     "axe_layout_tile_of": ([_vp, _pi64, _vp, _pi64, C.c_int, C.POINTER(_vp), _pi64], C.c_int),
     "axe_layout_direct_sum": ([_vp, _pi64, _vp, _pi64, C.c_int, C.POINTER(_vp)], C.c_int),
     "axe_layout_slice": ([_vp, _pi64, C.c_int, _pi64, _pi64, C.POINTER(_vp)], C.c_int),
+    "axe_layout_parse": ([C.c_char_p, C.POINTER(_vp), C.POINTER(C.c_int)], C.c_int),
+    "axe_layout_format": ([_vp, C.c_char_p, C.c_int], C.c_int),
+    "axe_layout_to_json": ([_vp, C.c_char_p, C.c_int], C.c_int),
+    "axe_layout_equivalent": ([_vp, _vp, _i64, C.POINTER(C.c_int)], C.c_int),
     "axe_copy_plan_create": ([_vp, C.POINTER(axe_storage), _vp, C.POINTER(axe_storage), C.c_int, C.c_int,
                               C.POINTER(_vp)], C.c_int),
     "axe_copy_plan_execute": ([_vp, _vp, _vp, _vp], C.c_int),
@@ -315,6 +319,37 @@ class Layout:
         _check(_lib.axe_layout_direct_sum(self._h, self._shape(SA), Layout.of(B).handle, self._shape(SB), len(SA),
                                           C.byref(h)), "axe_layout_direct_sum")
         return Layout(_handle=h)
+
+    @classmethod
+    def parse(cls, text: str) -> "Layout":
+        """axe_layout_parse: "(e0,e1):(s0@a0,s1) + [(r):(t@b)] + o@c" (axis m by default)."""
+        h, pos = C.c_void_p(), C.c_int(-1)
+        code = _lib.axe_layout_parse(text.encode(), C.byref(h), C.byref(pos))
+        if code != AXE_OK:
+            err = AxeError(code, "axe_layout_parse")
+            err.pos = pos.value
+            raise err
+        return Layout(_handle=h)
+
+    def format(self) -> str:
+        buf = C.create_string_buffer(1 << 14)
+        _check(_lib.axe_layout_format(self._h, buf, len(buf)), "axe_layout_format")
+        return buf.value.decode()
+
+    def __str__(self):
+        return self.format()
+
+    def to_json(self) -> dict:
+        buf = C.create_string_buffer(1 << 15)
+        _check(_lib.axe_layout_to_json(self._h, buf, len(buf)), "axe_layout_to_json")
+        return json.loads(buf.value.decode())
+
+    def equivalent(self, other, threshold: int = -1):
+        """True / False, or None when undecidable (no gap condition and too large to enumerate)."""
+        r = C.c_int()
+        _check(_lib.axe_layout_equivalent(self._h, Layout.of(other).handle, threshold, C.byref(r)),
+               "axe_layout_equivalent")
+        return None if r.value < 0 else bool(r.value)
 
     def slice(self, S, begin, extent):
         """L[R:S] (Alg. 4 per block) for the region [begin, begin + extent)."""
