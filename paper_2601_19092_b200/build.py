@@ -10,8 +10,8 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libaxe.so")
-BUILD = os.path.join(ROOT, "build", "axe")
+OUT = os.environ.get("AXE_BUILD_OUT") or os.path.join(HERE, "libaxe.so")  # dev A/B variants only
+BUILD = os.path.join(ROOT, "build", "axe" + ("_" + os.path.basename(OUT) if os.environ.get("AXE_BUILD_OUT") else ""))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -46,6 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
               "-I", CSRC, "-I", os.path.join(nccl, "include")] + ARCH
     if os.environ.get("AXE_PTXAS_VERBOSE"):
         common += ["-Xptxas", "-v"]
+    common += os.environ.get("AXE_EXTRA_NVCC", "").split()  # dev A/B variants only
 
     def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")

@@ -109,6 +109,9 @@ __global__ void __launch_bounds__(256) k0_generic(const __grid_constant__ K0Para
 
 // ------------------------------------------------------------------ K1
 constexpr int K1_THREADS = 256;
+#ifndef AXE_K1_MINB
+#define AXE_K1_MINB 1
+#endif
 
 // ND > 0: digit count known at compile time; ND == 0: runtime p.nd (<= K1_MAXD)
 template <int ND>
@@ -180,7 +183,7 @@ __device__ __forceinline__ void decode_digits(int n, const FastDiv *fd, const in
 }
 
 template <int VB, int U>
-__global__ void __launch_bounds__(K1_THREADS) k1_tiled(const __grid_constant__ K1Params p, const uint8_t *__restrict__ src,
+__global__ void __launch_bounds__(K1_THREADS, AXE_K1_MINB) k1_tiled(const __grid_constant__ K1Params p, const uint8_t *__restrict__ src,
                                                        uint8_t *__restrict__ dst) {
   using T = typename VecT<VB>::T;
   int64_t so[U], dof[U];

@@ -23,10 +23,20 @@ __device__ __forceinline__ uint32_t movm_t(uint32_t a) {
   return d;
 }
 
+// One 512-byte block per warp per iteration at full occupancy (8 CTAs x 8 warps per SM, <= 32
+// registers): measured on config 3b (B200) U = 1: 1422 us, U = 2: 1565 us, U = 4: 1669-1703 us.
+// With U > 1 a warp's blocks lie a whole grid apart, so the loads in flight across the GPU
+// scatter over U distant DRAM regions; with U = 1 they form one contiguous front.
 constexpr int K3_WARPS = 8;
-constexpr int K3_U = 4;
+#ifndef AXE_K3_U
+#define AXE_K3_U 1
+#endif
+#ifndef AXE_K3_MINB
+#define AXE_K3_MINB 8
+#endif
+constexpr int K3_U = AXE_K3_U;
 
-__global__ void __launch_bounds__(K3_WARPS * 32) k3_movmatrix(const __grid_constant__ K3Params p,
+__global__ void __launch_bounds__(K3_WARPS * 32, AXE_K3_MINB) k3_movmatrix(const __grid_constant__ K3Params p,
                                                               const uint8_t *__restrict__ src,
                                                               uint8_t *__restrict__ dst) {
   if (p.dep) asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -79,6 +89,7 @@ __global__ void __launch_bounds__(K3_WARPS * 32) k3_movmatrix(const __grid_const
 }
 
 cudaError_t launch_k3(const K3Params &p, unsigned blocks, const void *src, void *dst, cudaStream_t st) {
+  blocks = one_wave((const void *)k3_movmatrix, K3_WARPS * 32, 0, blocks);
   cudaError_t e = launch_ex(k3_movmatrix, dim3(blocks), dim3(K3_WARPS * 32), 0, st, p, (const uint8_t *)src,
                             (uint8_t *)dst);
   if (e != cudaSuccess) return e;

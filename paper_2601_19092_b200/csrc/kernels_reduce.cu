@@ -227,15 +227,15 @@ cudaError_t launch_k4_dt(const K4Params &p, int vb, unsigned blocks, const uint8
   constexpr int ES = (int)sizeof(typename Op<DT>::S);
   const dim3 g(blocks), b(K4_THREADS);
   switch (vb / ES) {
-    case 1: return launch_ex(k4_reduce<DT, 1>, g, b, 0, st, p, s, d);
+    case 1: return launch_ex(k4_reduce<DT, 1>, dim3(one_wave((const void *)k4_reduce<DT, 1>, K4_THREADS, 0, blocks)), b, 0, st, p, s, d);
     case 2:
-      if constexpr (2 * ES <= 16) return launch_ex(k4_reduce<DT, 2>, g, b, 0, st, p, s, d);
+      if constexpr (2 * ES <= 16) return launch_ex(k4_reduce<DT, 2>, dim3(one_wave((const void *)k4_reduce<DT, 2>, K4_THREADS, 0, blocks)), b, 0, st, p, s, d);
       break;
     case 4:
-      if constexpr (4 * ES <= 16) return launch_ex(k4_reduce<DT, 4>, g, b, 0, st, p, s, d);
+      if constexpr (4 * ES <= 16) return launch_ex(k4_reduce<DT, 4>, dim3(one_wave((const void *)k4_reduce<DT, 4>, K4_THREADS, 0, blocks)), b, 0, st, p, s, d);
       break;
     case 8:
-      if constexpr (8 * ES <= 16) return launch_ex(k4_reduce<DT, 8>, g, b, 0, st, p, s, d);
+      if constexpr (8 * ES <= 16) return launch_ex(k4_reduce<DT, 8>, dim3(one_wave((const void *)k4_reduce<DT, 8>, K4_THREADS, 0, blocks)), b, 0, st, p, s, d);
       break;
   }
   return cudaErrorInvalidValue;

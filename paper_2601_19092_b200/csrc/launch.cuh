@@ -11,9 +11,35 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <mutex>
+#include <unordered_map>
 #include <utility>
 
 namespace axe {
+
+int num_sms();
+
+// Grid-stride kernels: a grid larger than (resident CTAs per SM) x SMs only adds a partial
+// second wave that runs at low occupancy at the end (e.g. 8 CTAs/SM requested, 6 resident:
+// 1.33 waves).  Cap the grid at exactly one full wave of the kernel's measured occupancy.
+inline unsigned one_wave(const void *kern, int threads, size_t smem, unsigned blocks) {
+  static std::mutex mu;
+  static std::unordered_map<const void *, int> occ;
+  int o = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = occ.find(kern);
+    if (it != occ.end()) {
+      o = it->second;
+    } else {
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem) != cudaSuccess) o = 0;
+      occ[kern] = o;
+    }
+  }
+  if (o <= 0) return blocks;
+  const unsigned cap = (unsigned)(o * num_sms());
+  return blocks > cap ? cap : blocks;
+}
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }

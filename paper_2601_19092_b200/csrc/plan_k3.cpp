@@ -13,6 +13,8 @@
 
 #include "plan.hpp"
 
+#include <cstdlib>
+
 namespace axe {
 
 Swz make_swz(const Storage &st);
@@ -95,8 +97,10 @@ bool build_k3(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
   k.ssw = make_swz(sst);
   k.dsw = make_swz(dstst);
   P->align = 16;
-  const int64_t per_cta = 8 * 4;  // warps x blocks per warp per iteration
-  P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nb + per_cta - 1) / per_cta, (int64_t)num_sms() * 8));
+  const int64_t per_cta = 8;  // warps x blocks per warp per iteration (AXE_K3_U = 1)
+  const char *ev = getenv("AXE_K3_PER_SM");  // CTAs per SM (tuning knob)
+  const int64_t per_sm = (ev && *ev) ? std::max(1, atoi(ev)) : 8;
+  P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nb + per_cta - 1) / per_cta, (int64_t)num_sms() * per_sm));
   P->covers_all = (int64_t)reps.size() * nb * BLK == dstst.cells;
   char b[256];
   snprintf(b, sizeof b,
