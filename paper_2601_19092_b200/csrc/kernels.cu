@@ -109,8 +109,18 @@ __global__ void __launch_bounds__(256) k0_generic(const __grid_constant__ K0Para
 
 // ------------------------------------------------------------------ K1
 constexpr int K1_THREADS = 256;
-#ifndef AXE_K1_MINB
-#define AXE_K1_MINB 1
+// AXE_K1_MINB (dev A/B only): a minimum-CTAs-per-SM register cap.  Left undefined, the
+// launch bounds carry no second argument -- an explicit 1 lets ptxas raise the register count.
+#ifdef AXE_K1_MINB
+#define AXE_K1_BOUNDS __launch_bounds__(K1_THREADS, AXE_K1_MINB)
+#else
+#define AXE_K1_BOUNDS __launch_bounds__(K1_THREADS)
+#endif
+#ifndef AXE_K1_U_BIG  // vectors per thread per tile, 8- and 16-byte vectors
+#define AXE_K1_U_BIG 4
+#endif
+#ifndef AXE_K1_U_SMALL  // vectors per thread per tile, <= 4-byte vectors
+#define AXE_K1_U_SMALL 8
 #endif
 
 // ND > 0: digit count known at compile time; ND == 0: runtime p.nd (<= K1_MAXD)
@@ -183,7 +193,7 @@ __device__ __forceinline__ void decode_digits(int n, const FastDiv *fd, const in
 }
 
 template <int VB, int U>
-__global__ void __launch_bounds__(K1_THREADS, AXE_K1_MINB) k1_tiled(const __grid_constant__ K1Params p, const uint8_t *__restrict__ src,
+__global__ void AXE_K1_BOUNDS k1_tiled(const __grid_constant__ K1Params p, const uint8_t *__restrict__ src,
                                                        uint8_t *__restrict__ dst) {
   using T = typename VecT<VB>::T;
   int64_t so[U], dof[U];
@@ -247,7 +257,7 @@ cudaError_t launch_k0(const K0Params &p, const void *src, void *dst, cudaStream_
 
 template <int ND, int VB>
 static cudaError_t k1_launch_nd(const K1Params &p, unsigned blocks, const uint8_t *s, uint8_t *d, cudaStream_t st) {
-  constexpr int U = VB >= 8 ? 4 : 8;
+  constexpr int U = VB >= 8 ? AXE_K1_U_BIG : AXE_K1_U_SMALL;
   return launch_ex(k1_vector<ND, VB, U>, dim3(blocks), dim3(K1_THREADS), 0, st, p, s, d);
 }
 
@@ -268,11 +278,11 @@ static cudaError_t k1_launch_vb(const K1Params &p, unsigned blocks, const uint8_
   }
 }
 
-int k1_unroll(int vb) { return vb >= 8 ? 4 : 8; }
+int k1_unroll(int vb) { return vb >= 8 ? AXE_K1_U_BIG : AXE_K1_U_SMALL; }
 
 template <int VB>
 static cudaError_t k1_tiled_launch(const K1Params &p, unsigned blocks, const uint8_t *s, uint8_t *d, cudaStream_t st) {
-  constexpr int U = VB >= 8 ? 4 : 8;
+  constexpr int U = VB >= 8 ? AXE_K1_U_BIG : AXE_K1_U_SMALL;
   return launch_ex(k1_tiled<VB, U>, dim3(blocks), dim3(K1_THREADS), 0, st, p, s, d);
 }
 

@@ -49,9 +49,16 @@ __device__ __forceinline__ typename K2Vec<B>::T ldg(const uint8_t *p) {
 }
 
 constexpr int K2_MAXLJ = 8;
+// AXE_K2_MINB (dev A/B only): a minimum-CTAs-per-SM register cap.  Left undefined, the
+// launch bounds carry no second argument -- an explicit 1 lets ptxas raise the register count.
+#ifdef AXE_K2_MINB
+#define AXE_K2_BOUNDS __launch_bounds__(K2_NT, AXE_K2_MINB)
+#else
+#define AXE_K2_BOUNDS __launch_bounds__(K2_NT)
+#endif
 
 template <int VS, int VD, int GB>
-__global__ void __launch_bounds__(K2_NT) k2_tile(const __grid_constant__ K2Params p, const uint8_t *__restrict__ src,
+__global__ void AXE_K2_BOUNDS k2_tile(const __grid_constant__ K2Params p, const uint8_t *__restrict__ src,
                                                  uint8_t *__restrict__ dst) {
   extern __shared__ __align__(128) uint8_t sm[];
   using TS = typename K2Vec<VS>::T;
