@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "launch.cuh"
@@ -57,7 +58,9 @@ constexpr int K2_MAXLJ = 8;
 #define AXE_K2_BOUNDS __launch_bounds__(K2_NT)
 #endif
 
-template <int VS, int VD, int GB>
+// LJ > 0: loads per thread known at compile time (only the LJ vectors live in registers);
+// LJ == 0: runtime p.lj <= K2_MAXLJ.
+template <int VS, int VD, int GB, int LJ>
 __global__ void AXE_K2_BOUNDS k2_tile(const __grid_constant__ K2Params p, const uint8_t *__restrict__ src,
                                                  uint8_t *__restrict__ dst) {
   extern __shared__ __align__(128) uint8_t sm[];
@@ -66,7 +69,12 @@ __global__ void AXE_K2_BOUNDS k2_tile(const __grid_constant__ K2Params p, const 
   using TG = typename K2Vec<GB>::T;
   constexpr int KG = VD / GB;
   const int t = threadIdx.x;
-  const int32_t al = p.A_l[t], as = p.A_s[t], ad = p.A_d[t];
+  // per-thread table entries: pinned in registers (an indexed constant load with 32 different
+  // addresses per warp serialises; ptxas would otherwise re-load them inside the tile loop)
+  int32_t al, as, ad;
+  asm volatile("mov.b32 %0, %3;\n\tmov.b32 %1, %4;\n\tmov.b32 %2, %5;"
+               : "=r"(al), "=r"(as), "=r"(ad)
+               : "r"(p.A_l[t]), "r"(p.A_s[t]), "r"(p.A_d[t]));
   if (p.dep) pdl_wait();
   pdl_launch_dependents();
   for (uint32_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
@@ -87,13 +95,15 @@ __global__ void AXE_K2_BOUNDS k2_tile(const __grid_constant__ K2Params p, const 
         db += (int64_t)i * p.ods[0];
       }
     }
-    TS v[K2_MAXLJ];
+    constexpr int NJ = LJ > 0 ? LJ : K2_MAXLJ;
+    TS v[NJ];
 #pragma unroll
-    for (int j = 0; j < K2_MAXLJ; j++)
-      if (j < p.lj) v[j] = ldg<VS>(src + swz(p.ssw, sb + p.B_l[j] + al));
+    for (int j = 0; j < NJ; j++)
+      if (LJ > 0 || j < p.lj) v[j] = ldg<VS>(src + swz(p.ssw, sb + p.B_l[j] + al));
+    asm volatile("" ::: "memory");  // every load is in flight before the first shared store waits on one
 #pragma unroll
-    for (int j = 0; j < K2_MAXLJ; j++)
-      if (j < p.lj) *reinterpret_cast<TS *>(sm + swz32(p.smsw, (uint32_t)((j * K2_NT + t) * VS))) = v[j];
+    for (int j = 0; j < NJ; j++)
+      if (LJ > 0 || j < p.lj) *reinterpret_cast<TS *>(sm + swz32(p.smsw, (uint32_t)((j * K2_NT + t) * VS))) = v[j];
     __syncthreads();
     for (int j = 0; j < p.sj; j++) {
       TD out;
@@ -108,15 +118,32 @@ __global__ void AXE_K2_BOUNDS k2_tile(const __grid_constant__ K2Params p, const 
   }
 }
 
-template <int VS, int VD, int GB>
-static cudaError_t k2_go(const K2Params &p, unsigned blocks, size_t smem, const void *s, void *d, cudaStream_t st) {
+template <int VS, int VD, int GB, int LJ>
+static cudaError_t k2_go_lj(const K2Params &p, unsigned blocks, size_t smem, const void *s, void *d, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k2_tile<VS, VD, GB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaError_t e =
+        cudaFuncSetAttribute(k2_tile<VS, VD, GB, LJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_ex(k2_tile<VS, VD, GB>, dim3(blocks), dim3(K2_NT), smem, st, p, (const uint8_t *)s, (uint8_t *)d);
+  return launch_ex(k2_tile<VS, VD, GB, LJ>, dim3(blocks), dim3(K2_NT), smem, st, p, (const uint8_t *)s,
+                   (uint8_t *)d);
+}
+
+template <int VS, int VD, int GB>
+static cudaError_t k2_go(const K2Params &p, unsigned blocks, size_t smem, const void *s, void *d, cudaStream_t st) {
+  static const bool lj_fixed = [] {
+    const char *e = getenv("AXE_K2_LJ");
+    return !(e && *e == '0');
+  }();
+  if constexpr (VS == 16 && VD == 16) {  // the transposes: fixed load counts
+    if (!lj_fixed) return k2_go_lj<VS, VD, GB, 0>(p, blocks, smem, s, d, st);
+    // measured (8192^2 transposes): fixed LJ = 4 (fp32, 16 KiB tiles) 121 -> 104 us; fixed LJ = 8
+    // (bf16, 32 KiB tiles) 52 -> 58 us, so 8 keeps the runtime form
+    if (p.lj == 4) return k2_go_lj<VS, VD, GB, 4>(p, blocks, smem, s, d, st);
+  }
+  return k2_go_lj<VS, VD, GB, 0>(p, blocks, smem, s, d, st);
 }
 
 template <int VS, int VD>

@@ -15,6 +15,8 @@
 
 #include "plan.hpp"
 
+#include <cstdlib>
+
 namespace axe {
 
 Swz make_swz(const Storage &st);
@@ -157,7 +159,8 @@ bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
     }
     return L;
   };
-  const int64_t budget = 32768 / es;  // tile elements (32 KiB)
+  int64_t budget = 32768 / es;  // tile elements (32 KiB)
+  if (const char *ev = getenv("AXE_K2_TILE_BYTES")) budget = std::max<int64_t>(1024, atoll(ev)) / es;  // tuning knob
   const int NT = K2_NT;
   struct Choice {
     int64_t Ls, Ld, TE, Vs, Vd;
@@ -328,6 +331,7 @@ bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
   P->k2_gb = GBB;
   P->align = 16;
   int per_sm = std::max(1, std::min(8, (int)(200 * 1024 / (TE * es + 1024))));
+  if (const char *ev = getenv("AXE_K2_PER_SM")) per_sm = std::max(1, atoi(ev));  // tuning knob
   P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(k.ntiles, (int64_t)num_sms() * per_sm));
   int64_t total = 1;
   for (auto &j : J) total *= j.e;
