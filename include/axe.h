@@ -133,6 +133,36 @@ axe_status axe_layout_direct_sum(const axe_layout *A, const int64_t *S_A, const 
 axe_status axe_layout_slice(const axe_layout *layout, const int64_t *shape, int rank, const int64_t *begin,
                             const int64_t *extent, axe_layout **out);
 
+/* The paper's TMA lowering (§3.4): copy the region [begin, begin +
+ * extent) of a global tensor (layout LG, logical shape EG; begin = NULL: all of
+ * it) into a shared-memory tensor (layout LS, shape ES = the region's shape),
+ * with the hardware swizzle of swizzle_bytes in {32, 64, 128}.  Steps: slice
+ * (Alg. 4); the atom E_{d,a} = (1, .., 1, 8, swizzle_bytes / elem_size) and the
+ * tiler T with LS = T (x) atom (Alg. 1 grouping + Alg. 3 matching, reading R26);
+ * the atom's global counterpart as a suffix product of each group of the
+ * grouped LG.  Layouts must be on the memory axis m, without replicas; strides
+ * and offsets in elements.  *out receives the CuTensorMap encoding (dims and
+ * byte strides innermost first, the atom box, the logical dimension of each
+ * tensor-map dimension, the region's byte offset), the
+ * atom count |T| and fused_rows (rows one box may cover when consecutive atoms
+ * stack along rows in both memories, <= 256); *tiler (may be NULL) receives T.
+ * Errors: AXE_ERR_UNSUPPORTED (no tiling / suffix product / > 5 dimensions /
+ * non-contiguous innermost), AXE_ERR_SIZE_MISMATCH, AXE_ERR_ALIGNMENT. */
+typedef struct {
+  int rank;
+  uint64_t dims[5];
+  uint64_t strides[5]; /* bytes; strides[0] = elem_size */
+  uint32_t box[5];
+  int logical_dim[5];  /* the logical dimension (of EG) each tensor-map dimension belongs to */
+  int swizzle_bytes;
+  int64_t base_bytes;
+  int64_t atoms;
+  uint32_t fused_rows;
+} axe_tma_desc;
+axe_status axe_tma_lower(const axe_layout *LG, const int64_t *EG, const int64_t *begin, const int64_t *extent,
+                         const axe_layout *LS, const int64_t *ES, int rank, int elem_size, int swizzle_bytes,
+                         axe_tma_desc *out, axe_layout **tiler);
+
 /* Textual form of the paper's matrix notation (Figures 2 and 5):
  *   layout  := shard ( "+" replica )? ( "+" offset )*
  *   shard   := "(" INT ("," INT)* "):(" stride ("," stride)* ")"

@@ -45,6 +45,12 @@ class axe_storage_digit(C.Structure):
     _fields_ = [("axis", C.c_char_p), ("extent", C.c_int64), ("divisor", C.c_int64)]
 
 
+class axe_tma_desc(C.Structure):
+    _fields_ = [("rank", C.c_int), ("dims", C.c_uint64 * 5), ("strides", C.c_uint64 * 5), ("box", C.c_uint32 * 5),
+                ("logical_dim", C.c_int * 5), ("swizzle_bytes", C.c_int), ("base_bytes", C.c_int64), ("atoms", C.c_int64),
+                ("fused_rows", C.c_uint32)]
+
+
 class axe_storage(C.Structure):
     _fields_ = [("n", C.c_int), ("digits", C.POINTER(axe_storage_digit)), ("swz_bits", C.c_int),
                 ("swz_base", C.c_int), ("swz_shift", C.c_int)]
@@ -75,6 +81,8 @@ _SIGS = {
     "axe_layout_format": ([_vp, C.c_char_p, C.c_int], C.c_int),
     "axe_layout_to_json": ([_vp, C.c_char_p, C.c_int], C.c_int),
     "axe_layout_equivalent": ([_vp, _vp, _i64, C.POINTER(C.c_int)], C.c_int),
+    "axe_tma_lower": ([_vp, _pi64, _pi64, _pi64, _vp, _pi64, C.c_int, C.c_int, C.c_int, C.POINTER(axe_tma_desc),
+                       C.POINTER(_vp)], C.c_int),
     "axe_copy_plan_create": ([_vp, C.POINTER(axe_storage), _vp, C.POINTER(axe_storage), C.c_int, C.c_int,
                               C.POINTER(_vp)], C.c_int),
     "axe_copy_plan_execute": ([_vp, _vp, _vp, _vp], C.c_int),
@@ -577,6 +585,22 @@ def redist_emulate(plans, src_locals, dst_locals, stream=None):
     sp = (C.c_void_p * n)(*[_ptr(x) for x in src_locals])
     dp = (C.c_void_p * n)(*[_ptr(x) for x in dst_locals])
     _check(_lib.axe_redist_emulate(hp, n, sp, dp, _stream(stream)), "axe_redist_emulate")
+
+
+def tma_lower(LG, EG, LS, ES, elem_size: int, swizzle_bytes: int, begin=None, extent=None) -> dict:
+    """axe_tma_lower: the paper's TMA lowering -> CuTensorMap encoding + the atom tiler T."""
+    G, S = Layout.of(LG), Layout.of(LS)
+    r = len(EG)
+    arr = lambda v: (C.c_int64 * r)(*v) if v is not None else None
+    d = axe_tma_desc()
+    t = C.c_void_p()
+    _check(_lib.axe_tma_lower(G.handle, arr(EG), arr(begin), arr(extent), S.handle, arr(ES), r, elem_size,
+                              swizzle_bytes, C.byref(d), C.byref(t)), "axe_tma_lower")
+    n = d.rank
+    return {"rank": n, "dims": list(d.dims[:n]), "strides": list(d.strides[:n]), "box": list(d.box[:n]),
+            "logical_dim": list(d.logical_dim[:n]),
+            "swizzle_bytes": d.swizzle_bytes, "base_bytes": d.base_bytes, "atoms": d.atoms,
+            "fused_rows": d.fused_rows, "tiler": Layout(_handle=t)}
 
 
 def axe_layout_create(D, R=(), O=None) -> Layout:

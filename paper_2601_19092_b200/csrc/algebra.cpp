@@ -325,3 +325,178 @@ axe_status axe_layout_slice(const axe_layout *L, const int64_t *S, int rank, con
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// The paper's TMA lowering (§3.4 "TMA asynchronous copy"), on the
+// algebra above: (1) slice the global view L_G[R_G : E_G] (Alg. 4); (2) the
+// swizzle atom E_{d,a} = (1, .., 1, 8, a / sizeof(d)) (reading R14: rank equal to
+// E_S's) and the tiler T with (L_S)||E_S = T||E_o (x) (L_{d,a})||E_{d,a}: L_S is
+// grouped by the interleaved shape (E_o[0], E_{d,a}[0], ...) (Alg. 1, splitting
+// iters) and every inner block must equal the atom's block (Alg. 3's EqualIter);
+// the outer blocks, divided by the atom's span, are T (reading R26); (3) the
+// atom's global counterpart is a suffix product of the iters of each group of
+// (L_G)||E_G -- at most one iter split (Lemma split) -- and the iters of the
+// grouped L_G become the CuTensorMap dimensions (innermost first), the box
+// covering exactly the atom's iters.
+// ---------------------------------------------------------------------------
+extern "C" {
+
+axe_status axe_tma_lower(const axe_layout *LG, const int64_t *EG, const int64_t *begin, const int64_t *extent,
+                         const axe_layout *LS, const int64_t *ES, int rank, int elem_size, int swizzle_bytes,
+                         axe_tma_desc *out, axe_layout **tiler) {
+  if (!LG || !EG || !LS || !ES || !out || rank < 2 || rank > 5) AXE_FAIL(AXE_ERR_INVALID_ARG, "bad argument (rank 2..5)");
+  if (tiler) *tiler = nullptr;
+  memset(out, 0, sizeof(*out));
+  const int es = elem_size;
+  if (es != 1 && es != 2 && es != 4 && es != 8 && es != 16) AXE_FAIL(AXE_ERR_ALIGNMENT, "elem_size %d", es);
+  if (swizzle_bytes != 32 && swizzle_bytes != 64 && swizzle_bytes != 128)
+    AXE_FAIL(AXE_ERR_INVALID_ARG, "swizzle mode %d B is not 32 / 64 / 128 (P:527)", swizzle_bytes);
+  const int m = axis_m();
+  for (const axe_layout *L : {LG, LS}) {
+    if (!L->L.R.empty()) AXE_FAIL(AXE_ERR_UNSUPPORTED, "tma: replicated layouts are not a TMA box");
+    for (auto &it : L->L.D)
+      if (it.a != m) AXE_FAIL(AXE_ERR_UNSUPPORTED_AXIS, "tma: every iter must be on the memory axis m");
+    for (auto &o : L->L.O)
+      if (o.first != m) AXE_FAIL(AXE_ERR_UNSUPPORTED_AXIS, "tma: offsets must be on the memory axis m");
+  }
+  if (LS->L.offset(m)) AXE_FAIL(AXE_ERR_UNSUPPORTED, "tma: the shared-memory tensor starts at its base");
+  // (1) slice view of the global tensor
+  axe_layout *Gs = nullptr;
+  std::vector<int64_t> E(EG, EG + rank);
+  if (begin) {
+    if (!extent) AXE_FAIL(AXE_ERR_INVALID_ARG, "begin without extent");
+    AXE_TRY(axe_layout_slice(LG, EG, rank, begin, extent, &Gs));
+    E.assign(extent, extent + rank);
+  }
+  std::unique_ptr<axe_layout, void (*)(axe_layout *)> Gown(Gs, [](axe_layout *p) { delete p; });
+  const Layout &G = Gs ? Gs->L : LG->L;
+  for (int j = 0; j < rank; j++)
+    if (E[j] != ES[j]) AXE_FAIL(AXE_ERR_SIZE_MISMATCH, "region shape differs from E_S in dimension %d", j);
+  // (2) the swizzle atom and the tiler T
+  const int64_t inner = swizzle_bytes / es;
+  if (inner < 1) AXE_FAIL(AXE_ERR_UNSUPPORTED, "tma: element wider than the swizzle span");
+  std::vector<int64_t> Ea(rank, 1), Eo(rank), I;
+  Ea[rank - 1] = inner;
+  Ea[rank - 2] = 8;
+  for (int j = 0; j < rank; j++) {
+    if (ES[j] % Ea[j]) AXE_FAIL(AXE_ERR_UNSUPPORTED, "tma: atom extent %lld does not divide E_S[%d]", (long long)Ea[j], j);
+    Eo[j] = ES[j] / Ea[j];
+    I.push_back(Eo[j]);
+    I.push_back(Ea[j]);
+  }
+  std::vector<Iter> DS, DA;
+  std::vector<int> bS, bA;
+  AXE_TRY(group_by_shape(normalize_shard(LS->L.D), I, &DS, &bS));
+  const std::vector<Iter> atom{Iter{8, inner, m}, Iter{inner, 1, m}};
+  AXE_TRY(group_by_shape(normalize_shard(atom), Ea, &DA, &bA));
+  const int64_t W = 8 * inner;  // span of the atom on m
+  std::vector<Iter> DT;
+  for (int j = 0; j < rank; j++) {
+    std::vector<Iter> in(DS.begin() + bS[2 * j + 1], DS.begin() + bS[2 * j + 2]);
+    std::vector<Iter> at(DA.begin() + bA[j], DA.begin() + bA[j + 1]);
+    in = normalize_shard(in);
+    at = normalize_shard(at);
+    if (in.size() == 1 && in[0].e == 1) in.clear();
+    if (at.size() == 1 && at[0].e == 1) at.clear();
+    bool eq = in.size() == at.size();
+    for (size_t k = 0; eq && k < in.size(); k++) eq = in[k].e == at[k].e && in[k].s == at[k].s;
+    if (!eq) AXE_FAIL(AXE_ERR_UNSUPPORTED, "tma: L_S is not a tiling of the %d-byte swizzle atom (dimension %d)", swizzle_bytes, j);
+    for (int k = bS[2 * j]; k < bS[2 * j + 1]; k++) {
+      if (DS[k].s % W) AXE_FAIL(AXE_ERR_UNSUPPORTED, "tma: atom-grid stride %lld is not a multiple of the atom span", (long long)DS[k].s);
+      DT.push_back(Iter{DS[k].e, DS[k].s / W, m});
+    }
+  }
+  // (3) the tensor map from the grouped global layout
+  std::vector<Iter> DG;
+  std::vector<int> bG;
+  AXE_TRY(group_by_shape(G.D, E, &DG, &bG));
+  struct Dim {
+    int64_t e, s;
+    bool box;
+    int j;  // logical dimension
+  };
+  std::vector<Dim> dims;  // innermost first
+  for (int j = rank - 1; j >= 0; j--) {
+    std::vector<Iter> blk(DG.begin() + bG[j], DG.begin() + bG[j + 1]);
+    int64_t p = 1;
+    int k = (int)blk.size() - 1;
+    for (; k >= 0 && p < Ea[j]; k--) {
+      const int64_t need = Ea[j] / p;
+      if (Ea[j] % p) break;
+      if (blk[k].e <= need && need % blk[k].e == 0) {
+        dims.push_back(Dim{blk[k].e, blk[k].s, true, j});
+        p *= blk[k].e;
+      } else if (blk[k].e % need == 0) {  // split: inner `need` in the box, the rest outside (Lemma split)
+        dims.push_back(Dim{need, blk[k].s, true, j});
+        blk[k] = Iter{blk[k].e / need, blk[k].s * need, blk[k].a};
+        p *= need;
+        break;  // (no decrement: the outer part blk[k] is pushed next as a non-box iter)
+      } else {
+        break;
+      }
+    }
+    if (p != Ea[j])
+      AXE_FAIL(AXE_ERR_UNSUPPORTED, "tma: atom extent %lld is not a suffix product of group %d of L_G", (long long)Ea[j], j);
+    for (; k >= 0; k--)
+      if (blk[k].e > 1) dims.push_back(Dim{blk[k].e, blk[k].s, false, j});
+  }
+  if (dims.empty() || !dims[0].box || dims[0].s != 1)
+    AXE_FAIL(AXE_ERR_UNSUPPORTED, "tma: the innermost box dimension must be contiguous (stride 1)");
+  // fuse neighbours that continue one another with the same box status (fewer tensor-map dims)
+  std::vector<Dim> fz;
+  for (auto &d : dims) {
+    if (d.e == 1 && !d.box) continue;
+    if (!fz.empty() && fz.back().box == d.box && fz.back().j == d.j && d.s == fz.back().s * fz.back().e &&
+        (!d.box || fz.size() == 1))
+      fz.back().e *= d.e;
+    else
+      fz.push_back(d);
+  }
+  if (fz.size() > 5) AXE_FAIL(AXE_ERR_UNSUPPORTED, "tma: %zu tensor-map dimensions (max 5)", fz.size());
+  out->rank = (int)fz.size();
+  for (size_t i = 0; i < fz.size(); i++) {
+    out->dims[i] = (uint64_t)fz[i].e;
+    out->strides[i] = (uint64_t)(fz[i].s * es);
+    out->box[i] = (uint32_t)(fz[i].box ? fz[i].e : 1);
+    out->logical_dim[i] = fz[i].j;
+    if (fz[i].s < 0) AXE_FAIL(AXE_ERR_UNSUPPORTED, "tma: negative global stride");
+    if (i > 0 && (fz[i].s * es) % 16) AXE_FAIL(AXE_ERR_ALIGNMENT, "tma: global stride %lld B is not a multiple of 16", (long long)(fz[i].s * es));
+    if (out->box[i] > 256) AXE_FAIL(AXE_ERR_UNSUPPORTED, "tma: box dimension > 256");
+  }
+  out->swizzle_bytes = swizzle_bytes;
+  out->base_bytes = G.offset(m) * es;
+  int64_t atoms = 1;
+  for (auto &t : DT) atoms *= t.e;
+  out->atoms = atoms;
+  // atoms that stack along the row dimension in both memories can share one box: T's innermost
+  // row-dimension iter with unit (atom) stride, and the global rows continuing past the atom
+  out->fused_rows = 8;
+  {
+    std::vector<Iter> trow(DS.begin() + bS[2 * (rank - 2)], DS.begin() + bS[2 * (rank - 2) + 1]);
+    trow = normalize_shard(trow);
+    int64_t f = 1;
+    if (!trow.empty() && trow.back().s == W) f = trow.back().e;
+    // the global row iter just outside the box (stride = 8 rows) must hold at least f atoms
+    int64_t rows_out = 0;
+    for (size_t i = 0; i < dims.size(); i++)
+      if (!dims[i].box && i > 0 && dims[i - 1].box && dims[i].s == dims[i - 1].s * dims[i - 1].e) {
+        rows_out = dims[i].e;
+        break;
+      }
+    while (f > 1 && (8 * f > 256 || rows_out % f)) f /= 2;
+    if (rows_out > 0) out->fused_rows = (uint32_t)(8 * f);
+  }
+  if (tiler) {
+    if (DT.empty()) DT.push_back(Iter{1, 1, m});
+    auto *h = new axe_layout;
+    axe_status st = make_layout(DT, {}, {}, &h->L);
+    if (st != AXE_OK) {
+      delete h;
+      return st;
+    }
+    *tiler = h;
+  }
+  return AXE_OK;
+}
+
+}  // extern "C"

@@ -584,7 +584,15 @@ static bool build_tma(const std::vector<Joint> &J0, const Linear &ls, const Line
            "\"blocks\":%u,\"swizzle\":%d,\"replicas\":%d,\"joint\":",
            mode == 0 ? "tensor-load/bulk-store" : "bulk-load/tensor-store", (long long)B1, (long long)row_bytes,
            (long long)box_bytes, (long long)nboxes, stages, P->blocks, span, k.nrep);
-  P->desc = std::string(b) + joint_json(J0) + "}";
+  // the encoded tensor map (byte elements): dims / byte strides innermost first, box
+  std::string tm = ",\"tensor_map\":{\"dims\":[";
+  for (int i = 0; i < 5; i++) tm += (i ? "," : "") + std::to_string(P->tm_dims[i]);
+  tm += "],\"strides\":[1";
+  for (int i = 0; i < 4; i++) tm += "," + std::to_string(P->tm_strides[i]);
+  tm += "],\"box\":[";
+  for (int i = 0; i < 5; i++) tm += (i ? "," : "") + std::to_string(P->tm_box[i]);
+  tm += "],\"base\":" + std::to_string(P->tm_base) + "}";
+  P->desc = std::string(b) + joint_json(J0) + tm + "}";
   return true;
 }
 
