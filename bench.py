@@ -422,19 +422,35 @@ def run_axe(args):
     ms_step = ms / args.steps
     value = ws * alg_bytes / (ms_step * 1e-3) / 1e9
 
-    # end to end through the public host-buffer call: H2D of the inputs + kernel + D2H of the result
-    hs = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
-    hs.copy_(srcs[0].view(torch.uint8).cpu())
-    hd = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    # end to end through the public host-buffer call: H2D of the inputs + kernel + D2H of the result.
+    # Like a serving loop, consecutive steps alternate E2E_STREAMS user streams and host / device buffer
+    # sets, so step k+1's host->device copies overlap step k's device->host copies on the PCIe link
+    # (stream order alone would serialise the two directions across steps).
+    ns = max(1, int(os.environ.get("AXE_E2E_STREAMS", "2")))
+    # the same copy, planned with 2 host slabs of 16 MiB (measured best with 2 overlapping streams:
+    # 91 GB/s vs 86 (4 slabs) and 81 (8 slabs); PCIe moves large transfers more efficiently)
+    slabs = int(os.environ.get("AXE_E2E_SLABS", "2"))
+    eplan = axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], es, host_slabs=slabs)
+    hs = [torch.empty(nbytes, dtype=torch.uint8).pin_memory() for _ in range(ns)]
+    for h in hs:
+        h.copy_(srcs[0].view(torch.uint8).cpu())
+    hd = [torch.empty(nbytes, dtype=torch.uint8).pin_memory() for _ in range(ns)]
+    e_streams = [stream] + [torch.cuda.Stream() for _ in range(ns - 1)]
     e_steps = max(5, min(50, args.steps))
-    for i in range(2):
-        plan.execute_host(hs, hd, srcs[0], dsts[0], stream)
+    for i in range(2 * ns):
+        eplan.execute_host(hs[i % ns], hd[i % ns], srcs[i % pairs], dsts[i % pairs], e_streams[i % ns])
+    for s_ in e_streams:
+        s_.synchronize()
     barrier()
     t0 = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    for s_ in e_streams[1:]:
+        s_.wait_event(e0)
     for i in range(e_steps):
-        plan.execute_host(hs, hd, srcs[i % pairs], dsts[i % pairs], stream)
+        eplan.execute_host(hs[i % ns], hd[i % ns], srcs[i % pairs], dsts[i % pairs], e_streams[i % ns])
+    for s_ in e_streams[1:]:
+        stream.wait_stream(s_)
     e1.record(stream)
     barrier()
     e_ms = e0.elapsed_time(e1) / e_steps
@@ -486,7 +502,9 @@ def run_axe(args):
                          if graph is not None else "CUDA events over the timed region / launches"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-                    "api": "axe_copy_plan_execute_host (pinned host buffers)", "ms_per_step": e_ms},
+                    "api": "axe_copy_plan_execute_host (pinned host buffers)", "ms_per_step": e_ms,
+                    "streams": ns, "host_slabs": slabs,
+                    "pcie_note": "steps alternate user streams so H2D and D2H overlap"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }

@@ -249,6 +249,14 @@ axe_status axe_copy_plan_create(const axe_layout *src, const axe_storage *src_st
  * pointers are not aligned to the plan's vector width), AXE_ERR_ALIAS,
  * AXE_ERR_CUDA.  Launch count: 1 kernel. */
 axe_status axe_copy_plan_execute(const axe_copy_plan *plan, const void *src_ptr, void *dst_ptr, void *cuda_stream);
+/* As axe_copy_plan_create, with the host pipeline of axe_copy_plan_execute_host
+ * cut into at most host_slabs slabs (0: the default, 8 or AXE_HOST_CHUNKS).
+ * Fewer, larger slabs move PCIe data more efficiently when the caller overlaps
+ * consecutive calls on different streams; more slabs overlap the two
+ * directions within one call. */
+axe_status axe_copy_plan_create_ex(const axe_layout *src, const axe_storage *src_st, const axe_layout *dst,
+                                   const axe_storage *dst_st, int elem_size, int kernel, int host_slabs,
+                                   axe_copy_plan **out);
 /* End-to-end variant: src/dst are HOST buffers (pinned for async overlap),
  * staged through the caller's device buffers dev_src / dev_dst (storage sizes)
  * with cudaMemcpyAsync: H2D, copy kernel, D2H, all on cuda_stream.  Asynchronous

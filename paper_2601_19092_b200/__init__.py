@@ -85,6 +85,8 @@ _SIGS = {
                        C.POINTER(_vp)], C.c_int),
     "axe_copy_plan_create": ([_vp, C.POINTER(axe_storage), _vp, C.POINTER(axe_storage), C.c_int, C.c_int,
                               C.POINTER(_vp)], C.c_int),
+    "axe_copy_plan_create_ex": ([_vp, C.POINTER(axe_storage), _vp, C.POINTER(axe_storage), C.c_int, C.c_int, C.c_int,
+                                 C.POINTER(_vp)], C.c_int),
     "axe_copy_plan_execute": ([_vp, _vp, _vp, _vp], C.c_int),
     "axe_copy_plan_execute_host": ([_vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "axe_copy_plan_sizes": ([_vp, _pi64, _pi64], C.c_int),
@@ -371,13 +373,18 @@ class Layout:
 class CopyPlan:
     """axe_copy_plan_create / _execute / _describe (include/axe.h)."""
 
-    def __init__(self, src, src_st, dst, dst_st, elem_size: int, kernel: str = "auto"):
+    def __init__(self, src, src_st, dst, dst_st, elem_size: int, kernel: str = "auto", host_slabs: int = 0):
         self.src, self.dst = Layout.of(src), Layout.of(dst)
         ss, k1 = make_storage(src_st)
         ds, k2 = make_storage(dst_st)
         h = C.c_void_p()
-        _check(_lib.axe_copy_plan_create(self.src.handle, C.byref(ss), self.dst.handle, C.byref(ds), elem_size,
-                                         KERNELS[kernel], C.byref(h)), "axe_copy_plan_create")
+        if host_slabs:
+            _check(_lib.axe_copy_plan_create_ex(self.src.handle, C.byref(ss), self.dst.handle, C.byref(ds),
+                                                elem_size, KERNELS[kernel], host_slabs, C.byref(h)),
+                   "axe_copy_plan_create_ex")
+        else:
+            _check(_lib.axe_copy_plan_create(self.src.handle, C.byref(ss), self.dst.handle, C.byref(ds), elem_size,
+                                             KERNELS[kernel], C.byref(h)), "axe_copy_plan_create")
         self._h = h
         self.elem_size = elem_size
 

@@ -127,14 +127,32 @@ axe_status axe_layout_bounds(const axe_layout *l, const char *axis, int64_t *mn,
 
 // ------------------------------------------------------------------ copy
 static axe_status plan_create(const axe_layout *src, const axe_storage *src_st, const axe_layout *dst,
-                              const axe_storage *dst_st, int elem_size, int kernel, int max_align, CopyPlan *P) {
+                              const axe_storage *dst_st, int elem_size, int kernel, int max_align, CopyPlan *P,
+                              int host_slabs = 0) {
   CHECK_NULL(src, "src layout");
   CHECK_NULL(dst, "dst layout");
   Storage ss, ds;
   AXE_TRY(make_storage(src_st, &ss));
   AXE_TRY(make_storage(dst_st, &ds));
   PlanRequest rq{&src->L, &dst->L, &ss, &ds, elem_size, kernel, max_align, -1};
+  rq.host_slabs = host_slabs;
   return plan_copy(rq, P);
+}
+
+axe_status axe_copy_plan_create_ex(const axe_layout *src, const axe_storage *src_st, const axe_layout *dst,
+                                   const axe_storage *dst_st, int elem_size, int kernel, int host_slabs,
+                                   axe_copy_plan **out) {
+  CHECK_NULL(out, "out");
+  *out = nullptr;
+  if (host_slabs < 0) AXE_FAIL(AXE_ERR_INVALID_ARG, "host_slabs must be >= 0");
+  auto *h = new axe_copy_plan;
+  axe_status st = plan_create(src, src_st, dst, dst_st, elem_size, kernel, 16, &h->P, host_slabs);
+  if (st != AXE_OK) {
+    delete h;
+    return st;
+  }
+  *out = h;
+  return AXE_OK;
 }
 
 axe_status axe_copy_plan_create(const axe_layout *src, const axe_storage *src_st, const axe_layout *dst,

@@ -632,7 +632,7 @@ axe_status plan_chunks(const PlanRequest &rq, const std::vector<Joint> &J, const
   const Joint cj = J[best];
   // up to AXE_HOST_CHUNKS (8, measured best of 4..32) slabs of >= 1 MiB, each a whole number of swizzle blocks on both sides
   int n = 1;
-  const int64_t max_ch = env_int("AXE_HOST_CHUNKS", 8);
+  const int64_t max_ch = rq.host_slabs > 0 ? rq.host_slabs : env_int("AXE_HOST_CHUNKS", 8);
   for (int c = 2; c <= 32; c++) {
     if (cj.e % c) continue;
     int64_t sb = sc / c * es, db = dc / c * es;

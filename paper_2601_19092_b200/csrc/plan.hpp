@@ -90,6 +90,7 @@ struct PlanRequest {
   int max_align;         // pointer alignment known to hold (bytes, power of 2, <= 16)
   int skip_axis;         // -1 for copy; gpuid id for redistribute pieces
   int no_chunk = 0;      // do not build the host-pipeline slab plan
+  int host_slabs = 0;    // > 0: at most this many host-pipeline slabs (else AXE_HOST_CHUNKS, default 8)
 };
 
 void stream_forget(cudaStream_t st);

@@ -359,3 +359,30 @@ def test_execute_host_pipelined(axe, case):
         plan.execute_host(hs, hd, ds, dd)
     torch.cuda.synchronize()
     assert np.array_equal(hd.numpy(), exp)
+
+
+@pytest.mark.parametrize("slabs", [2, 4])
+def test_execute_host_alternating_streams(axe, slabs):
+    """The serving pattern bench.py's e2e uses: consecutive execute_host calls of one plan (host_slabs set
+    through axe_copy_plan_create_ex) on two user streams with two host / device buffer sets, so one call's
+    host->device copies overlap the previous call's device->host copies.  Every call's result is exact."""
+    cfg = synth.config2()
+    src, d_fill, exp = prepare(cfg)
+    plan = axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], 2, host_slabs=slabs)
+    assert plan.describe()["host_chunks"] == slabs
+    srcs = [src, np.ascontiguousarray(src[::-1])]       # a second, different input
+    exps = [exp]
+    e2 = d_fill.copy()
+    oracle.copy(cfg["src"], cfg["src_st"], srcs[1], cfg["dst"], cfg["dst_st"], e2, 2)
+    exps.append(e2)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    hs = [torch.from_numpy(s).pin_memory() for s in srcs]
+    hd = [torch.from_numpy(d_fill.copy()).pin_memory() for _ in range(2)]
+    ds = [torch.empty(src.nbytes, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    dd = [torch.empty(d_fill.nbytes, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    for i in range(6):
+        k = i % 2
+        plan.execute_host(hs[k], hd[k], ds[k], dd[k], streams[k])
+    torch.cuda.synchronize()
+    for k in range(2):
+        assert np.array_equal(hd[k].numpy(), exps[k])
