@@ -262,6 +262,25 @@ def measure_reshard_p2p(axe, torch, dist, ws, rank, local, stream, timed):
         out[name] = {"ms": ms, "ingress_bytes_per_gpu": ingress, "bus_GBps": ingress / (ms * 1e-3) / 1e9,
                      "frac_of_900": ingress / (ms * 1e-3) / 1e9 / 900}
         del buf, hdl, src
+    # §8(f) f2+f3: pull reduce-scatter -- one K4 kernel per rank reads every partial from its owner's
+    # symmetric buffer over NVLink and writes the sum (no staging, no NCCL)
+    rs = synth.reduce_scatter(ws, 16384, 8192, "bf16")
+    plan = axe.RedistPlan(rs["src"], rs["src_st"], rs["dst"], rs["dst_st"], 2, ws, rank, reduce_dtype="bf16")
+    sbuf = symm_mem.empty(synth.storage_cells(rs["src_st"]), dtype=torch.bfloat16, device=f"cuda:{local}")
+    sbuf.normal_()
+    hdl = symm_mem.rendezvous(sbuf, dist.group.WORLD)
+    peers = [int(p) for p in hdl.buffer_ptrs]
+    dst = torch.empty(synth.storage_cells(rs["dst_st"]), dtype=torch.bfloat16, device="cuda")
+
+    def fn_rs():
+        hdl.barrier(channel=0)
+        plan.execute_peers_reduce(peers, dst, stream)
+        hdl.barrier(channel=0)
+    ms = timed(fn_rs)
+    bus = (ws - 1) / ws * sbuf.numel() * 2
+    out["reduce_scatter_pull"] = {"ms": ms, "bus_bytes_per_gpu": bus, "bus_GBps": bus / (ms * 1e-3) / 1e9,
+                                  "pull_regions": plan.describe()["pull_regions"]}
+    del sbuf, hdl, dst
     return out
 
 

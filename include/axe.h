@@ -403,6 +403,18 @@ axe_status axe_reduce(const axe_layout *src, const axe_storage *src_st, const vo
 axe_status axe_redist_reduce_plan_create(const axe_layout *src, const axe_storage *src_st, const axe_layout *dst,
                                          const axe_storage *dst_st, int dtype, int nranks, int rank,
                                          axe_redist_plan **out);
+/* One-sided pull form of a single-phase reduction plan (SURVEY §8(f) f2 + f3):
+ * src_peers[r] is rank r's source buffer mapped into this process (peer memory
+ * over NVLink: torch symmetric memory / CUDA IPC; src_peers[rank] = this rank's
+ * own).  Each destination region is ONE kernel that reads its K partials
+ * straight from the owners' buffers and writes the sum into dst_local -- the
+ * exchange, the staging and the sum fused.  The caller orders it across ranks
+ * (every src ready before: a barrier; no src reuse until every rank finished:
+ * a barrier after).  AXE_ERR_UNSUPPORTED for two-phase plans, more than 256
+ * summands, destination memory replicas, or blocks that straddle stage slabs
+ * (describe(): "pull_regions" = 0). */
+axe_status axe_redist_plan_execute_peers_reduce(const axe_redist_plan *plan, const void *const *src_peers,
+                                                void *dst_local, void *cuda_stream);
 /* Phase i (0: reduce-scatter, 1: gather) of a two-phase reduction plan; the
  * sub-plan is owned by `plan` (do not destroy it).  AXE_ERR_UNSUPPORTED for
  * any other plan. */

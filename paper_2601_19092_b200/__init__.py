@@ -117,6 +117,7 @@ _SIGS = {
     "axe_redist_reduce_plan_create": ([_vp, C.POINTER(axe_storage), _vp, C.POINTER(axe_storage), C.c_int, C.c_int,
                                        C.c_int, C.POINTER(_vp)], C.c_int),
     "axe_redist_plan_phase": ([_vp, C.c_int, C.POINTER(_vp)], C.c_int),
+    "axe_redist_plan_execute_peers_reduce": ([_vp, C.POINTER(_vp), _vp, _vp], C.c_int),
     "axe_redistribute_reduce": ([_vp, C.POINTER(axe_storage), _vp, _vp, C.POINTER(axe_storage), _vp, C.c_int, _vp,
                                  _vp], C.c_int),
 }
@@ -510,6 +511,12 @@ class RedistPlan:
         arr = (C.c_void_p * len(dst_peers))(*[_ptr(d) for d in dst_peers])
         _check(_lib.axe_redist_plan_execute_peers(self._h, _ptr(src_local), arr, _stream(stream)),
                "axe_redist_plan_execute_peers")
+
+    def execute_peers_reduce(self, src_peers, dst_local, stream=None):
+        """One-sided pull reduction: K4 kernels read every partial straight from src_peers[owner]."""
+        arr = (C.c_void_p * len(src_peers))(*[_ptr(x) for x in src_peers])
+        _check(_lib.axe_redist_plan_execute_peers_reduce(self._h, arr, _ptr(dst_local), _stream(stream)),
+               "axe_redist_plan_execute_peers_reduce")
 
     def counts(self, peer: int):
         a, b = C.c_int64(), C.c_int64()

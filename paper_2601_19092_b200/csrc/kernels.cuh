@@ -202,6 +202,10 @@ struct K4Params {
   Swz ssw, dsw;
   int dep;
 };
+// one-sided (pull) form: summand k is read through its own base pointer (a peer's buffer)
+struct K4Ptrs {
+  uint64_t p[K4_MAXK];
+};
 // generic form: both layouts evaluated per element (K0 sides; the source side spans K * Y)
 struct K4GParams {
   K0Side src, dst;

@@ -109,9 +109,11 @@ struct Op<DT_I64> {
 constexpr int K4_THREADS = 256;
 constexpr int K4_BATCH = 8;  // summands loaded before they are added (loads in flight per thread)
 
-template <int DT, int V>
-__global__ void __launch_bounds__(K4_THREADS) k4_reduce(const __grid_constant__ K4Params p,
-                                                        const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
+// PEER: summand k lives at (uint8_t *)ptrs.p[k] + swz(so + koff[k]) (a peer's buffer mapped into this
+// process, read over NVLink), else at src + swz(so + koff[k]).
+template <int DT, int V, bool PEER>
+__device__ __forceinline__ void k4_body(const K4Params &p, const uint64_t *kp, const uint8_t *__restrict__ src,
+                                        uint8_t *__restrict__ dst) {
   using O = Op<DT>;
   using S = typename O::S;
   using A = typename O::A;
@@ -144,11 +146,13 @@ __global__ void __launch_bounds__(K4_THREADS) k4_reduce(const __grid_constant__ 
       for (; k + K4_BATCH <= p.nk; k += K4_BATCH) {
         R raw[K4_BATCH];
 #pragma unroll
-        for (int b = 0; b < K4_BATCH; b++) raw[b] = ld_raw<VB>(src + swz(p.ssw, so + p.koff[k + b]));
+        for (int b = 0; b < K4_BATCH; b++)
+          raw[b] = ld_raw<VB>((PEER ? (const uint8_t *)kp[k + b] : src) + swz(p.ssw, so + p.koff[k + b]));
 #pragma unroll
         for (int b = 0; b < K4_BATCH; b++) accumulate(raw[b]);  // k order
       }
-      for (; k < p.nk; k++) accumulate(ld_raw<VB>(src + swz(p.ssw, so + p.koff[k])));
+      for (; k < p.nk; k++)
+        accumulate(ld_raw<VB>((PEER ? (const uint8_t *)kp[k] : src) + swz(p.ssw, so + p.koff[k])));
     } else {
       for (uint32_t kk = 0; kk < p.ktotal; kk++) {
         int64_t off = 0;
@@ -167,6 +171,19 @@ __global__ void __launch_bounds__(K4_THREADS) k4_reduce(const __grid_constant__ 
     const R out = *reinterpret_cast<const R *>(o);
     for (int r = 0; r < p.nrep; r++) *reinterpret_cast<R *>(dst + swz(p.dsw, dof + p.rep[r])) = out;
   }
+}
+
+template <int DT, int V>
+__global__ void __launch_bounds__(K4_THREADS) k4_reduce(const __grid_constant__ K4Params p,
+                                                        const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
+  k4_body<DT, V, false>(p, nullptr, src, dst);
+}
+
+template <int DT, int V>
+__global__ void __launch_bounds__(K4_THREADS) k4_reduce_peer(const __grid_constant__ K4Params p,
+                                                             const __grid_constant__ K4Ptrs ptrs,
+                                                             uint8_t *__restrict__ dst) {
+  k4_body<DT, V, true>(p, ptrs.p, nullptr, dst);
 }
 
 // ---- generic form: the plain layout + storage evaluation per element
@@ -241,7 +258,43 @@ cudaError_t launch_k4_dt(const K4Params &p, int vb, unsigned blocks, const uint8
   return cudaErrorInvalidValue;
 }
 
+template <int DT>
+cudaError_t launch_k4p_dt(const K4Params &p, const K4Ptrs &q, int vb, unsigned blocks, uint8_t *d, cudaStream_t st) {
+  constexpr int ES = (int)sizeof(typename Op<DT>::S);
+  const dim3 g(blocks), b(K4_THREADS);
+  switch (vb / ES) {
+    case 1: return launch_ex(k4_reduce_peer<DT, 1>, g, b, 0, st, p, q, d);
+    case 2:
+      if constexpr (2 * ES <= 16) return launch_ex(k4_reduce_peer<DT, 2>, g, b, 0, st, p, q, d);
+      break;
+    case 4:
+      if constexpr (4 * ES <= 16) return launch_ex(k4_reduce_peer<DT, 4>, g, b, 0, st, p, q, d);
+      break;
+    case 8:
+      if constexpr (8 * ES <= 16) return launch_ex(k4_reduce_peer<DT, 8>, g, b, 0, st, p, q, d);
+      break;
+  }
+  return cudaErrorInvalidValue;
+}
+
 }  // namespace
+
+cudaError_t launch_k4_peer(const K4Params &p, const K4Ptrs &q, int dtype, int vb, unsigned blocks, void *dst,
+                           cudaStream_t st) {
+  uint8_t *d = (uint8_t *)dst;
+  cudaError_t e;
+  switch (dtype) {
+    case DT_F32: e = launch_k4p_dt<DT_F32>(p, q, vb, blocks, d, st); break;
+    case DT_F64: e = launch_k4p_dt<DT_F64>(p, q, vb, blocks, d, st); break;
+    case DT_F16: e = launch_k4p_dt<DT_F16>(p, q, vb, blocks, d, st); break;
+    case DT_BF16: e = launch_k4p_dt<DT_BF16>(p, q, vb, blocks, d, st); break;
+    case DT_I32: e = launch_k4p_dt<DT_I32>(p, q, vb, blocks, d, st); break;
+    case DT_I64: e = launch_k4p_dt<DT_I64>(p, q, vb, blocks, d, st); break;
+    default: return cudaErrorInvalidValue;
+  }
+  g_launches++;
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
 
 cudaError_t launch_k4(const K4Params &p, int dtype, int vb, unsigned blocks, const void *src, void *dst,
                       cudaStream_t st) {

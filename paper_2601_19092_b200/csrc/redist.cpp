@@ -75,6 +75,16 @@ struct axe_redist_plan {
   // evenly sharded temporary, phase_b redistributes (all-gathers) it into the destination
   std::shared_ptr<axe_redist_plan> phase_a, phase_b;
   int64_t tmp_bytes = 0;
+  // one-sided pull form of a reduction (axe_redist_plan_execute_peers_reduce): per destination
+  // region, one K4 launch summing the K partials straight from the senders' src buffers
+  struct Pull {
+    K4Params k;
+    std::vector<int> senders;  // rank owning summand k
+  };
+  std::vector<Pull> pulls;
+  int pull_vb = 0;
+  unsigned pull_blocks = 1;
+  std::string pull_why;
   // scratch owned by the plan (allocated on first execute, on the current device)
   mutable std::mutex mu;
   mutable void *send_buf = nullptr, *recv_buf = nullptr, *stage = nullptr, *tmp = nullptr;
@@ -382,6 +392,100 @@ static axe_status plan_redist(const Layout &S, const Storage &sst, const Layout 
   return AXE_OK;
 }
 
+// The pull form of a single-phase reduction: every block this rank's stage receives (or copies
+// locally) is summand k = md / C of the destination cells md mod C.  Blocks sharing those cells
+// form one region; a region with exactly one block per k becomes one K4 launch whose summand k is
+// read at senders[k]'s src buffer (peer memory) -- exchange, staging and sum fused in one kernel.
+static void build_pull(const axe_redist_plan &in, int64_t K, int64_t C, const Storage &sst, const Storage &dstst,
+                       int dtype, int es, axe_redist_plan *P) {
+  auto no = [&](const char *w) {
+    P->pulls.clear();
+    P->pull_why = w;
+  };
+  if (K > K4_MAXK) return no("more than 256 summands");
+  if (in.dst_rep != 1) return no("destination memory replicas");
+  int64_t lo = 0, hi = 0;  // stage offsets reached by the sub-box
+  for (auto &m : in.M) (m.ds < 0 ? lo : hi) += (m.e - 1) * m.ds;
+  struct Ent {
+    int64_t k;
+    int q;
+    int64_t ms;
+  };
+  std::map<int64_t, std::vector<Ent>> groups;
+  for (int pass = 0; pass < 2; pass++)
+    for (auto &x : pass == 0 ? in.locals : in.recvs) {
+      const int64_t k = x.md / C, r0 = x.md % C;
+      if (r0 + lo < 0 || r0 + hi >= C) return no("a block straddles two stage slabs");
+      groups[r0].push_back(Ent{k, pass == 0 ? in.rank : x.peer, x.ms});
+    }
+  // vector width over the sub-box (as K4: innermost digit contiguous on both sides)
+  std::vector<Joint> Y;
+  for (auto &m : in.M)
+    if (m.e > 1) Y.push_back(m);
+  int64_t V = 1;
+  if (!Y.empty() && Y.back().ss == 1 && Y.back().ds == 1) {
+    std::vector<int64_t> all;
+    for (size_t k = 0; k + 1 < Y.size(); k++) {
+      all.push_back(Y[k].ss);
+      all.push_back(Y[k].ds);
+    }
+    for (auto &g : groups) {
+      all.push_back(g.first);
+      for (auto &e : g.second) all.push_back(e.ms);
+    }
+    int64_t cap = 16 / es;
+    if (sst.swz_b > 0) cap = std::min<int64_t>(cap, std::max<int64_t>(1, (int64_t(1) << sst.swz_m) / es));
+    if (dstst.swz_b > 0) cap = std::min<int64_t>(cap, std::max<int64_t>(1, (int64_t(1) << dstst.swz_m) / es));
+    for (int64_t v = 2; v <= cap; v *= 2) {
+      bool ok = Y.back().e % v == 0;
+      for (int64_t a : all) ok = ok && a % v == 0;
+      if (ok) V = v;
+    }
+  }
+  if (V > 1) {
+    Joint last = Y.back();
+    Y.pop_back();
+    if (last.e / V > 1) Y.push_back(Joint{last.e / V, V, V});
+  }
+  if ((int)Y.size() > K4_MAXD) return no("too many sub-box digits");
+  int64_t total = 1;
+  for (auto &j : Y) total *= j.e;
+  if (total >= (int64_t(1) << 32)) return no("more than 2^32 vectors per region");
+  for (auto &g : groups) {
+    std::vector<Ent> v = g.second;
+    std::sort(v.begin(), v.end(), [](const Ent &a, const Ent &b) { return a.k < b.k; });
+    if ((int64_t)v.size() != K) return no("a region does not receive exactly K summands");
+    for (int64_t k = 0; k < K; k++)
+      if (v[k].k != k) return no("a region receives a summand twice");
+    axe_redist_plan::Pull pl;
+    K4Params &kp = pl.k;
+    memset(&kp, 0, sizeof(kp));
+    kp.total = (uint32_t)total;
+    kp.nd = (int)Y.size();
+    for (int i = 0; i < kp.nd; i++) {
+      kp.fd[i] = make_fastdiv((uint32_t)Y[i].e);
+      kp.ss[i] = Y[i].ss * es;
+      kp.ds[i] = Y[i].ds * es;
+    }
+    kp.nk = (int)K;
+    for (int64_t k = 0; k < K; k++) {
+      kp.koff[k] = v[k].ms * es;
+      pl.senders.push_back(v[k].q);
+    }
+    kp.sbase = 0;
+    kp.dbase = g.first * es;
+    kp.nrep = 1;
+    kp.rep[0] = 0;
+    kp.ssw = make_swz(sst);
+    kp.dsw = make_swz(dstst);
+    P->pulls.push_back(pl);
+  }
+  (void)dtype;
+  P->pull_vb = (int)(V * es);
+  const int64_t blocks = (total + 255) / 256, cap = (int64_t)num_sms() * 8;
+  P->pull_blocks = (unsigned)std::max<int64_t>(1, std::min(blocks, cap));
+}
+
 // Reduce-redistribute (reading R24): dst(y) = sum_k src(k E_D(dst) + y).
 // Phase 1 redistributes the source (its K partials) into a stage layout -- the destination
 // layout with the summed dimension prepended on a private storage axis, so rank g's stage
@@ -430,8 +534,10 @@ static axe_status plan_redist_reduce_1(const Layout &S, const Storage &sst, cons
   P->src_cells = sst.cells;
   P->dst_cells = dstst.cells;
   P->stage_bytes = K * C * es;
+  build_pull(*in, K, C, sst, dstst, dtype, es, P);
   P->desc = "{\"pattern\":\"reduce\",\"K\":" + std::to_string(K) + ",\"exchange\":" + in->desc +
-            ",\"reduce\":" + P->red.desc + "}";
+            ",\"reduce\":" + P->red.desc + ",\"pull_regions\":" + std::to_string(P->pulls.size()) +
+            ",\"pull_vec_bytes\":" + std::to_string(P->pull_vb) + "}";
   return AXE_OK;
 }
 
@@ -712,6 +818,31 @@ axe_status axe_redist_plan_execute_peers(const axe_redist_plan *plan, const void
   // remote blocks first (they cross NVLink), then the local ones
   for (auto &x : plan->sends) AXE_TRY(run_copy(*x.plan, src_local, dst_peers[x.peer], st));
   for (auto &x : plan->locals) AXE_TRY(run_copy(*x.plan, src_local, dst_peers[plan->rank], st));
+  return AXE_OK;
+}
+
+axe_status axe_redist_plan_execute_peers_reduce(const axe_redist_plan *plan, const void *const *src_peers,
+                                                void *dst_local, void *stream) {
+  if (!plan || !src_peers || !dst_local) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
+  if (!plan->inner) AXE_FAIL(AXE_ERR_UNSUPPORTED, "execute_peers_reduce: not a single-phase reduction plan");
+  if (plan->pulls.empty()) AXE_FAIL(AXE_ERR_UNSUPPORTED, "execute_peers_reduce: %s", plan->pull_why.c_str());
+  for (int r = 0; r < plan->nranks; r++)
+    if (!src_peers[r]) AXE_FAIL(AXE_ERR_INVALID_ARG, "src_peers[%d] is NULL", r);
+  if ((uintptr_t)dst_local % plan->pull_vb) AXE_FAIL(AXE_ERR_ALIGNMENT, "dst_local is not %d-byte aligned", plan->pull_vb);
+  cudaStream_t st = (cudaStream_t)stream;
+  stream_forget(st);  // peer buffers: no byte-range bookkeeping, full dependency
+  for (auto &pl : plan->pulls) {
+    K4Ptrs q;
+    for (size_t k = 0; k < pl.senders.size(); k++) {
+      q.p[k] = (uint64_t)(uintptr_t)src_peers[pl.senders[k]];
+      if (q.p[k] % plan->pull_vb) AXE_FAIL(AXE_ERR_ALIGNMENT, "src_peers[%d] is not %d-byte aligned", pl.senders[k], plan->pull_vb);
+    }
+    K4Params k = pl.k;
+    k.dep = 1;
+    cudaError_t e = launch_k4_peer(k, q, plan->red.dtype, plan->pull_vb, plan->pull_blocks, dst_local, st);
+    if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "pull reduce launch: %s", cudaGetErrorString(e));
+  }
+  stream_forget(st);
   return AXE_OK;
 }
 

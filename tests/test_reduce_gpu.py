@@ -242,3 +242,67 @@ def test_nccl_single_rank_reduce(axe):
     exp = np.zeros(R * C * 2, np.uint8)
     oracle.reduce(src, linear_storage(K * R * C), [vals], dst, linear_storage(R * C), [exp], "bf16", nranks=1)
     assert np.array_equal(y.cpu().numpy(), exp)
+
+
+# ------------------------------------------------------------------ one-sided pull form
+def run_pull(axe, cfg, dtype, seed=31):
+    """Every rank's pull plan on one device: the 'peer' table holds the ranks' separate source buffers (on a
+    multi-GPU box these are NVLink-mapped peer buffers; the kernel only sees pointers)."""
+    n, es = cfg["nranks"], synth.DTYPE_SIZE[dtype]
+    ed, _ = oracle.sizes(cfg["src"])
+    edd, _ = oracle.sizes(cfg["dst"])
+    K = ed // edd
+    vals = synth.numbers(ed, dtype, seed)
+    sfill = synth.sentinel(synth.storage_cells(cfg["src_st"]) * es, seed + 1)
+    src = oracle.scatter_ranks(cfg["src"], cfg["src_st"], vals, es, n, sfill, NT)
+    dfill = synth.sentinel(synth.storage_cells(cfg["dst_st"]) * es, seed + 2)
+    exp = [dfill.copy() for _ in range(n)]
+    oracle.reduce(cfg["src"], cfg["src_st"], src, cfg["dst"], cfg["dst_st"], exp, dtype, nranks=n, nthreads=NT)
+    s_dev = [torch.from_numpy(s).cuda() for s in src]
+    d_dev = [torch.from_numpy(dfill).cuda() for _ in range(n)]
+    n0 = axe.kernel_launch_count()
+    descs = []
+    for r in range(n):
+        p = axe.RedistPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], es, n, r, reduce_dtype=dtype)
+        d = p.describe()
+        descs.append(d)
+        p.execute_peers_reduce(s_dev, d_dev[r])
+    torch.cuda.synchronize()
+    assert axe.kernel_launch_count() - n0 == sum(d["pull_regions"] for d in descs)
+    for r in range(n):
+        compare(d_dev[r].cpu().numpy(), exp[r], dfill, dtype, K)
+    return descs[0]
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("dtype", ["bf16", "f32", "i32"])
+def test_pull_reduce_scatter(axe, P, dtype):
+    """P:399-403 reduce-scatter as one kernel per rank reading every partial from its owner."""
+    d = run_pull(axe, synth.reduce_scatter(P, 128, 256, dtype), dtype)
+    assert d["pull_regions"] == 1 and d["pull_vec_bytes"] == 16
+
+
+def test_pull_transposed_shard(axe):
+    """Column shards stored column-major: one region per rank, 2-byte vectors (no shared contiguous run)."""
+    P, R, C = 4, 32, 64
+    src = layout([(P, 1, "gpuid"), (R, C), (C, 1)])
+    dst = layout([(R, 1), (P, 1, "gpuid"), (C // P, R)])
+    cfg = dict(nranks=P, src=src, src_st=linear_storage(R * C), dst=dst, dst_st=linear_storage(R * C // P))
+    run_pull(axe, cfg, "bf16")
+
+
+def test_pull_mesh_partial_over_one_axis(axe):
+    R, C = 64, 32
+    src = layout([(2, 2, "gpuid"), (R, C), (C, 1)], [(2, 1, "gpuid")])
+    dst = layout([(2, 1, "gpuid"), (R // 2, C), (C, 1)], [(2, 2, "gpuid")])
+    cfg = dict(nranks=4, src=src, src_st=linear_storage(R * C), dst=dst, dst_st=linear_storage(R // 2 * C))
+    run_pull(axe, cfg, "f32")
+
+
+def test_pull_rejects_two_phase_plans(axe):
+    cfg = synth.all_reduce(4, 32, 64, "bf16")
+    p = axe.RedistPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], 2, 4, 0, reduce_dtype="bf16")
+    x = torch.zeros(32 * 64, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(axe.AxeError) as e:
+        p.execute_peers_reduce([x] * 4, x.clone())
+    assert e.value.name == "AXE_ERR_UNSUPPORTED"
