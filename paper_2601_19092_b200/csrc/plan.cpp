@@ -798,8 +798,9 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
   if (kernel == AXE_KERNEL_AUTO || kernel == AXE_KERNEL_VECTOR || kernel == AXE_KERNEL_TMA) {
     if (joint && build_k1(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &why)) {
       P.kernel = KK_VECTOR;
-      // narrower than 16-byte vectors on one side: stage through shared memory instead (K2)
-      if (kernel == AXE_KERNEL_AUTO && P.vb < 16 && (P.vb <= 2 || P.k1_sector_eff < 0.5)) {
+      // vectors of <= 4 bytes (or scattered sectors): stage through shared memory instead (K2), which
+      // moves 16-byte vectors on both sides (config 3a: K1 4-byte 1583 us, K2 1547 us on B200)
+      if (kernel == AXE_KERNEL_AUTO && P.vb < 16 && (P.vb <= 4 || P.k1_sector_eff < 0.5)) {
         // (K2T, the TMA-staged variant, stays opt-in: measured slower than K2 on B200 in round 1)
         CopyPlan T = P;
         std::string w2;
