@@ -218,3 +218,16 @@ def test_generic_injectivity_matches_oracle():
         assert ok_axe == ok_oracle, dst
         agree += 1
     assert agree == 300
+
+
+def test_copy_plan_create_ex_host_slabs():
+    """axe_copy_plan_create_ex bounds the host-pipeline slab count (bench.py's e2e uses 2)."""
+    cfg = synth.config2()
+    for n in (2, 4, 8):
+        p = axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], 2, host_slabs=n)
+        assert p.describe()["host_chunks"] == n
+    import ctypes as C
+    h = C.c_void_p()
+    s = axe.Layout(cfg["src"]["D"])
+    ss, _k = axe.make_storage(cfg["src_st"])
+    assert axe._lib.axe_copy_plan_create_ex(s.handle, C.byref(ss), s.handle, C.byref(ss), 2, 0, -1, C.byref(h)) == 1
