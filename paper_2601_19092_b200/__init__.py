@@ -229,9 +229,9 @@ class Layout:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None:  # (module globals may be gone at interpreter exit)
             _lib.axe_layout_destroy(h)
-            self._h = None
+        self._h = None
 
     @property
     def handle(self):
@@ -391,9 +391,9 @@ class CopyPlan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None:  # (module globals may be gone at interpreter exit)
             _lib.axe_copy_plan_destroy(h)
-            self._h = None
+        self._h = None
 
     def execute(self, src, dst, stream=None):
         _check(_lib.axe_copy_plan_execute(self._h, _ptr(src), _ptr(dst), _stream(stream)), "axe_copy_plan_execute")
@@ -449,9 +449,9 @@ class Comm:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None:  # (module globals may be gone at interpreter exit)
             _lib.axe_comm_destroy(h)
-            self._h = None
+        self._h = None
 
     @property
     def handle(self):
@@ -480,7 +480,7 @@ class RedistPlan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h and getattr(self, "_owned", True):
+        if h and getattr(self, "_owned", True) and _lib is not None:
             _lib.axe_redist_plan_destroy(h)
         self._h = None
 
@@ -556,9 +556,9 @@ class ReducePlan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None:  # (module globals may be gone at interpreter exit)
             _lib.axe_reduce_plan_destroy(h)
-            self._h = None
+        self._h = None
 
     def execute(self, src, dst, stream=None):
         _check(_lib.axe_reduce_plan_execute(self._h, _ptr(src), _ptr(dst), _stream(stream)), "axe_reduce_plan_execute")

@@ -149,6 +149,63 @@ def run_reduce(cfg, seed):
     return None
 
 
+def dist_side(rng, N, nranks, reps_ok):
+    """A random distributed layout of N logical elements over nranks devices: one shard digit of extent P on
+    gpuid at a random logical position (the rest a random mixed radix on m), and, when P < nranks, the
+    remaining nranks / P devices as a gpuid replica (contiguous or strided device ids)."""
+    Ps = [p for p in (1, 2, 4, 8) if nranks % p == 0 and N % p == 0 and (reps_ok or p == nranks)]
+    P = int(rng.choice(Ps))
+    Rn = nranks // P
+    exts = split(rng, N // P)
+    mem, cells = rand_layout(rng, exts, reps=False)
+    pos = int(rng.integers(0, len(mem["D"]) + 1))
+    contiguous = rng.random() < 0.5
+    gs, rs = (Rn, 1) if contiguous else (1, P)
+    D = list(mem["D"])
+    D.insert(pos, (P, gs, "gpuid"))
+    R = [(Rn, rs, "gpuid")] if Rn > 1 else []
+    return layout(D, R, mem["O"]), cells
+
+
+def redist_case(rng):
+    nranks = int(rng.choice([2, 4, 8]))
+    es = int(rng.choice([1, 2, 4, 8]))
+    N = nranks * int(rng.choice([16, 48, 64, 256, 1024, 4096]))
+    src, sc = dist_side(rng, N, nranks, True)
+    dst, dc = dist_side(rng, N, nranks, True)
+    return dict(es=es, nranks=nranks, src=src, src_st=linear_storage(sc), dst=dst, dst_st=linear_storage(dc))
+
+
+def run_redist(cfg, seed):
+    n, es = cfg["nranks"], cfg["es"]
+    try:
+        plans = [axe.RedistPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], es, n, r) for r in range(n)]
+    except axe.AxeError as e:
+        if e.name in ("AXE_ERR_NONINJECTIVE", "AXE_ERR_BOUNDS", "AXE_ERR_UNSUPPORTED"):
+            return "skip"
+        return f"plan failed: {e}"
+    ed, _ = oracle.sizes(cfg["src"])
+    v = synth.values(ed, es, seed)
+    sfill = synth.sentinel(synth.storage_cells(cfg["src_st"]) * es, seed + 1)
+    src = oracle.scatter_ranks(cfg["src"], cfg["src_st"], v, es, n, sfill, NT)
+    dfill = synth.sentinel(synth.storage_cells(cfg["dst_st"]) * es, seed + 2)
+    exp = [dfill.copy() for _ in range(n)]
+    oracle.redistribute(cfg["src"], cfg["src_st"], src, cfg["dst"], cfg["dst_st"], exp, es, nthreads=NT)
+    s_dev = [torch.from_numpy(x).cuda() for x in src]
+    for mode in ("emulate", "peers"):
+        d_dev = [torch.from_numpy(dfill).cuda() for _ in range(n)]
+        if mode == "emulate":
+            axe.redist_emulate(plans, s_dev, d_dev)
+        else:
+            for r in range(n):
+                plans[r].execute_peers(s_dev[r], d_dev)
+        torch.cuda.synchronize()
+        for r in range(n):
+            if not np.array_equal(d_dev[r].cpu().numpy(), exp[r]):
+                return f"{mode} mismatch on rank {r} ({plans[0].describe().get('pattern')})"
+    return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=300)
@@ -161,7 +218,19 @@ def main():
     while time.time() - t0 < a.seconds:
         case_seed = int(rng.integers(1 << 31))
         crng = np.random.default_rng(case_seed)
-        if crng.random() < 0.7:
+        u = crng.random()
+        if u < 0.15:
+            cfg = redist_case(crng)
+            err = run_redist(cfg, case_seed)
+            if err == "skip":
+                continue
+            n += 1
+            kinds["redistribute"] = kinds.get("redistribute", 0) + 1
+            if err:
+                fails += 1
+                print(json.dumps({"case_seed": case_seed, "kind": "redistribute", "error": err, "cfg": cfg},
+                                 default=str), flush=True)
+        elif u < 0.7:
             cfg = copy_case(crng)
             for k in KERNELS:
                 err = run_copy(cfg, k, case_seed)
