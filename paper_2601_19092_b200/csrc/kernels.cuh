@@ -104,6 +104,8 @@ struct TmaParams {
   int64_t bstride[TMA_MAXD];   // byte stride of the digit on the bulk side
   int64_t bbase;               // byte offset of box 0 on the bulk side
   uint32_t box_bytes;
+  uint32_t slot_bytes;         // ring slot stride: box_bytes rounded up to 128 B (TMA smem alignment;
+                               // 1024 B with a swizzle, so every slot starts a swizzle pattern)
   int stages;
   int mode;
   int nrep;

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(32) k1_tma(const __grid_constant__ CUtensorMap
   pdl_launch_dependents();
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int S = p.stages;
-  const uint32_t B = p.box_bytes;
+  const uint32_t B = p.box_bytes, SL = p.slot_bytes;
   for (int s = 0; s < S; s++) mbar_init(&full[s], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   fence_async_smem();
@@ -128,9 +128,9 @@ __global__ void __launch_bounds__(32) k1_tma(const __grid_constant__ CUtensorMap
     BoxAddr a = box_addr(p, first + k * step);
     mbar_expect_tx(&full[s], B);
     if (p.mode == 0)
-      tma_load5(smem + (size_t)s * B, &map, &full[s], a.c[0], a.c[1], a.c[2], a.c[3], a.c[4]);
+      tma_load5(smem + (size_t)s * SL, &map, &full[s], a.c[0], a.c[1], a.c[2], a.c[3], a.c[4]);
     else
-      bulk_load(smem + (size_t)s * B, src + a.boff, B, &full[s]);
+      bulk_load(smem + (size_t)s * SL, src + a.boff, B, &full[s]);
   };
 
   const uint32_t pre = mine < (uint32_t)S ? mine : (uint32_t)S;
@@ -140,9 +140,9 @@ __global__ void __launch_bounds__(32) k1_tma(const __grid_constant__ CUtensorMap
     mbar_wait(&full[s], (k / (uint32_t)S) & 1u);
     BoxAddr a = box_addr(p, first + k * step);
     if (p.mode == 0) {
-      for (int r = 0; r < p.nrep; r++) bulk_store(dst + a.boff + p.rep[r], smem + (size_t)s * B, B);
+      for (int r = 0; r < p.nrep; r++) bulk_store(dst + a.boff + p.rep[r], smem + (size_t)s * SL, B);
     } else {
-      tma_store5(&map, smem + (size_t)s * B, a.c[0], a.c[1], a.c[2], a.c[3], a.c[4]);
+      tma_store5(&map, smem + (size_t)s * SL, a.c[0], a.c[1], a.c[2], a.c[3], a.c[4]);
     }
     bulk_commit();
     // the stage of box k-1 is free once its store has read shared memory
@@ -339,7 +339,7 @@ int encode_tensor_map(void *out128, void *gaddr, const uint64_t dims[5], const u
   return (int)r;
 }
 
-size_t tma_smem_bytes(const TmaParams &p) { return (size_t)p.stages * p.box_bytes + 1024; }
+size_t tma_smem_bytes(const TmaParams &p) { return (size_t)p.stages * p.slot_bytes + 1024; }
 
 cudaError_t launch_tma(const void *map128, const TmaParams &p, unsigned blocks, const void *src, void *dst,
                        cudaStream_t st) {

@@ -562,13 +562,17 @@ static bool build_tma(const std::vector<Joint> &J0, const Linear &ls, const Line
   }
   k.bbase = lb.base * es;
   k.box_bytes = (uint32_t)box_bytes;
+  {
+    const int64_t al = span ? 1024 : 128;
+    k.slot_bytes = (uint32_t)((box_bytes + al - 1) / al * al);
+  }
   k.mode = mode;
   k.nrep = (int)reps.size();
   for (size_t i = 0; i < reps.size(); i++) k.rep[i] = reps[i] * es;
   // 24 KiB of boxes per CTA (3 x 8 KiB for config 2) and ~8 CTAs per SM measured best at
   // both 64 MiB and 1 GiB (profiles/r01_tuning.md)
   int64_t stage_bytes = env_int("AXE_TMA_STAGE_BYTES", 24576);
-  int stages = (int)std::max<int64_t>(2, std::min<int64_t>(16, stage_bytes / box_bytes));
+  int stages = (int)std::max<int64_t>(2, std::min<int64_t>(16, stage_bytes / k.slot_bytes));
   k.stages = stages;
   P->tm_swizzle = span;
   P->tm_base = lt.base * es;

@@ -386,3 +386,16 @@ def test_execute_host_alternating_streams(axe, slabs):
     torch.cuda.synchronize()
     for k in range(2):
         assert np.array_equal(hd[k].numpy(), exps[k])
+
+
+def test_tma_small_boxes_regression(axe):
+    """Found by tools/fuzz_gpu.py (case 1540651327): a TMA plan with 64-byte boxes placed ring slots 64 B
+    apart, but TMA needs 128-byte aligned shared-memory destinations (misaligned address).  Slots are now
+    rounded up to 128 B (1024 B when swizzled)."""
+    src = layout([(2, 16384), (2, 1), (2, 131072), (2, 65536), (4096, 4)])
+    dst = layout([(4, 1), (2, 32768), (8192, 4)])
+    cfg = dict(name="tma64", es=16, src=src, src_st=linear_storage(262144), dst=dst, dst_st=linear_storage(65536),
+               seed=11)
+    d = axe.CopyPlan(src, cfg["src_st"], dst, cfg["dst_st"], 16).describe()
+    assert d["kernel"] == "tma" and d["box_bytes"] == 64
+    check(axe, cfg, "auto")

@@ -210,13 +210,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=300)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--trace", action="store_true", help="print every case to stderr before it runs")
+    ap.add_argument("--case", type=int, default=None, help="run only this case seed")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     t0 = time.time()
     n = fails = 0
     kinds = {}
     while time.time() - t0 < a.seconds:
-        case_seed = int(rng.integers(1 << 31))
+        case_seed = int(rng.integers(1 << 31)) if a.case is None else a.case
         crng = np.random.default_rng(case_seed)
         u = crng.random()
         if u < 0.15:
@@ -233,6 +235,8 @@ def main():
         elif u < 0.7:
             cfg = copy_case(crng)
             for k in KERNELS:
+                if a.trace:
+                    print(json.dumps({"running": case_seed, "kernel": k}), file=sys.stderr, flush=True)
                 err = run_copy(cfg, k, case_seed)
                 if err == "skip":
                     continue
@@ -253,6 +257,8 @@ def main():
                 fails += 1
                 print(json.dumps({"case_seed": case_seed, "kind": "reduce", "error": err, "cfg": cfg}, default=str),
                       flush=True)
+        if a.case is not None:
+            break
     print(json.dumps({"summary": {"runs": n, "failures": fails, "per_kernel": kinds, "seconds": time.time() - t0}}))
 
 
