@@ -85,6 +85,33 @@ def copy_case(rng):
     return dict(es=es, src=src, src_st=linear_storage(sc, ssw), dst=dst, dst_st=linear_storage(dc, dsw))
 
 
+def tma_case(rng):
+    """Re-tilings in the TMA planner's reach: a (padded) row-major matrix <-> tiles of (tr x tc) elements,
+    tiles row- or column-ordered, optional SW32/64/128 on the tiled side, either direction."""
+    es = int(rng.choice([1, 2, 4, 8]))
+    tc = int(rng.choice([8, 16, 32, 64, 128])) // max(1, es // 2)
+    tc = max(1, tc)
+    tr = int(rng.choice([1, 2, 8, 16, 64]))
+    R, C = tr * int(rng.integers(1, 9)), tc * int(rng.integers(1, 9))
+    ld = C + (16 // es if es < 16 else 1) * int(rng.integers(0, 3))
+    rm = layout([(R, ld), (C, 1)])
+    bR, bC = R // tr, C // tc
+    if rng.random() < 0.5:
+        tl = layout([(bR, tr * C), (tr, tc), (bC, tr * tc), (tc, 1)])
+    else:
+        tl = layout([(bR, tr * tc), (tr, tc), (bC, bR * tr * tc), (tc, 1)])
+    cells = R * C
+    sw = (0, 0, 0)
+    if rng.random() < 0.6:
+        opts = [z for z in (synth.SW32, synth.SW64, synth.SW128) if (16 << z[0]) == tc * es and (cells * es) % 1024 == 0]
+        if opts:
+            sw = opts[0]
+    a = dict(es=es, src=rm, src_st=linear_storage(R * ld), dst=tl, dst_st=linear_storage(cells, sw))
+    if rng.random() < 0.5:
+        a = dict(es=es, src=tl, src_st=linear_storage(cells, sw), dst=rm, dst_st=linear_storage(R * ld))
+    return a
+
+
 def run_copy(cfg, kernel, seed):
     es = cfg["es"]
     try:
@@ -233,7 +260,7 @@ def main():
                 print(json.dumps({"case_seed": case_seed, "kind": "redistribute", "error": err, "cfg": cfg},
                                  default=str), flush=True)
         elif u < 0.7:
-            cfg = copy_case(crng)
+            cfg = copy_case(crng) if crng.random() < 0.7 else tma_case(crng)
             for k in KERNELS:
                 if a.trace:
                     print(json.dumps({"running": case_seed, "kernel": k}), file=sys.stderr, flush=True)
