@@ -569,16 +569,16 @@ static bool build_tma(const std::vector<Joint> &J0, const Linear &ls, const Line
   k.mode = mode;
   k.nrep = (int)reps.size();
   for (size_t i = 0; i < reps.size(); i++) k.rep[i] = reps[i] * es;
-  // 24 KiB of boxes per CTA (3 x 8 KiB for config 2) and ~8 CTAs per SM measured best at
-  // both 64 MiB and 1 GiB (profiles/r01_tuning.md)
-  int64_t stage_bytes = env_int("AXE_TMA_STAGE_BYTES", 24576);
+  // 16 KiB of boxes per CTA (2 x 8 KiB for config 2) and 8 CTAs per SM: measured on B200 at
+  // 1 GiB 174 us against 190 us with 3 stages or 10-12 CTAs/SM, unchanged at 64 MiB (10.1 us)
+  int64_t stage_bytes = env_int("AXE_TMA_STAGE_BYTES", 16384);
   int stages = (int)std::max<int64_t>(2, std::min<int64_t>(16, stage_bytes / k.slot_bytes));
   k.stages = stages;
   P->tm_swizzle = span;
   P->tm_base = lt.base * es;
   P->tm_cache = std::make_shared<TmaCache>();
   int per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(16, (220 * 1024) / (int64_t)tma_smem_bytes(k)));
-  per_sm = (int)std::min<int64_t>(per_sm, env_int("AXE_TMA_PER_SM", per_sm));
+  per_sm = (int)std::min<int64_t>(per_sm, env_int("AXE_TMA_PER_SM", 8));
   P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nboxes, (int64_t)num_sms() * per_sm));
   P->align = 16;
   P->covers_all = (int64_t)reps.size() * nboxes * box_bytes == dstst.cells * es;
