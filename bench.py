@@ -280,6 +280,28 @@ def measure_reshard_p2p(axe, torch, dist, ws, rank, local, stream, timed):
     bus = (ws - 1) / ws * sbuf.numel() * 2
     out["reduce_scatter_pull"] = {"ms": ms, "bus_bytes_per_gpu": bus, "bus_GBps": bus / (ms * 1e-3) / 1e9,
                                   "pull_regions": plan.describe()["pull_regions"]}
+    # NVLS: one multimem.ld_reduce per 16-byte vector on the multicast address; checked against
+    # the pull result (the switch's summation order differs, so the check is a bf16 tolerance)
+    mc = int(getattr(hdl, "multicast_ptr", 0) or 0)
+    has_mc = torch.tensor([1 if mc else 0], device="cuda")
+    dist.all_reduce(has_mc, op=dist.ReduceOp.MIN)
+    if int(has_mc.item()) and plan.describe().get("multicast"):
+        dst2 = torch.empty_like(dst)
+
+        def fn_mc():
+            hdl.barrier(channel=0)
+            plan.execute_multicast_reduce(mc, dst2, stream)
+            hdl.barrier(channel=0)
+        ms2 = timed(fn_mc)
+        fn_rs()
+        torch.cuda.synchronize()
+        diff = (dst2.float() - dst.float()).abs().max().reshape(1)
+        dist.all_reduce(diff, op=dist.ReduceOp.MAX)
+        out["reduce_scatter_multimem"] = {"ms": ms2, "bus_GBps": bus / (ms2 * 1e-3) / 1e9,
+                                          "max_abs_diff_vs_pull": float(diff.item())}
+        del dst2
+    else:
+        out["reduce_scatter_multimem"] = {"skipped": "no multicast object (NVLS) on this group"}
     del sbuf, hdl, dst
     return out
 

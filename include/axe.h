@@ -415,6 +415,18 @@ axe_status axe_redist_reduce_plan_create(const axe_layout *src, const axe_storag
  * (describe(): "pull_regions" = 0). */
 axe_status axe_redist_plan_execute_peers_reduce(const axe_redist_plan *plan, const void *const *src_peers,
                                                 void *dst_local, void *cuda_stream);
+/* NVLS form of the same (the paper's reduce-scatter "dispatch[es] to
+ * multimem.ld_reduce on B200"): src_multicast is the multicast address of the
+ * ranks' source buffers (an NVSwitch multicast object bound to every rank's
+ * src, e.g. torch symmetric memory's multicast_ptr).  Every 16-byte output
+ * vector is one multimem.ld_reduce -- the switch sums the vector over all
+ * ranks -- stored into dst_local.  Requires each region to take exactly one
+ * partial from every rank at the same offset (describe(): "multicast": true),
+ * f32 / bf16 / f16 (bf16 / f16 accumulate in f32 inside the switch; the
+ * summation order is the hardware's).  Same cross-rank ordering contract as
+ * axe_redist_plan_execute_peers_reduce. */
+axe_status axe_redist_plan_execute_multicast_reduce(const axe_redist_plan *plan, const void *src_multicast,
+                                                    void *dst_local, void *cuda_stream);
 /* Phase i (0: reduce-scatter, 1: gather) of a two-phase reduction plan; the
  * sub-plan is owned by `plan` (do not destroy it).  AXE_ERR_UNSUPPORTED for
  * any other plan. */

@@ -118,6 +118,7 @@ _SIGS = {
                                        C.c_int, C.POINTER(_vp)], C.c_int),
     "axe_redist_plan_phase": ([_vp, C.c_int, C.POINTER(_vp)], C.c_int),
     "axe_redist_plan_execute_peers_reduce": ([_vp, C.POINTER(_vp), _vp, _vp], C.c_int),
+    "axe_redist_plan_execute_multicast_reduce": ([_vp, _vp, _vp, _vp], C.c_int),
     "axe_redistribute_reduce": ([_vp, C.POINTER(axe_storage), _vp, _vp, C.POINTER(axe_storage), _vp, C.c_int, _vp,
                                  _vp], C.c_int),
 }
@@ -517,6 +518,12 @@ class RedistPlan:
         arr = (C.c_void_p * len(src_peers))(*[_ptr(x) for x in src_peers])
         _check(_lib.axe_redist_plan_execute_peers_reduce(self._h, arr, _ptr(dst_local), _stream(stream)),
                "axe_redist_plan_execute_peers_reduce")
+
+    def execute_multicast_reduce(self, src_multicast, dst_local, stream=None):
+        """NVLS reduction: one multimem.ld_reduce per 16-byte output vector on the multicast address."""
+        _check(_lib.axe_redist_plan_execute_multicast_reduce(self._h, _ptr(src_multicast), _ptr(dst_local),
+                                                             _stream(stream)),
+               "axe_redist_plan_execute_multicast_reduce")
 
     def counts(self, peer: int):
         a, b = C.c_int64(), C.c_int64()

@@ -258,6 +258,51 @@ cudaError_t launch_k4_dt(const K4Params &p, int vb, unsigned blocks, const uint8
   return cudaErrorInvalidValue;
 }
 
+// NVLS form (the paper's GEMM + reduce-scatter "dispatch to multimem.ld_reduce on B200"):
+// every output vector is ONE multimem.ld_reduce on the multicast address of the partials -- the
+// NVSwitch reads the vector from every rank's buffer and returns the sum.  16-byte vectors.
+template <int DT>
+__device__ __forceinline__ uint4 mc_ld_reduce(const uint8_t *a) {
+  uint4 r;
+  if constexpr (DT == DT_F32)
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(a)
+                 : "memory");
+  else if constexpr (DT == DT_BF16)
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(a)
+                 : "memory");
+  else
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.f16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(a)
+                 : "memory");
+  return r;
+}
+
+template <int DT>
+__global__ void __launch_bounds__(K4_THREADS) k4_multimem(const __grid_constant__ K4Params p,
+                                                          const uint8_t *__restrict__ mc, uint8_t *__restrict__ dst) {
+  if (p.dep) pdl_wait();
+  pdl_launch_dependents();
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < p.total; i += stride) {
+    int64_t so = p.sbase + p.koff[0], dof = p.dbase;
+    uint32_t rem = i;
+    for (int k = p.nd - 1; k >= 0; k--) {
+      const uint32_t q = fdiv(p.fd[k], rem);
+      const uint32_t d = rem - q * p.fd[k].d;
+      rem = q;
+      so += (int64_t)d * p.ss[k];
+      dof += (int64_t)d * p.ds[k];
+    }
+    const uint4 v = mc_ld_reduce<DT>(mc + swz(p.ssw, so));
+    *reinterpret_cast<uint4 *>(dst + swz(p.dsw, dof)) = v;
+  }
+}
+
 template <int DT>
 cudaError_t launch_k4p_dt(const K4Params &p, const K4Ptrs &q, int vb, unsigned blocks, uint8_t *d, cudaStream_t st) {
   constexpr int ES = (int)sizeof(typename Op<DT>::S);
@@ -290,6 +335,22 @@ cudaError_t launch_k4_peer(const K4Params &p, const K4Ptrs &q, int dtype, int vb
     case DT_BF16: e = launch_k4p_dt<DT_BF16>(p, q, vb, blocks, d, st); break;
     case DT_I32: e = launch_k4p_dt<DT_I32>(p, q, vb, blocks, d, st); break;
     case DT_I64: e = launch_k4p_dt<DT_I64>(p, q, vb, blocks, d, st); break;
+    default: return cudaErrorInvalidValue;
+  }
+  g_launches++;
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_k4_multimem(const K4Params &p, int dtype, unsigned blocks, const void *mc, void *dst,
+                               cudaStream_t st) {
+  const uint8_t *m = (const uint8_t *)mc;
+  uint8_t *d = (uint8_t *)dst;
+  const dim3 g(blocks), b(K4_THREADS);
+  cudaError_t e;
+  switch (dtype) {
+    case DT_F32: e = launch_ex(k4_multimem<DT_F32>, g, b, 0, st, p, m, d); break;
+    case DT_BF16: e = launch_ex(k4_multimem<DT_BF16>, g, b, 0, st, p, m, d); break;
+    case DT_F16: e = launch_ex(k4_multimem<DT_F16>, g, b, 0, st, p, m, d); break;
     default: return cudaErrorInvalidValue;
   }
   g_launches++;

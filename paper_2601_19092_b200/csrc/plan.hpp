@@ -141,6 +141,8 @@ axe_status run_reduce(const ReducePlan &p, const void *src, void *dst, cudaStrea
 cudaError_t launch_k4(const K4Params &p, int dtype, int vb, unsigned blocks, const void *src, void *dst,
                       cudaStream_t st);
 cudaError_t launch_k4g(const K4GParams &p, int dtype, const void *src, void *dst, cudaStream_t st);
+cudaError_t launch_k4_multimem(const K4Params &p, int dtype, unsigned blocks, const void *mc, void *dst,
+                               cudaStream_t st);
 cudaError_t launch_k4_peer(const K4Params &p, const K4Ptrs &q, int dtype, int vb, unsigned blocks, void *dst,
                            cudaStream_t st);
 

@@ -82,6 +82,7 @@ struct axe_redist_plan {
     std::vector<int> senders;  // rank owning summand k
   };
   std::vector<Pull> pulls;
+  bool multicast_ok = false;  // every region: one partial per rank at the same offset (NVLS form)
   int pull_vb = 0;
   unsigned pull_blocks = 1;
   std::string pull_why;
@@ -480,8 +481,20 @@ static void build_pull(const axe_redist_plan &in, int64_t K, int64_t C, const St
     kp.dsw = make_swz(dstst);
     P->pulls.push_back(pl);
   }
-  (void)dtype;
   P->pull_vb = (int)(V * es);
+  // NVLS: a multicast load at one offset reduces over every rank's buffer, so each region must take
+  // exactly one partial from every rank, all at the same source offset; 16-byte float vectors
+  P->multicast_ok = (dtype == DT_F32 || dtype == DT_BF16 || dtype == DT_F16) && V * es == 16 &&
+                    K == in.nranks && !sst.swz_b;
+  for (auto &pl : P->pulls) {
+    std::vector<int> seen(in.nranks, 0);
+    for (size_t k = 0; k < pl.senders.size(); k++) {
+      seen[pl.senders[k]]++;
+      if (pl.k.koff[k] != pl.k.koff[0]) P->multicast_ok = false;
+    }
+    for (int c : seen)
+      if (c != 1) P->multicast_ok = false;
+  }
   const int64_t blocks = (total + 255) / 256, cap = (int64_t)num_sms() * 8;
   P->pull_blocks = (unsigned)std::max<int64_t>(1, std::min(blocks, cap));
 }
@@ -537,7 +550,8 @@ static axe_status plan_redist_reduce_1(const Layout &S, const Storage &sst, cons
   build_pull(*in, K, C, sst, dstst, dtype, es, P);
   P->desc = "{\"pattern\":\"reduce\",\"K\":" + std::to_string(K) + ",\"exchange\":" + in->desc +
             ",\"reduce\":" + P->red.desc + ",\"pull_regions\":" + std::to_string(P->pulls.size()) +
-            ",\"pull_vec_bytes\":" + std::to_string(P->pull_vb) + "}";
+            ",\"pull_vec_bytes\":" + std::to_string(P->pull_vb) + ",\"multicast\":" +
+            (P->multicast_ok ? "true" : "false") + "}";
   return AXE_OK;
 }
 
@@ -841,6 +855,24 @@ axe_status axe_redist_plan_execute_peers_reduce(const axe_redist_plan *plan, con
     k.dep = 1;
     cudaError_t e = launch_k4_peer(k, q, plan->red.dtype, plan->pull_vb, plan->pull_blocks, dst_local, st);
     if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "pull reduce launch: %s", cudaGetErrorString(e));
+  }
+  stream_forget(st);
+  return AXE_OK;
+}
+
+axe_status axe_redist_plan_execute_multicast_reduce(const axe_redist_plan *plan, const void *src_multicast,
+                                                    void *dst_local, void *stream) {
+  if (!plan || !src_multicast || !dst_local) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
+  if (!plan->inner || plan->pulls.empty() || !plan->multicast_ok)
+    AXE_FAIL(AXE_ERR_UNSUPPORTED, "multicast reduce: needs one partial per rank at one offset, 16-byte f32/bf16/f16");
+  if ((uintptr_t)src_multicast % 16 || (uintptr_t)dst_local % 16) AXE_FAIL(AXE_ERR_ALIGNMENT, "16-byte alignment");
+  cudaStream_t st = (cudaStream_t)stream;
+  stream_forget(st);
+  for (auto &pl : plan->pulls) {
+    K4Params k = pl.k;
+    k.dep = 1;
+    cudaError_t e = launch_k4_multimem(k, plan->red.dtype, plan->pull_blocks, src_multicast, dst_local, st);
+    if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "multimem reduce launch: %s", cudaGetErrorString(e));
   }
   stream_forget(st);
   return AXE_OK;
