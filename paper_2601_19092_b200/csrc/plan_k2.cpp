@@ -186,7 +186,11 @@ bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
       if (Vs * es < 4 || Vd * es < 4) continue;
       if (TE % (Vs * NT) || TE % (Vd * NT)) continue;
       if (TE / (Vs * NT) > 8 || TE / (Vd * NT) > K2_MAXJ || Vd / G > K2_MAXK) continue;
-      int score = (int)(std::min<int64_t>(Ls * es, 256) + std::min<int64_t>(Ld * es, 256));
+      static const int64_t run_cap = [] {
+        const char *e = getenv("AXE_K2_RUN_CAP");  // tuning knob: run bytes worth rewarding
+        return (e && *e) ? (int64_t)atoll(e) : (int64_t)256;
+      }();
+      int score = (int)(std::min<int64_t>(Ls * es, run_cap) + std::min<int64_t>(Ld * es, run_cap));
       score = score * 4 + (int)std::min<int64_t>(TE * es / 4096, 4);  // then prefer tiles up to 16 KiB
       if (score > best.score) best = Choice{Ls, Ld, TE, Vs, Vd, inc, score};
     }
