@@ -231,3 +231,39 @@ def test_copy_plan_create_ex_host_slabs():
     s = axe.Layout(cfg["src"]["D"])
     ss, _k = axe.make_storage(cfg["src_st"])
     assert axe._lib.axe_copy_plan_create_ex(s.handle, C.byref(ss), s.handle, C.byref(ss), 2, 0, -1, C.byref(h)) == 1
+
+
+def test_concurrent_planning_is_thread_safe():
+    """include/axe.h promises thread-safe calls: 8 threads plan and describe copies, reductions and
+    redistributions at once (shared axis interning, plan caches, error slots); results match a serial run."""
+    import threading
+    cfgs = [synth.config2(512), synth.config2(512, reverse=True), synth.config3(8, "a"), synth.config3(8, "b"),
+            synth.config1()]
+    serial = [plan(c).describe()["kernel"] for c in cfgs]
+    errors, out = [], {}
+
+    def work(tid):
+        try:
+            for rep in range(20):
+                for i, c in enumerate(cfgs):
+                    k = plan(c).describe()["kernel"]
+                    out.setdefault((tid, i), set()).add(k)
+                r = synth.reduce_scatter(4, 64, 64, "bf16")
+                axe.RedistPlan(r["src"], r["src_st"], r["dst"], r["dst_st"], 2, 4, tid % 4, reduce_dtype="bf16")
+                L = axe.Layout.parse(f"({tid + 2},8):(8,1) + [(2):(64@lane)] + {rep}@warp")
+                assert L.E_D == (tid + 2) * 8
+                try:
+                    axe.Layout([(4, 0)])
+                except axe.AxeError as e:
+                    assert "stride" in str(e)
+        except Exception as e:  # collected, asserted below
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=work, args=(t,)) for t in range(8)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors[:3]
+    for (tid, i), ks in out.items():
+        assert ks == {serial[i]}, (tid, i, ks)

@@ -399,3 +399,36 @@ def test_tma_small_boxes_regression(axe):
     d = axe.CopyPlan(src, cfg["src_st"], dst, cfg["dst_st"], 16).describe()
     assert d["kernel"] == "tma" and d["box_bytes"] == 64
     check(axe, cfg, "auto")
+
+
+def test_concurrent_streams_from_threads(axe):
+    """Two host threads, each on its own stream, issue one-shot axe_copy calls (shared plan cache and PDL
+    bookkeeping) back to back; every result is exact."""
+    import threading
+    cfgs = [synth.config2(512), synth.config2(512, reverse=True)]
+    data = []
+    for c in cfgs:
+        src, d_fill, exp = prepare(c)
+        data.append((c, torch.from_numpy(src).cuda(), d_fill, exp))
+    errors = []
+
+    def work(i):
+        try:
+            c, s, d_fill, exp = data[i]
+            st = torch.cuda.Stream()
+            outs = [torch.from_numpy(d_fill).cuda() for _ in range(4)]
+            with torch.cuda.stream(st):
+                for rep in range(25):
+                    axe.axe_copy(c["src"], c["src_st"], s, c["dst"], c["dst_st"], outs[rep % 4], c["es"], st)
+            st.synchronize()
+            for o in outs:
+                assert np.array_equal(o.cpu().numpy(), exp)
+        except Exception as e:
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
