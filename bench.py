@@ -385,7 +385,10 @@ def run_axe(args):
     plan = axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], es)
     desc = plan.describe()
     l2 = torch.cuda.get_device_properties(local).L2_cache_size
-    pairs = max(2, -(-4 * l2 // (2 * nbytes)))
+    # independent buffer pairs: > 4x L2 of footprint, and enough of them (32) that the copy of pair i
+    # and the next reuse of pair i lie 32 steps apart -- the library lets independent copies overlap
+    # (PDL) and makes a copy wait only for in-flight copies touching its bytes
+    pairs = max(int(os.environ.get("AXE_BENCH_PAIRS", "32")), -(-4 * l2 // (2 * nbytes)))
     g = torch.Generator(device="cuda").manual_seed(cfg["seed"] + rank)
     srcs = [torch.randint(-2**31, 2**31 - 1, (nbytes // 4,), dtype=torch.int32, device="cuda", generator=g)
             for _ in range(pairs)]

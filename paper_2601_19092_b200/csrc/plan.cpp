@@ -837,18 +837,26 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
   return AXE_OK;
 }
 
-// Programmatic-dependent-launch bookkeeping: the byte ranges of the last libaxe
-// kernel launched on each stream.  A new kernel that neither reads nor writes
-// what that kernel wrote, and does not write what it read, may run without
-// griddepcontrol.wait and so overlap the previous kernel's tail.  Any kernel
-// the caller put in between is not a PDL primary of ours (it never triggers
-// early), so the new kernel still starts only after it completes.
+// Programmatic-dependent-launch bookkeeping.  A kernel launched without
+// griddepcontrol.wait may run concurrently with every libaxe kernel still in
+// flight on its stream -- not only the previous one: when the previous kernel
+// itself skipped the wait, it can be running beside ITS predecessor, and so on
+// (measured: a read of a 1 GiB copy's output two launches later saw stale data
+// when only the immediate predecessor was checked, tools/pdl_chain_probe.py).
+// A kernel that does wait sees every earlier kernel complete (completion is
+// transitive: a PDL secondary completes only after its primary; the same probe
+// shows no stale read once the reader waits).  So each stream keeps the byte
+// ranges of the kernels launched since its last waiting kernel (that one
+// included); a new kernel skips the wait only when it neither reads nor writes
+// what any of them writes and does not write what any of them reads.  Work the
+// library did not launch (NCCL, memcpy) resets the window (stream_forget): the
+// next kernel waits.  Windows are capped at 64 kernels.
 namespace {
 struct Ranges {
   uintptr_t s0, s1, d0, d1;
 };
 std::mutex g_dep_mu;
-std::unordered_map<cudaStream_t, Ranges> g_last;
+std::unordered_map<cudaStream_t, std::vector<Ranges>> g_win;
 }  // namespace
 
 int stream_dependency(cudaStream_t st, uintptr_t s0, uintptr_t s1, uintptr_t d0, uintptr_t d1) {
@@ -859,13 +867,19 @@ int stream_dependency(cudaStream_t st, uintptr_t s0, uintptr_t s1, uintptr_t d0,
   auto hit = [](uintptr_t a0, uintptr_t a1, uintptr_t b0, uintptr_t b1) { return a0 < b1 && b0 < a1; };
   std::lock_guard<std::mutex> lk(g_dep_mu);
   int dep = 1;
-  auto it = g_last.find(st);
-  if (overlap_ok && it != g_last.end()) {
-    const Ranges &L = it->second;
-    dep = (hit(d0, d1, L.d0, L.d1) || hit(d0, d1, L.s0, L.s1) || hit(s0, s1, L.d0, L.d1)) ? 1 : 0;
+  auto it = g_win.find(st);
+  if (overlap_ok && it != g_win.end() && !it->second.empty() && it->second.size() < 64) {
+    dep = 0;
+    for (const Ranges &L : it->second)
+      if (hit(d0, d1, L.d0, L.d1) || hit(d0, d1, L.s0, L.s1) || hit(s0, s1, L.d0, L.d1)) {
+        dep = 1;
+        break;
+      }
   }
-  if (g_last.size() > 256) g_last.clear();
-  g_last[st] = Ranges{s0, s1, d0, d1};
+  if (g_win.size() > 256) g_win.clear();
+  std::vector<Ranges> &w = g_win[st];
+  if (dep) w.clear();  // waiting: every earlier kernel is complete when this one proceeds
+  w.push_back(Ranges{s0, s1, d0, d1});
   return dep;
 }
 
@@ -891,7 +905,7 @@ static axe_status tensor_map_for(const CopyPlan &p, const void *tptr, std::array
 // the next libaxe kernel there must wait (full dependency).
 void stream_forget(cudaStream_t st) {
   std::lock_guard<std::mutex> lk(g_dep_mu);
-  g_last.erase(st);
+  g_win.erase(st);
 }
 
 axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t st) {

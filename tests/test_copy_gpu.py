@@ -432,3 +432,27 @@ def test_concurrent_streams_from_threads(axe):
     for t in ts:
         t.join()
     assert not errors, errors
+
+
+def test_pdl_window_two_launches_back(axe):
+    """Regression (tools/pdl_chain_probe.py): A writes X (a 256 MiB copy), B touches unrelated buffers, C reads
+    the tail of X.  C must not skip griddepcontrol.wait just because it is disjoint from B: B itself did not
+    wait, so A may still be running.  The per-stream window of in-flight ranges catches it."""
+    N, n = 1 << 27, 1 << 12
+    big = axe.CopyPlan(layout([(N, 1)]), linear_storage(N), layout([(N, 1)]), linear_storage(N), 2)
+    small = axe.CopyPlan(layout([(n, 1)]), linear_storage(n), layout([(n, 1)]), linear_storage(n), 2)
+    readc = axe.CopyPlan(layout([(n, 1)], O={"m": N - n}), linear_storage(N), layout([(n, 1)]), linear_storage(n), 2)
+    S = torch.full((N,), 7, dtype=torch.int16, device="cuda")
+    X = torch.zeros(N, dtype=torch.int16, device="cuda")
+    a, b = torch.zeros(n, dtype=torch.int16, device="cuda"), torch.zeros(n, dtype=torch.int16, device="cuda")
+    Y = torch.zeros(n, dtype=torch.int16, device="cuda")
+    st = torch.cuda.current_stream()
+    for _ in range(20):
+        X.zero_()
+        Y.fill_(-1)
+        torch.cuda.synchronize()
+        big.execute(S, X, st)
+        small.execute(a, b, st)
+        readc.execute(X, Y, st)
+        torch.cuda.synchronize()
+        assert bool((Y == 7).all())

@@ -52,7 +52,8 @@ def time_cfg(cfg, kernel, reps=20):
     er = plan.dst.E_R
     alg = ed * es * (1 + er)
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
-    pairs = max(1, min(8, -(-4 * l2 // (sb + db))))
+    pairs = max(1, min(32, -(-4 * l2 // (sb + db)), (16 << 30) // (sb + db)))
+    pairs = max(pairs, min(32, (2 << 30) // (sb + db)))  # >= 2 GiB of rotation when it fits
     srcs = [torch.empty(sb, dtype=torch.uint8, device="cuda") for _ in range(pairs)]
     dsts = [torch.empty(db, dtype=torch.uint8, device="cuda") for _ in range(pairs)]
     for s in srcs:
