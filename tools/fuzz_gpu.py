@@ -233,12 +233,69 @@ def run_redist(cfg, seed):
     return None
 
 
+def perm_layout(rng, exts):
+    """A gap-free mixed radix over exts in random digit order (negative strides compensated by the offset):
+    a bijection onto [0, prod(exts))."""
+    order = rng.permutation(len(exts))
+    strides, cur = [0] * len(exts), 1
+    for i in order:
+        strides[i] = cur
+        cur *= exts[i]
+    O, D = 0, []
+    for i, e in enumerate(exts):
+        s_ = strides[i]
+        if rng.random() < 0.15:
+            O += (e - 1) * s_
+            s_ = -s_
+        D.append((e, s_))
+    return layout(D, [], {"m": O} if O else {})
+
+
+def run_chain(rng, seed):
+    """A random sequence of dependent and independent copies among a pool of large (2^24-element) and small
+    (2^12) buffers, launched back to back on one stream without synchronisation (the PDL overlap decisions
+    under test: a long copy, short unrelated copies, then a reader of the long copy's output), then compared
+    with the same sequence applied by the oracle."""
+    es = int(rng.choice([2, 4]))
+    sizes = {"big": 1 << 24, "small": 1 << 12}
+    pool = {k: [] for k in sizes}
+    host, dev, cls = [], [], []
+    for k, C in sizes.items():
+        for _ in range(int(rng.integers(2, 4))):
+            b = len(host)
+            host.append(synth.values(C, es, seed + b))
+            dev.append(torch.from_numpy(host[-1].copy()).cuda())
+            cls.append(k)
+            pool[k].append(b)
+    torch.cuda.synchronize()
+    steps = []
+    for _ in range(int(rng.integers(4, 16))):
+        k = "big" if rng.random() < 0.4 else "small"
+        C = sizes[k]
+        i, j = rng.choice(pool[k], 2, replace=False)
+        src, dst = perm_layout(rng, split(rng, C)), perm_layout(rng, split(rng, C))
+        st = linear_storage(C)
+        plan = axe.CopyPlan(src, st, dst, st, es)
+        steps.append((int(i), int(j), src, dst, st))
+        plan.execute(dev[i], dev[j])
+    torch.cuda.synchronize()
+    for i, j, src, dst, st in steps:
+        out = host[j].copy()
+        oracle.copy(src, st, host[i], dst, st, out, es, NT)
+        host[j] = out
+    for b in range(len(host)):
+        if not np.array_equal(dev[b].cpu().numpy(), host[b]):
+            return f"chain mismatch in {cls[b]} buffer {b} after {len(steps)} copies"
+    return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=300)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--trace", action="store_true", help="print every case to stderr before it runs")
     ap.add_argument("--case", type=int, default=None, help="run only this case seed")
+    ap.add_argument("--only", default="", help="chain | copy | reduce | redistribute (default: all)")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     t0 = time.time()
@@ -248,7 +305,18 @@ def main():
         case_seed = int(rng.integers(1 << 31)) if a.case is None else a.case
         crng = np.random.default_rng(case_seed)
         u = crng.random()
-        if u < 0.15:
+        if a.only:
+            u = {"chain": 0.0, "redistribute": 0.1, "copy": 0.5, "reduce": 0.9}[a.only]
+        if u < 0.08:
+            err = run_chain(crng, case_seed)
+            if err == "skip":
+                continue
+            n += 1
+            kinds["chain"] = kinds.get("chain", 0) + 1
+            if err:
+                fails += 1
+                print(json.dumps({"case_seed": case_seed, "kind": "chain", "error": err}), flush=True)
+        elif u < 0.15:
             cfg = redist_case(crng)
             err = run_redist(cfg, case_seed)
             if err == "skip":
