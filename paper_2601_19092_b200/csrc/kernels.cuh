@@ -103,6 +103,8 @@ struct TmaParams {
   int32_t cmul[TMA_MAXD];      // coordinate step per digit value
   int64_t bstride[TMA_MAXD];   // byte stride of the digit on the bulk side
   int64_t bbase;               // byte offset of box 0 on the bulk side
+  int64_t sstride[TMA_MAXD];   // mode 2 (bulk load + bulk store): byte stride on the source side
+  int64_t sbase;               // mode 2: byte offset of box 0 on the source side
   uint32_t box_bytes;
   uint32_t slot_bytes;         // ring slot stride: box_bytes rounded up to 128 B (TMA smem alignment;
                                // 1024 B with a swizzle, so every slot starts a swizzle pattern)

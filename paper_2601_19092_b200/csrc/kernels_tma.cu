@@ -3,7 +3,9 @@
 // One elected thread per CTA runs an S-stage ring of shared-memory boxes:
 //   mode 0: cp.async.bulk.tensor (TMA, 5-D map, swizzle in smem) global->smem,
 //           then cp.async.bulk smem->global for every destination replica;
-//   mode 1: cp.async.bulk global->smem, then cp.async.bulk.tensor smem->global.
+//   mode 1: cp.async.bulk global->smem, then cp.async.bulk.tensor smem->global;
+//   mode 2: cp.async.bulk global->smem and cp.async.bulk smem->global (a run
+//           contiguous on both sides: no tensor map, no thread touches data).
 // The swizzled smem image of a box is exactly the destination's swizzled bytes
 // (SW128: 16-byte chunk j of row r at j ^ (r mod 8), reading R16), so no thread
 // ever touches the data.
@@ -76,7 +78,7 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 
 struct BoxAddr {
   int c[5];
-  int64_t boff;
+  int64_t boff, soff;
 };
 
 __device__ __forceinline__ BoxAddr box_addr(const TmaParams &p, uint32_t b) {
@@ -84,6 +86,7 @@ __device__ __forceinline__ BoxAddr box_addr(const TmaParams &p, uint32_t b) {
 #pragma unroll
   for (int i = 0; i < 5; i++) a.c[i] = 0;
   a.boff = p.bbase;
+  a.soff = p.sbase;
 #pragma unroll
   for (int k = TMA_MAXD - 1; k >= 0; k--) {
     if (k >= p.nd) continue;
@@ -99,6 +102,7 @@ __device__ __forceinline__ BoxAddr box_addr(const TmaParams &p, uint32_t b) {
     for (int i = 0; i < 5; i++)
       if (p.cdim[k] == i) a.c[i] += (int)d * p.cmul[k];
     a.boff += (int64_t)d * p.bstride[k];
+    a.soff += (int64_t)d * p.sstride[k];
   }
   return a;
 }
@@ -130,7 +134,7 @@ __global__ void __launch_bounds__(32) k1_tma(const __grid_constant__ CUtensorMap
     if (p.mode == 0)
       tma_load5(smem + (size_t)s * SL, &map, &full[s], a.c[0], a.c[1], a.c[2], a.c[3], a.c[4]);
     else
-      bulk_load(smem + (size_t)s * SL, src + a.boff, B, &full[s]);
+      bulk_load(smem + (size_t)s * SL, src + (p.mode == 2 ? a.soff : a.boff), B, &full[s]);
   };
 
   const uint32_t pre = mine < (uint32_t)S ? mine : (uint32_t)S;
@@ -139,7 +143,7 @@ __global__ void __launch_bounds__(32) k1_tma(const __grid_constant__ CUtensorMap
     const int s = (int)(k % (uint32_t)S);
     mbar_wait(&full[s], (k / (uint32_t)S) & 1u);
     BoxAddr a = box_addr(p, first + k * step);
-    if (p.mode == 0) {
+    if (p.mode != 1) {
       for (int r = 0; r < p.nrep; r++) bulk_store(dst + a.boff + p.rep[r], smem + (size_t)s * SL, B);
     } else {
       tma_store5(&map, smem + (size_t)s * SL, a.c[0], a.c[1], a.c[2], a.c[3], a.c[4]);

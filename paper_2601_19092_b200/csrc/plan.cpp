@@ -600,6 +600,91 @@ static bool build_tma(const std::vector<Joint> &J0, const Linear &ls, const Line
   return true;
 }
 
+// K1-TMA mode 2: a run contiguous on BOTH sides (the innermost joint digit with unit strides,
+// >= 1 KiB) moves as whole boxes: cp.async.bulk global->smem, cp.async.bulk smem->global per
+// destination replica.  No tensor map; the box-index digits give both byte offsets.
+static bool build_bulk(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, const Storage &sst,
+                       const Storage &dstst, int es, int64_t min_run_bytes, CopyPlan *P, std::string *why) {
+  auto fail = [&](const char *m) {
+    *why = m;
+    return false;
+  };
+  if (sst.swz_b || dstst.swz_b) return fail("bulk: swizzled storage");
+  std::vector<Joint> J;
+  for (auto &j : J0)
+    if (j.e > 1) J.push_back(j);
+  if (J.empty() || J.back().ss != 1 || J.back().ds != 1) return fail("bulk: no run contiguous on both sides");
+  const int64_t run = J.back().e;
+  if (run * es < min_run_bytes) return fail("bulk: contiguous run too short");
+  // box: the largest divisor of the run with <= 16 KiB and a multiple of 16 bytes
+  int64_t be = 0;
+  for (int64_t d = 1; d * d <= run; d++)
+    if (run % d == 0)
+      for (int64_t c : {d, run / d})
+        if (c * es <= 16384 && (c * es) % 16 == 0 && c > be) be = c;
+  if (be * es < 1024) return fail("bulk: no box of 1-16 KiB divides the run");
+  std::vector<int64_t> reps{0};
+  for (auto &r : ld.R) {
+    std::vector<int64_t> nx;
+    for (int64_t b : reps)
+      for (int64_t d = 0; d < r.e; d++) nx.push_back(b + d * r.s);
+    reps.swap(nx);
+    if (reps.size() > 4096) break;
+  }
+  std::sort(reps.begin(), reps.end());
+  reps.erase(std::unique(reps.begin(), reps.end()), reps.end());
+  if ((int)reps.size() > K1_MAXREP) return fail("bulk: too many replicas");
+  std::vector<Joint> D(J.begin(), J.end() - 1);
+  if (run / be > 1) D.push_back(Joint{run / be, be, be});
+  // box order: destination order, fused where contiguous on both sides
+  std::stable_sort(D.begin(), D.end(), [](const Joint &a, const Joint &b) { return std::llabs(a.ds) > std::llabs(b.ds); });
+  sort_fuse_outer(D);
+  if ((int)D.size() > TMA_MAXD) return fail("bulk: too many box digits");
+  int64_t nboxes = 1;
+  for (auto &j : D) nboxes *= j.e;
+  if (nboxes >= (int64_t(1) << 32)) return fail("bulk: too many boxes");
+  auto a16 = [&](int64_t v) { return (v * es) % 16 == 0; };
+  if (!a16(ls.base) || !a16(ld.base)) return fail("bulk: bases not 16-byte aligned");
+  for (auto &j : D)
+    if (!a16(j.ss) || !a16(j.ds)) return fail("bulk: strides not 16-byte aligned");
+  for (int64_t r : reps)
+    if (!a16(r)) return fail("bulk: replica offsets not 16-byte aligned");
+  TmaParams &k = P->tma;
+  memset(&k, 0, sizeof(k));
+  k.nboxes = (uint32_t)nboxes;
+  k.nd = (int)D.size();
+  for (int i = 0; i < k.nd; i++) {
+    k.fd[i] = make_fastdiv((uint32_t)D[i].e);
+    k.cdim[i] = -1;
+    k.bstride[i] = D[i].ds * es;
+    k.sstride[i] = D[i].ss * es;
+  }
+  k.bbase = ld.base * es;
+  k.sbase = ls.base * es;
+  k.box_bytes = (uint32_t)(be * es);
+  k.slot_bytes = (uint32_t)((k.box_bytes + 127) / 128 * 128);
+  k.mode = 2;
+  k.nrep = (int)reps.size();
+  for (size_t i = 0; i < reps.size(); i++) k.rep[i] = reps[i] * es;
+  const int64_t stage_bytes = env_int("AXE_TMA_STAGE_BYTES", 16384);
+  k.stages = (int)std::max<int64_t>(2, std::min<int64_t>(16, stage_bytes / k.slot_bytes));
+  P->tm_swizzle = 0;
+  P->tm_cache.reset();
+  // 4 CTAs per SM with 2 x 16 KiB boxes each: identity 1 GiB 334 us (6/8 per SM: 354 us; K1: 375 us)
+  int per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(16, (220 * 1024) / (int64_t)tma_smem_bytes(k)));
+  per_sm = (int)std::min<int64_t>(per_sm, env_int("AXE_TMA_BULK_PER_SM", 4));
+  P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nboxes, (int64_t)num_sms() * per_sm));
+  P->align = 16;
+  P->covers_all = (int64_t)reps.size() * nboxes * be == dstst.cells;
+  char b[320];
+  snprintf(b, sizeof b,
+           "{\"kernel\":\"tma\",\"mode\":\"bulk-load/bulk-store\",\"box_bytes\":%lld,\"boxes\":%lld,\"stages\":%d,"
+           "\"blocks\":%u,\"replicas\":%d,\"joint\":",
+           (long long)(be * es), (long long)nboxes, k.stages, P->blocks, k.nrep);
+  P->desc = std::string(b) + joint_json(J0) + "}";
+  return true;
+}
+
 static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out);
 
 axe_status plan_copy(const PlanRequest &rq, CopyPlan *out) {
@@ -763,15 +848,22 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
   std::string why = lin ? (joint ? "" : "digit systems are not nested (no joint refinement)")
                         : "storage composition is not affine";
   if (joint && rq.max_align >= 16 && (kernel == AXE_KERNEL_AUTO || kernel == AXE_KERNEL_TMA)) {
-    std::string w0, w1;
-    if (build_tma(J, ls, ld, *rq.sst, *rq.dstst, es, 0, &P, &w0) ||
-        build_tma(J, ls, ld, *rq.sst, *rq.dstst, es, 1, &P, &w1)) {
+    std::string w0, w1, w2;
+    // AUTO takes a TMA plan only with boxes of >= 4 KiB: 1 KiB boxes measured 35 us against K1's 21 us
+    // on a 64 MiB copy of 1 KiB rows (tools/perf_configs.py rows_1k); forced TMA takes any box
+    const int64_t min_box = kernel == AXE_KERNEL_TMA ? 0 : env_int("AXE_TMA_MIN_BOX", 4096);
+    const int64_t min_run = kernel == AXE_KERNEL_TMA ? 1024 : std::max<int64_t>(min_box, 1024);
+    auto big = [&](bool ok) { return ok && (int64_t)P.tma.box_bytes >= min_box; };
+    if (big(build_tma(J, ls, ld, *rq.sst, *rq.dstst, es, 0, &P, &w0)) ||
+        big(build_tma(J, ls, ld, *rq.sst, *rq.dstst, es, 1, &P, &w1)) ||
+        big(build_bulk(J, ls, ld, *rq.sst, *rq.dstst, es, min_run, &P, &w2))) {
       P.kernel = KK_TMA;
       *out = std::move(P);
       return AXE_OK;
     }
     if (kernel == AXE_KERNEL_TMA)
-      AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced TMA kernel cannot run these layouts: %s / %s", w0.c_str(), w1.c_str());
+      AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced TMA kernel cannot run these layouts: %s / %s / %s", w0.c_str(), w1.c_str(),
+               w2.c_str());
   }
   if (joint && (kernel == AXE_KERNEL_AUTO || kernel == AXE_KERNEL_REGISTER)) {
     std::string w3;
@@ -864,11 +956,16 @@ int stream_dependency(cudaStream_t st, uintptr_t s0, uintptr_t s1, uintptr_t d0,
     const char *e = getenv("AXE_PDL_OVERLAP");
     return (e && *e == '0') ? 0 : 1;
   }();
+  // only kernels moving <= 256 MiB overlap their predecessors: for them ramp-up and tail are a
+  // visible share of the run (64 MiB config 2: 10.1 us overlapped vs ~10.9 us serialised), while two
+  // interleaved full-GPU 1 GiB copies contend (191 us vs 175 us serialised)
+  static const uintptr_t max_bytes = (uintptr_t)env_int("AXE_PDL_MAX_OVERLAP_BYTES", int64_t(256) << 20);
   auto hit = [](uintptr_t a0, uintptr_t a1, uintptr_t b0, uintptr_t b1) { return a0 < b1 && b0 < a1; };
   std::lock_guard<std::mutex> lk(g_dep_mu);
   int dep = 1;
   auto it = g_win.find(st);
-  if (overlap_ok && it != g_win.end() && !it->second.empty() && it->second.size() < 64) {
+  if (overlap_ok && (s1 - s0) + (d1 - d0) <= max_bytes && it != g_win.end() && !it->second.empty() &&
+      it->second.size() < 64) {
     dep = 0;
     for (const Ranges &L : it->second)
       if (hit(d0, d1, L.d0, L.d1) || hit(d0, d1, L.s0, L.s1) || hit(s0, s1, L.d0, L.d1)) {
@@ -951,8 +1048,8 @@ axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t 
     }
     case KK_TMA: {
       const void *tptr = p.tma.mode == 0 ? src : (const void *)dst;
-      std::array<uint64_t, 16> map;
-      AXE_TRY(tensor_map_for(p, tptr, &map));
+      std::array<uint64_t, 16> map{};
+      if (p.tma.mode != 2) AXE_TRY(tensor_map_for(p, tptr, &map));  // mode 2 has no tensor map
       TmaParams k = p.tma;
       k.dep = dep;
       e = launch_tma(map.data(), k, p.blocks, src, dst, st);

@@ -396,9 +396,9 @@ def test_tma_small_boxes_regression(axe):
     dst = layout([(4, 1), (2, 32768), (8192, 4)])
     cfg = dict(name="tma64", es=16, src=src, src_st=linear_storage(262144), dst=dst, dst_st=linear_storage(65536),
                seed=11)
-    d = axe.CopyPlan(src, cfg["src_st"], dst, cfg["dst_st"], 16).describe()
+    d = axe.CopyPlan(src, cfg["src_st"], dst, cfg["dst_st"], 16, "tma").describe()  # AUTO now prefers K1 here
     assert d["kernel"] == "tma" and d["box_bytes"] == 64
-    check(axe, cfg, "auto")
+    check(axe, cfg, "tma")
 
 
 def test_concurrent_streams_from_threads(axe):

@@ -137,7 +137,7 @@ def test_agrees_with_the_k1_tma_planner(n, tile, es, swz):
     """The K1-TMA planner derives its box from joint digits; for config-2 style re-tilings it must agree
     with the paper's lowering of one tile: box row bytes, rows per box (fused atoms), row stride."""
     cfg = synth.config2(n, tile, es, swz)
-    d = axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], es).describe()
+    d = axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], es, "tma").describe()
     if d["kernel"] != "tma" or d["mode"] != "tensor-load/bulk-store":
         pytest.skip(f"planner chose {d['kernel']}")
     tm = d["tensor_map"]

@@ -39,6 +39,12 @@ CONFIGS = {
     "identity_1g": lambda: dict(name="identity_1g", es=2, src=synth.layout([(1 << 29, 1)]),
                                 src_st=synth.linear_storage(1 << 29), dst=synth.layout([(1 << 29, 1)]),
                                 dst_st=synth.linear_storage(1 << 29), seed=3),
+    "rows_4k": lambda: dict(name="rows_4k", es=2, src=synth.layout([(16384, 8192), (2048, 1)]),
+                            src_st=synth.linear_storage(16384 * 8192), dst=synth.layout([(16384, 2048), (2048, 1)]),
+                            dst_st=synth.linear_storage(16384 * 2048), seed=5),
+    "rows_1k": lambda: dict(name="rows_1k", es=2, src=synth.layout([(65536, 2048), (512, 1)]),
+                            src_st=synth.linear_storage(65536 * 2048), dst=synth.layout([(65536, 512), (512, 1)]),
+                            dst_st=synth.linear_storage(65536 * 512), seed=5),
     "transpose_bf16": lambda: transpose_cfg(8192, 8192, 2),
     "transpose_f32": lambda: transpose_cfg(8192, 8192, 4),
 }
