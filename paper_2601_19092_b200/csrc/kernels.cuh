@@ -110,6 +110,7 @@ struct TmaParams {
                                // 1024 B with a swizzle, so every slot starts a swizzle pattern)
   int stages;
   int mode;
+  int xform;                   // 1: movmatrix.trans of every 512-byte block in shared memory (K3-TMA)
   int nrep;
   int64_t rep[K1_MAXREP];      // mode 0: byte offsets of the destination replicas
   int dep;                     // 1: wait for the previous kernel in the stream (griddepcontrol.wait)

@@ -109,19 +109,32 @@ __device__ __forceinline__ BoxAddr box_addr(const TmaParams &p, uint32_t b) {
 
 constexpr int TMA_MAX_STAGES = 16;
 
+__device__ __forceinline__ uint32_t movm_trans(uint32_t a) {
+  uint32_t d;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+  return d;
+}
+
+// p.xform == 1 (K3-TMA): between the bulk load and the bulk store the whole warp applies
+// movmatrix.m8n8.trans.b16 to every 32-bit word of each 512-byte block of the box in shared memory
+// (lane l owns bytes [16 l, 16 l + 16) of the block: the K3 register image), then the stores leave.
 __global__ void __launch_bounds__(32) k1_tma(const __grid_constant__ CUtensorMap map, const __grid_constant__ TmaParams p,
                                              const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[TMA_MAX_STAGES];
-  if (threadIdx.x != 0) return;
+  const bool leader = threadIdx.x == 0;
+  if (!p.xform && !leader) return;
   if (p.dep) pdl_wait();
   pdl_launch_dependents();
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int S = p.stages;
   const uint32_t B = p.box_bytes, SL = p.slot_bytes;
-  for (int s = 0; s < S; s++) mbar_init(&full[s], 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  fence_async_smem();
+  if (leader) {
+    for (int s = 0; s < S; s++) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_async_smem();
+  }
+  if (p.xform) __syncwarp();
 
   const uint32_t nb = p.nboxes;
   const uint32_t first = blockIdx.x, step = gridDim.x;
@@ -138,10 +151,27 @@ __global__ void __launch_bounds__(32) k1_tma(const __grid_constant__ CUtensorMap
   };
 
   const uint32_t pre = mine < (uint32_t)S ? mine : (uint32_t)S;
-  for (uint32_t k = 0; k < pre; k++) issue_load(k);
+  if (leader)
+    for (uint32_t k = 0; k < pre; k++) issue_load(k);
   for (uint32_t k = 0; k < mine; k++) {
     const int s = (int)(k % (uint32_t)S);
     mbar_wait(&full[s], (k / (uint32_t)S) & 1u);
+    if (p.xform) {
+      __syncwarp();  // reconverge after the per-lane barrier waits: movmatrix is .sync.aligned
+      uint8_t *box = smem + (size_t)s * SL;
+      for (uint32_t blk = 0; blk < B / 512; blk++) {
+        uint4 *q = reinterpret_cast<uint4 *>(box + blk * 512 + threadIdx.x * 16);
+        uint4 v = *q;
+        v.x = movm_trans(v.x);
+        v.y = movm_trans(v.y);
+        v.z = movm_trans(v.z);
+        v.w = movm_trans(v.w);
+        *q = v;
+      }
+      fence_async_smem();  // the generic-proxy writes above before the async-proxy bulk store reads them
+      __syncwarp();
+    }
+    if (!leader) continue;
     BoxAddr a = box_addr(p, first + k * step);
     if (p.mode != 1) {
       for (int r = 0; r < p.nrep; r++) bulk_store(dst + a.boff + p.rep[r], smem + (size_t)s * SL, B);
@@ -155,7 +185,7 @@ __global__ void __launch_bounds__(32) k1_tma(const __grid_constant__ CUtensorMap
       issue_load(k - 1 + S);
     }
   }
-  bulk_wait_all();
+  if (leader) bulk_wait_all();
 }
 
 // ------------------------------------------------------------------ K2T: TMA-staged transpose

@@ -869,6 +869,10 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
     std::string w3;
     if (build_k3(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &w3)) {
       P.kernel = KK_REGISTER;
+      // AUTO: the same permute with bulk-copied 16 KiB boxes and movmatrix in shared memory (config 3b:
+      // 1373 us vs 1423 us for the register kernel); a forced "register" keeps the register kernel
+      std::string w4;
+      if (kernel == AXE_KERNEL_AUTO && env_int("AXE_K3_TMA", 1) && build_k3_bulk(&P, &w4)) P.kernel = KK_TMA;
       *out = std::move(P);
       return AXE_OK;
     }

@@ -66,6 +66,7 @@ axe_status run_copy_host(const CopyPlan &p, const void *host_src, void *host_dst
 bool build_k3(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,
               const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why);
 cudaError_t launch_k3(const K3Params &p, unsigned blocks, const void *src, void *dst, cudaStream_t st);
+bool build_k3_bulk(CopyPlan *P, std::string *why);  // K3 as K1-TMA mode 2 + movmatrix in smem
 bool build_k2t(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,
                const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why);
 cudaError_t launch_k2t(const void *map128, const K2TParams &p, int es, unsigned blocks, void *dst, cudaStream_t st);

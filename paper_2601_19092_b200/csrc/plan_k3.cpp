@@ -111,4 +111,77 @@ bool build_k3(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
   return true;
 }
 
+// K3-TMA: the K3 copy with its 512-byte blocks moved by cp.async.bulk -- boxes of up to 32 blocks
+// (16 KiB) where consecutive blocks are contiguous on both sides; the warp applies the movmatrix atom
+// to the box in shared memory between the bulk load and the bulk store (TmaParams.xform).
+size_t tma_smem_bytes(const TmaParams &p);
+bool build_k3_bulk(CopyPlan *P, std::string *why) {
+  auto fail = [&](const char *m) {
+    *why = m;
+    return false;
+  };
+  const K3Params &k = P->k3;
+  if (k.ssw.mask || k.dsw.mask) return fail("k3-tma: swizzled storage");
+  struct D3 {
+    int64_t e, ss, ds;
+  };
+  std::vector<D3> D;
+  for (int i = 0; i < k.nd; i++) D.push_back(D3{(int64_t)k.fd[i].d, k.ss[i], k.ds[i]});
+  // a digit whose blocks are consecutive on both sides (byte stride 512) gives the box run
+  int r = -1;
+  for (int i = 0; i < (int)D.size(); i++)
+    if (D[i].ss == 512 && D[i].ds == 512) r = i;
+  if (r < 0) return fail("k3-tma: no run of blocks contiguous on both sides");
+  int64_t bb = 1;
+  for (int64_t c = 1; c <= 32; c++)
+    if (D[r].e % c == 0) bb = c;
+  if (bb < 4) return fail("k3-tma: box under 2 KiB");
+  std::vector<D3> B;
+  for (int i = 0; i < (int)D.size(); i++) {
+    if (i == r) {
+      if (D[i].e / bb > 1) B.push_back(D3{D[i].e / bb, 512 * bb, 512 * bb});
+    } else {
+      B.push_back(D[i]);
+    }
+  }
+  if ((int)B.size() > TMA_MAXD) return fail("k3-tma: too many box digits");
+  int64_t nboxes = 1;
+  for (auto &d : B) nboxes *= d.e;
+  TmaParams &t = P->tma;
+  memset(&t, 0, sizeof(t));
+  t.nboxes = (uint32_t)nboxes;
+  t.nd = (int)B.size();
+  for (int i = 0; i < t.nd; i++) {
+    t.fd[i] = make_fastdiv((uint32_t)B[i].e);
+    t.cdim[i] = -1;
+    t.bstride[i] = B[i].ds;
+    t.sstride[i] = B[i].ss;
+  }
+  t.bbase = k.dbase;
+  t.sbase = k.sbase;
+  t.box_bytes = (uint32_t)(512 * bb);
+  t.slot_bytes = (uint32_t)((t.box_bytes + 127) / 128 * 128);
+  t.mode = 2;
+  t.xform = 1;
+  t.nrep = k.nrep;
+  for (int i = 0; i < k.nrep; i++) t.rep[i] = k.rep[i];
+  const char *sb = getenv("AXE_TMA_STAGE_BYTES");
+  const int64_t stage_bytes = (sb && *sb) ? atoll(sb) : 16384;
+  t.stages = (int)std::max<int64_t>(2, std::min<int64_t>(16, stage_bytes / t.slot_bytes));
+  const char *ps = getenv("AXE_K3_TMA_PER_SM");
+  int per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(16, (220 * 1024) / (int64_t)tma_smem_bytes(t)));
+  per_sm = std::min(per_sm, (ps && *ps) ? std::max(1, atoi(ps)) : 8);
+  P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nboxes, (int64_t)num_sms() * per_sm));
+  P->tm_swizzle = 0;
+  P->tm_cache.reset();
+  P->align = 16;
+  char b[256];
+  snprintf(b, sizeof b,
+           "{\"kernel\":\"tma\",\"mode\":\"bulk-load/movmatrix/bulk-store\",\"atom\":\"movmatrix.m8n8.trans.b16\","
+           "\"box_bytes\":%u,\"boxes\":%lld,\"stages\":%d,\"blocks\":%u,\"replicas\":%d}",
+           t.box_bytes, (long long)nboxes, t.stages, P->blocks, t.nrep);
+  P->desc = b;
+  return true;
+}
+
 }  // namespace axe

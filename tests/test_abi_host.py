@@ -156,8 +156,10 @@ def test_config1_plan():
 def test_config3_plans_are_affine():
     for v in "ab":
         d = plan(synth.config3(64, v)).describe()
-        # 3a: 4-byte pieces, staged through shared memory (K2); 3b: the movmatrix atom (K3)
-        assert d["kernel"] == {"a": "tile", "b": "register"}[v], d
+        # 3a: 4-byte pieces, staged through shared memory (K2); 3b: the movmatrix atom on bulk-copied
+        # boxes in shared memory (K3-TMA); a forced "register" plan is the register kernel K3
+        assert d["kernel"] == {"a": "tile", "b": "tma"}[v], d
+    assert plan(synth.config3(64, "b"), "register").describe()["kernel"] == "register"
 
 
 def test_nonnested_falls_back_to_generic():

@@ -96,8 +96,8 @@ def test_config3_small(axe, variant, kernel):
                          synth.config3(16, "a")["dst"], synth.config3(16, "a")["dst_st"], 2, "register")
         return
     d = check(axe, synth.config3(16, variant), kernel)
-    if variant == "b" and kernel == "auto":
-        assert d["kernel"] == "register"
+    if variant == "b" and kernel == "auto":   # K3-TMA: bulk boxes + movmatrix in shared memory
+        assert d["kernel"] == "tma" and d["mode"] == "bulk-load/movmatrix/bulk-store", d
 
 
 @pytest.mark.parametrize("variant", ["a", "b"])
