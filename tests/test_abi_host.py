@@ -269,3 +269,23 @@ def test_concurrent_planning_is_thread_safe():
     assert not errors, errors[:3]
     for (tid, i), ks in out.items():
         assert ks == {serial[i]}, (tid, i, ks)
+
+
+def test_tma_bulk_and_k3_tma_plans():
+    """Plan structure of the TMA-family schedules: a run contiguous on both sides (identity, >= 4 KiB) is the
+    bulk mode (no tensor map, 16 KiB boxes); 1 KiB rows stay on K1 in AUTO but a forced TMA plan takes them;
+    config 3b is the movmatrix atom on bulk boxes (K3-TMA)."""
+    ident = dict(es=2, src=layout([(1 << 24, 1)]), src_st=linear_storage(1 << 24), dst=layout([(1 << 24, 1)]),
+                 dst_st=linear_storage(1 << 24))
+    d = plan(ident).describe()
+    assert d["kernel"] == "tma" and d["mode"] == "bulk-load/bulk-store" and d["box_bytes"] == 16384
+    rows1k = dict(es=2, src=layout([(4096, 2048), (512, 1)]), src_st=linear_storage(4096 * 2048),
+                  dst=layout([(4096, 512), (512, 1)]), dst_st=linear_storage(4096 * 512))
+    assert plan(rows1k).describe()["kernel"] == "vector"
+    assert plan(rows1k, "tma").describe()["kernel"] == "tma"
+    d = plan(synth.config3(64, "b")).describe()
+    assert d["mode"] == "bulk-load/movmatrix/bulk-store" and d["box_bytes"] == 16384
+    # swizzled storages never take the bulk mode (bytes move verbatim)
+    sw = dict(es=2, src=layout([(1 << 16, 1)]), src_st=linear_storage(1 << 16, synth.SW128),
+              dst=layout([(1 << 16, 1)]), dst_st=linear_storage(1 << 16))
+    assert plan(sw).describe().get("mode") != "bulk-load/bulk-store"

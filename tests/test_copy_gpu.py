@@ -456,3 +456,15 @@ def test_pdl_window_two_launches_back(axe):
         readc.execute(X, Y, st)
         torch.cuda.synchronize()
         assert bool((Y == 7).all())
+
+
+def test_k3_tma_with_destination_replicas(axe):
+    """K3-TMA with two destination replicas (the permuted 3b tiles written twice, 16 tiles apart on the cta
+    axis): every box is stored once per replica after the in-smem movmatrix."""
+    tiles = 16
+    dst = synth.config3b_dst(tiles)
+    dst = layout(dst["D"], [(2, tiles, "cta")], dst["O"])
+    cfg = dict(name="3b_rep", es=2, src=synth.config3_src(tiles), src_st=synth._regdump_storage(tiles), dst=dst,
+               dst_st=synth._regdump_storage(2 * tiles), seed=13)
+    d = check(axe, cfg, "auto")
+    assert d["kernel"] == "tma" and d["replicas"] == 2, d
