@@ -310,7 +310,9 @@ def _time_plan(torch, plan, reps=10):
     """Graph-replayed back-to-back executes over rotating buffers (> 4x L2); returns ms per launch."""
     sb, db = plan.sizes()
     l2 = torch.cuda.get_device_properties(torch.cuda.current_device()).L2_cache_size
-    pairs = max(1, min(8, -(-4 * l2 // (sb + db))))
+    # > 4x L2 of rotation, and >= 2 GiB (up to 32 pairs) so independent copies may overlap (PDL) as in
+    # the headline loop
+    pairs = max(1, min(32, max(-(-4 * l2 // (sb + db)), (2 << 30) // (sb + db))))
     srcs = [torch.empty(sb, dtype=torch.uint8, device="cuda").random_() for _ in range(pairs)]
     dsts = [torch.empty(db, dtype=torch.uint8, device="cuda") for _ in range(pairs)]
     G = pairs * max(1, 32 // pairs) if sb < (1 << 27) else pairs
