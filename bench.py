@@ -530,8 +530,16 @@ def run_axe(args):
         if ws == 1 and not args.no_cpu_baseline:
             nthreads = os.cpu_count() or 1
             gbs, bands, sec = oracle_sample_seconds(args.cpu_seconds, nthreads)
+            gbs1, bands1, sec1 = oracle_sample_seconds(max(1.0, args.cpu_seconds / 4), 1)
+            model = None
+            try:
+                with open("/proc/cpuinfo") as f:
+                    model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), None)
+            except OSError:
+                pass
             cpu = {"value": gbs, "unit": "GB/s", "cores": nthreads, "kind": "oracle",
-                   "sample": f"{bands} 64-row bands of the config-2 conversion ({sec:.1f} s)"}
+                   "sample": f"{bands} 64-row bands of the config-2 conversion ({sec:.1f} s)",
+                   "value_1_thread": gbs1, "sample_1_thread": f"{bands1} bands ({sec1:.1f} s)", "cpu_model": model}
         out = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
