@@ -468,3 +468,35 @@ def test_k3_tma_with_destination_replicas(axe):
                dst_st=synth._regdump_storage(2 * tiles), seed=13)
     d = check(axe, cfg, "auto")
     assert d["kernel"] == "tma" and d["replicas"] == 2, d
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 31, 33])
+@pytest.mark.parametrize("es", [1, 2, 4, 8, 16])
+def test_degenerate_sizes(axe, n, es):
+    """Tiny and odd sizes (the degenerate cases of every kernel): a single element, odd extents, a reversed
+    order with an offset, and a replicated destination -- every forced kernel that accepts the plan."""
+    src = layout([(n, 1)])
+    dst = layout([(n, -1)], [(2, n)], {"m": n - 1})
+    cfg = dict(name=f"tiny{n}x{es}", es=es, src=src, src_st=linear_storage(n), dst=dst,
+               dst_st=linear_storage(2 * n + 3), seed=n * 16 + es)
+    check(axe, cfg, "auto")
+    for k in ("generic", "vector", "tile", "tma", "register", "tma_tile"):
+        try:
+            axe.CopyPlan(src, cfg["src_st"], dst, cfg["dst_st"], es, k)
+        except axe.AxeError:
+            continue
+        check(axe, cfg, k)
+
+
+@pytest.mark.parametrize("K,n", [(1, 1), (2, 1), (3, 5), (5, 3), (300, 1)])
+def test_degenerate_reductions(axe, K, n):
+    """Reductions with one output element, odd extents, and K > 256 over a single element."""
+    cfg = synth.reduce_local(K, 1, n, "i32")
+    vals = synth.numbers(K * n, "i32", K + n)
+    fill = synth.sentinel(n * 4, 3)
+    exp = fill.copy()
+    oracle.reduce(cfg["src"], cfg["src_st"], vals, cfg["dst"], cfg["dst_st"], exp, "i32")
+    s_dev, d_dev = torch.from_numpy(vals.copy()).cuda(), torch.from_numpy(fill.copy()).cuda()
+    axe.ReducePlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], "i32").execute(s_dev, d_dev)
+    torch.cuda.synchronize()
+    assert np.array_equal(d_dev.cpu().numpy(), exp)
