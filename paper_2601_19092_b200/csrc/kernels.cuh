@@ -185,6 +185,30 @@ struct K3Params {
   int dep;
 };
 
+// ------------------------------------------------ K6 granule transpose (config 3a)
+// A copy whose 16-byte source vectors, taken n = 16 / G at a time (G = the shared contiguous
+// granule, 4 or 8 bytes), form an n x n matrix of granules that the destination wants transposed:
+// n threads load n consecutive source vectors, transpose the granules with warp shuffles, and each
+// stores one 16-byte destination vector -- no shared memory.
+constexpr int K6_U = 4;  // groups per thread per tile
+struct K6Params {
+  uint32_t ngroups;                  // groups of n threads
+  int n;                             // 4 (4-byte granules) or 2 (8-byte granules)
+  // tiles of (256 / n) * K6_U groups: inner digits give every thread fixed offsets, outer digits a
+  // tile base (decoded once per tile)
+  uint32_t tile_g, ntiles;
+  int nin, nout;
+  FastDiv ifd[K1_MAXD], ofd[K1_MAXD];
+  int64_t iss[K1_MAXD], ids[K1_MAXD], oss[K1_MAXD], ods[K1_MAXD];  // bytes
+  int64_t sbase, dbase;
+  int64_t sstep;                     // bytes between the n source vectors of a group (16)
+  int64_t dpos[4];                   // destination offset of the vector holding granule position j
+  int nrep;
+  int64_t rep[K1_MAXREP];
+  Swz ssw, dsw;
+  int dep;
+};
+
 // ------------------------------------------------------- K4 reduce (§8(f) f3)
 // dst(y) = sum_k src(k * E_D(dst) + y) (reading R24).  Element types:
 enum DType { DT_F32 = 1, DT_F64 = 2, DT_F16 = 3, DT_BF16 = 4, DT_I32 = 5, DT_I64 = 6 };

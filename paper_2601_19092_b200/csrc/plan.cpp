@@ -215,6 +215,7 @@ static int env_kernel() {
   if (!strcmp(e, "tile")) return AXE_KERNEL_TILE;
   if (!strcmp(e, "register")) return AXE_KERNEL_REGISTER;
   if (!strcmp(e, "tma_tile")) return AXE_KERNEL_TMA_TILE;
+  if (!strcmp(e, "shuffle")) return AXE_KERNEL_SHUFFLE;
   return AXE_KERNEL_AUTO;
 }
 
@@ -879,6 +880,16 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
     if (kernel == AXE_KERNEL_REGISTER)
       AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced register kernel cannot run these layouts: %s", w3.c_str());
   }
+  if (joint && (kernel == AXE_KERNEL_AUTO || kernel == AXE_KERNEL_SHUFFLE)) {
+    std::string w6;
+    if (build_k6(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &w6)) {
+      P.kernel = KK_SHUFFLE;
+      *out = std::move(P);
+      return AXE_OK;
+    }
+    if (kernel == AXE_KERNEL_SHUFFLE)
+      AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced shuffle kernel cannot run these layouts: %s", w6.c_str());
+  }
   if (joint && kernel == AXE_KERNEL_TMA_TILE) {
     if (build_k2t(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &why)) {
       P.kernel = KK_TMA_TILE;
@@ -1034,6 +1045,12 @@ axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t 
       K3Params k = p.k3;
       k.dep = dep;
       e = launch_k3(k, p.blocks, src, dst, st);
+      break;
+    }
+    case KK_SHUFFLE: {
+      K6Params k = p.k6;
+      k.dep = dep;
+      e = launch_k6(k, p.blocks, src, dst, st);
       break;
     }
     case KK_TILE: {

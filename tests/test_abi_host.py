@@ -156,9 +156,9 @@ def test_config1_plan():
 def test_config3_plans_are_affine():
     for v in "ab":
         d = plan(synth.config3(64, v)).describe()
-        # 3a: 4-byte pieces, staged through shared memory (K2); 3b: the movmatrix atom on bulk-copied
+        # 3a: 4 x 4 transposes of 4-byte granules across lanes (K6); 3b: the movmatrix atom on bulk-copied
         # boxes in shared memory (K3-TMA); a forced "register" plan is the register kernel K3
-        assert d["kernel"] == {"a": "tile", "b": "tma"}[v], d
+        assert d["kernel"] == {"a": "shuffle", "b": "tma"}[v], d
     assert plan(synth.config3(64, "b"), "register").describe()["kernel"] == "register"
 
 

@@ -87,9 +87,11 @@ def test_config2_full(axe, rev, kernel):
     assert desc["kernel"] == ("tma" if kernel == "auto" else kernel)
 
 
-@pytest.mark.parametrize("kernel", ["auto", "generic", "vector", "tile", "register"])
+@pytest.mark.parametrize("kernel", ["auto", "generic", "vector", "tile", "register", "shuffle"])
 @pytest.mark.parametrize("variant", ["a", "b"])
 def test_config3_small(axe, variant, kernel):
+    if kernel == "shuffle" and variant == "b":  # 3b moves 2-byte elements: no 4-byte granule transpose
+        return
     if kernel == "register" and variant == "a":
         with pytest.raises(axe.AxeError):   # 3a moves data across warps: not a movmatrix atom
             axe.CopyPlan(synth.config3(16, "a")["src"], synth.config3(16, "a")["src_st"],
@@ -98,6 +100,8 @@ def test_config3_small(axe, variant, kernel):
     d = check(axe, synth.config3(16, variant), kernel)
     if variant == "b" and kernel == "auto":   # K3-TMA: bulk boxes + movmatrix in shared memory
         assert d["kernel"] == "tma" and d["mode"] == "bulk-load/movmatrix/bulk-store", d
+    if variant == "a" and kernel == "auto":   # K6: 4 x 4 transposes of 4-byte granules across lanes
+        assert d["kernel"] == "shuffle", d
 
 
 @pytest.mark.parametrize("variant", ["a", "b"])
