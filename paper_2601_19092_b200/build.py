@@ -33,7 +33,8 @@ def needs_build() -> bool:
     if not os.path.exists(OUT):
         return True
     t = os.path.getmtime(OUT)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.h*")) + [os.path.join(ROOT, "include", "axe.h"), __file__]
+    deps = (sources() + glob.glob(os.path.join(CSRC, "*.h*")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
+            [os.path.join(ROOT, "include", "axe.h"), __file__])
     return any(os.path.getmtime(d) > t for d in deps)
 
 

@@ -190,7 +190,10 @@ struct K3Params {
 // granule, 4 or 8 bytes), form an n x n matrix of granules that the destination wants transposed:
 // n threads load n consecutive source vectors, transpose the granules with warp shuffles, and each
 // stores one 16-byte destination vector -- no shared memory.
-constexpr int K6_U = 4;  // groups per thread per tile
+#ifndef AXE_K6_U
+#define AXE_K6_U 8  // measured on config 3a: U = 4: 1402 us, 8: 1358 us, 16: 1884 us (147 registers)
+#endif
+constexpr int K6_U = AXE_K6_U;  // groups per thread per tile
 struct K6Params {
   uint32_t ngroups;                  // groups of n threads
   int n;                             // 4 (4-byte granules) or 2 (8-byte granules)
