@@ -284,7 +284,7 @@ def test_tma_bulk_and_k3_tma_plans():
     assert plan(rows1k).describe()["kernel"] == "vector"
     assert plan(rows1k, "tma").describe()["kernel"] == "tma"
     d = plan(synth.config3(64, "b")).describe()
-    assert d["mode"] == "bulk-load/movmatrix/bulk-store" and d["box_bytes"] == 16384
+    assert d["mode"] == "bulk-load/movmatrix/bulk-store" and d["box_bytes"] == 8192
     # swizzled storages never take the bulk mode (bytes move verbatim)
     sw = dict(es=2, src=layout([(1 << 16, 1)]), src_st=linear_storage(1 << 16, synth.SW128),
               dst=layout([(1 << 16, 1)]), dst_st=linear_storage(1 << 16))
