@@ -221,7 +221,7 @@ typedef struct {
 
 /* Kernel choice for plans (flags of axe_copy_plan_create); AUTO picks from the
  * layouts.  The environment variable AXE_FORCE_KERNEL
- * (generic | vector | tma | tile | register | tma_tile | shuffle) overrides AUTO. */
+ * (generic | vector | tma | tile | register | tma_tile | shuffle | transpose) overrides AUTO. */
 enum {
   AXE_KERNEL_AUTO = 0,
   AXE_KERNEL_GENERIC = 1, /* K0: per-element evaluation of both layouts (always applicable) */
@@ -230,7 +230,8 @@ enum {
   AXE_KERNEL_TILE = 4,    /* K2: smem-staged tile permute / transpose                        */
   AXE_KERNEL_REGISTER = 5, /* K3: warp-register permute through movmatrix (b16 8x8 atoms)    */
   AXE_KERNEL_TMA_TILE = 6, /* K2T: TMA SW128 box staging + conflict-free gather (transposes)  */
-  AXE_KERNEL_SHUFFLE = 7   /* K6: n x n granule transpose across lanes with warp shuffles       */
+  AXE_KERNEL_SHUFFLE = 7,  /* K6: n x n granule transpose across lanes with warp shuffles       */
+  AXE_KERNEL_TRANSPOSE = 8 /* K7: smem tile + n x n register-block transpose (2-D transposes)   */
 };
 
 typedef struct axe_copy_plan axe_copy_plan;

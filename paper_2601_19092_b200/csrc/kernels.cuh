@@ -212,6 +212,26 @@ struct K6Params {
   int dep;
 };
 
+// ------------------------------------------------ K7 register-block transpose
+// A 2-D transpose of es = 2 / 4 / 8-byte elements (n = 16 / es): tiles of (32 n) source rows x
+// (8 n) source columns are staged in shared memory in source order (16-byte chunks XOR-swizzled by
+// (row / n) mod 8); each thread then loads an n x n element block with n LDS.128, transposes it in
+// registers (byte permutes for 2-byte elements, register renaming for 4-byte ones) and stores n
+// destination vectors; a warp's 32 threads take 32 consecutive row blocks, so each store
+// instruction writes 512 contiguous destination bytes.
+struct K7Params {
+  uint32_t ntiles;
+  int nd;                              // tile-index digits, outermost first
+  FastDiv fd[K1_MAXD];
+  int64_t ss[K1_MAXD], ds[K1_MAXD];    // bytes
+  int64_t sbase, dbase;
+  int64_t src_row, dst_col;            // bytes between source rows / destination columns
+  int cw;                              // chunk columns per warp (tile columns = 8 n cw)
+  int nrep;
+  int64_t rep[K1_MAXREP];
+  int dep;
+};
+
 // ------------------------------------------------------- K4 reduce (§8(f) f3)
 // dst(y) = sum_k src(k * E_D(dst) + y) (reading R24).  Element types:
 enum DType { DT_F32 = 1, DT_F64 = 2, DT_F16 = 3, DT_BF16 = 4, DT_I32 = 5, DT_I64 = 6 };

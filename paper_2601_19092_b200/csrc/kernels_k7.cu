@@ -1,0 +1,142 @@
+// kernels_k7.cu -- K7: register-block transpose through shared memory (sm_100a).
+//
+// Row-major -> column-major (any 2-D transpose of 2-, 4- or 8-byte elements).
+// The smem-staged K2 gathers one element per shared load (8 LDS.U16 per 16-byte
+// bf16 output) and is limited by the SM, not by HBM.  K7 reads n x n element
+// blocks with n LDS.128 (n = 16 / es) and transposes them in registers: for
+// 4-byte elements a block is just renamed, for 2-byte elements 4 PRMT build
+// each output word, for 8-byte elements the two halves swap.  Tile: 32 n source
+// rows x 8 n source columns (8 chunks of 16 bytes per row); warp w owns chunk
+// column w, lane l owns rows [n l, n l + n).  Chunk c of row r is stored at
+// chunk c ^ ((r / n) mod 8), so the 32 lanes of every LDS.128 read 8 distinct
+// chunk positions (4 wavefronts, the minimum for 512 bytes).
+#include <cuda_runtime.h>
+
+#include <atomic>
+
+#include "kernels.cuh"
+#include "launch.cuh"
+
+namespace axe {
+
+extern std::atomic<int64_t> g_launches;
+
+namespace {
+
+constexpr int K7_THREADS = 256;
+
+__device__ __forceinline__ uint4 ldg128(const uint8_t *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t word(const uint4 &v, int m) { return m == 0 ? v.x : m == 1 ? v.y : m == 2 ? v.z : v.w; }
+
+template <int ES, int CW>
+__global__ void __launch_bounds__(K7_THREADS) k7_transpose(const __grid_constant__ K7Params p,
+                                                           const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
+  constexpr int N = 16 / ES;          // elements per 16-byte vector
+  constexpr int TR = 32 * N;          // tile rows (source)
+  constexpr int CH = 8 * CW;          // 16-byte chunks per tile row (8 n CW columns; warp w owns w, w + 8, ..)
+  constexpr int LOADS = TR * CH / K7_THREADS;  // 16-byte loads per thread per tile
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (p.dep) pdl_wait();
+  pdl_launch_dependents();
+  for (uint32_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+    int64_t sb = p.sbase, db = p.dbase;
+    {
+      uint32_t i = tile;
+      for (int k = p.nd - 1; k >= 1; k--) {
+        const uint32_t q = fdiv(p.fd[k], i);
+        const uint32_t d = i - q * p.fd[k].d;
+        i = q;
+        sb += (int64_t)d * p.ss[k];
+        db += (int64_t)d * p.ds[k];
+      }
+      if (p.nd > 0) {
+        sb += (int64_t)i * p.ss[0];
+        db += (int64_t)i * p.ds[0];
+      }
+    }
+    // load: 8 consecutive threads read one 128-byte source row
+    uint4 v[LOADS];
+#pragma unroll
+    for (int u = 0; u < LOADS; u++) {
+      const int idx = t + u * K7_THREADS, r = idx / CH, c = idx % CH;
+      v[u] = ldg128(src + sb + (int64_t)r * p.src_row + c * 16);
+    }
+#pragma unroll
+    for (int u = 0; u < LOADS; u++) {
+      const int idx = t + u * K7_THREADS, r = idx / CH, c = idx % CH;
+      *reinterpret_cast<uint4 *>(sm + (r * CH + (c ^ ((r / N) & 7))) * 16) = v[u];  // XOR on the low 3 bits
+    }
+    __syncthreads();
+    // gather: lane = row block, warp (+ 8 cw) = chunk column
+#pragma unroll
+    for (int cw = 0; cw < CW; cw++) {
+    const int cc = warp + 8 * cw;
+    uint4 w[N];
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+      const int r = lane * N + i;
+      w[i] = *reinterpret_cast<const uint4 *>(sm + (r * CH + (cc ^ (lane & 7))) * 16);
+    }
+    const int64_t d0 = db + (int64_t)(cc * N) * p.dst_col + (int64_t)lane * 16;
+#pragma unroll
+    for (int k = 0; k < N; k++) {
+      uint4 o;
+      if constexpr (ES == 4) {
+        o = make_uint4(word(w[0], k), word(w[1], k), word(w[2], k), word(w[3], k));
+      } else if constexpr (ES == 2) {
+        const uint32_t sel = (k & 1) ? 0x7632u : 0x5410u;  // high or low halves of the rows' words
+        const int m = k >> 1;
+        o.x = __byte_perm(word(w[0], m), word(w[1], m), sel);
+        o.y = __byte_perm(word(w[2], m), word(w[3], m), sel);
+        o.z = __byte_perm(word(w[4], m), word(w[5], m), sel);
+        o.w = __byte_perm(word(w[6], m), word(w[7], m), sel);
+      } else {  // ES == 8: element k of rows 0 and 1
+        o = k == 0 ? make_uint4(w[0].x, w[0].y, w[1].x, w[1].y) : make_uint4(w[0].z, w[0].w, w[1].z, w[1].w);
+      }
+      const int64_t d = d0 + (int64_t)k * p.dst_col;
+      for (int r = 0; r < p.nrep; r++) *reinterpret_cast<uint4 *>(dst + d + p.rep[r]) = o;
+    }
+    }
+    __syncthreads();
+  }
+}
+
+template <int ES, int CW>
+cudaError_t go(const K7Params &p, unsigned blocks, const uint8_t *s, uint8_t *d, cudaStream_t st) {
+  constexpr int N = 16 / ES;
+  const size_t smem = (size_t)32 * N * 8 * CW * 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k7_transpose<ES, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  return launch_ex(k7_transpose<ES, CW>, dim3(blocks), dim3(K7_THREADS), smem, st, p, s, d);
+}
+
+}  // namespace
+
+cudaError_t launch_k7(const K7Params &p, int es, unsigned blocks, const void *src, void *dst, cudaStream_t st) {
+  const uint8_t *s = (const uint8_t *)src;
+  uint8_t *d = (uint8_t *)dst;
+  cudaError_t e;
+  switch (es) {
+    case 2: e = p.cw == 2 ? go<2, 2>(p, blocks, s, d, st) : go<2, 1>(p, blocks, s, d, st); break;
+    case 4: e = p.cw == 2 ? go<4, 2>(p, blocks, s, d, st) : go<4, 1>(p, blocks, s, d, st); break;
+    case 8: e = p.cw == 2 ? go<8, 2>(p, blocks, s, d, st) : go<8, 1>(p, blocks, s, d, st); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
+  g_launches++;
+  return cudaGetLastError();
+}
+
+}  // namespace axe

@@ -216,6 +216,7 @@ static int env_kernel() {
   if (!strcmp(e, "register")) return AXE_KERNEL_REGISTER;
   if (!strcmp(e, "tma_tile")) return AXE_KERNEL_TMA_TILE;
   if (!strcmp(e, "shuffle")) return AXE_KERNEL_SHUFFLE;
+  if (!strcmp(e, "transpose")) return AXE_KERNEL_TRANSPOSE;
   return AXE_KERNEL_AUTO;
 }
 
@@ -890,6 +891,16 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
     if (kernel == AXE_KERNEL_SHUFFLE)
       AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced shuffle kernel cannot run these layouts: %s", w6.c_str());
   }
+  if (joint && (kernel == AXE_KERNEL_AUTO || kernel == AXE_KERNEL_TRANSPOSE) && env_int("AXE_K7", 1)) {
+    std::string w7;
+    if (build_k7(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &w7)) {
+      P.kernel = KK_TRANSPOSE;
+      *out = std::move(P);
+      return AXE_OK;
+    }
+    if (kernel == AXE_KERNEL_TRANSPOSE)
+      AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced transpose kernel cannot run these layouts: %s", w7.c_str());
+  }
   if (joint && kernel == AXE_KERNEL_TMA_TILE) {
     if (build_k2t(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &why)) {
       P.kernel = KK_TMA_TILE;
@@ -1045,6 +1056,12 @@ axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t 
       K3Params k = p.k3;
       k.dep = dep;
       e = launch_k3(k, p.blocks, src, dst, st);
+      break;
+    }
+    case KK_TRANSPOSE: {
+      K7Params k = p.k7;
+      k.dep = dep;
+      e = launch_k7(k, p.es, p.blocks, src, dst, st);
       break;
     }
     case KK_SHUFFLE: {

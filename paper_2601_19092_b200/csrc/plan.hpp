@@ -13,7 +13,7 @@
 
 namespace axe {
 
-enum KernelKind { KK_GENERIC = 1, KK_VECTOR = 2, KK_TMA = 3, KK_TILE = 4, KK_REGISTER = 5, KK_TMA_TILE = 6, KK_SHUFFLE = 7 };
+enum KernelKind { KK_GENERIC = 1, KK_VECTOR = 2, KK_TMA = 3, KK_TILE = 4, KK_REGISTER = 5, KK_TMA_TILE = 6, KK_SHUFFLE = 7, KK_TRANSPOSE = 8 };
 
 struct CopyPlan {
   int kernel = KK_GENERIC;
@@ -44,6 +44,8 @@ struct CopyPlan {
   K3Params k3;
   // K6 granule transpose (warp shuffles)
   K6Params k6;
+  // K7 register-block transpose
+  K7Params k7;
   // K2T TMA-staged transpose (uses the tm_* tensor map of the source)
   K2TParams k2t;
   // host-buffer pipeline (axe_copy_plan_execute_host): the copy splits into n_chunks
@@ -71,7 +73,10 @@ cudaError_t launch_k3(const K3Params &p, unsigned blocks, const void *src, void 
 bool build_k3_bulk(CopyPlan *P, std::string *why);
 bool build_k6(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,
               const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why);
-cudaError_t launch_k6(const K6Params &p, unsigned blocks, const void *src, void *dst, cudaStream_t st);  // K3 as K1-TMA mode 2 + movmatrix in smem
+cudaError_t launch_k6(const K6Params &p, unsigned blocks, const void *src, void *dst, cudaStream_t st);
+bool build_k7(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,
+              const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why);
+cudaError_t launch_k7(const K7Params &p, int es, unsigned blocks, const void *src, void *dst, cudaStream_t st);  // K3 as K1-TMA mode 2 + movmatrix in smem
 bool build_k2t(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,
                const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why);
 cudaError_t launch_k2t(const void *map128, const K2TParams &p, int es, unsigned blocks, void *dst, cudaStream_t st);

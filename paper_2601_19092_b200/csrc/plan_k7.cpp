@@ -1,0 +1,111 @@
+// plan_k7.cpp -- planner of K7, the register-block transpose (kernels_k7.cu).
+//
+// The copy qualifies when its joint digits (element strides) contain a digit a
+// contiguous on the source (source stride 1: the columns of a source row) and
+// a digit b contiguous on the destination (destination stride 1: the rows of a
+// destination column) -- a 2-D transpose -- with 2-, 4- or 8-byte elements,
+// a multiple of 8 n columns and 32 n rows (n = 16 / es), and every other digit
+// (and both row / column pitches) moving whole 16-byte vectors.  The tiles are
+// (32 n rows) x (16 n or 8 n columns); the other digits and the outer parts of a
+// and b index tiles.  The paper's dispatch matches layouts against instruction
+// atoms; this atom is LDS.128 + an n x n register transpose.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "plan.hpp"
+
+namespace axe {
+
+int num_sms();
+
+bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, const Storage &sst,
+              const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why) {
+  auto fail = [&](const char *m) {
+    *why = m;
+    return false;
+  };
+  if (es != 2 && es != 4 && es != 8) return fail("transpose: 2-, 4- or 8-byte elements");
+  if (max_align < 16) return fail("transpose: needs 16-byte aligned buffers");
+  if (sst.swz_b || dstst.swz_b) return fail("transpose: swizzled storage");
+  const int64_t n = 16 / es;
+  // chunk columns per warp: 2 (tiles of 32 n x 16 n) when the columns allow it, measured on 8192^2
+  // transposes bf16 43.2 / fp32 100.6 / fp64 94.2 us against 44.9 / 104.5 / 94.3 with 1
+  const char *cwe = getenv("AXE_K7_CW");
+  int64_t cw = (cwe && *cwe) ? std::max(1, std::min(2, atoi(cwe))) : 2;
+  std::vector<Joint> J;
+  for (auto &j : J0)
+    if (j.e > 1) J.push_back(j);
+  int a = -1, b = -1;
+  for (int i = 0; i < (int)J.size(); i++) {
+    if (J[i].ss == 1 && J[i].ds != 1) a = i;
+    if (J[i].ds == 1 && J[i].ss != 1) b = i;
+  }
+  if (a < 0 || b < 0) return fail("transpose: no source-contiguous and destination-contiguous digit pair");
+  const Joint A = J[a], B = J[b];
+  if (cw == 2 && A.e % (16 * n)) cw = 1;
+  const int64_t TC = 8 * n * cw, TR = 32 * n;
+  if (A.e % TC || B.e % TR) return fail("transpose: extents are not whole tiles");
+  auto v16 = [&](int64_t s) { return (s * es) % 16 == 0; };
+  if (!v16(A.ds) || !v16(B.ss) || A.ds < 0 || B.ss < 0) return fail("transpose: row / column pitch not 16-byte aligned");
+  if (!v16(ls.base) || !v16(ld.base)) return fail("transpose: bases not 16-byte aligned");
+  std::vector<Joint> outer;
+  for (int i = 0; i < (int)J.size(); i++) {
+    if (i == a || i == b) continue;
+    if (!v16(J[i].ss) || !v16(J[i].ds)) return fail("transpose: a digit moves partial vectors");
+    outer.push_back(J[i]);
+  }
+  if (A.e / TC > 1) outer.push_back(Joint{A.e / TC, TC, TC * A.ds});
+  if (B.e / TR > 1) outer.push_back(Joint{B.e / TR, TR * B.ss, TR});
+  std::stable_sort(outer.begin(), outer.end(), [](const Joint &x, const Joint &y) { return std::llabs(x.ds) > std::llabs(y.ds); });
+  sort_fuse_outer(outer);
+  if ((int)outer.size() > K1_MAXD) return fail("transpose: too many tile digits");
+  int64_t nt = 1;
+  for (auto &o : outer) nt *= o.e;
+  if (nt >= (int64_t(1) << 32)) return fail("transpose: too many tiles");
+  std::vector<int64_t> reps{0};
+  for (auto &r : ld.R) {
+    std::vector<int64_t> nx;
+    for (int64_t x : reps)
+      for (int64_t d = 0; d < r.e; d++) nx.push_back(x + d * r.s);
+    reps.swap(nx);
+    if (reps.size() > 4096) break;
+  }
+  std::sort(reps.begin(), reps.end());
+  reps.erase(std::unique(reps.begin(), reps.end()), reps.end());
+  if ((int)reps.size() > K1_MAXREP) return fail("transpose: too many replicas");
+  for (int64_t r : reps)
+    if (!v16(r)) return fail("transpose: replica offsets not 16-byte aligned");
+  K7Params &k = P->k7;
+  memset(&k, 0, sizeof(k));
+  k.ntiles = (uint32_t)nt;
+  k.nd = (int)outer.size();
+  for (int i = 0; i < k.nd; i++) {
+    k.fd[i] = make_fastdiv((uint32_t)outer[i].e);
+    k.ss[i] = outer[i].ss * es;
+    k.ds[i] = outer[i].ds * es;
+  }
+  k.sbase = ls.base * es;
+  k.dbase = ld.base * es;
+  k.src_row = B.ss * es;
+  k.dst_col = A.ds * es;
+  k.cw = (int)cw;
+  k.nrep = (int)reps.size();
+  for (size_t i = 0; i < reps.size(); i++) k.rep[i] = reps[i] * es;
+  P->align = 16;
+  const int64_t tile_bytes = TR * TC * es;
+  const int per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(8, (220 * 1024) / (tile_bytes + 1024)));
+  P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt, (int64_t)num_sms() * per_sm));
+  int64_t total = 1;
+  for (auto &j : J0) total *= j.e;
+  P->covers_all = (int64_t)reps.size() * total == dstst.cells;
+  char buf[256];
+  snprintf(buf, sizeof buf,
+           "{\"kernel\":\"transpose\",\"block\":\"%lldx%lld register transpose\",\"tile\":[%lld,%lld],\"tiles\":%lld,"
+           "\"ctas\":%u,\"replicas\":%d,\"joint\":",
+           (long long)n, (long long)n, (long long)TR, (long long)TC, (long long)nt, P->blocks, k.nrep);
+  P->desc = std::string(buf) + joint_json(J0) + "}";
+  return true;
+}
+
+}  // namespace axe

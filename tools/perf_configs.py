@@ -47,6 +47,7 @@ CONFIGS = {
                             dst_st=synth.linear_storage(65536 * 512), seed=5),
     "transpose_bf16": lambda: transpose_cfg(8192, 8192, 2),
     "transpose_f32": lambda: transpose_cfg(8192, 8192, 4),
+    "transpose_f64": lambda: transpose_cfg(8192, 4096, 8),
 }
 
 
