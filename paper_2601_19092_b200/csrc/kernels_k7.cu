@@ -130,8 +130,12 @@ cudaError_t launch_k7(const K7Params &p, int es, unsigned blocks, const void *sr
   cudaError_t e;
   switch (es) {
     case 2: e = p.cw == 2 ? go<2, 2>(p, blocks, s, d, st) : go<2, 1>(p, blocks, s, d, st); break;
-    case 4: e = p.cw == 2 ? go<4, 2>(p, blocks, s, d, st) : go<4, 1>(p, blocks, s, d, st); break;
-    case 8: e = p.cw == 2 ? go<8, 2>(p, blocks, s, d, st) : go<8, 1>(p, blocks, s, d, st); break;
+    case 4:
+      e = p.cw == 4 ? go<4, 4>(p, blocks, s, d, st) : p.cw == 2 ? go<4, 2>(p, blocks, s, d, st) : go<4, 1>(p, blocks, s, d, st);
+      break;
+    case 8:
+      e = p.cw == 4 ? go<8, 4>(p, blocks, s, d, st) : p.cw == 2 ? go<8, 2>(p, blocks, s, d, st) : go<8, 1>(p, blocks, s, d, st);
+      break;
     default: return cudaErrorInvalidValue;
   }
   if (e != cudaSuccess) return e;

@@ -29,10 +29,12 @@ bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   if (max_align < 16) return fail("transpose: needs 16-byte aligned buffers");
   if (sst.swz_b || dstst.swz_b) return fail("transpose: swizzled storage");
   const int64_t n = 16 / es;
-  // chunk columns per warp: 2 (tiles of 32 n x 16 n) when the columns allow it, measured on 8192^2
-  // transposes bf16 43.2 / fp32 100.6 / fp64 94.2 us against 44.9 / 104.5 / 94.3 with 1
+  // chunk columns per warp (tiles of 32 n rows x 8 n cw columns), as wide as the columns allow:
+  // 4 for 4-byte elements (8192^2 fp32: 94.9 us vs 100.8 / 104.3 with 2 / 1), 2 otherwise (bf16:
+  // 43.2 us vs 44.9 with 1; 8192x4096 fp64: 94.1 us vs 98.6 with 4)
   const char *cwe = getenv("AXE_K7_CW");
-  int64_t cw = (cwe && *cwe) ? std::max(1, std::min(2, atoi(cwe))) : 2;
+  const int cwmax = es == 4 ? 4 : 2;
+  int64_t cw = (cwe && *cwe) ? std::max(1, std::min(cwmax, atoi(cwe))) : cwmax;
   std::vector<Joint> J;
   for (auto &j : J0)
     if (j.e > 1) J.push_back(j);
@@ -43,7 +45,7 @@ bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   }
   if (a < 0 || b < 0) return fail("transpose: no source-contiguous and destination-contiguous digit pair");
   const Joint A = J[a], B = J[b];
-  if (cw == 2 && A.e % (16 * n)) cw = 1;
+  while (cw > 1 && A.e % (8 * n * cw)) cw /= 2;
   const int64_t TC = 8 * n * cw, TR = 32 * n;
   if (A.e % TC || B.e % TR) return fail("transpose: extents are not whole tiles");
   auto v16 = [&](int64_t s) { return (s * es) % 16 == 0; };
