@@ -252,6 +252,7 @@ struct K4Params {
   int nrep;
   int64_t rep[K1_MAXREP];
   Swz ssw, dsw;
+  uint32_t box_bytes;                  // bulk form: output bytes per box (total counts boxes)
   int dep;
 };
 // one-sided (pull) form: summand k is read through its own base pointer (a peer's buffer)

@@ -135,7 +135,7 @@ Swz make_swz(const Storage &st);
 
 // ---- K4 reduction over the leading logical dimension (plan_reduce.cpp, kernels_reduce.cu)
 struct ReducePlan {
-  int kind = 0;          // 1: generic (k4_generic), 2: vector (k4_reduce)
+  int kind = 0;          // 1: generic (k4_generic), 2: vector (k4_reduce), 3: bulk boxes (k4_bulk)
   int dtype = 0, es = 0;
   int64_t K = 1;         // summands per output element
   int64_t src_bytes = 0, dst_bytes = 0;
@@ -152,6 +152,8 @@ axe_status run_reduce(const ReducePlan &p, const void *src, void *dst, cudaStrea
 cudaError_t launch_k4(const K4Params &p, int dtype, int vb, unsigned blocks, const void *src, void *dst,
                       cudaStream_t st);
 cudaError_t launch_k4g(const K4GParams &p, int dtype, const void *src, void *dst, cudaStream_t st);
+cudaError_t launch_k4_bulk(const K4Params &p, int dtype, unsigned blocks, const void *src, void *dst,
+                           cudaStream_t st);
 cudaError_t launch_k4_multimem(const K4Params &p, int dtype, unsigned blocks, const void *mc, void *dst,
                                cudaStream_t st);
 cudaError_t launch_k4_peer(const K4Params &p, const K4Ptrs &q, int dtype, int vb, unsigned blocks, void *dst,

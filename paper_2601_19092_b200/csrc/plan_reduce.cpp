@@ -8,6 +8,7 @@
 // Joint digits with destination stride 0 are the reduction digits; the others
 // index output vectors.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -16,6 +17,11 @@
 #include "handles.hpp"
 
 namespace axe {
+
+static int64_t env_int_r(const char *name, int64_t dflt) {
+  const char *e = getenv(name);
+  return (e && *e) ? atoll(e) : dflt;
+}
 
 int dtype_size(int dt) {
   switch (dt) {
@@ -108,11 +114,43 @@ axe_status plan_reduce(const Layout &S, const Storage &sst, const Layout &D, con
         if (ok) V = v;
       }
     }
+    // bulk form (k4_bulk): the innermost output run, contiguous on both sides, cut into boxes of
+    // box_bytes moved by cp.async.bulk per summand; every other output digit moves whole boxes
+    std::vector<Joint> Yb;
+    int64_t box = 0;
+    {
+      const int64_t bb = env_int_r("AXE_K4_BULK_BOX", 4096);
+      const bool table = P.K <= K4_MAXK, nosw = !sst.swz_b && !dstst.swz_b;
+      // K = 8 bf16 / f32 (8192 x 4096 outputs): 93.8 / 92.6 us vs 95.1 / 95.2 with k4_reduce; K = 2
+      // (16384 x 8192): 148 us vs 130 -- two 4 KiB summand boxes per stage keep too little in flight
+      const int64_t min_k = env_int_r("AXE_K4_BULK_MIN_K", 4);
+      if (bb > 0 && P.K >= min_k && table && nosw && !Y.empty() && Y.back().ss == 1 && Y.back().ds == 1 &&
+          (Y.back().e * es) % bb == 0 && P.K * bb <= 48 * 1024 && bb % 16 == 0) {
+        const int64_t be = bb / es;
+        std::vector<int64_t> all{ls.base, ld.base};
+        for (size_t k = 0; k + 1 < Y.size(); k++) {
+          all.push_back(Y[k].ss);
+          all.push_back(Y[k].ds);
+        }
+        for (auto &j : Kd) all.push_back(j.ss);
+        for (int64_t r : reps) all.push_back(r);
+        bool ok = true;
+        for (int64_t a : all) ok = ok && (a * es) % 16 == 0;
+        if (ok) {
+          Yb.assign(Y.begin(), Y.end() - 1);
+          if (Y.back().e / be > 1) Yb.push_back(Joint{Y.back().e / be, be, be});
+          std::stable_sort(Yb.begin(), Yb.end(), [](const Joint &a, const Joint &b) { return std::llabs(a.ds) > std::llabs(b.ds); });
+          sort_fuse_outer(Yb);
+          box = bb;
+        }
+      }
+    }
     if (V > 1) {
       Joint last = Y.back();
       Y.pop_back();
       if (last.e / V > 1) Y.push_back(Joint{last.e / V, V, V});
     }
+    if (box) Y = Yb;  // the bulk form indexes boxes instead of vectors
     // destination-contiguous output digits first (every warp writes whole lines)
     std::stable_sort(Y.begin(), Y.end(), [](const Joint &a, const Joint &b) { return std::llabs(a.ds) > std::llabs(b.ds); });
     sort_fuse_outer(Y);
@@ -155,16 +193,24 @@ axe_status plan_reduce(const Layout &S, const Storage &sst, const Layout &D, con
           k.kss[t] = Kd[t].ss * es;
         }
       }
-      P.kind = 2;
-      P.vb = (int)(V * es);
+      P.kind = box ? 3 : 2;
+      P.vb = box ? 16 : (int)(V * es);
       P.align = P.vb;
-      const int64_t blocks = (total + 255) / 256, cap = (int64_t)num_sms() * 8;
-      P.blocks = (unsigned)std::max<int64_t>(1, std::min(blocks, cap));
+      k.box_bytes = (uint32_t)box;
+      if (box) {  // 2 stages of K boxes per CTA
+        const int64_t smem = 2 * P.K * box + 1024;
+        const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(16, (220 * 1024) / smem));
+        P.blocks = (unsigned)std::max<int64_t>(1, std::min(total, (int64_t)num_sms() * per_sm));
+      } else {
+        const int64_t blocks = (total + 255) / 256, cap = (int64_t)num_sms() * 8;
+        P.blocks = (unsigned)std::max<int64_t>(1, std::min(blocks, cap));
+      }
       char b[256];
       snprintf(b, sizeof b,
-               "{\"kernel\":\"reduce\",\"dtype\":\"%s\",\"K\":%lld,\"vec_bytes\":%d,\"vectors\":%lld,\"replicas\":%d,"
-               "\"blocks\":%u,\"table\":%d,\"digits\":",
-               dtype_name(dtype), (long long)P.K, P.vb, (long long)total, k.nrep, P.blocks, k.nk > 0);
+               "{\"kernel\":\"reduce\",\"mode\":\"%s\",\"dtype\":\"%s\",\"K\":%lld,\"vec_bytes\":%d,\"%s\":%lld,"
+               "\"replicas\":%d,\"blocks\":%u,\"table\":%d,\"box_bytes\":%lld,\"digits\":",
+               box ? "bulk" : "vector", dtype_name(dtype), (long long)P.K, P.vb, box ? "boxes" : "vectors",
+               (long long)total, k.nrep, P.blocks, k.nk > 0, (long long)box);
       P.desc = std::string(b) + joint_json(Y) + ",\"reduce_digits\":" + joint_json(Kd) + "}";
       *out = std::move(P);
       return AXE_OK;
@@ -194,7 +240,11 @@ axe_status run_reduce(const ReducePlan &p, const void *src, void *dst, cudaStrea
   if (s < d + p.dst_bytes && d < s + p.src_bytes) AXE_FAIL(AXE_ERR_ALIAS, "source and destination buffers overlap");
   const int dep = stream_dependency(st, s, s + p.src_bytes, d, d + p.dst_bytes);
   cudaError_t e;
-  if (p.kind == 2) {
+  if (p.kind == 3) {
+    K4Params k = p.k4;
+    k.dep = dep;
+    e = launch_k4_bulk(k, p.dtype, p.blocks, src, dst, st);
+  } else if (p.kind == 2) {
     K4Params k = p.k4;
     k.dep = dep;
     e = launch_k4(k, p.dtype, p.vb, p.blocks, src, dst, st);

@@ -56,7 +56,9 @@ def test_reduce_scatter_plan(P):
         # each rank sends its partial of every other rank's rows and receives P-1 partials of its own
         assert ex["send_elems"] == (P - 1) * 64 * 64 // P == ex["recv_elems"]
         assert ex["packs"] == 0 and ex["unpacks"] == 0  # partial rows and stage slabs are contiguous
-        assert d["reduce"]["K"] == P and d["reduce"]["vectors"] * 8 == 64 * 64 // P
+        red = d["reduce"]
+        moved = red["boxes"] * red["box_bytes"] if red["mode"] == "bulk" else red["vectors"] * 16
+        assert red["K"] == P and moved == 64 * 64 // P * 2
 
 
 @pytest.mark.parametrize("P", [2, 4, 8])
