@@ -121,9 +121,10 @@ axe_status plan_reduce(const Layout &S, const Storage &sst, const Layout &D, con
     {
       const int64_t bb = env_int_r("AXE_K4_BULK_BOX", 4096);
       const bool table = P.K <= K4_MAXK, nosw = !sst.swz_b && !dstst.swz_b;
-      // K = 8 bf16 / f32 (8192 x 4096 outputs): 93.8 / 92.6 us vs 95.1 / 95.2 with k4_reduce; K = 2
-      // (16384 x 8192): 148 us vs 130 -- two 4 KiB summand boxes per stage keep too little in flight
-      const int64_t min_k = env_int_r("AXE_K4_BULK_MIN_K", 4);
+      // K = 8 bf16 / f32 (8192 x 4096 outputs): 93.8-94.1 / 92.6 us vs 95.1-96.6 / 95.2 with k4_reduce;
+      // K = 16 (4096^2): 82.0 vs 81.5; K = 4 (16384 x 4096): 109.3 vs 105.2; K = 2 (16384 x 8192): 148
+      // vs 130 -- with few summands a 2-stage ring of K boxes keeps too little in flight per CTA
+      const int64_t min_k = env_int_r("AXE_K4_BULK_MIN_K", 8);
       if (bb > 0 && P.K >= min_k && table && nosw && !Y.empty() && Y.back().ss == 1 && Y.back().ds == 1 &&
           (Y.back().e * es) % bb == 0 && P.K * bb <= 48 * 1024 && bb % 16 == 0) {
         const int64_t be = bb / es;
