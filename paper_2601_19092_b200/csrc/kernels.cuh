@@ -253,6 +253,8 @@ struct K4Params {
   int64_t rep[K1_MAXREP];
   Swz ssw, dsw;
   uint32_t box_bytes;                  // bulk form: output bytes per box (total counts boxes)
+  int stages;                          // bulk form: ring stages (2..4), K boxes each
+  int threads;                         // bulk form: CTA size (128 or 256)
   int dep;
 };
 // one-sided (pull) form: summand k is read through its own base pointer (a peer's buffer)

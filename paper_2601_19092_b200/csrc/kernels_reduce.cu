@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(K4_THREADS) k4_multimem(const __grid_constant_
 // Bulk form: output boxes contiguous on the destination and on every summand's slab.  One thread
 // issues the K cp.async.bulk loads of a box (one per summand) into a 2-stage ring; all threads then
 // sum the box from shared memory in k order (same arithmetic as k4_reduce) and store it.
-constexpr int K4B_THREADS = 128;
+constexpr int K4B_THREADS = 256;  // launch bound; the plan picks 128 or 256
 template <int DT>
 __global__ void __launch_bounds__(K4B_THREADS) k4_bulk(const __grid_constant__ K4Params p,
                                                        const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
@@ -316,12 +316,12 @@ __global__ void __launch_bounds__(K4B_THREADS) k4_bulk(const __grid_constant__ K
   using A = typename O::A;
   constexpr int V = 16 / (int)sizeof(S);
   extern __shared__ __align__(128) uint8_t sm[];
-  __shared__ __align__(8) uint64_t full[2];
+  __shared__ __align__(8) uint64_t full[4];
   const int t = threadIdx.x;
   const uint32_t B = p.box_bytes, K = (uint32_t)p.nk, stage = K * B;
+  const uint32_t NS = (uint32_t)p.stages;
   if (t == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
+    for (uint32_t s = 0; s < NS; s++) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
   }
@@ -342,23 +342,21 @@ __global__ void __launch_bounds__(K4B_THREADS) k4_bulk(const __grid_constant__ K
     }
   };
   auto issue = [&](uint32_t k) {
-    const int s = (int)(k & 1u);
+    const uint32_t s = k % NS;
     int64_t so, dof;
     offs(first + k * step, so, dof);
     mbar_expect_tx(&full[s], stage);
     for (uint32_t kk = 0; kk < K; kk++) bulk_load(sm + s * stage + kk * B, src + so + p.koff[kk], B, &full[s]);
   };
-  if (t == 0) {
-    if (mine > 0) issue(0);
-    if (mine > 1) issue(1);
-  }
+  if (t == 0)
+    for (uint32_t k = 0; k < NS && k < mine; k++) issue(k);
   for (uint32_t k = 0; k < mine; k++) {
-    const int s = (int)(k & 1u);
-    mbar_wait(&full[s], (k >> 1) & 1u);
+    const uint32_t s = k % NS;
+    mbar_wait(&full[s], (k / NS) & 1u);
     int64_t so, dof;
     offs(first + k * step, so, dof);
     const uint8_t *base = sm + s * stage;
-    for (uint32_t v = t; v < B / 16; v += K4B_THREADS) {
+    for (uint32_t v = t; v < B / 16; v += blockDim.x) {
       A acc[V];
 #pragma unroll
       for (int e = 0; e < V; e++) acc[e] = A(0);
@@ -375,7 +373,7 @@ __global__ void __launch_bounds__(K4B_THREADS) k4_bulk(const __grid_constant__ K
         *reinterpret_cast<uint4 *>(dst + dof + p.rep[r] + v * 16) = *reinterpret_cast<const uint4 *>(o);
     }
     __syncthreads();  // stage s consumed by every thread
-    if (t == 0 && k + 2 < mine) issue(k + 2);
+    if (t == 0 && k + NS < mine) issue(k + NS);
   }
 }
 
@@ -421,8 +419,8 @@ cudaError_t launch_k4_bulk(const K4Params &p, int dtype, unsigned blocks, const 
                            cudaStream_t st) {
   const uint8_t *s = (const uint8_t *)src;
   uint8_t *d = (uint8_t *)dst;
-  const size_t smem = 2 * (size_t)p.nk * p.box_bytes;
-  const dim3 g(blocks), b(K4B_THREADS);
+  const size_t smem = (size_t)p.stages * p.nk * p.box_bytes;
+  const dim3 g(blocks), b(p.threads);
   static bool attr[8] = {};
   auto prep = [&](const void *kern) -> cudaError_t {
     if (attr[dtype]) return cudaSuccess;

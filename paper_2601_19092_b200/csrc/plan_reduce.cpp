@@ -198,8 +198,10 @@ axe_status plan_reduce(const Layout &S, const Storage &sst, const Layout &D, con
       P.vb = box ? 16 : (int)(V * es);
       P.align = P.vb;
       k.box_bytes = (uint32_t)box;
-      if (box) {  // 2 stages of K boxes per CTA
-        const int64_t smem = 2 * P.K * box + 1024;
+      if (box) {  // a ring of K boxes per stage per CTA
+        k.stages = (int)std::max<int64_t>(2, std::min<int64_t>(4, env_int_r("AXE_K4_BULK_STAGES", 2)));
+        k.threads = env_int_r("AXE_K4_BULK_THREADS", 128) > 128 ? 256 : 128;
+        const int64_t smem = k.stages * P.K * box + 1024;
         const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(16, (220 * 1024) / smem));
         P.blocks = (unsigned)std::max<int64_t>(1, std::min(total, (int64_t)num_sms() * per_sm));
       } else {
@@ -209,9 +211,9 @@ axe_status plan_reduce(const Layout &S, const Storage &sst, const Layout &D, con
       char b[256];
       snprintf(b, sizeof b,
                "{\"kernel\":\"reduce\",\"mode\":\"%s\",\"dtype\":\"%s\",\"K\":%lld,\"vec_bytes\":%d,\"%s\":%lld,"
-               "\"replicas\":%d,\"blocks\":%u,\"table\":%d,\"box_bytes\":%lld,\"digits\":",
+               "\"replicas\":%d,\"blocks\":%u,\"table\":%d,\"box_bytes\":%lld,\"stages\":%d,\"threads\":%d,\"digits\":",
                box ? "bulk" : "vector", dtype_name(dtype), (long long)P.K, P.vb, box ? "boxes" : "vectors",
-               (long long)total, k.nrep, P.blocks, k.nk > 0, (long long)box);
+               (long long)total, k.nrep, P.blocks, k.nk > 0, (long long)box, k.stages, k.threads);
       P.desc = std::string(b) + joint_json(Y) + ",\"reduce_digits\":" + joint_json(Kd) + "}";
       *out = std::move(P);
       return AXE_OK;
