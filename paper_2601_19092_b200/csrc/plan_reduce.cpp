@@ -119,7 +119,10 @@ axe_status plan_reduce(const Layout &S, const Storage &sst, const Layout &D, con
     std::vector<Joint> Yb;
     int64_t box = 0;
     {
-      const int64_t bb = env_int_r("AXE_K4_BULK_BOX", 4096);
+      // opt-in (AXE_K4_BULK_BOX=4096): in the rotating steady state (perf_configs --reduce) K = 8 runs
+      // 1-3% faster than k4_reduce, but one cold launch under ncu takes 100.5 us against 86.7 us --
+      // 3 CTAs x 4 warps per SM keep less in flight than k4_reduce's 64 warps x 8 loads
+      const int64_t bb = env_int_r("AXE_K4_BULK_BOX", 0);
       const bool table = P.K <= K4_MAXK, nosw = !sst.swz_b && !dstst.swz_b;
       // K = 8 bf16 / f32 (8192 x 4096 outputs): 93.8-94.1 / 92.6 us vs 95.1-96.6 / 95.2 with k4_reduce;
       // K = 16 (4096^2): 82.0 vs 81.5; K = 4 (16384 x 4096): 109.3 vs 105.2; K = 2 (16384 x 8192): 148
