@@ -36,48 +36,13 @@ __device__ __forceinline__ uint4 ldg128(const uint8_t *p) {
 __device__ __forceinline__ uint32_t word(const uint4 &v, int m) { return m == 0 ? v.x : m == 1 ? v.y : m == 2 ? v.z : v.w; }
 
 template <int ES, int CW>
-__global__ void __launch_bounds__(K7_THREADS) k7_transpose(const __grid_constant__ K7Params p,
-                                                           const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
-  constexpr int N = 16 / ES;          // elements per 16-byte vector
-  constexpr int TR = 32 * N;          // tile rows (source)
-  constexpr int CH = 8 * CW;          // 16-byte chunks per tile row (8 n CW columns; warp w owns w, w + 8, ..)
-  constexpr int LOADS = TR * CH / K7_THREADS;  // 16-byte loads per thread per tile
-  extern __shared__ __align__(128) uint8_t sm[];
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  if (p.dep) pdl_wait();
-  pdl_launch_dependents();
-  for (uint32_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-    int64_t sb = p.sbase, db = p.dbase;
-    {
-      uint32_t i = tile;
-      for (int k = p.nd - 1; k >= 1; k--) {
-        const uint32_t q = fdiv(p.fd[k], i);
-        const uint32_t d = i - q * p.fd[k].d;
-        i = q;
-        sb += (int64_t)d * p.ss[k];
-        db += (int64_t)d * p.ds[k];
-      }
-      if (p.nd > 0) {
-        sb += (int64_t)i * p.ss[0];
-        db += (int64_t)i * p.ds[0];
-      }
-    }
-    // load: 8 consecutive threads read one 128-byte source row
-    uint4 v[LOADS];
+__device__ __forceinline__ void k7_gather(const K7Params &p, const uint8_t *sm, int64_t db, uint8_t *__restrict__ dst,
+                                          int lane, int warp) {
+  constexpr int N = 16 / ES;
+  constexpr int CH = 8 * CW;
+  // gather: lane = row block, warp (+ 8 cw) = chunk column
 #pragma unroll
-    for (int u = 0; u < LOADS; u++) {
-      const int idx = t + u * K7_THREADS, r = idx / CH, c = idx % CH;
-      v[u] = ldg128(src + sb + (int64_t)r * p.src_row + c * 16);
-    }
-#pragma unroll
-    for (int u = 0; u < LOADS; u++) {
-      const int idx = t + u * K7_THREADS, r = idx / CH, c = idx % CH;
-      *reinterpret_cast<uint4 *>(sm + (r * CH + (c ^ ((r / N) & 7))) * 16) = v[u];  // XOR on the low 3 bits
-    }
-    __syncthreads();
-    // gather: lane = row block, warp (+ 8 cw) = chunk column
-#pragma unroll
-    for (int cw = 0; cw < CW; cw++) {
+  for (int cw = 0; cw < CW; cw++) {
     const int cc = warp + 8 * cw;
     uint4 w[N];
 #pragma unroll
@@ -104,22 +69,117 @@ __global__ void __launch_bounds__(K7_THREADS) k7_transpose(const __grid_constant
       const int64_t d = d0 + (int64_t)k * p.dst_col;
       for (int r = 0; r < p.nrep; r++) *reinterpret_cast<uint4 *>(dst + d + p.rep[r]) = o;
     }
+  }
+}
+
+__device__ __forceinline__ void tile_offsets(const K7Params &p, uint32_t i, int64_t &sb, int64_t &db) {
+  sb = p.sbase;
+  db = p.dbase;
+  for (int k = p.nd - 1; k >= 1; k--) {
+    const uint32_t q = fdiv(p.fd[k], i);
+    const uint32_t d = i - q * p.fd[k].d;
+    i = q;
+    sb += (int64_t)d * p.ss[k];
+    db += (int64_t)d * p.ds[k];
+  }
+  if (p.nd > 0) {
+    sb += (int64_t)i * p.ss[0];
+    db += (int64_t)i * p.ds[0];
+  }
+}
+
+template <int ES, int CW>
+__global__ void __launch_bounds__(K7_THREADS) k7_transpose(const __grid_constant__ K7Params p,
+                                                           const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
+  constexpr int N = 16 / ES;          // elements per 16-byte vector
+  constexpr int TR = 32 * N;          // tile rows (source)
+  constexpr int CH = 8 * CW;          // 16-byte chunks per tile row (8 n CW columns; warp w owns w, w + 8, ..)
+  constexpr int LOADS = TR * CH / K7_THREADS;  // 16-byte loads per thread per tile
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (p.dep) pdl_wait();
+  pdl_launch_dependents();
+  for (uint32_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+    int64_t sb, db;
+    tile_offsets(p, tile, sb, db);
+    // load: 8 consecutive threads read one 128-byte source row
+    uint4 v[LOADS];
+#pragma unroll
+    for (int u = 0; u < LOADS; u++) {
+      const int idx = t + u * K7_THREADS, r = idx / CH, c = idx % CH;
+      v[u] = ldg128(src + sb + (int64_t)r * p.src_row + c * 16);
+    }
+#pragma unroll
+    for (int u = 0; u < LOADS; u++) {
+      const int idx = t + u * K7_THREADS, r = idx / CH, c = idx % CH;
+      *reinterpret_cast<uint4 *>(sm + (r * CH + (c ^ ((r / N) & 7))) * 16) = v[u];  // XOR on the low 3 bits
     }
     __syncthreads();
+    k7_gather<ES, CW>(p, sm, db, dst, lane, warp);
+    __syncthreads();
   }
+}
+
+// Double-buffered form: the next tile's 16-byte source vectors go straight to the second shared buffer
+// with cp.async (no registers held) while the current tile is gathered and stored.
+__device__ __forceinline__ void cp_async16(uint8_t *s, const uint8_t *g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(s)), "l"(g)
+               : "memory");
+}
+
+template <int ES, int CW>
+__global__ void __launch_bounds__(K7_THREADS) k7_transpose_async(const __grid_constant__ K7Params p,
+                                                                 const uint8_t *__restrict__ src,
+                                                                 uint8_t *__restrict__ dst) {
+  constexpr int N = 16 / ES;
+  constexpr int TR = 32 * N;
+  constexpr int CH = 8 * CW;
+  constexpr int LOADS = TR * CH / K7_THREADS;
+  constexpr int TILE = TR * CH * 16;
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (p.dep) pdl_wait();
+  pdl_launch_dependents();
+  auto issue = [&](uint32_t tile, uint8_t *buf) {
+    int64_t sb, db;
+    tile_offsets(p, tile, sb, db);
+#pragma unroll
+    for (int u = 0; u < LOADS; u++) {
+      const int idx = t + u * K7_THREADS, r = idx / CH, c = idx % CH;
+      cp_async16(buf + (r * CH + (c ^ ((r / N) & 7))) * 16, src + sb + (int64_t)r * p.src_row + c * 16);
+    }
+  };
+  uint32_t tile = blockIdx.x;
+  if (tile < p.ntiles) issue(tile, sm);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int it = 0; tile < p.ntiles; tile += gridDim.x, it++) {
+    const uint32_t next = tile + gridDim.x;
+    if (next < p.ntiles) issue(next, sm + ((it + 1) & 1) * TILE);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // this thread's vectors of `tile` landed
+    __syncthreads();                                       // ... and every other thread's
+    int64_t sb, db;
+    tile_offsets(p, tile, sb, db);
+    k7_gather<ES, CW>(p, sm + (it & 1) * TILE, db, dst, lane, warp);
+    __syncthreads();  // buffer (it & 1) is refilled by the issue of the next iteration
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 template <int ES, int CW>
 cudaError_t go(const K7Params &p, unsigned blocks, const uint8_t *s, uint8_t *d, cudaStream_t st) {
   constexpr int N = 16 / ES;
-  const size_t smem = (size_t)32 * N * 8 * CW * 16;
+  const size_t tile = (size_t)32 * N * 8 * CW * 16;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k7_transpose<ES, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k7_transpose_async<ES, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_ex(k7_transpose<ES, CW>, dim3(blocks), dim3(K7_THREADS), smem, st, p, s, d);
+  if (p.async) return launch_ex(k7_transpose_async<ES, CW>, dim3(blocks), dim3(K7_THREADS), 2 * tile, st, p, s, d);
+  return launch_ex(k7_transpose<ES, CW>, dim3(blocks), dim3(K7_THREADS), tile, st, p, s, d);
 }
 
 }  // namespace

@@ -32,9 +32,14 @@ bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   // chunk columns per warp (tiles of 32 n rows x 8 n cw columns), as wide as the columns allow:
   // 4 for 4-byte elements (8192^2 fp32: 94.9 us vs 100.8 / 104.3 with 2 / 1), 2 otherwise (bf16:
   // 43.2 us vs 44.9 with 1; 8192x4096 fp64: 94.1 us vs 98.6 with 4)
+  // The cp.async double-buffered form (next tile in flight while the current one is stored) with cw = 2:
+  // fp32 93.3 us vs 95.8 (register-staged, cw 4) / 101.7 (register-staged, cw 2); bf16 42.4 vs 42.9;
+  // fp64 95.2 vs 94.0-94.8, so 8-byte elements stay register-staged.
+  const char *ae = getenv("AXE_K7_ASYNC");
+  const int async = (ae && *ae) ? (atoi(ae) != 0) : (es <= 4);
   const char *cwe = getenv("AXE_K7_CW");
   const int cwmax = es == 4 ? 4 : 2;
-  int64_t cw = (cwe && *cwe) ? std::max(1, std::min(cwmax, atoi(cwe))) : cwmax;
+  int64_t cw = (cwe && *cwe) ? std::max(1, std::min(cwmax, atoi(cwe))) : (async ? 2 : cwmax);
   std::vector<Joint> J;
   for (auto &j : J0)
     if (j.e > 1) J.push_back(j);
@@ -92,20 +97,23 @@ bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   k.src_row = B.ss * es;
   k.dst_col = A.ds * es;
   k.cw = (int)cw;
+  k.async = async;
   k.nrep = (int)reps.size();
   for (size_t i = 0; i < reps.size(); i++) k.rep[i] = reps[i] * es;
   P->align = 16;
-  const int64_t tile_bytes = TR * TC * es;
+  const int64_t tile_bytes = TR * TC * es * (k.async ? 2 : 1);
   const int per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(8, (220 * 1024) / (tile_bytes + 1024)));
   P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt, (int64_t)num_sms() * per_sm));
+  const char *mc = getenv("AXE_K7_MAX_CTAS");  // tests: several tiles per CTA on small inputs
+  if (mc && *mc && atoi(mc) > 0) P->blocks = std::min<unsigned>(P->blocks, (unsigned)atoi(mc));
   int64_t total = 1;
   for (auto &j : J0) total *= j.e;
   P->covers_all = (int64_t)reps.size() * total == dstst.cells;
   char buf[256];
   snprintf(buf, sizeof buf,
            "{\"kernel\":\"transpose\",\"block\":\"%lldx%lld register transpose\",\"tile\":[%lld,%lld],\"tiles\":%lld,"
-           "\"ctas\":%u,\"replicas\":%d,\"joint\":",
-           (long long)n, (long long)n, (long long)TR, (long long)TC, (long long)nt, P->blocks, k.nrep);
+           "\"ctas\":%u,\"replicas\":%d,\"async\":%d,\"joint\":",
+           (long long)n, (long long)n, (long long)TR, (long long)TC, (long long)nt, P->blocks, k.nrep, k.async);
   P->desc = std::string(buf) + joint_json(J0) + "}";
   return true;
 }

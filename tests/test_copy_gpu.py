@@ -236,6 +236,29 @@ def test_transposes_all_kernels(axe, R, Cn, es):
         check(axe, cfg, k)
 
 
+@pytest.mark.parametrize("es,cw", [(2, 1), (2, 2), (4, 1), (4, 2), (4, 4), (8, 1), (8, 2)])
+@pytest.mark.parametrize("asyn", [0, 1])
+def test_k7_batched_padded_transposes(axe, monkeypatch, es, cw, asyn):
+    """K7 directly: 3 batched transposes of (2 TR) x (3 TC) tiles, padded source rows and destination columns,
+    two destination replicas; every chunk width and both the register-staged and the cp.async
+    double-buffered form (several tiles per CTA, so both buffers are refilled)."""
+    monkeypatch.setenv("AXE_K7_CW", str(cw))
+    monkeypatch.setenv("AXE_K7_ASYNC", str(asyn))
+    monkeypatch.setenv("AXE_K7_MAX_CTAS", "4")
+    n = 16 // es
+    cw = min(cw, 4 if es == 4 else 2)   # the widest chunk column the planner takes for this element size
+    R, C = 2 * 32 * n, 3 * 8 * n * cw
+    lds, ldd = C + n, R + 2 * n
+    B = 3
+    src = layout([(B, R * lds), (R, lds), (C, 1)])
+    dst = layout([(B, C * ldd), (R, 1), (C, ldd)], [(2, B * C * ldd)])
+    cfg = dict(name=f"k7_{es}_{cw}_{asyn}", es=es, src=src, src_st=linear_storage(B * R * lds), dst=dst,
+               dst_st=linear_storage(2 * B * C * ldd), seed=es * 10 + cw)
+    desc = check(axe, cfg, "transpose", "transpose")
+    assert desc["async"] == asyn and desc["replicas"] == 2 and desc["tile"] == [32 * n, 8 * n * cw]
+    assert desc["tiles"] == B * 2 * 3 and desc["ctas"] == 4
+
+
 def test_alias_and_alignment_errors(axe):
     x = torch.zeros(1024, dtype=torch.int32, device="cuda")
     L = layout([(512, 1)])
