@@ -521,7 +521,7 @@ static bool build_tma(const std::vector<Joint> &J0, const Linear &ls, const Line
       break;
     }
   if (!B1) return fail("tma: no legal box height");
-  const int64_t box_bytes = B1 * row_bytes;
+  int64_t box_bytes = B1 * row_bytes;
   const int64_t blk = span ? span * 8 : 16;  // the bulk-side box base must be a whole swizzle block
   TmaParams &k = P->tma;
   memset(&k, 0, sizeof(k));
@@ -533,13 +533,26 @@ static bool build_tma(const std::vector<Joint> &J0, const Linear &ls, const Line
   P->tm_dims[1] = (uint64_t)E1;
   P->tm_strides[0] = (uint64_t)(t1 * es);
   P->tm_box[1] = (uint32_t)B1;
+  // opt-in (AXE_TMA_BOX_MAX_BYTES): a box may span several whole (B1 x row) blocks of the next digit
+  // when they are consecutive on the bulk side (config 2: adjacent 64 x 64 tiles, 8 KiB apart).  16 KiB
+  // boxes: config 2 10.01 us vs 10.16, reverse 10.16 vs 10.48, but 16384^2 188 us vs 178 (6 CTAs/SM
+  // instead of 8), so the default keeps one block per box
+  const int64_t box_max = env_int("AXE_TMA_BOX_MAX_BYTES", 0);
   for (size_t i = 2; i < d.size(); i++) {
     if (dim > 4) return fail("tma: more than 5 tensor dimensions");
     if ((d[i].t * es) % 16) return fail("tma: outer stride not a multiple of 16 bytes");
+    int64_t k = 1;
+    if (i == 2 && d[i].b * es == box_bytes && E1 == B1)
+      for (int64_t c = std::min<int64_t>(d[i].e, 256); c > 1; c--)
+        if (d[i].e % c == 0 && c * box_bytes <= box_max) {
+          k = c;
+          break;
+        }
     P->tm_dims[dim] = (uint64_t)d[i].e;
     P->tm_strides[dim - 1] = (uint64_t)(d[i].t * es);
-    P->tm_box[dim] = 1;
-    digs.push_back({d[i].e, dim, 1, d[i].b * es});
+    P->tm_box[dim] = (uint32_t)k;
+    if (d[i].e / k > 1) digs.push_back({d[i].e / k, dim, k, k * d[i].b * es});
+    box_bytes *= k;
     dim++;
   }
   for (int i = dim; i < 5; i++) P->tm_strides[i - 1] = P->tm_strides[dim - 2 > 0 ? dim - 2 : 0];

@@ -87,6 +87,20 @@ def test_config2_full(axe, rev, kernel):
     assert desc["kernel"] == ("tma" if kernel == "auto" else kernel)
 
 
+@pytest.mark.parametrize("rev", [False, True])
+@pytest.mark.parametrize("box_max,n,t,es,sw", [(16384, 512, 64, 2, synth.SW128), (32768, 1024, 64, 2, synth.SW128),
+                                               (16384, 256, 32, 4, synth.SW128), (65536, 512, 64, 1, synth.SW64)])
+def test_tma_boxes_spanning_adjacent_tiles(axe, monkeypatch, box_max, n, t, es, sw, rev):
+    """AXE_TMA_BOX_MAX_BYTES > one tile: a 3-D TMA box covers k adjacent destination tiles (consecutive on the
+    bulk side) -- box k along the tile-column digit, the remaining tile digits index boxes of k tiles."""
+    monkeypatch.setenv("AXE_TMA_BOX_MAX_BYTES", str(box_max))
+    cfg = synth.config2(n, t, es, sw, rev)
+    desc = check(axe, cfg, "tma", "tma")
+    tile = t * t * es
+    k = desc["tensor_map"]["box"][2]
+    assert k > 1 and desc["box_bytes"] == k * tile <= box_max
+
+
 @pytest.mark.parametrize("kernel", ["auto", "generic", "vector", "tile", "register", "shuffle"])
 @pytest.mark.parametrize("variant", ["a", "b"])
 def test_config3_small(axe, variant, kernel):
