@@ -163,6 +163,26 @@ axe_status axe_tma_lower(const axe_layout *LG, const int64_t *EG, const int64_t 
                          const axe_layout *LS, const int64_t *ES, int rank, int elem_size, int swizzle_bytes,
                          axe_tma_desc *out, axe_layout **tiler);
 
+/* Executing a lowering on the device ("the shared memory layout is tiled by the
+ * swizzle atom ... each tile issues one TMA instruction").  axe_tma_plan_create takes the
+ * descriptor and tiler T that axe_tma_lower returned (the plan copies the descriptor and reads T
+ * once; the caller keeps ownership of both).  axe_tma_plan_execute(plan, g_base, s_image, stream):
+ * g_base is the device address of the global tensor's element m = 0 (the region's offset
+ * base_bytes is added by the plan); s_image is a device buffer of image_bytes that receives the
+ * shared-memory tensor L_S byte for byte -- atom t (row-major over the atom grid) at T(t) * 8 *
+ * swizzle_bytes bytes, its bytes in the hardware's swizzled order (CUTLASS Swizzle<B,4,3> relative
+ * to the image start, B = log2(swizzle_bytes / 16)).  One TMA tensor load per atom into a shared
+ * ring slot, one bulk store per atom; stream-ordered, asynchronous.  Both the region start and
+ * s_image must be 16-byte aligned (AXE_ERR_ALIGNMENT).  The atom table is uploaded to the current
+ * device by the first execute (synchronous); the tensor map is re-encoded when g_base changes.
+ * Errors: AXE_ERR_INVALID_ARG (not a lowering: box != one atom, bad rank / element size),
+ * AXE_ERR_SIZE_MISMATCH (|T| != atoms), AXE_ERR_CUDA. */
+typedef struct axe_tma_plan axe_tma_plan;
+axe_status axe_tma_plan_create(const axe_tma_desc *desc, const axe_layout *tiler, axe_tma_plan **out);
+axe_status axe_tma_plan_sizes(const axe_tma_plan *plan, int64_t *atoms, int64_t *image_bytes);
+axe_status axe_tma_plan_execute(axe_tma_plan *plan, const void *g_base, void *s_image, void *stream);
+void axe_tma_plan_destroy(axe_tma_plan *plan);
+
 /* Textual form of the paper's matrix notation (Figures 2 and 5):
  *   layout  := shard ( "+" replica )? ( "+" offset )*
  *   shard   := "(" INT ("," INT)* "):(" stride ("," stride)* ")"

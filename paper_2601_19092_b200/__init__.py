@@ -92,6 +92,10 @@ _SIGS = {
     "axe_copy_plan_sizes": ([_vp, _pi64, _pi64], C.c_int),
     "axe_copy_plan_describe": ([_vp, C.c_char_p, C.c_int], C.c_int),
     "axe_copy_plan_destroy": ([_vp], None),
+    "axe_tma_plan_create": ([C.POINTER(axe_tma_desc), _vp, C.POINTER(_vp)], C.c_int),
+    "axe_tma_plan_sizes": ([_vp, _pi64, _pi64], C.c_int),
+    "axe_tma_plan_execute": ([_vp, _vp, _vp, _vp], C.c_int),
+    "axe_tma_plan_destroy": ([_vp], None),
     "axe_copy": ([_vp, C.POINTER(axe_storage), _vp, _vp, C.POINTER(axe_storage), _vp, C.c_int, _vp], C.c_int),
     "axe_get_unique_id": ([C.c_char_p], C.c_int),
     "axe_comm_create": ([C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)], C.c_int),
@@ -621,7 +625,33 @@ def tma_lower(LG, EG, LS, ES, elem_size: int, swizzle_bytes: int, begin=None, ex
     return {"rank": n, "dims": list(d.dims[:n]), "strides": list(d.strides[:n]), "box": list(d.box[:n]),
             "logical_dim": list(d.logical_dim[:n]),
             "swizzle_bytes": d.swizzle_bytes, "base_bytes": d.base_bytes, "atoms": d.atoms,
-            "fused_rows": d.fused_rows, "tiler": Layout(_handle=t)}
+            "fused_rows": d.fused_rows, "tiler": Layout(_handle=t), "_desc": d}
+
+
+class TmaPlan:
+    """axe_tma_plan_create / _sizes / _execute: the lowering of tma_lower() run on the device -- one TMA
+    tensor load + one bulk store per swizzle atom, into an HBM image of the shared-memory tensor L_S."""
+
+    def __init__(self, LG, EG, LS, ES, elem_size: int, swizzle_bytes: int, begin=None, extent=None):
+        self.lowering = tma_lower(LG, EG, LS, ES, elem_size, swizzle_bytes, begin, extent)
+        h = C.c_void_p()
+        _check(_lib.axe_tma_plan_create(C.byref(self.lowering["_desc"]), self.lowering["tiler"].handle, C.byref(h)),
+               "axe_tma_plan_create")
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.axe_tma_plan_destroy(h)
+        self._h = None
+
+    def sizes(self):
+        a, b = C.c_int64(), C.c_int64()
+        _check(_lib.axe_tma_plan_sizes(self._h, C.byref(a), C.byref(b)), "axe_tma_plan_sizes")
+        return a.value, b.value   # atoms, image bytes
+
+    def execute(self, g_base, s_image, stream=None):
+        _check(_lib.axe_tma_plan_execute(self._h, _ptr(g_base), _ptr(s_image), _stream(stream)), "axe_tma_plan_execute")
 
 
 def axe_layout_create(D, R=(), O=None) -> Layout:

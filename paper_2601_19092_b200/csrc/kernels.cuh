@@ -95,6 +95,14 @@ struct K1Params {
 //   mode 0: TMA tensor load (src)  -> smem -> bulk store (dst, every replica)
 //   mode 1: bulk load (src)        -> smem -> TMA tensor store (dst)
 constexpr int TMA_MAXD = 6;
+// one swizzle atom of a lowered TMA region (tma_region.cpp): tensor-map coordinates (dim 0 in bytes)
+// and the byte offset of its slot in the shared-memory image
+struct TmaAtom {
+  int32_t c[5];
+  int32_t pad;
+  int64_t off;
+};
+
 struct TmaParams {
   uint32_t nboxes;
   int nd;                      // box-index digits, outermost first

@@ -205,26 +205,16 @@ __global__ void AXE_K2_BOUNDS k2_tile_async(const __grid_constant__ K2Params p, 
 template <int VD, int GB, int LJ>
 static cudaError_t k2_go_async(const K2Params &p, unsigned blocks, size_t smem, const void *s, void *d,
                                cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(k2_tile_async<VD, GB, LJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  const cudaError_t e = smem_attr((const void *)k2_tile_async<VD, GB, LJ>, 200 * 1024);
+  if (e != cudaSuccess) return e;
   return launch_ex(k2_tile_async<VD, GB, LJ>, dim3(blocks), dim3(K2_NT), 2 * smem, st, p, (const uint8_t *)s,
                    (uint8_t *)d);
 }
 
 template <int VS, int VD, int GB, int LJ>
 static cudaError_t k2_go_lj(const K2Params &p, unsigned blocks, size_t smem, const void *s, void *d, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(k2_tile<VS, VD, GB, LJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  const cudaError_t e = smem_attr((const void *)k2_tile<VS, VD, GB, LJ>, 100 * 1024);
+  if (e != cudaSuccess) return e;
   return launch_ex(k2_tile<VS, VD, GB, LJ>, dim3(blocks), dim3(K2_NT), smem, st, p, (const uint8_t *)s,
                    (uint8_t *)d);
 }

@@ -170,14 +170,9 @@ template <int ES, int CW>
 cudaError_t go(const K7Params &p, unsigned blocks, const uint8_t *s, uint8_t *d, cudaStream_t st) {
   constexpr int N = 16 / ES;
   const size_t tile = (size_t)32 * N * 8 * CW * 16;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k7_transpose<ES, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k7_transpose_async<ES, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = smem_attr((const void *)k7_transpose<ES, CW>, 100 * 1024);
+  if (e == cudaSuccess) e = smem_attr((const void *)k7_transpose_async<ES, CW>, 200 * 1024);
+  if (e != cudaSuccess) return e;
   if (p.async) return launch_ex(k7_transpose_async<ES, CW>, dim3(blocks), dim3(K7_THREADS), 2 * tile, st, p, s, d);
   return launch_ex(k7_transpose<ES, CW>, dim3(blocks), dim3(K7_THREADS), tile, st, p, s, d);
 }

@@ -421,12 +421,7 @@ cudaError_t launch_k4_bulk(const K4Params &p, int dtype, unsigned blocks, const 
   uint8_t *d = (uint8_t *)dst;
   const size_t smem = (size_t)p.stages * p.nk * p.box_bytes;
   const dim3 g(blocks), b(p.threads);
-  static bool attr[8] = {};
-  auto prep = [&](const void *kern) -> cudaError_t {
-    if (attr[dtype]) return cudaSuccess;
-    attr[dtype] = true;
-    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  };
+  auto prep = [&](const void *kern) -> cudaError_t { return smem_attr(kern, 200 * 1024); };
   cudaError_t e;
   switch (dtype) {
     case DT_F32: e = prep((const void *)k4_bulk<DT_F32>); if (e == cudaSuccess) e = launch_ex(k4_bulk<DT_F32>, g, b, smem, st, p, s, d); break;

@@ -12,6 +12,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include <atomic>
 #include <cstring>
 #include <mutex>
@@ -269,15 +271,9 @@ __global__ void __launch_bounds__(K2T_THREADS) k2t_transpose(const __grid_consta
 size_t k2t_smem_bytes(const K2TParams &p) { return (size_t)p.stages * p.H * 128 + 1024; }
 
 cudaError_t launch_k2t(const void *map128, const K2TParams &p, int es, unsigned blocks, void *dst, cudaStream_t st) {
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(k2t_transpose<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(k2t_transpose<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(k2t_transpose<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  });
+  cudaError_t attr_err = smem_attr((const void *)k2t_transpose<2>, 200 * 1024);
+  if (attr_err == cudaSuccess) attr_err = smem_attr((const void *)k2t_transpose<4>, 200 * 1024);
+  if (attr_err == cudaSuccess) attr_err = smem_attr((const void *)k2t_transpose<8>, 200 * 1024);
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap m;
   memcpy(&m, map128, sizeof(m));
@@ -292,6 +288,45 @@ cudaError_t launch_k2t(const void *map128, const K2TParams &p, int es, unsigned 
   if (e != cudaSuccess) return e;
   g_launches++;
   return cudaGetLastError();
+}
+
+// The lowered TMA region (tma_region.cpp): one elected thread per CTA streams atoms through a
+// ring of 1 KiB-aligned slots -- tensor load (the hardware applies the atom's swizzle), then one
+// bulk store of the slot into the image at the tiler's offset.  Both copies run in the async
+// proxy, so no proxy fence is needed between them.
+constexpr int TR_STAGES = 8;
+__global__ void __launch_bounds__(32) k_tma_region(const __grid_constant__ CUtensorMap map,
+                                                   const TmaAtom *__restrict__ atoms, uint32_t n, uint32_t box,
+                                                   uint8_t *__restrict__ dst) {
+  extern __shared__ __align__(1024) uint8_t raw[];
+  __shared__ __align__(8) uint64_t full[TR_STAGES];
+  uint8_t *sm = (uint8_t *)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t slot = (box + 1023) & ~1023u;
+  pdl_wait();
+  pdl_launch_dependents();
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < TR_STAGES; s++) mbar_init(&full[s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const uint32_t first = blockIdx.x, step = gridDim.x;
+  const uint32_t mine = first < n ? (n - first + step - 1) / step : 0;
+  auto issue = [&](uint32_t k) {
+    const int s = (int)(k % TR_STAGES);
+    const TmaAtom a = atoms[first + k * step];
+    mbar_expect_tx(&full[s], box);
+    tma_load5(sm + (size_t)s * slot, &map, &full[s], a.c[0], a.c[1], a.c[2], a.c[3], a.c[4]);
+  };
+  for (uint32_t k = 0; k < mine && k < (uint32_t)TR_STAGES; k++) issue(k);
+  for (uint32_t k = 0; k < mine; k++) {
+    const int s = (int)(k % TR_STAGES);
+    mbar_wait(&full[s], (k / TR_STAGES) & 1u);
+    bulk_store(dst + atoms[first + k * step].off, sm + (size_t)s * slot, box);
+    bulk_commit();
+    if (k + TR_STAGES < mine) {
+      bulk_wait_read<0>();  // slot s has been read by its store
+      issue(k + TR_STAGES);
+    }
+  }
+  bulk_wait_all();
 }
 
 // ------------------------------------------------------------------ host side
@@ -336,15 +371,27 @@ int encode_tensor_map(void *out128, void *gaddr, const uint64_t dims[5], const u
   return (int)r;
 }
 
+cudaError_t launch_tma_region(const void *map128, const TmaAtom *atoms, uint32_t n, uint32_t box_bytes, void *dst,
+                              cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  const cudaError_t attr_err = smem_attr((const void *)k_tma_region, 200 * 1024);
+  if (attr_err != cudaSuccess) return attr_err;
+  CUtensorMap m;
+  memcpy(&m, map128, sizeof(m));
+  const size_t slot = (box_bytes + 1023) & ~(size_t)1023;
+  const unsigned blocks = (unsigned)std::min<int64_t>(n, (int64_t)num_sms() * 16);
+  cudaError_t e = launch_ex(k_tma_region, dim3(blocks), dim3(32), TR_STAGES * slot + 1024, st, m, atoms, n,
+                            box_bytes, (uint8_t *)dst);
+  if (e != cudaSuccess) return e;
+  g_launches++;
+  return cudaGetLastError();
+}
+
 size_t tma_smem_bytes(const TmaParams &p) { return (size_t)p.stages * p.slot_bytes + 1024; }
 
 cudaError_t launch_tma(const void *map128, const TmaParams &p, unsigned blocks, const void *src, void *dst,
                        cudaStream_t st) {
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(k1_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  });
+  const cudaError_t attr_err = smem_attr((const void *)k1_tma, 200 * 1024);
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap m;
   memcpy(&m, map128, sizeof(m));

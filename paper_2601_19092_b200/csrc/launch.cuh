@@ -12,6 +12,7 @@
 
 #include <cstdlib>
 #include <mutex>
+#include <set>
 #include <unordered_map>
 #include <utility>
 
@@ -39,6 +40,21 @@ inline unsigned one_wave(const void *kern, int threads, size_t smem, unsigned bl
   if (o <= 0) return blocks;
   const unsigned cap = (unsigned)(o * num_sms());
   return blocks > cap ? cap : blocks;
+}
+
+// Opt a kernel into more than 48 KiB of dynamic shared memory, once per (device, kernel): the
+// attribute belongs to the current device's context, and several host threads may launch at once.
+inline cudaError_t smem_attr(const void *kern, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void *>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({dev, kern})) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({dev, kern});
+  return e;
 }
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

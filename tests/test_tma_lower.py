@@ -148,3 +148,19 @@ def test_agrees_with_the_k1_tma_planner(n, tile, es, swz):
     assert r["box"][0] * es == tm["box"][0]              # bytes of one box row
     assert r["fused_rows"] == tm["box"][1]               # rows per box
     assert r["strides"][1] == tm["strides"][1]           # global row stride (bytes)
+
+
+def test_device_plan_from_the_lowering():
+    """axe_tma_plan_create consumes the lowering (descriptor + T) without a GPU: atom count and image size
+    of L_S; a descriptor that is not one atom per box is rejected."""
+    p = axe.TmaPlan(layout([(4096, 4096), (4096, 1)]), [4096, 4096], layout([(64, 64), (64, 1)]), [64, 64], 2, 128,
+                    begin=[128, 192], extent=[64, 64])
+    assert p.sizes() == (8, 64 * 64 * 2)
+    rng = np.random.default_rng(3)
+    LS = atom_tiled_smem(rng, [32, 128], 32)              # fp32, 128-byte atoms (8 x 32), 4 x 4 grid
+    q = axe.TmaPlan(layout([(64, 256), (256, 1)]), [64, 256], LS, [32, 128], 4, 128, begin=[8, 64], extent=[32, 128])
+    assert q.sizes() == (16, 32 * 128 * 4)
+    d = q.lowering["_desc"]
+    d.box[1] = 4                                          # half an atom per box
+    h = axe.C.c_void_p()
+    assert axe._lib.axe_tma_plan_create(axe.C.byref(d), q.lowering["tiler"].handle, axe.C.byref(h)) == 1
