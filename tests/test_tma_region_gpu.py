@@ -93,6 +93,31 @@ def test_many_atoms_per_cta(axe):
     run_case(axe, 1024, 512, 512, [256, 128], ES, atom_tiled_smem(None, ES, 64, 1), 2, 128, 5)
 
 
+@pytest.mark.parametrize("order", [0, 1])
+def test_rank3_region_five_tensor_dims(axe, order):
+    """A 3-D region (2 x 16 x 64 of a padded 4 x 48 x 96 bf16 tensor, 64-byte swizzle): the lowering
+    needs all 5 CuTensorMap dims (column atoms split off the box); atom grid (b, row-tile, col-tile)
+    in row-major or reversed order."""
+    B, rows, cols, ld, es, sw = 4, 48, 96, 104, 2, 64
+    inner, ES = sw // es, [2, 16, 64]
+    W = 8 * inner
+    strides = [4 * W, 2 * W, W] if order == 0 else [W, 2 * W, 4 * W]
+    LS = layout([(2, strides[0]), (2, strides[1]), (8, inner), (2, strides[2]), (inner, 1)])
+    LG = layout([(B, rows * ld), (rows, ld), (cols, 1)])
+    begin = [1, 8, 16]
+    plan = axe.TmaPlan(LG, [B, rows, cols], LS, ES, es, sw, begin=begin, extent=ES)
+    assert plan.lowering["rank"] == 5 and plan.sizes() == (8, 2 * 16 * 64 * es)
+    g = synth.sentinel(B * rows * ld * es, 21)
+    fill = synth.sentinel(2 * 16 * 64 * es, 22)
+    exp = fill.copy()
+    region = layout([(2, rows * ld), (16, ld), (64, 1)], O={"m": begin[0] * rows * ld + begin[1] * ld + begin[2]})
+    oracle.copy(region, linear_storage(B * rows * ld), g, LS, linear_storage(2 * 16 * 64, SW[sw]), exp, es)
+    out = torch.from_numpy(fill).cuda()
+    plan.execute(torch.from_numpy(g).cuda(), out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), exp)
+
+
 def test_misaligned_region_rejected(axe):
     plan = axe.TmaPlan(layout([(64, 64), (64, 1)]), [64, 64], layout([(8, 64), (64, 1)]), [8, 64], 2, 128,
                        begin=[0, 0], extent=[8, 64])
