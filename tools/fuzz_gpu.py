@@ -289,13 +289,72 @@ def run_chain(rng, seed):
     return None
 
 
+def run_tma_region(crng, case_seed):
+    """A random 2- or 3-D region of a padded row-major tensor lowered by axe_tma_lower and executed by
+    axe_tma_plan_* into the L_S image; expected = the oracle's copy of the hand-written region layout
+    into L_S with the atom's swizzle."""
+    es = int(crng.choice([1, 2, 4, 8]))
+    sw = int(crng.choice([32, 64, 128]))
+    inner = sw // es
+    if inner < 1:
+        return "skip"
+    v = 16 // es if es < 16 else 1
+    rank = int(crng.choice([2, 3]))
+    ES = ([int(crng.integers(1, 4))] if rank == 3 else []) + [8 * int(crng.integers(1, 5)),
+                                                            inner * int(crng.integers(1, 4))]
+    EG = [e + int(crng.integers(0, 3)) for e in ES[:-1]] + [ES[-1] + v * int(crng.integers(0, 4))]
+    ld = EG[-1] + v * int(crng.integers(0, 3))
+    pitch = [0] * rank
+    pitch[-1], pitch[-2] = 1, ld
+    if rank == 3:
+        pitch[0] = ld * EG[1]
+    begin = [int(crng.integers(0, EG[j] - ES[j] + 1)) for j in range(rank - 1)]
+    begin.append(v * int(crng.integers(0, (EG[-1] - ES[-1]) // v + 1)))
+    # L_S: the atom grid (outer iters) in a random order, atoms (8, inner) innermost
+    Ea = [1] * rank
+    Ea[-1], Ea[-2] = inner, 8
+    Eo = [e // a for e, a in zip(ES, Ea)]
+    order = list(crng.permutation(rank))
+    W = 8 * inner
+    gs, stride = {}, 1
+    for d in reversed(order):
+        gs[int(d)] = stride
+        stride *= Eo[int(d)]
+    D = []
+    for j in range(rank):
+        D.append((Eo[j], gs[j] * W))
+        if Ea[j] > 1:
+            D.append((Ea[j], inner if j == rank - 2 else 1))
+    LS = layout(D)
+    LG = layout([(EG[j], pitch[j]) for j in range(rank)])
+    try:
+        plan = axe.TmaPlan(LG, EG, LS, ES, es, sw, begin=begin, extent=ES)
+    except axe.AxeError:
+        return "skip"
+    cells = int(np.prod(ES))
+    gbytes = (EG[0] * pitch[0] if rank == 3 else EG[0] * ld) * es
+    g = synth.sentinel(gbytes, case_seed % 1000)
+    fill = synth.sentinel(cells * es, case_seed % 1000 + 1)
+    exp = fill.copy()
+    region = layout([(ES[j], pitch[j]) for j in range(rank)], O={"m": sum(b * p for b, p in zip(begin, pitch))})
+    oracle.copy(region, linear_storage(gbytes // es), g, LS, linear_storage(cells, {32: synth.SW32, 64: synth.SW64,
+                                                                                       128: synth.SW128}[sw]), exp, es)
+    out = torch.from_numpy(fill).cuda()
+    plan.execute(torch.from_numpy(g).cuda(), out)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    if not np.array_equal(got, exp):
+        return f"{int((got != exp).sum())} bytes differ (ES={ES}, EG={EG}, begin={begin}, es={es}, sw={sw})"
+    return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=300)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--trace", action="store_true", help="print every case to stderr before it runs")
     ap.add_argument("--case", type=int, default=None, help="run only this case seed")
-    ap.add_argument("--only", default="", help="chain | copy | reduce | redistribute (default: all)")
+    ap.add_argument("--only", default="", help="chain | copy | reduce | redistribute | tma_region (default: all)")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     t0 = time.time()
@@ -306,7 +365,7 @@ def main():
         crng = np.random.default_rng(case_seed)
         u = crng.random()
         if a.only:
-            u = {"chain": 0.0, "redistribute": 0.1, "copy": 0.5, "reduce": 0.9}[a.only]
+            u = {"chain": 0.0, "redistribute": 0.1, "copy": 0.5, "reduce": 0.9, "tma_region": 0.99}[a.only]
         if u < 0.08:
             err = run_chain(crng, case_seed)
             if err == "skip":
@@ -341,6 +400,15 @@ def main():
                     fails += 1
                     print(json.dumps({"case_seed": case_seed, "kind": "copy", "kernel": k, "error": err,
                                       "cfg": {**cfg, "es": cfg["es"]}}, default=str), flush=True)
+        elif u >= 0.96:
+            err = run_tma_region(crng, case_seed)
+            if err == "skip":
+                continue
+            n += 1
+            kinds["tma_region"] = kinds.get("tma_region", 0) + 1
+            if err:
+                fails += 1
+                print(json.dumps({"case_seed": case_seed, "kind": "tma_region", "error": err}), flush=True)
         else:
             cfg = reduce_case(crng)
             err = run_reduce(cfg, case_seed)
