@@ -172,14 +172,17 @@ axe_status axe_tma_lower(const axe_layout *LG, const int64_t *EG, const int64_t 
  * shared-memory tensor L_S byte for byte -- atom t (row-major over the atom grid) at T(t) * 8 *
  * swizzle_bytes bytes, its bytes in the hardware's swizzled order (CUTLASS Swizzle<B,4,3> relative
  * to the image start, B = log2(swizzle_bytes / 16)).  One TMA tensor load per atom into a shared
- * ring slot, one bulk store per atom; stream-ordered, asynchronous.  Both the region start and
+ * ring slot, one bulk store per atom -- or per box of up to fused_rows / 8 atoms stacked along the
+ * rows when T places them in consecutive slots (*boxes from axe_tma_plan_sizes; AXE_TMA_FUSE=0
+ * keeps one atom per box); stream-ordered, asynchronous.  Both the region start and
  * s_image must be 16-byte aligned (AXE_ERR_ALIGNMENT).  The atom table is uploaded to the current
- * device by the first execute (synchronous); the tensor map is re-encoded when g_base changes.
+ * device at create (or by the first execute on another device -- synchronous, so that execute fails
+ * with AXE_ERR_CUDA inside graph capture); the tensor map is re-encoded when g_base changes.
  * Errors: AXE_ERR_INVALID_ARG (not a lowering: box != one atom, bad rank / element size),
  * AXE_ERR_SIZE_MISMATCH (|T| != atoms), AXE_ERR_CUDA. */
 typedef struct axe_tma_plan axe_tma_plan;
 axe_status axe_tma_plan_create(const axe_tma_desc *desc, const axe_layout *tiler, axe_tma_plan **out);
-axe_status axe_tma_plan_sizes(const axe_tma_plan *plan, int64_t *atoms, int64_t *image_bytes);
+axe_status axe_tma_plan_sizes(const axe_tma_plan *plan, int64_t *atoms, int64_t *boxes, int64_t *image_bytes);
 axe_status axe_tma_plan_execute(axe_tma_plan *plan, const void *g_base, void *s_image, void *stream);
 void axe_tma_plan_destroy(axe_tma_plan *plan);
 
@@ -251,7 +254,10 @@ enum {
   AXE_KERNEL_REGISTER = 5, /* K3: warp-register permute through movmatrix (b16 8x8 atoms)    */
   AXE_KERNEL_TMA_TILE = 6, /* K2T: TMA SW128 box staging + conflict-free gather (transposes)  */
   AXE_KERNEL_SHUFFLE = 7,  /* K6: n x n granule transpose across lanes with warp shuffles       */
-  AXE_KERNEL_TRANSPOSE = 8 /* K7: smem tile + n x n register-block transpose (2-D transposes)   */
+  AXE_KERNEL_TRANSPOSE = 8, /* K7: smem tile + n x n register-block transpose (2-D transposes)  */
+  AXE_KERNEL_LOWERED = 9    /* the paper's TMA lowering (axe_tma_lower) as a copy schedule: the
+                               destination is a tiling of the swizzle atom over the joint digits,
+                               one TMA load + bulk store per (fused) atom box; opt-in             */
 };
 
 typedef struct axe_copy_plan axe_copy_plan;

@@ -30,7 +30,8 @@ ERRORS = {0: "AXE_OK", 1: "AXE_ERR_INVALID_ARG", 2: "AXE_ERR_OVERFLOW", 3: "AXE_
           5: "AXE_ERR_SIZE_MISMATCH", 6: "AXE_ERR_NONINJECTIVE", 7: "AXE_ERR_BOUNDS",
           8: "AXE_ERR_UNSUPPORTED_AXIS", 9: "AXE_ERR_ALIGNMENT", 10: "AXE_ERR_ALIAS", 11: "AXE_ERR_CUDA",
           12: "AXE_ERR_NCCL", 13: "AXE_ERR_UNSUPPORTED"}
-KERNELS = {"auto": 0, "generic": 1, "vector": 2, "tma": 3, "tile": 4, "register": 5, "tma_tile": 6, "shuffle": 7, "transpose": 8}
+KERNELS = {"auto": 0, "generic": 1, "vector": 2, "tma": 3, "tile": 4, "register": 5, "tma_tile": 6, "shuffle": 7, "transpose": 8,
+           "lowered": 9}
 
 
 class axe_iter(C.Structure):
@@ -93,7 +94,7 @@ _SIGS = {
     "axe_copy_plan_describe": ([_vp, C.c_char_p, C.c_int], C.c_int),
     "axe_copy_plan_destroy": ([_vp], None),
     "axe_tma_plan_create": ([C.POINTER(axe_tma_desc), _vp, C.POINTER(_vp)], C.c_int),
-    "axe_tma_plan_sizes": ([_vp, _pi64, _pi64], C.c_int),
+    "axe_tma_plan_sizes": ([_vp, _pi64, _pi64, _pi64], C.c_int),
     "axe_tma_plan_execute": ([_vp, _vp, _vp, _vp], C.c_int),
     "axe_tma_plan_destroy": ([_vp], None),
     "axe_copy": ([_vp, C.POINTER(axe_storage), _vp, _vp, C.POINTER(axe_storage), _vp, C.c_int, _vp], C.c_int),
@@ -647,8 +648,13 @@ class TmaPlan:
 
     def sizes(self):
         a, b = C.c_int64(), C.c_int64()
-        _check(_lib.axe_tma_plan_sizes(self._h, C.byref(a), C.byref(b)), "axe_tma_plan_sizes")
+        _check(_lib.axe_tma_plan_sizes(self._h, C.byref(a), None, C.byref(b)), "axe_tma_plan_sizes")
         return a.value, b.value   # atoms, image bytes
+
+    def boxes(self) -> int:
+        n = C.c_int64()
+        _check(_lib.axe_tma_plan_sizes(self._h, None, C.byref(n), None), "axe_tma_plan_sizes")
+        return n.value
 
     def execute(self, g_base, s_image, stream=None):
         _check(_lib.axe_tma_plan_execute(self._h, _ptr(g_base), _ptr(s_image), _stream(stream)), "axe_tma_plan_execute")

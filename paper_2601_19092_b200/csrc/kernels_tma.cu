@@ -15,6 +15,7 @@
 #include <algorithm>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -294,36 +295,38 @@ cudaError_t launch_k2t(const void *map128, const K2TParams &p, int es, unsigned 
 // ring of 1 KiB-aligned slots -- tensor load (the hardware applies the atom's swizzle), then one
 // bulk store of the slot into the image at the tiler's offset.  Both copies run in the async
 // proxy, so no proxy fence is needed between them.
-constexpr int TR_STAGES = 8;
+constexpr int TR_STAGES = 8;  // ring capacity; the launch picks 2..8 stages (16 KiB of boxes per CTA)
 __global__ void __launch_bounds__(32) k_tma_region(const __grid_constant__ CUtensorMap map,
                                                    const TmaAtom *__restrict__ atoms, uint32_t n, uint32_t box,
-                                                   uint8_t *__restrict__ dst) {
+                                                   int stages, int dep, uint8_t *__restrict__ dst) {
   extern __shared__ __align__(1024) uint8_t raw[];
   __shared__ __align__(8) uint64_t full[TR_STAGES];
   uint8_t *sm = (uint8_t *)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
   const uint32_t slot = (box + 1023) & ~1023u;
-  pdl_wait();
+  const uint32_t S = (uint32_t)stages;
+  if (dep) pdl_wait();
   pdl_launch_dependents();
   if (threadIdx.x != 0) return;
-  for (int s = 0; s < TR_STAGES; s++) mbar_init(&full[s], 1);
+  for (uint32_t s = 0; s < S; s++) mbar_init(&full[s], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   const uint32_t first = blockIdx.x, step = gridDim.x;
   const uint32_t mine = first < n ? (n - first + step - 1) / step : 0;
   auto issue = [&](uint32_t k) {
-    const int s = (int)(k % TR_STAGES);
+    const uint32_t s = k % S;
     const TmaAtom a = atoms[first + k * step];
     mbar_expect_tx(&full[s], box);
     tma_load5(sm + (size_t)s * slot, &map, &full[s], a.c[0], a.c[1], a.c[2], a.c[3], a.c[4]);
   };
-  for (uint32_t k = 0; k < mine && k < (uint32_t)TR_STAGES; k++) issue(k);
+  for (uint32_t k = 0; k < mine && k < S; k++) issue(k);
   for (uint32_t k = 0; k < mine; k++) {
-    const int s = (int)(k % TR_STAGES);
-    mbar_wait(&full[s], (k / TR_STAGES) & 1u);
+    const uint32_t s = k % S;
+    mbar_wait(&full[s], (k / S) & 1u);
     bulk_store(dst + atoms[first + k * step].off, sm + (size_t)s * slot, box);
     bulk_commit();
-    if (k + TR_STAGES < mine) {
-      bulk_wait_read<0>();  // slot s has been read by its store
-      issue(k + TR_STAGES);
+    // refill the slot of the previous store (one store may still be reading: its own slot)
+    if (k >= 1 && k - 1 + S < mine) {
+      bulk_wait_read<1>();
+      issue(k - 1 + S);
     }
   }
   bulk_wait_all();
@@ -372,16 +375,24 @@ int encode_tensor_map(void *out128, void *gaddr, const uint64_t dims[5], const u
 }
 
 cudaError_t launch_tma_region(const void *map128, const TmaAtom *atoms, uint32_t n, uint32_t box_bytes, void *dst,
-                              cudaStream_t st) {
+                              cudaStream_t st, int dep) {
   if (n == 0) return cudaSuccess;
   const cudaError_t attr_err = smem_attr((const void *)k_tma_region, 200 * 1024);
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap m;
   memcpy(&m, map128, sizeof(m));
   const size_t slot = (box_bytes + 1023) & ~(size_t)1023;
-  const unsigned blocks = (unsigned)std::min<int64_t>(n, (int64_t)num_sms() * 16);
-  cudaError_t e = launch_ex(k_tma_region, dim3(blocks), dim3(32), TR_STAGES * slot + 1024, st, m, atoms, n,
-                            box_bytes, (uint8_t *)dst);
+  const int stages = (int)std::max<size_t>(2, std::min<size_t>(TR_STAGES, 16384 / slot));
+  const size_t smem = stages * slot + 1024;
+  // CTAs per SM (AXE_TMA_PER_SM; capped by occupancy)
+  static const int per_sm = [] {
+    const char *e = getenv("AXE_TMA_PER_SM");
+    return (e && *e) ? std::max(1, atoi(e)) : 16;
+  }();
+  const unsigned blocks = one_wave((const void *)k_tma_region, 32, smem,
+                                   (unsigned)std::min<int64_t>(n, (int64_t)num_sms() * per_sm));
+  cudaError_t e = launch_ex(k_tma_region, dim3(blocks), dim3(32), smem, st, m, atoms, n, box_bytes, stages, dep,
+                            (uint8_t *)dst);
   if (e != cudaSuccess) return e;
   g_launches++;
   return cudaGetLastError();

@@ -11,9 +11,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <set>
-#include <unordered_map>
+#include <tuple>
 #include <utility>
 
 namespace axe {
@@ -25,16 +26,17 @@ int num_sms();
 // 1.33 waves).  Cap the grid at exactly one full wave of the kernel's measured occupancy.
 inline unsigned one_wave(const void *kern, int threads, size_t smem, unsigned blocks) {
   static std::mutex mu;
-  static std::unordered_map<const void *, int> occ;
+  static std::map<std::tuple<const void *, int, size_t>, int> occ;
   int o = 0;
   {
     std::lock_guard<std::mutex> lk(mu);
-    auto it = occ.find(kern);
+    const auto key = std::make_tuple(kern, threads, smem);
+    auto it = occ.find(key);
     if (it != occ.end()) {
       o = it->second;
     } else {
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem) != cudaSuccess) o = 0;
-      occ[kern] = o;
+      occ[key] = o;
     }
   }
   if (o <= 0) return blocks;

@@ -217,6 +217,7 @@ static int env_kernel() {
   if (!strcmp(e, "tma_tile")) return AXE_KERNEL_TMA_TILE;
   if (!strcmp(e, "shuffle")) return AXE_KERNEL_SHUFFLE;
   if (!strcmp(e, "transpose")) return AXE_KERNEL_TRANSPOSE;
+  if (!strcmp(e, "lowered")) return AXE_KERNEL_LOWERED;
   return AXE_KERNEL_AUTO;
 }
 
@@ -862,6 +863,16 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
 
   std::string why = lin ? (joint ? "" : "digit systems are not nested (no joint refinement)")
                         : "storage composition is not affine";
+  if (kernel == AXE_KERNEL_LOWERED) {
+    std::string wl = joint ? "" : why;
+    if (joint && rq.max_align >= 16 && build_lowered(J, ls, ld, *rq.sst, *rq.dstst, es, &P, &wl)) {
+      P.kernel = KK_LOWERED;
+      *out = std::move(P);
+      return AXE_OK;
+    }
+    AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced lowered schedule cannot run these layouts: %s",
+             rq.max_align < 16 ? "needs 16-byte aligned buffers" : wl.c_str());
+  }
   if (joint && rq.max_align >= 16 && (kernel == AXE_KERNEL_AUTO || kernel == AXE_KERNEL_TMA)) {
     std::string w0, w1, w2;
     // AUTO takes a TMA plan only with boxes of >= 4 KiB: 1 KiB boxes measured 35 us against K1's 21 us
@@ -869,6 +880,19 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
     const int64_t min_box = kernel == AXE_KERNEL_TMA ? 0 : env_int("AXE_TMA_MIN_BOX", 4096);
     const int64_t min_run = kernel == AXE_KERNEL_TMA ? 1024 : std::max<int64_t>(min_box, 1024);
     auto big = [&](bool ok) { return ok && (int64_t)P.tma.box_bytes >= min_box; };
+    if (big(build_tma(J, ls, ld, *rq.sst, *rq.dstst, es, 0, &P, &w0)) && kernel == AXE_KERNEL_AUTO &&
+        env_int("AXE_LOWERED_AUTO", 1)) {
+      // the paper's own lowering (slice -> tile_of the swizzle atom -> tensor map) when it
+      // reaches boxes as large as the joint-digit box: config 2 10.01 us vs 10.15 (64 MiB), 16384^2
+      // 180.4 vs 177.5 us
+      CopyPlan L = P;
+      std::string wl;
+      if (build_lowered(J, ls, ld, *rq.sst, *rq.dstst, es, &L, &wl) && lowered_box_bytes(L) >= P.tma.box_bytes) {
+        L.kernel = KK_LOWERED;
+        *out = std::move(L);
+        return AXE_OK;
+      }
+    }
     if (big(build_tma(J, ls, ld, *rq.sst, *rq.dstst, es, 0, &P, &w0)) ||
         big(build_tma(J, ls, ld, *rq.sst, *rq.dstst, es, 1, &P, &w1)) ||
         big(build_bulk(J, ls, ld, *rq.sst, *rq.dstst, es, min_run, &P, &w2))) {
@@ -1071,6 +1095,8 @@ axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t 
       e = launch_k3(k, p.blocks, src, dst, st);
       break;
     }
+    case KK_LOWERED:
+      return run_lowered(p, src, dst, st, dep);
     case KK_TRANSPOSE: {
       K7Params k = p.k7;
       k.dep = dep;

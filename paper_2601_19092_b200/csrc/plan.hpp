@@ -13,7 +13,7 @@
 
 namespace axe {
 
-enum KernelKind { KK_GENERIC = 1, KK_VECTOR = 2, KK_TMA = 3, KK_TILE = 4, KK_REGISTER = 5, KK_TMA_TILE = 6, KK_SHUFFLE = 7, KK_TRANSPOSE = 8 };
+enum KernelKind { KK_GENERIC = 1, KK_VECTOR = 2, KK_TMA = 3, KK_TILE = 4, KK_REGISTER = 5, KK_TMA_TILE = 6, KK_SHUFFLE = 7, KK_TRANSPOSE = 8, KK_LOWERED = 9 };
 
 struct CopyPlan {
   int kernel = KK_GENERIC;
@@ -48,6 +48,9 @@ struct CopyPlan {
   K7Params k7;
   // K2T TMA-staged transpose (uses the tm_* tensor map of the source)
   K2TParams k2t;
+  // the paper's TMA lowering as the schedule (tma_region.cpp): plan + destination byte offset of L_S
+  std::shared_ptr<axe_tma_plan> lowered;
+  int64_t lowered_dst_off = 0;
   // host-buffer pipeline (axe_copy_plan_execute_host): the copy splits into n_chunks
   // independent slabs (a joint digit spanning both whole buffers); each slab's
   // H2D, kernel and D2H run on three streams so PCIe traffic in both directions overlaps.
@@ -87,6 +90,10 @@ bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
 cudaError_t launch_k2(const K2Params &p, int vs, int vd, int gb, unsigned blocks, const void *src, void *dst,
                       cudaStream_t st);
 std::string joint_json(const std::vector<Joint> &J);
+bool build_lowered(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, const Storage &sst,
+                   const Storage &dstst, int es, CopyPlan *P, std::string *why);
+axe_status run_lowered(const CopyPlan &P, const void *src, void *dst, cudaStream_t st, int dep);
+uint32_t lowered_box_bytes(const CopyPlan &P);
 
 struct TmaCache {
   std::mutex mu;

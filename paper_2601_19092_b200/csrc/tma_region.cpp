@@ -8,7 +8,10 @@
 // (an HBM image of it: L_S on m with the swizzle of the atom).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <algorithm>
 #include <cstring>
+#include <string>
 #include <mutex>
 #include <vector>
 
@@ -18,23 +21,46 @@ namespace axe {
 int encode_tensor_map(void *out128, void *gaddr, const uint64_t dims[5], const uint64_t strides[4],
                       const uint32_t box[5], int swizzle_bytes);
 cudaError_t launch_tma_region(const void *map128, const TmaAtom *atoms, uint32_t n, uint32_t box_bytes, void *dst,
-                              cudaStream_t st);
+                              cudaStream_t st, int dep);
 }  // namespace axe
 
 using namespace axe;
+
+static bool getenv_fuse() {  // AXE_TMA_FUSE=0: one atom per box (tests compare both forms)
+  const char *e = getenv("AXE_TMA_FUSE");
+  return !(e && *e == '0');
+}
 
 struct axe_tma_plan {
   axe_tma_desc desc;
   int es = 1;
   uint32_t box_bytes = 0;     // one atom: 8 rows x swizzle_bytes
   int64_t image_bytes = 0;    // |T| atoms
-  std::vector<TmaAtom> host;  // per atom: tensor-map coordinates (byte units on dim 0) + image offset
+  std::vector<TmaAtom> host;  // per box: tensor-map coordinates (byte units on dim 0) + image offset
+  int fuse = 1, fuse_dim = -1;  // atoms per box along the rows (box[fuse_dim] = fuse)
   std::mutex mu;
   int dev = -1;
   TmaAtom *table = nullptr;  // device copy, uploaded by the first execute
   const void *map_for = nullptr;
   alignas(64) unsigned char map[128];
 };
+
+// the atom table on device `dev` (synchronous; not allowed inside graph capture)
+static cudaError_t upload(axe_tma_plan *plan, int dev) {
+  if (plan->table) cudaFree(plan->table);
+  plan->table = nullptr;
+  const size_t bytes = plan->host.size() * sizeof(TmaAtom);
+  cudaError_t e = cudaMalloc(&plan->table, bytes);
+  if (e == cudaSuccess) e = cudaMemcpy(plan->table, plan->host.data(), bytes, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    if (plan->table) cudaFree(plan->table);
+    plan->table = nullptr;
+    return e;
+  }
+  plan->dev = dev;
+  plan->map_for = nullptr;
+  return cudaSuccess;
+}
 
 extern "C" {
 
@@ -107,18 +133,65 @@ axe_status axe_tma_plan_create(const axe_tma_desc *desc, const axe_layout *tiler
     top = std::max(top, a.off + box);
   }
   p->image_bytes = top;
+  // fused boxes (desc->fused_rows > 8): f atoms stacked along the rows -- the row box dim rd (8 rows)
+  // continued by dim rd + 1 -- that sit in f consecutive slots become one box of f x 8 rows (one TMA
+  // instruction, "multiple atoms per instruction" as far as the box limits allow).  Checked
+  // against T atom by atom; any mismatch keeps one atom per box.
+  const int64_t f = desc->fused_rows / 8;
+  int rd = -1;
+  for (int d = 0; d + 1 < n; d++)
+    if (desc->logical_dim[d] == rank - 2 && desc->box[d] == 8 && desc->dims[d] == 8 &&
+        desc->logical_dim[d + 1] == rank - 2 && desc->box[d + 1] == 1 &&
+        desc->strides[d + 1] == desc->strides[d] * 8) {
+      rd = d;
+      break;
+    }
+  if (f > 1 && rd >= 0 && (int64_t)desc->dims[rd + 1] % f == 0 && getenv_fuse()) {
+    const int64_t rstep = Eo[rank - 1];  // atom-index step of one row tile (row-major over E_o)
+    bool ok = true;
+    std::vector<TmaAtom> heads;
+    for (int64_t t = 0; t < atoms && ok; t++) {
+      const TmaAtom &a = p->host[(size_t)t];
+      if (a.c[rd + 1] % f) continue;
+      for (int64_t k = 1; k < f && ok; k++) {
+        const int64_t u = t + k * rstep;
+        ok = u < atoms && p->host[(size_t)u].off == a.off + k * box && p->host[(size_t)u].c[rd + 1] == a.c[rd + 1] + k;
+      }
+      heads.push_back(a);
+    }
+    if (ok && (int64_t)heads.size() * f == atoms) {
+      p->host.swap(heads);
+      p->box_bytes = (uint32_t)(box * f);
+      p->fuse = (int)f;
+      p->fuse_dim = rd + 1;
+    }
+  }
+  // upload now when a device is current (so executes can be graph-captured); on a host without a
+  // GPU the first execute would upload -- there is no execute there
+  int ndev = 0, dev = 0;
+  if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0 && cudaGetDevice(&dev) == cudaSuccess) upload(p, dev);
+  cudaGetLastError();  // (clear a sticky-free error from the probe)
   *out = p;
   return AXE_OK;
 }
 
-axe_status axe_tma_plan_sizes(const axe_tma_plan *plan, int64_t *atoms, int64_t *image_bytes) {
+axe_status axe_tma_plan_sizes(const axe_tma_plan *plan, int64_t *atoms, int64_t *boxes, int64_t *image_bytes) {
   if (!plan) AXE_FAIL(AXE_ERR_INVALID_ARG, "plan is NULL");
-  if (atoms) *atoms = (int64_t)plan->host.size();
+  if (atoms) *atoms = (int64_t)plan->host.size() * plan->fuse;
+  if (boxes) *boxes = (int64_t)plan->host.size();
   if (image_bytes) *image_bytes = plan->image_bytes;
   return AXE_OK;
 }
 
+static axe_status tma_plan_run(axe_tma_plan *plan, const void *g_base, void *s_image, void *stream, int dep);
+
 axe_status axe_tma_plan_execute(axe_tma_plan *plan, const void *g_base, void *s_image, void *stream) {
+  return tma_plan_run(plan, g_base, s_image, stream, 1);  // (outside the copy planner's PDL window)
+}
+
+}  // extern "C"
+
+static axe_status tma_plan_run(axe_tma_plan *plan, const void *g_base, void *s_image, void *stream, int dep) {
   if (!plan || !g_base || !s_image) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
   const uint8_t *g = (const uint8_t *)g_base + plan->desc.base_bytes;
   if ((uintptr_t)g % 16 || (uintptr_t)s_image % 16)
@@ -128,14 +201,11 @@ axe_status axe_tma_plan_execute(axe_tma_plan *plan, const void *g_base, void *s_
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "cudaGetDevice");
   if (!plan->table || plan->dev != dev) {
-    if (plan->table) cudaFree(plan->table);
-    plan->table = nullptr;
-    const size_t bytes = plan->host.size() * sizeof(TmaAtom);
-    cudaError_t e = cudaMalloc(&plan->table, bytes);
-    if (e == cudaSuccess) e = cudaMemcpy(plan->table, plan->host.data(), bytes, cudaMemcpyHostToDevice);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+      AXE_FAIL(AXE_ERR_CUDA, "the atom table is not on this device yet: execute once outside graph capture");
+    const cudaError_t e = upload(plan, dev);
     if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "atom table: %s", cudaGetErrorString(e));
-    plan->dev = dev;
-    plan->map_for = nullptr;
   }
   if (plan->map_for != g) {
     // uint8 elements: dim 0 in bytes, the other dims as lowered (byte strides)
@@ -148,6 +218,7 @@ axe_status axe_tma_plan_execute(axe_tma_plan *plan, const void *g_base, void *s_
     }
     dims[0] *= (uint64_t)plan->es;
     box[0] *= (uint32_t)plan->es;
+    if (plan->fuse > 1) box[plan->fuse_dim] = (uint32_t)plan->fuse;
     uint64_t last = 16;  // unused trailing dims: extent 1, the last real stride
     for (int i = 1; i < 5; i++) {
       if (i < d.rank) last = d.strides[i];
@@ -158,10 +229,12 @@ axe_status axe_tma_plan_execute(axe_tma_plan *plan, const void *g_base, void *s_
     plan->map_for = g;
   }
   const cudaError_t e = launch_tma_region(plan->map, plan->table, (uint32_t)plan->host.size(), plan->box_bytes,
-                                          s_image, st);
+                                          s_image, st, dep);
   if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "tma region launch: %s", cudaGetErrorString(e));
   return AXE_OK;
 }
+
+extern "C" {
 
 void axe_tma_plan_destroy(axe_tma_plan *plan) {
   if (!plan) return;
@@ -170,3 +243,82 @@ void axe_tma_plan_destroy(axe_tma_plan *plan) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// The lowering as a copy schedule (AXE_KERNEL_LOWERED).  The joint digits of the copy, destination-
+// outermost first, are the logical dimensions of both tensors: L_G = (e_k):(src stride_k) + the
+// source base, L_S = (e_k):(dst stride_k).  When the destination storage carries a TMA swizzle and
+// L_S tiles its atom, axe_tma_lower gives the tensor map and T, and every (fused) atom box is one
+// TMA load + one bulk store -- config 2 is 4096 tiles x 8 atoms, fused into 64-row boxes.
+namespace axe {
+
+std::string joint_json(const std::vector<Joint> &J);
+
+bool build_lowered(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, const Storage &sst,
+                   const Storage &dstst, int es, CopyPlan *P, std::string *why) {
+  auto fail = [&](const std::string &m) {
+    *why = "lowered: " + m;
+    return false;
+  };
+  if (sst.swz_b) return fail("swizzled source");
+  if (!dstst.swz_b || dstst.swz_m != 4 || dstst.swz_s != 3 || dstst.swz_b > 3)
+    return fail("destination swizzle is not a TMA mode (Swizzle<1..3,4,3>)");
+  if (!ld.R.empty()) return fail("destination replicas");
+  const int sw = 16 << dstst.swz_b;
+  if ((ld.base * es) % (8 * sw)) return fail("destination base is not a whole swizzle atom");
+  std::vector<Joint> J;
+  for (auto &j : J0)
+    if (j.e > 1) J.push_back(j);
+  std::stable_sort(J.begin(), J.end(), [](const Joint &a, const Joint &b) { return std::llabs(a.ds) > std::llabs(b.ds); });
+  const int rank = (int)J.size();
+  if (rank < 2 || rank > 5) return fail("needs 2..5 joint digits");
+  const int m = axis_m();
+  std::vector<Iter> DG, DS;
+  std::vector<int64_t> E;
+  for (auto &j : J) {
+    if (j.ss <= 0 || j.ds <= 0) return fail("negative strides");
+    DG.push_back(Iter{j.e, j.ss, m});
+    DS.push_back(Iter{j.e, j.ds, m});
+    E.push_back(j.e);
+  }
+  axe_layout G, S;
+  std::vector<std::pair<int, int64_t>> O;
+  if (ls.base) O.push_back({m, ls.base});
+  if (make_layout(DG, {}, O, &G.L) != AXE_OK || make_layout(DS, {}, {}, &S.L) != AXE_OK) return fail(last_error());
+  axe_tma_desc d;
+  axe_layout *T = nullptr;
+  if (axe_tma_lower(&G, E.data(), nullptr, nullptr, &S, E.data(), rank, es, sw, &d, &T) != AXE_OK)
+    return fail(last_error());
+  axe_tma_plan *tp = nullptr;
+  const axe_status st = axe_tma_plan_create(&d, T, &tp);
+  axe_layout_destroy(T);
+  if (st != AXE_OK) return fail(last_error());
+  P->lowered = std::shared_ptr<axe_tma_plan>(tp, axe_tma_plan_destroy);
+  P->lowered_dst_off = ld.base * es;
+  P->align = 16;
+  int64_t total = 1;
+  for (auto &j : J) total *= j.e;
+  P->covers_all = total == dstst.cells;
+  char b[320];
+  snprintf(b, sizeof b,
+           "{\"kernel\":\"lowered\",\"atoms\":%lld,\"boxes\":%lld,\"box_bytes\":%u,\"swizzle\":%d,\"tensor_map\":{\"dims\":[",
+           (long long)(tp->host.size() * tp->fuse), (long long)tp->host.size(), tp->box_bytes, sw);
+  std::string s = b;
+  for (int i = 0; i < d.rank; i++) s += (i ? "," : "") + std::to_string(d.dims[i]);
+  s += "],\"strides\":[";
+  for (int i = 0; i < d.rank; i++) s += (i ? "," : "") + std::to_string(d.strides[i]);
+  s += "],\"box\":[";
+  for (int i = 0; i < d.rank; i++)
+    s += (i ? "," : "") + std::to_string(i == tp->fuse_dim ? (uint32_t)tp->fuse : d.box[i]);
+  s += "],\"base\":" + std::to_string(d.base_bytes) + "},\"joint\":" + joint_json(J0) + "}";
+  P->desc = s;
+  return true;
+}
+
+uint32_t lowered_box_bytes(const CopyPlan &P) { return P.lowered ? P.lowered->box_bytes : 0; }
+
+axe_status run_lowered(const CopyPlan &P, const void *src, void *dst, cudaStream_t st, int dep) {
+  return tma_plan_run(P.lowered.get(), src, (uint8_t *)dst + P.lowered_dst_off, st, dep);
+}
+
+}  // namespace axe

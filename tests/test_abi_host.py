@@ -134,11 +134,16 @@ def plan(cfg, kernel="auto"):
 
 
 def test_config2_plan_is_tma_box_copy():
-    """Config 2 lowers to the paper's TMA recipe: 64x128 B boxes, SW128 in smem."""
+    """Config 2 lowers to the paper's TMA recipe: AUTO runs the lowering itself (slice ->
+    tile_of the SW128 atom -> tensor map; 8 atoms fused per 64-row box); the joint-digit TMA planner
+    (forced "tma") finds the same 64 x 128 B boxes."""
     d = plan(synth.config2()).describe()
-    assert d["kernel"] == "tma" and d["box"] == [64, 128] and d["boxes"] == 4096 and d["swizzle"] == 128
+    assert d["kernel"] == "lowered" and d["atoms"] == 32768 and d["boxes"] == 4096 and d["box_bytes"] == 8192
+    assert d["swizzle"] == 128 and d["tensor_map"]["box"] == [64, 8, 8, 1, 1]
     # SURVEY §8(a) a4: joint digits (64:262144|262144),(64:4096|64),(64:64|4096),(64:1|1)
     assert d["joint"] == [[64, 262144, 262144], [64, 4096, 64], [64, 64, 4096], [64, 1, 1]]
+    t = plan(synth.config2(), "tma").describe()
+    assert t["kernel"] == "tma" and t["box"] == [64, 128] and t["boxes"] == 4096 and t["swizzle"] == 128
     r = plan(synth.config2(reverse=True)).describe()
     assert r["kernel"] == "tma" and r["mode"] == "bulk-load/tensor-store"
 

@@ -84,7 +84,7 @@ def test_config2_small(axe, n, es, sw, rev, kernel):
 def test_config2_full(axe, rev, kernel):
     """BASELINE config 2 at full size (4096^2 bf16); "auto" is the launch configuration bench.py times."""
     desc = check(axe, synth.config2(reverse=rev), kernel)
-    assert desc["kernel"] == ("tma" if kernel == "auto" else kernel)
+    assert desc["kernel"] == (("tma" if rev else "lowered") if kernel == "auto" else kernel)
 
 
 @pytest.mark.parametrize("rev", [False, True])
@@ -99,6 +99,33 @@ def test_tma_boxes_spanning_adjacent_tiles(axe, monkeypatch, box_max, n, t, es, 
     tile = t * t * es
     k = desc["tensor_map"]["box"][2]
     assert k > 1 and desc["box_bytes"] == k * tile <= box_max
+
+
+@pytest.mark.parametrize("fuse", ["1", "0"])
+@pytest.mark.parametrize("n,t,es,sw", [(4096, 64, 2, synth.SW128), (1024, 64, 2, synth.SW128),
+                                       (512, 32, 4, synth.SW128), (512, 64, 1, synth.SW64), (256, 16, 4, synth.SW64),
+                                       (256, 8, 4, synth.SW32), (128, 16, 8, synth.SW128)])
+def test_lowered_schedule(axe, monkeypatch, n, t, es, sw, fuse):
+    """The paper's TMA lowering as the copy schedule (AXE_KERNEL_LOWERED): config-2 re-tilings through
+    axe_tma_lower's tensor map and tiler, one TMA load + bulk store per atom (fuse=0) or per fused box."""
+    monkeypatch.setenv("AXE_TMA_FUSE", fuse)
+    cfg = synth.config2(n, t, es, sw)
+    desc = check(axe, cfg, "lowered", "lowered")
+    atom = 8 * (16 << sw[0])
+    assert desc["atoms"] * atom == n * n * es
+    assert desc["box_bytes"] == (atom if fuse == "0" else atom * desc["atoms"] // desc["boxes"])
+
+
+def test_lowered_schedule_offsets_and_grid_order(axe):
+    """Source base offset (a sub-matrix), destination base offset (whole atoms) and tiles stored
+    column-of-tiles first: the lowering's tiler T carries the tile order."""
+    R, Cn, ld, t, es = 256, 512, 640, 64, 2
+    src = layout([(R // t, t * ld), (t, ld), (Cn // t, t), (t, 1)], O={"m": 3 * ld + 64})
+    dst = layout([(R // t, t * t), (t, t), (Cn // t, (R // t) * t * t), (t, 1)], O={"m": 2 * t * t})
+    cfg = dict(name="lowered_off", es=es, src=src, src_st=linear_storage((R + 3) * ld),
+               dst=dst, dst_st=linear_storage(R * Cn + 2 * t * t, synth.SW128), seed=41)
+    d = check(axe, cfg, "lowered", "lowered")
+    assert d["tensor_map"]["base"] == (3 * ld + 64) * es
 
 
 @pytest.mark.parametrize("kernel", ["auto", "generic", "vector", "tile", "register", "shuffle"])
@@ -311,6 +338,33 @@ def test_dependent_chain_with_pdl(axe, kernel):
     torch.cuda.synchronize()
     assert torch.equal(a, x)
     # independent copies interleaved with dependent ones
+    outs = [torch.empty_like(x) for _ in range(4)]
+    for i in range(40):
+        pf.execute(x, outs[i % 4])
+    pr.execute(outs[1], c)
+    torch.cuda.synchronize()
+    assert torch.equal(c, x)
+
+
+def test_lowered_schedule_in_pdl_chains(axe):
+    """The lowered schedule joins the PDL window like every copy kernel: dependent chains forward
+    (lowered) / reverse (TMA store) return the input; independent lowered copies overlap."""
+    n = 1024
+    fwd, rev = synth.config2(n), synth.config2(n, reverse=True)
+    pf = axe.CopyPlan(fwd["src"], fwd["src_st"], fwd["dst"], fwd["dst_st"], 2, "lowered")
+    pr = axe.CopyPlan(rev["src"], rev["src_st"], rev["dst"], rev["dst_st"], 2)
+    x = torch.randint(-2**31, 2**31 - 1, (n * n // 2,), dtype=torch.int32, device="cuda")
+    a, b, c = x.clone(), torch.empty_like(x), torch.empty_like(x)
+    for _ in range(50):
+        pf.execute(a, b)
+        pr.execute(b, c)
+        pf.execute(c, a)
+        pr.execute(a, b)
+        pf.execute(b, a)
+        pr.execute(a, c)
+        a, c = c, a
+    torch.cuda.synchronize()
+    assert torch.equal(a, x)
     outs = [torch.empty_like(x) for _ in range(4)]
     for i in range(40):
         pf.execute(x, outs[i % 4])
