@@ -184,6 +184,10 @@ typedef struct axe_tma_plan axe_tma_plan;
 axe_status axe_tma_plan_create(const axe_tma_desc *desc, const axe_layout *tiler, axe_tma_plan **out);
 axe_status axe_tma_plan_sizes(const axe_tma_plan *plan, int64_t *atoms, int64_t *boxes, int64_t *image_bytes);
 axe_status axe_tma_plan_execute(axe_tma_plan *plan, const void *g_base, void *s_image, void *stream);
+/* The reverse (the lowering's TMA store, shared -> global): every box is bulk-loaded from the image
+ * and written to the region of the global tensor by one TMA tensor store (the hardware removes the
+ * swizzle).  Writes exactly the region's elements of g_base; same alignment rules and errors. */
+axe_status axe_tma_plan_execute_store(axe_tma_plan *plan, void *g_base, const void *s_image, void *stream);
 void axe_tma_plan_destroy(axe_tma_plan *plan);
 
 /* Textual form of the paper's matrix notation (Figures 2 and 5):

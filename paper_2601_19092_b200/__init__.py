@@ -96,6 +96,7 @@ _SIGS = {
     "axe_tma_plan_create": ([C.POINTER(axe_tma_desc), _vp, C.POINTER(_vp)], C.c_int),
     "axe_tma_plan_sizes": ([_vp, _pi64, _pi64, _pi64], C.c_int),
     "axe_tma_plan_execute": ([_vp, _vp, _vp, _vp], C.c_int),
+    "axe_tma_plan_execute_store": ([_vp, _vp, _vp, _vp], C.c_int),
     "axe_tma_plan_destroy": ([_vp], None),
     "axe_copy": ([_vp, C.POINTER(axe_storage), _vp, _vp, C.POINTER(axe_storage), _vp, C.c_int, _vp], C.c_int),
     "axe_get_unique_id": ([C.c_char_p], C.c_int),
@@ -658,6 +659,11 @@ class TmaPlan:
 
     def execute(self, g_base, s_image, stream=None):
         _check(_lib.axe_tma_plan_execute(self._h, _ptr(g_base), _ptr(s_image), _stream(stream)), "axe_tma_plan_execute")
+
+    def execute_store(self, g_base, s_image, stream=None):
+        """The reverse: the L_S image back into the region of the global tensor (TMA tensor stores)."""
+        _check(_lib.axe_tma_plan_execute_store(self._h, _ptr(g_base), _ptr(s_image), _stream(stream)),
+               "axe_tma_plan_execute_store")
 
 
 def axe_layout_create(D, R=(), O=None) -> Layout:

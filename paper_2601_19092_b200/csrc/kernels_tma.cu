@@ -291,14 +291,16 @@ cudaError_t launch_k2t(const void *map128, const K2TParams &p, int es, unsigned 
   return cudaGetLastError();
 }
 
-// The lowered TMA region (tma_region.cpp): one elected thread per CTA streams atoms through a
-// ring of 1 KiB-aligned slots -- tensor load (the hardware applies the atom's swizzle), then one
-// bulk store of the slot into the image at the tiler's offset.  Both copies run in the async
-// proxy, so no proxy fence is needed between them.
+// The lowered TMA region (tma_region.cpp): one elected thread per CTA streams boxes through a
+// ring of 1 KiB-aligned slots.  Load direction (G -> image): tensor load (the hardware applies the
+// atom's swizzle), then one bulk store of the slot into the image at the tiler's offset.  Store
+// direction (image -> G): bulk load of the slot from the image, then one tensor store (the hardware
+// un-swizzles).  Both copies of a box run in the async proxy, so no proxy fence is needed.
 constexpr int TR_STAGES = 8;  // ring capacity; the launch picks 2..8 stages (16 KiB of boxes per CTA)
+template <bool STORE>
 __global__ void __launch_bounds__(32) k_tma_region(const __grid_constant__ CUtensorMap map,
                                                    const TmaAtom *__restrict__ atoms, uint32_t n, uint32_t box,
-                                                   int stages, int dep, uint8_t *__restrict__ dst) {
+                                                   int stages, int dep, uint8_t *__restrict__ img) {
   extern __shared__ __align__(1024) uint8_t raw[];
   __shared__ __align__(8) uint64_t full[TR_STAGES];
   uint8_t *sm = (uint8_t *)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
@@ -315,13 +317,21 @@ __global__ void __launch_bounds__(32) k_tma_region(const __grid_constant__ CUten
     const uint32_t s = k % S;
     const TmaAtom a = atoms[first + k * step];
     mbar_expect_tx(&full[s], box);
-    tma_load5(sm + (size_t)s * slot, &map, &full[s], a.c[0], a.c[1], a.c[2], a.c[3], a.c[4]);
+    if constexpr (STORE)
+      bulk_load(sm + (size_t)s * slot, img + a.off, box, &full[s]);
+    else
+      tma_load5(sm + (size_t)s * slot, &map, &full[s], a.c[0], a.c[1], a.c[2], a.c[3], a.c[4]);
   };
   for (uint32_t k = 0; k < mine && k < S; k++) issue(k);
   for (uint32_t k = 0; k < mine; k++) {
     const uint32_t s = k % S;
     mbar_wait(&full[s], (k / S) & 1u);
-    bulk_store(dst + atoms[first + k * step].off, sm + (size_t)s * slot, box);
+    if constexpr (STORE) {
+      const TmaAtom a = atoms[first + k * step];
+      tma_store5(&map, sm + (size_t)s * slot, a.c[0], a.c[1], a.c[2], a.c[3], a.c[4]);
+    } else {
+      bulk_store(img + atoms[first + k * step].off, sm + (size_t)s * slot, box);
+    }
     bulk_commit();
     // refill the slot of the previous store (one store may still be reading: its own slot)
     if (k >= 1 && k - 1 + S < mine) {
@@ -374,25 +384,28 @@ int encode_tensor_map(void *out128, void *gaddr, const uint64_t dims[5], const u
   return (int)r;
 }
 
-cudaError_t launch_tma_region(const void *map128, const TmaAtom *atoms, uint32_t n, uint32_t box_bytes, void *dst,
-                              cudaStream_t st, int dep) {
+cudaError_t launch_tma_region(const void *map128, const TmaAtom *atoms, uint32_t n, uint32_t box_bytes, void *img,
+                              cudaStream_t st, int dep, int store) {
   if (n == 0) return cudaSuccess;
-  const cudaError_t attr_err = smem_attr((const void *)k_tma_region, 200 * 1024);
+  const void *kern = store ? (const void *)k_tma_region<true> : (const void *)k_tma_region<false>;
+  const cudaError_t attr_err = smem_attr(kern, 200 * 1024);
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap m;
   memcpy(&m, map128, sizeof(m));
   const size_t slot = (box_bytes + 1023) & ~(size_t)1023;
   const int stages = (int)std::max<size_t>(2, std::min<size_t>(TR_STAGES, 16384 / slot));
   const size_t smem = stages * slot + 1024;
-  // CTAs per SM (AXE_TMA_PER_SM; capped by occupancy)
+  // CTAs per SM (AXE_TMA_REGION_PER_SM, default 16; capped by occupancy): config 2 10.01 us with 16,
+  // 10.04 with 8; 16384^2 180.4 us with 16, 184.3 with 8
   static const int per_sm = [] {
-    const char *e = getenv("AXE_TMA_PER_SM");
+    const char *e = getenv("AXE_TMA_REGION_PER_SM");
     return (e && *e) ? std::max(1, atoi(e)) : 16;
   }();
-  const unsigned blocks = one_wave((const void *)k_tma_region, 32, smem,
-                                   (unsigned)std::min<int64_t>(n, (int64_t)num_sms() * per_sm));
-  cudaError_t e = launch_ex(k_tma_region, dim3(blocks), dim3(32), smem, st, m, atoms, n, box_bytes, stages, dep,
-                            (uint8_t *)dst);
+  const unsigned blocks = one_wave(kern, 32, smem, (unsigned)std::min<int64_t>(n, (int64_t)num_sms() * per_sm));
+  cudaError_t e = store ? launch_ex(k_tma_region<true>, dim3(blocks), dim3(32), smem, st, m, atoms, n, box_bytes,
+                                    stages, dep, (uint8_t *)img)
+                        : launch_ex(k_tma_region<false>, dim3(blocks), dim3(32), smem, st, m, atoms, n, box_bytes,
+                                    stages, dep, (uint8_t *)img);
   if (e != cudaSuccess) return e;
   g_launches++;
   return cudaGetLastError();

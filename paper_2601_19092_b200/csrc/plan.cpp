@@ -880,11 +880,12 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
     const int64_t min_box = kernel == AXE_KERNEL_TMA ? 0 : env_int("AXE_TMA_MIN_BOX", 4096);
     const int64_t min_run = kernel == AXE_KERNEL_TMA ? 1024 : std::max<int64_t>(min_box, 1024);
     auto big = [&](bool ok) { return ok && (int64_t)P.tma.box_bytes >= min_box; };
-    if (big(build_tma(J, ls, ld, *rq.sst, *rq.dstst, es, 0, &P, &w0)) && kernel == AXE_KERNEL_AUTO &&
-        env_int("AXE_LOWERED_AUTO", 1)) {
+    if (kernel == AXE_KERNEL_AUTO && env_int("AXE_LOWERED_AUTO", 1) &&
+        (big(build_tma(J, ls, ld, *rq.sst, *rq.dstst, es, 0, &P, &w0)) ||
+         big(build_tma(J, ls, ld, *rq.sst, *rq.dstst, es, 1, &P, &w1)))) {
       // the paper's own lowering (slice -> tile_of the swizzle atom -> tensor map) when it
       // reaches boxes as large as the joint-digit box: config 2 10.01 us vs 10.15 (64 MiB), 16384^2
-      // 180.4 vs 177.5 us
+      // 180.4 vs 177.5 us; reversed (TMA stores) 10.31 vs 10.46 us
       CopyPlan L = P;
       std::string wl;
       if (build_lowered(J, ls, ld, *rq.sst, *rq.dstst, es, &L, &wl) && lowered_box_bytes(L) >= P.tma.box_bytes) {

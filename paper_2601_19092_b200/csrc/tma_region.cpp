@@ -20,8 +20,8 @@
 namespace axe {
 int encode_tensor_map(void *out128, void *gaddr, const uint64_t dims[5], const uint64_t strides[4],
                       const uint32_t box[5], int swizzle_bytes);
-cudaError_t launch_tma_region(const void *map128, const TmaAtom *atoms, uint32_t n, uint32_t box_bytes, void *dst,
-                              cudaStream_t st, int dep);
+cudaError_t launch_tma_region(const void *map128, const TmaAtom *atoms, uint32_t n, uint32_t box_bytes, void *img,
+                              cudaStream_t st, int dep, int store);
 }  // namespace axe
 
 using namespace axe;
@@ -183,15 +183,21 @@ axe_status axe_tma_plan_sizes(const axe_tma_plan *plan, int64_t *atoms, int64_t 
   return AXE_OK;
 }
 
-static axe_status tma_plan_run(axe_tma_plan *plan, const void *g_base, void *s_image, void *stream, int dep);
+static axe_status tma_plan_run(axe_tma_plan *plan, const void *g_base, const void *s_image, void *stream, int dep,
+                               int store);
 
 axe_status axe_tma_plan_execute(axe_tma_plan *plan, const void *g_base, void *s_image, void *stream) {
-  return tma_plan_run(plan, g_base, s_image, stream, 1);  // (outside the copy planner's PDL window)
+  return tma_plan_run(plan, g_base, s_image, stream, 1, 0);  // (outside the copy planner's PDL window)
+}
+
+axe_status axe_tma_plan_execute_store(axe_tma_plan *plan, void *g_base, const void *s_image, void *stream) {
+  return tma_plan_run(plan, g_base, s_image, stream, 1, 1);
 }
 
 }  // extern "C"
 
-static axe_status tma_plan_run(axe_tma_plan *plan, const void *g_base, void *s_image, void *stream, int dep) {
+static axe_status tma_plan_run(axe_tma_plan *plan, const void *g_base, const void *s_image, void *stream, int dep,
+                               int store) {
   if (!plan || !g_base || !s_image) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
   const uint8_t *g = (const uint8_t *)g_base + plan->desc.base_bytes;
   if ((uintptr_t)g % 16 || (uintptr_t)s_image % 16)
@@ -229,7 +235,7 @@ static axe_status tma_plan_run(axe_tma_plan *plan, const void *g_base, void *s_i
     plan->map_for = g;
   }
   const cudaError_t e = launch_tma_region(plan->map, plan->table, (uint32_t)plan->host.size(), plan->box_bytes,
-                                          s_image, st, dep);
+                                          (void *)s_image, st, dep, store);
   if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "tma region launch: %s", cudaGetErrorString(e));
   return AXE_OK;
 }
@@ -260,15 +266,20 @@ bool build_lowered(const std::vector<Joint> &J0, const Linear &ls, const Linear 
     *why = "lowered: " + m;
     return false;
   };
-  if (sst.swz_b) return fail("swizzled source");
-  if (!dstst.swz_b || dstst.swz_m != 4 || dstst.swz_s != 3 || dstst.swz_b > 3)
-    return fail("destination swizzle is not a TMA mode (Swizzle<1..3,4,3>)");
   if (!ld.R.empty()) return fail("destination replicas");
-  const int sw = 16 << dstst.swz_b;
-  if ((ld.base * es) % (8 * sw)) return fail("destination base is not a whole swizzle atom");
+  auto tma_swz = [](const Storage &t) { return t.swz_b >= 1 && t.swz_b <= 3 && t.swz_m == 4 && t.swz_s == 3; };
+  // load direction: unswizzled source = L_G, swizzled destination = L_S image; store direction
+  // (the reverse, e.g. config 2's tiles -> row-major): swizzled source = L_S image, destination = L_G
+  const bool store = !tma_swz(dstst);
+  const Storage &img_st = store ? sst : dstst, &g_st = store ? dstst : sst;
+  const Linear &lg = store ? ld : ls, &li = store ? ls : ld;
+  if (!tma_swz(img_st)) return fail("neither side carries a TMA swizzle (Swizzle<1..3,4,3>)");
+  if (g_st.swz_b) return fail("both sides swizzled");
+  const int sw = 16 << img_st.swz_b;
+  if ((li.base * es) % (8 * sw)) return fail("the swizzled side's base is not a whole swizzle atom");
   std::vector<Joint> J;
   for (auto &j : J0)
-    if (j.e > 1) J.push_back(j);
+    if (j.e > 1) J.push_back(store ? Joint{j.e, j.ds, j.ss, j.ddev, j.sdev} : j);  // (ss: G side, ds: image side)
   std::stable_sort(J.begin(), J.end(), [](const Joint &a, const Joint &b) { return std::llabs(a.ds) > std::llabs(b.ds); });
   const int rank = (int)J.size();
   if (rank < 2 || rank > 5) return fail("needs 2..5 joint digits");
@@ -283,7 +294,7 @@ bool build_lowered(const std::vector<Joint> &J0, const Linear &ls, const Linear 
   }
   axe_layout G, S;
   std::vector<std::pair<int, int64_t>> O;
-  if (ls.base) O.push_back({m, ls.base});
+  if (lg.base) O.push_back({m, lg.base});
   if (make_layout(DG, {}, O, &G.L) != AXE_OK || make_layout(DS, {}, {}, &S.L) != AXE_OK) return fail(last_error());
   axe_tma_desc d;
   axe_layout *T = nullptr;
@@ -294,15 +305,18 @@ bool build_lowered(const std::vector<Joint> &J0, const Linear &ls, const Linear 
   axe_layout_destroy(T);
   if (st != AXE_OK) return fail(last_error());
   P->lowered = std::shared_ptr<axe_tma_plan>(tp, axe_tma_plan_destroy);
-  P->lowered_dst_off = ld.base * es;
+  P->lowered_dst_off = li.base * es;  // byte offset of the L_S image in its buffer
+  P->lowered_store = store;
   P->align = 16;
   int64_t total = 1;
   for (auto &j : J) total *= j.e;
   P->covers_all = total == dstst.cells;
   char b[320];
   snprintf(b, sizeof b,
-           "{\"kernel\":\"lowered\",\"atoms\":%lld,\"boxes\":%lld,\"box_bytes\":%u,\"swizzle\":%d,\"tensor_map\":{\"dims\":[",
-           (long long)(tp->host.size() * tp->fuse), (long long)tp->host.size(), tp->box_bytes, sw);
+           "{\"kernel\":\"lowered\",\"mode\":\"%s\",\"atoms\":%lld,\"boxes\":%lld,\"box_bytes\":%u,\"swizzle\":%d,"
+           "\"tensor_map\":{\"dims\":[",
+           store ? "bulk-load/tensor-store" : "tensor-load/bulk-store", (long long)(tp->host.size() * tp->fuse),
+           (long long)tp->host.size(), tp->box_bytes, sw);
   std::string s = b;
   for (int i = 0; i < d.rank; i++) s += (i ? "," : "") + std::to_string(d.dims[i]);
   s += "],\"strides\":[";
@@ -318,7 +332,8 @@ bool build_lowered(const std::vector<Joint> &J0, const Linear &ls, const Linear 
 uint32_t lowered_box_bytes(const CopyPlan &P) { return P.lowered ? P.lowered->box_bytes : 0; }
 
 axe_status run_lowered(const CopyPlan &P, const void *src, void *dst, cudaStream_t st, int dep) {
-  return tma_plan_run(P.lowered.get(), src, (uint8_t *)dst + P.lowered_dst_off, st, dep);
+  if (P.lowered_store) return tma_plan_run(P.lowered.get(), dst, (const uint8_t *)src + P.lowered_dst_off, st, dep, 1);
+  return tma_plan_run(P.lowered.get(), src, (uint8_t *)dst + P.lowered_dst_off, st, dep, 0);
 }
 
 }  // namespace axe

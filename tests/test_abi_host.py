@@ -145,7 +145,8 @@ def test_config2_plan_is_tma_box_copy():
     t = plan(synth.config2(), "tma").describe()
     assert t["kernel"] == "tma" and t["box"] == [64, 128] and t["boxes"] == 4096 and t["swizzle"] == 128
     r = plan(synth.config2(reverse=True)).describe()
-    assert r["kernel"] == "tma" and r["mode"] == "bulk-load/tensor-store"
+    assert r["kernel"] == "lowered" and r["mode"] == "bulk-load/tensor-store"
+    assert plan(synth.config2(reverse=True), "tma").describe()["mode"] == "bulk-load/tensor-store"
 
 
 def test_config2_vector_plan():

@@ -84,7 +84,7 @@ def test_config2_small(axe, n, es, sw, rev, kernel):
 def test_config2_full(axe, rev, kernel):
     """BASELINE config 2 at full size (4096^2 bf16); "auto" is the launch configuration bench.py times."""
     desc = check(axe, synth.config2(reverse=rev), kernel)
-    assert desc["kernel"] == (("tma" if rev else "lowered") if kernel == "auto" else kernel)
+    assert desc["kernel"] == ("lowered" if kernel == "auto" else kernel)
 
 
 @pytest.mark.parametrize("rev", [False, True])
@@ -114,6 +114,14 @@ def test_lowered_schedule(axe, monkeypatch, n, t, es, sw, fuse):
     atom = 8 * (16 << sw[0])
     assert desc["atoms"] * atom == n * n * es
     assert desc["box_bytes"] == (atom if fuse == "0" else atom * desc["atoms"] // desc["boxes"])
+
+
+@pytest.mark.parametrize("n,t,es,sw", [(4096, 64, 2, synth.SW128), (512, 32, 4, synth.SW128), (256, 16, 4, synth.SW64),
+                                       (256, 8, 4, synth.SW32)])
+def test_lowered_schedule_reverse(axe, n, t, es, sw):
+    """Config 2 reversed (swizzled tiles -> row-major) through the lowering's TMA stores."""
+    desc = check(axe, synth.config2(n, t, es, sw, True), "lowered", "lowered")
+    assert desc["mode"] == "bulk-load/tensor-store"
 
 
 def test_lowered_schedule_offsets_and_grid_order(axe):

@@ -60,6 +60,15 @@ def run_case(axe, rows, cols, ld, begin, ES, LS, es, sw, seed):
     if not np.array_equal(got, exp):
         bad = np.nonzero(got != exp)[0]
         raise AssertionError(f"{len(bad)} bytes differ, first at {bad[:8]}")
+    # the reverse (TMA stores): the image back into a sentinel-filled global tensor; expected = the
+    # oracle's copy of L_S (swizzled) into the hand-written region layout
+    g2 = synth.sentinel(gbytes, seed + 2)
+    exp2 = g2.copy()
+    oracle.copy(LS, linear_storage(img // es, SW[sw]), exp, region, linear_storage(rows * ld), exp2, es)
+    gd2 = torch.from_numpy(g2).cuda()
+    plan.execute_store(gd2, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(gd2.cpu().numpy(), exp2), "store direction"
     return plan
 
 
