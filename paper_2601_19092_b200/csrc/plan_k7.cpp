@@ -32,14 +32,15 @@ bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   // chunk columns per warp (tiles of 32 n rows x 8 n cw columns), as wide as the columns allow:
   // 4 for 4-byte elements (8192^2 fp32: 94.9 us vs 100.8 / 104.3 with 2 / 1), 2 otherwise (bf16:
   // 43.2 us vs 44.9 with 1; 8192x4096 fp64: 94.1 us vs 98.6 with 4)
-  // The cp.async double-buffered form (next tile in flight while the current one is stored) with cw = 2:
-  // fp32 93.3 us vs 95.8 (register-staged, cw 4) / 101.7 (register-staged, cw 2); bf16 42.4 vs 42.9;
-  // fp64 95.2 vs 94.0-94.8, so 8-byte elements stay register-staged.
+  // The cp.async double-buffered form (next tile in flight while the current one is stored): fp32
+  // (cw 2) 93.3 us vs 95.8 register-staged (cw 4) / 101.7 (cw 2); bf16 (cw 2) 42.4 vs 42.9; fp64 (cw 4,
+  // 64 x 64 tiles) 92.8 vs 94.5 register-staged (cw 2) / 94.6 (async, cw 2)
   const char *ae = getenv("AXE_K7_ASYNC");
-  const int async = (ae && *ae) ? (atoi(ae) != 0) : (es <= 4);
+  const int async = (ae && *ae) ? (atoi(ae) != 0) : 1;
   const char *cwe = getenv("AXE_K7_CW");
-  const int cwmax = es == 4 ? 4 : 2;
-  int64_t cw = (cwe && *cwe) ? std::max(1, std::min(cwmax, atoi(cwe))) : (async ? 2 : cwmax);
+  const int cwmax = es == 2 ? 2 : 4;
+  const int cwdef = async ? (es == 8 ? 4 : 2) : (es == 4 ? 4 : 2);
+  int64_t cw = (cwe && *cwe) ? std::max(1, std::min(cwmax, atoi(cwe))) : cwdef;
   std::vector<Joint> J;
   for (auto &j : J0)
     if (j.e > 1) J.push_back(j);

@@ -285,7 +285,7 @@ def test_transposes_all_kernels(axe, R, Cn, es):
         check(axe, cfg, k)
 
 
-@pytest.mark.parametrize("es,cw", [(2, 1), (2, 2), (4, 1), (4, 2), (4, 4), (8, 1), (8, 2)])
+@pytest.mark.parametrize("es,cw", [(2, 1), (2, 2), (4, 1), (4, 2), (4, 4), (8, 1), (8, 2), (8, 4)])
 @pytest.mark.parametrize("asyn", [0, 1])
 def test_k7_batched_padded_transposes(axe, monkeypatch, es, cw, asyn):
     """K7 directly: 3 batched transposes of (2 TR) x (3 TC) tiles, padded source rows and destination columns,
@@ -295,7 +295,7 @@ def test_k7_batched_padded_transposes(axe, monkeypatch, es, cw, asyn):
     monkeypatch.setenv("AXE_K7_ASYNC", str(asyn))
     monkeypatch.setenv("AXE_K7_MAX_CTAS", "4")
     n = 16 // es
-    cw = min(cw, 4 if es == 4 else 2)   # the widest chunk column the planner takes for this element size
+    cw = min(cw, 2 if es == 2 else 4)   # the widest chunk column the planner takes for this element size
     R, C = 2 * 32 * n, 3 * 8 * n * cw
     lds, ldd = C + n, R + 2 * n
     B = 3
