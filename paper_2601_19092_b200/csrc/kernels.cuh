@@ -102,6 +102,11 @@ struct TmaAtom {
   int32_t pad;
   int64_t off;
 };
+// destination replicas of a lowered load (byte offsets added to every box's image offset)
+struct TmaReps {
+  int n;
+  int64_t r[K1_MAXREP];
+};
 
 struct TmaParams {
   uint32_t nboxes;

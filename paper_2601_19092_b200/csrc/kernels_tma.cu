@@ -300,7 +300,8 @@ constexpr int TR_STAGES = 8;  // ring capacity; the launch picks 2..8 stages (16
 template <bool STORE>
 __global__ void __launch_bounds__(32) k_tma_region(const __grid_constant__ CUtensorMap map,
                                                    const TmaAtom *__restrict__ atoms, uint32_t n, uint32_t box,
-                                                   int stages, int dep, uint8_t *__restrict__ img) {
+                                                   int stages, int dep, uint8_t *__restrict__ img,
+                                                   const __grid_constant__ TmaReps reps) {
   extern __shared__ __align__(1024) uint8_t raw[];
   __shared__ __align__(8) uint64_t full[TR_STAGES];
   uint8_t *sm = (uint8_t *)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
@@ -330,7 +331,8 @@ __global__ void __launch_bounds__(32) k_tma_region(const __grid_constant__ CUten
       const TmaAtom a = atoms[first + k * step];
       tma_store5(&map, sm + (size_t)s * slot, a.c[0], a.c[1], a.c[2], a.c[3], a.c[4]);
     } else {
-      bulk_store(img + atoms[first + k * step].off, sm + (size_t)s * slot, box);
+      const int64_t off = atoms[first + k * step].off;
+      for (int r = 0; r < reps.n; r++) bulk_store(img + off + reps.r[r], sm + (size_t)s * slot, box);
     }
     bulk_commit();
     // refill the slot of the previous store (one store may still be reading: its own slot)
@@ -385,7 +387,7 @@ int encode_tensor_map(void *out128, void *gaddr, const uint64_t dims[5], const u
 }
 
 cudaError_t launch_tma_region(const void *map128, const TmaAtom *atoms, uint32_t n, uint32_t box_bytes, void *img,
-                              cudaStream_t st, int dep, int store) {
+                              cudaStream_t st, int dep, int store, const TmaReps &reps) {
   if (n == 0) return cudaSuccess;
   const void *kern = store ? (const void *)k_tma_region<true> : (const void *)k_tma_region<false>;
   const cudaError_t attr_err = smem_attr(kern, 200 * 1024);
@@ -403,9 +405,9 @@ cudaError_t launch_tma_region(const void *map128, const TmaAtom *atoms, uint32_t
   }();
   const unsigned blocks = one_wave(kern, 32, smem, (unsigned)std::min<int64_t>(n, (int64_t)num_sms() * per_sm));
   cudaError_t e = store ? launch_ex(k_tma_region<true>, dim3(blocks), dim3(32), smem, st, m, atoms, n, box_bytes,
-                                    stages, dep, (uint8_t *)img)
+                                    stages, dep, (uint8_t *)img, reps)
                         : launch_ex(k_tma_region<false>, dim3(blocks), dim3(32), smem, st, m, atoms, n, box_bytes,
-                                    stages, dep, (uint8_t *)img);
+                                    stages, dep, (uint8_t *)img, reps);
   if (e != cudaSuccess) return e;
   g_launches++;
   return cudaGetLastError();

@@ -52,6 +52,7 @@ struct CopyPlan {
   std::shared_ptr<axe_tma_plan> lowered;
   int64_t lowered_dst_off = 0;  // byte offset of the L_S image (the destination, or the source when storing)
   bool lowered_store = false;    // image -> G (bulk load + TMA tensor store)
+  TmaReps lowered_reps{};        // destination replica byte offsets (load direction)
   // host-buffer pipeline (axe_copy_plan_execute_host): the copy splits into n_chunks
   // independent slabs (a joint digit spanning both whole buffers); each slab's
   // H2D, kernel and D2H run on three streams so PCIe traffic in both directions overlaps.

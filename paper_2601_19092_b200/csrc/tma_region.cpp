@@ -21,7 +21,7 @@ namespace axe {
 int encode_tensor_map(void *out128, void *gaddr, const uint64_t dims[5], const uint64_t strides[4],
                       const uint32_t box[5], int swizzle_bytes);
 cudaError_t launch_tma_region(const void *map128, const TmaAtom *atoms, uint32_t n, uint32_t box_bytes, void *img,
-                              cudaStream_t st, int dep, int store);
+                              cudaStream_t st, int dep, int store, const TmaReps &reps);
 }  // namespace axe
 
 using namespace axe;
@@ -184,7 +184,7 @@ axe_status axe_tma_plan_sizes(const axe_tma_plan *plan, int64_t *atoms, int64_t 
 }
 
 static axe_status tma_plan_run(axe_tma_plan *plan, const void *g_base, const void *s_image, void *stream, int dep,
-                               int store);
+                               int store, const TmaReps *reps = nullptr);
 
 axe_status axe_tma_plan_execute(axe_tma_plan *plan, const void *g_base, void *s_image, void *stream) {
   return tma_plan_run(plan, g_base, s_image, stream, 1, 0);  // (outside the copy planner's PDL window)
@@ -197,7 +197,7 @@ axe_status axe_tma_plan_execute_store(axe_tma_plan *plan, void *g_base, const vo
 }  // extern "C"
 
 static axe_status tma_plan_run(axe_tma_plan *plan, const void *g_base, const void *s_image, void *stream, int dep,
-                               int store) {
+                               int store, const TmaReps *reps) {
   if (!plan || !g_base || !s_image) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
   const uint8_t *g = (const uint8_t *)g_base + plan->desc.base_bytes;
   if ((uintptr_t)g % 16 || (uintptr_t)s_image % 16)
@@ -234,8 +234,11 @@ static axe_status tma_plan_run(axe_tma_plan *plan, const void *g_base, const voi
     if (r != 0) AXE_FAIL(AXE_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", r);
     plan->map_for = g;
   }
+  TmaReps one;
+  memset(&one, 0, sizeof(one));
+  one.n = 1;
   const cudaError_t e = launch_tma_region(plan->map, plan->table, (uint32_t)plan->host.size(), plan->box_bytes,
-                                          (void *)s_image, st, dep, store);
+                                          (void *)s_image, st, dep, store, reps ? *reps : one);
   if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "tma region launch: %s", cudaGetErrorString(e));
   return AXE_OK;
 }
@@ -266,7 +269,6 @@ bool build_lowered(const std::vector<Joint> &J0, const Linear &ls, const Linear 
     *why = "lowered: " + m;
     return false;
   };
-  if (!ld.R.empty()) return fail("destination replicas");
   auto tma_swz = [](const Storage &t) { return t.swz_b >= 1 && t.swz_b <= 3 && t.swz_m == 4 && t.swz_s == 3; };
   // load direction: unswizzled source = L_G, swizzled destination = L_S image; store direction
   // (the reverse, e.g. config 2's tiles -> row-major): swizzled source = L_S image, destination = L_G
@@ -277,6 +279,21 @@ bool build_lowered(const std::vector<Joint> &J0, const Linear &ls, const Linear 
   if (g_st.swz_b) return fail("both sides swizzled");
   const int sw = 16 << img_st.swz_b;
   if ((li.base * es) % (8 * sw)) return fail("the swizzled side's base is not a whole swizzle atom");
+  // destination replicas: every box leaves once per replica (load direction; a TMA store writes one place)
+  std::vector<int64_t> reps{0};
+  for (auto &r : ld.R) {
+    std::vector<int64_t> nx;
+    for (int64_t x : reps)
+      for (int64_t q = 0; q < r.e; q++) nx.push_back(x + q * r.s);
+    reps.swap(nx);
+    if (reps.size() > 4096) break;
+  }
+  std::sort(reps.begin(), reps.end());
+  reps.erase(std::unique(reps.begin(), reps.end()), reps.end());
+  if (reps.size() > 1 && store) return fail("destination replicas with TMA stores");
+  if ((int)reps.size() > K1_MAXREP) return fail("too many replicas");
+  for (int64_t r : reps)
+    if ((r * es) % (8 * sw)) return fail("replica offsets are not whole swizzle atoms");
   std::vector<Joint> J;
   for (auto &j : J0)
     if (j.e > 1) J.push_back(store ? Joint{j.e, j.ds, j.ss, j.ddev, j.sdev} : j);  // (ss: G side, ds: image side)
@@ -307,16 +324,19 @@ bool build_lowered(const std::vector<Joint> &J0, const Linear &ls, const Linear 
   P->lowered = std::shared_ptr<axe_tma_plan>(tp, axe_tma_plan_destroy);
   P->lowered_dst_off = li.base * es;  // byte offset of the L_S image in its buffer
   P->lowered_store = store;
+  memset(&P->lowered_reps, 0, sizeof(P->lowered_reps));
+  P->lowered_reps.n = (int)reps.size();
+  for (size_t i = 0; i < reps.size(); i++) P->lowered_reps.r[i] = reps[i] * es;
   P->align = 16;
   int64_t total = 1;
   for (auto &j : J) total *= j.e;
-  P->covers_all = total == dstst.cells;
+  P->covers_all = total * (int64_t)reps.size() == dstst.cells;
   char b[320];
   snprintf(b, sizeof b,
            "{\"kernel\":\"lowered\",\"mode\":\"%s\",\"atoms\":%lld,\"boxes\":%lld,\"box_bytes\":%u,\"swizzle\":%d,"
-           "\"tensor_map\":{\"dims\":[",
+           "\"replicas\":%d,\"tensor_map\":{\"dims\":[",
            store ? "bulk-load/tensor-store" : "tensor-load/bulk-store", (long long)(tp->host.size() * tp->fuse),
-           (long long)tp->host.size(), tp->box_bytes, sw);
+           (long long)tp->host.size(), tp->box_bytes, sw, (int)reps.size());
   std::string s = b;
   for (int i = 0; i < d.rank; i++) s += (i ? "," : "") + std::to_string(d.dims[i]);
   s += "],\"strides\":[";
@@ -333,7 +353,7 @@ uint32_t lowered_box_bytes(const CopyPlan &P) { return P.lowered ? P.lowered->bo
 
 axe_status run_lowered(const CopyPlan &P, const void *src, void *dst, cudaStream_t st, int dep) {
   if (P.lowered_store) return tma_plan_run(P.lowered.get(), dst, (const uint8_t *)src + P.lowered_dst_off, st, dep, 1);
-  return tma_plan_run(P.lowered.get(), src, (uint8_t *)dst + P.lowered_dst_off, st, dep, 0);
+  return tma_plan_run(P.lowered.get(), src, (uint8_t *)dst + P.lowered_dst_off, st, dep, 0, &P.lowered_reps);
 }
 
 }  // namespace axe

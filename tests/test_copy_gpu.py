@@ -124,6 +124,18 @@ def test_lowered_schedule_reverse(axe, n, t, es, sw):
     assert desc["mode"] == "bulk-load/tensor-store"
 
 
+@pytest.mark.parametrize("kernel", ["lowered", "auto"])
+def test_lowered_schedule_destination_replicas(axe, kernel):
+    """Config 2 into three replicas of the tiled destination (whole tiles apart): each fused box leaves
+    once per replica."""
+    n = 512
+    cfg = synth.config2(n)
+    cfg = dict(cfg, name="c2_rep", dst=layout(cfg["dst"]["D"], [(3, n * n)]),
+               dst_st=linear_storage(3 * n * n, synth.SW128))
+    d = check(axe, cfg, kernel, "lowered")
+    assert d["replicas"] == 3
+
+
 def test_lowered_schedule_offsets_and_grid_order(axe):
     """Source base offset (a sub-matrix), destination base offset (whole atoms) and tiles stored
     column-of-tiles first: the lowering's tiler T carries the tile order."""
