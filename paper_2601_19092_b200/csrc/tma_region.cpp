@@ -40,7 +40,7 @@ struct axe_tma_plan {
   int fuse = 1, fuse_dim = -1;  // atoms per box along the rows (box[fuse_dim] = fuse)
   std::mutex mu;
   int dev = -1;
-  TmaAtom *table = nullptr;  // device copy, uploaded by the first execute
+  TmaAtom *table = nullptr;  // device copy (uploaded at create, or by an execute on another device)
   const void *map_for = nullptr;
   alignas(64) unsigned char map[128];
 };
@@ -60,6 +60,53 @@ static cudaError_t upload(axe_tma_plan *plan, int dev) {
   plan->dev = dev;
   plan->map_for = nullptr;
   return cudaSuccess;
+}
+
+static axe_status tma_plan_run(axe_tma_plan *plan, const void *g_base, const void *s_image, void *stream, int dep,
+                               int store, const TmaReps *reps = nullptr) {
+  if (!plan || !g_base || !s_image) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
+  const uint8_t *g = (const uint8_t *)g_base + plan->desc.base_bytes;
+  if ((uintptr_t)g % 16 || (uintptr_t)s_image % 16)
+    AXE_FAIL(AXE_ERR_ALIGNMENT, "region start and image must be 16-byte aligned");
+  cudaStream_t st = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> lk(plan->mu);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "cudaGetDevice");
+  if (!plan->table || plan->dev != dev) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+      AXE_FAIL(AXE_ERR_CUDA, "the atom table is not on this device yet: execute once outside graph capture");
+    const cudaError_t e = upload(plan, dev);
+    if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "atom table: %s", cudaGetErrorString(e));
+  }
+  if (plan->map_for != g) {
+    // uint8 elements: dim 0 in bytes, the other dims as lowered (byte strides)
+    uint64_t dims[5], strides[4];
+    uint32_t box[5];
+    const axe_tma_desc &d = plan->desc;
+    for (int i = 0; i < 5; i++) {
+      dims[i] = i < d.rank ? d.dims[i] : 1;
+      box[i] = i < d.rank ? d.box[i] : 1;
+    }
+    dims[0] *= (uint64_t)plan->es;
+    box[0] *= (uint32_t)plan->es;
+    if (plan->fuse > 1) box[plan->fuse_dim] = (uint32_t)plan->fuse;
+    uint64_t last = 16;  // unused trailing dims: extent 1, the last real stride
+    for (int i = 1; i < 5; i++) {
+      if (i < d.rank) last = d.strides[i];
+      strides[i - 1] = last;
+    }
+    const int r = encode_tensor_map(plan->map, (void *)g, dims, strides, box, d.swizzle_bytes);
+    if (r != 0) AXE_FAIL(AXE_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", r);
+    plan->map_for = g;
+  }
+  TmaReps one;
+  memset(&one, 0, sizeof(one));
+  one.n = 1;
+  const cudaError_t e = launch_tma_region(plan->map, plan->table, (uint32_t)plan->host.size(), plan->box_bytes,
+                                          (void *)s_image, st, dep, store, reps ? *reps : one);
+  if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "tma region launch: %s", cudaGetErrorString(e));
+  return AXE_OK;
 }
 
 extern "C" {
@@ -183,9 +230,6 @@ axe_status axe_tma_plan_sizes(const axe_tma_plan *plan, int64_t *atoms, int64_t 
   return AXE_OK;
 }
 
-static axe_status tma_plan_run(axe_tma_plan *plan, const void *g_base, const void *s_image, void *stream, int dep,
-                               int store, const TmaReps *reps = nullptr);
-
 axe_status axe_tma_plan_execute(axe_tma_plan *plan, const void *g_base, void *s_image, void *stream) {
   return tma_plan_run(plan, g_base, s_image, stream, 1, 0);  // (outside the copy planner's PDL window)
 }
@@ -193,57 +237,6 @@ axe_status axe_tma_plan_execute(axe_tma_plan *plan, const void *g_base, void *s_
 axe_status axe_tma_plan_execute_store(axe_tma_plan *plan, void *g_base, const void *s_image, void *stream) {
   return tma_plan_run(plan, g_base, s_image, stream, 1, 1);
 }
-
-}  // extern "C"
-
-static axe_status tma_plan_run(axe_tma_plan *plan, const void *g_base, const void *s_image, void *stream, int dep,
-                               int store, const TmaReps *reps) {
-  if (!plan || !g_base || !s_image) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
-  const uint8_t *g = (const uint8_t *)g_base + plan->desc.base_bytes;
-  if ((uintptr_t)g % 16 || (uintptr_t)s_image % 16)
-    AXE_FAIL(AXE_ERR_ALIGNMENT, "region start and image must be 16-byte aligned");
-  cudaStream_t st = (cudaStream_t)stream;
-  std::lock_guard<std::mutex> lk(plan->mu);
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "cudaGetDevice");
-  if (!plan->table || plan->dev != dev) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
-      AXE_FAIL(AXE_ERR_CUDA, "the atom table is not on this device yet: execute once outside graph capture");
-    const cudaError_t e = upload(plan, dev);
-    if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "atom table: %s", cudaGetErrorString(e));
-  }
-  if (plan->map_for != g) {
-    // uint8 elements: dim 0 in bytes, the other dims as lowered (byte strides)
-    uint64_t dims[5], strides[4];
-    uint32_t box[5];
-    const axe_tma_desc &d = plan->desc;
-    for (int i = 0; i < 5; i++) {
-      dims[i] = i < d.rank ? d.dims[i] : 1;
-      box[i] = i < d.rank ? d.box[i] : 1;
-    }
-    dims[0] *= (uint64_t)plan->es;
-    box[0] *= (uint32_t)plan->es;
-    if (plan->fuse > 1) box[plan->fuse_dim] = (uint32_t)plan->fuse;
-    uint64_t last = 16;  // unused trailing dims: extent 1, the last real stride
-    for (int i = 1; i < 5; i++) {
-      if (i < d.rank) last = d.strides[i];
-      strides[i - 1] = last;
-    }
-    const int r = encode_tensor_map(plan->map, (void *)g, dims, strides, box, d.swizzle_bytes);
-    if (r != 0) AXE_FAIL(AXE_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", r);
-    plan->map_for = g;
-  }
-  TmaReps one;
-  memset(&one, 0, sizeof(one));
-  one.n = 1;
-  const cudaError_t e = launch_tma_region(plan->map, plan->table, (uint32_t)plan->host.size(), plan->box_bytes,
-                                          (void *)s_image, st, dep, store, reps ? *reps : one);
-  if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "tma region launch: %s", cudaGetErrorString(e));
-  return AXE_OK;
-}
-
-extern "C" {
 
 void axe_tma_plan_destroy(axe_tma_plan *plan) {
   if (!plan) return;
