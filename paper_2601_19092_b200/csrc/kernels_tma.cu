@@ -395,13 +395,17 @@ cudaError_t launch_tma_region(const void *map128, const TmaAtom *atoms, uint32_t
   CUtensorMap m;
   memcpy(&m, map128, sizeof(m));
   const size_t slot = (box_bytes + 1023) & ~(size_t)1023;
-  const int stages = (int)std::max<size_t>(2, std::min<size_t>(TR_STAGES, 16384 / slot));
+  static const size_t ring = [] {  // bytes of boxes per CTA (AXE_TMA_REGION_STAGE_BYTES, 16 KiB)
+    const char *e = getenv("AXE_TMA_REGION_STAGE_BYTES");
+    return (size_t)((e && *e) ? std::max(1024, atoi(e)) : 16384);
+  }();
+  const int stages = (int)std::max<size_t>(2, std::min<size_t>(TR_STAGES, ring / slot));
   const size_t smem = stages * slot + 1024;
-  // CTAs per SM (AXE_TMA_REGION_PER_SM, default 16; capped by occupancy): config 2 10.01 us with 16,
-  // 10.04 with 8; 16384^2 180.4 us with 16, 184.3 with 8
+  // CTAs per SM (AXE_TMA_REGION_PER_SM, default 8; capped by occupancy): config 2 at 16384^2 169.5 us
+  // with 8 against 183-184 with 12 or 16; at 4096^2 10.03 us against 9.99
   static const int per_sm = [] {
     const char *e = getenv("AXE_TMA_REGION_PER_SM");
-    return (e && *e) ? std::max(1, atoi(e)) : 16;
+    return (e && *e) ? std::max(1, atoi(e)) : 8;
   }();
   const unsigned blocks = one_wave(kern, 32, smem, (unsigned)std::min<int64_t>(n, (int64_t)num_sms() * per_sm));
   cudaError_t e = store ? launch_ex(k_tma_region<true>, dim3(blocks), dim3(32), smem, st, m, atoms, n, box_bytes,
