@@ -295,3 +295,20 @@ def test_tma_bulk_and_k3_tma_plans():
     sw = dict(es=2, src=layout([(1 << 16, 1)]), src_st=linear_storage(1 << 16, synth.SW128),
               dst=layout([(1 << 16, 1)]), dst_st=linear_storage(1 << 16))
     assert plan(sw).describe().get("mode") != "bulk-load/bulk-store"
+
+
+def test_lowered_schedule_plans():
+    """AXE_KERNEL_LOWERED (the paper's TMA lowering as the copy schedule) on the host: config 2 both ways,
+    fused 64-row boxes; refusals name the reason (no TMA swizzle on either side, both sides swizzled)."""
+    f = plan(synth.config2(512), "lowered").describe()
+    assert f["mode"] == "tensor-load/bulk-store" and f["atoms"] == 512 and f["boxes"] == 64 and f["box_bytes"] == 8192
+    r = plan(synth.config2(512, reverse=True), "lowered").describe()
+    assert r["mode"] == "bulk-load/tensor-store" and r["boxes"] == 64
+    plain = synth.config2(512, 64, 2, (0, 0, 0))
+    with pytest.raises(axe.AxeError) as e:
+        plan(plain, "lowered")
+    assert e.value.name == "AXE_ERR_UNSUPPORTED" and "TMA swizzle" in str(e.value)
+    both = dict(synth.config2(512), src_st=linear_storage(512 * 512, synth.SW128))
+    with pytest.raises(axe.AxeError) as e:
+        plan(both, "lowered")
+    assert "both sides swizzled" in str(e.value)
