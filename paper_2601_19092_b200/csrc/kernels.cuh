@@ -269,6 +269,7 @@ struct K4Params {
   uint32_t box_bytes;                  // bulk form: output bytes per box (total counts boxes)
   int stages;                          // bulk form: ring stages (2..4), K boxes each
   int threads;                         // bulk form: CTA size (128 or 256)
+  int stcs;                            // vector form: streaming (evict-first) stores of the sums
   int dep;
 };
 // one-sided (pull) form: summand k is read through its own base pointer (a peer's buffer)

@@ -170,7 +170,18 @@ __device__ __forceinline__ void k4_body(const K4Params &p, const uint64_t *kp, c
 #pragma unroll
     for (int v = 0; v < V; v++) o[v] = O::out(acc[v]);
     const R out = *reinterpret_cast<const R *>(o);
-    for (int r = 0; r < p.nrep; r++) *reinterpret_cast<R *>(dst + swz(p.dsw, dof + p.rep[r])) = out;
+    for (int r = 0; r < p.nrep; r++) {
+      uint8_t *q = dst + swz(p.dsw, dof + p.rep[r]);
+      if constexpr (VB == 16) {
+        if (p.stcs) {
+          asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(q), "r"(out.x), "r"(out.y), "r"(out.z),
+                       "r"(out.w)
+                       : "memory");
+          continue;
+        }
+      }
+      *reinterpret_cast<R *>(q) = out;
+    }
   }
 }
 

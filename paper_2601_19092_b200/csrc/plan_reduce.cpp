@@ -155,7 +155,9 @@ axe_status plan_reduce(const Layout &S, const Storage &sst, const Layout &D, con
       if (last.e / V > 1) Y.push_back(Joint{last.e / V, V, V});
     }
     if (box) Y = Yb;  // the bulk form indexes boxes instead of vectors
-    // destination-contiguous output digits first (every warp writes whole lines)
+    // destination-contiguous output digits first (every warp writes whole lines). Ordering by the
+    // summand strides instead (every warp reads whole source runs) measured the same on a B200:
+    // K = 8 bf16 into SW128 tiles 99.3-99.6 us either way, row-major rows 96.4-96.6
     std::stable_sort(Y.begin(), Y.end(), [](const Joint &a, const Joint &b) { return std::llabs(a.ds) > std::llabs(b.ds); });
     sort_fuse_outer(Y);
     int64_t total = 1;
@@ -208,7 +210,11 @@ axe_status plan_reduce(const Layout &S, const Storage &sst, const Layout &D, con
         const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(16, (220 * 1024) / smem));
         P.blocks = (unsigned)std::max<int64_t>(1, std::min(total, (int64_t)num_sms() * per_sm));
       } else {
-        const int64_t blocks = (total + 255) / 256, cap = (int64_t)num_sms() * 8;
+        // streaming (st.global.cs) stores for 4- and 8-byte elements, measured on a B200 (perf_configs
+        // --reduce, 2 runs each): f32 K = 8 (8192 x 2048) 88.4 us vs 94.9 plain; bf16 K = 8 96.9-97.1
+        // vs 96.2 and into SW128 tiles 99.7-100.0 vs 99.7, so 2-byte elements keep plain stores
+        k.stcs = (int)env_int_r("AXE_K4_STCS", es >= 4 ? 1 : 0);
+        const int64_t blocks = (total + 255) / 256, cap = (int64_t)num_sms() * 8;  // 4 per SM: 5-19% slower
         P.blocks = (unsigned)std::max<int64_t>(1, std::min(blocks, cap));
       }
       char b[256];
