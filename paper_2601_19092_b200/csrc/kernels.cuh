@@ -241,6 +241,7 @@ struct K7Params {
   int64_t src_row, dst_col;            // bytes between source rows / destination columns
   int cw;                              // chunk columns per warp (tile columns = 8 n cw)
   int async;                           // 1: cp.async into a second tile buffer while the first is stored
+  int stcs;                            // streaming (evict-first) stores
   int nrep;
   int64_t rep[K1_MAXREP];
   int dep;

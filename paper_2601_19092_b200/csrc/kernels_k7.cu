@@ -67,7 +67,14 @@ __device__ __forceinline__ void k7_gather(const K7Params &p, const uint8_t *sm, 
         o = k == 0 ? make_uint4(w[0].x, w[0].y, w[1].x, w[1].y) : make_uint4(w[0].z, w[0].w, w[1].z, w[1].w);
       }
       const int64_t d = d0 + (int64_t)k * p.dst_col;
-      for (int r = 0; r < p.nrep; r++) *reinterpret_cast<uint4 *>(dst + d + p.rep[r]) = o;
+      for (int r = 0; r < p.nrep; r++) {
+        uint8_t *q = dst + d + p.rep[r];
+        if (p.stcs)
+          asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(q), "r"(o.x), "r"(o.y), "r"(o.z), "r"(o.w)
+                       : "memory");
+        else
+          *reinterpret_cast<uint4 *>(q) = o;
+      }
     }
   }
 }

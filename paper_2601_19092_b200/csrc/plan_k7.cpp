@@ -99,6 +99,10 @@ bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   k.dst_col = A.ds * es;
   k.cw = (int)cw;
   k.async = async;
+  {  // opt-in streaming stores: no gain on a B200 (fp32 8192^2 93.9-94.1 us vs 93.3; fp64 93.7-94.0 vs 93.2)
+    const char *se = getenv("AXE_K7_STCS");
+    k.stcs = (se && *se) ? (atoi(se) != 0) : 0;
+  }
   k.nrep = (int)reps.size();
   for (size_t i = 0; i < reps.size(); i++) k.rep[i] = reps[i] * es;
   P->align = 16;
