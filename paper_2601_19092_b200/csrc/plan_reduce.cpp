@@ -217,12 +217,13 @@ axe_status plan_reduce(const Layout &S, const Storage &sst, const Layout &D, con
         const int64_t blocks = (total + 255) / 256, cap = (int64_t)num_sms() * 8;  // 4 per SM: 5-19% slower
         P.blocks = (unsigned)std::max<int64_t>(1, std::min(blocks, cap));
       }
-      char b[256];
+      char b[320];
       snprintf(b, sizeof b,
                "{\"kernel\":\"reduce\",\"mode\":\"%s\",\"dtype\":\"%s\",\"K\":%lld,\"vec_bytes\":%d,\"%s\":%lld,"
-               "\"replicas\":%d,\"blocks\":%u,\"table\":%d,\"box_bytes\":%lld,\"stages\":%d,\"threads\":%d,\"digits\":",
+               "\"replicas\":%d,\"blocks\":%u,\"table\":%d,\"box_bytes\":%lld,\"stages\":%d,\"threads\":%d,"
+               "\"streaming_stores\":%d,\"digits\":",
                box ? "bulk" : "vector", dtype_name(dtype), (long long)P.K, P.vb, box ? "boxes" : "vectors",
-               (long long)total, k.nrep, P.blocks, k.nk > 0, (long long)box, k.stages, k.threads);
+               (long long)total, k.nrep, P.blocks, k.nk > 0, (long long)box, k.stages, k.threads, k.stcs);
       P.desc = std::string(b) + joint_json(Y) + ",\"reduce_digits\":" + joint_json(Kd) + "}";
       *out = std::move(P);
       return AXE_OK;

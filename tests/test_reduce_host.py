@@ -24,6 +24,10 @@ def test_local_plan_structure():
                        "bf16").describe()
     assert d["kernel"] == "reduce" and d["K"] == 8 and d["vec_bytes"] == 16 and d["table"]
     assert d["reduce_digits"] == [[8, 8192, 0]]          # k stride = one (64 x 128) slab, no destination stride
+    assert d["streaming_stores"] == 0                     # 2-byte sums keep plain stores (measured)
+    f = synth.reduce_local(8, 64, 64, "f32")
+    d = axe.ReducePlan(f["src"], f["src_st"], f["dst"], f["dst_st"], "f32").describe()
+    assert d["streaming_stores"] == 1                     # 4-byte sums: st.global.cs (measured 88.4 vs 94.9 us)
     big = synth.reduce_local(300, 4, 32, "f32")
     d = axe.ReducePlan(big["src"], big["src_st"], big["dst"], big["dst_st"], "f32").describe()
     assert d["K"] == 300 and not d["table"]             # decoded summand offsets beyond 256
