@@ -387,9 +387,9 @@ def run_axe(args):
     plan = axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], es)
     desc = plan.describe()
     l2 = torch.cuda.get_device_properties(local).L2_cache_size
-    # independent buffer pairs: > 4x L2 of footprint, and enough of them (32) that the copy of pair i
-    # and the next reuse of pair i lie 32 steps apart -- the library lets independent copies overlap
-    # (PDL) and makes a copy wait only for in-flight copies touching its bytes
+    # buffer pairs: > 4x L2 of footprint (32 pairs, 2 GiB), so no step finds its source in L2.  Every
+    # kernel waits for its predecessor (griddepcontrol.wait) by default; AXE_PDL_OVERLAP=1 lets copies
+    # proven disjoint from the in-flight ones skip it (opt-in, reported in roofline.pdl_overlap)
     pairs = max(int(os.environ.get("AXE_BENCH_PAIRS", "32")), -(-4 * l2 // (2 * nbytes)))
     g = torch.Generator(device="cuda").manual_seed(cfg["seed"] + rank)
     srcs = [torch.randint(-2**31, 2**31 - 1, (nbytes // 4,), dtype=torch.int32, device="cuda", generator=g)
@@ -404,9 +404,10 @@ def run_axe(args):
         step(i)
     torch.cuda.synchronize()
 
-    # The launch-bound inner loop is captured once in a CUDA graph (G steps, one kernel each) and
-    # replayed; steps beyond a multiple of G are launched directly.
-    G = pairs * 8
+    # The timed region is exactly args.steps launches, captured once in a CUDA graph (one kernel per
+    # step, each on the next buffer pair) and replayed once: the device time of those launches, not
+    # the host's ctypes / launch path.  A short sleep kernel ahead of the start event keeps the
+    # stream busy while the host submits the graph, so the region starts with the first copy.
     graph = None
     if not args.no_graph:
         n_cap = axe.kernel_launch_count()
@@ -414,22 +415,19 @@ def run_axe(args):
         cap_stream = torch.cuda.Stream()
         cap_stream.wait_stream(stream)
         with torch.cuda.graph(graph, stream=cap_stream):
-            for j in range(G):
+            for j in range(args.steps):
                 step(j, torch.cuda.current_stream())
-        assert axe.kernel_launch_count() - n_cap == G, "one kernel per step"
+        assert axe.kernel_launch_count() - n_cap == args.steps, "one kernel per step"
         torch.cuda.synchronize()
 
-    def run_steps(k):
-        """k steps on `stream`; returns the number of library kernels launched."""
+    def run_steps():
+        """args.steps steps on `stream`; returns the number of library kernels launched."""
         if graph is None:
-            for i in range(k):
+            for i in range(args.steps):
                 step(i)
-            return k
-        for _ in range(k // G):
+        else:
             graph.replay()
-        for i in range(k % G):
-            step(i)
-        return k
+        return args.steps
 
     def barrier():
         if dist:
@@ -440,18 +438,34 @@ def run_axe(args):
         # keep the GPU loaded long enough for the clock sampler to see the timed region's clocks
         t_end = time.perf_counter() + 0.4
         while time.perf_counter() < t_end:
-            run_steps(max(G, 512))
+            for _ in range(max(1, 512 // args.steps)):
+                run_steps()
             torch.cuda.synchronize()
         barrier()
         n0 = axe.kernel_launch_count()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(2_000_000)  # ~1 ms of GPU time: the graph is queued before the region starts
         ev0.record(stream)
-        launches = run_steps(args.steps)
+        launches = run_steps()
         ev1.record(stream)
         barrier()
         direct = axe.kernel_launch_count() - n0
-        assert direct == (args.steps % G if graph is not None else args.steps)
+        assert direct == (0 if graph is not None else args.steps)
         ms = ev0.elapsed_time(ev1)
+        # the same steps launched one by one from Python (ctypes + launch path on the host each step)
+        torch.cuda._sleep(2_000_000)
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        d1.record(stream)
+        torch.cuda.synchronize()
+        direct_ms = d0.elapsed_time(d1) / args.steps
+        t0 = time.perf_counter()
+        for i in range(200):
+            step(i)
+        host_us = (time.perf_counter() - t0) / 200 * 1e6
+        torch.cuda.synchronize()
         # isolated launches bracketed by events (same stream), for reference
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(100)]
         for j, (a, b) in enumerate(evs):
@@ -551,8 +565,10 @@ def run_axe(args):
             "pct_of_peak": 100.0 * (value / ws) / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": ncu_traffic(), "peak_source": peak_src,
-                         "kernel_ms": k_ms, "isolated_launch_ms": iso_ms, "alg_bytes_per_launch": alg_bytes,
-                         "timing": "CUDA events over the timed region / launches (graph replay)"
+                         "kernel_ms": k_ms, "isolated_launch_ms": iso_ms, "direct_launch_ms": direct_ms,
+                         "host_us_per_call": host_us, "alg_bytes_per_launch": alg_bytes,
+                         "pdl_overlap": os.environ.get("AXE_PDL_OVERLAP", "0") == "1",
+                         "timing": f"CUDA events around one replay of a graph of exactly {args.steps} launches"
                          if graph is not None else "CUDA events over the timed region / launches"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
@@ -576,8 +592,8 @@ def run_axe(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
-    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="axe", choices=["axe", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -107,6 +107,32 @@ struct TmaReps {
   int n;
   int64_t r[K1_MAXREP];
 };
+// The box table of a lowered region as a mixed-radix program (tma_region.cpp fit_program): box b has
+// digits d_k (innermost first, extents fd[k].d) and coordinates c0 + sum_k d_k dc[k], image offset
+// off0 + sum_k d_k doff[k].  The tiler T and the row-major atom grid of the lowering are both
+// mixed-radix, so every box table the planner builds so far has this form; nd = -1 (a table the fit
+// does not reproduce exactly) reads the table from global memory instead.
+constexpr int TR_MAXD = 10;
+struct TrProg {
+  int nd;
+  FastDiv fd[TR_MAXD];
+  int32_t c0[5];
+  int32_t dc[TR_MAXD][5];
+  int64_t off0;
+  int64_t doff[TR_MAXD];
+};
+struct TrParams {
+  TrProg prog;
+  const TmaAtom *atoms;  // the table (prog.nd < 0 only)
+  uint8_t *img;
+  uint32_t n;            // boxes
+  uint32_t box;          // bytes per box
+  uint32_t slot;         // ring slot stride (box rounded up to 1 KiB: every slot starts a swizzle pattern)
+  uint32_t stages;       // ring slots per CTA
+  int dep;               // 1: griddepcontrol.wait before the first TMA
+  int strided;           // 1: CTA c takes boxes c, c + grid, ... (0: a contiguous range per CTA)
+  TmaReps reps;
+};
 
 struct TmaParams {
   uint32_t nboxes;

@@ -291,57 +291,100 @@ cudaError_t launch_k2t(const void *map128, const K2TParams &p, int es, unsigned 
   return cudaGetLastError();
 }
 
-// The lowered TMA region (tma_region.cpp): one elected thread per CTA streams boxes through a
-// ring of 1 KiB-aligned slots.  Load direction (G -> image): tensor load (the hardware applies the
-// atom's swizzle), then one bulk store of the slot into the image at the tiler's offset.  Store
-// direction (image -> G): bulk load of the slot from the image, then one tensor store (the hardware
-// un-swizzles).  Both copies of a box run in the async proxy, so no proxy fence is needed.
-constexpr int TR_STAGES = 8;  // ring capacity; the launch picks 2..8 stages (16 KiB of boxes per CTA)
+// The lowered TMA region (tma_region.cpp): a persistent grid (one CTA of one issuing thread per SM by
+// default), each CTA owning a contiguous range of boxes and a deep ring of 1 KiB-aligned slots that
+// fills its shared memory (config 2: 28 slots of 8 KiB -- the SM's whole share of the 4096 boxes is
+// in flight at once, so the first wave of loads covers the copy and no CTA waits on a ring refill).
+// Load direction (G -> image): tensor load (the hardware applies the atom's swizzle), then one bulk
+// store of the slot into the image at the tiler's offset.  Store direction (image -> G): bulk load
+// of the slot from the image, then one tensor store (the hardware un-swizzles).  Both copies of a
+// box run in the async proxy, so no proxy fence is needed.  Box coordinates come from the fitted
+// mixed-radix program (no dependent global load before a TMA issue); the table is the fallback.
+constexpr int TR_STAGES = 32;  // ring capacity (slots per CTA)
+constexpr int TR_LAG = 2;      // a slot is refilled once the store two boxes back has read it
+
+__device__ __forceinline__ void tr_box(const TrParams &p, uint32_t b, int c[5], int64_t &off) {
+  if (p.prog.nd < 0) {
+    const TmaAtom a = p.atoms[b];
+#pragma unroll
+    for (int i = 0; i < 5; i++) c[i] = a.c[i];
+    off = a.off;
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 5; i++) c[i] = p.prog.c0[i];
+  off = p.prog.off0;
+#pragma unroll
+  for (int k = 0; k < TR_MAXD; k++) {
+    if (k >= p.prog.nd) break;
+    const uint32_t q = fdiv(p.prog.fd[k], b);
+    const uint32_t d = b - q * p.prog.fd[k].d;
+    b = q;
+#pragma unroll
+    for (int i = 0; i < 5; i++) c[i] += (int)d * p.prog.dc[k][i];
+    off += (int64_t)d * p.prog.doff[k];
+  }
+}
+
 template <bool STORE>
-__global__ void __launch_bounds__(32) k_tma_region(const __grid_constant__ CUtensorMap map,
-                                                   const TmaAtom *__restrict__ atoms, uint32_t n, uint32_t box,
-                                                   int stages, int dep, uint8_t *__restrict__ img,
-                                                   const __grid_constant__ TmaReps reps) {
+__global__ void __launch_bounds__(32, 1) k_tma_region(const __grid_constant__ CUtensorMap map,
+                                                      const __grid_constant__ TrParams p) {
   extern __shared__ __align__(1024) uint8_t raw[];
   __shared__ __align__(8) uint64_t full[TR_STAGES];
+  if (threadIdx.x != 0) {
+    pdl_launch_dependents();
+    return;
+  }
   uint8_t *sm = (uint8_t *)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t slot = (box + 1023) & ~1023u;
-  const uint32_t S = (uint32_t)stages;
-  if (dep) pdl_wait();
-  pdl_launch_dependents();
-  if (threadIdx.x != 0) return;
+  const uint32_t S = p.stages, slot = p.slot, box = p.box;
+  // boxes of this CTA: box(k) = lo + k * bstep
+  uint32_t lo, mine, bstep;
+  if (p.strided) {
+    lo = blockIdx.x;
+    bstep = gridDim.x;
+    mine = lo < p.n ? (p.n - lo + bstep - 1) / bstep : 0;
+  } else {
+    lo = (uint32_t)((uint64_t)p.n * blockIdx.x / gridDim.x);
+    mine = (uint32_t)((uint64_t)p.n * (blockIdx.x + 1) / gridDim.x) - lo;
+    bstep = 1;
+  }
   for (uint32_t s = 0; s < S; s++) mbar_init(&full[s], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  const uint32_t first = blockIdx.x, step = gridDim.x;
-  const uint32_t mine = first < n ? (n - first + step - 1) / step : 0;
+  asm volatile("prefetch.tensormap [%0];" ::"l"(&map) : "memory");
+  if (p.dep) pdl_wait();
+  pdl_launch_dependents();
   auto issue = [&](uint32_t k) {
     const uint32_t s = k % S;
-    const TmaAtom a = atoms[first + k * step];
+    int c[5];
+    int64_t off;
+    tr_box(p, lo + k * bstep, c, off);
     mbar_expect_tx(&full[s], box);
     if constexpr (STORE)
-      bulk_load(sm + (size_t)s * slot, img + a.off, box, &full[s]);
+      bulk_load(sm + (size_t)s * slot, p.img + off, box, &full[s]);
     else
-      tma_load5(sm + (size_t)s * slot, &map, &full[s], a.c[0], a.c[1], a.c[2], a.c[3], a.c[4]);
+      tma_load5(sm + (size_t)s * slot, &map, &full[s], c[0], c[1], c[2], c[3], c[4]);
   };
   for (uint32_t k = 0; k < mine && k < S; k++) issue(k);
   for (uint32_t k = 0; k < mine; k++) {
     const uint32_t s = k % S;
+    int c[5];
+    int64_t off;
+    tr_box(p, lo + k * bstep, c, off);
     mbar_wait(&full[s], (k / S) & 1u);
     if constexpr (STORE) {
-      const TmaAtom a = atoms[first + k * step];
-      tma_store5(&map, sm + (size_t)s * slot, a.c[0], a.c[1], a.c[2], a.c[3], a.c[4]);
+      tma_store5(&map, sm + (size_t)s * slot, c[0], c[1], c[2], c[3], c[4]);
     } else {
-      const int64_t off = atoms[first + k * step].off;
-      for (int r = 0; r < reps.n; r++) bulk_store(img + off + reps.r[r], sm + (size_t)s * slot, box);
+      for (int r = 0; r < p.reps.n; r++) bulk_store(p.img + off + p.reps.r[r], sm + (size_t)s * slot, box);
     }
     bulk_commit();
-    // refill the slot of the previous store (one store may still be reading: its own slot)
-    if (k >= 1 && k - 1 + S < mine) {
-      bulk_wait_read<1>();
-      issue(k - 1 + S);
+    // refill the slot of box k - TR_LAG once its store has read shared memory
+    if (k >= (uint32_t)TR_LAG && k - TR_LAG + S < mine) {
+      bulk_wait_read<TR_LAG>();
+      issue(k - TR_LAG + S);
     }
   }
-  bulk_wait_all();
+  // shared memory must outlive the stores' reads; their global writes complete with the grid
+  bulk_wait_read<0>();
 }
 
 // ------------------------------------------------------------------ host side
@@ -386,32 +429,61 @@ int encode_tensor_map(void *out128, void *gaddr, const uint64_t dims[5], const u
   return (int)r;
 }
 
-cudaError_t launch_tma_region(const void *map128, const TmaAtom *atoms, uint32_t n, uint32_t box_bytes, void *img,
-                              cudaStream_t st, int dep, int store, const TmaReps &reps) {
-  if (n == 0) return cudaSuccess;
+// CTAs per SM of the lowered schedule (AXE_TMA_REGION_PER_SM, default 2: two rings filling the SM)
+int tma_region_per_sm() {
+  static const int v = [] {
+    const char *e = getenv("AXE_TMA_REGION_PER_SM");
+    return (e && *e) ? std::max(1, std::min(8, atoi(e))) : 2;
+  }();
+  return v;
+}
+
+cudaError_t launch_tma_region(const void *map128, TrParams p, int store, cudaStream_t st) {
+  if (p.n == 0) return cudaSuccess;
   const void *kern = store ? (const void *)k_tma_region<true> : (const void *)k_tma_region<false>;
-  const cudaError_t attr_err = smem_attr(kern, 200 * 1024);
+  static int optin = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v;
+  }();
+  static int per_sm_bytes = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    return v;
+  }();
+  const int per_sm = tma_region_per_sm();
+  // ring: the CTA's share of the SM's shared memory (1 KiB per CTA is reserved by the system, the
+  // static barriers and the 1 KiB alignment pad come off the top), at most TR_STAGES slots
+  static const int static_bytes = [] {  // the barriers (+ alignment) of the kernel's static shared memory
+    cudaFuncAttributes a0{}, a1{};
+    cudaFuncGetAttributes(&a0, (const void *)k_tma_region<false>);
+    cudaFuncGetAttributes(&a1, (const void *)k_tma_region<true>);
+    return (int)std::max(a0.sharedSizeBytes, a1.sharedSizeBytes);
+  }();
+  const int max_dyn = std::min(optin, per_sm_bytes / per_sm - 1024) - static_bytes;
+  const size_t budget = (size_t)max_dyn - 1024;
+  static const size_t ring_cap = [] {  // AXE_TMA_REGION_STAGE_BYTES: cap the ring (A/B only)
+    const char *e = getenv("AXE_TMA_REGION_STAGE_BYTES");
+    return (size_t)((e && *e) ? std::max(1024, atoi(e)) : (1 << 30));
+  }();
+  const size_t ring = std::min(budget, ring_cap);
+  p.stages = (uint32_t)std::max<size_t>(1, std::min<size_t>(TR_STAGES, ring / p.slot));
+  if (p.stages < 2 && ring < p.slot) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)p.stages * p.slot + 1024;
+  const cudaError_t attr_err = smem_attr(kern, max_dyn);
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap m;
   memcpy(&m, map128, sizeof(m));
-  const size_t slot = (box_bytes + 1023) & ~(size_t)1023;
-  static const size_t ring = [] {  // bytes of boxes per CTA (AXE_TMA_REGION_STAGE_BYTES, 16 KiB)
-    const char *e = getenv("AXE_TMA_REGION_STAGE_BYTES");
-    return (size_t)((e && *e) ? std::max(1024, atoi(e)) : 16384);
+  const unsigned blocks = (unsigned)std::min<int64_t>(p.n, (int64_t)num_sms() * per_sm);
+  static const int strided = [] {  // AXE_TMA_REGION_STRIDED: box order per CTA (A/B)
+    const char *e = getenv("AXE_TMA_REGION_STRIDED");
+    return (e && *e) ? atoi(e) : 1;
   }();
-  const int stages = (int)std::max<size_t>(2, std::min<size_t>(TR_STAGES, ring / slot));
-  const size_t smem = stages * slot + 1024;
-  // CTAs per SM (AXE_TMA_REGION_PER_SM, default 8; capped by occupancy): config 2 at 16384^2 169.5 us
-  // with 8 against 183-184 with 12 or 16; at 4096^2 10.03 us against 9.99
-  static const int per_sm = [] {
-    const char *e = getenv("AXE_TMA_REGION_PER_SM");
-    return (e && *e) ? std::max(1, atoi(e)) : 8;
-  }();
-  const unsigned blocks = one_wave(kern, 32, smem, (unsigned)std::min<int64_t>(n, (int64_t)num_sms() * per_sm));
-  cudaError_t e = store ? launch_ex(k_tma_region<true>, dim3(blocks), dim3(32), smem, st, m, atoms, n, box_bytes,
-                                    stages, dep, (uint8_t *)img, reps)
-                        : launch_ex(k_tma_region<false>, dim3(blocks), dim3(32), smem, st, m, atoms, n, box_bytes,
-                                    stages, dep, (uint8_t *)img, reps);
+  p.strided = strided;
+  cudaError_t e = store ? launch_ex(k_tma_region<true>, dim3(blocks), dim3(32), smem, st, m, p)
+                        : launch_ex(k_tma_region<false>, dim3(blocks), dim3(32), smem, st, m, p);
   if (e != cudaSuccess) return e;
   g_launches++;
   return cudaGetLastError();

@@ -7,6 +7,8 @@
 #include <cstring>
 #include <numeric>
 #include <set>
+#include <mutex>
+#include <thread>
 #include <unordered_map>
 
 namespace axe {
@@ -282,8 +284,8 @@ static bool build_k1(const std::vector<Joint> &J0, const Linear &ls, const Linea
   if (D.empty()) D.push_back(Joint{1, 0, 0});
   int64_t total = 1;
   for (auto &j : D) total *= j.e;
-  if (total >= (int64_t(1) << 32)) {
-    *why = "more than 2^32 vectors";
+  if (total >= (int64_t(1) << 31)) {  // 32-bit grid-stride index: base + step must not wrap
+    *why = "2^31 or more vectors";
     return false;
   }
   K1Params &k = P->k1;
@@ -658,7 +660,7 @@ static bool build_bulk(const std::vector<Joint> &J0, const Linear &ls, const Lin
   if ((int)D.size() > TMA_MAXD) return fail("bulk: too many box digits");
   int64_t nboxes = 1;
   for (auto &j : D) nboxes *= j.e;
-  if (nboxes >= (int64_t(1) << 32)) return fail("bulk: too many boxes");
+  if (nboxes >= (int64_t(1) << 31)) return fail("bulk: too many boxes");
   auto a16 = [&](int64_t v) { return (v * es) % 16 == 0; };
   if (!a16(ls.base) || !a16(ld.base)) return fail("bulk: bases not 16-byte aligned");
   for (auto &j : D)
@@ -1011,25 +1013,55 @@ namespace {
 struct Ranges {
   uintptr_t s0, s1, d0, d1;
 };
+// A window belongs to one stream of one device: the handles 0 (legacy default stream) and
+// cudaStreamPerThread name a different stream on every device, and the per-thread stream a different
+// one on every host thread.
+struct WinKey {
+  cudaStream_t st;
+  int dev;
+  uint64_t tid;
+  bool operator==(const WinKey &o) const { return st == o.st && dev == o.dev && tid == o.tid; }
+};
+struct WinKeyHash {
+  size_t operator()(const WinKey &k) const {
+    return std::hash<uintptr_t>()((uintptr_t)k.st) ^ (std::hash<uint64_t>()(k.tid) * 31) ^ ((size_t)k.dev << 20);
+  }
+};
 std::mutex g_dep_mu;
-std::unordered_map<cudaStream_t, std::vector<Ranges>> g_win;
+std::unordered_map<WinKey, std::vector<Ranges>, WinKeyHash> g_win;
+
+WinKey win_key(cudaStream_t st) {
+  WinKey k{st, 0, 0};
+  cudaGetDevice(&k.dev);
+  if (st == cudaStreamPerThread) k.tid = (uint64_t)std::hash<std::thread::id>()(std::this_thread::get_id());
+  return k;
+}
 }  // namespace
 
-int stream_dependency(cudaStream_t st, uintptr_t s0, uintptr_t s1, uintptr_t d0, uintptr_t d1) {
-  static const int overlap_ok = [] {
+// Skipping griddepcontrol.wait across calls is opt-in (AXE_PDL_OVERLAP=1): the window sees only libaxe
+// kernels, and a foreign kernel on the stream that triggers its dependents early (several libraries
+// do) would be invisible to it.  By default every kernel waits (dep = 1): PDL then only overlaps the
+// next kernel's launch and prologue with the previous kernel's tail.
+bool pdl_overlap_enabled() {
+  static const int on = [] {
     const char *e = getenv("AXE_PDL_OVERLAP");
-    return (e && *e == '0') ? 0 : 1;
+    return (e && *e == '1') ? 1 : 0;
   }();
+  return on != 0;
+}
+
+int stream_dependency(cudaStream_t st, uintptr_t s0, uintptr_t s1, uintptr_t d0, uintptr_t d1) {
+  if (!pdl_overlap_enabled()) return 1;
   // only kernels moving <= 256 MiB overlap their predecessors: for them ramp-up and tail are a
-  // visible share of the run (64 MiB config 2: 10.1 us overlapped vs ~10.9 us serialised), while two
-  // interleaved full-GPU 1 GiB copies contend (191 us vs 175 us serialised)
+  // visible share of the run, while two interleaved full-GPU 1 GiB copies contend (191 us vs 175 us
+  // serialised)
   static const uintptr_t max_bytes = (uintptr_t)env_int("AXE_PDL_MAX_OVERLAP_BYTES", int64_t(256) << 20);
   auto hit = [](uintptr_t a0, uintptr_t a1, uintptr_t b0, uintptr_t b1) { return a0 < b1 && b0 < a1; };
+  const WinKey key = win_key(st);
   std::lock_guard<std::mutex> lk(g_dep_mu);
   int dep = 1;
-  auto it = g_win.find(st);
-  if (overlap_ok && (s1 - s0) + (d1 - d0) <= max_bytes && it != g_win.end() && !it->second.empty() &&
-      it->second.size() < 64) {
+  auto it = g_win.find(key);
+  if ((s1 - s0) + (d1 - d0) <= max_bytes && it != g_win.end() && !it->second.empty() && it->second.size() < 64) {
     dep = 0;
     for (const Ranges &L : it->second)
       if (hit(d0, d1, L.d0, L.d1) || hit(d0, d1, L.s0, L.s1) || hit(s0, s1, L.d0, L.d1)) {
@@ -1038,7 +1070,7 @@ int stream_dependency(cudaStream_t st, uintptr_t s0, uintptr_t s1, uintptr_t d0,
       }
   }
   if (g_win.size() > 256) g_win.clear();
-  std::vector<Ranges> &w = g_win[st];
+  std::vector<Ranges> &w = g_win[key];
   if (dep) w.clear();  // waiting: every earlier kernel is complete when this one proceeds
   w.push_back(Ranges{s0, s1, d0, d1});
   return dep;
@@ -1065,8 +1097,10 @@ static axe_status tensor_map_for(const CopyPlan &p, const void *tptr, std::array
 // Work the library does not launch itself (NCCL, memcpy) was enqueued on st:
 // the next libaxe kernel there must wait (full dependency).
 void stream_forget(cudaStream_t st) {
+  if (!pdl_overlap_enabled()) return;
+  const WinKey key = win_key(st);
   std::lock_guard<std::mutex> lk(g_dep_mu);
-  g_win.erase(st);
+  g_win.erase(key);
 }
 
 axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t st) {

@@ -79,7 +79,7 @@ bool build_k3(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
   if ((int)out.size() > K1_MAXD) return fail("register: too many block digits");
   int64_t nb = 1;
   for (auto &o : out) nb *= o.e;
-  if (nb >= (int64_t(1) << 32)) return fail("register: too many blocks");
+  if (nb >= (int64_t(1) << 31)) return fail("register: too many blocks");
   K3Params &k = P->k3;
   memset(&k, 0, sizeof(k));
   sort_fuse_outer(out);

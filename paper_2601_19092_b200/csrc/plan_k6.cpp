@@ -100,7 +100,7 @@ bool build_k6(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   sort_fuse_outer(grp);
   int64_t ng = 1;
   for (auto &g : grp) ng *= g.e;
-  if (ng >= (int64_t(1) << 32)) return fail("shuffle: too many groups");
+  if (ng >= (int64_t(1) << 31)) return fail("shuffle: too many groups");
   // tiles of (256 / n) * K6_U groups: the innermost group digits (split where needed, Lemma split)
   const int64_t tile_g = (256 / n) * K6_U;
   if (ng % tile_g) return fail("shuffle: group count is not a whole number of tiles");

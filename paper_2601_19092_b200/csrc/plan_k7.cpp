@@ -70,7 +70,7 @@ bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   if ((int)outer.size() > K1_MAXD) return fail("transpose: too many tile digits");
   int64_t nt = 1;
   for (auto &o : outer) nt *= o.e;
-  if (nt >= (int64_t(1) << 32)) return fail("transpose: too many tiles");
+  if (nt >= (int64_t(1) << 31)) return fail("transpose: too many tiles");
   std::vector<int64_t> reps{0};
   for (auto &r : ld.R) {
     std::vector<int64_t> nx;

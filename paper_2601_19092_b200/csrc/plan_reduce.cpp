@@ -162,7 +162,8 @@ axe_status plan_reduce(const Layout &S, const Storage &sst, const Layout &D, con
     sort_fuse_outer(Y);
     int64_t total = 1;
     for (auto &j : Y) total *= j.e;
-    if ((int)Y.size() > K4_MAXD || total >= (int64_t(1) << 32)) joint = false;
+    // (32-bit grid-stride index in k4_reduce / k4_multimem: i + stride must not wrap)
+    if ((int)Y.size() > K4_MAXD || total >= (int64_t(1) << 31)) joint = false;
     if (joint) {
       K4Params &k = P.k4;
       memset(&k, 0, sizeof(k));

@@ -451,7 +451,7 @@ static void build_pull(const axe_redist_plan &in, int64_t K, int64_t C, const St
   if ((int)Y.size() > K4_MAXD) return no("too many sub-box digits");
   int64_t total = 1;
   for (auto &j : Y) total *= j.e;
-  if (total >= (int64_t(1) << 32)) return no("more than 2^32 vectors per region");
+  if (total >= (int64_t(1) << 31)) return no("2^31 or more vectors per region");
   for (auto &g : groups) {
     std::vector<Ent> v = g.second;
     std::sort(v.begin(), v.end(), [](const Ent &a, const Ent &b) { return a.k < b.k; });

@@ -17,11 +17,15 @@
 
 #include "handles.hpp"
 
+#include <unordered_map>
+#include <map>
+#include <array>
+
 namespace axe {
 int encode_tensor_map(void *out128, void *gaddr, const uint64_t dims[5], const uint64_t strides[4],
                       const uint32_t box[5], int swizzle_bytes);
-cudaError_t launch_tma_region(const void *map128, const TmaAtom *atoms, uint32_t n, uint32_t box_bytes, void *img,
-                              cudaStream_t st, int dep, int store, const TmaReps &reps);
+cudaError_t launch_tma_region(const void *map128, TrParams p, int store, cudaStream_t st);
+void stream_forget(cudaStream_t st);
 }  // namespace axe
 
 using namespace axe;
@@ -38,27 +42,89 @@ struct axe_tma_plan {
   int64_t image_bytes = 0;    // |T| atoms
   std::vector<TmaAtom> host;  // per box: tensor-map coordinates (byte units on dim 0) + image offset
   int fuse = 1, fuse_dim = -1;  // atoms per box along the rows (box[fuse_dim] = fuse)
-  std::mutex mu;
-  int dev = -1;
-  TmaAtom *table = nullptr;  // device copy (uploaded at create, or by an execute on another device)
-  const void *map_for = nullptr;
-  alignas(64) unsigned char map[128];
+  TrProg prog{};              // the table as a mixed-radix program (prog.nd < 0: use the table)
+  std::mutex mu;              // guards the caches below
+  std::map<int, TmaAtom *> tables;  // device -> its copy of the table (prog.nd < 0 only)
+  std::unordered_map<const void *, std::array<unsigned char, 128>> maps;  // region start -> CUtensorMap
 };
 
-// the atom table on device `dev` (synchronous; not allowed inside graph capture)
-static cudaError_t upload(axe_tma_plan *plan, int dev) {
-  if (plan->table) cudaFree(plan->table);
-  plan->table = nullptr;
+// Fit the box table with a mixed-radix program (kernels.cuh TrProg): the innermost digit's step is
+// box 1 - box 0, its extent the longest run of equal steps (a divisor of what is left), and so on
+// outwards; the result must reproduce every box exactly, else the kernel reads the table.
+static TrProg fit_program(const std::vector<TmaAtom> &A) {
+  TrProg p;
+  memset(&p, 0, sizeof(p));
+  p.nd = -1;
+  const int64_t n = (int64_t)A.size();
+  if (n == 0 || n >= (int64_t(1) << 32)) return p;
+  auto vec = [](const TmaAtom &a, int64_t v[6]) {
+    for (int i = 0; i < 5; i++) v[i] = a.c[i];
+    v[5] = a.off;
+  };
+  int64_t a0[6];
+  vec(A[0], a0);
+  int nd = 0;
+  int64_t stride = 1;
+  int64_t delta[TR_MAXD][6], ext[TR_MAXD];
+  while (stride < n) {
+    if (nd == TR_MAXD || n % stride) return p;
+    int64_t d[6], v[6];
+    vec(A[(size_t)stride], v);
+    for (int i = 0; i < 6; i++) d[i] = v[i] - a0[i];
+    int64_t e = 2;
+    while (e * stride < n) {
+      vec(A[(size_t)(e * stride)], v);
+      bool ok = true;
+      for (int i = 0; i < 6; i++) ok = ok && v[i] == a0[i] + e * d[i];
+      if (!ok) break;
+      e++;
+    }
+    const int64_t left = n / stride;
+    while (e > 1 && left % e) e--;
+    if (e < 2) return p;
+    for (int i = 0; i < 6; i++) {
+      if (i < 5 && (d[i] > INT32_MAX || d[i] < INT32_MIN)) return p;
+      delta[nd][i] = d[i];
+    }
+    ext[nd++] = e;
+    stride *= e;
+  }
+  // verify every box
+  for (int64_t b = 0; b < n; b++) {
+    int64_t r = b, v[6], w[6];
+    for (int i = 0; i < 6; i++) w[i] = a0[i];
+    for (int k = 0; k < nd; k++) {
+      const int64_t dk = r % ext[k];
+      r /= ext[k];
+      for (int i = 0; i < 6; i++) w[i] += dk * delta[k][i];
+    }
+    vec(A[(size_t)b], v);
+    for (int i = 0; i < 6; i++)
+      if (v[i] != w[i]) return p;
+  }
+  p.nd = nd;
+  for (int i = 0; i < 5; i++) p.c0[i] = (int32_t)a0[i];
+  p.off0 = a0[5];
+  for (int k = 0; k < nd; k++) {
+    p.fd[k] = make_fastdiv((uint32_t)ext[k]);
+    for (int i = 0; i < 5; i++) p.dc[k][i] = (int32_t)delta[k][i];
+    p.doff[k] = delta[k][5];
+  }
+  return p;
+}
+
+// the atom table on device `dev` (synchronous; not allowed inside graph capture); plan->mu held
+static cudaError_t upload(axe_tma_plan *plan, int dev, TmaAtom **out) {
+  TmaAtom *t = nullptr;
   const size_t bytes = plan->host.size() * sizeof(TmaAtom);
-  cudaError_t e = cudaMalloc(&plan->table, bytes);
-  if (e == cudaSuccess) e = cudaMemcpy(plan->table, plan->host.data(), bytes, cudaMemcpyHostToDevice);
+  cudaError_t e = cudaMalloc(&t, bytes);
+  if (e == cudaSuccess) e = cudaMemcpy(t, plan->host.data(), bytes, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
-    if (plan->table) cudaFree(plan->table);
-    plan->table = nullptr;
+    if (t) cudaFree(t);
     return e;
   }
-  plan->dev = dev;
-  plan->map_for = nullptr;
+  plan->tables[dev] = t;
+  *out = t;
   return cudaSuccess;
 }
 
@@ -69,42 +135,67 @@ static axe_status tma_plan_run(axe_tma_plan *plan, const void *g_base, const voi
   if ((uintptr_t)g % 16 || (uintptr_t)s_image % 16)
     AXE_FAIL(AXE_ERR_ALIGNMENT, "region start and image must be 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;
-  std::lock_guard<std::mutex> lk(plan->mu);
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "cudaGetDevice");
-  if (!plan->table || plan->dev != dev) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
-      AXE_FAIL(AXE_ERR_CUDA, "the atom table is not on this device yet: execute once outside graph capture");
-    const cudaError_t e = upload(plan, dev);
-    if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "atom table: %s", cudaGetErrorString(e));
+  TrParams p;
+  memset(&p, 0, sizeof(p));
+  p.prog = plan->prog;
+  p.img = (uint8_t *)s_image;
+  p.n = (uint32_t)plan->host.size();
+  p.box = plan->box_bytes;
+  p.slot = (plan->box_bytes + 1023) & ~1023u;
+  p.dep = dep;
+  if (reps) {
+    p.reps = *reps;
+  } else {
+    p.reps.n = 1;
   }
-  if (plan->map_for != g) {
-    // uint8 elements: dim 0 in bytes, the other dims as lowered (byte strides)
-    uint64_t dims[5], strides[4];
-    uint32_t box[5];
-    const axe_tma_desc &d = plan->desc;
-    for (int i = 0; i < 5; i++) {
-      dims[i] = i < d.rank ? d.dims[i] : 1;
-      box[i] = i < d.rank ? d.box[i] : 1;
+  std::array<unsigned char, 128> map;
+  {
+    std::lock_guard<std::mutex> lk(plan->mu);
+    if (p.prog.nd < 0) {
+      int dev = 0;
+      if (cudaGetDevice(&dev) != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "cudaGetDevice");
+      auto it = plan->tables.find(dev);
+      if (it != plan->tables.end()) {
+        p.atoms = it->second;
+      } else {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+          AXE_FAIL(AXE_ERR_CUDA, "the atom table is not on this device yet: execute once outside graph capture");
+        TmaAtom *t = nullptr;
+        const cudaError_t e = upload(plan, dev, &t);
+        if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "atom table: %s", cudaGetErrorString(e));
+        p.atoms = t;
+      }
     }
-    dims[0] *= (uint64_t)plan->es;
-    box[0] *= (uint32_t)plan->es;
-    if (plan->fuse > 1) box[plan->fuse_dim] = (uint32_t)plan->fuse;
-    uint64_t last = 16;  // unused trailing dims: extent 1, the last real stride
-    for (int i = 1; i < 5; i++) {
-      if (i < d.rank) last = d.strides[i];
-      strides[i - 1] = last;
+    auto it = plan->maps.find(g);
+    if (it != plan->maps.end()) {
+      map = it->second;
+    } else {
+      // uint8 elements: dim 0 in bytes, the other dims as lowered (byte strides)
+      uint64_t dims[5], strides[4];
+      uint32_t box[5];
+      const axe_tma_desc &d = plan->desc;
+      for (int i = 0; i < 5; i++) {
+        dims[i] = i < d.rank ? d.dims[i] : 1;
+        box[i] = i < d.rank ? d.box[i] : 1;
+      }
+      dims[0] *= (uint64_t)plan->es;
+      box[0] *= (uint32_t)plan->es;
+      if (plan->fuse > 1) box[plan->fuse_dim] = (uint32_t)plan->fuse;
+      uint64_t last = 16;  // unused trailing dims: extent 1, the last real stride
+      for (int i = 1; i < 5; i++) {
+        if (i < d.rank) last = d.strides[i];
+        strides[i - 1] = last;
+      }
+      alignas(64) unsigned char m[128];
+      const int r = encode_tensor_map(m, (void *)g, dims, strides, box, d.swizzle_bytes);
+      if (r != 0) AXE_FAIL(AXE_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", r);
+      memcpy(map.data(), m, 128);
+      if (plan->maps.size() >= 1024) plan->maps.clear();
+      plan->maps.emplace(g, map);
     }
-    const int r = encode_tensor_map(plan->map, (void *)g, dims, strides, box, d.swizzle_bytes);
-    if (r != 0) AXE_FAIL(AXE_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", r);
-    plan->map_for = g;
   }
-  TmaReps one;
-  memset(&one, 0, sizeof(one));
-  one.n = 1;
-  const cudaError_t e = launch_tma_region(plan->map, plan->table, (uint32_t)plan->host.size(), plan->box_bytes,
-                                          (void *)s_image, st, dep, store, reps ? *reps : one);
+  const cudaError_t e = launch_tma_region(map.data(), p, store, st);
   if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "tma region launch: %s", cudaGetErrorString(e));
   return AXE_OK;
 }
@@ -213,10 +304,16 @@ axe_status axe_tma_plan_create(const axe_tma_desc *desc, const axe_layout *tiler
       p->fuse_dim = rd + 1;
     }
   }
-  // upload now when a device is current (so executes can be graph-captured); on a host without a
-  // GPU the first execute would upload -- there is no execute there
+  p->prog = fit_program(p->host);
+  const char *force_table = getenv("AXE_TMA_REGION_TABLE");  // tests: run the table form
+  if (force_table && *force_table == '1') p->prog.nd = -1;
+  // a table the program does not reproduce is uploaded now when a device is current (so executes can
+  // be graph-captured); on a host without a GPU the first execute would upload -- there is no execute
   int ndev = 0, dev = 0;
-  if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0 && cudaGetDevice(&dev) == cudaSuccess) upload(p, dev);
+  if (p->prog.nd < 0 && cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0 && cudaGetDevice(&dev) == cudaSuccess) {
+    TmaAtom *t = nullptr;
+    upload(p, dev, &t);
+  }
   cudaGetLastError();  // (clear a sticky-free error from the probe)
   *out = p;
   return AXE_OK;
@@ -230,17 +327,30 @@ axe_status axe_tma_plan_sizes(const axe_tma_plan *plan, int64_t *atoms, int64_t 
   return AXE_OK;
 }
 
+// The public executes wait for everything before them on the stream (dep = 1) and, since the kernel
+// lets its dependents launch at entry without joining the copy planner's byte-range window, reset
+// that window: the next libaxe kernel on the stream waits for this one.
 axe_status axe_tma_plan_execute(axe_tma_plan *plan, const void *g_base, void *s_image, void *stream) {
-  return tma_plan_run(plan, g_base, s_image, stream, 1, 0);  // (outside the copy planner's PDL window)
+  AXE_TRY(tma_plan_run(plan, g_base, s_image, stream, 1, 0));
+  stream_forget((cudaStream_t)stream);
+  return AXE_OK;
 }
 
 axe_status axe_tma_plan_execute_store(axe_tma_plan *plan, void *g_base, const void *s_image, void *stream) {
-  return tma_plan_run(plan, g_base, s_image, stream, 1, 1);
+  AXE_TRY(tma_plan_run(plan, g_base, s_image, stream, 1, 1));
+  stream_forget((cudaStream_t)stream);
+  return AXE_OK;
 }
 
 void axe_tma_plan_destroy(axe_tma_plan *plan) {
   if (!plan) return;
-  if (plan->table) cudaFree(plan->table);
+  for (auto &t : plan->tables) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(t.first);
+    cudaFree(t.second);
+    cudaSetDevice(cur);
+  }
   delete plan;
 }
 
@@ -327,9 +437,9 @@ bool build_lowered(const std::vector<Joint> &J0, const Linear &ls, const Linear 
   char b[320];
   snprintf(b, sizeof b,
            "{\"kernel\":\"lowered\",\"mode\":\"%s\",\"atoms\":%lld,\"boxes\":%lld,\"box_bytes\":%u,\"swizzle\":%d,"
-           "\"replicas\":%d,\"tensor_map\":{\"dims\":[",
+           "\"replicas\":%d,\"box_program_digits\":%d,\"tensor_map\":{\"dims\":[",
            store ? "bulk-load/tensor-store" : "tensor-load/bulk-store", (long long)(tp->host.size() * tp->fuse),
-           (long long)tp->host.size(), tp->box_bytes, sw, (int)reps.size());
+           (long long)tp->host.size(), tp->box_bytes, sw, (int)reps.size(), tp->prog.nd);
   std::string s = b;
   for (int i = 0; i < d.rank; i++) s += (i ? "," : "") + std::to_string(d.dims[i]);
   s += "],\"strides\":[";

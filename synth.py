@@ -40,9 +40,10 @@ def values(n: int, es: int, seed: int) -> np.ndarray:
     words include NaN/Inf/denormal encodings, so compare as integers, never floats).
     """
     out = np.empty(n * es, dtype=np.uint8)
-    chunk = 1 << 24
+    chunk = 1 << 22
     words = max(1, es // 8)
-    for s in range(0, n, chunk):
+
+    def fill(s):
         e = min(n, s + chunk)
         x = np.arange(s, e, dtype=np.uint64)
         if es <= 8:
@@ -55,15 +56,40 @@ def values(n: int, es: int, seed: int) -> np.ndarray:
                 with np.errstate(over="ignore"):
                     parts.append(_splitmix64(np.uint64(seed) ^ ((x * np.uint64(words) + np.uint64(w)) * GOLDEN)))
             out[s * es:e * es] = np.stack(parts, axis=1).reshape(-1).view(np.uint8)
+
+    starts = range(0, n, chunk)
+    if n > 4 * chunk:  # numpy releases the GIL inside these ufuncs: chunks in parallel, same values
+        from concurrent.futures import ThreadPoolExecutor
+        import os
+        with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
+            list(ex.map(fill, starts))
+    else:
+        for s in starts:
+            fill(s)
     return out
 
 
 def sentinel(nbytes: int, seed: int) -> np.ndarray:
     """Untouched-cell sentinel bytes s(i) = splitmix64(~seed ^ i)."""
     n8 = (nbytes + 7) // 8
-    with np.errstate(over="ignore"):
-        h = _splitmix64(np.uint64(~np.uint64(seed)) ^ (np.arange(n8, dtype=np.uint64) * GOLDEN))
-    return h.view(np.uint8)[:nbytes].copy()
+    h = np.empty(n8, dtype=np.uint64)
+    chunk = 1 << 22
+
+    def fill(s):
+        e = min(n8, s + chunk)
+        with np.errstate(over="ignore"):
+            h[s:e] = _splitmix64(np.uint64(~np.uint64(seed)) ^ (np.arange(s, e, dtype=np.uint64) * GOLDEN))
+
+    starts = range(0, n8, chunk)
+    if n8 > 4 * chunk:  # chunks in parallel (numpy releases the GIL), same bytes
+        from concurrent.futures import ThreadPoolExecutor
+        import os
+        with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
+            list(ex.map(fill, starts))
+    else:
+        for s in starts:
+            fill(s)
+    return h.view(np.uint8)[:nbytes]
 
 
 # ----------------------------------------------------------------------------
@@ -192,9 +218,19 @@ _FLOAT_FORMATS = {
 DTYPE_SIZE = {"f16": 2, "bf16": 2, "f32": 4, "f64": 8, "i32": 4, "i64": 8}
 
 
-def numbers(n: int, dtype: str, seed: int) -> np.ndarray:
-    """n summands of `dtype` as raw bytes.  Floats: random sign, |v| in [2^-8, 1) (exponent
-    bias-8 .. bias-1 from draw bits 56-58, fraction from the low draw bits).  Integers: the
+# exponent-field ranges of the "wide" summands: the whole range of binary16 (subnormals up to 65504, so
+# f16 sums overflow and straddle the largest finite value); for bf16 / f32 / f64 everything from the
+# subnormals up to bias + 110 (bias + 900 for f64), so no fp32 (fp64) partial sum of K <= 256 terms
+# can overflow the accumulator -- 237 binades of bf16 / f32 in one sum
+_WIDE_EXP = {"f16": (0, 30), "bf16": (0, 127 + 110), "f32": (0, 127 + 110), "f64": (0, 1023 + 900)}
+
+
+def numbers(n: int, dtype: str, seed: int, dist: str = "wide") -> np.ndarray:
+    """n summands of `dtype` as raw bytes.  Floats: random sign and fraction; the exponent field
+    uniform over `dist`'s range -- "wide": _WIDE_EXP (subnormals, cancellation between terms of
+    similar size, sums of terms hundreds of binades apart, f16 overflow); "narrow": bias-8 .. bias-1
+    (|v| in [2^-8, 1): every partial sum of K <= 32 bf16 / f16 terms is exact in fp32, used where a
+    test needs exact sums); "top": the top 4 binades of f16 (sums land around 65504).  Integers: the
     raw draws (sums wrap modulo 2^bits)."""
     with np.errstate(over="ignore"):
         h = _splitmix64(np.uint64(seed) ^ (np.arange(n, dtype=np.uint64) * GOLDEN))
@@ -204,9 +240,32 @@ def numbers(n: int, dtype: str, seed: int) -> np.ndarray:
         return h.view(np.uint8)
     sbit, eshift, bias, fbits, st = _FLOAT_FORMATS[dtype]
     sign = (h >> np.uint64(63)) << np.uint64(sbit)
-    expo = (np.uint64(bias - 8) + ((h >> np.uint64(56)) & np.uint64(7))) << np.uint64(eshift)
     frac = h & np.uint64((1 << fbits) - 1)
-    return (sign | expo | frac).astype(st).view(np.uint8)
+    if dist == "narrow":
+        efield = np.uint64(bias - 8) + ((h >> np.uint64(56)) & np.uint64(7))
+    elif dist == "wide" or dist == "top":
+        lo, hi = _WIDE_EXP[dtype] if dist == "wide" else (27, 30)
+        if dist == "top" and dtype != "f16":
+            raise ValueError("'top' is the f16 overflow range")
+        efield = np.uint64(lo) + (h >> np.uint64(40)) % np.uint64(hi - lo + 1)
+    else:
+        raise ValueError(dist)
+    return (sign | (efield << np.uint64(eshift)) | frac).astype(st).view(np.uint8)
+
+
+def cancelling(K: int, Y: int, dtype: str, seed: int) -> np.ndarray:
+    """(K, Y) summands (logical order k * Y + y) where summand 1 of every output is summand 0 with its
+    sign bit flipped (exact cancellation when K >= 2) and the rest are "wide" numbers: whenever the
+    pair is the largest term the result is small against sum |x_k|."""
+    es = DTYPE_SIZE[dtype]
+    a = numbers(K * Y, dtype, seed, "wide").copy()
+    if K < 2:
+        return a
+    sbit = _FLOAT_FORMATS[dtype][0]
+    st = _FLOAT_FORMATS[dtype][4]
+    v = a.view(st)
+    v[Y:2 * Y] = v[:Y] ^ st(1 << sbit)
+    return v.view(np.uint8)[:K * Y * es]
 
 
 def reduce_local(K: int = 8, rows: int = 8192, cols: int = 4096, dtype: str = "bf16", tiled: bool = False):

@@ -44,7 +44,7 @@ def test_sum_over_leading_dim_is_numpy_sum(dtype):
     so the only rounding is the final cast, which numpy / torch perform independently."""
     K, R, Cc = 5, 24, 40
     cfg = synth.reduce_local(K, R, Cc, dtype)
-    s = synth.numbers(K * R * Cc, dtype, 11)
+    s = synth.numbers(K * R * Cc, dtype, 11, "narrow")
     got = run_local(cfg, s)
     exp = to_dtype_bytes(as_float64(s, dtype).reshape(K, R * Cc).sum(axis=0), dtype)
     assert np.array_equal(got, exp)
@@ -103,7 +103,7 @@ def test_dtensor_reduce_scatter_example():
     (64, 64) output sharded by rows: rank g holds rows [16 g, 16 g + 16) of numpy's sum."""
     P = 4
     cfg = synth.reduce_scatter(P, 64, 64, "f32")
-    parts = [synth.numbers(64 * 64, "f32", 20 + g) for g in range(P)]
+    parts = [synth.numbers(64 * 64, "f32", 20 + g, "narrow") for g in range(P)]
     outs = [synth.sentinel(16 * 64 * 4, g) for g in range(P)]
     oracle.reduce(cfg["src"], cfg["src_st"], parts, cfg["dst"], cfg["dst_st"], outs, "f32", nranks=P)
     tot = np.stack([p.view(np.float32).astype(np.float64) for p in parts]).sum(axis=0).astype(np.float32)
@@ -115,7 +115,7 @@ def test_dtensor_reduce_scatter_example():
 def test_all_reduce_every_rank_holds_the_sum():
     P = 3
     cfg = synth.all_reduce(P, 8, 32, "bf16")
-    parts = [synth.numbers(8 * 32, "bf16", 30 + g) for g in range(P)]
+    parts = [synth.numbers(8 * 32, "bf16", 30 + g, "narrow") for g in range(P)]
     outs = [synth.sentinel(8 * 32 * 2, g) for g in range(P)]
     oracle.reduce(cfg["src"], cfg["src_st"], parts, cfg["dst"], cfg["dst_st"], outs, "bf16", nranks=P)
     tot = to_dtype_bytes(np.stack([as_float64(p, "bf16") for p in parts]).sum(axis=0), "bf16")
@@ -130,7 +130,7 @@ def test_transposed_destination_and_untouched_cells():
     src = layout([(K, R * Cc), (R, Cc), (Cc, 1)])
     dst = layout([(R, 1), (Cc, ld)])
     cfg = dict(dtype="f32", src=src, src_st=linear_storage(K * R * Cc), dst=dst, dst_st=linear_storage(Cc * ld))
-    s = synth.numbers(K * R * Cc, "f32", 40)
+    s = synth.numbers(K * R * Cc, "f32", 40, "narrow")
     got = run_local(cfg, s)
     tot = s.view(np.float32).astype(np.float64).reshape(K, R, Cc).sum(axis=0).astype(np.float32)
     g = got.view(np.float32).reshape(Cc, ld)
@@ -144,7 +144,7 @@ def test_source_replicas_and_destination_replicas():
     K, N = 4, 32
     src = layout([(K, N), (N, 1)], [(2, K * N)])
     dst = layout([(N, 1)], [(2, N)])
-    s = synth.numbers(K * N, "f32", 41)
+    s = synth.numbers(K * N, "f32", 41, "narrow")
     sbuf = np.concatenate([s, s])
     cfg = dict(dtype="f32", src=src, src_st=linear_storage(2 * K * N), dst=dst, dst_st=linear_storage(2 * N))
     got = run_local(cfg, sbuf).view(np.float32)
@@ -170,3 +170,34 @@ def test_errors():
         oracle.reduce(layout([(30, 1)]), linear_storage(30), s, layout([(3, 0 + 1), (5, 1)]), linear_storage(8),
                       np.zeros(32, np.uint8), "f32")
     assert e.value.status == "collide"
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16", "f32"])
+def test_wide_range_sums_are_the_correctly_rounded_sum(dtype):
+    """Summands spanning the whole exponent range (subnormals, cancellation, f16 overflow): the oracle's
+    fp64 sum rounded once equals math.fsum (the exactly rounded sum) cast to the type -- except where the
+    two roundings of fp64-then-type differ from one rounding, which leaves at most one unit in the last
+    place (and never changes the result's sign or overflow)."""
+    import math
+    K, R, Cc = 6, 16, 64
+    cfg = synth.reduce_local(K, R, Cc, dtype)
+    s = synth.numbers(K * R * Cc, dtype, 51)
+    got = run_local(cfg, s)
+    x = as_float64(s, dtype).reshape(K, R * Cc)
+    exact = np.array([math.fsum(x[:, j]) for j in range(R * Cc)])
+    exp = to_dtype_bytes(exact, dtype)
+    ut = np.uint16 if dtype in ("f16", "bf16") else np.uint32
+    g, e = got.view(ut).astype(np.int64), exp.view(ut).astype(np.int64)
+    assert (g == e).mean() > 0.99
+    assert np.all(np.abs(g - e) <= 1)
+
+
+def test_cancelling_pairs_sum_to_the_rest():
+    """synth.cancelling: summand 1 is summand 0 negated, so the sum is exactly that of summands 2..K-1."""
+    K, Y = 4, 256
+    s = synth.cancelling(K, Y, "f32", 52)
+    cfg = synth.reduce_local(K, 1, Y, "f32")
+    got = run_local(cfg, s).view(np.float32)
+    x = s.view(np.float32).astype(np.float64).reshape(K, Y)
+    assert np.array_equal(x[0], -x[1])
+    assert np.array_equal(got, (x[2] + x[3]).astype(np.float32))

@@ -118,7 +118,7 @@ def enact_rank(p, rank, n, K, C_cells, dtype, src_of, wire_in):
 def dist_inputs(cfg, dtype, seed=5):
     n, es = cfg["nranks"], synth.DTYPE_SIZE[dtype]
     ed, _ = oracle.sizes(cfg["src"])
-    vals = synth.numbers(ed, dtype, seed)
+    vals = synth.numbers(ed, dtype, seed, "narrow")  # exact fp64 sums: the enactment sums by numpy
     fill = synth.sentinel(synth.storage_cells(cfg["src_st"]) * es, seed + 1)
     src = oracle.scatter_ranks(cfg["src"], cfg["src_st"], vals, es, n, fill)
     dfill = synth.sentinel(synth.storage_cells(cfg["dst_st"]) * es, seed + 2)

@@ -135,3 +135,50 @@ def test_misaligned_region_rejected(axe):
     with pytest.raises(axe.AxeError) as e:
         plan.execute(g[1:], img)
     assert e.value.name == "AXE_ERR_ALIGNMENT"
+
+
+@pytest.mark.parametrize("es,sw", [(1, 128), (2, 64), (4, 128), (8, 32)])
+def test_random_regions_table_form(axe, es, sw, monkeypatch):
+    """The kernel's fallback form (box coordinates read from the atom table in global memory instead of
+    the fitted mixed-radix program) on the same random regions."""
+    monkeypatch.setenv("AXE_TMA_REGION_TABLE", "1")
+    rng = np.random.default_rng(es * 7 + sw)
+    inner = sw // es
+    for trial in range(6):
+        ES = [8 * int(rng.integers(1, 6)), inner * int(rng.integers(1, 4))]
+        v = 16 // es
+        rows = ES[0] * int(rng.integers(1, 4)) + int(rng.integers(0, 9))
+        cols = ES[1] + v * int(rng.integers(0, 5))
+        ld = cols + v * int(rng.integers(0, 3))
+        begin = [int(rng.integers(0, rows - ES[0] + 1)), v * int(rng.integers(0, (cols - ES[1]) // v + 1))]
+        run_case(axe, rows, cols, ld, begin, ES, atom_tiled_smem(rng, ES, inner, trial % 2), es, sw, 100 + trial)
+
+
+def test_copy_then_tma_plan_then_copy_without_sync(axe):
+    """a copy writes G, the TMA plan turns G into the image, a small copy reads the image --
+    back to back on one stream with no synchronize.  The TMA plan's kernel lets its dependents launch at
+    entry, so the copy after it must still wait for it (the public execute resets the PDL window)."""
+    n = 512
+    ES = [64, 64]
+    LS = layout([(64, 64), (64, 1)])
+    rm = layout([(n, n), (n, 1)])
+    plan = axe.TmaPlan(rm, [n, n], LS, ES, 2, 128, begin=[64, 128], extent=ES)
+    ident = axe.CopyPlan(rm, linear_storage(n * n), rm, linear_storage(n * n), 2)
+    sub = layout([(64 * 64, 1)])
+    read = axe.CopyPlan(sub, linear_storage(64 * 64), sub, linear_storage(64 * 64), 2)
+    fwd = synth.sentinel(n * n * 2, 41)
+    exp_img = synth.sentinel(64 * 64 * 2, 42)
+    region = layout([(64, n), (64, 1)], O={"m": 64 * n + 128})
+    oracle.copy(region, linear_storage(n * n), fwd, LS, linear_storage(64 * 64, SW[128]), exp_img, 2)
+    src = torch.from_numpy(fwd).cuda()
+    st = torch.cuda.current_stream()
+    for _ in range(20):
+        g = torch.zeros(n * n, dtype=torch.int16, device="cuda")
+        img = torch.zeros(64 * 64, dtype=torch.int16, device="cuda")
+        out = torch.zeros(64 * 64, dtype=torch.int16, device="cuda")
+        torch.cuda.synchronize()
+        ident.execute(src, g, st)
+        plan.execute(g, img, st)
+        read.execute(img, out, st)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint8), exp_img)

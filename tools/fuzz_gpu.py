@@ -161,7 +161,7 @@ def run_reduce(cfg, seed):
             return "skip"
         return f"plan failed: {e}"
     ed, _ = oracle.sizes(cfg["src"])
-    v = synth.numbers(ed, dtype, seed)
+    v = synth.numbers(ed, dtype, seed, "narrow")  # exact partial sums: compared bit for bit
     sfill = synth.sentinel(synth.storage_cells(cfg["src_st"]) * es, seed + 1)
     src = oracle.scatter_logical(cfg["src"], cfg["src_st"], v, es, sfill, NT)
     dfill = synth.sentinel(synth.storage_cells(cfg["dst_st"]) * es, seed + 2)

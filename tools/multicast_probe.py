@@ -69,7 +69,7 @@ def main():
         out["multicast"] = True
         cfg = synth.reduce_scatter(1, rows, cols, "bf16")
         plan = axe.RedistPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], 2, 1, 0, reduce_dtype="bf16")
-        vals = synth.numbers(rows * cols, "bf16", 9)
+        vals = synth.numbers(rows * cols, "bf16", 9, "narrow")
         host = torch.from_numpy(vals.copy())
         ok(d.cuMemcpyHtoD(uva, host.numpy().ctypes.data, nbytes))
         dst = torch.zeros(rows * cols, dtype=torch.bfloat16, device="cuda")
