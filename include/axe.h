@@ -45,7 +45,8 @@ enum {
   AXE_ERR_ALIAS = 10,           /* source and destination byte ranges overlap (no in-place)               */
   AXE_ERR_CUDA = 11,            /* a CUDA runtime call failed (message has the CUDA error string)         */
   AXE_ERR_NCCL = 12,            /* an NCCL call failed                                                    */
-  AXE_ERR_UNSUPPORTED = 13      /* a forced kernel cannot run this pair of layouts                        */
+  AXE_ERR_UNSUPPORTED = 13,     /* a forced kernel cannot run this pair of layouts                        */
+  AXE_ERR_TIMEOUT = 14          /* axe_comm_wait: the stream did not finish in time (communicator aborted) */
 };
 
 /* ------------------------------------------------------------------------- */
@@ -318,6 +319,26 @@ axe_status axe_get_unique_id(uint8_t out[128]);
 /* Collective over nranks processes, one device each (cuda_device). */
 axe_status axe_comm_create(const uint8_t id[128], int nranks, int rank, int cuda_device, axe_comm **out);
 void axe_comm_destroy(axe_comm *comm);
+/* Wait on the host until every operation enqueued on cuda_stream so far has finished, polling the
+ * communicator's asynchronous NCCL error state (ncclCommGetAsyncError) every 50 us.  On an
+ * asynchronous error (AXE_ERR_NCCL) or when timeout_ms (< 0: no limit) passes first
+ * (AXE_ERR_TIMEOUT), the communicator is aborted (ncclCommAbort: the NCCL kernels waiting on a
+ * failed peer return) and every later call on it fails with AXE_ERR_NCCL; destroy it and create a
+ * new one.  Every execute on a communicator also checks the asynchronous error before and after its
+ * enqueue.  Executes of one plan are serialised: on the host, and on the device each waits for the
+ * previous execute of the same plan (they share its staging buffers). */
+axe_status axe_comm_wait(axe_comm *comm, void *cuda_stream, int timeout_ms);
+
+/* CUDA IPC for the one-sided forms (axe_redist_plan_execute_peers / _peers_reduce) between processes
+ * of one node: export writes a 128-byte handle for the device allocation holding dev_ptr (the
+ * cudaIpcMemHandle_t of the allocation + dev_ptr's byte offset in it, so sub-allocated framework
+ * tensors work); import maps a handle exported by ANOTHER process (same or another GPU; peer access
+ * is enabled lazily) and returns the pointer to use in dst_peers / src_peers; close unmaps it.
+ * Errors: AXE_ERR_INVALID_ARG (not a device allocation / not an imported pointer), AXE_ERR_CUDA
+ * (the driver refused, e.g. importing a handle of the same process). */
+axe_status axe_ipc_export(const void *dev_ptr, uint8_t handle[128]);
+axe_status axe_ipc_import(const uint8_t handle[128], void **dev_ptr);
+axe_status axe_ipc_close(void *dev_ptr);
 
 typedef struct axe_redist_plan axe_redist_plan;
 

@@ -17,7 +17,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "axe_oracle.c")
-_LIB = os.path.join(_HERE, "liboracle.so")
+_LIB = os.environ.get("AXE_ORACLE_LIB") or os.path.join(_HERE, "liboracle.so")  # (tools/asan_host.sh build)
 
 OK, EINVAL, EDOMAIN, ESIZE, EBOUNDS, ECOLLIDE, ECAPACITY, ENOMEM = range(8)
 STATUS = {OK: "ok", EINVAL: "invalid", EDOMAIN: "domain", ESIZE: "size", EBOUNDS: "bounds",

@@ -29,7 +29,7 @@ AXE_OK = 0
 ERRORS = {0: "AXE_OK", 1: "AXE_ERR_INVALID_ARG", 2: "AXE_ERR_OVERFLOW", 3: "AXE_ERR_DOMAIN", 4: "AXE_ERR_CAPACITY",
           5: "AXE_ERR_SIZE_MISMATCH", 6: "AXE_ERR_NONINJECTIVE", 7: "AXE_ERR_BOUNDS",
           8: "AXE_ERR_UNSUPPORTED_AXIS", 9: "AXE_ERR_ALIGNMENT", 10: "AXE_ERR_ALIAS", 11: "AXE_ERR_CUDA",
-          12: "AXE_ERR_NCCL", 13: "AXE_ERR_UNSUPPORTED"}
+          12: "AXE_ERR_NCCL", 13: "AXE_ERR_UNSUPPORTED", 14: "AXE_ERR_TIMEOUT"}
 KERNELS = {"auto": 0, "generic": 1, "vector": 2, "tma": 3, "tile": 4, "register": 5, "tma_tile": 6, "shuffle": 7, "transpose": 8,
            "lowered": 9}
 
@@ -102,6 +102,10 @@ _SIGS = {
     "axe_get_unique_id": ([C.c_char_p], C.c_int),
     "axe_comm_create": ([C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)], C.c_int),
     "axe_comm_destroy": ([_vp], None),
+    "axe_comm_wait": ([_vp, _vp, C.c_int], C.c_int),
+    "axe_ipc_export": ([_vp, C.c_char_p], C.c_int),
+    "axe_ipc_import": ([C.c_char_p, C.POINTER(_vp)], C.c_int),
+    "axe_ipc_close": ([_vp], C.c_int),
     "axe_redist_plan_create": ([_vp, C.POINTER(axe_storage), _vp, C.POINTER(axe_storage), C.c_int, C.c_int, C.c_int,
                                 C.POINTER(_vp)], C.c_int),
     "axe_redist_plan_execute": ([_vp, _vp, _vp, _vp, _vp], C.c_int),
@@ -463,6 +467,30 @@ class Comm:
     @property
     def handle(self):
         return self._h
+
+    def wait(self, stream=None, timeout_ms: int = -1):
+        """axe_comm_wait: block until the stream is done, polling NCCL's asynchronous errors; on an error or
+        a timeout the communicator is aborted and AxeError (AXE_ERR_NCCL / AXE_ERR_TIMEOUT) raised."""
+        _check(_lib.axe_comm_wait(self._h, _stream(stream), int(timeout_ms)), "axe_comm_wait")
+
+
+def ipc_export(buf) -> bytes:
+    """axe_ipc_export: a 128-byte CUDA IPC handle for the device buffer (tensor or pointer)."""
+    h = C.create_string_buffer(128)
+    _check(_lib.axe_ipc_export(_ptr(buf), h), "axe_ipc_export")
+    return h.raw
+
+
+def ipc_import(handle: bytes) -> int:
+    """axe_ipc_import: map another process's exported buffer; returns the device pointer (int)."""
+    assert len(handle) == 128
+    p = C.c_void_p()
+    _check(_lib.axe_ipc_import(handle, C.byref(p)), "axe_ipc_import")
+    return int(p.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _check(_lib.axe_ipc_close(C.c_void_p(ptr)), "axe_ipc_close")
 
 
 class RedistPlan:

@@ -64,7 +64,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(compile_one, sources()))
     tmp = OUT + f".tmp{os.getpid()}"
-    cmd = [NVCC, "-shared"] + ARCH + ["-cudart", "static", "-o", tmp] + objs + [
+    cmd = [NVCC, "-shared"] + ARCH + os.environ.get("AXE_EXTRA_LINK", "").split() + ["-cudart", "static", "-o", tmp] + objs + [
         "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nccl, "lib")]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -135,6 +135,14 @@ struct Joint {
 // Refine two linear shard lists over the same domain into one joint digit list
 // (innermost-first gcd/divisibility pairing; Alg. 1 generalised, R21).
 bool joint_refine(const std::vector<LinIter> &src, const std::vector<LinIter> &dst, std::vector<Joint> *out);
+// When the two digit systems do not nest (joint_refine fails), the innermost part still refines: pair
+// from the fastest digit as joint_refine does, and at the first pair whose extents do not divide each
+// other split off their gcd g as one more joint digit (both digits are multiples of g, so an aligned run
+// of g consecutive x stays inside both).  What is left -- the outer index x / G over the two
+// remaining lists -- has two independent decodings (src_rest, dst_rest, outermost first; the same
+// product).  Returns false if nothing refines (G = 1 with no joint digit).
+bool joint_refine_partial(const std::vector<LinIter> &src, const std::vector<LinIter> &dst, std::vector<Joint> *inner,
+                          std::vector<LinIter> *src_rest, std::vector<LinIter> *dst_rest);
 
 // Order digits by |dst stride| (outermost first) and fuse neighbours that are
 // contiguous on both sides (Cor. fuse): fewer digits to decode.

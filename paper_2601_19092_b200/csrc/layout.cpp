@@ -457,4 +457,54 @@ bool joint_refine(const std::vector<LinIter> &src_in, const std::vector<LinIter>
   return true;
 }
 
+bool joint_refine_partial(const std::vector<LinIter> &src_in, const std::vector<LinIter> &dst_in,
+                          std::vector<Joint> *inner, std::vector<LinIter> *src_rest, std::vector<LinIter> *dst_rest) {
+  std::vector<LinIter> a = normalize_lin(src_in), b = normalize_lin(dst_in);
+  std::vector<Joint> J;
+  while (!a.empty() && !b.empty()) {
+    LinIter &x = a.back(), &y = b.back();
+    if (x.e == y.e) {
+      J.push_back(Joint{x.e, x.s, y.s, x.dev, y.dev});
+      a.pop_back();
+      b.pop_back();
+    } else if (x.e % y.e == 0) {
+      J.push_back(Joint{y.e, x.s, y.s, x.dev, y.dev});
+      x = LinIter{x.e / y.e, x.s * y.e, x.dev};
+      b.pop_back();
+    } else if (y.e % x.e == 0) {
+      J.push_back(Joint{x.e, x.s, y.s, x.dev, y.dev});
+      y = LinIter{y.e / x.e, y.s * x.e, y.dev};
+      a.pop_back();
+    } else {
+      const int64_t g = std::gcd(x.e, y.e);
+      if (g > 1) {
+        J.push_back(Joint{g, x.s, y.s, x.dev, y.dev});
+        x = LinIter{x.e / g, x.s * g, x.dev};
+        y = LinIter{y.e / g, y.s * g, y.dev};
+      }
+      break;
+    }
+  }
+  if (J.empty()) return false;
+  std::reverse(J.begin(), J.end());
+  std::vector<Joint> F;  // joint D1 (Cor. fuse)
+  for (auto &j : J) {
+    F.push_back(j);
+    while (F.size() >= 2) {
+      Joint &p = F[F.size() - 2], &q = F.back();
+      if (p.sdev == q.sdev && p.ddev == q.ddev && p.ss == q.e * q.ss && p.ds == q.e * q.ds) {
+        Joint m{p.e * q.e, q.ss, q.ds, q.sdev, q.ddev};
+        F.pop_back();
+        F.back() = m;
+      } else {
+        break;
+      }
+    }
+  }
+  *inner = std::move(F);
+  *src_rest = a;
+  *dst_rest = b;
+  return true;
+}
+
 }  // namespace axe

@@ -15,6 +15,7 @@
 //      block, unpack plans (recv staging -> dst_local), local copy plans;
 //      pack/unpack are elided when a block is contiguous on that side, and an
 //      all-gather pattern is lowered to ncclAllGather.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -25,6 +26,10 @@
 #include <mutex>
 #include <numeric>
 #include <unordered_map>
+#include <chrono>
+#include <thread>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "handles.hpp"
 
@@ -37,7 +42,17 @@ void stream_forget(cudaStream_t st);
 struct axe_comm {
   ncclComm_t comm = nullptr;
   int nranks = 0, rank = 0, device = 0;
+  std::mutex mu;         // NCCL enqueues on one communicator are not concurrent-safe: one call at a time
+  bool aborted = false;  // axe_comm_wait aborted it (timeout or asynchronous error)
 };
+
+namespace {
+// NVTX range for the timeline (nsys / ncu --nvtx): plan, pack, wire, unpack phases
+struct Nvtx {
+  explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace {
 
@@ -93,6 +108,11 @@ struct axe_redist_plan {
   mutable cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
   mutable cudaStream_t pk = nullptr, up = nullptr;  // pack / unpack streams
   mutable std::vector<cudaEvent_t> ev_pack, ev_recv;
+  // executes of one plan are serialised: the host enqueue under exec_mu, and on the device every
+  // execute waits for the previous one (ev_done) -- they share the staging buffers and side streams
+  mutable std::mutex exec_mu;
+  mutable cudaEvent_t ev_done = nullptr;
+  mutable bool done_valid = false;
   ~axe_redist_plan() {
     if (send_buf) cudaFree(send_buf);
     if (recv_buf) cudaFree(recv_buf);
@@ -100,7 +120,7 @@ struct axe_redist_plan {
     if (tmp) cudaFree(tmp);
     for (cudaStream_t x : {side, pk, up})
       if (x) cudaStreamDestroy(x);
-    for (cudaEvent_t x : {ev_fork, ev_join, ev_join2})
+    for (cudaEvent_t x : {ev_fork, ev_join, ev_join2, ev_done})
       if (x) cudaEventDestroy(x);
     for (auto &v : {ev_pack, ev_recv})
       for (cudaEvent_t x : v)
@@ -642,6 +662,7 @@ static axe_status exec_redist(const axe_redist_plan *P, axe_comm *C, const void 
   uint8_t *d = (uint8_t *)dst;
   const size_t bytes = (size_t)(P->n * P->es);
   if (P->allgather) {
+    Nvtx r("axe.redist.allgather");
     NCCL_TRY(ncclAllGather(s + P->ag_src * P->es, d + P->ag_dst * P->es, bytes, ncclUint8, C->comm, st));
     stream_forget(st);
     return AXE_OK;
@@ -659,12 +680,14 @@ static axe_status exec_redist(const axe_redist_plan *P, axe_comm *C, const void 
   CU_TRY(cudaEventRecord(P->ev_fork, st));
   // local copies on a side stream, overlapping pack + exchange
   if (!P->locals.empty()) {
+    Nvtx r("axe.redist.local");
     CU_TRY(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
     stream_forget(P->side);
     for (auto &x : P->locals) AXE_TRY(run_copy(*x.plan, src, dst, P->side));
   }
   // packs, chunk by chunk, on the pack stream
   if (packs) {
+    Nvtx r("axe.redist.pack");
     CU_TRY(cudaStreamWaitEvent(P->pk, P->ev_fork, 0));
     stream_forget(P->pk);
     for (int c = 0; c < P->nchunk; c++) {
@@ -678,6 +701,7 @@ static axe_status exec_redist(const axe_redist_plan *P, axe_comm *C, const void 
   }
   // the wire: one NCCL group per chunk (chunk c of every block), after that chunk is packed
   const size_t cbytes = (size_t)(P->cn * P->es);
+  Nvtx wire("axe.redist.wire+unpack");
   for (int c = 0; c < P->nchunk; c++) {
     if (packs) CU_TRY(cudaStreamWaitEvent(st, P->ev_pack[c], 0));
     NCCL_TRY(ncclGroupStart());
@@ -711,6 +735,44 @@ static axe_status exec_redist(const axe_redist_plan *P, axe_comm *C, const void 
   }
 #undef CU_TRY
   return AXE_OK;
+}
+
+// NCCL reports errors of kernels already enqueued (a peer that died, a network failure) only
+// asynchronously: checked before and after every enqueue on the communicator.
+static axe_status comm_check(axe_comm *C) {
+  if (!C) return AXE_OK;
+  if (C->aborted || !C->comm) AXE_FAIL(AXE_ERR_NCCL, "communicator was aborted (axe_comm_wait)");
+  ncclResult_t ar = ncclSuccess;
+  const ncclResult_t r = ncclCommGetAsyncError(C->comm, &ar);
+  if (r != ncclSuccess) AXE_FAIL(AXE_ERR_NCCL, "ncclCommGetAsyncError: %s", ncclGetErrorString(r));
+  if (ar != ncclSuccess && ar != ncclInProgress)
+    AXE_FAIL(AXE_ERR_NCCL, "asynchronous NCCL error: %s", ncclGetErrorString(ar));
+  return AXE_OK;
+}
+
+// Every public execute of a plan: one at a time on the host (exec_mu, and the communicator's lock when
+// it enqueues NCCL work), and on the device after the previous execute of the same plan (ev_done) --
+// executes on different streams would otherwise share the plan's staging buffers and side streams.
+template <class F>
+static axe_status serialized(const axe_redist_plan *P, axe_comm *C, cudaStream_t st, F &&fn) {
+  std::lock_guard<std::mutex> lk(P->exec_mu);
+  std::unique_lock<std::mutex> ck;
+  if (C) ck = std::unique_lock<std::mutex>(C->mu);
+  AXE_TRY(comm_check(C));
+  if (P->done_valid) {
+    const cudaError_t e = cudaStreamWaitEvent(st, P->ev_done, 0);
+    if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "cudaStreamWaitEvent: %s", cudaGetErrorString(e));
+    stream_forget(st);
+  }
+  AXE_TRY(fn());
+  if (!P->ev_done) {
+    const cudaError_t e = cudaEventCreateWithFlags(&P->ev_done, cudaEventDisableTiming);
+    if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "cudaEventCreate: %s", cudaGetErrorString(e));
+  }
+  const cudaError_t e = cudaEventRecord(P->ev_done, st);
+  if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "cudaEventRecord: %s", cudaGetErrorString(e));
+  P->done_valid = true;
+  return comm_check(C);
 }
 
 extern "C" {
@@ -747,8 +809,105 @@ axe_status axe_comm_create(const uint8_t id[128], int nranks, int rank, int cuda
 
 void axe_comm_destroy(axe_comm *c) {
   if (!c) return;
-  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->comm) {
+    if (c->aborted) ncclCommAbort(c->comm);
+    else ncclCommDestroy(c->comm);
+  }
   delete c;
+}
+
+axe_status axe_comm_wait(axe_comm *c, void *stream, int timeout_ms) {
+  if (!c) AXE_FAIL(AXE_ERR_INVALID_ARG, "comm is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(st);
+    if (q != cudaSuccess && q != cudaErrorNotReady) AXE_FAIL(AXE_ERR_CUDA, "cudaStreamQuery: %s", cudaGetErrorString(q));
+    {
+      std::lock_guard<std::mutex> lk(c->mu);
+      const axe_status a = comm_check(c);
+      if (a != AXE_OK) {
+        if (c->comm && !c->aborted) {
+          ncclCommAbort(c->comm);  // unblocks the NCCL kernels waiting on the failed peer
+          c->comm = nullptr;
+          c->aborted = true;
+        }
+        return a;
+      }
+    }
+    if (q == cudaSuccess) return AXE_OK;
+    const auto ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0);
+    if (timeout_ms >= 0 && ms.count() >= timeout_ms) {
+      std::lock_guard<std::mutex> lk(c->mu);
+      if (c->comm && !c->aborted) {
+        ncclCommAbort(c->comm);
+        c->comm = nullptr;
+        c->aborted = true;
+      }
+      AXE_FAIL(AXE_ERR_TIMEOUT, "stream not done after %d ms: communicator aborted", timeout_ms);
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
+// ---------------------------------------------------------------- CUDA IPC (one-sided forms)
+// A handle = cudaIpcMemHandle_t of the allocation holding the pointer (64 bytes) + the pointer's
+// byte offset inside that allocation (the caching allocators of frameworks sub-allocate).
+typedef CUresult (*PFN_getAddressRange)(CUdeviceptr *, size_t *, CUdeviceptr);
+static std::mutex g_ipc_mu;
+static std::map<void *, void *> g_ipc_open;  // imported pointer -> mapped allocation base
+
+axe_status axe_ipc_export(const void *dev_ptr, uint8_t handle[128]) {
+  if (!dev_ptr || !handle) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
+  static PFN_getAddressRange range = [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return (PFN_getAddressRange)p;
+  }();
+  if (!range) AXE_FAIL(AXE_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (CUdeviceptr)(uintptr_t)dev_ptr) != CUDA_SUCCESS)
+    AXE_FAIL(AXE_ERR_INVALID_ARG, "not a device allocation");
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, (void *)(uintptr_t)base);
+  if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  memset(handle, 0, 128);
+  memcpy(handle, &h, 64);
+  const int64_t off = (int64_t)((uintptr_t)dev_ptr - (uintptr_t)base);
+  memcpy(handle + 64, &off, 8);
+  return AXE_OK;
+}
+
+axe_status axe_ipc_import(const uint8_t handle[128], void **dev_ptr) {
+  if (!handle || !dev_ptr) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
+  *dev_ptr = nullptr;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, 64);
+  int64_t off = 0;
+  memcpy(&off, handle + 64, 8);
+  void *base = nullptr;
+  const cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+  void *p = (uint8_t *)base + off;
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  g_ipc_open[p] = base;
+  *dev_ptr = p;
+  return AXE_OK;
+}
+
+axe_status axe_ipc_close(void *dev_ptr) {
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  auto it = g_ipc_open.find(dev_ptr);
+  if (it == g_ipc_open.end()) AXE_FAIL(AXE_ERR_INVALID_ARG, "pointer was not imported by axe_ipc_import");
+  const cudaError_t e = cudaIpcCloseMemHandle(it->second);
+  g_ipc_open.erase(it);
+  if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+  return AXE_OK;
 }
 
 axe_status axe_redist_plan_create(const axe_layout *src, const axe_storage *src_st, const axe_layout *dst,
@@ -812,13 +971,15 @@ axe_status axe_redistribute_reduce(const axe_layout *src, const axe_storage *src
     std::lock_guard<std::mutex> lk(mu);
     cache[key] = p;
   }
-  return exec_redist(p.get(), comm, src_local, dst_local, (cudaStream_t)stream);
+  return serialized(p.get(), comm, (cudaStream_t)stream,
+                    [&] { return exec_redist(p.get(), comm, src_local, dst_local, (cudaStream_t)stream); });
 }
 
 axe_status axe_redist_plan_execute(const axe_redist_plan *plan, axe_comm *comm, const void *src_local, void *dst_local,
                                    void *stream) {
   if (!plan) AXE_FAIL(AXE_ERR_INVALID_ARG, "plan is NULL");
-  return exec_redist(plan, comm, src_local, dst_local, (cudaStream_t)stream);
+  return serialized(plan, comm, (cudaStream_t)stream,
+                    [&] { return exec_redist(plan, comm, src_local, dst_local, (cudaStream_t)stream); });
 }
 
 axe_status axe_redist_plan_execute_peers(const axe_redist_plan *plan, const void *src_local, void *const *dst_peers,
@@ -969,7 +1130,8 @@ axe_status axe_redistribute(const axe_layout *src, const axe_storage *src_st, co
     std::lock_guard<std::mutex> lk(mu);
     cache[key] = p;
   }
-  return exec_redist(p.get(), comm, src_local, dst_local, (cudaStream_t)stream);
+  return serialized(p.get(), comm, (cudaStream_t)stream,
+                    [&] { return exec_redist(p.get(), comm, src_local, dst_local, (cudaStream_t)stream); });
 }
 
 axe_status axe_redist_emulate(const axe_redist_plan *const *plans, int nranks, const void *const *src_locals,
