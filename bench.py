@@ -349,6 +349,19 @@ def measure_extras(axe, torch):
                                                  src_st=synth.linear_storage(8192 * 8192),
                                                  dst=synth.layout([(8192, 1), (8192, 8192)]),
                                                  dst_st=synth.linear_storage(8192 * 8192)),
+        "transpose_8192sq_f32": dict(es=4, src=synth.layout([(8192, 8192), (8192, 1)]),
+                                     src_st=synth.linear_storage(8192 * 8192),
+                                     dst=synth.layout([(8192, 1), (8192, 8192)]),
+                                     dst_st=synth.linear_storage(8192 * 8192)),
+        "transpose_8192x4096_f64": dict(es=8, src=synth.layout([(8192, 4096), (4096, 1)]),
+                                        src_st=synth.linear_storage(8192 * 4096),
+                                        dst=synth.layout([(8192, 1), (4096, 8192)]),
+                                        dst_st=synth.linear_storage(8192 * 4096)),
+        # non-nested digit systems: (3*2^13, 2*2^13) padded -> (2*2^13, 3*2^13) padded, 768 MiB each side
+        "nonnested_3x2_bf16_dual": dict(es=2, src=synth.layout([(3 << 13, (2 << 13) + 64), (2 << 13, 1)]),
+                                        src_st=synth.linear_storage((3 << 13) * ((2 << 13) + 64)),
+                                        dst=synth.layout([(2 << 13, (3 << 13) + 128), (3 << 13, 1)]),
+                                        dst_st=synth.linear_storage((2 << 13) * ((3 << 13) + 128))),
     }
     for name, cfg in cases.items():
         plan = axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], cfg["es"])

@@ -249,7 +249,7 @@ typedef struct {
 
 /* Kernel choice for plans (flags of axe_copy_plan_create); AUTO picks from the
  * layouts.  The environment variable AXE_FORCE_KERNEL
- * (generic | vector | tma | tile | register | tma_tile | shuffle | transpose) overrides AUTO. */
+ * (generic | vector | tma | tile | register | shuffle | transpose | lowered | dual) overrides AUTO. */
 enum {
   AXE_KERNEL_AUTO = 0,
   AXE_KERNEL_GENERIC = 1, /* K0: per-element evaluation of both layouts (always applicable) */
@@ -257,12 +257,16 @@ enum {
   AXE_KERNEL_TMA = 3,     /* K1-TMA: TMA box load into swizzled smem + bulk store            */
   AXE_KERNEL_TILE = 4,    /* K2: smem-staged tile permute / transpose                        */
   AXE_KERNEL_REGISTER = 5, /* K3: warp-register permute through movmatrix (b16 8x8 atoms)    */
-  AXE_KERNEL_TMA_TILE = 6, /* K2T: TMA SW128 box staging + conflict-free gather (transposes)  */
+  /* 6: retired (K2T, a TMA-staged transpose AUTO never chose: K7 is faster); forcing it returns
+        AXE_ERR_UNSUPPORTED */
   AXE_KERNEL_SHUFFLE = 7,  /* K6: n x n granule transpose across lanes with warp shuffles       */
   AXE_KERNEL_TRANSPOSE = 8, /* K7: smem tile + n x n register-block transpose (2-D transposes)  */
-  AXE_KERNEL_LOWERED = 9    /* the paper's TMA lowering (axe_tma_lower) as a copy schedule: the
+  AXE_KERNEL_LOWERED = 9,   /* the paper's TMA lowering (axe_tma_lower) as a copy schedule: the
                                destination is a tiling of the swizzle atom over the joint digits,
-                               one TMA load + bulk store per (fused) atom box; opt-in             */
+                               one TMA load + bulk store per (fused) atom box; AUTO takes it for
+                               copies into / out of TMA-swizzled storage (config 2)               */
+  AXE_KERNEL_DUAL = 10      /* K8: non-nested digit systems: the shared innermost run is
+                               vectorised, the outer index decoded once per side                  */
 };
 
 typedef struct axe_copy_plan axe_copy_plan;

@@ -30,8 +30,8 @@ ERRORS = {0: "AXE_OK", 1: "AXE_ERR_INVALID_ARG", 2: "AXE_ERR_OVERFLOW", 3: "AXE_
           5: "AXE_ERR_SIZE_MISMATCH", 6: "AXE_ERR_NONINJECTIVE", 7: "AXE_ERR_BOUNDS",
           8: "AXE_ERR_UNSUPPORTED_AXIS", 9: "AXE_ERR_ALIGNMENT", 10: "AXE_ERR_ALIAS", 11: "AXE_ERR_CUDA",
           12: "AXE_ERR_NCCL", 13: "AXE_ERR_UNSUPPORTED", 14: "AXE_ERR_TIMEOUT"}
-KERNELS = {"auto": 0, "generic": 1, "vector": 2, "tma": 3, "tile": 4, "register": 5, "tma_tile": 6, "shuffle": 7, "transpose": 8,
-           "lowered": 9}
+KERNELS = {"auto": 0, "generic": 1, "vector": 2, "tma": 3, "tile": 4, "register": 5, "shuffle": 7, "transpose": 8,
+           "lowered": 9, "dual": 10}
 
 
 class axe_iter(C.Structure):

@@ -12,6 +12,7 @@
 // copy operator's schedule is chosen from the two layouts.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 
@@ -259,6 +260,122 @@ template <int ND, int VB>
 static cudaError_t k1_launch_nd(const K1Params &p, unsigned blocks, const uint8_t *s, uint8_t *d, cudaStream_t st) {
   constexpr int U = VB >= 8 ? AXE_K1_U_BIG : AXE_K1_U_SMALL;
   return launch_ex(k1_vector<ND, VB, U>, dim3(blocks), dim3(K1_THREADS), 0, st, p, s, d);
+}
+
+
+// ------------------------------------------------------------------ K8 dual decoding
+template <int N>
+__device__ __forceinline__ int64_t k8_digits(int n, const FastDiv *fd, const int64_t *st, uint32_t i) {
+  int64_t off = 0;
+#pragma unroll
+  for (int k = N - 1; k >= 1; k--) {
+    if (k >= n) continue;
+    const uint32_t q = fdiv(fd[k], i);
+    off += (int64_t)(i - q * fd[k].d) * st[k];
+    i = q;
+  }
+  if (n > 0) off += (int64_t)i * st[0];
+  return off;
+}
+
+template <int VB, int U>
+__global__ void __launch_bounds__(K1_THREADS) k8_dual(const __grid_constant__ K8Params p, const uint8_t *__restrict__ src,
+                                                      uint8_t *__restrict__ dst) {
+  using T = typename VecT<VB>::T;
+  if (p.dep) pdl_wait();
+  pdl_launch_dependents();
+  if (p.chunked) {
+    // item = (o, c): vectors [c * CH, c * CH + CH) of block o, CH = K1_THREADS * U; the outer offsets are
+    // uniform over the item (two decodings per item), the inner offset is w times the run's stride
+    constexpr uint32_t CH = K1_THREADS * U;
+    const uint32_t vin = p.vin.d;
+    for (uint32_t it = blockIdx.x; it < p.nitems; it += gridDim.x) {
+      const uint32_t o = fdiv(p.nchunks, it);
+      const uint32_t c = it - o * p.nchunks.d;
+      const int64_t so = p.sbase + k8_digits<K8_MAXD>(p.na, p.afd, p.as, o);
+      const int64_t d = p.dbase + k8_digits<K8_MAXD>(p.nb, p.bfd, p.bs, o);
+      T v[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const uint32_t w = c * CH + u * K1_THREADS + threadIdx.x;
+        if (w < vin) v[u] = ld_stream<VB>(src + swz(p.ssw, so + (int64_t)w * p.iss[0]));
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const uint32_t w = c * CH + u * K1_THREADS + threadIdx.x;
+        if (w < vin)
+          for (int r = 0; r < p.nrep; r++) st_vec<VB>(dst + swz(p.dsw, d + (int64_t)w * p.ids[0] + p.rep[r]), v[u]);
+      }
+    }
+    return;
+  }
+  const uint32_t total = p.total;
+  const uint32_t step = gridDim.x * (K1_THREADS * U);
+  for (uint32_t base = blockIdx.x * (K1_THREADS * U) + threadIdx.x; base < total; base += step) {
+    T v[U];
+    int64_t dof[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t i = base + u * K1_THREADS;
+      if (i < total) {
+        const uint32_t o = fdiv(p.vin, i);
+        uint32_t w = i - o * p.vin.d;
+        int64_t so = p.sbase, d = p.dbase;
+#pragma unroll
+        for (int k = K1_MAXD - 1; k >= 1; k--) {
+          if (k >= p.nin) continue;
+          const uint32_t q = fdiv(p.ifd[k], w);
+          const int64_t dg = (int64_t)(w - q * p.ifd[k].d);
+          w = q;
+          so += dg * p.iss[k];
+          d += dg * p.ids[k];
+        }
+        if (p.nin > 0) {
+          so += (int64_t)w * p.iss[0];
+          d += (int64_t)w * p.ids[0];
+        }
+        so += k8_digits<K8_MAXD>(p.na, p.afd, p.as, o);
+        d += k8_digits<K8_MAXD>(p.nb, p.bfd, p.bs, o);
+        v[u] = ld_stream<VB>(src + swz(p.ssw, so));
+        dof[u] = d;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t i = base + u * K1_THREADS;
+      if (i < total)
+        for (int r = 0; r < p.nrep; r++) st_vec<VB>(dst + swz(p.dsw, dof[u] + p.rep[r]), v[u]);
+    }
+  }
+}
+
+template <int VB>
+static cudaError_t k8_launch(const K8Params &p, const uint8_t *s, uint8_t *d, cudaStream_t st) {
+  constexpr int U = VB >= 8 ? 4 : 8;
+  const void *kern = (const void *)k8_dual<VB, U>;
+  const unsigned want = p.chunked ? p.nitems
+                                  : (unsigned)((p.total + (uint64_t)K1_THREADS * U - 1) / ((uint64_t)K1_THREADS * U));
+  const unsigned blocks = one_wave(kern, K1_THREADS, 0, std::max(1u, want));
+  return launch_ex(k8_dual<VB, U>, dim3(blocks), dim3(K1_THREADS), 0, st, p, s, d);
+}
+
+int k8_chunk(int vb) { return K1_THREADS * (vb >= 8 ? 4 : 8); }
+
+cudaError_t launch_k8(const K8Params &p, int vb, const void *src, void *dst, cudaStream_t st) {
+  const uint8_t *s = (const uint8_t *)src;
+  uint8_t *d = (uint8_t *)dst;
+  cudaError_t e;
+  switch (vb) {
+    case 1: e = k8_launch<1>(p, s, d, st); break;
+    case 2: e = k8_launch<2>(p, s, d, st); break;
+    case 4: e = k8_launch<4>(p, s, d, st); break;
+    case 8: e = k8_launch<8>(p, s, d, st); break;
+    case 16: e = k8_launch<16>(p, s, d, st); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
+  g_launches++;
+  return cudaGetLastError();
 }
 
 template <int VB>

@@ -87,6 +87,36 @@ struct K1Params {
   int dep;           // 1: wait for the previous kernel in the stream (griddepcontrol.wait)
 };
 
+// ---------------------------------------------------------------- K8 dual decoding
+// Layout pairs whose digit systems do not nest (no joint refinement, the gcd = 1 failure of Alg. 1,
+// P:978): the innermost digits still refine jointly (joint_refine_partial, down to the gcd of the
+// first non-nesting pair), and the outer index o = x / G is decoded twice -- once per side.  Vector i
+// of the grid = (o, w): w indexes the vectors of one inner block (K1's inner digits, the shared
+// contiguous run as the vector), o the block; a warp's lanes take consecutive vectors, so runs stay
+// coalesced on both sides.
+constexpr int K8_MAXD = 12;
+struct K8Params {
+  uint32_t total;              // vectors
+  FastDiv vin;                 // vectors per inner block
+  int nin;                     // inner digits (vector digit excluded), outermost first
+  FastDiv ifd[K1_MAXD];
+  int64_t iss[K1_MAXD], ids[K1_MAXD];  // byte strides
+  int na, nb;                  // outer digits of the source / destination decoding, outermost first
+  FastDiv afd[K8_MAXD], bfd[K8_MAXD];
+  int64_t as[K8_MAXD], bs[K8_MAXD];    // byte strides
+  int64_t sbase, dbase;
+  int nrep;
+  int64_t rep[K1_MAXREP];
+  Swz ssw, dsw;
+  // chunked form (inner block = one run of vin >= K8_CHUNK vectors contiguous in vector units on both
+  // sides: iss[0] / ids[0] its byte strides): work item = (o, chunk of K8_CHUNK vectors of block o),
+  // the two outer decodings once per item instead of once per vector
+  int chunked;
+  uint32_t nitems;
+  FastDiv nchunks;
+  int dep;
+};
+
 // ---------------------------------------------------------------- K1-TMA
 // The paper's TMA lowering: every box is (rows x row bytes), whole
 // in shared memory; one side is addressed through a CUtensorMap (5-D, byte
@@ -183,29 +213,6 @@ struct K2Params {
   int dep;
 };
 
-// ---------------------------------------------------------------- K2T: TMA-staged transpose
-// The source box (H rows of 128 bytes along the source-contiguous digit) is
-// TMA-loaded with SWIZZLE_128B into an S-stage smem ring; the 8 warps gather
-// 16-byte destination vectors along the destination-contiguous digit (thread
-// lanes walk the 128-byte row, which the swizzle makes bank-conflict free) and
-// store them with st.global.v4.  Box loads need no registers, so many boxes
-// are in flight per SM.
-struct K2TParams {
-  uint32_t ntiles;
-  int nd;                      // tile-index digits, outermost first
-  FastDiv fd[TMA_MAXD];
-  int32_t cdim[TMA_MAXD];      // tensor-map dimension of the digit (1: rows, 2..4: outer dims)
-  int32_t cmul[TMA_MAXD];
-  int64_t dstride[TMA_MAXD];   // destination byte stride of the digit
-  int64_t dbase;
-  uint32_t W;                  // elements per box row (128 / es)
-  uint32_t H;                  // box rows
-  int64_t dcol;                // destination byte stride of the source-contiguous digit (one column)
-  int stages;
-  int nrep;
-  int64_t rep[K1_MAXREP];
-  int dep;
-};
 
 // ---------------------------------------------------------------- K3 movmatrix
 // Register-layout permute that is, on every 512-byte "warp row" of a register
@@ -293,9 +300,6 @@ struct K4Params {
   int nrep;
   int64_t rep[K1_MAXREP];
   Swz ssw, dsw;
-  uint32_t box_bytes;                  // bulk form: output bytes per box (total counts boxes)
-  int stages;                          // bulk form: ring stages (2..4), K boxes each
-  int threads;                         // bulk form: CTA size (128 or 256)
   int stcs;                            // vector form: streaming (evict-first) stores of the sums
   int dep;
 };

@@ -118,99 +118,6 @@ __global__ void AXE_K2_BOUNDS k2_tile(const __grid_constant__ K2Params p, const 
   }
 }
 
-// Double-buffered form (16-byte loads): the next tile's source vectors go straight to shared memory
-// with cp.async (no registers) while the current tile is gathered and stored.
-__device__ __forceinline__ void cp_async16(uint32_t saddr, const void *g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <int VD, int GB, int LJ>
-__global__ void AXE_K2_BOUNDS k2_tile_async(const __grid_constant__ K2Params p, const uint8_t *__restrict__ src,
-                                            uint8_t *__restrict__ dst) {
-  extern __shared__ __align__(128) uint8_t sm[];
-  using TD = typename K2Vec<VD>::T;
-  using TG = typename K2Vec<GB>::T;
-  constexpr int KG = VD / GB;
-  constexpr int NJ = LJ > 0 ? LJ : K2_MAXLJ;
-  const int t = threadIdx.x;
-  int32_t al, as, ad;
-  asm volatile("mov.b32 %0, %3;\n\tmov.b32 %1, %4;\n\tmov.b32 %2, %5;"
-               : "=r"(al), "=r"(as), "=r"(ad)
-               : "r"(p.A_l[t]), "r"(p.A_s[t]), "r"(p.A_d[t]));
-  const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(sm);
-  const uint32_t TB = p.tile_bytes;
-  auto bases = [&](uint32_t tile, int64_t &sb, int64_t &db) {
-    sb = p.sbase;
-    db = p.dbase;
-    uint32_t i = tile;
-#pragma unroll
-    for (int k = K1_MAXD - 1; k >= 1; k--) {
-      if (k >= p.nout) continue;
-      uint32_t q = fdiv(p.ofd[k], i);
-      uint32_t d = i - q * p.ofd[k].d;
-      i = q;
-      sb += (int64_t)d * p.oss[k];
-      db += (int64_t)d * p.ods[k];
-    }
-    if (p.nout > 0) {
-      sb += (int64_t)i * p.oss[0];
-      db += (int64_t)i * p.ods[0];
-    }
-  };
-  auto issue = [&](uint32_t tile, uint32_t buf) {
-    int64_t sb, db;
-    bases(tile, sb, db);
-#pragma unroll
-    for (int j = 0; j < NJ; j++)
-      if (LJ > 0 || j < p.lj)
-        cp_async16(sm0 + buf + swz32(p.smsw, (uint32_t)((j * K2_NT + t) * 16)), src + swz(p.ssw, sb + p.B_l[j] + al));
-    cp_commit();
-  };
-  if (p.dep) pdl_wait();
-  pdl_launch_dependents();
-  int s = 0;
-  uint32_t tile = blockIdx.x;
-  if (tile < p.ntiles) issue(tile, 0);
-  for (; tile < p.ntiles; tile += gridDim.x) {
-    const uint32_t next = tile + gridDim.x;
-    if (next < p.ntiles) {
-      issue(next, (uint32_t)(s ^ 1) * TB);
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    __syncthreads();
-    int64_t sb, db;
-    bases(tile, sb, db);
-    const uint8_t *smb = sm + (uint32_t)s * TB;
-    for (int j = 0; j < p.sj; j++) {
-      TD out;
-      TG *o = reinterpret_cast<TG *>(&out);
-      const uint32_t base = (uint32_t)(as + p.B_s[j]);
-#pragma unroll
-      for (int k = 0; k < KG; k++) o[k] = *reinterpret_cast<const TG *>(smb + swz32(p.smsw, base + p.C_s[k]));
-      const int64_t d = db + p.B_d[j] + ad;
-      for (int r = 0; r < p.nrep; r++) *reinterpret_cast<TD *>(dst + swz(p.dsw, d + p.rep[r])) = out;
-    }
-    __syncthreads();
-    s ^= 1;
-  }
-}
-
-template <int VD, int GB, int LJ>
-static cudaError_t k2_go_async(const K2Params &p, unsigned blocks, size_t smem, const void *s, void *d,
-                               cudaStream_t st) {
-  const cudaError_t e = smem_attr((const void *)k2_tile_async<VD, GB, LJ>, 200 * 1024);
-  if (e != cudaSuccess) return e;
-  return launch_ex(k2_tile_async<VD, GB, LJ>, dim3(blocks), dim3(K2_NT), 2 * smem, st, p, (const uint8_t *)s,
-                   (uint8_t *)d);
-}
-
 template <int VS, int VD, int GB, int LJ>
 static cudaError_t k2_go_lj(const K2Params &p, unsigned blocks, size_t smem, const void *s, void *d, cudaStream_t st) {
   const cudaError_t e = smem_attr((const void *)k2_tile<VS, VD, GB, LJ>, 100 * 1024);
@@ -225,16 +132,6 @@ static cudaError_t k2_go(const K2Params &p, unsigned blocks, size_t smem, const 
     const char *e = getenv("AXE_K2_LJ");
     return !(e && *e == '0');
   }();
-  static const bool async = [] {
-    const char *e = getenv("AXE_K2_ASYNC");
-    return e && *e == '1';
-  }();
-  if constexpr (VS == 16) {
-    if (async) {
-      if (p.lj == 4) return k2_go_async<VD, GB, 4>(p, blocks, smem, s, d, st);
-      return k2_go_async<VD, GB, 0>(p, blocks, smem, s, d, st);
-    }
-  }
   if constexpr (VS == 16 && VD == 16) {  // the transposes: fixed load counts
     if (!lj_fixed) return k2_go_lj<VS, VD, GB, 0>(p, blocks, smem, s, d, st);
     // measured (8192^2 transposes): fixed LJ = 4 (fp32, 16 KiB tiles) 121 -> 104 us; fixed LJ = 8

@@ -319,79 +319,6 @@ __global__ void __launch_bounds__(K4_THREADS) k4_multimem(const __grid_constant_
   }
 }
 
-// Bulk form: output boxes contiguous on the destination and on every summand's slab.  One thread
-// issues the K cp.async.bulk loads of a box (one per summand) into a 2-stage ring; all threads then
-// sum the box from shared memory in k order (same arithmetic as k4_reduce) and store it.
-constexpr int K4B_THREADS = 256;  // launch bound; the plan picks 128 or 256
-template <int DT>
-__global__ void __launch_bounds__(K4B_THREADS) k4_bulk(const __grid_constant__ K4Params p,
-                                                       const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
-  using O = Op<DT>;
-  using S = typename O::S;
-  using A = typename O::A;
-  constexpr int V = 16 / (int)sizeof(S);
-  extern __shared__ __align__(128) uint8_t sm[];
-  __shared__ __align__(8) uint64_t full[4];
-  const int t = threadIdx.x;
-  const uint32_t B = p.box_bytes, K = (uint32_t)p.nk, stage = K * B;
-  const uint32_t NS = (uint32_t)p.stages;
-  if (t == 0) {
-    for (uint32_t s = 0; s < NS; s++) mbar_init(&full[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    fence_async_smem();
-  }
-  __syncthreads();
-  if (p.dep) pdl_wait();
-  pdl_launch_dependents();
-  const uint32_t nb = p.total, first = blockIdx.x, step = gridDim.x;
-  const uint32_t mine = first < nb ? (nb - first + step - 1) / step : 0;
-  auto offs = [&](uint32_t b, int64_t &so, int64_t &dof) {
-    so = p.sbase;
-    dof = p.dbase;
-    for (int k = p.nd - 1; k >= 0; k--) {
-      const uint32_t q = fdiv(p.fd[k], b);
-      const uint32_t d = b - q * p.fd[k].d;
-      b = q;
-      so += (int64_t)d * p.ss[k];
-      dof += (int64_t)d * p.ds[k];
-    }
-  };
-  auto issue = [&](uint32_t k) {
-    const uint32_t s = k % NS;
-    int64_t so, dof;
-    offs(first + k * step, so, dof);
-    mbar_expect_tx(&full[s], stage);
-    for (uint32_t kk = 0; kk < K; kk++) bulk_load(sm + s * stage + kk * B, src + so + p.koff[kk], B, &full[s]);
-  };
-  if (t == 0)
-    for (uint32_t k = 0; k < NS && k < mine; k++) issue(k);
-  for (uint32_t k = 0; k < mine; k++) {
-    const uint32_t s = k % NS;
-    mbar_wait(&full[s], (k / NS) & 1u);
-    int64_t so, dof;
-    offs(first + k * step, so, dof);
-    const uint8_t *base = sm + s * stage;
-    for (uint32_t v = t; v < B / 16; v += blockDim.x) {
-      A acc[V];
-#pragma unroll
-      for (int e = 0; e < V; e++) acc[e] = A(0);
-      for (uint32_t kk = 0; kk < K; kk++) {
-        alignas(16) S x[V];
-        *reinterpret_cast<uint4 *>(x) = *reinterpret_cast<const uint4 *>(base + kk * B + v * 16);
-#pragma unroll
-        for (int e = 0; e < V; e++) acc[e] = O::add(acc[e], O::in(x[e]));
-      }
-      alignas(16) S o[V];
-#pragma unroll
-      for (int e = 0; e < V; e++) o[e] = O::out(acc[e]);
-      for (int r = 0; r < p.nrep; r++)
-        *reinterpret_cast<uint4 *>(dst + dof + p.rep[r] + v * 16) = *reinterpret_cast<const uint4 *>(o);
-    }
-    __syncthreads();  // stage s consumed by every thread
-    if (t == 0 && k + NS < mine) issue(k + NS);
-  }
-}
-
 template <int DT>
 cudaError_t launch_k4p_dt(const K4Params &p, const K4Ptrs &q, int vb, unsigned blocks, uint8_t *d, cudaStream_t st) {
   constexpr int ES = (int)sizeof(typename Op<DT>::S);
@@ -424,27 +351,6 @@ cudaError_t launch_k4_peer(const K4Params &p, const K4Ptrs &q, int dtype, int vb
     case DT_BF16: e = launch_k4p_dt<DT_BF16>(p, q, vb, blocks, d, st); break;
     case DT_I32: e = launch_k4p_dt<DT_I32>(p, q, vb, blocks, d, st); break;
     case DT_I64: e = launch_k4p_dt<DT_I64>(p, q, vb, blocks, d, st); break;
-    default: return cudaErrorInvalidValue;
-  }
-  g_launches++;
-  return e != cudaSuccess ? e : cudaGetLastError();
-}
-
-cudaError_t launch_k4_bulk(const K4Params &p, int dtype, unsigned blocks, const void *src, void *dst,
-                           cudaStream_t st) {
-  const uint8_t *s = (const uint8_t *)src;
-  uint8_t *d = (uint8_t *)dst;
-  const size_t smem = (size_t)p.stages * p.nk * p.box_bytes;
-  const dim3 g(blocks), b(p.threads);
-  auto prep = [&](const void *kern) -> cudaError_t { return smem_attr(kern, 200 * 1024); };
-  cudaError_t e;
-  switch (dtype) {
-    case DT_F32: e = prep((const void *)k4_bulk<DT_F32>); if (e == cudaSuccess) e = launch_ex(k4_bulk<DT_F32>, g, b, smem, st, p, s, d); break;
-    case DT_F64: e = prep((const void *)k4_bulk<DT_F64>); if (e == cudaSuccess) e = launch_ex(k4_bulk<DT_F64>, g, b, smem, st, p, s, d); break;
-    case DT_F16: e = prep((const void *)k4_bulk<DT_F16>); if (e == cudaSuccess) e = launch_ex(k4_bulk<DT_F16>, g, b, smem, st, p, s, d); break;
-    case DT_BF16: e = prep((const void *)k4_bulk<DT_BF16>); if (e == cudaSuccess) e = launch_ex(k4_bulk<DT_BF16>, g, b, smem, st, p, s, d); break;
-    case DT_I32: e = prep((const void *)k4_bulk<DT_I32>); if (e == cudaSuccess) e = launch_ex(k4_bulk<DT_I32>, g, b, smem, st, p, s, d); break;
-    case DT_I64: e = prep((const void *)k4_bulk<DT_I64>); if (e == cudaSuccess) e = launch_ex(k4_bulk<DT_I64>, g, b, smem, st, p, s, d); break;
     default: return cudaErrorInvalidValue;
   }
   g_launches++;

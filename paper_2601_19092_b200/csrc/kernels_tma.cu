@@ -154,143 +154,6 @@ __global__ void __launch_bounds__(32) k1_tma(const __grid_constant__ CUtensorMap
   if (leader) bulk_wait_all();
 }
 
-// ------------------------------------------------------------------ K2T: TMA-staged transpose
-template <int ES>
-struct EsT;
-template <>
-struct EsT<2> { using T = uint16_t; };
-template <>
-struct EsT<4> { using T = uint32_t; };
-template <>
-struct EsT<8> { using T = uint2; };
-
-constexpr int K2T_THREADS = 256;
-
-template <int ES>
-__global__ void __launch_bounds__(K2T_THREADS) k2t_transpose(const __grid_constant__ CUtensorMap map,
-                                                             const __grid_constant__ K2TParams p,
-                                                             uint8_t *__restrict__ dst) {
-  using T = typename EsT<ES>::T;
-  constexpr int VD = 16 / ES;  // elements per destination vector
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full[TMA_MAX_STAGES];
-  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const int t = threadIdx.x;
-  const int S = p.stages;
-  const uint32_t B = p.H * 128u;
-  if (t == 0) {
-    for (int s = 0; s < S; s++) mbar_init(&full[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    fence_async_smem();
-  }
-  __syncthreads();
-  if (p.dep) pdl_wait();
-  pdl_launch_dependents();
-  const uint32_t nb = p.ntiles, first = blockIdx.x, step = gridDim.x;
-  const uint32_t mine = first < nb ? (nb - first + step - 1) / step : 0;
-  auto decode = [&](uint32_t b, int c[5], int64_t &doff) {
-#pragma unroll
-    for (int i = 0; i < 5; i++) c[i] = 0;
-    doff = p.dbase;
-#pragma unroll
-    for (int k = TMA_MAXD - 1; k >= 0; k--) {
-      if (k >= p.nd) continue;
-      uint32_t d;
-      if (k > 0) {
-        uint32_t q = fdiv(p.fd[k], b);
-        d = b - q * p.fd[k].d;
-        b = q;
-      } else {
-        d = b;
-      }
-#pragma unroll
-      for (int i = 0; i < 5; i++)
-        if (p.cdim[k] == i) c[i] += (int)d * p.cmul[k];
-      doff += (int64_t)d * p.dstride[k];
-    }
-  };
-  auto issue = [&](uint32_t k) {
-    const int s = (int)(k % (uint32_t)S);
-    int c[5];
-    int64_t unused;
-    decode(first + k * step, c, unused);
-    mbar_expect_tx(&full[s], B);
-    tma_load5(smem + (size_t)s * B, &map, &full[s], c[0], c[1], c[2], c[3], c[4]);
-  };
-  if (t == 0) {
-    const uint32_t pre = mine < (uint32_t)S ? mine : (uint32_t)S;
-    for (uint32_t k = 0; k < pre; k++) issue(k);
-  }
-  const uint32_t W = p.W;
-  const uint32_t QN = p.H / VD;  // destination vectors per column of a box
-  const uint32_t nvec = W * QN;
-  for (uint32_t k = 0; k < mine; k++) {
-    const int s = (int)(k % (uint32_t)S);
-    mbar_wait(&full[s], (k / (uint32_t)S) & 1u);
-    int c5[5];
-    int64_t db;
-    decode(first + k * step, c5, db);
-    const uint8_t *box = smem + (size_t)s * B;
-    for (uint32_t v = t; v < nvec; v += K2T_THREADS) {
-      // consecutive lanes take consecutive destination vectors of one column (coalesced stores);
-      // lane q reads its rows in an order rotated by q, so in every load instruction the lanes hit
-      // rows with different (r mod 8) -- different 16-byte chunks of the SWIZZLE_128B image
-      const uint32_t q = v % QN, col = v / QN;
-      const uint32_t cb = col * ES;
-      const uint32_t rot = q % VD;
-      uint4 reg;
-      T *o = reinterpret_cast<T *>(&reg);
-#pragma unroll
-      for (int i = 0; i < VD; i++) {
-        const uint32_t j = (i + rot) % VD;
-        const uint32_t r = q * VD + j;
-        o[i] = *reinterpret_cast<const T *>(box + r * 128u + ((((cb >> 4) ^ (r & 7u)) << 4) | (cb & 15u)));
-      }
-      // reg holds element (i + rot) at slot i: rotate the 16 bytes up by rot * ES bytes
-      const uint32_t b = rot * ES, kw = b >> 2, m = b & 3;
-      const uint32_t w[4] = {reg.x, reg.y, reg.z, reg.w};
-      uint32_t hi[4], lo[4];
-#pragma unroll
-      for (int i = 0; i < 4; i++) {
-        const uint32_t a = (uint32_t)(i - (int)kw) & 3u, c = (uint32_t)(i - (int)kw - 1) & 3u;
-        hi[i] = a == 0 ? w[0] : a == 1 ? w[1] : a == 2 ? w[2] : w[3];
-        lo[i] = c == 0 ? w[0] : c == 1 ? w[1] : c == 2 ? w[2] : w[3];
-      }
-      uint4 out;
-      out.x = __funnelshift_l(lo[0], hi[0], 8 * m);
-      out.y = __funnelshift_l(lo[1], hi[1], 8 * m);
-      out.z = __funnelshift_l(lo[2], hi[2], 8 * m);
-      out.w = __funnelshift_l(lo[3], hi[3], 8 * m);
-      const int64_t d = db + (int64_t)col * p.dcol + (int64_t)q * 16;
-      for (int rr = 0; rr < p.nrep; rr++) *reinterpret_cast<uint4 *>(dst + d + p.rep[rr]) = out;
-    }
-    __syncthreads();  // every warp is done with stage s
-    if (t == 0 && k + S < mine) issue(k + S);
-  }
-}
-
-size_t k2t_smem_bytes(const K2TParams &p) { return (size_t)p.stages * p.H * 128 + 1024; }
-
-cudaError_t launch_k2t(const void *map128, const K2TParams &p, int es, unsigned blocks, void *dst, cudaStream_t st) {
-  cudaError_t attr_err = smem_attr((const void *)k2t_transpose<2>, 200 * 1024);
-  if (attr_err == cudaSuccess) attr_err = smem_attr((const void *)k2t_transpose<4>, 200 * 1024);
-  if (attr_err == cudaSuccess) attr_err = smem_attr((const void *)k2t_transpose<8>, 200 * 1024);
-  if (attr_err != cudaSuccess) return attr_err;
-  CUtensorMap m;
-  memcpy(&m, map128, sizeof(m));
-  cudaError_t e;
-  const size_t sm = k2t_smem_bytes(p);
-  switch (es) {
-    case 2: e = launch_ex(k2t_transpose<2>, dim3(blocks), dim3(K2T_THREADS), sm, st, m, p, (uint8_t *)dst); break;
-    case 4: e = launch_ex(k2t_transpose<4>, dim3(blocks), dim3(K2T_THREADS), sm, st, m, p, (uint8_t *)dst); break;
-    case 8: e = launch_ex(k2t_transpose<8>, dim3(blocks), dim3(K2T_THREADS), sm, st, m, p, (uint8_t *)dst); break;
-    default: return cudaErrorInvalidValue;
-  }
-  if (e != cudaSuccess) return e;
-  g_launches++;
-  return cudaGetLastError();
-}
-
 // The lowered TMA region (tma_region.cpp): a persistent grid (one CTA of one issuing thread per SM by
 // default), each CTA owning a contiguous range of boxes and a deep ring of 1 KiB-aligned slots that
 // fills its shared memory (config 2: 28 slots of 8 KiB -- the SM's whole share of the 4096 boxes is

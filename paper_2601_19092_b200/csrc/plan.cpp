@@ -216,10 +216,10 @@ static int env_kernel() {
   if (!strcmp(e, "tma")) return AXE_KERNEL_TMA;
   if (!strcmp(e, "tile")) return AXE_KERNEL_TILE;
   if (!strcmp(e, "register")) return AXE_KERNEL_REGISTER;
-  if (!strcmp(e, "tma_tile")) return AXE_KERNEL_TMA_TILE;
   if (!strcmp(e, "shuffle")) return AXE_KERNEL_SHUFFLE;
   if (!strcmp(e, "transpose")) return AXE_KERNEL_TRANSPOSE;
   if (!strcmp(e, "lowered")) return AXE_KERNEL_LOWERED;
+  if (!strcmp(e, "dual")) return AXE_KERNEL_DUAL;
   return AXE_KERNEL_AUTO;
 }
 
@@ -536,26 +536,13 @@ static bool build_tma(const std::vector<Joint> &J0, const Linear &ls, const Line
   P->tm_dims[1] = (uint64_t)E1;
   P->tm_strides[0] = (uint64_t)(t1 * es);
   P->tm_box[1] = (uint32_t)B1;
-  // opt-in (AXE_TMA_BOX_MAX_BYTES): a box may span several whole (B1 x row) blocks of the next digit
-  // when they are consecutive on the bulk side (config 2: adjacent 64 x 64 tiles, 8 KiB apart).  16 KiB
-  // boxes: config 2 10.01 us vs 10.16, reverse 10.16 vs 10.48, but 16384^2 188 us vs 178 (6 CTAs/SM
-  // instead of 8), so the default keeps one block per box
-  const int64_t box_max = env_int("AXE_TMA_BOX_MAX_BYTES", 0);
   for (size_t i = 2; i < d.size(); i++) {
     if (dim > 4) return fail("tma: more than 5 tensor dimensions");
     if ((d[i].t * es) % 16) return fail("tma: outer stride not a multiple of 16 bytes");
-    int64_t k = 1;
-    if (i == 2 && d[i].b * es == box_bytes && E1 == B1)
-      for (int64_t c = std::min<int64_t>(d[i].e, 256); c > 1; c--)
-        if (d[i].e % c == 0 && c * box_bytes <= box_max) {
-          k = c;
-          break;
-        }
     P->tm_dims[dim] = (uint64_t)d[i].e;
     P->tm_strides[dim - 1] = (uint64_t)(d[i].t * es);
-    P->tm_box[dim] = (uint32_t)k;
-    if (d[i].e / k > 1) digs.push_back({d[i].e / k, dim, k, k * d[i].b * es});
-    box_bytes *= k;
+    P->tm_box[dim] = 1;
+    if (d[i].e > 1) digs.push_back({d[i].e, dim, 1, d[i].b * es});
     dim++;
   }
   for (int i = dim; i < 5; i++) P->tm_strides[i - 1] = P->tm_strides[dim - 2 > 0 ? dim - 2 : 0];
@@ -855,6 +842,8 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
   P.dst_bytes = rq.dstst->cells * es;
   P.align = es;
   int kernel = rq.kernel == AXE_KERNEL_AUTO ? env_kernel() : rq.kernel;
+  if (kernel == 6) AXE_FAIL(AXE_ERR_UNSUPPORTED, "kernel 6 (K2T) was retired: K7 / K2 run these transposes");
+  if (kernel < AXE_KERNEL_AUTO || kernel > AXE_KERNEL_DUAL) AXE_FAIL(AXE_ERR_INVALID_ARG, "unknown kernel %d", kernel);
 
   Linear ls, ld;
   bool lin = compose_linear(S, *rq.sst, rq.skip_axis, &ls) && compose_linear(D, *rq.dstst, rq.skip_axis, &ld);
@@ -941,14 +930,6 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
     if (kernel == AXE_KERNEL_TRANSPOSE)
       AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced transpose kernel cannot run these layouts: %s", w7.c_str());
   }
-  if (joint && kernel == AXE_KERNEL_TMA_TILE) {
-    if (build_k2t(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &why)) {
-      P.kernel = KK_TMA_TILE;
-      *out = std::move(P);
-      return AXE_OK;
-    }
-    AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced tma_tile kernel cannot run these layouts: %s", why.c_str());
-  }
   if (joint && kernel == AXE_KERNEL_TILE) {
     if (build_k2(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &why)) {
       P.kernel = KK_TILE;
@@ -963,7 +944,6 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
       // vectors of <= 4 bytes (or scattered sectors): stage through shared memory instead (K2), which
       // moves 16-byte vectors on both sides (config 3a: K1 4-byte 1583 us, K2 1547 us on B200)
       if (kernel == AXE_KERNEL_AUTO && P.vb < 16 && (P.vb <= 4 || P.k1_sector_eff < 0.5)) {
-        // (K2T, the TMA-staged variant, stays opt-in: measured slower than K2 on B200 in round 1)
         CopyPlan T = P;
         std::string w2;
         if (build_k2(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &T, &w2)) {
@@ -978,6 +958,18 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
     if (kernel != AXE_KERNEL_AUTO)
       AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced kernel cannot run these layouts: %s", why.c_str());
   }
+  // K8: the digit systems do not nest -- the shared innermost run still vectorises, the outer index is
+  // decoded once per side (measured against K0 in profiles/r02_k8_dual.json)
+  if (lin && !joint && (kernel == AXE_KERNEL_AUTO || kernel == AXE_KERNEL_DUAL)) {
+    std::string w8;
+    if (build_k8(ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &w8)) {
+      P.kernel = KK_DUAL;
+      *out = std::move(P);
+      return AXE_OK;
+    }
+    if (kernel == AXE_KERNEL_DUAL) AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced dual kernel cannot run these layouts: %s", w8.c_str());
+  }
+  if (kernel == AXE_KERNEL_DUAL) AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced dual kernel: %s", why.c_str());
   // K0 generic
   memset(&P.k0, 0, sizeof(P.k0));
   AXE_TRY(build_k0_side(S, *rq.sst, rq.skip_axis, &P.k0.src));
@@ -1118,6 +1110,12 @@ axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t 
       e = launch_k1(k, p.vb, p.blocks, src, dst, st);
       break;
     }
+    case KK_DUAL: {
+      K8Params k = p.k8;
+      k.dep = dep;
+      e = launch_k8(k, p.vb, src, dst, st);
+      break;
+    }
     case KK_GENERIC: {
       K0Params k = p.k0;
       k.dep = dep;
@@ -1148,14 +1146,6 @@ axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t 
       K2Params k = p.k2;
       k.dep = dep;
       e = launch_k2(k, p.k2_vs, p.k2_vd, p.k2_gb, p.blocks, src, dst, st);
-      break;
-    }
-    case KK_TMA_TILE: {
-      std::array<uint64_t, 16> map;
-      AXE_TRY(tensor_map_for(p, src, &map));
-      K2TParams k = p.k2t;
-      k.dep = dep;
-      e = launch_k2t(map.data(), k, p.es, p.blocks, dst, st);
       break;
     }
     case KK_TMA: {

@@ -13,7 +13,7 @@
 
 namespace axe {
 
-enum KernelKind { KK_GENERIC = 1, KK_VECTOR = 2, KK_TMA = 3, KK_TILE = 4, KK_REGISTER = 5, KK_TMA_TILE = 6, KK_SHUFFLE = 7, KK_TRANSPOSE = 8, KK_LOWERED = 9 };
+enum KernelKind { KK_GENERIC = 1, KK_VECTOR = 2, KK_TMA = 3, KK_TILE = 4, KK_REGISTER = 5, KK_SHUFFLE = 7, KK_TRANSPOSE = 8, KK_LOWERED = 9, KK_DUAL = 10 };
 
 struct CopyPlan {
   int kernel = KK_GENERIC;
@@ -46,8 +46,8 @@ struct CopyPlan {
   K6Params k6;
   // K7 register-block transpose
   K7Params k7;
-  // K2T TMA-staged transpose (uses the tm_* tensor map of the source)
-  K2TParams k2t;
+  // K8 dual decoding (non-nested digit systems)
+  K8Params k8;
   // the paper's TMA lowering as the schedule (tma_region.cpp): plan + destination byte offset of L_S
   std::shared_ptr<axe_tma_plan> lowered;
   int64_t lowered_dst_off = 0;  // byte offset of the L_S image (the destination, or the source when storing)
@@ -82,10 +82,9 @@ cudaError_t launch_k6(const K6Params &p, unsigned blocks, const void *src, void 
 bool build_k7(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,
               const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why);
 cudaError_t launch_k7(const K7Params &p, int es, unsigned blocks, const void *src, void *dst, cudaStream_t st);  // K3 as K1-TMA mode 2 + movmatrix in smem
-bool build_k2t(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,
-               const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why);
-cudaError_t launch_k2t(const void *map128, const K2TParams &p, int es, unsigned blocks, void *dst, cudaStream_t st);
-size_t k2t_smem_bytes(const K2TParams &p);
+bool build_k8(const Linear &ls, const Linear &ld, const Storage &sst, const Storage &dstst, int es, int max_align,
+              CopyPlan *P, std::string *why);
+cudaError_t launch_k8(const K8Params &p, int vb, const void *src, void *dst, cudaStream_t st);
 
 bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,
               const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why);
@@ -144,7 +143,7 @@ Swz make_swz(const Storage &st);
 
 // ---- K4 reduction over the leading logical dimension (plan_reduce.cpp, kernels_reduce.cu)
 struct ReducePlan {
-  int kind = 0;          // 1: generic (k4_generic), 2: vector (k4_reduce), 3: bulk boxes (k4_bulk)
+  int kind = 0;          // 1: generic (k4_generic), 2: vector (k4_reduce)
   int dtype = 0, es = 0;
   int64_t K = 1;         // summands per output element
   int64_t src_bytes = 0, dst_bytes = 0;
@@ -161,8 +160,6 @@ axe_status run_reduce(const ReducePlan &p, const void *src, void *dst, cudaStrea
 cudaError_t launch_k4(const K4Params &p, int dtype, int vb, unsigned blocks, const void *src, void *dst,
                       cudaStream_t st);
 cudaError_t launch_k4g(const K4GParams &p, int dtype, const void *src, void *dst, cudaStream_t st);
-cudaError_t launch_k4_bulk(const K4Params &p, int dtype, unsigned blocks, const void *src, void *dst,
-                           cudaStream_t st);
 cudaError_t launch_k4_multimem(const K4Params &p, int dtype, unsigned blocks, const void *mc, void *dst,
                                cudaStream_t st);
 cudaError_t launch_k4_peer(const K4Params &p, const K4Ptrs &q, int dtype, int vb, unsigned blocks, void *dst,

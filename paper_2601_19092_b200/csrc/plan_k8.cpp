@@ -1,0 +1,136 @@
+// plan_k8.cpp -- planner of K8, the dual-decoding copy (kernels.cu k8_dual) for layout pairs whose digit
+// systems do not nest (SURVEY §7 hard part 3; Alg. 1's gcd = 1 failure, P:960-993 / P:978).
+//
+// joint_refine_partial gives the innermost joint digits (down to the gcd of the first non-nesting
+// pair: an aligned run of that many consecutive x lies inside one digit on both sides) and the two
+// remaining digit lists, which decode the outer index o = x / G independently.  The inner block is
+// vectorised exactly as K1 does (the shared contiguous run, <= 16 bytes, dividing every stride, base
+// and replica offset); the outer digits cost two fast-division chains per vector.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "plan.hpp"
+
+namespace axe {
+
+int k8_chunk(int vb);
+
+static bool env_chunked() {  // AXE_K8_CHUNKED=0: per-vector decoding only (tests compare both forms)
+  const char *e = getenv("AXE_K8_CHUNKED");
+  return !(e && *e == '0');
+}
+
+bool build_k8(const Linear &ls, const Linear &ld, const Storage &sst, const Storage &dstst, int es, int max_align,
+              CopyPlan *P, std::string *why) {
+  auto fail = [&](const std::string &m) {
+    *why = "dual: " + m;
+    return false;
+  };
+  std::vector<Joint> Jin;
+  std::vector<LinIter> A, B;
+  if (!joint_refine_partial(ls.D, ld.D, &Jin, &A, &B)) return fail("no common innermost digit (gcd 1)");
+  for (auto &j : Jin)
+    if (j.sdev || j.ddev) return fail("device-axis digits");
+  for (auto *L : {&A, &B})
+    for (auto &x : *L)
+      if (x.dev) return fail("device-axis digits");
+  if ((int)A.size() > K8_MAXD || (int)B.size() > K8_MAXD) return fail("too many outer digits");
+  // destination replicas (set semantics)
+  std::vector<int64_t> reps{0};
+  for (auto &r : ld.R) {
+    std::vector<int64_t> nx;
+    for (int64_t b : reps)
+      for (int64_t d = 0; d < r.e; d++) nx.push_back(b + d * r.s);
+    reps.swap(nx);
+    if (reps.size() > 4096) break;
+  }
+  std::sort(reps.begin(), reps.end());
+  reps.erase(std::unique(reps.begin(), reps.end()), reps.end());
+  if ((int)reps.size() > K1_MAXREP) return fail("too many destination replicas");
+  // vector width V (elements): K1's rule on the inner block, and every outer stride must be a multiple
+  int64_t V = 1;
+  const Joint in = Jin.back();
+  if (in.ss == 1 && in.ds == 1) {
+    std::vector<int64_t> all{ls.base, ld.base};
+    for (size_t k = 0; k + 1 < Jin.size(); k++) {
+      all.push_back(Jin[k].ss);
+      all.push_back(Jin[k].ds);
+    }
+    for (auto &x : A) all.push_back(x.s);
+    for (auto &x : B) all.push_back(x.s);
+    for (int64_t r : reps) all.push_back(r);
+    int64_t cap = std::min<int64_t>(16, max_align) / es;
+    if (sst.swz_b > 0) cap = std::min<int64_t>(cap, std::max<int64_t>(1, (int64_t(1) << sst.swz_m) / es));
+    if (dstst.swz_b > 0) cap = std::min<int64_t>(cap, std::max<int64_t>(1, (int64_t(1) << dstst.swz_m) / es));
+    for (int64_t v = 2; v <= cap; v *= 2) {
+      bool ok = in.e % v == 0;
+      for (int64_t x : all) ok = ok && x % v == 0;
+      if (ok) V = v;
+    }
+  }
+  std::vector<Joint> I;  // inner digits without the vector, outermost first
+  for (size_t k = 0; k + 1 < Jin.size(); k++)
+    if (Jin[k].e > 1) I.push_back(Jin[k]);
+  if (in.e / V > 1) I.push_back(Joint{in.e / V, in.ss * V, in.ds * V});
+  if ((int)I.size() > K1_MAXD) return fail("too many inner digits");
+  int64_t vin = 1, nout = 1;
+  for (auto &j : I) vin *= j.e;
+  for (auto &x : A) nout *= x.e;
+  int64_t nb = 1;
+  for (auto &x : B) nb *= x.e;
+  if (nb != nout) return fail("outer decodings of different sizes");
+  if (vin * nout >= (int64_t(1) << 31)) return fail("2^31 or more vectors");
+  K8Params &k = P->k8;
+  memset(&k, 0, sizeof(k));
+  k.total = (uint32_t)(vin * nout);
+  k.vin = make_fastdiv((uint32_t)vin);
+  k.nin = (int)I.size();
+  for (size_t i = 0; i < I.size(); i++) {
+    k.ifd[i] = make_fastdiv((uint32_t)I[i].e);
+    k.iss[i] = I[i].ss * es;
+    k.ids[i] = I[i].ds * es;
+  }
+  k.na = (int)A.size();
+  for (size_t i = 0; i < A.size(); i++) {
+    k.afd[i] = make_fastdiv((uint32_t)A[i].e);
+    k.as[i] = A[i].s * es;
+  }
+  k.nb = (int)B.size();
+  for (size_t i = 0; i < B.size(); i++) {
+    k.bfd[i] = make_fastdiv((uint32_t)B[i].e);
+    k.bs[i] = B[i].s * es;
+  }
+  k.sbase = ls.base * es;
+  k.dbase = ld.base * es;
+  k.nrep = (int)reps.size();
+  for (size_t i = 0; i < reps.size(); i++) k.rep[i] = reps[i] * es;
+  k.ssw = make_swz(sst);
+  k.dsw = make_swz(dstst);
+  P->vb = (int)(V * es);
+  // chunked form: the inner block is one run (a single digit) of at least one vector per thread
+  const int64_t CH = k8_chunk(P->vb);
+  if (I.size() == 1 && vin >= CH / (P->vb >= 8 ? 4 : 8) && env_chunked()) {  // >= one vector per thread
+    const int64_t nch = (vin + CH - 1) / CH;
+    if (nch * nout < (int64_t(1) << 31)) {
+      k.chunked = 1;
+      k.nchunks = make_fastdiv((uint32_t)nch);
+      k.nitems = (uint32_t)(nch * nout);
+    }
+  }
+  P->align = std::max(P->align, P->vb);
+  P->covers_all = (int64_t)reps.size() * vin * nout * V == dstst.cells;
+  auto lin_json = [](const std::vector<LinIter> &L) {
+    std::string s = "[";
+    for (size_t i = 0; i < L.size(); i++)
+      s += (i ? "," : "") + std::string("[") + std::to_string(L[i].e) + "," + std::to_string(L[i].s) + "]";
+    return s + "]";
+  };
+  P->desc = "{\"kernel\":\"dual\",\"chunked\":" + std::to_string(k.chunked) + ",\"vec_bytes\":" + std::to_string(P->vb) + ",\"vectors\":" +
+            std::to_string(k.total) + ",\"inner_block_vectors\":" + std::to_string(vin) +
+            ",\"outer_blocks\":" + std::to_string(nout) + ",\"replicas\":" + std::to_string(reps.size()) +
+            ",\"inner\":" + joint_json(Jin) + ",\"outer_src\":" + lin_json(A) + ",\"outer_dst\":" + lin_json(B) + "}";
+  return true;
+}
+
+}  // namespace axe

@@ -114,47 +114,11 @@ axe_status plan_reduce(const Layout &S, const Storage &sst, const Layout &D, con
         if (ok) V = v;
       }
     }
-    // bulk form (k4_bulk): the innermost output run, contiguous on both sides, cut into boxes of
-    // box_bytes moved by cp.async.bulk per summand; every other output digit moves whole boxes
-    std::vector<Joint> Yb;
-    int64_t box = 0;
-    {
-      // opt-in (AXE_K4_BULK_BOX=4096): in the rotating steady state (perf_configs --reduce) K = 8 runs
-      // 1-3% faster than k4_reduce, but one cold launch under ncu takes 100.5 us against 86.7 us --
-      // 3 CTAs x 4 warps per SM keep less in flight than k4_reduce's 64 warps x 8 loads
-      const int64_t bb = env_int_r("AXE_K4_BULK_BOX", 0);
-      const bool table = P.K <= K4_MAXK, nosw = !sst.swz_b && !dstst.swz_b;
-      // K = 8 bf16 / f32 (8192 x 4096 outputs): 93.8-94.1 / 92.6 us vs 95.1-96.6 / 95.2 with k4_reduce;
-      // K = 16 (4096^2): 82.0 vs 81.5; K = 4 (16384 x 4096): 109.3 vs 105.2; K = 2 (16384 x 8192): 148
-      // vs 130 -- with few summands a 2-stage ring of K boxes keeps too little in flight per CTA
-      const int64_t min_k = env_int_r("AXE_K4_BULK_MIN_K", 8);
-      if (bb > 0 && P.K >= min_k && table && nosw && !Y.empty() && Y.back().ss == 1 && Y.back().ds == 1 &&
-          (Y.back().e * es) % bb == 0 && P.K * bb <= 48 * 1024 && bb % 16 == 0) {
-        const int64_t be = bb / es;
-        std::vector<int64_t> all{ls.base, ld.base};
-        for (size_t k = 0; k + 1 < Y.size(); k++) {
-          all.push_back(Y[k].ss);
-          all.push_back(Y[k].ds);
-        }
-        for (auto &j : Kd) all.push_back(j.ss);
-        for (int64_t r : reps) all.push_back(r);
-        bool ok = true;
-        for (int64_t a : all) ok = ok && (a * es) % 16 == 0;
-        if (ok) {
-          Yb.assign(Y.begin(), Y.end() - 1);
-          if (Y.back().e / be > 1) Yb.push_back(Joint{Y.back().e / be, be, be});
-          std::stable_sort(Yb.begin(), Yb.end(), [](const Joint &a, const Joint &b) { return std::llabs(a.ds) > std::llabs(b.ds); });
-          sort_fuse_outer(Yb);
-          box = bb;
-        }
-      }
-    }
     if (V > 1) {
       Joint last = Y.back();
       Y.pop_back();
       if (last.e / V > 1) Y.push_back(Joint{last.e / V, V, V});
     }
-    if (box) Y = Yb;  // the bulk form indexes boxes instead of vectors
     // destination-contiguous output digits first (every warp writes whole lines). Ordering by the
     // summand strides instead (every warp reads whole source runs) measured the same on a B200:
     // K = 8 bf16 into SW128 tiles 99.3-99.6 us either way, row-major rows 96.4-96.6
@@ -200,17 +164,10 @@ axe_status plan_reduce(const Layout &S, const Storage &sst, const Layout &D, con
           k.kss[t] = Kd[t].ss * es;
         }
       }
-      P.kind = box ? 3 : 2;
-      P.vb = box ? 16 : (int)(V * es);
+      P.kind = 2;
+      P.vb = (int)(V * es);
       P.align = P.vb;
-      k.box_bytes = (uint32_t)box;
-      if (box) {  // a ring of K boxes per stage per CTA
-        k.stages = (int)std::max<int64_t>(2, std::min<int64_t>(4, env_int_r("AXE_K4_BULK_STAGES", 2)));
-        k.threads = env_int_r("AXE_K4_BULK_THREADS", 128) > 128 ? 256 : 128;
-        const int64_t smem = k.stages * P.K * box + 1024;
-        const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(16, (220 * 1024) / smem));
-        P.blocks = (unsigned)std::max<int64_t>(1, std::min(total, (int64_t)num_sms() * per_sm));
-      } else {
+      {
         // streaming (st.global.cs) stores for 4- and 8-byte elements, measured on a B200 (perf_configs
         // --reduce, 2 runs each): f32 K = 8 (8192 x 2048) 88.4 us vs 94.9 plain; bf16 K = 8 96.9-97.1
         // vs 96.2 and into SW128 tiles 99.7-100.0 vs 99.7, so 2-byte elements keep plain stores
@@ -220,11 +177,9 @@ axe_status plan_reduce(const Layout &S, const Storage &sst, const Layout &D, con
       }
       char b[320];
       snprintf(b, sizeof b,
-               "{\"kernel\":\"reduce\",\"mode\":\"%s\",\"dtype\":\"%s\",\"K\":%lld,\"vec_bytes\":%d,\"%s\":%lld,"
-               "\"replicas\":%d,\"blocks\":%u,\"table\":%d,\"box_bytes\":%lld,\"stages\":%d,\"threads\":%d,"
-               "\"streaming_stores\":%d,\"digits\":",
-               box ? "bulk" : "vector", dtype_name(dtype), (long long)P.K, P.vb, box ? "boxes" : "vectors",
-               (long long)total, k.nrep, P.blocks, k.nk > 0, (long long)box, k.stages, k.threads, k.stcs);
+               "{\"kernel\":\"reduce\",\"mode\":\"vector\",\"dtype\":\"%s\",\"K\":%lld,\"vec_bytes\":%d,"
+               "\"vectors\":%lld,\"replicas\":%d,\"blocks\":%u,\"table\":%d,\"streaming_stores\":%d,\"digits\":",
+               dtype_name(dtype), (long long)P.K, P.vb, (long long)total, k.nrep, P.blocks, k.nk > 0, k.stcs);
       P.desc = std::string(b) + joint_json(Y) + ",\"reduce_digits\":" + joint_json(Kd) + "}";
       *out = std::move(P);
       return AXE_OK;
@@ -254,11 +209,7 @@ axe_status run_reduce(const ReducePlan &p, const void *src, void *dst, cudaStrea
   if (s < d + p.dst_bytes && d < s + p.src_bytes) AXE_FAIL(AXE_ERR_ALIAS, "source and destination buffers overlap");
   const int dep = stream_dependency(st, s, s + p.src_bytes, d, d + p.dst_bytes);
   cudaError_t e;
-  if (p.kind == 3) {
-    K4Params k = p.k4;
-    k.dep = dep;
-    e = launch_k4_bulk(k, p.dtype, p.blocks, src, dst, st);
-  } else if (p.kind == 2) {
+  if (p.kind == 2) {
     K4Params k = p.k4;
     k.dep = dep;
     e = launch_k4(k, p.dtype, p.vb, p.blocks, src, dst, st);

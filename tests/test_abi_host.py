@@ -175,6 +175,17 @@ def test_nonnested_falls_back_to_generic():
     assert d["kernel"] == "generic"
 
 
+def test_nonnested_with_common_factor_plans_dual():
+    """(6, 8) padded -> (4, 12) padded: innermost extents 8 and 12 do not nest but share 4 -- K8 keeps the
+    4-element run (8 bytes of 2-byte elements here) as its vector and decodes the outer index twice."""
+    src = layout([(6, 12), (8, 1)])
+    dst = layout([(4, 16), (12, 1)])
+    d = axe.CopyPlan(src, linear_storage(72), dst, linear_storage(64), 2).describe()
+    assert d["kernel"] == "dual" and d["vec_bytes"] == 8, d
+    assert d["inner"] == [[4, 1, 1]] and d["outer_blocks"] == 12, d
+    assert d["outer_src"] == [[6, 12], [2, 4]] and d["outer_dst"] == [[4, 16], [3, 4]], d
+
+
 def test_plan_errors():
     st = linear_storage(16)
     cases = [

@@ -87,20 +87,6 @@ def test_config2_full(axe, rev, kernel):
     assert desc["kernel"] == ("lowered" if kernel == "auto" else kernel)
 
 
-@pytest.mark.parametrize("rev", [False, True])
-@pytest.mark.parametrize("box_max,n,t,es,sw", [(16384, 512, 64, 2, synth.SW128), (32768, 1024, 64, 2, synth.SW128),
-                                               (16384, 256, 32, 4, synth.SW128), (65536, 512, 64, 1, synth.SW64)])
-def test_tma_boxes_spanning_adjacent_tiles(axe, monkeypatch, box_max, n, t, es, sw, rev):
-    """AXE_TMA_BOX_MAX_BYTES > one tile: a 3-D TMA box covers k adjacent destination tiles (consecutive on the
-    bulk side) -- box k along the tile-column digit, the remaining tile digits index boxes of k tiles."""
-    monkeypatch.setenv("AXE_TMA_BOX_MAX_BYTES", str(box_max))
-    cfg = synth.config2(n, t, es, sw, rev)
-    desc = check(axe, cfg, "tma", "tma")
-    tile = t * t * es
-    k = desc["tensor_map"]["box"][2]
-    assert k > 1 and desc["box_bytes"] == k * tile <= box_max
-
-
 @pytest.mark.parametrize("fuse", ["1", "0"])
 @pytest.mark.parametrize("n,t,es,sw", [(4096, 64, 2, synth.SW128), (1024, 64, 2, synth.SW128),
                                        (512, 32, 4, synth.SW128), (512, 64, 1, synth.SW64), (256, 16, 4, synth.SW64),
@@ -188,6 +174,46 @@ def test_config3_full_exhaustive(axe, variant):
     torch.cuda.empty_cache()
 
 
+def nonnested_pair(p, q, g, h, pad_s, pad_d, es, rev=False, reps=1, name="nn"):
+    """x in [0, p*q*g*h) read as (p*h, q*g) on the source (row pitch q*g + pad_s) and re-split as
+    (q*h, p*g) on the destination (row pitch p*g + pad_d): innermost extents q*g and p*g with
+    gcd(p, q) = 1 -- suffix products not nested except through their common factor g."""
+    A1, A2, B1, B2 = p * h, q * g, q * h, p * g
+    ls, ld = A2 + pad_s, B2 + pad_d
+    src = layout([(A1, ls), (A2, 1)])
+    if rev:   # the destination rows in reverse order (negative stride on the outer digit)
+        dst = layout([(B1, -ld), (B2, 1)], [(reps, B1 * ld)] if reps > 1 else [], {"m": (B1 - 1) * ld})
+    else:
+        dst = layout([(B1, ld), (B2, 1)], [(reps, B1 * ld)] if reps > 1 else [])
+    return dict(name=name, es=es, src=src, src_st=linear_storage(A1 * ls), dst=dst,
+                dst_st=linear_storage(reps * B1 * ld), seed=p * 100 + q * 10 + g)
+
+
+@pytest.mark.parametrize("p,q,g,h,pad_s,pad_d,es,rev,reps", [
+    (3, 2, 64, 8, 8, 16, 2, False, 1), (3, 2, 16, 5, 4, 8, 4, True, 1), (5, 3, 32, 3, 4, 4, 8, False, 2),
+    (7, 4, 2, 6, 1, 3, 2, False, 1), (3, 2, 8, 4, 2, 6, 16, True, 3), (2, 3, 128, 2, 64, 32, 1, False, 1),
+    (3, 2, 4096, 3, 64, 128, 2, False, 1), (5, 2, 2048, 2, 32, 16, 4, True, 2)])
+def test_dual_decoding_non_nested(axe, p, q, g, h, pad_s, pad_d, es, rev, reps):
+    """K8 on non-nested digit systems (re-pitching reshapes between padded buffers), against the oracle
+    and the generic kernel K0; AUTO picks K8 whenever the innermost extents share a factor (g >= 2; both
+    pitches padded, else one side is a single run and the pair nests).  g = 4096 / 2048: inner blocks of
+    >= 256 vectors, the chunked form (one outer decode per CTA chunk)."""
+    cfg = nonnested_pair(p, q, g, h, pad_s, pad_d, es, rev, reps)
+    d = check(axe, cfg, "auto")
+    assert d["kernel"] == "dual", d
+    check(axe, cfg, "generic")
+
+
+@pytest.mark.parametrize("chunked", ["1", "0"])
+def test_dual_decoding_large(axe, chunked, monkeypatch):
+    """The bench row's shape at a size that still checks quickly: (3*2^13, 2*2^7) blocks of 2^13 bf16 ->
+    (2*2^7, 3*2^13) with padded pitches, 16-byte vectors; the chunked form and the per-vector form."""
+    monkeypatch.setenv("AXE_K8_CHUNKED", chunked)
+    cfg = nonnested_pair(3, 2, 8192, 128, 64, 128, 2)
+    d = check(axe, cfg, "auto")
+    assert d["kernel"] == "dual" and d["vec_bytes"] == 16 and d["chunked"] == int(chunked), d
+
+
 def test_identity_and_transpose_reduce_to_torch(axe):
     """Special cases that reduce to library routines: identity = clone, row->column major = .t()."""
     R, Cn = 1000, 777
@@ -269,7 +295,7 @@ def test_random_layout_pairs(axe, seed):
                dst_st=linear_storage(dc, sw), seed=seed)
     check(axe, cfg, "auto")
     check(axe, cfg, "generic")
-    if axe.CopyPlan(src, cfg["src_st"], dst, cfg["dst_st"], es).describe()["kernel"] != "generic":
+    if axe.CopyPlan(src, cfg["src_st"], dst, cfg["dst_st"], es).describe()["kernel"] not in ("generic", "dual"):
         check(axe, cfg, "vector")
     try:
         axe.CopyPlan(src, cfg["src_st"], dst, cfg["dst_st"], es, "tile")
@@ -286,7 +312,7 @@ def test_transposes_all_kernels(axe, R, Cn, es):
                dst=layout([(R, 1), (Cn, R)]), dst_st=linear_storage(R * Cn), seed=R + es)
     for k in ("auto", "vector", "generic"):
         check(axe, cfg, k)
-    for k in ("tile", "tma_tile"):
+    for k in ("tile",):
         try:
             axe.CopyPlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], es, k)
         except axe.AxeError:
@@ -438,7 +464,7 @@ def test_random_permutes_reduce_to_numpy(axe, seed):
     dt = {1: np.uint8, 2: np.uint16, 4: np.uint32, 8: np.uint64}[es]
     v = synth.values(N, es, seed)
     expect = np.ascontiguousarray(v.view(dt).reshape(shape).transpose(perm)).reshape(-1)
-    for kernel in ("auto", "vector", "tile", "tma_tile", "generic"):
+    for kernel in ("auto", "vector", "tile", "generic"):
         try:
             plan = axe.CopyPlan(src, linear_storage(N), dst, linear_storage(N), es, kernel)
         except axe.AxeError:
@@ -592,7 +618,7 @@ def test_degenerate_sizes(axe, n, es):
     cfg = dict(name=f"tiny{n}x{es}", es=es, src=src, src_st=linear_storage(n), dst=dst,
                dst_st=linear_storage(2 * n + 3), seed=n * 16 + es)
     check(axe, cfg, "auto")
-    for k in ("generic", "vector", "tile", "tma", "register", "tma_tile"):
+    for k in ("generic", "vector", "tile", "tma", "register", "dual"):
         try:
             axe.CopyPlan(src, cfg["src_st"], dst, cfg["dst_st"], es, k)
         except axe.AxeError:

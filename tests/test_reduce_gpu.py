@@ -230,33 +230,6 @@ def test_replicas_and_offsets(axe):
     assert d["replicas"] == 2
 
 
-@pytest.mark.parametrize("K,box,dtype,rows,stages,threads", [
-    (4, 256, "bf16", 4096, 2, 128), (5, 4096, "f32", 8192, 3, 256), (8, 64, "f64", 1024, 4, 128),
-    (40, 1024, "i32", 1024, 2, 256), (4, 128, "f16", 2048, 3, 128), (9, 512, "i64", 2048, 4, 256)])
-def test_bulk_boxes(axe, monkeypatch, K, box, dtype, rows, stages, threads):
-    """k4_bulk: the contiguous output run cut into boxes of `box` bytes, K cp.async.bulk loads per box
-    (more than 2 x stages boxes per CTA, so every ring stage and the mbarrier phase flip are exercised)."""
-    monkeypatch.setenv("AXE_K4_BULK_BOX", str(box))
-    monkeypatch.setenv("AXE_K4_BULK_MIN_K", "1")
-    monkeypatch.setenv("AXE_K4_BULK_STAGES", str(stages))
-    monkeypatch.setenv("AXE_K4_BULK_THREADS", str(threads))
-    d = run_local(axe, synth.reduce_local(K, rows, 512, dtype), dtype, seed=K)
-    assert d["mode"] == "bulk" and d["box_bytes"] == box and d["stages"] == stages
-    assert d["boxes"] > 2 * stages * d["blocks"]
-
-
-def test_bulk_replicas_and_padded_rows(axe, monkeypatch):
-    """Bulk boxes inside padded rows (one box per row, row pitch > row) into two destination replicas."""
-    monkeypatch.setenv("AXE_K4_BULK_BOX", "256")
-    monkeypatch.setenv("AXE_K4_BULK_MIN_K", "1")
-    K, R, C, ld = 6, 64, 128, 160
-    src = layout([(K, R * ld), (R, ld), (C, 1)])
-    dst = layout([(R, C), (C, 1)], [(2, R * C)])
-    cfg = dict(src=src, src_st=linear_storage(K * R * ld), dst=dst, dst_st=linear_storage(2 * R * C))
-    d = run_local(axe, cfg, "bf16")
-    assert d["mode"] == "bulk" and d["replicas"] == 2 and d["boxes"] == R
-
-
 def test_generic_fallback(axe):
     """Digit systems that do not nest: the source is a column-major 30x7 matrix (K = 6 blocks of 35), the
     destination a 7x5 matrix with rows padded to 8 -- innermost extents 7 and 5 share no divisor -> k4_generic."""

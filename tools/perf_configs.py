@@ -27,7 +27,18 @@ def transpose_cfg(R, C, es):
                 dst_st=synth.linear_storage(R * C), seed=7)
 
 
+def nonnested_cfg(k=13, es=2):
+    """(3*2^k, 2*2^k) row pitch 2*2^k + 64 -> the same x re-split as (2*2^k, 3*2^k), pitch 3*2^k + 128:
+    innermost extents share only 2^k -- K8 dual decoding (K0 when forced generic)."""
+    p, q, g = 3, 2, 1 << k
+    A1, A2, B1, B2 = p * g, q * g, q * g, p * g
+    return dict(name=f"nonnested_3x2_k{k}", es=es, src=synth.layout([(A1, A2 + 64), (A2, 1)]),
+                src_st=synth.linear_storage(A1 * (A2 + 64)), dst=synth.layout([(B1, B2 + 128), (B2, 1)]),
+                dst_st=synth.linear_storage(B1 * (B2 + 128)), seed=9)
+
+
 CONFIGS = {
+    "nonnested_3x2": lambda: nonnested_cfg(13),
     "config2": lambda: synth.config2(),
     "config2r": lambda: synth.config2(reverse=True),
     "config2_16k": lambda: synth.config2(16384),
