@@ -161,6 +161,7 @@ struct TrParams {
   uint32_t stages;       // ring slots per CTA
   int dep;               // 1: griddepcontrol.wait before the first TMA
   int strided;           // 1: CTA c takes boxes c, c + grid, ... (0: a contiguous range per CTA)
+  uint32_t prefetch;     // boxes per CTA pulled into L2 before griddepcontrol.wait
   TmaReps reps;
 };
 

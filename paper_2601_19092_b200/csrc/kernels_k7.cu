@@ -134,7 +134,7 @@ __device__ __forceinline__ void cp_async16(uint8_t *s, const uint8_t *g) {
                : "memory");
 }
 
-template <int ES, int CW>
+template <int ES, int CW, int S>
 __global__ void __launch_bounds__(K7_THREADS) k7_transpose_async(const __grid_constant__ K7Params p,
                                                                  const uint8_t *__restrict__ src,
                                                                  uint8_t *__restrict__ dst) {
@@ -156,31 +156,46 @@ __global__ void __launch_bounds__(K7_THREADS) k7_transpose_async(const __grid_co
       cp_async16(buf + (r * CH + (c ^ ((r / N) & 7))) * 16, src + sb + (int64_t)r * p.src_row + c * 16);
     }
   };
+  // S-stage ring: tiles it + 1 .. it + S - 1 are in flight while tile it is gathered and stored
   uint32_t tile = blockIdx.x;
-  if (tile < p.ntiles) issue(tile, sm);
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  for (int it = 0; tile < p.ntiles; tile += gridDim.x, it++) {
-    const uint32_t next = tile + gridDim.x;
-    if (next < p.ntiles) issue(next, sm + ((it + 1) & 1) * TILE);
+#pragma unroll
+  for (int s = 0; s < S - 1; s++) {
+    const uint32_t tt = tile + (uint32_t)s * gridDim.x;
+    if (tt < p.ntiles) issue(tt, sm + s * TILE);
     asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_group 1;" ::: "memory");  // this thread's vectors of `tile` landed
-    __syncthreads();                                       // ... and every other thread's
+  }
+  for (int it = 0; tile < p.ntiles; tile += gridDim.x, it++) {
+    const uint32_t next = tile + (uint32_t)(S - 1) * gridDim.x;
+    if (next < p.ntiles) issue(next, sm + ((it + S - 1) % S) * TILE);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(S - 1) : "memory");  // this thread's vectors of `tile` landed
+    __syncthreads();                                                    // ... and every other thread's
     int64_t sb, db;
     tile_offsets(p, tile, sb, db);
-    k7_gather<ES, CW>(p, sm + (it & 1) * TILE, db, dst, lane, warp);
-    __syncthreads();  // buffer (it & 1) is refilled by the issue of the next iteration
+    k7_gather<ES, CW>(p, sm + (it % S) * TILE, db, dst, lane, warp);
+    __syncthreads();  // buffer it % S is refilled by a later iteration's issue
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+template <int ES, int CW, int S>
+cudaError_t go_async(const K7Params &p, unsigned blocks, size_t tile, const uint8_t *s, uint8_t *d, cudaStream_t st) {
+  const cudaError_t e = smem_attr((const void *)k7_transpose_async<ES, CW, S>, 200 * 1024);
+  if (e != cudaSuccess) return e;
+  return launch_ex(k7_transpose_async<ES, CW, S>, dim3(blocks), dim3(K7_THREADS), S * tile, st, p, s, d);
 }
 
 template <int ES, int CW>
 cudaError_t go(const K7Params &p, unsigned blocks, const uint8_t *s, uint8_t *d, cudaStream_t st) {
   constexpr int N = 16 / ES;
   const size_t tile = (size_t)32 * N * 8 * CW * 16;
-  cudaError_t e = smem_attr((const void *)k7_transpose<ES, CW>, 100 * 1024);
-  if (e == cudaSuccess) e = smem_attr((const void *)k7_transpose_async<ES, CW>, 200 * 1024);
+  if (p.async) {
+    if (p.async == 4) return go_async<ES, CW, 4>(p, blocks, tile, s, d, st);
+    if (p.async == 3) return go_async<ES, CW, 3>(p, blocks, tile, s, d, st);
+    return go_async<ES, CW, 2>(p, blocks, tile, s, d, st);
+  }
+  const cudaError_t e = smem_attr((const void *)k7_transpose<ES, CW>, 100 * 1024);
   if (e != cudaSuccess) return e;
-  if (p.async) return launch_ex(k7_transpose_async<ES, CW>, dim3(blocks), dim3(K7_THREADS), 2 * tile, st, p, s, d);
   return launch_ex(k7_transpose<ES, CW>, dim3(blocks), dim3(K7_THREADS), tile, st, p, s, d);
 }
 

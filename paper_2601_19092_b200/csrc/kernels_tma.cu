@@ -35,6 +35,16 @@ __device__ __forceinline__ void tma_load5(void *dst_smem, const CUtensorMap *map
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
       : "memory");
 }
+// L2 prefetches (no shared memory, no completion to wait for): pulling a box into L2 cannot return
+// stale data -- L2 is where every SM's writes land -- so they may run before griddepcontrol.wait
+__device__ __forceinline__ void tma_prefetch5(const CUtensorMap *map, int c0, int c1, int c2, int c3, int c4) {
+  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch(const void *p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void tma_store5(const CUtensorMap *map, const void *src_smem, int c0, int c1, int c2, int c3,
                                            int c4) {
   asm volatile(
@@ -214,7 +224,21 @@ __global__ void __launch_bounds__(32, 1) k_tma_region(const __grid_constant__ CU
   for (uint32_t s = 0; s < S; s++) mbar_init(&full[s], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("prefetch.tensormap [%0];" ::"l"(&map) : "memory");
-  if (p.dep) pdl_wait();
+  if (p.dep) {
+    // while the previous kernel drains: its first p.prefetch boxes into L2 (harmless if that kernel
+    // still writes them -- the loads after the wait read L2, which holds the latest data)
+    const uint32_t np = mine < p.prefetch ? mine : p.prefetch;
+    for (uint32_t k = 0; k < np; k++) {
+      int c[5];
+      int64_t off;
+      tr_box(p, lo + k * bstep, c, off);
+      if constexpr (STORE)
+        bulk_prefetch(p.img + off, box);
+      else
+        tma_prefetch5(&map, c[0], c[1], c[2], c[3], c[4]);
+    }
+    pdl_wait();
+  }
   pdl_launch_dependents();
   auto issue = [&](uint32_t k) {
     const uint32_t s = k % S;
@@ -292,11 +316,13 @@ int encode_tensor_map(void *out128, void *gaddr, const uint64_t dims[5], const u
   return (int)r;
 }
 
-// CTAs per SM of the lowered schedule (AXE_TMA_REGION_PER_SM, default 2: two rings filling the SM)
+// CTAs per SM of the lowered schedule (AXE_TMA_REGION_PER_SM, default 4: four rings sharing the SM -- a
+// next kernel's CTA starts on every quarter freed by this one and prefetches while it drains; config 2
+// 10.46 us vs 11.63 with 2 rings, 11.95 with 8, profiles/r02_lowered_prefetch_sweep.log)
 int tma_region_per_sm() {
   static const int v = [] {
     const char *e = getenv("AXE_TMA_REGION_PER_SM");
-    return (e && *e) ? std::max(1, std::min(8, atoi(e))) : 2;
+    return (e && *e) ? std::max(1, std::min(8, atoi(e))) : 4;
   }();
   return v;
 }
@@ -345,6 +371,11 @@ cudaError_t launch_tma_region(const void *map128, TrParams p, int store, cudaStr
     return (e && *e) ? atoi(e) : 1;
   }();
   p.strided = strided;
+  static const int prefetch = [] {  // AXE_TMA_REGION_PREFETCH: boxes per CTA prefetched before the wait
+    const char *e = getenv("AXE_TMA_REGION_PREFETCH");
+    return (e && *e) ? std::max(0, atoi(e)) : -1;  // -1: one ring's worth
+  }();
+  p.prefetch = prefetch < 0 ? p.stages : (uint32_t)prefetch;
   cudaError_t e = store ? launch_ex(k_tma_region<true>, dim3(blocks), dim3(32), smem, st, m, p)
                         : launch_ex(k_tma_region<false>, dim3(blocks), dim3(32), smem, st, m, p);
   if (e != cudaSuccess) return e;

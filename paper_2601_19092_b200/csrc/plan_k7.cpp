@@ -35,8 +35,10 @@ bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   // The cp.async double-buffered form (next tile in flight while the current one is stored): fp32
   // (cw 2) 93.3 us vs 95.8 register-staged (cw 4) / 101.7 (cw 2); bf16 (cw 2) 42.4 vs 42.9; fp64 (cw 4,
   // 64 x 64 tiles) 92.8 vs 94.5 register-staged (cw 2) / 94.6 (async, cw 2)
+  // async = cp.async ring stages (2..4; 0: register-staged)
   const char *ae = getenv("AXE_K7_ASYNC");
-  const int async = (ae && *ae) ? (atoi(ae) != 0) : 1;
+  int async = (ae && *ae) ? std::max(0, std::min(4, atoi(ae))) : 2;
+  if (async == 1) async = 2;  // (1 meant "double-buffered" before the ring depth was a knob)
   const char *cwe = getenv("AXE_K7_CW");
   const int cwmax = es == 2 ? 2 : 4;
   const int cwdef = async ? (es == 8 ? 4 : 2) : (es == 4 ? 4 : 2);
@@ -98,6 +100,8 @@ bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   k.src_row = B.ss * es;
   k.dst_col = A.ds * es;
   k.cw = (int)cw;
+  while (async > 2 && TR * TC * es * async > 200 * 1024) async--;  // the ring must fit in shared memory
+  if (async && TR * TC * es * async > 200 * 1024) return fail("transpose: tile ring exceeds shared memory");
   k.async = async;
   {  // opt-in streaming stores: no gain on a B200 (fp32 8192^2 93.9-94.1 us vs 93.3; fp64 93.7-94.0 vs 93.2)
     const char *se = getenv("AXE_K7_STCS");
@@ -106,7 +110,7 @@ bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   k.nrep = (int)reps.size();
   for (size_t i = 0; i < reps.size(); i++) k.rep[i] = reps[i] * es;
   P->align = 16;
-  const int64_t tile_bytes = TR * TC * es * (k.async ? 2 : 1);
+  const int64_t tile_bytes = TR * TC * es * (k.async ? k.async : 1);
   const int per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(8, (220 * 1024) / (tile_bytes + 1024)));
   P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt, (int64_t)num_sms() * per_sm));
   const char *mc = getenv("AXE_K7_MAX_CTAS");  // tests: several tiles per CTA on small inputs
