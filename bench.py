@@ -46,7 +46,8 @@ def peaks():
 
 
 def ncu_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu --set full capture."""
+    """DRAM bytes per launch of the dominant kernel in the steady state, from the committed ncu range capture
+    (tools/traffic_range.py: 32 back-to-back launches in one ncu app-range, read + write bytes / 32)."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:

@@ -321,11 +321,11 @@ def test_transposes_all_kernels(axe, R, Cn, es):
 
 
 @pytest.mark.parametrize("es,cw", [(2, 1), (2, 2), (4, 1), (4, 2), (4, 4), (8, 1), (8, 2), (8, 4)])
-@pytest.mark.parametrize("asyn", [0, 1])
+@pytest.mark.parametrize("asyn", [0, 2, 3])
 def test_k7_batched_padded_transposes(axe, monkeypatch, es, cw, asyn):
     """K7 directly: 3 batched transposes of (2 TR) x (3 TC) tiles, padded source rows and destination columns,
-    two destination replicas; every chunk width and both the register-staged and the cp.async
-    double-buffered form (several tiles per CTA, so both buffers are refilled)."""
+    two destination replicas; every chunk width, the register-staged form and the cp.async rings of 2 and 3
+    stages (several tiles per CTA, so every buffer is refilled)."""
     monkeypatch.setenv("AXE_K7_CW", str(cw))
     monkeypatch.setenv("AXE_K7_ASYNC", str(asyn))
     monkeypatch.setenv("AXE_K7_MAX_CTAS", "4")

@@ -59,6 +59,12 @@ CONFIGS = {
     "transpose_bf16": lambda: transpose_cfg(8192, 8192, 2),
     "transpose_f32": lambda: transpose_cfg(8192, 8192, 4),
     "transpose_f64": lambda: transpose_cfg(8192, 4096, 8),
+    # padded pitches (8192 + 32 elements on both sides): does the 32 KiB power-of-two stride matter?
+    "transpose_f32_pad": lambda: dict(name="transpose_f32_pad", es=4,
+                                      src=synth.layout([(8192, 8224), (8192, 1)]),
+                                      src_st=synth.linear_storage(8192 * 8224),
+                                      dst=synth.layout([(8192, 1), (8192, 8224)]),
+                                      dst_st=synth.linear_storage(8192 * 8224), seed=7),
 }
 
 
