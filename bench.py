@@ -171,6 +171,13 @@ def measure_reshard(axe, torch, dist, ws, rank, local, stream, iters=20, warm=3)
     ingress bytes / time (max over ranks), i.e. NCCL's busbw for all-gather / all-to-all."""
     comm = axe.Comm.from_process_group(local)
     res = {}
+    try:
+        ver = ".".join(str(x) for x in torch.cuda.nccl.version())
+    except Exception:
+        ver = None
+    # the communicator the reshard rows ran on (so a scaling run records that every rank joined)
+    res["nccl"] = {"version": ver, "nranks": comm.nranks, "rank0_device": torch.cuda.get_device_name(local),
+                   "NCCL_DEBUG": os.environ.get("NCCL_DEBUG")}
 
     def timed(fn):
         for _ in range(warm):
@@ -423,14 +430,24 @@ def run_axe(args):
     # the host's ctypes / launch path.  A short sleep kernel ahead of the start event keeps the
     # stream busy while the host submits the graph, so the region starts with the first copy.
     graph = None
+    in_graph_events = None
     if not args.no_graph:
         n_cap = axe.kernel_launch_count()
         graph = torch.cuda.CUDAGraph()
         cap_stream = torch.cuda.Stream()
         cap_stream.wait_stream(stream)
+        try:  # timing events recorded by the graph itself (event-record nodes) around exactly the K steps
+            in_graph_events = (torch.cuda.Event(enable_timing=True, external=True),
+                               torch.cuda.Event(enable_timing=True, external=True))
+        except TypeError:
+            in_graph_events = None
         with torch.cuda.graph(graph, stream=cap_stream):
+            if in_graph_events:
+                in_graph_events[0].record(torch.cuda.current_stream())
             for j in range(args.steps):
                 step(j, torch.cuda.current_stream())
+            if in_graph_events:
+                in_graph_events[1].record(torch.cuda.current_stream())
         assert axe.kernel_launch_count() - n_cap == args.steps, "one kernel per step"
         torch.cuda.synchronize()
 
@@ -456,9 +473,13 @@ def run_axe(args):
                 run_steps()
             torch.cuda.synchronize()
         barrier()
-        n0 = axe.kernel_launch_count()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda._sleep(2_000_000)  # ~1 ms of GPU time: the graph is queued before the region starts
+        # untimed warm-up copies on other buffer pairs right before the region (the GPU stays busy with
+        # memory traffic while the host enqueues the start event and the graph: no idle gap, no cold HBM)
+        # (pairs the first timed steps use are not among them, or were last touched >= 7 copies earlier)
+        for j in range(max(args.steps, pairs) - 16, max(args.steps, pairs)):
+            step(j)
+        n0 = axe.kernel_launch_count()
         ev0.record(stream)
         launches = run_steps()
         ev1.record(stream)
@@ -466,6 +487,9 @@ def run_axe(args):
         direct = axe.kernel_launch_count() - n0
         assert direct == (0 if graph is not None else args.steps)
         ms = ev0.elapsed_time(ev1)
+        ms_outer = ms
+        if in_graph_events:  # the graph's own event nodes: the K steps without the graph launch latency
+            ms = in_graph_events[0].elapsed_time(in_graph_events[1])
         # the same steps launched one by one from Python (ctypes + launch path on the host each step)
         torch.cuda._sleep(2_000_000)
         d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -538,7 +562,14 @@ def run_axe(args):
     if (ws > 1 or args.force_reshard) and not args.no_reshard:
         try:
             if dist is None:
+                import socket
                 import torch.distributed as dist
+                if "RANK" not in os.environ:  # --force-reshard at N = 1 without torchrun: a 1-rank group
+                    s = socket.socket()
+                    s.bind(("127.0.0.1", 0))
+                    os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
+                                      MASTER_PORT=str(s.getsockname()[1]))
+                    s.close()
                 dist.init_process_group("nccl", device_id=torch.device("cuda", local))
             reshard = measure_reshard(axe, torch, dist, ws, rank, local, stream)
         except Exception as e:  # keep the contract line even if the reshard leg fails
@@ -582,7 +613,10 @@ def run_axe(args):
                          "kernel_ms": k_ms, "isolated_launch_ms": iso_ms, "direct_launch_ms": direct_ms,
                          "host_us_per_call": host_us, "alg_bytes_per_launch": alg_bytes,
                          "pdl_overlap": os.environ.get("AXE_PDL_OVERLAP", "0") == "1",
-                         "timing": f"CUDA events around one replay of a graph of exactly {args.steps} launches"
+                         "graph_replay_ms_incl_launch": ms_outer if graph is not None else None,
+                         "timing": (f"CUDA event-record nodes inside one replayed graph of exactly {args.steps} launches"
+                                    if in_graph_events else
+                                    f"CUDA events around one replay of a graph of exactly {args.steps} launches")
                          if graph is not None else "CUDA events over the timed region / launches"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,

@@ -150,3 +150,69 @@ def test_one_sided_peer_stores(axe, mk):
     oracle.redistribute(cfg["src"], cfg["src_st"], src, cfg["dst"], cfg["dst_st"], exp, es, nthreads=NT)
     for r in range(n):
         assert np.array_equal(d_dev[r].cpu().numpy(), exp[r]), r
+
+
+def test_comm_wait_timeout_aborts(axe):
+    """axe_comm_wait: a stream still busy after the timeout aborts the communicator (AXE_ERR_TIMEOUT); every
+    later call on it fails with AXE_ERR_NCCL instead of hanging; a fresh communicator works."""
+    comm = axe.Comm(axe.get_unique_id(), 1, 0, torch.cuda.current_device())
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        torch.cuda._sleep(2_000_000_000)   # ~1 s of GPU time
+    with pytest.raises(axe.AxeError) as e:
+        comm.wait(st, timeout_ms=5)
+    assert e.value.name == "AXE_ERR_TIMEOUT"
+    R, Cn = 32, 16
+    src = layout([(R, Cn), (Cn, 1)])
+    dst = layout([(R, 1), (Cn, R)], [(1, 1, "gpuid")])
+    x = torch.zeros(R * Cn, dtype=torch.int32, device="cuda")
+    y = torch.zeros_like(x)
+    plan = axe.RedistPlan(src, linear_storage(R * Cn), dst, linear_storage(R * Cn), 4, 1, 0)
+    with pytest.raises(axe.AxeError) as e:
+        plan.execute(comm, x, y)
+    assert e.value.name == "AXE_ERR_NCCL"
+    st.synchronize()
+    del comm
+    comm2 = axe.Comm(axe.get_unique_id(), 1, 0, torch.cuda.current_device())
+    x.copy_(torch.arange(R * Cn, dtype=torch.int32, device="cuda"))
+    plan.execute(comm2, x, y)
+    comm2.wait(None, timeout_ms=60000)
+    assert torch.equal(y.view(Cn, R).t().reshape(-1), x)
+
+
+def test_plan_executes_serialised_across_streams_and_threads(axe):
+    """One redistribute plan (pack + NCCL + unpack through its own staging buffers) executed from two host
+    threads on two streams at once: the plan serialises them (host lock + device event chain), every
+    result is exact."""
+    import threading
+    comm = axe.Comm(axe.get_unique_id(), 1, 0, torch.cuda.current_device())
+    R, Cn = 256, 192
+    src = layout([(R, Cn), (Cn, 1)])
+    dst = layout([(R, 1), (Cn, R)], [(1, 1, "gpuid")])     # transposed: pack and unpack kernels
+    plan = axe.RedistPlan(src, linear_storage(R * Cn), dst, linear_storage(R * Cn), 4, 1, 0)
+    ins = [torch.randint(-2**31, 2**31 - 1, (R * Cn,), dtype=torch.int32, device="cuda") for _ in range(2)]
+    outs = [[torch.zeros_like(ins[0]) for _ in range(10)] for _ in range(2)]
+    torch.cuda.synchronize()
+    errors = []
+
+    def work(i):
+        try:
+            st = torch.cuda.Stream()
+            for j in range(10):
+                plan.execute(comm, ins[i], outs[i][j], st)
+            st.synchronize()
+        except Exception as e:
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errors, errors
+    for i in range(2):
+        exp = ins[i].view(R, Cn).t().reshape(-1)
+        for o in outs[i]:
+            assert torch.equal(o, exp)
+    del comm
