@@ -282,13 +282,24 @@ template <int VB, int U>
 __global__ void __launch_bounds__(K1_THREADS) k8_dual(const __grid_constant__ K8Params p, const uint8_t *__restrict__ src,
                                                       uint8_t *__restrict__ dst) {
   using T = typename VecT<VB>::T;
-  if (p.dep) pdl_wait();
-  pdl_launch_dependents();
+  if (p.dep && !p.chunked) pdl_wait();
   if (p.chunked) {
     // item = (o, c): vectors [c * CH, c * CH + CH) of block o, CH = K1_THREADS * U; the outer offsets are
     // uniform over the item (two decodings per item), the inner offset is w times the run's stride
     constexpr uint32_t CH = K1_THREADS * U;
     const uint32_t vin = p.vin.d;
+    if (p.dep && blockIdx.x < p.nitems) {  // the first item's vectors into L2 before the wait (R28)
+      const uint32_t o = fdiv(p.nchunks, blockIdx.x);
+      const uint32_t c = blockIdx.x - o * p.nchunks.d;
+      const int64_t so = p.sbase + k8_digits<K8_MAXD>(p.na, p.afd, p.as, o);
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const uint32_t w = c * CH + u * K1_THREADS + threadIdx.x;
+        if (w < vin && (w * VB) % 128 < VB) prefetch_l2(src + swz(p.ssw, so + (int64_t)w * p.iss[0]));
+      }
+    }
+    if (p.dep) pdl_wait();
+    pdl_launch_dependents();
     for (uint32_t it = blockIdx.x; it < p.nitems; it += gridDim.x) {
       const uint32_t o = fdiv(p.nchunks, it);
       const uint32_t c = it - o * p.nchunks.d;
@@ -309,6 +320,7 @@ __global__ void __launch_bounds__(K1_THREADS) k8_dual(const __grid_constant__ K8
     }
     return;
   }
+  pdl_launch_dependents();
   const uint32_t total = p.total;
   const uint32_t step = gridDim.x * (K1_THREADS * U);
   for (uint32_t base = blockIdx.x * (K1_THREADS * U) + threadIdx.x; base < total; base += step) {

@@ -145,7 +145,19 @@ __global__ void __launch_bounds__(K7_THREADS) k7_transpose_async(const __grid_co
   constexpr int TILE = TR * CH * 16;
   extern __shared__ __align__(128) uint8_t sm[];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  if (p.dep) pdl_wait();
+  if (p.dep) {
+    // while the previous kernel drains: the ring's first tiles into L2, one 128-byte line per thread and
+    // pass (R28)
+    for (int s = 0; s < S - 1; s++) {
+      const uint32_t tt = blockIdx.x + (uint32_t)s * gridDim.x;
+      if (tt >= p.ntiles) break;
+      int64_t sb, db;
+      tile_offsets(p, tt, sb, db);
+      for (int idx = t; idx < TR * (CH / 8); idx += K7_THREADS)
+        prefetch_l2(src + sb + (int64_t)(idx / (CH / 8)) * p.src_row + (idx % (CH / 8)) * 128);
+    }
+    pdl_wait();
+  }
   pdl_launch_dependents();
   auto issue = [&](uint32_t tile, uint8_t *buf) {
     int64_t sb, db;

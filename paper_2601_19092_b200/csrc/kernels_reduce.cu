@@ -124,7 +124,21 @@ __device__ __forceinline__ void k4_body(const K4Params &p, const uint64_t *kp, c
   using A = typename O::A;
   constexpr int VB = V * (int)sizeof(S);
   using R = typename RawT<VB>::T;
-  if (p.dep) pdl_wait();
+  if (p.dep) {
+    // while the previous kernel drains: this thread's first summands into L2 (R28)
+    const uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (!PEER && p.nk > 0 && i0 < p.total) {
+      int64_t so = p.sbase;
+      uint32_t rem = i0;
+      for (int k = p.nd - 1; k >= 0; k--) {
+        const uint32_t q = fdiv(p.fd[k], rem);
+        so += (int64_t)(rem - q * p.fd[k].d) * p.ss[k];
+        rem = q;
+      }
+      for (int k = 0; k < p.nk; k++) prefetch_l2(src + swz(p.ssw, so + p.koff[k]));
+    }
+    pdl_wait();
+  }
   pdl_launch_dependents();
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < p.total; i += stride) {

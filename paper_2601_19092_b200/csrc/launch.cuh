@@ -60,6 +60,9 @@ inline cudaError_t smem_attr(const void *kern, int bytes) {
 }
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// L2 prefetch of the line holding p (a hint: no data returns, nothing to wait for; issued before
+// griddepcontrol.wait it cannot observe stale data -- every SM's writes land in L2, R28)
+__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.L2 [%0];" ::"l"(p)); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
 inline bool pdl_enabled() {
