@@ -165,6 +165,13 @@ struct TrParams {
   TmaReps reps;
 };
 
+// K4T (kernels_reduce.cu k4_tma): the K summand tensor maps of a reduction into a TMA-swizzled destination
+// (one lowered-region map per summand, base = source + that summand's offset), 128 bytes each
+constexpr int K4T_MAXK = 8;
+struct K4TMaps {
+  alignas(64) unsigned char m[K4T_MAXK][128];
+};
+
 struct TmaParams {
   uint32_t nboxes;
   int nd;                      // box-index digits, outermost first

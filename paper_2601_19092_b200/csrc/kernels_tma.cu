@@ -27,24 +27,6 @@ namespace axe {
 
 extern std::atomic<int64_t> g_launches;
 
-__device__ __forceinline__ void tma_load5(void *dst_smem, const CUtensorMap *map, uint64_t *bar, int c0, int c1, int c2,
-                                          int c3, int c4) {
-  asm volatile(
-      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, "
-      "%7}], [%2];" ::"r"(smem_u32(dst_smem)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
-      : "memory");
-}
-// L2 prefetches (no shared memory, no completion to wait for): pulling a box into L2 cannot return
-// stale data -- L2 is where every SM's writes land -- so they may run before griddepcontrol.wait
-__device__ __forceinline__ void tma_prefetch5(const CUtensorMap *map, int c0, int c1, int c2, int c3, int c4) {
-  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(map), "r"(c0),
-               "r"(c1), "r"(c2), "r"(c3), "r"(c4)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_prefetch(const void *p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void tma_store5(const CUtensorMap *map, const void *src_smem, int c0, int c1, int c2, int c3,
                                            int c4) {
   asm volatile(
@@ -175,29 +157,6 @@ __global__ void __launch_bounds__(32) k1_tma(const __grid_constant__ CUtensorMap
 // mixed-radix program (no dependent global load before a TMA issue); the table is the fallback.
 constexpr int TR_STAGES = 32;  // ring capacity (slots per CTA)
 constexpr int TR_LAG = 2;      // a slot is refilled once the store two boxes back has read it
-
-__device__ __forceinline__ void tr_box(const TrParams &p, uint32_t b, int c[5], int64_t &off) {
-  if (p.prog.nd < 0) {
-    const TmaAtom a = p.atoms[b];
-#pragma unroll
-    for (int i = 0; i < 5; i++) c[i] = a.c[i];
-    off = a.off;
-    return;
-  }
-#pragma unroll
-  for (int i = 0; i < 5; i++) c[i] = p.prog.c0[i];
-  off = p.prog.off0;
-#pragma unroll
-  for (int k = 0; k < TR_MAXD; k++) {
-    if (k >= p.prog.nd) break;
-    const uint32_t q = fdiv(p.prog.fd[k], b);
-    const uint32_t d = b - q * p.prog.fd[k].d;
-    b = q;
-#pragma unroll
-    for (int i = 0; i < 5; i++) c[i] += (int)d * p.prog.dc[k][i];
-    off += (int64_t)d * p.prog.doff[k];
-  }
-}
 
 template <bool STORE>
 __global__ void __launch_bounds__(32, 1) k_tma_region(const __grid_constant__ CUtensorMap map,

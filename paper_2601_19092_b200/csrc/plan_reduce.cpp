@@ -93,6 +93,39 @@ axe_status plan_reduce(const Layout &S, const Storage &sst, const Layout &D, con
       if (j.e > 1) (j.ds == 0 ? Kd : Y).push_back(j);
     if ((int)Kd.size() > K4_MAXD) joint = false;
   }
+  if (joint && P.K > 1 && P.K <= K4T_MAXK && dstst.swz_b && env_int_r("AXE_K4_TMA", 1)) {
+    // K4T: the destination carries a TMA swizzle -- the paper's lowering of one summand slab into it
+    // (build_lowered on the output digits), K TMA loads per output box, the sum in shared memory
+    CopyPlan L;
+    std::string why;
+    if (build_lowered(Y, ls, ld, sst, dstst, es, &L, &why) && !L.lowered_store) {
+      std::vector<int64_t> koff;
+      for (int64_t kk = 0; kk < P.K; kk++) {
+        int64_t rem = kk, off = 0;
+        for (int t = (int)Kd.size() - 1; t >= 0; t--) {
+          off += (rem % Kd[t].e) * Kd[t].ss;
+          rem /= Kd[t].e;
+        }
+        koff.push_back(off * es);
+      }
+      bool ok = true;
+      for (int64_t o : koff) ok = ok && o % 16 == 0;
+      if (ok) {
+        P.kind = 3;
+        P.lowered = L.lowered;
+        P.lowered_dst_off = L.lowered_dst_off;
+        P.lowered_reps = L.lowered_reps;
+        P.koff_bytes = koff;
+        P.vb = 16;
+        P.align = 16;
+        P.desc = "{\"kernel\":\"reduce\",\"mode\":\"tma\",\"dtype\":\"" + std::string(dtype_name(dtype)) +
+                 "\",\"K\":" + std::to_string(P.K) + ",\"vec_bytes\":16,\"lowering\":" + L.desc +
+                 ",\"reduce_digits\":" + joint_json(Kd) + "}";
+        *out = std::move(P);
+        return AXE_OK;
+      }
+    }
+  }
   if (joint) {
     // vector width: a power of two V with V * es <= 16 dividing the innermost shared stride-1 run,
     // every other stride, both bases and every replica offset (as K1)
@@ -209,6 +242,9 @@ axe_status run_reduce(const ReducePlan &p, const void *src, void *dst, cudaStrea
   if (s < d + p.dst_bytes && d < s + p.src_bytes) AXE_FAIL(AXE_ERR_ALIAS, "source and destination buffers overlap");
   const int dep = stream_dependency(st, s, s + p.src_bytes, d, d + p.dst_bytes);
   cudaError_t e;
+  if (p.kind == 3)
+    return tma_run_reduce(p.lowered.get(), src, p.koff_bytes.data(), (int)p.K, (uint8_t *)dst + p.lowered_dst_off,
+                          p.lowered_reps, p.dtype, dep, st);
   if (p.kind == 2) {
     K4Params k = p.k4;
     k.dep = dep;

@@ -25,6 +25,7 @@ namespace axe {
 int encode_tensor_map(void *out128, void *gaddr, const uint64_t dims[5], const uint64_t strides[4],
                       const uint32_t box[5], int swizzle_bytes);
 cudaError_t launch_tma_region(const void *map128, TrParams p, int store, cudaStream_t st);
+cudaError_t launch_k4_tma(const K4TMaps &maps, TrParams p, int K, int dtype, cudaStream_t st);
 void stream_forget(cudaStream_t st);
 }  // namespace axe
 
@@ -128,6 +129,67 @@ static cudaError_t upload(axe_tma_plan *plan, int dev, TmaAtom **out) {
   return cudaSuccess;
 }
 
+// the plan's CuTensorMap for region start g (cached per pointer); plan->mu held
+static axe_status map_for(axe_tma_plan *plan, const uint8_t *g, std::array<unsigned char, 128> *map) {
+  auto it = plan->maps.find(g);
+  if (it != plan->maps.end()) {
+    *map = it->second;
+    return AXE_OK;
+  }
+  // uint8 elements: dim 0 in bytes, the other dims as lowered (byte strides)
+  uint64_t dims[5], strides[4];
+  uint32_t box[5];
+  const axe_tma_desc &d = plan->desc;
+  for (int i = 0; i < 5; i++) {
+    dims[i] = i < d.rank ? d.dims[i] : 1;
+    box[i] = i < d.rank ? d.box[i] : 1;
+  }
+  dims[0] *= (uint64_t)plan->es;
+  box[0] *= (uint32_t)plan->es;
+  if (plan->fuse > 1) box[plan->fuse_dim] = (uint32_t)plan->fuse;
+  uint64_t last = 16;  // unused trailing dims: extent 1, the last real stride
+  for (int i = 1; i < 5; i++) {
+    if (i < d.rank) last = d.strides[i];
+    strides[i - 1] = last;
+  }
+  alignas(64) unsigned char m[128];
+  const int r = encode_tensor_map(m, (void *)g, dims, strides, box, d.swizzle_bytes);
+  if (r != 0) AXE_FAIL(AXE_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", r);
+  memcpy(map->data(), m, 128);
+  if (plan->maps.size() >= 1024) plan->maps.clear();
+  plan->maps.emplace(g, *map);
+  return AXE_OK;
+}
+
+// launch parameters of a plan's region (the box program, or the table on the current device); plan->mu held
+static axe_status region_params(axe_tma_plan *plan, const void *s_image, cudaStream_t st, int dep, TrParams *p) {
+  memset(p, 0, sizeof(*p));
+  p->prog = plan->prog;
+  p->img = (uint8_t *)s_image;
+  p->n = (uint32_t)plan->host.size();
+  p->box = plan->box_bytes;
+  p->slot = (plan->box_bytes + 1023) & ~1023u;
+  p->dep = dep;
+  p->reps.n = 1;
+  if (p->prog.nd < 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "cudaGetDevice");
+    auto it = plan->tables.find(dev);
+    if (it != plan->tables.end()) {
+      p->atoms = it->second;
+    } else {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+        AXE_FAIL(AXE_ERR_CUDA, "the atom table is not on this device yet: execute once outside graph capture");
+      TmaAtom *t = nullptr;
+      const cudaError_t e = upload(plan, dev, &t);
+      if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "atom table: %s", cudaGetErrorString(e));
+      p->atoms = t;
+    }
+  }
+  return AXE_OK;
+}
+
 static axe_status tma_plan_run(axe_tma_plan *plan, const void *g_base, const void *s_image, void *stream, int dep,
                                int store, const TmaReps *reps = nullptr) {
   if (!plan || !g_base || !s_image) AXE_FAIL(AXE_ERR_INVALID_ARG, "NULL argument");
@@ -136,69 +198,44 @@ static axe_status tma_plan_run(axe_tma_plan *plan, const void *g_base, const voi
     AXE_FAIL(AXE_ERR_ALIGNMENT, "region start and image must be 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;
   TrParams p;
-  memset(&p, 0, sizeof(p));
-  p.prog = plan->prog;
-  p.img = (uint8_t *)s_image;
-  p.n = (uint32_t)plan->host.size();
-  p.box = plan->box_bytes;
-  p.slot = (plan->box_bytes + 1023) & ~1023u;
-  p.dep = dep;
-  if (reps) {
-    p.reps = *reps;
-  } else {
-    p.reps.n = 1;
-  }
   std::array<unsigned char, 128> map;
   {
     std::lock_guard<std::mutex> lk(plan->mu);
-    if (p.prog.nd < 0) {
-      int dev = 0;
-      if (cudaGetDevice(&dev) != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "cudaGetDevice");
-      auto it = plan->tables.find(dev);
-      if (it != plan->tables.end()) {
-        p.atoms = it->second;
-      } else {
-        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-        if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
-          AXE_FAIL(AXE_ERR_CUDA, "the atom table is not on this device yet: execute once outside graph capture");
-        TmaAtom *t = nullptr;
-        const cudaError_t e = upload(plan, dev, &t);
-        if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "atom table: %s", cudaGetErrorString(e));
-        p.atoms = t;
-      }
-    }
-    auto it = plan->maps.find(g);
-    if (it != plan->maps.end()) {
-      map = it->second;
-    } else {
-      // uint8 elements: dim 0 in bytes, the other dims as lowered (byte strides)
-      uint64_t dims[5], strides[4];
-      uint32_t box[5];
-      const axe_tma_desc &d = plan->desc;
-      for (int i = 0; i < 5; i++) {
-        dims[i] = i < d.rank ? d.dims[i] : 1;
-        box[i] = i < d.rank ? d.box[i] : 1;
-      }
-      dims[0] *= (uint64_t)plan->es;
-      box[0] *= (uint32_t)plan->es;
-      if (plan->fuse > 1) box[plan->fuse_dim] = (uint32_t)plan->fuse;
-      uint64_t last = 16;  // unused trailing dims: extent 1, the last real stride
-      for (int i = 1; i < 5; i++) {
-        if (i < d.rank) last = d.strides[i];
-        strides[i - 1] = last;
-      }
-      alignas(64) unsigned char m[128];
-      const int r = encode_tensor_map(m, (void *)g, dims, strides, box, d.swizzle_bytes);
-      if (r != 0) AXE_FAIL(AXE_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", r);
-      memcpy(map.data(), m, 128);
-      if (plan->maps.size() >= 1024) plan->maps.clear();
-      plan->maps.emplace(g, map);
-    }
+    AXE_TRY(region_params(plan, s_image, st, dep, &p));
+    if (reps) p.reps = *reps;
+    AXE_TRY(map_for(plan, g, &map));
   }
   const cudaError_t e = launch_tma_region(map.data(), p, store, st);
   if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "tma region launch: %s", cudaGetErrorString(e));
   return AXE_OK;
 }
+
+namespace axe {
+// K4T (plan_reduce.cpp): the reduction into a TMA-swizzled destination -- one map of the lowered region per
+// summand (base = src + koff[k]), K TMA loads per output box, sum in shared memory, bulk store
+axe_status tma_run_reduce(axe_tma_plan *plan, const void *src, const int64_t *koff, int K, void *img,
+                          const TmaReps &reps, int dtype, int dep, cudaStream_t st) {
+  if (K < 1 || K > K4T_MAXK) AXE_FAIL(AXE_ERR_UNSUPPORTED, "K4T: K = %d", K);
+  if ((uintptr_t)img % 16) AXE_FAIL(AXE_ERR_ALIGNMENT, "image must be 16-byte aligned");
+  TrParams p;
+  K4TMaps maps;
+  {
+    std::lock_guard<std::mutex> lk(plan->mu);
+    AXE_TRY(region_params(plan, img, st, dep, &p));
+    p.reps = reps;
+    for (int k = 0; k < K; k++) {
+      const uint8_t *g = (const uint8_t *)src + plan->desc.base_bytes + koff[k];
+      if ((uintptr_t)g % 16) AXE_FAIL(AXE_ERR_ALIGNMENT, "summand %d region start is not 16-byte aligned", k);
+      std::array<unsigned char, 128> m;
+      AXE_TRY(map_for(plan, g, &m));
+      memcpy(maps.m[k], m.data(), 128);
+    }
+  }
+  const cudaError_t e = launch_k4_tma(maps, p, K, dtype, st);
+  if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "K4T launch: %s", cudaGetErrorString(e));
+  return AXE_OK;
+}
+}  // namespace axe
 
 extern "C" {
 

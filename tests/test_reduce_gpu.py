@@ -180,6 +180,48 @@ def test_sum_into_swizzled_tiles(axe, dtype):
     assert d["kernel"] == "reduce" and d["vec_bytes"] == 16
 
 
+def tiled_reduce_cfg(K, rows, cols, dtype, reps=1):
+    """(K, rows, cols) row-major -> (rows, cols) in t x t tiles with the 128-byte swizzle, t = 128 bytes of
+    elements (one SW128 atom row per tile row), optionally `reps` destination replicas."""
+    es = synth.DTYPE_SIZE[dtype]
+    t = 128 // es
+    src = layout([(K, rows * cols), (rows, cols), (cols, 1)])
+    R = [(reps, rows * cols)] if reps > 1 else []
+    dst = layout([(rows // t, t * cols), (t, t), (cols // t, t * t), (t, 1)], R)
+    return dict(src=src, src_st=linear_storage(K * rows * cols), dst=dst,
+                dst_st=linear_storage(reps * rows * cols, synth.SW128))
+
+
+@pytest.mark.parametrize("K,dtype,reps", [(2, "bf16", 1), (3, "f16", 1), (5, "f32", 1), (8, "bf16", 2), (8, "f64", 1),
+                                          (4, "i32", 1), (6, "i64", 1), (7, "bf16", 1)])
+def test_k4t_tma_sum_into_swizzled_tiles(axe, K, dtype, reps):
+    """K4T: the paper's TMA lowering for every summand (K tensor loads per 64-row box, the hardware swizzle
+    applied to each summand image alike), the sum in shared memory in k order, one bulk store per replica."""
+    es = synth.DTYPE_SIZE[dtype]
+    rows, cols = 128 * (2 if es <= 4 else 1), 128 // es * 6
+    d = run_local(axe, tiled_reduce_cfg(K, rows, cols, dtype, reps), dtype, seed=K * 3 + es)
+    assert d["kernel"] == "reduce" and d["mode"] == "tma", d
+
+
+def test_k4t_matches_vector_form_bitwise(axe, monkeypatch):
+    """K4T performs K4's arithmetic (fp32 accumulators in k order from 0, one rounding): its output equals the
+    vector kernel's bit for bit on the bench's shape scaled down."""
+    cfg = synth.reduce_local(8, 1024, 512, "bf16", tiled=True)
+    vals = synth.numbers(8 * 1024 * 512, "bf16", 77)
+    sbuf = oracle.scatter_logical(cfg["src"], cfg["src_st"], vals, 2, np.zeros(8 * 1024 * 512 * 2, np.uint8), NT)
+    s = torch.from_numpy(sbuf).cuda()
+    outs = []
+    for tma in ("1", "0"):
+        monkeypatch.setenv("AXE_K4_TMA", tma)
+        p = axe.ReducePlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], "bf16")
+        assert p.describe()["mode"] == ("tma" if tma == "1" else "vector")
+        o = torch.zeros(1024 * 512, dtype=torch.int16, device="cuda")
+        p.execute(s, o)
+        torch.cuda.synchronize()
+        outs.append(o.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("K", [1, 2, 3, 17, 300])
 def test_k_values(axe, K):
     """K = 1 (a copy), odd K (tail of the 8-wide load batch), K > 256 (decoded summand offsets)."""
