@@ -114,6 +114,11 @@ struct K8Params {
   int chunked;
   uint32_t nitems;
   FastDiv nchunks;
+  // bulk form (k8_bulk, kernels_tma.cu): the inner block is one run contiguous on both sides, moved as
+  // boxes of `box` bytes by cp.async.bulk global -> smem -> global; box b = (o, r): run o, piece r
+  int bulk;
+  uint32_t box, nboxes, stages, prefetch;
+  FastDiv per_run;                     // boxes per run
   int dep;
 };
 

@@ -233,6 +233,110 @@ __global__ void __launch_bounds__(32, 1) k_tma_region(const __grid_constant__ CU
   bulk_wait_read<0>();
 }
 
+
+// ------------------------------------------------------------------ K8 bulk form
+// Non-nested digit systems whose shared innermost run is contiguous on both sides (R27): every run moves as
+// boxes of p.box bytes by cp.async.bulk -- global -> shared ring -> global per destination replica, one
+// issuing thread per CTA, no thread touches the data -- and the run's two addresses come from the two
+// independent outer decodings.  Persistent strided grid; half a ring prefetched into L2 before the wait.
+__device__ __forceinline__ int64_t k8b_digits(int n, const FastDiv *fd, const int64_t *st, uint32_t i) {
+  int64_t off = 0;
+#pragma unroll
+  for (int k = K8_MAXD - 1; k >= 1; k--) {
+    if (k >= n) continue;
+    const uint32_t q = fdiv(fd[k], i);
+    off += (int64_t)(i - q * fd[k].d) * st[k];
+    i = q;
+  }
+  if (n > 0) off += (int64_t)i * st[0];
+  return off;
+}
+
+constexpr int K8B_STAGES = 32;
+
+__global__ void __launch_bounds__(32, 1) k8_bulk(const __grid_constant__ K8Params p, const uint8_t *__restrict__ src,
+                                                 uint8_t *__restrict__ dst) {
+  extern __shared__ __align__(128) uint8_t raw[];
+  __shared__ __align__(8) uint64_t full[K8B_STAGES];
+  if (threadIdx.x != 0) {
+    pdl_launch_dependents();
+    return;
+  }
+  uint8_t *sm = (uint8_t *)(((uintptr_t)raw + 127) & ~(uintptr_t)127);
+  const uint32_t S = p.stages, box = p.box, slot = (box + 127) & ~127u;
+  const uint32_t lo = blockIdx.x, bstep = gridDim.x;
+  const uint32_t mine = lo < p.nboxes ? (p.nboxes - lo + bstep - 1) / bstep : 0;
+  auto addr = [&](uint32_t b, int64_t &so, int64_t &dof) {
+    const uint32_t o = fdiv(p.per_run, b);
+    const int64_t r = (int64_t)(b - o * p.per_run.d) * box;
+    so = p.sbase + k8b_digits(p.na, p.afd, p.as, o) + r;
+    dof = p.dbase + k8b_digits(p.nb, p.bfd, p.bs, o) + r;
+  };
+  for (uint32_t s = 0; s < S; s++) mbar_init(&full[s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  if (p.dep) {
+    const uint32_t np = mine < p.prefetch ? mine : p.prefetch;
+    for (uint32_t k = 0; k < np; k++) {
+      int64_t so, dof;
+      addr(lo + k * bstep, so, dof);
+      bulk_prefetch(src + so, box);
+    }
+    pdl_wait();
+  }
+  pdl_launch_dependents();
+  auto issue = [&](uint32_t k) {
+    const uint32_t s = k % S;
+    int64_t so, dof;
+    addr(lo + k * bstep, so, dof);
+    mbar_expect_tx(&full[s], box);
+    bulk_load(sm + (size_t)s * slot, src + so, box, &full[s]);
+  };
+  for (uint32_t k = 0; k < mine && k < S; k++) issue(k);
+  for (uint32_t k = 0; k < mine; k++) {
+    const uint32_t s = k % S;
+    int64_t so, dof;
+    addr(lo + k * bstep, so, dof);
+    mbar_wait(&full[s], (k / S) & 1u);
+    for (int r = 0; r < p.nrep; r++) bulk_store(dst + dof + p.rep[r], sm + (size_t)s * slot, box);
+    bulk_commit();
+    if (k >= 2u && k - 2 + S < mine) {
+      bulk_wait_read<2>();
+      issue(k - 2 + S);
+    }
+  }
+  bulk_wait_read<0>();
+}
+
+cudaError_t launch_k8_bulk(K8Params p, const void *src, void *dst, cudaStream_t st) {
+  if (p.nboxes == 0) return cudaSuccess;
+  static int optin = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v;
+  }();
+  static const int per_sm = [] {
+    const char *e = getenv("AXE_K8_BULK_PER_SM");
+    return (e && *e) ? std::max(1, std::min(8, atoi(e))) : 4;
+  }();
+  const uint32_t slot = (p.box + 127) & ~127u;
+  // CTAs per SM: the knob, as long as each CTA keeps a ring of >= 4 boxes
+  int ps = per_sm;
+  while (ps > 1 && (size_t)(233472 / ps - 1024 - 2048 - 128) < 4 * (size_t)slot) ps--;
+  const size_t budget = (size_t)std::min(optin, 233472 / ps - 1024) - 2048 - 128;
+  p.stages = (uint32_t)std::min<size_t>(K8B_STAGES, budget / slot);
+  if (p.stages < 2) return cudaErrorInvalidValue;
+  p.prefetch = std::max<uint32_t>(1, p.stages / 2);
+  const size_t smem = (size_t)p.stages * slot + 128;
+  const cudaError_t attr_err = smem_attr((const void *)k8_bulk, optin - 2048);
+  if (attr_err != cudaSuccess) return attr_err;
+  const unsigned blocks = (unsigned)std::min<int64_t>(p.nboxes, (int64_t)num_sms() * ps);
+  const cudaError_t e = launch_ex(k8_bulk, dim3(blocks), dim3(32), smem, st, p, (const uint8_t *)src, (uint8_t *)dst);
+  if (e != cudaSuccess) return e;
+  g_launches++;
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                     const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,

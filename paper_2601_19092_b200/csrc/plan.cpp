@@ -1113,7 +1113,7 @@ axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t 
     case KK_DUAL: {
       K8Params k = p.k8;
       k.dep = dep;
-      e = launch_k8(k, p.vb, src, dst, st);
+      e = k.bulk ? launch_k8_bulk(k, src, dst, st) : launch_k8(k, p.vb, src, dst, st);
       break;
     }
     case KK_GENERIC: {

@@ -85,6 +85,7 @@ cudaError_t launch_k7(const K7Params &p, int es, unsigned blocks, const void *sr
 bool build_k8(const Linear &ls, const Linear &ld, const Storage &sst, const Storage &dstst, int es, int max_align,
               CopyPlan *P, std::string *why);
 cudaError_t launch_k8(const K8Params &p, int vb, const void *src, void *dst, cudaStream_t st);
+cudaError_t launch_k8_bulk(K8Params p, const void *src, void *dst, cudaStream_t st);
 
 bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,
               const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why);

@@ -16,6 +16,11 @@ namespace axe {
 
 int k8_chunk(int vb);
 
+static int64_t env_i8(const char *name, int64_t dflt) {
+  const char *e = getenv(name);
+  return (e && *e) ? atoll(e) : dflt;
+}
+
 static bool env_chunked() {  // AXE_K8_CHUNKED=0: per-vector decoding only (tests compare both forms)
   const char *e = getenv("AXE_K8_CHUNKED");
   return !(e && *e == '0');
@@ -108,6 +113,30 @@ bool build_k8(const Linear &ls, const Linear &ld, const Storage &sst, const Stor
   k.ssw = make_swz(sst);
   k.dsw = make_swz(dstst);
   P->vb = (int)(V * es);
+  // bulk form: the inner block is ONE run contiguous on both sides, unswizzled, 16-byte aligned throughout
+  // -- it moves by cp.async.bulk in boxes of at most 16 KiB (AUTO: runs of >= 1 KiB)
+  {
+    const int64_t run = in.e * es;
+    bool ok = Jin.size() == 1 && in.ss == 1 && in.ds == 1 && !sst.swz_b && !dstst.swz_b && max_align >= 16 &&
+              run % 16 == 0 && run >= env_i8("AXE_K8_BULK_MIN_RUN", 1024) && env_i8("AXE_K8_BULK", 1) &&
+              (ls.base * es) % 16 == 0 && (ld.base * es) % 16 == 0;
+    for (auto &x : A) ok = ok && (x.s * es) % 16 == 0;
+    for (auto &x : B) ok = ok && (x.s * es) % 16 == 0;
+    for (int64_t r : reps) ok = ok && (r * es) % 16 == 0;
+    int64_t box = 0;
+    if (ok)
+      for (int64_t d = std::min<int64_t>(run, 16384); d >= 16; d -= 16)
+        if (run % d == 0) {
+          box = d;
+          break;
+        }
+    if (ok && box && (run / box) * nout < (int64_t(1) << 31)) {
+      k.bulk = 1;
+      k.box = (uint32_t)box;
+      k.per_run = make_fastdiv((uint32_t)(run / box));
+      k.nboxes = (uint32_t)((run / box) * nout);
+    }
+  }
   // chunked form: the inner block is one run (a single digit) of at least one vector per thread
   const int64_t CH = k8_chunk(P->vb);
   if (I.size() == 1 && vin >= CH / (P->vb >= 8 ? 4 : 8) && env_chunked()) {  // >= one vector per thread
@@ -126,7 +155,8 @@ bool build_k8(const Linear &ls, const Linear &ld, const Storage &sst, const Stor
       s += (i ? "," : "") + std::string("[") + std::to_string(L[i].e) + "," + std::to_string(L[i].s) + "]";
     return s + "]";
   };
-  P->desc = "{\"kernel\":\"dual\",\"chunked\":" + std::to_string(k.chunked) + ",\"vec_bytes\":" + std::to_string(P->vb) + ",\"vectors\":" +
+  P->desc = "{\"kernel\":\"dual\",\"bulk\":" + std::to_string(k.bulk) + ",\"box_bytes\":" +
+            std::to_string(k.box) + ",\"chunked\":" + std::to_string(k.chunked) + ",\"vec_bytes\":" + std::to_string(P->vb) + ",\"vectors\":" +
             std::to_string(k.total) + ",\"inner_block_vectors\":" + std::to_string(vin) +
             ",\"outer_blocks\":" + std::to_string(nout) + ",\"replicas\":" + std::to_string(reps.size()) +
             ",\"inner\":" + joint_json(Jin) + ",\"outer_src\":" + lin_json(A) + ",\"outer_dst\":" + lin_json(B) + "}";

@@ -204,14 +204,28 @@ def test_dual_decoding_non_nested(axe, p, q, g, h, pad_s, pad_d, es, rev, reps):
     check(axe, cfg, "generic")
 
 
-@pytest.mark.parametrize("chunked", ["1", "0"])
-def test_dual_decoding_large(axe, chunked, monkeypatch):
+@pytest.mark.parametrize("form", ["bulk", "chunked", "per_vector"])
+def test_dual_decoding_large(axe, form, monkeypatch):
     """The bench row's shape at a size that still checks quickly: (3*2^13, 2*2^7) blocks of 2^13 bf16 ->
-    (2*2^7, 3*2^13) with padded pitches, 16-byte vectors; the chunked form and the per-vector form."""
-    monkeypatch.setenv("AXE_K8_CHUNKED", chunked)
+    (2*2^7, 3*2^13) with padded pitches; K8's bulk form (16 KiB cp.async.bulk boxes), its chunked vector
+    form and its per-vector form."""
+    monkeypatch.setenv("AXE_K8_BULK", "1" if form == "bulk" else "0")
+    monkeypatch.setenv("AXE_K8_CHUNKED", "1" if form == "chunked" else "0")
     cfg = nonnested_pair(3, 2, 8192, 128, 64, 128, 2)
     d = check(axe, cfg, "auto")
-    assert d["kernel"] == "dual" and d["vec_bytes"] == 16 and d["chunked"] == int(chunked), d
+    assert d["kernel"] == "dual" and d["vec_bytes"] == 16, d
+    assert d["bulk"] == (form == "bulk") and d["chunked"] == (form == "chunked"), d
+
+
+@pytest.mark.parametrize("p,q,g,h,pad_s,pad_d,es,reps", [
+    (3, 2, 64, 8, 8, 16, 2, 1), (5, 3, 32, 3, 4, 4, 8, 2), (3, 2, 8, 4, 2, 6, 16, 3), (2, 3, 1024, 5, 8, 24, 4, 1)])
+def test_dual_decoding_bulk_small_runs(axe, p, q, g, h, pad_s, pad_d, es, reps, monkeypatch):
+    """K8's bulk form down to 16-byte runs (AXE_K8_BULK_MIN_RUN=16), with destination replicas, and runs
+    longer than one 16 KiB box (g = 1024 fp32: 12 / 8 KiB runs)."""
+    monkeypatch.setenv("AXE_K8_BULK_MIN_RUN", "16")
+    cfg = nonnested_pair(p, q, g, h, pad_s, pad_d, es, False, reps)
+    d = check(axe, cfg, "auto")
+    assert d["kernel"] == "dual" and d["bulk"] == 1, d
 
 
 def test_identity_and_transpose_reduce_to_torch(axe):
