@@ -11,7 +11,7 @@ import pytest
 
 import oracle
 import synth
-from synth import layout
+from synth import layout, linear_storage
 
 import paper_2601_19092_b200 as axe
 
@@ -164,3 +164,21 @@ def test_device_plan_from_the_lowering():
     d.box[1] = 4                                          # half an atom per box
     h = axe.C.c_void_p()
     assert axe._lib.axe_tma_plan_create(axe.C.byref(d), q.lowering["tiler"].handle, axe.C.byref(h)) == 1
+
+
+def test_lowered_copy_plans_have_box_programs():
+    """The lowered schedule's box table (tensor-map coordinates + image offset per fused atom box) is
+    re-expressed as a mixed-radix program the kernel evaluates (tma_region.cpp fit_program, verified
+    against every box): config 2 both ways, at 16384^2, with other element sizes / swizzles, and with the
+    tiles stored column-of-tiles first -- none needs the global-memory table."""
+    import paper_2601_19092_b200 as axe
+    cfgs = [synth.config2(), synth.config2(reverse=True), synth.config2(16384), synth.config2(512, 32, 4),
+            synth.config2(512, 64, 1, synth.SW64), synth.config2(256, 16, 4, synth.SW64, True)]
+    R, Cn, t = 256, 512, 64
+    cfgs.append(dict(src=layout([(R // t, t * Cn), (t, Cn), (Cn // t, t), (t, 1)]), src_st=linear_storage(R * Cn),
+                     dst=layout([(R // t, t * t), (t, t), (Cn // t, (R // t) * t * t), (t, 1)]),
+                     dst_st=linear_storage(R * Cn, synth.SW128), es=2))
+    for c in cfgs:
+        d = axe.CopyPlan(c["src"], c["src_st"], c["dst"], c["dst_st"], c["es"], "lowered").describe()
+        assert d["kernel"] == "lowered", d
+        assert d["box_program_digits"] >= 1, d
