@@ -87,6 +87,36 @@ def test_config2_full(axe, rev, kernel):
     assert desc["kernel"] == ("lowered" if kernel == "auto" else kernel)
 
 
+@pytest.mark.parametrize("R,Cn,es", [(8192, 8192, 2), (8192, 8192, 4), (8192, 4096, 8)])
+def test_bench_transposes_full_size(axe, R, Cn, es):
+    """bench.py's transpose rows at the size it times (K7, the AUTO plan), every byte against the oracle."""
+    cfg = dict(name=f"T{R}x{Cn}x{es}", es=es, src=layout([(R, Cn), (Cn, 1)]), src_st=linear_storage(R * Cn),
+               dst=layout([(R, 1), (Cn, R)]), dst_st=linear_storage(R * Cn), seed=R + Cn + es)
+    d = check(axe, cfg)
+    assert d["kernel"] == "transpose", d
+    torch.cuda.empty_cache()
+
+
+def test_bench_nonnested_row_full_size(axe):
+    """bench.py's non-nested row at the size it times ((3*2^13, 2*2^13) -> (2*2^13, 3*2^13) bf16, padded, 768
+    MiB each side): K8's bulk form, every byte against the oracle (the source storage filled with synth.values
+    cell by cell -- padding included -- so the oracle's copy is the only pass over 2^28.6 elements)."""
+    g = 1 << 13
+    cfg = nonnested_pair(3, 2, g, g, 64, 128, 2)
+    cells = synth.storage_cells(cfg["src_st"])
+    src = synth.values(cells, 2, cfg["seed"])
+    d_fill = synth.sentinel(synth.storage_cells(cfg["dst_st"]) * 2, cfg["seed"])
+    exp = d_fill.copy()
+    oracle.copy(cfg["src"], cfg["src_st"], src, cfg["dst"], cfg["dst_st"], exp, 2, NT)
+    got, d = run_gpu(axe, cfg, src, d_fill)
+    assert d["kernel"] == "dual" and d["bulk"] == 1, d
+    if not np.array_equal(got, exp):
+        bad = np.nonzero(got != exp)[0]
+        raise AssertionError(f"{len(bad)} bytes differ, first at {bad[:8]}")
+    del got, exp, src, d_fill
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("fuse", ["1", "0"])
 @pytest.mark.parametrize("n,t,es,sw", [(4096, 64, 2, synth.SW128), (1024, 64, 2, synth.SW128),
                                        (512, 32, 4, synth.SW128), (512, 64, 1, synth.SW64), (256, 16, 4, synth.SW64),
