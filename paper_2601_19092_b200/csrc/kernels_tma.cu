@@ -325,7 +325,7 @@ cudaError_t launch_k8_bulk(K8Params p, const void *src, void *dst, cudaStream_t 
   while (ps > 1 && (size_t)(233472 / ps - 1024 - 2048 - 128) < 4 * (size_t)slot) ps--;
   const size_t budget = (size_t)std::min(optin, 233472 / ps - 1024) - 2048 - 128;
   p.stages = (uint32_t)std::min<size_t>(K8B_STAGES, budget / slot);
-  if (p.stages < 2) return cudaErrorInvalidValue;
+  if (p.stages < 3) return cudaErrorInvalidValue;  // a slot is refilled two boxes after its store
   p.prefetch = std::max<uint32_t>(1, p.stages / 2);
   const size_t smem = (size_t)p.stages * slot + 128;
   const cudaError_t attr_err = smem_attr((const void *)k8_bulk, optin - 2048);
@@ -405,7 +405,12 @@ cudaError_t launch_tma_region(const void *map128, TrParams p, int store, cudaStr
     cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     return v;
   }();
-  const int per_sm = tma_region_per_sm();
+  // CTAs per SM: the knob, lowered until every CTA's ring holds TR_LAG + 1 slots (a slot is refilled
+  // TR_LAG boxes after its store, so fewer slots would wait on a box never issued)
+  int per_sm = tma_region_per_sm();
+  auto ring_of = [&](int ps) { return (size_t)std::min(optin, per_sm_bytes / ps - 1024) - 4096; };
+  while (per_sm > 1 && ring_of(per_sm) / p.slot < (size_t)TR_LAG + 1) per_sm--;
+  if (ring_of(per_sm) / p.slot < (size_t)TR_LAG + 1) return cudaErrorInvalidValue;
   // ring: the CTA's share of the SM's shared memory (1 KiB per CTA is reserved by the system, the
   // static barriers and the 1 KiB alignment pad come off the top), at most TR_STAGES slots
   static const int static_bytes = [] {  // the barriers (+ alignment) of the kernel's static shared memory
@@ -421,10 +426,10 @@ cudaError_t launch_tma_region(const void *map128, TrParams p, int store, cudaStr
     return (size_t)((e && *e) ? std::max(1024, atoi(e)) : (1 << 30));
   }();
   const size_t ring = std::min(budget, ring_cap);
-  p.stages = (uint32_t)std::max<size_t>(1, std::min<size_t>(TR_STAGES, ring / p.slot));
-  if (p.stages < 2 && ring < p.slot) return cudaErrorInvalidValue;
+  p.stages = (uint32_t)std::min<size_t>(TR_STAGES, ring / p.slot);
+  if (p.stages < (uint32_t)TR_LAG + 1) return cudaErrorInvalidValue;
   const size_t smem = (size_t)p.stages * p.slot + 1024;
-  const cudaError_t attr_err = smem_attr(kern, max_dyn);
+  const cudaError_t attr_err = smem_attr(kern, optin - static_bytes);  // (the largest any launch asks for)
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap m;
   memcpy(&m, map128, sizeof(m));

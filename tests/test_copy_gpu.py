@@ -87,6 +87,21 @@ def test_config2_full(axe, rev, kernel):
     assert desc["kernel"] == ("lowered" if kernel == "auto" else kernel)
 
 
+@pytest.mark.parametrize("rev", [False, True])
+@pytest.mark.parametrize("tr,tc,es", [(256, 64, 2), (128, 128, 1), (256, 32, 4), (64, 64, 2)])
+def test_lowered_large_boxes(axe, rev, tr, tc, es):
+    """Tall tiles: the lowered schedule fuses up to 256 atom rows into one box (32 KiB); the launch lowers the
+    CTAs per SM until every ring holds the 3 slots its refill lag needs, both directions."""
+    R, C = 2 * tr * 2, tc * 8
+    rm = layout([(R, C), (C, 1)])
+    tiles = layout([(R // tr, tr * C), (tr, tc), (C // tc, tr * tc), (tc, 1)])
+    st_rm, st_t = linear_storage(R * C), linear_storage(R * C, synth.SW128)
+    cfg = dict(name=f"tall{tr}x{tc}x{es}", es=es, src=tiles if rev else rm, src_st=st_t if rev else st_rm,
+               dst=rm if rev else tiles, dst_st=st_rm if rev else st_t, seed=tr + tc + es)
+    d = check(axe, cfg)
+    assert d["kernel"] == "lowered" and d["box_bytes"] == tr * tc * es, d
+
+
 @pytest.mark.parametrize("R,Cn,es", [(8192, 8192, 2), (8192, 8192, 4), (8192, 4096, 8)])
 def test_bench_transposes_full_size(axe, R, Cn, es):
     """bench.py's transpose rows at the size it times (K7, the AUTO plan), every byte against the oracle."""
