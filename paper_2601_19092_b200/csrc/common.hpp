@@ -140,7 +140,7 @@ bool joint_refine(const std::vector<LinIter> &src, const std::vector<LinIter> &d
 // other split off their gcd g as one more joint digit (both digits are multiples of g, so an aligned run
 // of g consecutive x stays inside both).  What is left -- the outer index x / G over the two
 // remaining lists -- has two independent decodings (src_rest, dst_rest, outermost first; the same
-// product).  Returns false if nothing refines (G = 1 with no joint digit).
+// product).  The inner list is empty when even the fastest pair shares no factor (gcd 1).
 bool joint_refine_partial(const std::vector<LinIter> &src, const std::vector<LinIter> &dst, std::vector<Joint> *inner,
                           std::vector<LinIter> *src_rest, std::vector<LinIter> *dst_rest);
 

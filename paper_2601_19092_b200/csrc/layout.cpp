@@ -485,7 +485,6 @@ bool joint_refine_partial(const std::vector<LinIter> &src_in, const std::vector<
       break;
     }
   }
-  if (J.empty()) return false;
   std::reverse(J.begin(), J.end());
   std::vector<Joint> F;  // joint D1 (Cor. fuse)
   for (auto &j : J) {

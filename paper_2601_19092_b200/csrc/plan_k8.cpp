@@ -34,7 +34,8 @@ bool build_k8(const Linear &ls, const Linear &ld, const Storage &sst, const Stor
   };
   std::vector<Joint> Jin;
   std::vector<LinIter> A, B;
-  if (!joint_refine_partial(ls.D, ld.D, &Jin, &A, &B)) return fail("no common innermost digit (gcd 1)");
+  if (!joint_refine_partial(ls.D, ld.D, &Jin, &A, &B)) return fail("no digit lists");
+  if (Jin.empty()) Jin.push_back(Joint{1, 1, 1});  // gcd 1: element by element, both decodings per element
   for (auto &j : Jin)
     if (j.sdev || j.ddev) return fail("device-axis digits");
   for (auto *L : {&A, &B})

@@ -168,11 +168,13 @@ def test_config3_plans_are_affine():
     assert plan(synth.config3(64, "b"), "register").describe()["kernel"] == "register"
 
 
-def test_nonnested_falls_back_to_generic():
-    """(2,3):(1,2) vs (3,2):(1,3): suffix products {1,3,6} vs {1,2,6} are not nested (SURVEY §7 hard part 3)."""
+def test_nonnested_gcd1_decodes_both_sides_per_element():
+    """(2,3):(1,2) vs (3,2):(1,3): suffix products {1,3,6} vs {1,2,6} are not nested and the innermost extents
+    share no factor (SURVEY §7 hard part 3): K8 with an empty inner block, both digit lists decoded per
+    element with fast divisions (the generic K0 stays for non-affine storage compositions)."""
     src, dst = layout([(2, 1), (3, 2)]), layout([(3, 1), (2, 3)])
     d = axe.CopyPlan(src, linear_storage(6), dst, linear_storage(6), 4).describe()
-    assert d["kernel"] == "generic"
+    assert d["kernel"] == "dual" and d["inner_block_vectors"] == 1 and d["vec_bytes"] == 4, d
 
 
 def test_nonnested_with_common_factor_plans_dual():

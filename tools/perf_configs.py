@@ -37,8 +37,19 @@ def nonnested_cfg(k=13, es=2):
                 dst_st=synth.linear_storage(B1 * (B2 + 128)), seed=9)
 
 
+def nonnested_gcd1_cfg(m=32, es=2):
+    """(2187 m, 4096) row-major, pitch 4096 + 64 -> the same x re-split as (4096 m, 2187), pitch 2187 + 5:
+    innermost extents 4096 and 3^7 share no factor -- element by element (K8 with an empty inner block;
+    K0 when forced generic)."""
+    A1, A2, B1, B2 = 2187 * m, 4096, 4096 * m, 2187
+    return dict(name=f"nonnested_gcd1_m{m}", es=es, src=synth.layout([(A1, A2 + 64), (A2, 1)]),
+                src_st=synth.linear_storage(A1 * (A2 + 64)), dst=synth.layout([(B1, B2 + 5), (B2, 1)]),
+                dst_st=synth.linear_storage(B1 * (B2 + 5)), seed=11)
+
+
 CONFIGS = {
     "nonnested_3x2": lambda: nonnested_cfg(13),
+    "nonnested_gcd1": lambda: nonnested_gcd1_cfg(32),
     "config2": lambda: synth.config2(),
     "config2r": lambda: synth.config2(reverse=True),
     "config2_16k": lambda: synth.config2(16384),
