@@ -370,6 +370,64 @@ __global__ void __launch_bounds__(K1_THREADS) k8_dual(const __grid_constant__ K8
   }
 }
 
+
+// K8 odometer form: gcd-1 digit systems (no run is shared by the two sides).  Lane l of a warp takes
+// x = x0 + l, x0 + l + 32, ... over a chunk of 32 K8_ODO_J elements; per side it keeps the innermost digit
+// r = x mod E and the byte offset of the outer digits of q = x / E, and when r wraps it decodes q again
+// (fast divisions) -- so consecutive lanes move consecutive x (coalesced wherever a side's innermost
+// digit is contiguous), and an element costs a compare and two adds per side instead of two full
+// decodings.  8 loads in flight per lane before their stores.
+template <int ES>
+__global__ void __launch_bounds__(K1_THREADS) k8_odo(const __grid_constant__ K8Params p, const uint8_t *__restrict__ src,
+                                                     uint8_t *__restrict__ dst) {
+  using T = typename VecT<ES>::T;
+  constexpr int U = 8;
+  if (p.dep) pdl_wait();
+  pdl_launch_dependents();
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (K1_THREADS / 32);
+  const FastDiv EA = p.afd[p.na - 1], EB = p.bfd[p.nb - 1];
+  const int64_t sA = p.as[p.na - 1], sB = p.bs[p.nb - 1];
+  for (uint32_t c = blockIdx.x * (K1_THREADS / 32) + (threadIdx.x >> 5); c < p.nchunk; c += warps) {
+    uint32_t x = c * (uint32_t)(K8_ODO_J * 32) + lane;
+    const uint32_t xend = min(p.total, (c + 1) * (uint32_t)(K8_ODO_J * 32));
+    uint32_t qa = fdiv(EA, x), ra = x - qa * EA.d;
+    uint32_t qb = fdiv(EB, x), rb = x - qb * EB.d;
+    int64_t oa = p.sbase + k8_digits<K8_MAXD>(p.na - 1, p.afd, p.as, qa);
+    int64_t ob = p.dbase + k8_digits<K8_MAXD>(p.nb - 1, p.bfd, p.bs, qb);
+    for (int j0 = 0; j0 < K8_ODO_J; j0 += U) {
+      T v[U];
+      int64_t d[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        if (x < xend) {
+          v[u] = ld_stream<ES>(src + swz(p.ssw, oa + (int64_t)ra * sA));
+          d[u] = ob + (int64_t)rb * sB;
+        }
+        x += 32;
+        ra += 32;
+        rb += 32;
+        if (ra >= EA.d) {  // the innermost source digit wrapped: decode the outer ones again
+          qa = fdiv(EA, x);
+          ra = x - qa * EA.d;
+          oa = p.sbase + k8_digits<K8_MAXD>(p.na - 1, p.afd, p.as, qa);
+        }
+        if (rb >= EB.d) {
+          qb = fdiv(EB, x);
+          rb = x - qb * EB.d;
+          ob = p.dbase + k8_digits<K8_MAXD>(p.nb - 1, p.bfd, p.bs, qb);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const uint32_t xu = x - (uint32_t)(U - u) * 32;
+        if (xu < xend)
+          for (int r = 0; r < p.nrep; r++) st_vec<ES>(dst + swz(p.dsw, d[u] + p.rep[r]), v[u]);
+      }
+    }
+  }
+}
+
 template <int VB>
 static cudaError_t k8_launch(const K8Params &p, const uint8_t *s, uint8_t *d, cudaStream_t st) {
   constexpr int U = VB >= 8 ? 4 : 8;
@@ -386,6 +444,24 @@ cudaError_t launch_k8(const K8Params &p, int vb, const void *src, void *dst, cud
   const uint8_t *s = (const uint8_t *)src;
   uint8_t *d = (uint8_t *)dst;
   cudaError_t e;
+  if (p.odo) {
+    auto go = [&](auto kern) {
+      const unsigned want = (p.nchunk + K1_THREADS / 32 - 1) / (K1_THREADS / 32);
+      const unsigned blocks = one_wave((const void *)kern, K1_THREADS, 0, std::max(1u, want));
+      return launch_ex(kern, dim3(blocks), dim3(K1_THREADS), 0, st, p, s, d);
+    };
+    switch (vb) {
+      case 1: e = go(k8_odo<1>); break;
+      case 2: e = go(k8_odo<2>); break;
+      case 4: e = go(k8_odo<4>); break;
+      case 8: e = go(k8_odo<8>); break;
+      case 16: e = go(k8_odo<16>); break;
+      default: return cudaErrorInvalidValue;
+    }
+    if (e != cudaSuccess) return e;
+    g_launches++;
+    return cudaGetLastError();
+  }
   switch (vb) {
     case 1: e = k8_launch<1>(p, s, d, st); break;
     case 2: e = k8_launch<2>(p, s, d, st); break;

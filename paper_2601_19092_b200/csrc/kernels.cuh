@@ -119,8 +119,14 @@ struct K8Params {
   int bulk;
   uint32_t box, nboxes, stages, prefetch;
   FastDiv per_run;                     // boxes per run
+  // odometer form (odo = 1; gcd 1, vectors of one element): a warp walks K8_ODO_J * 32 consecutive x,
+  // lane by lane; each lane carries (x / E, x mod E) of the innermost digit of both lists (extents
+  // afd[na-1] / bfd[nb-1]) and re-decodes the outer digits only when its innermost digit wraps
+  int odo;
+  uint32_t nchunk;                     // chunks of K8_ODO_J * 32 elements
   int dep;
 };
+constexpr int K8_ODO_J = 64;
 
 // ---------------------------------------------------------------- K1-TMA
 // The paper's TMA lowering: every box is (rows x row bytes), whole

@@ -138,6 +138,12 @@ bool build_k8(const Linear &ls, const Linear &ld, const Storage &sst, const Stor
       k.nboxes = (uint32_t)((run / box) * nout);
     }
   }
+  // odometer form: gcd 1 (an empty inner block, one element per vector) -- per-lane digit carries
+  if (vin == 1 && V == 1 && Jin.size() == 1 && in.e == 1 && !A.empty() && !B.empty() && env_i8("AXE_K8_ODO", 1) &&
+      k.total < (uint32_t)0xFFFFFFFF - 32 * K8_ODO_J) {
+    k.odo = 1;
+    k.nchunk = (uint32_t)((k.total + 32 * K8_ODO_J - 1) / (32 * K8_ODO_J));
+  }
   // chunked form: the inner block is one run (a single digit) of at least one vector per thread
   const int64_t CH = k8_chunk(P->vb);
   if (I.size() == 1 && vin >= CH / (P->vb >= 8 ? 4 : 8) && env_chunked()) {  // >= one vector per thread
@@ -156,7 +162,7 @@ bool build_k8(const Linear &ls, const Linear &ld, const Storage &sst, const Stor
       s += (i ? "," : "") + std::string("[") + std::to_string(L[i].e) + "," + std::to_string(L[i].s) + "]";
     return s + "]";
   };
-  P->desc = "{\"kernel\":\"dual\",\"bulk\":" + std::to_string(k.bulk) + ",\"box_bytes\":" +
+  P->desc = "{\"kernel\":\"dual\",\"odometer\":" + std::to_string(k.odo) + ",\"bulk\":" + std::to_string(k.bulk) + ",\"box_bytes\":" +
             std::to_string(k.box) + ",\"chunked\":" + std::to_string(k.chunked) + ",\"vec_bytes\":" + std::to_string(P->vb) + ",\"vectors\":" +
             std::to_string(k.total) + ",\"inner_block_vectors\":" + std::to_string(vin) +
             ",\"outer_blocks\":" + std::to_string(nout) + ",\"replicas\":" + std::to_string(reps.size()) +

@@ -249,6 +249,19 @@ def test_dual_decoding_non_nested(axe, p, q, g, h, pad_s, pad_d, es, rev, reps):
     check(axe, cfg, "generic")
 
 
+@pytest.mark.parametrize("p,q,h,pad_s,pad_d,es,rev,reps", [
+    (3, 2, 40, 1, 3, 2, False, 1), (7, 4, 33, 1, 2, 4, True, 1), (5, 3, 64, 3, 5, 8, False, 2),
+    (4096, 2187, 3, 64, 5, 2, False, 1), (2187, 4096, 2, 5, 64, 1, True, 1), (31, 17, 50, 2, 1, 16, False, 3)])
+def test_dual_decoding_gcd1_odometer(axe, p, q, h, pad_s, pad_d, es, rev, reps):
+    """gcd-1 digit systems (no factor shared even by the fastest pair): K8's odometer form -- per-lane
+    carries of both innermost digits, the outer digits re-decoded on wrap -- against the oracle and K0.
+    Innermost extents below and above 32 lanes, a reversed destination, replicas, 1..16-byte elements."""
+    cfg = nonnested_pair(p, q, 1, h, pad_s, pad_d, es, rev, reps)
+    d = check(axe, cfg, "auto")
+    assert d["kernel"] == "dual" and d["odometer"] == 1, d
+    check(axe, cfg, "generic")
+
+
 @pytest.mark.parametrize("form", ["bulk", "chunked", "per_vector"])
 def test_dual_decoding_large(axe, form, monkeypatch):
     """The bench row's shape at a size that still checks quickly: (3*2^13, 2*2^7) blocks of 2^13 bf16 ->
