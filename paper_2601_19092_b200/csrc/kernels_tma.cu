@@ -82,7 +82,19 @@ __global__ void __launch_bounds__(32) k1_tma(const __grid_constant__ CUtensorMap
   __shared__ __align__(8) uint64_t full[TMA_MAX_STAGES];
   const bool leader = threadIdx.x == 0;
   if (!p.xform && !leader) return;
-  if (p.dep) pdl_wait();
+  if (p.dep) {
+    if (leader) {  // the first ring of boxes into L2 while the previous kernel drains (R28)
+      const uint32_t nb0 = p.nboxes, f0 = blockIdx.x, st0 = gridDim.x;
+      for (int k = 0; k < p.stages && f0 + (uint32_t)k * st0 < nb0; k++) {
+        const BoxAddr a = box_addr(p, f0 + (uint32_t)k * st0);
+        if (p.mode == 0)
+          tma_prefetch5(&map, a.c[0], a.c[1], a.c[2], a.c[3], a.c[4]);
+        else
+          bulk_prefetch(src + (p.mode == 2 ? a.soff : a.boff), p.box_bytes);
+      }
+    }
+    pdl_wait();
+  }
   pdl_launch_dependents();
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int S = p.stages;
@@ -317,7 +329,7 @@ cudaError_t launch_k8_bulk(K8Params p, const void *src, void *dst, cudaStream_t 
   }();
   static const int per_sm = [] {
     const char *e = getenv("AXE_K8_BULK_PER_SM");
-    return (e && *e) ? std::max(1, std::min(8, atoi(e))) : 4;
+    return (e && *e) ? std::max(1, std::min(8, atoi(e))) : 2;
   }();
   const uint32_t slot = (p.box + 127) & ~127u;
   // CTAs per SM: the knob, as long as each CTA keeps a ring of >= 4 boxes
@@ -379,13 +391,14 @@ int encode_tensor_map(void *out128, void *gaddr, const uint64_t dims[5], const u
   return (int)r;
 }
 
-// CTAs per SM of the lowered schedule (AXE_TMA_REGION_PER_SM, default 4: four rings sharing the SM -- a
-// next kernel's CTA starts on every quarter freed by this one and prefetches while it drains; config 2
-// 10.46 us vs 11.63 with 2 rings, 11.95 with 8, profiles/r02_lowered_prefetch_sweep.log)
+// CTAs per SM of the lowered schedule (AXE_TMA_REGION_PER_SM, default 2).  With the half-ring L2
+// prefetch before the wait, 2 and 4 rings per SM tie on config 2 (10.04 / 10.03 us per dependent step,
+// bench 6512-6572 / 6508 GB/s) and 2 wins at 16384^2 (177.0 vs 183.5 us); without the prefetch 4 rings
+// were needed (11.63 us with 2), profiles/r02_lowered_prefetch_sweep.log)
 int tma_region_per_sm() {
   static const int v = [] {
     const char *e = getenv("AXE_TMA_REGION_PER_SM");
-    return (e && *e) ? std::max(1, std::min(8, atoi(e))) : 4;
+    return (e && *e) ? std::max(1, std::min(8, atoi(e))) : 2;
   }();
   return v;
 }

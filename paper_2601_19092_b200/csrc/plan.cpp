@@ -671,13 +671,19 @@ static bool build_bulk(const std::vector<Joint> &J0, const Linear &ls, const Lin
   k.mode = 2;
   k.nrep = (int)reps.size();
   for (size_t i = 0; i < reps.size(); i++) k.rep[i] = reps[i] * es;
-  const int64_t stage_bytes = env_int("AXE_TMA_STAGE_BYTES", 16384);
+  // ring per CTA and CTAs per SM by size (identity copies, profiles/r02_bulk_ring_sweep.log): up to 64 MiB
+  // a side, 96 KiB rings x 2 CTAs/SM (32 MiB: 10.6 us vs 13.1 with 16 KiB x 4: the whole copy is in flight
+  // at once); up to 256 MiB, 64 KiB x 3 (128 MiB: 44.5 vs 46.2); beyond, 16 KiB x 4 (512 MiB: 171 vs 176 --
+  // long copies stream, and deep rings only delay the first stores)
+  const int64_t bytes = nboxes * be * es;
+  const int64_t ring_def = bytes <= (int64_t(64) << 20) ? 98304 : bytes <= (int64_t(256) << 20) ? 65536 : 16384;
+  const int64_t per_def = bytes <= (int64_t(64) << 20) ? 2 : bytes <= (int64_t(256) << 20) ? 3 : 4;
+  const int64_t stage_bytes = env_int("AXE_TMA_STAGE_BYTES", ring_def);
   k.stages = (int)std::max<int64_t>(2, std::min<int64_t>(16, stage_bytes / k.slot_bytes));
   P->tm_swizzle = 0;
   P->tm_cache.reset();
-  // 4 CTAs per SM with 2 x 16 KiB boxes each: identity 1 GiB 334 us (6/8 per SM: 354 us; K1: 375 us)
   int per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(16, (220 * 1024) / (int64_t)tma_smem_bytes(k)));
-  per_sm = (int)std::min<int64_t>(per_sm, env_int("AXE_TMA_BULK_PER_SM", 4));
+  per_sm = (int)std::min<int64_t>(per_sm, env_int("AXE_TMA_BULK_PER_SM", per_def));
   P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nboxes, (int64_t)num_sms() * per_sm));
   P->align = 16;
   P->covers_all = (int64_t)reps.size() * nboxes * be == dstst.cells;
