@@ -133,6 +133,7 @@ bool build_k8(const Linear &ls, const Linear &ld, const Storage &sst, const Stor
         }
     if (ok && box && (run / box) * nout < (int64_t(1) << 31)) {
       k.bulk = 1;
+      P->align = std::max(P->align, 16);  // cp.async.bulk: 16-byte aligned global addresses
       k.box = (uint32_t)box;
       k.per_run = make_fastdiv((uint32_t)(run / box));
       k.nboxes = (uint32_t)((run / box) * nout);
