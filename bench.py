@@ -610,7 +610,10 @@ def run_axe(args):
             "pct_of_peak": 100.0 * (value / ws) / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": ncu_traffic(), "peak_source": peak_src,
-                         "kernel_ms": k_ms, "isolated_launch_ms": iso_ms, "direct_launch_ms": direct_ms,
+                         "kernel_ms": k_ms, "event_bracketed_single_launch_ms": iso_ms,
+                         "event_bracketed_note": "one launch between two event records (no PDL overlap, event and "
+                                                 "launch latency included); not the kernel's duration",
+                         "direct_launch_ms": direct_ms,
                          "host_us_per_call": host_us, "alg_bytes_per_launch": alg_bytes,
                          "pdl_overlap": os.environ.get("AXE_PDL_OVERLAP", "0") == "1",
                          "graph_replay_ms_incl_launch": ms_outer if graph is not None else None,
