@@ -2,7 +2,10 @@
  * config-2 plan (the lowered TMA schedule) over 32 rotating buffer pairs, N enqueues timed with
  * CLOCK_MONOTONIC, then the device time of the same N launches with CUDA events.  Shows the library's
  * own per-call work (tensor-map cache lookup, parameter block, cudaLaunchKernelEx) apart from the
- * ctypes overhead the bench's host_us_per_call includes.
+ * ctypes overhead the bench's host_us_per_call includes.  Measured (round 2, profiles/r02_host_path_c.json):
+ * 4.0 us per call, of which the library's own work is 0.1 us (a build whose launcher returns before
+ * cudaLaunchKernelEx: 0.10 us per call) -- the rest is the launch; past ~1000 queued launches the host
+ * waits for the GPU to drain the launch queue (5.1 us per call over 2000).
  *
  *   gcc -O2 -I include tools/host_path_bench.c -o /tmp/hpb -L paper_2601_19092_b200 -laxe \
  *       -Wl,-rpath,$PWD/paper_2601_19092_b200 -L /usr/local/cuda/lib64 -lcudart && /tmp/hpb */
@@ -54,6 +57,13 @@ int main(void) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
+  // host cost: the first H calls after an idle stream (fewer than the launch queue holds, so no call
+  // waits for the GPU to drain it); device time: N back-to-back launches
+  enum { H = 200 };
+  const double h0 = now_us();
+  for (int i = 0; i < H; i++) CK(axe_copy_plan_execute(plan, s[i % PAIRS], d[i % PAIRS], st));
+  const double h1 = now_us();
+  cudaStreamSynchronize(st);
   cudaEventRecord(e0, st);
   const double t0 = now_us();
   for (int i = 0; i < N; i++) CK(axe_copy_plan_execute(plan, s[i % PAIRS], d[i % PAIRS], st));
@@ -62,8 +72,8 @@ int main(void) {
   cudaEventSynchronize(e1);
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
-  printf("{\"host_us_per_call\": %.3f, \"device_us_per_step_direct_launches\": %.3f, \"calls\": %d, "
-         "\"GBps\": %.1f, \"plan\": %s}\n",
-         (t1 - t0) / N, ms * 1e3 / N, N, 2.0 * n * n * 2 / (ms * 1e-3 / N) / 1e9, desc);
+  printf("{\"host_us_per_call\": %.3f, \"host_us_per_call_queue_full\": %.3f, "
+         "\"device_us_per_step_direct_launches\": %.3f, \"calls\": %d, \"GBps\": %.1f, \"plan\": %s}\n",
+         (h1 - h0) / H, (t1 - t0) / N, ms * 1e3 / N, N, 2.0 * n * n * 2 / (ms * 1e-3 / N) / 1e9, desc);
   return 0;
 }
