@@ -27,7 +27,7 @@ from synth import layout, linear_storage  # noqa: E402
 import paper_2601_19092_b200 as axe  # noqa: E402
 
 NT = os.cpu_count() or 4
-KERNELS = ["auto", "generic", "vector", "tma", "tile", "register", "shuffle", "transpose", "lowered"]
+KERNELS = ["auto", "generic", "vector", "tma", "tile", "register", "shuffle", "transpose", "lowered", "dual"]
 
 
 def split(rng, N):
