@@ -299,6 +299,25 @@ struct K7Params {
   int dep;
 };
 
+// ---------------------------------------------------------------- K9 ragged transpose
+// 2-D transposes of any extents and pitches (element-aligned only): tiles of 64 rows x 128 bytes staged
+// in shared memory (rows padded so column reads are conflict-free), element-granular loads along the
+// source rows and stores along the destination rows -- both coalesced -- predicated at the edges.
+struct K9Params {
+  uint32_t ntiles;
+  FastDiv fa, fb;                      // tiles along a (source-contiguous) / b (destination-contiguous)
+  int nd;                              // batch digits, outermost first
+  FastDiv fd[K1_MAXD];
+  int64_t ss[K1_MAXD], ds[K1_MAXD];    // bytes
+  int64_t ea, eb;                      // extents of a and b
+  int64_t s_b, d_a;                    // source byte stride of b (row pitch), destination byte stride of a
+  int64_t sbase, dbase;
+  Swz ssw, dsw;
+  int nrep;
+  int64_t rep[K1_MAXREP];
+  int dep;
+};
+
 // ------------------------------------------------------- K4 reduce (§8(f) f3)
 // dst(y) = sum_k src(k * E_D(dst) + y) (reading R24).  Element types:
 enum DType { DT_F32 = 1, DT_F64 = 2, DT_F16 = 3, DT_BF16 = 4, DT_I32 = 5, DT_I64 = 6 };

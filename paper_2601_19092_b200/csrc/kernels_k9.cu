@@ -1,0 +1,173 @@
+// kernels_k9.cu -- K9: ragged 2-D transposes (sm_100a).
+//
+// K7 needs whole 16-byte vectors along both pitches and whole tiles; shapes like 4095 x 4097 bf16 (rows
+// that start at every 2-byte alignment) or 8000 x 8000 leave it out, and K1 then moves 2-byte vectors
+// whose stores scatter one per 32-byte sector (0.13 of peak).  K9 is the classic shared-memory transpose
+// with element-granular accesses: a tile of TB = 64 rows (b, destination-contiguous) x TA = 128 / es
+// elements (a, source-contiguous) is loaded along the source rows (consecutive lanes, consecutive
+// elements: coalesced whatever the alignment), written to shared memory with each row padded to an odd
+// number of 4-byte words (the column reads that follow hit 32 distinct banks), then stored along the
+// destination rows (consecutive lanes, consecutive b).  Edges are predicated; batch digits index tiles.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+
+#include "kernels.cuh"
+#include "launch.cuh"
+
+namespace axe {
+
+extern std::atomic<int64_t> g_launches;
+int num_sms();
+
+namespace {
+
+template <int B>
+struct ElemT;
+template <>
+struct ElemT<1> { using T = uint8_t; };
+template <>
+struct ElemT<2> { using T = uint16_t; };
+template <>
+struct ElemT<4> { using T = uint32_t; };
+template <>
+struct ElemT<8> { using T = uint2; };
+template <>
+struct ElemT<16> { using T = uint4; };
+
+constexpr int K9_THREADS = 256;
+constexpr int K9_TB = 64;
+
+template <int ES>
+struct K9Geom {
+  static constexpr int TA = 128 / ES;                        // elements per tile row (128 bytes)
+  static constexpr int PAD = ES <= 4 ? 4 / ES : 1;           // row = 132 bytes = 33 words for es <= 4
+  static constexpr int LOADS = TA * K9_TB / K9_THREADS;      // elements per thread per tile
+};
+
+template <int ES, bool SWZ>
+__global__ void __launch_bounds__(K9_THREADS) k9_ragged(const __grid_constant__ K9Params p,
+                                                        const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
+  using T = typename ElemT<ES>::T;
+  using G = K9Geom<ES>;
+  constexpr int TA = G::TA, TB = K9_TB, L = G::LOADS;
+  constexpr int RS = K9_THREADS / TA;  // load phase: rows per pass (a thread keeps its column ia)
+  constexpr int CS = K9_THREADS / TB;  // store phase: columns per pass (a thread keeps its row jb)
+  __shared__ T tile[TB][TA + G::PAD];
+  const int t = threadIdx.x;
+  const int ia_l = t % TA, jb_l0 = t / TA;  // load phase: column ia_l, rows jb_l0 + u RS
+  const int jb_s = t % TB, ia_s0 = t / TB;  // store phase: row jb_s, columns ia_s0 + u CS
+  if (p.dep) pdl_wait();
+  pdl_launch_dependents();
+  // tile geometry: batch digits outermost, then a-tiles, b-tiles fastest (consecutive CTAs extend the
+  // same destination rows)
+  struct Tile {
+    int64_t sbo, dbo, a0, b0;
+    bool full;
+  };
+  auto tile_of = [&](uint32_t tt) {
+    uint32_t r = tt;
+    uint32_t q = fdiv(p.fb, r);
+    const uint32_t tb = r - q * p.fb.d;
+    r = q;
+    q = fdiv(p.fa, r);
+    const uint32_t ta = r - q * p.fa.d;
+    r = q;
+    Tile x;
+    x.sbo = p.sbase;
+    x.dbo = p.dbase;
+    for (int k = p.nd - 1; k >= 0; k--) {
+      uint32_t d;
+      if (k > 0) {
+        const uint32_t qq = fdiv(p.fd[k], r);
+        d = r - qq * p.fd[k].d;
+        r = qq;
+      } else {
+        d = r;
+      }
+      x.sbo += (int64_t)d * p.ss[k];
+      x.dbo += (int64_t)d * p.ds[k];
+    }
+    x.a0 = (int64_t)ta * TA;
+    x.b0 = (int64_t)tb * TB;
+    x.full = x.a0 + TA <= p.ea && x.b0 + TB <= p.eb;  // an interior tile: no predicates
+    return x;
+  };
+  // load: this thread's column ia_l of rows jb_l0 + u RS; one 64-bit add per element
+  T v[L];
+  auto load = [&](const Tile &x) {
+    const int64_t sl = x.sbo + (x.b0 + jb_l0) * p.s_b + (x.a0 + ia_l) * ES, sstep = RS * p.s_b;
+#pragma unroll
+    for (int u = 0; u < L; u++) {
+      const int64_t off = sl + u * sstep;
+      if (x.full || (x.a0 + ia_l < p.ea && x.b0 + jb_l0 + u * RS < p.eb))
+        v[u] = *reinterpret_cast<const T *>(src + (SWZ ? swz(p.ssw, off) : off));
+    }
+  };
+  uint32_t tt = blockIdx.x;
+  Tile cur;
+  if (tt < p.ntiles) {
+    cur = tile_of(tt);
+    load(cur);
+  }
+  for (; tt < p.ntiles; tt += gridDim.x) {
+#pragma unroll
+    for (int u = 0; u < L; u++) tile[jb_l0 + u * RS][ia_l] = v[u];
+    __syncthreads();
+    // the next tile's loads go out before this tile's stores (register double buffering)
+    const uint32_t nt = tt + gridDim.x;
+    Tile nxt;
+    if (nt < p.ntiles) {
+      nxt = tile_of(nt);
+      load(nxt);
+    }
+    // store: this thread's row jb_s of columns ia_s0 + u CS (destination rows: consecutive lanes,
+    // consecutive b)
+    const int64_t dl = cur.dbo + (cur.a0 + ia_s0) * p.d_a + (cur.b0 + jb_s) * ES, dstep = CS * p.d_a;
+#pragma unroll
+    for (int u = 0; u < L; u++) {
+      if (cur.full || (cur.a0 + ia_s0 + u * CS < p.ea && cur.b0 + jb_s < p.eb)) {
+        const T x = tile[jb_s][ia_s0 + u * CS];
+        const int64_t off = dl + u * dstep;
+        for (int rr = 0; rr < p.nrep; rr++)
+          *reinterpret_cast<T *>(dst + (SWZ ? swz(p.dsw, off + p.rep[rr]) : off + p.rep[rr])) = x;
+      }
+    }
+    __syncthreads();
+    cur = nxt;
+  }
+}
+
+template <int ES>
+cudaError_t go(const K9Params &p, const uint8_t *s, uint8_t *d, cudaStream_t st) {
+  const bool sw = p.ssw.mask || p.dsw.mask;
+  const void *kern = sw ? (const void *)k9_ragged<ES, true> : (const void *)k9_ragged<ES, false>;
+  const unsigned blocks = one_wave(kern, K9_THREADS, 0, std::max(1u, p.ntiles));
+  return sw ? launch_ex(k9_ragged<ES, true>, dim3(blocks), dim3(K9_THREADS), 0, st, p, s, d)
+            : launch_ex(k9_ragged<ES, false>, dim3(blocks), dim3(K9_THREADS), 0, st, p, s, d);
+}
+
+}  // namespace
+
+int k9_tile_a(int es) { return 128 / es; }
+int k9_tile_b() { return K9_TB; }
+
+cudaError_t launch_k9(const K9Params &p, int es, const void *src, void *dst, cudaStream_t st) {
+  const uint8_t *s = (const uint8_t *)src;
+  uint8_t *d = (uint8_t *)dst;
+  cudaError_t e;
+  switch (es) {
+    case 1: e = go<1>(p, s, d, st); break;
+    case 2: e = go<2>(p, s, d, st); break;
+    case 4: e = go<4>(p, s, d, st); break;
+    case 8: e = go<8>(p, s, d, st); break;
+    case 16: e = go<16>(p, s, d, st); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
+  g_launches++;
+  return cudaGetLastError();
+}
+
+}  // namespace axe

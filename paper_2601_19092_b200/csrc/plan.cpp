@@ -927,14 +927,22 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
       AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced shuffle kernel cannot run these layouts: %s", w6.c_str());
   }
   if (joint && (kernel == AXE_KERNEL_AUTO || kernel == AXE_KERNEL_TRANSPOSE) && env_int("AXE_K7", 1)) {
-    std::string w7;
+    std::string w7, w9;
     if (build_k7(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &w7)) {
       P.kernel = KK_TRANSPOSE;
       *out = std::move(P);
       return AXE_OK;
     }
+    // forced: K9, the same 2-D transpose with ragged extents or pitches that are not whole 16-byte
+    // vectors (AUTO tries it after K2, below)
+    if (kernel == AXE_KERNEL_TRANSPOSE && build_k9(J, ls, ld, *rq.sst, *rq.dstst, es, &P, &w9)) {
+      P.kernel = KK_RAGGED;
+      *out = std::move(P);
+      return AXE_OK;
+    }
     if (kernel == AXE_KERNEL_TRANSPOSE)
-      AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced transpose kernel cannot run these layouts: %s", w7.c_str());
+      AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced transpose kernel cannot run these layouts: %s / %s", w7.c_str(),
+               w9.c_str());
   }
   if (joint && kernel == AXE_KERNEL_TILE) {
     if (build_k2(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &why)) {
@@ -951,10 +959,18 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
       // moves 16-byte vectors on both sides (config 3a: K1 4-byte 1583 us, K2 1547 us on B200)
       if (kernel == AXE_KERNEL_AUTO && P.vb < 16 && (P.vb <= 4 || P.k1_sector_eff < 0.5)) {
         CopyPlan T = P;
-        std::string w2;
+        std::string w2, w9;
         if (build_k2(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &T, &w2)) {
           T.kernel = KK_TILE;
           *out = std::move(T);
+          return AXE_OK;
+        }
+        // no legal K2 tile (prime-ish extents, rows at any alignment): a 2-D transpose goes to K9
+        // (4095 x 4097 bf16: 33.9 us vs K1's 78.4 with 2-byte vectors)
+        CopyPlan R = P;
+        if (env_int("AXE_K9", 1) && build_k9(J, ls, ld, *rq.sst, *rq.dstst, es, &R, &w9)) {
+          R.kernel = KK_RAGGED;
+          *out = std::move(R);
           return AXE_OK;
         }
       }
@@ -1114,6 +1130,12 @@ axe_status run_copy(const CopyPlan &p, const void *src, void *dst, cudaStream_t 
       K1Params k = p.k1;
       k.dep = dep;
       e = launch_k1(k, p.vb, p.blocks, src, dst, st);
+      break;
+    }
+    case KK_RAGGED: {
+      K9Params k = p.k9;
+      k.dep = dep;
+      e = launch_k9(k, p.es, src, dst, st);
       break;
     }
     case KK_DUAL: {

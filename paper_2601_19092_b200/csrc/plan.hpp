@@ -13,7 +13,7 @@
 
 namespace axe {
 
-enum KernelKind { KK_GENERIC = 1, KK_VECTOR = 2, KK_TMA = 3, KK_TILE = 4, KK_REGISTER = 5, KK_SHUFFLE = 7, KK_TRANSPOSE = 8, KK_LOWERED = 9, KK_DUAL = 10 };
+enum KernelKind { KK_GENERIC = 1, KK_VECTOR = 2, KK_TMA = 3, KK_TILE = 4, KK_REGISTER = 5, KK_SHUFFLE = 7, KK_TRANSPOSE = 8, KK_LOWERED = 9, KK_DUAL = 10, KK_RAGGED = 11 };
 
 struct CopyPlan {
   int kernel = KK_GENERIC;
@@ -48,6 +48,8 @@ struct CopyPlan {
   K7Params k7;
   // K8 dual decoding (non-nested digit systems)
   K8Params k8;
+  // K9 ragged transpose
+  K9Params k9;
   // the paper's TMA lowering as the schedule (tma_region.cpp): plan + destination byte offset of L_S
   std::shared_ptr<axe_tma_plan> lowered;
   int64_t lowered_dst_off = 0;  // byte offset of the L_S image (the destination, or the source when storing)
@@ -82,6 +84,9 @@ cudaError_t launch_k6(const K6Params &p, unsigned blocks, const void *src, void 
 bool build_k7(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,
               const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why);
 cudaError_t launch_k7(const K7Params &p, int es, unsigned blocks, const void *src, void *dst, cudaStream_t st);  // K3 as K1-TMA mode 2 + movmatrix in smem
+bool build_k9(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,
+              const Storage &dstst, int es, CopyPlan *P, std::string *why);
+cudaError_t launch_k9(const K9Params &p, int es, const void *src, void *dst, cudaStream_t st);
 bool build_k8(const Linear &ls, const Linear &ld, const Storage &sst, const Storage &dstst, int es, int max_align,
               CopyPlan *P, std::string *why);
 cudaError_t launch_k8(const K8Params &p, int vb, const void *src, void *dst, cudaStream_t st);

@@ -102,6 +102,25 @@ def test_lowered_large_boxes(axe, rev, tr, tc, es):
     assert d["kernel"] == "lowered" and d["box_bytes"] == tr * tc * es, d
 
 
+@pytest.mark.parametrize("R,Cn,es,pad_s,pad_d,B,reps", [
+    (4095, 4097, 2, 0, 0, 1, 1), (8000, 8000, 2, 0, 0, 1, 1), (333, 777, 1, 5, 3, 2, 1), (130, 70, 4, 1, 0, 3, 2),
+    (65, 129, 8, 0, 7, 1, 1), (31, 33, 16, 2, 2, 2, 3), (1, 1000, 2, 0, 0, 1, 1), (1000, 2, 4, 3, 0, 1, 1),
+    (4096, 4097, 4, 0, 0, 1, 1)])
+def test_ragged_transposes(axe, R, Cn, es, pad_s, pad_d, B, reps):
+    """K9 (the fallback of K7 and K2): 2-D transposes with ragged extents and pitches that are not whole
+    16-byte vectors (rows starting at any element alignment), padded pitches, a batch digit, destination
+    replicas, 1..16-byte elements -- against the oracle, through AUTO and forced."""
+    lds, ldd = Cn + pad_s, R + pad_d
+    src = layout([(B, R * lds), (R, lds), (Cn, 1)])
+    dst = layout([(B, Cn * ldd), (R, 1), (Cn, ldd)], [(reps, B * Cn * ldd)] if reps > 1 else [])
+    cfg = dict(name=f"rag{R}x{Cn}x{es}", es=es, src=src, src_st=linear_storage(B * R * lds), dst=dst,
+               dst_st=linear_storage(reps * B * Cn * ldd), seed=R * 7 + Cn + es)
+    check(axe, cfg)                      # AUTO: K2 where a legal tile exists, else K9
+    if R > 1 and Cn > 1:                 # (a single row is a plain copy)
+        d = check(axe, cfg, "transpose")  # forced transpose: K7 cannot run these, so K9
+        assert d["kernel"] == "transpose" and d.get("mode") == "ragged", d
+
+
 @pytest.mark.parametrize("R,Cn,es", [(8192, 8192, 2), (8192, 8192, 4), (8192, 4096, 8)])
 def test_bench_transposes_full_size(axe, R, Cn, es):
     """bench.py's transpose rows at the size it times (K7, the AUTO plan), every byte against the oracle."""

@@ -70,6 +70,11 @@ CONFIGS = {
     "transpose_bf16": lambda: transpose_cfg(8192, 8192, 2),
     "transpose_f32": lambda: transpose_cfg(8192, 8192, 4),
     "transpose_f64": lambda: transpose_cfg(8192, 4096, 8),
+    "transpose_bf16_8000": lambda: transpose_cfg(8000, 8000, 2),
+    "transpose_f32_8000x8192": lambda: transpose_cfg(8000, 8192, 4),
+    "transpose_bf16_4095x4097": lambda: transpose_cfg(4095, 4097, 2),
+    "transpose_f32_4095x4097": lambda: transpose_cfg(4095, 4097, 4),
+    "transpose_u8_8191x8193": lambda: transpose_cfg(8191, 8193, 1),
     # padded pitches (8192 + 32 elements on both sides): does the 32 KiB power-of-two stride matter?
     "transpose_f32_pad": lambda: dict(name="transpose_f32_pad", es=4,
                                       src=synth.layout([(8192, 8224), (8192, 1)]),
