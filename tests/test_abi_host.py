@@ -188,6 +188,18 @@ def test_nonnested_with_common_factor_plans_dual():
     assert d["outer_src"] == [[6, 12], [2, 4]] and d["outer_dst"] == [[4, 16], [3, 4]], d
 
 
+def test_ragged_transposes_plan_k9():
+    """Transposes K7 cannot take (rows not whole 16-byte vectors) and K2 cannot tile (4095 = 3^2.5.7.13,
+    4097 = 17.241) plan K9, the element-granular tile transpose; one whose extents factor stays on K2."""
+    for R, C, es in [(4095, 4097, 2), (8191, 8193, 1), (333, 777, 4)]:
+        d = axe.CopyPlan(layout([(R, C), (C, 1)]), linear_storage(R * C), layout([(R, 1), (C, R)]),
+                         linear_storage(R * C), es).describe()
+        assert d["kernel"] == "transpose" and d["mode"] == "ragged", (R, C, es, d)
+    d = axe.CopyPlan(layout([(8000, 8000), (8000, 1)]), linear_storage(8000 * 8000), layout([(8000, 1), (8000, 8000)]),
+                     linear_storage(8000 * 8000), 2).describe()
+    assert d["kernel"] == "tile", d
+
+
 def test_plan_errors():
     st = linear_storage(16)
     cases = [
