@@ -315,6 +315,11 @@ struct K9Params {
   Swz ssw, dsw;
   int nrep;
   int64_t rep[K1_MAXREP];
+  // vector-load form (vec = 1; 16-byte aligned source buffer): every tile row is fetched as the 16-byte
+  // chunks covering it (whatever its alignment); chunks at or past src_limit (the source storage's bytes
+  // rounded up to 16) are not read
+  int vec;
+  int64_t src_limit;
   int dep;
 };
 

@@ -75,14 +75,20 @@ bool build_k9(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   k.dsw = make_swz(dstst);
   k.nrep = (int)reps.size();
   for (size_t i = 0; i < reps.size(); i++) k.rep[i] = reps[i] * es;
-  P->align = es;
+  // vector-load form: source buffers 16-byte aligned (the plan's alignment), 1..8-byte elements, the
+  // source pitch positive (rows fetched as whole 16-byte chunks)
+  const char *ve = getenv("AXE_K9_VEC");
+  k.vec = (es <= 8 && B.ss > 0 && !(ve && *ve == '0')) ? 1 : 0;
+  k.src_limit = (sst.cells * es + 15) / 16 * 16;
+  P->align = k.vec ? 16 : es;
   int64_t total = 1;
   for (auto &j : J0) total *= j.e;
   P->covers_all = (int64_t)reps.size() * total == dstst.cells;
   char buf[256];
   snprintf(buf, sizeof buf,
-           "{\"kernel\":\"transpose\",\"mode\":\"ragged\",\"tile\":[%lld,%lld],\"tiles\":%lld,\"replicas\":%d,\"joint\":",
-           (long long)TB, (long long)TA, (long long)nt, k.nrep);
+           "{\"kernel\":\"transpose\",\"mode\":\"ragged\",\"vector_loads\":%d,\"tile\":[%lld,%lld],\"tiles\":%lld,"
+           "\"replicas\":%d,\"joint\":",
+           k.vec, (long long)TB, (long long)TA, (long long)nt, k.nrep);
   P->desc = std::string(buf) + joint_json(J0) + "}";
   return true;
 }

@@ -106,10 +106,13 @@ def test_lowered_large_boxes(axe, rev, tr, tc, es):
     (4095, 4097, 2, 0, 0, 1, 1), (8000, 8000, 2, 0, 0, 1, 1), (333, 777, 1, 5, 3, 2, 1), (130, 70, 4, 1, 0, 3, 2),
     (65, 129, 8, 0, 7, 1, 1), (31, 33, 16, 2, 2, 2, 3), (1, 1000, 2, 0, 0, 1, 1), (1000, 2, 4, 3, 0, 1, 1),
     (4096, 4097, 4, 0, 0, 1, 1)])
-def test_ragged_transposes(axe, R, Cn, es, pad_s, pad_d, B, reps):
+@pytest.mark.parametrize("vec", ["1", "0"])
+def test_ragged_transposes(axe, R, Cn, es, pad_s, pad_d, B, reps, vec, monkeypatch):
     """K9 (the fallback of K7 and K2): 2-D transposes with ragged extents and pitches that are not whole
     16-byte vectors (rows starting at any element alignment), padded pitches, a batch digit, destination
-    replicas, 1..16-byte elements -- against the oracle, through AUTO and forced."""
+    replicas, 1..16-byte elements -- against the oracle, through AUTO and forced; the vector-load form
+    (16-byte chunks covering each tile row at any alignment) and the element form."""
+    monkeypatch.setenv("AXE_K9_VEC", vec)
     lds, ldd = Cn + pad_s, R + pad_d
     src = layout([(B, R * lds), (R, lds), (Cn, 1)])
     dst = layout([(B, Cn * ldd), (R, 1), (Cn, ldd)], [(reps, B * Cn * ldd)] if reps > 1 else [])
