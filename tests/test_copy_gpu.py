@@ -483,6 +483,34 @@ def test_dependent_chain_with_pdl(axe, kernel):
     assert torch.equal(c, x)
 
 
+def test_prefetch_before_wait_raw_chains(axe):
+    """The kernels prefetch their first boxes / tiles into L2 BEFORE griddepcontrol.wait (reading R28), i.e.
+    while the previous kernel may still be writing those very bytes.  RAW chains at the bench's size:
+    forward (lowered, TMA tensor loads + L2 tensor prefetch) then reverse (lowered, bulk prefetch) then K7
+    transposes there and back (line prefetches), each reading what the kernel before it is writing; fresh
+    data every round, compared at the end of every round."""
+    n = 4096
+    fwd, rev = synth.config2(n), synth.config2(n, reverse=True)
+    pf = axe.CopyPlan(fwd["src"], fwd["src_st"], fwd["dst"], fwd["dst_st"], 2)
+    pr = axe.CopyPlan(rev["src"], rev["src_st"], rev["dst"], rev["dst_st"], 2)
+    rm, cm = layout([(n, n), (n, 1)]), layout([(n, 1), (n, n)])
+    pt = axe.CopyPlan(rm, linear_storage(n * n), cm, linear_storage(n * n), 2)
+    ptb = axe.CopyPlan(cm, linear_storage(n * n), rm, linear_storage(n * n), 2, "transpose")
+    assert pf.describe()["kernel"] == "lowered" and pr.describe()["kernel"] == "lowered"
+    assert pt.describe()["kernel"] == "transpose"
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a, b, c, d = (torch.empty(n * n // 2, dtype=torch.int32, device="cuda") for _ in range(4))
+    for _ in range(30):
+        x = torch.randint(-2**31, 2**31 - 1, (n * n // 2,), dtype=torch.int32, device="cuda", generator=g)
+        a.copy_(x)
+        pf.execute(a, b)     # b <- tiles(a)
+        pr.execute(b, c)     # c <- rowmajor(b) = x      (reads b while pf may still write it)
+        pt.execute(c, d)     # d <- c^T                  (reads c while pr may still write it)
+        ptb.execute(d, a)    # a <- d^T = x              (reads d while pt may still write it)
+        torch.cuda.synchronize()
+        assert torch.equal(c, x) and torch.equal(a, x)
+
+
 def test_lowered_schedule_in_pdl_chains(axe):
     """The lowered schedule joins the PDL window like every copy kernel: dependent chains forward
     (lowered) / reverse (TMA store) return the input; independent lowered copies overlap."""
