@@ -969,6 +969,7 @@ axe_status axe_redistribute_reduce(const axe_layout *src, const axe_storage *src
     p = std::make_shared<axe_redist_plan>();
     AXE_TRY(plan_redist_reduce(src->L, ss, dst->L, ds, dtype, comm->nranks, comm->rank, p.get()));
     std::lock_guard<std::mutex> lk(mu);
+    if (cache.size() >= 256) cache.clear();  // (plans hold staging memory; callers keep their own copies)
     cache[key] = p;
   }
   return serialized(p.get(), comm, (cudaStream_t)stream,
@@ -1128,6 +1129,7 @@ axe_status axe_redistribute(const axe_layout *src, const axe_storage *src_st, co
     p = std::make_shared<axe_redist_plan>();
     AXE_TRY(plan_redist(src->L, ss, dst->L, ds, elem_size, comm->nranks, comm->rank, p.get()));
     std::lock_guard<std::mutex> lk(mu);
+    if (cache.size() >= 256) cache.clear();  // (plans hold staging memory; callers keep their own copies)
     cache[key] = p;
   }
   return serialized(p.get(), comm, (cudaStream_t)stream,
