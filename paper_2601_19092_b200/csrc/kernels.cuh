@@ -179,8 +179,25 @@ struct TrParams {
 // K4T (kernels_reduce.cu k4_tma): the K summand tensor maps of a reduction into a TMA-swizzled destination
 // (one lowered-region map per summand, base = source + that summand's offset), 128 bytes each
 constexpr int K4T_MAXK = 8;
+constexpr int K4_MAXD_FWD = 12;  // (= K4_MAXD, declared below)
 struct K4TMaps {
   alignas(64) unsigned char m[K4T_MAXK][128];
+};
+
+// K4B (kernels_reduce.cu k4_bulk): a reduction whose innermost output run is contiguous on both sides (and on
+// every summand), unswizzled: output boxes of `box` bytes; box b = (run o, piece r), the run's source and
+// destination byte offsets decoded over the outer output digits; K cp.async.bulk summand loads per box
+struct K4BParams {
+  uint32_t nboxes, box, stages, prefetch;
+  FastDiv per_run;                     // boxes per run
+  int nd;                              // outer output digits, outermost first
+  FastDiv fd[K4_MAXD_FWD];
+  int64_t ss[K4_MAXD_FWD], ds[K4_MAXD_FWD];
+  int64_t sbase, dbase;
+  int K;
+  int64_t koff[K4T_MAXK];
+  TmaReps reps;
+  int dep;
 };
 
 struct TmaParams {

@@ -444,7 +444,145 @@ __global__ void __launch_bounds__(K4T_THREADS, 1) k4_tma(const __grid_constant__
   if (t == 0) bulk_wait_read<0>();
 }
 
+
+// K4B: the same ring and in-smem sum as K4T for a reduction whose innermost output run is contiguous on both
+// sides and unswizzled (row-major partials summed into a row-major output): the K summand pieces of each
+// output box arrive by cp.async.bulk from source + koff[k] + the run's offset, the sum overwrites summand 0
+// in shared memory and leaves as one bulk store per replica.
+template <int DT>
+__global__ void __launch_bounds__(K4T_THREADS, 1) k4_bulk(const __grid_constant__ K4BParams p,
+                                                         const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
+  using O = Op<DT>;
+  using S = typename O::S;
+  using A = typename O::A;
+  constexpr int V = 16 / (int)sizeof(S);
+  extern __shared__ __align__(128) uint8_t raw[];
+  __shared__ __align__(8) uint64_t full[K4T_STAGES];
+  uint8_t *sm = (uint8_t *)(((uintptr_t)raw + 127) & ~(uintptr_t)127);
+  const int t = threadIdx.x;
+  const uint32_t NS = p.stages, box = p.box, slot = (box + 127) & ~127u;
+  const int K = p.K;
+  const uint32_t stage = (uint32_t)K * slot;
+  const uint32_t lo = blockIdx.x, bstep = gridDim.x;
+  const uint32_t mine = lo < p.nboxes ? (p.nboxes - lo + bstep - 1) / bstep : 0;
+  auto addr = [&](uint32_t b, int64_t &so, int64_t &dof) {
+    uint32_t o = fdiv(p.per_run, b);
+    const int64_t r = (int64_t)(b - o * p.per_run.d) * box;
+    so = p.sbase + r;
+    dof = p.dbase + r;
+    for (int k = p.nd - 1; k >= 0; k--) {
+      uint32_t d;
+      if (k > 0) {
+        const uint32_t q = fdiv(p.fd[k], o);
+        d = o - q * p.fd[k].d;
+        o = q;
+      } else {
+        d = o;
+      }
+      so += (int64_t)d * p.ss[k];
+      dof += (int64_t)d * p.ds[k];
+    }
+  };
+  if (t == 0) {
+    for (uint32_t s = 0; s < NS; s++) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (p.dep) {  // L2 prefetches while the previous kernel drains (R28)
+      const uint32_t np = mine < p.prefetch ? mine : p.prefetch;
+      for (uint32_t k = 0; k < np; k++) {
+        int64_t so, dof;
+        addr(lo + k * bstep, so, dof);
+        for (int kk = 0; kk < K; kk++) bulk_prefetch(src + so + p.koff[kk], box);
+      }
+    }
+  }
+  __syncthreads();
+  if (p.dep) pdl_wait();
+  pdl_launch_dependents();
+  auto issue = [&](uint32_t k) {
+    const uint32_t s = k % NS;
+    int64_t so, dof;
+    addr(lo + k * bstep, so, dof);
+    mbar_expect_tx(&full[s], (uint32_t)K * box);
+    for (int kk = 0; kk < K; kk++)
+      bulk_load(sm + (size_t)s * stage + (size_t)kk * slot, src + so + p.koff[kk], box, &full[s]);
+  };
+  if (t == 0)
+    for (uint32_t k = 0; k < mine && k < NS; k++) issue(k);
+  for (uint32_t k = 0; k < mine; k++) {
+    const uint32_t s = k % NS;
+    mbar_wait(&full[s], (k / NS) & 1u);
+    uint8_t *st = sm + (size_t)s * stage;
+    for (uint32_t v = t; v < box / 16; v += K4T_THREADS) {
+      A acc[V];
+#pragma unroll
+      for (int i = 0; i < V; i++) acc[i] = A(0);
+      for (int kk = 0; kk < K; kk++) {  // k order
+        alignas(16) S e[V];
+        *reinterpret_cast<uint4 *>(e) = *reinterpret_cast<const uint4 *>(st + (size_t)kk * slot + v * 16);
+#pragma unroll
+        for (int i = 0; i < V; i++) acc[i] = O::add(acc[i], O::in(e[i]));
+      }
+      alignas(16) S o[V];
+#pragma unroll
+      for (int i = 0; i < V; i++) o[i] = O::out(acc[i]);
+      *reinterpret_cast<uint4 *>(st + v * 16) = *reinterpret_cast<const uint4 *>(o);
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (t == 0) {
+      int64_t so, dof;
+      addr(lo + k * bstep, so, dof);
+      for (int r = 0; r < p.reps.n; r++) bulk_store(dst + dof + p.reps.r[r], st, box);
+      bulk_commit();
+      if (k >= 1 && k - 1 + NS < mine) {
+        bulk_wait_read<1>();
+        issue(k - 1 + NS);
+      }
+    }
+  }
+  if (t == 0) bulk_wait_read<0>();
+}
+
 }  // namespace
+
+cudaError_t launch_k4_bulk(K4BParams p, int dtype, const void *src, void *dst, cudaStream_t st) {
+  if (p.nboxes == 0) return cudaSuccess;
+  if (p.K < 1 || p.K > K4T_MAXK) return cudaErrorInvalidValue;
+  static int optin = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v;
+  }();
+  const uint32_t slot = (p.box + 127) & ~127u;
+  const size_t budget = (size_t)optin - 2048 - 128;
+  p.stages = (uint32_t)std::min<size_t>(K4T_STAGES, budget / ((size_t)p.K * slot));
+  if (p.stages < 2) return cudaErrorInvalidValue;
+  p.prefetch = std::max<uint32_t>(1, p.stages / 2);
+  const size_t smem = (size_t)p.stages * p.K * slot + 128;
+  const unsigned blocks = (unsigned)std::min<int64_t>(p.nboxes, (int64_t)num_sms());
+  const uint8_t *s = (const uint8_t *)src;
+  uint8_t *d = (uint8_t *)dst;
+  cudaError_t e;
+  switch (dtype) {
+#define K4B_CASE(D)                                                                                   \
+  case D:                                                                                             \
+    e = smem_attr((const void *)k4_bulk<D>, optin - 2048);                                            \
+    if (e == cudaSuccess) e = launch_ex(k4_bulk<D>, dim3(blocks), dim3(K4T_THREADS), smem, st, p, s, d); \
+    break;
+    K4B_CASE(DT_F32)
+    K4B_CASE(DT_F64)
+    K4B_CASE(DT_F16)
+    K4B_CASE(DT_BF16)
+    K4B_CASE(DT_I32)
+    K4B_CASE(DT_I64)
+#undef K4B_CASE
+    default: return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
+  g_launches++;
+  return cudaGetLastError();
+}
 
 // K4T launch: stages (K boxes each) as many as the shared memory holds (>= 2), one CTA per SM
 cudaError_t launch_k4_tma(const K4TMaps &maps, TrParams p, int K, int dtype, cudaStream_t st) {

@@ -203,6 +203,38 @@ def test_k4t_tma_sum_into_swizzled_tiles(axe, K, dtype, reps):
     assert d["kernel"] == "reduce" and d["mode"] == "tma", d
 
 
+@pytest.mark.parametrize("K,dtype,rows,cols,ld,reps", [
+    (2, "bf16", 64, 512, 512, 1), (3, "f32", 48, 1024, 1040, 1), (8, "f16", 32, 2048, 2048, 2), (5, "f64", 16, 256, 264, 1),
+    (4, "i32", 40, 1024, 1028, 1), (8, "bf16", 96, 4096, 4096, 1), (7, "i64", 8, 512, 512, 3)])
+def test_k4b_bulk_boxes(axe, K, dtype, rows, cols, ld, reps, monkeypatch):
+    """K4B: contiguous output runs (whole rows, or each padded row when ld > cols) arrive as cp.async.bulk
+    boxes from every summand, the sum in shared memory in k order, one bulk store per replica (AUTO takes it
+    from K = 4; the smaller K are forced here)."""
+    monkeypatch.setenv("AXE_K4_BULK_MIN_K", "2")
+    src = layout([(K, rows * ld), (rows, ld), (cols, 1)])
+    dst = layout([(rows, cols), (cols, 1)], [(reps, rows * cols)] if reps > 1 else [])
+    cfg = dict(src=src, src_st=linear_storage(K * rows * ld), dst=dst, dst_st=linear_storage(reps * rows * cols))
+    d = run_local(axe, cfg, dtype, seed=K * 5 + rows)
+    assert d["kernel"] == "reduce" and d["mode"] == "bulk" and d["replicas"] == reps, d
+
+
+def test_k4b_matches_vector_form_bitwise(axe, monkeypatch):
+    """K4B performs K4's arithmetic: its output equals the vector kernel's bit for bit (bench shape, scaled)."""
+    cfg = synth.reduce_local(8, 1024, 1024, "f32")
+    vals = synth.numbers(8 * 1024 * 1024, "f32", 78)
+    s = torch.from_numpy(vals.copy()).cuda()
+    outs = []
+    for bulk in ("1", "0"):
+        monkeypatch.setenv("AXE_K4_BULK", bulk)
+        p = axe.ReducePlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], "f32")
+        assert p.describe()["mode"] == ("bulk" if bulk == "1" else "vector")
+        o = torch.zeros(1024 * 1024, dtype=torch.int32, device="cuda")
+        p.execute(s, o)
+        torch.cuda.synchronize()
+        outs.append(o.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+
+
 def test_k4t_matches_vector_form_bitwise(axe, monkeypatch):
     """K4T performs K4's arithmetic (fp32 accumulators in k order from 0, one rounding): its output equals the
     vector kernel's bit for bit on the bench's shape scaled down."""

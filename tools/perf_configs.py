@@ -128,6 +128,7 @@ REDUCE = {
     "reduce_f32_k8": lambda: synth.reduce_local(8, 8192, 2048, "f32"),
     "reduce_bf16_k2": lambda: synth.reduce_local(2, 16384, 8192, "bf16"),
     "reduce_bf16_k4": lambda: synth.reduce_local(4, 16384, 4096, "bf16"),
+    "reduce_bf16_k3": lambda: synth.reduce_local(3, 16384, 8192, "bf16"),
     "reduce_bf16_k16": lambda: synth.reduce_local(16, 4096, 4096, "bf16"),
 }
 
