@@ -284,7 +284,14 @@ axe_status axe_copy_plan_create(const axe_layout *src, const axe_storage *src_st
  * stream), asynchronously.  src_ptr / dst_ptr are DEVICE pointers to buffers
  * of the storage sizes; the caller owns them.  Errors: AXE_ERR_ALIGNMENT (the
  * pointers are not aligned to the plan's vector width), AXE_ERR_ALIAS,
- * AXE_ERR_CUDA.  Launch count: 1 kernel. */
+ * AXE_ERR_CUDA.  Launch count: 1 kernel.
+ * Stream order: every libaxe kernel is launched with programmatic dependent
+ * launch and waits (griddepcontrol.wait) for all work before it on the stream
+ * before it touches its data; before that wait it may only prefetch its own
+ * source into L2 (reading R28: a prefetch cannot observe stale data).  With
+ * AXE_PDL_OVERLAP=1 (opt-in) a kernel proven disjoint from every libaxe kernel
+ * in flight on its stream skips the wait -- only for streams that carry no
+ * foreign kernels that trigger their dependents early. */
 axe_status axe_copy_plan_execute(const axe_copy_plan *plan, const void *src_ptr, void *dst_ptr, void *cuda_stream);
 /* As axe_copy_plan_create, with the host pipeline of axe_copy_plan_execute_host
  * cut into at most host_slabs slabs (0: the default, 8 or AXE_HOST_CHUNKS).
