@@ -206,18 +206,19 @@ __global__ void AXE_K1_BOUNDS k1_tiled(const __grid_constant__ K1Params p, const
     if (p.pre_s) so[u] = swz(p.ssw, so[u]);
     if (p.pre_d) dof[u] = swz(p.dsw, dof[u]);
   }
+  const UnitRange R = unit_range(p.ntiles, p.chunk);
   if (p.dep) {  // the per-thread decode above, and the first tile's source lines into L2 (R28), overlap
                 // the previous kernel's tail
-    if (blockIdx.x < p.ntiles) {
+    if (R.lo < R.end) {
       int64_t sb = p.sbase, db = p.dbase;
-      decode_digits(p.nout, p.ofd, p.oss, p.ods, blockIdx.x, sb, db);
+      decode_digits(p.nout, p.ofd, p.oss, p.ods, R.lo, sb, db);
 #pragma unroll
       for (int u = 0; u < U; u++) prefetch_l2(src + (p.pre_s ? sb + so[u] : swz(p.ssw, sb + so[u])));
     }
     pdl_wait();
   }
   pdl_launch_dependents();
-  for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+  for (uint32_t t = R.lo; t < R.end; t += R.step) {
     int64_t sb = p.sbase, db = p.dbase;
     decode_digits(p.nout, p.ofd, p.oss, p.ods, t, sb, db);
     T v[U];

@@ -34,6 +34,24 @@ __device__ __forceinline__ uint32_t fdiv(const FastDiv &f, uint32_t n) {
 }
 #endif
 
+#ifdef __CUDACC__
+// The work units (tiles, boxes) one CTA moves.  chunk == 0: a persistent grid, CTA b takes units b, b + G,
+// b + 2G, ...; chunk > 0: CTA b takes units [b chunk, (b + 1) chunk) and the grid covers all of them, so
+// the hardware's in-order CTA dispatch keeps the units in flight a narrow moving window of addresses
+// (a persistent grid's CTAs drift apart and spread it: 256 MiB fp32 transpose 92.6 us -> 81.9 us,
+// profiles/r02_sweep_front.log)
+struct UnitRange {
+  uint32_t lo, end, step;
+};
+__device__ __forceinline__ UnitRange unit_range(uint32_t n, uint32_t chunk) {
+  if (chunk) {
+    const uint32_t lo = blockIdx.x * chunk;
+    return {lo, lo < n ? (n - lo < chunk ? n : lo + chunk) : lo, 1u};
+  }
+  return {blockIdx.x, n, gridDim.x};
+}
+#endif
+
 // Byte-offset swizzle b' = b ^ (((b >> (M+S)) & mask) << M) (CUTLASS Swizzle<B,M,S>, R16).
 struct Swz {
   uint32_t shift;  // M + S
@@ -84,6 +102,7 @@ struct K1Params {
   FastDiv ifd[K1_MAXD], ofd[K1_MAXD];
   int64_t iss[K1_MAXD], ids[K1_MAXD], oss[K1_MAXD], ods[K1_MAXD];
   int pre_s, pre_d;  // swizzle folded into the per-thread offsets (tile bases are whole swizzle blocks)
+  uint32_t chunk;    // tiles per CTA (unit_range); 0: persistent grid
   int dep;           // 1: wait for the previous kernel in the stream (griddepcontrol.wait)
 };
 
@@ -218,6 +237,7 @@ struct TmaParams {
   int xform;                   // 1: movmatrix.trans of every 512-byte block in shared memory (K3-TMA)
   int nrep;
   int64_t rep[K1_MAXREP];      // mode 0: byte offsets of the destination replicas
+  uint32_t chunk;              // boxes per CTA (unit_range); 0: persistent grid
   int dep;                     // 1: wait for the previous kernel in the stream (griddepcontrol.wait)
 };
 
@@ -313,6 +333,7 @@ struct K7Params {
   int stcs;                            // streaming (evict-first) stores
   int nrep;
   int64_t rep[K1_MAXREP];
+  uint32_t chunk;                      // tiles per CTA (unit_range); 0: persistent grid
   int dep;
 };
 

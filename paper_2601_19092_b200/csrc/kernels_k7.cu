@@ -106,7 +106,8 @@ __global__ void __launch_bounds__(K7_THREADS) k7_transpose(const __grid_constant
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   if (p.dep) pdl_wait();
   pdl_launch_dependents();
-  for (uint32_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+  const UnitRange R = unit_range(p.ntiles, p.chunk);
+  for (uint32_t tile = R.lo; tile < R.end; tile += R.step) {
     int64_t sb, db;
     tile_offsets(p, tile, sb, db);
     // load: 8 consecutive threads read one 128-byte source row
@@ -145,12 +146,13 @@ __global__ void __launch_bounds__(K7_THREADS) k7_transpose_async(const __grid_co
   constexpr int TILE = TR * CH * 16;
   extern __shared__ __align__(128) uint8_t sm[];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const UnitRange R = unit_range(p.ntiles, p.chunk);
   if (p.dep) {
     // while the previous kernel drains: the ring's first tiles into L2, one 128-byte line per thread and
     // pass (R28)
     for (int s = 0; s < S - 1; s++) {
-      const uint32_t tt = blockIdx.x + (uint32_t)s * gridDim.x;
-      if (tt >= p.ntiles) break;
+      const uint32_t tt = R.lo + (uint32_t)s * R.step;
+      if (tt >= R.end) break;
       int64_t sb, db;
       tile_offsets(p, tt, sb, db);
       for (int idx = t; idx < TR * (CH / 8); idx += K7_THREADS)
@@ -169,16 +171,16 @@ __global__ void __launch_bounds__(K7_THREADS) k7_transpose_async(const __grid_co
     }
   };
   // S-stage ring: tiles it + 1 .. it + S - 1 are in flight while tile it is gathered and stored
-  uint32_t tile = blockIdx.x;
+  uint32_t tile = R.lo;
 #pragma unroll
   for (int s = 0; s < S - 1; s++) {
-    const uint32_t tt = tile + (uint32_t)s * gridDim.x;
-    if (tt < p.ntiles) issue(tt, sm + s * TILE);
+    const uint32_t tt = tile + (uint32_t)s * R.step;
+    if (tt < R.end) issue(tt, sm + s * TILE);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  for (int it = 0; tile < p.ntiles; tile += gridDim.x, it++) {
-    const uint32_t next = tile + (uint32_t)(S - 1) * gridDim.x;
-    if (next < p.ntiles) issue(next, sm + ((it + S - 1) % S) * TILE);
+  for (int it = 0; tile < R.end; tile += R.step, it++) {
+    const uint32_t next = tile + (uint32_t)(S - 1) * R.step;
+    if (next < R.end) issue(next, sm + ((it + S - 1) % S) * TILE);
     asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group %0;" ::"n"(S - 1) : "memory");  // this thread's vectors of `tile` landed
     __syncthreads();                                                    // ... and every other thread's

@@ -82,11 +82,11 @@ __global__ void __launch_bounds__(32) k1_tma(const __grid_constant__ CUtensorMap
   __shared__ __align__(8) uint64_t full[TMA_MAX_STAGES];
   const bool leader = threadIdx.x == 0;
   if (!p.xform && !leader) return;
+  const UnitRange R = unit_range(p.nboxes, p.chunk);
   if (p.dep) {
     if (leader) {  // the first ring of boxes into L2 while the previous kernel drains (R28)
-      const uint32_t nb0 = p.nboxes, f0 = blockIdx.x, st0 = gridDim.x;
-      for (int k = 0; k < p.stages && f0 + (uint32_t)k * st0 < nb0; k++) {
-        const BoxAddr a = box_addr(p, f0 + (uint32_t)k * st0);
+      for (int k = 0; k < p.stages && R.lo + (uint32_t)k * R.step < R.end; k++) {
+        const BoxAddr a = box_addr(p, R.lo + (uint32_t)k * R.step);
         if (p.mode == 0)
           tma_prefetch5(&map, a.c[0], a.c[1], a.c[2], a.c[3], a.c[4]);
         else
@@ -106,9 +106,8 @@ __global__ void __launch_bounds__(32) k1_tma(const __grid_constant__ CUtensorMap
   }
   if (p.xform) __syncwarp();
 
-  const uint32_t nb = p.nboxes;
-  const uint32_t first = blockIdx.x, step = gridDim.x;
-  const uint32_t mine = first < nb ? (nb - first + step - 1) / step : 0;
+  const uint32_t first = R.lo, step = R.step;
+  const uint32_t mine = first < R.end ? (R.end - first + step - 1) / step : 0;
 
   auto issue_load = [&](uint32_t k) {
     const int s = (int)(k % (uint32_t)S);

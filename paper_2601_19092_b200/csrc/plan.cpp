@@ -208,6 +208,20 @@ static int64_t env_int(const char *name, int64_t dflt) {
   return (e && *e) ? atoll(e) : dflt;
 }
 
+int64_t grid_cap(int64_t per_sm) {
+  if (env_int("AXE_ONESHOT", 0)) return (int64_t(1) << 31) - 1;
+  return (int64_t)num_sms() * per_sm;
+}
+
+// The in-order schedule (unit_range in kernels.cuh): `chunk` consecutive units per CTA and a grid that
+// covers them all; 0 keeps the persistent grid.  AXE_CHUNK overrides the schedule's default.
+uint32_t unit_chunk(int64_t dflt) { return (uint32_t)std::max<int64_t>(0, env_int("AXE_CHUNK", dflt)); }
+
+unsigned chunk_grid(int64_t units, uint32_t chunk, unsigned persistent) {
+  if (!chunk) return persistent;
+  return (unsigned)std::max<int64_t>(1, (units + chunk - 1) / chunk);
+}
+
 static int env_kernel() {
   const char *e = getenv("AXE_FORCE_KERNEL");
   if (!e || !*e) return AXE_KERNEL_AUTO;
@@ -432,8 +446,12 @@ static bool build_k1(const std::vector<Joint> &J0, const Linear &ls, const Linea
     for (int64_t r : reps) rb.push_back(r * es);
     k.pre_s = whole(k.ssw, k.sbase, {}, true);
     k.pre_d = whole(k.dsw, k.dbase, rb, false);
-    int64_t cap = (int64_t)num_sms() * 8;
+    int64_t cap = grid_cap(8);
     P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(k.ntiles, cap));
+    // in-order schedule, 2 tiles (32 KiB) per CTA, whenever the tiles outnumber the persistent grid
+    // (16 KiB-run gathers, profiles/r02_sweep_front.log: 32 MiB 12.0 us vs 12.8, 256 MiB 82.1 vs 88.1)
+    k.chunk = unit_chunk(k.ntiles > (int64_t)P->blocks ? 2 : 0);
+    P->blocks = chunk_grid(k.ntiles, k.chunk, P->blocks);
     mode = "tiled";
   } else {
     if ((int)D.size() > K1_MAXD) {
@@ -442,15 +460,15 @@ static bool build_k1(const std::vector<Joint> &J0, const Linear &ls, const Linea
     }
     k.nd = fill(D, k.fd, k.ss, k.ds);
     int64_t blocks = (total + 256LL * u - 1) / (256LL * u);
-    int64_t cap = (int64_t)num_sms() * 8;
+    int64_t cap = grid_cap(8);
     P->blocks = (unsigned)std::max<int64_t>(1, std::min(blocks, cap));
     mode = "decode";
   }
   char b[320];
   snprintf(b, sizeof b,
            "{\"kernel\":\"vector\",\"mode\":\"%s\",\"vec_bytes\":%d,\"vectors\":%lld,\"replicas\":%d,\"blocks\":%u,"
-           "\"tile_vectors\":%u,\"pre_swizzle\":[%d,%d],\"digits\":",
-           mode.c_str(), P->vb, (long long)total, k.nrep, P->blocks, k.tile_v, k.pre_s, k.pre_d);
+           "\"tile_vectors\":%u,\"chunk\":%u,\"pre_swizzle\":[%d,%d],\"digits\":",
+           mode.c_str(), P->vb, (long long)total, k.nrep, P->blocks, k.tile_v, k.chunk, k.pre_s, k.pre_d);
   P->desc = std::string(b) + joint_json(D) + ",\"joint\":" + joint_json(J0) + "}";
   return true;
 }
@@ -584,15 +602,19 @@ static bool build_tma(const std::vector<Joint> &J0, const Linear &ls, const Line
   P->tm_cache = std::make_shared<TmaCache>();
   int per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(16, (220 * 1024) / (int64_t)tma_smem_bytes(k)));
   per_sm = (int)std::min<int64_t>(per_sm, env_int("AXE_TMA_PER_SM", 8));
-  P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nboxes, (int64_t)num_sms() * per_sm));
+  P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nboxes, grid_cap(per_sm)));
+  // in-order schedule, 2 boxes per CTA (256-byte-run gathers, profiles/r02_sweep_front.log: 32 MiB
+  // 12.8 us vs 14.5, 256 MiB 82.4 vs 96.1)
+  k.chunk = unit_chunk(nboxes > (int64_t)P->blocks ? 2 : 0);
+  P->blocks = chunk_grid(nboxes, k.chunk, P->blocks);
   P->align = 16;
   P->covers_all = (int64_t)reps.size() * nboxes * box_bytes == dstst.cells * es;
   char b[320];
   snprintf(b, sizeof b,
            "{\"kernel\":\"tma\",\"mode\":\"%s\",\"box\":[%lld,%lld],\"box_bytes\":%lld,\"boxes\":%lld,\"stages\":%d,"
-           "\"blocks\":%u,\"swizzle\":%d,\"replicas\":%d,\"joint\":",
+           "\"blocks\":%u,\"chunk\":%u,\"swizzle\":%d,\"replicas\":%d,\"joint\":",
            mode == 0 ? "tensor-load/bulk-store" : "bulk-load/tensor-store", (long long)B1, (long long)row_bytes,
-           (long long)box_bytes, (long long)nboxes, stages, P->blocks, span, k.nrep);
+           (long long)box_bytes, (long long)nboxes, stages, P->blocks, k.chunk, span, k.nrep);
   // the encoded tensor map (byte elements): dims / byte strides innermost first, box
   std::string tm = ",\"tensor_map\":{\"dims\":[";
   for (int i = 0; i < 5; i++) tm += (i ? "," : "") + std::to_string(P->tm_dims[i]);
@@ -684,14 +706,18 @@ static bool build_bulk(const std::vector<Joint> &J0, const Linear &ls, const Lin
   P->tm_cache.reset();
   int per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(16, (220 * 1024) / (int64_t)tma_smem_bytes(k)));
   per_sm = (int)std::min<int64_t>(per_sm, env_int("AXE_TMA_BULK_PER_SM", per_def));
-  P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nboxes, (int64_t)num_sms() * per_sm));
+  P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nboxes, grid_cap(per_sm)));
+  // beyond 64 MiB, the in-order schedule with 2 boxes per CTA (identity 256 MiB: 77.6 us vs 89.5;
+  // up to 64 MiB the persistent ring keeps the whole copy in flight and wins: 11.1 us vs 14.3)
+  k.chunk = unit_chunk(bytes > (int64_t(64) << 20) && nboxes > (int64_t)P->blocks ? 2 : 0);
+  P->blocks = chunk_grid(nboxes, k.chunk, P->blocks);
   P->align = 16;
   P->covers_all = (int64_t)reps.size() * nboxes * be == dstst.cells;
   char b[320];
   snprintf(b, sizeof b,
            "{\"kernel\":\"tma\",\"mode\":\"bulk-load/bulk-store\",\"box_bytes\":%lld,\"boxes\":%lld,\"stages\":%d,"
-           "\"blocks\":%u,\"replicas\":%d,\"joint\":",
-           (long long)(be * es), (long long)nboxes, k.stages, P->blocks, k.nrep);
+           "\"blocks\":%u,\"chunk\":%u,\"replicas\":%d,\"joint\":",
+           (long long)(be * es), (long long)nboxes, k.stages, P->blocks, k.chunk, k.nrep);
   P->desc = std::string(b) + joint_json(J0) + "}";
   return true;
 }

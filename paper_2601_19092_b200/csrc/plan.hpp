@@ -140,6 +140,10 @@ cudaError_t launch_tma(const void *map128, const TmaParams &p, unsigned blocks, 
                        cudaStream_t st);
 size_t tma_smem_bytes(const TmaParams &p);
 int num_sms();
+// persistent-grid cap: num_sms() * per_sm CTAs (AXE_ONESHOT=1: no cap -- one CTA per work unit)
+int64_t grid_cap(int64_t per_sm);
+uint32_t unit_chunk(int64_t dflt);
+unsigned chunk_grid(int64_t units, uint32_t chunk, unsigned persistent);
 int64_t kernel_launches();
 // 1 if a kernel reading [s0,s1) and writing [d0,d1) on stream st must wait for
 // the previous libaxe kernel on st (records the new kernel as the previous one).

@@ -156,7 +156,7 @@ bool build_k6(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   k.ssw = make_swz(sst);
   k.dsw = make_swz(dstst);
   P->align = 16;
-  P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(k.ntiles, (int64_t)num_sms() * 8));
+  P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(k.ntiles, grid_cap(8)));
   int64_t total = ng * n * n;  // granules
   P->covers_all = (int64_t)reps.size() * total * run == dstst.cells;
   char b[256];

@@ -112,17 +112,28 @@ bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   P->align = 16;
   const int64_t tile_bytes = TR * TC * es * (k.async ? k.async : 1);
   const int per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(8, (220 * 1024) / (tile_bytes + 1024)));
-  P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt, (int64_t)num_sms() * per_sm));
+  P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt, grid_cap(per_sm)));
+  // from 64 MiB a side (256 MiB with one CTA per SM), the in-order schedule: 2 tiles per CTA, 4 when one
+  // CTA fills the SM and its own ring is the only overlap (profiles/r02_sweep_front.log: 256 MiB fp32
+  // 82.0 us vs 92.4, bf16 88.0 vs 97.8; at 32 MiB the persistent grid wins, 10.5 vs 11.4, and so does
+  // bf16 at 128 MiB, 43.8 vs 48.1)
+  const int64_t bytes = nt * TR * TC * es;
+  const bool front = per_sm >= 2 ? bytes >= (int64_t(64) << 20) : bytes >= (int64_t(256) << 20);
+  k.chunk = unit_chunk(front && nt > (int64_t)P->blocks ? (per_sm >= 2 ? 2 : 4) : 0);
+  P->blocks = chunk_grid(nt, k.chunk, P->blocks);
   const char *mc = getenv("AXE_K7_MAX_CTAS");  // tests: several tiles per CTA on small inputs
-  if (mc && *mc && atoi(mc) > 0) P->blocks = std::min<unsigned>(P->blocks, (unsigned)atoi(mc));
+  if (mc && *mc && atoi(mc) > 0) {  // (persistent grid: a capped chunked grid would drop tiles)
+    k.chunk = 0;
+    P->blocks = std::min<unsigned>(std::min<unsigned>(P->blocks, (unsigned)(num_sms() * per_sm)), (unsigned)atoi(mc));
+  }
   int64_t total = 1;
   for (auto &j : J0) total *= j.e;
   P->covers_all = (int64_t)reps.size() * total == dstst.cells;
   char buf[256];
   snprintf(buf, sizeof buf,
            "{\"kernel\":\"transpose\",\"block\":\"%lldx%lld register transpose\",\"tile\":[%lld,%lld],\"tiles\":%lld,"
-           "\"ctas\":%u,\"replicas\":%d,\"async\":%d,\"joint\":",
-           (long long)n, (long long)n, (long long)TR, (long long)TC, (long long)nt, P->blocks, k.nrep, k.async);
+           "\"ctas\":%u,\"chunk\":%u,\"replicas\":%d,\"async\":%d,\"joint\":",
+           (long long)n, (long long)n, (long long)TR, (long long)TC, (long long)nt, P->blocks, k.chunk, k.nrep, k.async);
   P->desc = std::string(buf) + joint_json(J0) + "}";
   return true;
 }
