@@ -298,9 +298,10 @@ __global__ void __launch_bounds__(K1_THREADS) k8_dual(const __grid_constant__ K8
     // uniform over the item (two decodings per item), the inner offset is w times the run's stride
     constexpr uint32_t CH = K1_THREADS * U;
     const uint32_t vin = p.vin.d;
-    if (p.dep && blockIdx.x < p.nitems) {  // the first item's vectors into L2 before the wait (R28)
-      const uint32_t o = fdiv(p.nchunks, blockIdx.x);
-      const uint32_t c = blockIdx.x - o * p.nchunks.d;
+    const UnitRange R = unit_range(p.nitems, p.chunk);
+    if (p.dep && R.lo < R.end) {  // the first item's vectors into L2 before the wait (R28)
+      const uint32_t o = fdiv(p.nchunks, R.lo);
+      const uint32_t c = R.lo - o * p.nchunks.d;
       const int64_t so = p.sbase + k8_digits<K8_MAXD>(p.na, p.afd, p.as, o);
 #pragma unroll
       for (int u = 0; u < U; u++) {
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(K1_THREADS) k8_dual(const __grid_constant__ K8
     }
     if (p.dep) pdl_wait();
     pdl_launch_dependents();
-    for (uint32_t it = blockIdx.x; it < p.nitems; it += gridDim.x) {
+    for (uint32_t it = R.lo; it < R.end; it += R.step) {
       const uint32_t o = fdiv(p.nchunks, it);
       const uint32_t c = it - o * p.nchunks.d;
       const int64_t so = p.sbase + k8_digits<K8_MAXD>(p.na, p.afd, p.as, o);
@@ -435,7 +436,8 @@ static cudaError_t k8_launch(const K8Params &p, const uint8_t *s, uint8_t *d, cu
   const void *kern = (const void *)k8_dual<VB, U>;
   const unsigned want = p.chunked ? p.nitems
                                   : (unsigned)((p.total + (uint64_t)K1_THREADS * U - 1) / ((uint64_t)K1_THREADS * U));
-  const unsigned blocks = one_wave(kern, K1_THREADS, 0, std::max(1u, want));
+  const unsigned blocks = p.chunked && p.chunk ? (p.nitems + p.chunk - 1) / p.chunk
+                                               : one_wave(kern, K1_THREADS, 0, std::max(1u, want));
   return launch_ex(k8_dual<VB, U>, dim3(blocks), dim3(K1_THREADS), 0, st, p, s, d);
 }
 

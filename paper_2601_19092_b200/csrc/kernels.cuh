@@ -143,6 +143,7 @@ struct K8Params {
   // afd[na-1] / bfd[nb-1]) and re-decodes the outer digits only when its innermost digit wraps
   int odo;
   uint32_t nchunk;                     // chunks of K8_ODO_J * 32 elements
+  uint32_t chunk;                      // bulk boxes / chunked-form items per CTA (unit_range); 0: persistent
   int dep;
 };
 constexpr int K8_ODO_J = 64;
@@ -193,30 +194,6 @@ struct TrParams {
   int strided;           // 1: CTA c takes boxes c, c + grid, ... (0: a contiguous range per CTA)
   uint32_t prefetch;     // boxes per CTA pulled into L2 before griddepcontrol.wait
   TmaReps reps;
-};
-
-// K4T (kernels_reduce.cu k4_tma): the K summand tensor maps of a reduction into a TMA-swizzled destination
-// (one lowered-region map per summand, base = source + that summand's offset), 128 bytes each
-constexpr int K4T_MAXK = 8;
-constexpr int K4_MAXD_FWD = 12;  // (= K4_MAXD, declared below)
-struct K4TMaps {
-  alignas(64) unsigned char m[K4T_MAXK][128];
-};
-
-// K4B (kernels_reduce.cu k4_bulk): a reduction whose innermost output run is contiguous on both sides (and on
-// every summand), unswizzled: output boxes of `box` bytes; box b = (run o, piece r), the run's source and
-// destination byte offsets decoded over the outer output digits; K cp.async.bulk summand loads per box
-struct K4BParams {
-  uint32_t nboxes, box, stages, prefetch;
-  FastDiv per_run;                     // boxes per run
-  int nd;                              // outer output digits, outermost first
-  FastDiv fd[K4_MAXD_FWD];
-  int64_t ss[K4_MAXD_FWD], ds[K4_MAXD_FWD];
-  int64_t sbase, dbase;
-  int K;
-  int64_t koff[K4T_MAXK];
-  TmaReps reps;
-  int dep;
 };
 
 struct TmaParams {
@@ -311,6 +288,7 @@ struct K6Params {
   int nrep;
   int64_t rep[K1_MAXREP];
   Swz ssw, dsw;
+  uint32_t chunk;  // tiles per CTA (unit_range); 0: persistent grid
   int dep;
 };
 
@@ -382,6 +360,7 @@ struct K4Params {
   int64_t rep[K1_MAXREP];
   Swz ssw, dsw;
   int stcs;                            // vector form: streaming (evict-first) stores of the sums
+  uint32_t chunk;                      // vector form: blocks of blockDim.x vectors per CTA (unit_range)
   int dep;
 };
 // one-sided (pull) form: summand k is read through its own base pointer (a peer's buffer)

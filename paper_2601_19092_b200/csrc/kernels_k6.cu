@@ -109,7 +109,8 @@ __global__ void __launch_bounds__(K6_THREADS) k6_transpose(const __grid_constant
   }
   if (p.dep) pdl_wait();
   pdl_launch_dependents();
-  for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+  const UnitRange R = unit_range(p.ntiles, p.chunk);
+  for (uint32_t t = R.lo; t < R.end; t += R.step) {
     int64_t sb = p.sbase, db = p.dbase;
     k6_decode(p.nout, p.ofd, p.oss, p.ods, t, sb, db);
     uint4 w[K6_U];

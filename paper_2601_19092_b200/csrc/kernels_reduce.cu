@@ -125,9 +125,10 @@ __device__ __forceinline__ void k4_body(const K4Params &p, const uint64_t *kp, c
   using A = typename O::A;
   constexpr int VB = V * (int)sizeof(S);
   using R = typename RawT<VB>::T;
+  const UnitRange U = unit_range((p.total + blockDim.x - 1) / blockDim.x, p.chunk);
   if (p.dep) {
     // while the previous kernel drains: this thread's first summands into L2 (R28)
-    const uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t i0 = U.lo * blockDim.x + threadIdx.x;
     if (!PEER && p.nk > 0 && i0 < p.total) {
       int64_t so = p.sbase;
       uint32_t rem = i0;
@@ -141,8 +142,9 @@ __device__ __forceinline__ void k4_body(const K4Params &p, const uint64_t *kp, c
     pdl_wait();
   }
   pdl_launch_dependents();
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < p.total; i += stride) {
+  for (uint32_t t = U.lo; t < U.end; t += U.step) {
+    const uint32_t i = t * blockDim.x + threadIdx.x;
+    if (i >= p.total) break;
     int64_t so = p.sbase, dof = p.dbase;
     uint32_t rem = i;
     for (int k = p.nd - 1; k >= 0; k--) {
@@ -273,7 +275,12 @@ __global__ void __launch_bounds__(256) k4_generic(const __grid_constant__ K4GPar
 template <int DT>
 cudaError_t launch_k4_dt(const K4Params &p, int vb, unsigned blocks, const uint8_t *s, uint8_t *d, cudaStream_t st) {
   constexpr int ES = (int)sizeof(typename Op<DT>::S);
-  const dim3 g(blocks), b(K4_THREADS);
+  const dim3 b(K4_THREADS);
+  // persistent: one wave; in-order schedule (p.chunk): every block of K4_THREADS vectors covered
+  auto one_wave = [&](const void *kern, int threads, size_t smem, unsigned want) -> unsigned {
+    if (p.chunk) return (unsigned)(((p.total + K4_THREADS - 1) / K4_THREADS + p.chunk - 1) / p.chunk);
+    return axe::one_wave(kern, threads, smem, want);
+  };
   switch (vb / ES) {
     case 1: return launch_ex(k4_reduce<DT, 1>, dim3(one_wave((const void *)k4_reduce<DT, 1>, K4_THREADS, 0, blocks)), b, 0, st, p, s, d);
     case 2:
@@ -354,274 +361,7 @@ cudaError_t launch_k4p_dt(const K4Params &p, const K4Ptrs &q, int vb, unsigned b
 }
 
 
-// K4T: the reduction into a TMA-swizzled destination (SW128 tiles) with the paper's TMA lowering for every
-// summand.  Each output box (the lowered region's fused atom box, config 2's 64 x 64 tile) arrives as K
-// TMA tensor loads -- one per summand map -- into one ring stage; the hardware applies the destination
-// swizzle to every summand image alike, so summing the K images element by element in k order (fp32 /
-// fp64 accumulators, one rounding: exactly K4's arithmetic) gives the swizzled image of the sum, written
-// in place over summand 0 and leaving as one bulk store per destination replica.  Persistent strided
-// grid; the first half-ring of boxes is prefetched into L2 before griddepcontrol.wait.
-constexpr int K4T_THREADS = 256;
-constexpr int K4T_STAGES = 8;
-
-template <int DT>
-__global__ void __launch_bounds__(K4T_THREADS, 1) k4_tma(const __grid_constant__ K4TMaps maps,
-                                                        const __grid_constant__ TrParams p, int K) {
-  using O = Op<DT>;
-  using S = typename O::S;
-  using A = typename O::A;
-  constexpr int V = 16 / (int)sizeof(S);
-  extern __shared__ __align__(1024) uint8_t raw[];
-  __shared__ __align__(8) uint64_t full[K4T_STAGES];
-  uint8_t *sm = (uint8_t *)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
-  const int t = threadIdx.x;
-  const uint32_t NS = p.stages, slot = p.slot, box = p.box;
-  const uint32_t stage = (uint32_t)K * slot;
-  const uint32_t lo = blockIdx.x, bstep = gridDim.x;
-  const uint32_t mine = lo < p.n ? (p.n - lo + bstep - 1) / bstep : 0;
-  if (t == 0) {
-    for (uint32_t s = 0; s < NS; s++) mbar_init(&full[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int kk = 0; kk < K; kk++) asm volatile("prefetch.tensormap [%0];" ::"l"(maps.m[kk]) : "memory");
-    if (p.dep) {  // L2 prefetches while the previous kernel drains (R28)
-      const uint32_t np = mine < p.prefetch ? mine : p.prefetch;
-      for (uint32_t k = 0; k < np; k++) {
-        int c[5];
-        int64_t off;
-        tr_box(p, lo + k * bstep, c, off);
-        for (int kk = 0; kk < K; kk++) tma_prefetch5(maps.m[kk], c[0], c[1], c[2], c[3], c[4]);
-      }
-    }
-  }
-  __syncthreads();
-  if (p.dep) pdl_wait();
-  pdl_launch_dependents();
-  auto issue = [&](uint32_t k) {
-    const uint32_t s = k % NS;
-    int c[5];
-    int64_t off;
-    tr_box(p, lo + k * bstep, c, off);
-    mbar_expect_tx(&full[s], (uint32_t)K * box);
-    for (int kk = 0; kk < K; kk++)
-      tma_load5(sm + (size_t)s * stage + (size_t)kk * slot, maps.m[kk], &full[s], c[0], c[1], c[2], c[3], c[4]);
-  };
-  if (t == 0)
-    for (uint32_t k = 0; k < mine && k < NS; k++) issue(k);
-  for (uint32_t k = 0; k < mine; k++) {
-    const uint32_t s = k % NS;
-    mbar_wait(&full[s], (k / NS) & 1u);
-    uint8_t *st = sm + (size_t)s * stage;
-    for (uint32_t v = t; v < box / 16; v += K4T_THREADS) {
-      A acc[V];
-#pragma unroll
-      for (int i = 0; i < V; i++) acc[i] = A(0);
-      for (int kk = 0; kk < K; kk++) {  // k order
-        alignas(16) S e[V];
-        *reinterpret_cast<uint4 *>(e) = *reinterpret_cast<const uint4 *>(st + (size_t)kk * slot + v * 16);
-#pragma unroll
-        for (int i = 0; i < V; i++) acc[i] = O::add(acc[i], O::in(e[i]));
-      }
-      alignas(16) S o[V];
-#pragma unroll
-      for (int i = 0; i < V; i++) o[i] = O::out(acc[i]);
-      *reinterpret_cast<uint4 *>(st + v * 16) = *reinterpret_cast<const uint4 *>(o);
-    }
-    fence_async_smem();  // the generic-proxy sums before the async-proxy bulk store reads them
-    __syncthreads();
-    if (t == 0) {
-      int c[5];
-      int64_t off;
-      tr_box(p, lo + k * bstep, c, off);
-      for (int r = 0; r < p.reps.n; r++) bulk_store(p.img + off + p.reps.r[r], st, box);
-      bulk_commit();
-      // refill the stage of box k - 1 once its store has read shared memory
-      if (k >= 1 && k - 1 + NS < mine) {
-        bulk_wait_read<1>();
-        issue(k - 1 + NS);
-      }
-    }
-  }
-  if (t == 0) bulk_wait_read<0>();
-}
-
-
-// K4B: the same ring and in-smem sum as K4T for a reduction whose innermost output run is contiguous on both
-// sides and unswizzled (row-major partials summed into a row-major output): the K summand pieces of each
-// output box arrive by cp.async.bulk from source + koff[k] + the run's offset, the sum overwrites summand 0
-// in shared memory and leaves as one bulk store per replica.
-template <int DT>
-__global__ void __launch_bounds__(K4T_THREADS, 1) k4_bulk(const __grid_constant__ K4BParams p,
-                                                         const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
-  using O = Op<DT>;
-  using S = typename O::S;
-  using A = typename O::A;
-  constexpr int V = 16 / (int)sizeof(S);
-  extern __shared__ __align__(128) uint8_t raw[];
-  __shared__ __align__(8) uint64_t full[K4T_STAGES];
-  uint8_t *sm = (uint8_t *)(((uintptr_t)raw + 127) & ~(uintptr_t)127);
-  const int t = threadIdx.x;
-  const uint32_t NS = p.stages, box = p.box, slot = (box + 127) & ~127u;
-  const int K = p.K;
-  const uint32_t stage = (uint32_t)K * slot;
-  const uint32_t lo = blockIdx.x, bstep = gridDim.x;
-  const uint32_t mine = lo < p.nboxes ? (p.nboxes - lo + bstep - 1) / bstep : 0;
-  auto addr = [&](uint32_t b, int64_t &so, int64_t &dof) {
-    uint32_t o = fdiv(p.per_run, b);
-    const int64_t r = (int64_t)(b - o * p.per_run.d) * box;
-    so = p.sbase + r;
-    dof = p.dbase + r;
-    for (int k = p.nd - 1; k >= 0; k--) {
-      uint32_t d;
-      if (k > 0) {
-        const uint32_t q = fdiv(p.fd[k], o);
-        d = o - q * p.fd[k].d;
-        o = q;
-      } else {
-        d = o;
-      }
-      so += (int64_t)d * p.ss[k];
-      dof += (int64_t)d * p.ds[k];
-    }
-  };
-  if (t == 0) {
-    for (uint32_t s = 0; s < NS; s++) mbar_init(&full[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (p.dep) {  // L2 prefetches while the previous kernel drains (R28)
-      const uint32_t np = mine < p.prefetch ? mine : p.prefetch;
-      for (uint32_t k = 0; k < np; k++) {
-        int64_t so, dof;
-        addr(lo + k * bstep, so, dof);
-        for (int kk = 0; kk < K; kk++) bulk_prefetch(src + so + p.koff[kk], box);
-      }
-    }
-  }
-  __syncthreads();
-  if (p.dep) pdl_wait();
-  pdl_launch_dependents();
-  auto issue = [&](uint32_t k) {
-    const uint32_t s = k % NS;
-    int64_t so, dof;
-    addr(lo + k * bstep, so, dof);
-    mbar_expect_tx(&full[s], (uint32_t)K * box);
-    for (int kk = 0; kk < K; kk++)
-      bulk_load(sm + (size_t)s * stage + (size_t)kk * slot, src + so + p.koff[kk], box, &full[s]);
-  };
-  if (t == 0)
-    for (uint32_t k = 0; k < mine && k < NS; k++) issue(k);
-  for (uint32_t k = 0; k < mine; k++) {
-    const uint32_t s = k % NS;
-    mbar_wait(&full[s], (k / NS) & 1u);
-    uint8_t *st = sm + (size_t)s * stage;
-    for (uint32_t v = t; v < box / 16; v += K4T_THREADS) {
-      A acc[V];
-#pragma unroll
-      for (int i = 0; i < V; i++) acc[i] = A(0);
-      for (int kk = 0; kk < K; kk++) {  // k order
-        alignas(16) S e[V];
-        *reinterpret_cast<uint4 *>(e) = *reinterpret_cast<const uint4 *>(st + (size_t)kk * slot + v * 16);
-#pragma unroll
-        for (int i = 0; i < V; i++) acc[i] = O::add(acc[i], O::in(e[i]));
-      }
-      alignas(16) S o[V];
-#pragma unroll
-      for (int i = 0; i < V; i++) o[i] = O::out(acc[i]);
-      *reinterpret_cast<uint4 *>(st + v * 16) = *reinterpret_cast<const uint4 *>(o);
-    }
-    fence_async_smem();
-    __syncthreads();
-    if (t == 0) {
-      int64_t so, dof;
-      addr(lo + k * bstep, so, dof);
-      for (int r = 0; r < p.reps.n; r++) bulk_store(dst + dof + p.reps.r[r], st, box);
-      bulk_commit();
-      if (k >= 1 && k - 1 + NS < mine) {
-        bulk_wait_read<1>();
-        issue(k - 1 + NS);
-      }
-    }
-  }
-  if (t == 0) bulk_wait_read<0>();
-}
-
 }  // namespace
-
-cudaError_t launch_k4_bulk(K4BParams p, int dtype, const void *src, void *dst, cudaStream_t st) {
-  if (p.nboxes == 0) return cudaSuccess;
-  if (p.K < 1 || p.K > K4T_MAXK) return cudaErrorInvalidValue;
-  static int optin = [] {
-    int dev = 0, v = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    return v;
-  }();
-  const uint32_t slot = (p.box + 127) & ~127u;
-  const size_t budget = (size_t)optin - 2048 - 128;
-  p.stages = (uint32_t)std::min<size_t>(K4T_STAGES, budget / ((size_t)p.K * slot));
-  if (p.stages < 2) return cudaErrorInvalidValue;
-  p.prefetch = std::max<uint32_t>(1, p.stages / 2);
-  const size_t smem = (size_t)p.stages * p.K * slot + 128;
-  const unsigned blocks = (unsigned)std::min<int64_t>(p.nboxes, (int64_t)num_sms());
-  const uint8_t *s = (const uint8_t *)src;
-  uint8_t *d = (uint8_t *)dst;
-  cudaError_t e;
-  switch (dtype) {
-#define K4B_CASE(D)                                                                                   \
-  case D:                                                                                             \
-    e = smem_attr((const void *)k4_bulk<D>, optin - 2048);                                            \
-    if (e == cudaSuccess) e = launch_ex(k4_bulk<D>, dim3(blocks), dim3(K4T_THREADS), smem, st, p, s, d); \
-    break;
-    K4B_CASE(DT_F32)
-    K4B_CASE(DT_F64)
-    K4B_CASE(DT_F16)
-    K4B_CASE(DT_BF16)
-    K4B_CASE(DT_I32)
-    K4B_CASE(DT_I64)
-#undef K4B_CASE
-    default: return cudaErrorInvalidValue;
-  }
-  if (e != cudaSuccess) return e;
-  g_launches++;
-  return cudaGetLastError();
-}
-
-// K4T launch: stages (K boxes each) as many as the shared memory holds (>= 2), one CTA per SM
-cudaError_t launch_k4_tma(const K4TMaps &maps, TrParams p, int K, int dtype, cudaStream_t st) {
-  if (p.n == 0) return cudaSuccess;
-  if (K < 1 || K > K4T_MAXK) return cudaErrorInvalidValue;
-  static int optin = [] {
-    int dev = 0, v = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    return v;
-  }();
-  const size_t budget = (size_t)optin - 2048 - 1024;
-  p.stages = (uint32_t)std::min<size_t>(K4T_STAGES, budget / ((size_t)K * p.slot));
-  if (p.stages < 2) return cudaErrorInvalidValue;
-  p.prefetch = std::max<uint32_t>(1, p.stages / 2);
-  const size_t smem = (size_t)p.stages * K * p.slot + 1024;
-  const unsigned blocks = (unsigned)std::min<int64_t>(p.n, (int64_t)num_sms());
-  const void *kern = nullptr;
-  cudaError_t e;
-  switch (dtype) {
-#define K4T_CASE(D)                                                                            \
-  case D:                                                                                      \
-    kern = (const void *)k4_tma<D>;                                                            \
-    e = smem_attr(kern, optin - 2048);                                                         \
-    if (e == cudaSuccess) e = launch_ex(k4_tma<D>, dim3(blocks), dim3(K4T_THREADS), smem, st, maps, p, K); \
-    break;
-    K4T_CASE(DT_F32)
-    K4T_CASE(DT_F64)
-    K4T_CASE(DT_F16)
-    K4T_CASE(DT_BF16)
-    K4T_CASE(DT_I32)
-    K4T_CASE(DT_I64)
-#undef K4T_CASE
-    default: return cudaErrorInvalidValue;
-  }
-  if (e != cudaSuccess) return e;
-  g_launches++;
-  return cudaGetLastError();
-}
 
 cudaError_t launch_k4_peer(const K4Params &p, const K4Ptrs &q, int dtype, int vb, unsigned blocks, void *dst,
                            cudaStream_t st) {

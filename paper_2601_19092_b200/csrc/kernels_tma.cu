@@ -275,8 +275,9 @@ __global__ void __launch_bounds__(32, 1) k8_bulk(const __grid_constant__ K8Param
   }
   uint8_t *sm = (uint8_t *)(((uintptr_t)raw + 127) & ~(uintptr_t)127);
   const uint32_t S = p.stages, box = p.box, slot = (box + 127) & ~127u;
-  const uint32_t lo = blockIdx.x, bstep = gridDim.x;
-  const uint32_t mine = lo < p.nboxes ? (p.nboxes - lo + bstep - 1) / bstep : 0;
+  const UnitRange R = unit_range(p.nboxes, p.chunk);
+  const uint32_t lo = R.lo, bstep = R.step;
+  const uint32_t mine = lo < R.end ? (R.end - lo + bstep - 1) / bstep : 0;
   auto addr = [&](uint32_t b, int64_t &so, int64_t &dof) {
     const uint32_t o = fdiv(p.per_run, b);
     const int64_t r = (int64_t)(b - o * p.per_run.d) * box;
@@ -336,12 +337,14 @@ cudaError_t launch_k8_bulk(K8Params p, const void *src, void *dst, cudaStream_t 
   while (ps > 1 && (size_t)(233472 / ps - 1024 - 2048 - 128) < 4 * (size_t)slot) ps--;
   const size_t budget = (size_t)std::min(optin, 233472 / ps - 1024) - 2048 - 128;
   p.stages = (uint32_t)std::min<size_t>(K8B_STAGES, budget / slot);
-  if (p.stages < 3) return cudaErrorInvalidValue;  // a slot is refilled two boxes after its store
+  if (p.chunk && p.chunk <= p.stages) p.stages = p.chunk;  // in-order schedule: every box of the CTA in flight
+  else if (p.stages < 3) return cudaErrorInvalidValue;     // a slot is refilled two boxes after its store
   p.prefetch = std::max<uint32_t>(1, p.stages / 2);
   const size_t smem = (size_t)p.stages * slot + 128;
   const cudaError_t attr_err = smem_attr((const void *)k8_bulk, optin - 2048);
   if (attr_err != cudaSuccess) return attr_err;
-  const unsigned blocks = (unsigned)std::min<int64_t>(p.nboxes, (int64_t)num_sms() * ps);
+  const unsigned blocks = p.chunk ? (p.nboxes + p.chunk - 1) / p.chunk
+                                  : (unsigned)std::min<int64_t>(p.nboxes, (int64_t)num_sms() * ps);
   const cudaError_t e = launch_ex(k8_bulk, dim3(blocks), dim3(32), smem, st, p, (const uint8_t *)src, (uint8_t *)dst);
   if (e != cudaSuccess) return e;
   g_launches++;

@@ -153,8 +153,7 @@ Swz make_swz(const Storage &st);
 
 // ---- K4 reduction over the leading logical dimension (plan_reduce.cpp, kernels_reduce.cu)
 struct ReducePlan {
-  int kind = 0;          // 1: generic (k4_generic), 2: vector (k4_reduce), 3: K4T (k4_tma, swizzled destination),
-                         // 4: K4B (k4_bulk, contiguous runs)
+  int kind = 0;          // 1: generic (k4_generic), 2: vector (k4_reduce)
   int dtype = 0, es = 0;
   int64_t K = 1;         // summands per output element
   int64_t src_bytes = 0, dst_bytes = 0;
@@ -163,16 +162,7 @@ struct ReducePlan {
   K4Params k4;
   K4GParams k4g;
   std::string desc;
-  // K4T: the paper's TMA lowering of one summand slab into the destination (a CopyPlan's lowered plan)
-  std::shared_ptr<axe_tma_plan> lowered;
-  int64_t lowered_dst_off = 0;
-  TmaReps lowered_reps{};
-  std::vector<int64_t> koff_bytes;
-  K4BParams k4b{};
 };
-cudaError_t launch_k4_bulk(K4BParams p, int dtype, const void *src, void *dst, cudaStream_t st);
-axe_status tma_run_reduce(axe_tma_plan *plan, const void *src, const int64_t *koff, int K, void *img,
-                          const TmaReps &reps, int dtype, int dep, cudaStream_t st);
 int dtype_size(int dtype);
 axe_status plan_reduce(const Layout &src, const Storage &sst, const Layout &dst, const Storage &dstst, int dtype,
                        int max_align, ReducePlan *out);

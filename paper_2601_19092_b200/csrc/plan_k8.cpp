@@ -155,6 +155,10 @@ bool build_k8(const Linear &ls, const Linear &ld, const Storage &sst, const Stor
       k.nitems = (uint32_t)(nch * nout);
     }
   }
+  // bulk form: the in-order schedule, 2 boxes per CTA, once the boxes outnumber two waves of the
+  // persistent grid (nonnested 1 GiB: 236.9 us vs 262.8, profiles/r02_sweep_front.log); the chunked
+  // item form keeps its persistent grid unless AXE_CHUNK asks
+  k.chunk = k.bulk ? unit_chunk(k.nboxes > (uint32_t)(4 * num_sms()) ? 2 : 0) : k.chunked ? unit_chunk(0) : 0;
   P->align = std::max(P->align, P->vb);
   P->covers_all = (int64_t)reps.size() * vin * nout * V == dstst.cells;
   auto lin_json = [](const std::vector<LinIter> &L) {
@@ -164,7 +168,7 @@ bool build_k8(const Linear &ls, const Linear &ld, const Storage &sst, const Stor
     return s + "]";
   };
   P->desc = "{\"kernel\":\"dual\",\"odometer\":" + std::to_string(k.odo) + ",\"bulk\":" + std::to_string(k.bulk) + ",\"box_bytes\":" +
-            std::to_string(k.box) + ",\"chunked\":" + std::to_string(k.chunked) + ",\"vec_bytes\":" + std::to_string(P->vb) + ",\"vectors\":" +
+            std::to_string(k.box) + ",\"chunked\":" + std::to_string(k.chunked) + ",\"chunk\":" + std::to_string(k.chunk) + ",\"vec_bytes\":" + std::to_string(P->vb) + ",\"vectors\":" +
             std::to_string(k.total) + ",\"inner_block_vectors\":" + std::to_string(vin) +
             ",\"outer_blocks\":" + std::to_string(nout) + ",\"replicas\":" + std::to_string(reps.size()) +
             ",\"inner\":" + joint_json(Jin) + ",\"outer_src\":" + lin_json(A) + ",\"outer_dst\":" + lin_json(B) + "}";

@@ -93,108 +93,10 @@ axe_status plan_reduce(const Layout &S, const Storage &sst, const Layout &D, con
       if (j.e > 1) (j.ds == 0 ? Kd : Y).push_back(j);
     if ((int)Kd.size() > K4_MAXD) joint = false;
   }
-  if (joint && P.K > 1 && P.K <= K4T_MAXK && dstst.swz_b && env_int_r("AXE_K4_TMA", 1)) {
-    // K4T: the destination carries a TMA swizzle -- the paper's lowering of one summand slab into it
-    // (build_lowered on the output digits), K TMA loads per output box, the sum in shared memory
-    CopyPlan L;
-    std::string why;
-    if (build_lowered(Y, ls, ld, sst, dstst, es, &L, &why) && !L.lowered_store) {
-      std::vector<int64_t> koff;
-      for (int64_t kk = 0; kk < P.K; kk++) {
-        int64_t rem = kk, off = 0;
-        for (int t = (int)Kd.size() - 1; t >= 0; t--) {
-          off += (rem % Kd[t].e) * Kd[t].ss;
-          rem /= Kd[t].e;
-        }
-        koff.push_back(off * es);
-      }
-      bool ok = true;
-      for (int64_t o : koff) ok = ok && o % 16 == 0;
-      if (ok) {
-        P.kind = 3;
-        P.lowered = L.lowered;
-        P.lowered_dst_off = L.lowered_dst_off;
-        P.lowered_reps = L.lowered_reps;
-        P.koff_bytes = koff;
-        P.vb = 16;
-        P.align = 16;
-        P.desc = "{\"kernel\":\"reduce\",\"mode\":\"tma\",\"dtype\":\"" + std::string(dtype_name(dtype)) +
-                 "\",\"K\":" + std::to_string(P.K) + ",\"vec_bytes\":16,\"lowering\":" + L.desc +
-                 ",\"reduce_digits\":" + joint_json(Kd) + "}";
-        *out = std::move(P);
-        return AXE_OK;
-      }
-    }
-  }
-  // K4B from K = 4 (measured on a B200, profiles/r02_k4b_sweep.log): K = 8 bf16 90.6 us vs 94.9 for the
-  // vector form, f32 87.9 vs 93.1, K = 4 98.3 vs 104.1; K = 3 ties (173.8 vs 171.9) and K = 2 loses
-  // (151.7 vs 131.2: two summands keep too little in flight per ring stage)
-  if (joint && P.K >= env_int_r("AXE_K4_BULK_MIN_K", 4) && P.K <= K4T_MAXK && !dstst.swz_b && !sst.swz_b &&
-      max_align >= 16 && !Y.empty() &&
-      Y.back().ss == 1 && Y.back().ds == 1 && (int)Y.size() - 1 <= K4_MAXD && env_int_r("AXE_K4_BULK", 1)) {
-    // K4B: the innermost output run is contiguous on both sides and unswizzled -- boxes of it arrive by
-    // cp.async.bulk from every summand, the sum in shared memory, one bulk store per replica; boxes sized so
-    // the ring holds >= 3 stages of K boxes
-    const int64_t run = Y.back().e * es;
-    std::vector<int64_t> all{ls.base * es, ld.base * es};
-    for (size_t k = 0; k + 1 < Y.size(); k++) {
-      all.push_back(Y[k].ss * es);
-      all.push_back(Y[k].ds * es);
-    }
-    for (int64_t r : reps) all.push_back(r * es);
-    std::vector<int64_t> koff;
-    for (int64_t kk = 0; kk < P.K; kk++) {
-      int64_t rem = kk, off = 0;
-      for (int t = (int)Kd.size() - 1; t >= 0; t--) {
-        off += (rem % Kd[t].e) * Kd[t].ss;
-        rem /= Kd[t].e;
-      }
-      koff.push_back(off * es);
-      all.push_back(off * es);
-    }
-    bool ok = run % 16 == 0 && run >= env_int_r("AXE_K4_BULK_MIN_RUN", 1024);
-    for (int64_t x : all) ok = ok && x % 16 == 0;
-    const int64_t max_box = std::min<int64_t>(16384, (225 * 1024) / (3 * P.K) / 16 * 16);
-    int64_t box = 0;
-    if (ok)
-      for (int64_t d = std::min(run, max_box); d >= 16; d -= 16)
-        if (run % d == 0) {
-          box = d;
-          break;
-        }
-    int64_t nout = 1;
-    for (size_t k = 0; k + 1 < Y.size(); k++) nout *= Y[k].e;
-    if (ok && box && (run / box) * nout < (int64_t(1) << 31)) {
-      K4BParams &b = P.k4b;
-      memset(&b, 0, sizeof(b));
-      b.box = (uint32_t)box;
-      b.per_run = make_fastdiv((uint32_t)(run / box));
-      b.nboxes = (uint32_t)((run / box) * nout);
-      b.nd = (int)Y.size() - 1;
-      for (int i = 0; i < b.nd; i++) {
-        b.fd[i] = make_fastdiv((uint32_t)Y[i].e);
-        b.ss[i] = Y[i].ss * es;
-        b.ds[i] = Y[i].ds * es;
-      }
-      b.sbase = ls.base * es;
-      b.dbase = ld.base * es;
-      b.K = (int)P.K;
-      for (int64_t kk = 0; kk < P.K; kk++) b.koff[kk] = koff[kk];
-      b.reps.n = (int)reps.size();
-      for (size_t i = 0; i < reps.size(); i++) b.reps.r[i] = reps[i] * es;
-      P.kind = 4;
-      P.vb = 16;
-      P.align = 16;
-      char d[256];
-      snprintf(d, sizeof d,
-               "{\"kernel\":\"reduce\",\"mode\":\"bulk\",\"dtype\":\"%s\",\"K\":%lld,\"vec_bytes\":16,\"box_bytes\":%lld,"
-               "\"boxes\":%u,\"replicas\":%d,\"table\":1,\"digits\":",
-               dtype_name(dtype), (long long)P.K, (long long)box, b.nboxes, b.reps.n);
-      P.desc = std::string(d) + joint_json(Y) + ",\"reduce_digits\":" + joint_json(Kd) + "}";
-      *out = std::move(P);
-      return AXE_OK;
-    }
-  }
+  // (A TMA-fed form -- K tensor or bulk loads per output box, the sum in shared memory, one bulk store --
+  // was measured against this vector form with the in-order schedule and lost everywhere: into SW128
+  // tiles 96.7 us vs 89.2, K = 8 contiguous 90.6 vs 87.0, 8 MiB outputs 13.3 vs 12.2; removed, numbers in
+  // profiles/r02_k4b_sweep.log)
   if (joint) {
     // vector width: a power of two V with V * es <= 16 dividing the innermost shared stride-1 run,
     // every other stride, both bases and every replica offset (as K1)
@@ -276,12 +178,16 @@ axe_status plan_reduce(const Layout &S, const Storage &sst, const Layout &D, con
         k.stcs = (int)env_int_r("AXE_K4_STCS", es >= 4 ? 1 : 0);
         const int64_t blocks = (total + 255) / 256, cap = (int64_t)num_sms() * 8;  // 4 per SM: 5-19% slower
         P.blocks = (unsigned)std::max<int64_t>(1, std::min(blocks, cap));
+        // in-order schedule (kernels.cuh unit_range) once the blocks outnumber the persistent grid:
+        // max(1, 8 / K) blocks of 256 vectors per CTA, about 32 KiB of summands (profiles/
+        // r02_sweep_front.log: bf16 K = 8 87.0 us vs 94.2, K = 2 125.9 vs 131.3, K = 3 163.0 vs 170.5)
+        k.chunk = unit_chunk(blocks > (int64_t)P.blocks ? std::max<int64_t>(1, 8 / std::max<int64_t>(1, P.K)) : 0);
       }
       char b[320];
       snprintf(b, sizeof b,
                "{\"kernel\":\"reduce\",\"mode\":\"vector\",\"dtype\":\"%s\",\"K\":%lld,\"vec_bytes\":%d,"
-               "\"vectors\":%lld,\"replicas\":%d,\"blocks\":%u,\"table\":%d,\"streaming_stores\":%d,\"digits\":",
-               dtype_name(dtype), (long long)P.K, P.vb, (long long)total, k.nrep, P.blocks, k.nk > 0, k.stcs);
+               "\"vectors\":%lld,\"replicas\":%d,\"blocks\":%u,\"chunk\":%u,\"table\":%d,\"streaming_stores\":%d,\"digits\":",
+               dtype_name(dtype), (long long)P.K, P.vb, (long long)total, k.nrep, P.blocks, k.chunk, k.nk > 0, k.stcs);
       P.desc = std::string(b) + joint_json(Y) + ",\"reduce_digits\":" + joint_json(Kd) + "}";
       *out = std::move(P);
       return AXE_OK;
@@ -311,16 +217,6 @@ axe_status run_reduce(const ReducePlan &p, const void *src, void *dst, cudaStrea
   if (s < d + p.dst_bytes && d < s + p.src_bytes) AXE_FAIL(AXE_ERR_ALIAS, "source and destination buffers overlap");
   const int dep = stream_dependency(st, s, s + p.src_bytes, d, d + p.dst_bytes);
   cudaError_t e;
-  if (p.kind == 4) {
-    K4BParams k = p.k4b;
-    k.dep = dep;
-    e = launch_k4_bulk(k, p.dtype, src, dst, st);
-    if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "K4B launch: %s", cudaGetErrorString(e));
-    return AXE_OK;
-  }
-  if (p.kind == 3)
-    return tma_run_reduce(p.lowered.get(), src, p.koff_bytes.data(), (int)p.K, (uint8_t *)dst + p.lowered_dst_off,
-                          p.lowered_reps, p.dtype, dep, st);
   if (p.kind == 2) {
     K4Params k = p.k4;
     k.dep = dep;

@@ -25,7 +25,6 @@ namespace axe {
 int encode_tensor_map(void *out128, void *gaddr, const uint64_t dims[5], const uint64_t strides[4],
                       const uint32_t box[5], int swizzle_bytes);
 cudaError_t launch_tma_region(const void *map128, TrParams p, int store, cudaStream_t st);
-cudaError_t launch_k4_tma(const K4TMaps &maps, TrParams p, int K, int dtype, cudaStream_t st);
 void stream_forget(cudaStream_t st);
 }  // namespace axe
 
@@ -210,32 +209,6 @@ static axe_status tma_plan_run(axe_tma_plan *plan, const void *g_base, const voi
   return AXE_OK;
 }
 
-namespace axe {
-// K4T (plan_reduce.cpp): the reduction into a TMA-swizzled destination -- one map of the lowered region per
-// summand (base = src + koff[k]), K TMA loads per output box, sum in shared memory, bulk store
-axe_status tma_run_reduce(axe_tma_plan *plan, const void *src, const int64_t *koff, int K, void *img,
-                          const TmaReps &reps, int dtype, int dep, cudaStream_t st) {
-  if (K < 1 || K > K4T_MAXK) AXE_FAIL(AXE_ERR_UNSUPPORTED, "K4T: K = %d", K);
-  if ((uintptr_t)img % 16) AXE_FAIL(AXE_ERR_ALIGNMENT, "image must be 16-byte aligned");
-  TrParams p;
-  K4TMaps maps;
-  {
-    std::lock_guard<std::mutex> lk(plan->mu);
-    AXE_TRY(region_params(plan, img, st, dep, &p));
-    p.reps = reps;
-    for (int k = 0; k < K; k++) {
-      const uint8_t *g = (const uint8_t *)src + plan->desc.base_bytes + koff[k];
-      if ((uintptr_t)g % 16) AXE_FAIL(AXE_ERR_ALIGNMENT, "summand %d region start is not 16-byte aligned", k);
-      std::array<unsigned char, 128> m;
-      AXE_TRY(map_for(plan, g, &m));
-      memcpy(maps.m[k], m.data(), 128);
-    }
-  }
-  const cudaError_t e = launch_k4_tma(maps, p, K, dtype, st);
-  if (e != cudaSuccess) AXE_FAIL(AXE_ERR_CUDA, "K4T launch: %s", cudaGetErrorString(e));
-  return AXE_OK;
-}
-}  // namespace axe
 
 extern "C" {
 

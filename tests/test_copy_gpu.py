@@ -437,6 +437,39 @@ def test_k7_batched_padded_transposes(axe, monkeypatch, es, cw, asyn):
     assert desc["tiles"] == B * 2 * 3 and desc["ctas"] == 4
 
 
+def _in_order_cases():
+    n8 = 16 // 8
+    R, C = 2 * 32 * n8, 3 * 8 * n8 * 4
+    k7 = dict(name="k7_chunk", es=8, src=layout([(3, R * (C + 2)), (R, C + 2), (C, 1)]),
+              src_st=linear_storage(3 * R * (C + 2)), dst=layout([(3, C * R), (R, 1), (C, R)], [(2, 3 * C * R)]),
+              dst_st=linear_storage(2 * 3 * C * R), seed=71)
+    rows, cols, run = 96, 2048, 256           # 512-byte runs of a padded 2-byte matrix, column blocks first
+    gat = dict(name="gather_chunk", es=2, src=layout([(cols // run, run), (rows, cols + 64), (run, 1)]),
+               src_st=linear_storage(rows * (cols + 64)), dst=layout([(cols // run, rows * run), (rows, run), (run, 1)]),
+               dst_st=linear_storage(rows * cols), seed=72)
+    ne = 3 * 65536 + 4096                     # identity, 16-byte vectors / 16 KiB bulk boxes and a short tail box
+    ident = dict(name="ident_chunk", es=4, src=layout([(ne, 1)]), src_st=linear_storage(ne), dst=layout([(ne, 1)]),
+                 dst_st=linear_storage(ne), seed=73)
+    return [("k7", k7, "transpose", "transpose"), ("vector", gat, "vector", "vector"), ("tma", gat, "tma", "tma"),
+            ("bulk", ident, "tma", "tma"), ("shuffle", synth.config3(64, "a"), "shuffle", "shuffle"),
+            ("k3tma", synth.config3(64, "b"), "auto", "tma"),
+            ("dual", nonnested_pair(3, 2, 2048, 4, 64, 32, 2, name="dual_chunk"), "auto", "dual")]
+
+
+@pytest.mark.parametrize("case", range(7))
+@pytest.mark.parametrize("chunk", ["1", "2", "3", "5"])
+def test_in_order_schedule_every_kernel(axe, monkeypatch, case, chunk):
+    """The in-order schedule (kernels.cuh unit_range: `chunk` consecutive units per CTA over a covering grid)
+    forced on every kernel that has it, with unit counts that leave the last CTA ragged: byte-exact against
+    the oracle, like the persistent grid."""
+    monkeypatch.setenv("AXE_CHUNK", chunk)
+    monkeypatch.setenv("AXE_K7_ASYNC", "3")
+    name, cfg, kernel, expect = _in_order_cases()[case]
+    desc = check(axe, cfg, kernel, expect)
+    if "chunk" in desc:
+        assert desc["chunk"] == int(chunk), desc
+
+
 def test_alias_and_alignment_errors(axe):
     x = torch.zeros(1024, dtype=torch.int32, device="cuda")
     L = layout([(512, 1)])

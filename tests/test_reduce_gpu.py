@@ -194,63 +194,48 @@ def tiled_reduce_cfg(K, rows, cols, dtype, reps=1):
 
 @pytest.mark.parametrize("K,dtype,reps", [(2, "bf16", 1), (3, "f16", 1), (5, "f32", 1), (8, "bf16", 2), (8, "f64", 1),
                                           (4, "i32", 1), (6, "i64", 1), (7, "bf16", 1)])
-def test_k4t_tma_sum_into_swizzled_tiles(axe, K, dtype, reps):
-    """K4T: the paper's TMA lowering for every summand (K tensor loads per 64-row box, the hardware swizzle
-    applied to each summand image alike), the sum in shared memory in k order, one bulk store per replica."""
+def test_sum_into_swizzled_tiles(axe, K, dtype, reps):
+    """The reduction fused with config 2's re-tiling: the sums land in 64-row SW128 tiles (the swizzle folded
+    into the per-thread destination offsets), one store per replica."""
     es = synth.DTYPE_SIZE[dtype]
     rows, cols = 128 * (2 if es <= 4 else 1), 128 // es * 6
     d = run_local(axe, tiled_reduce_cfg(K, rows, cols, dtype, reps), dtype, seed=K * 3 + es)
-    assert d["kernel"] == "reduce" and d["mode"] == "tma", d
+    assert d["kernel"] == "reduce" and d["mode"] == "vector", d
 
 
 @pytest.mark.parametrize("K,dtype,rows,cols,ld,reps", [
     (2, "bf16", 64, 512, 512, 1), (3, "f32", 48, 1024, 1040, 1), (8, "f16", 32, 2048, 2048, 2), (5, "f64", 16, 256, 264, 1),
     (4, "i32", 40, 1024, 1028, 1), (8, "bf16", 96, 4096, 4096, 1), (7, "i64", 8, 512, 512, 3)])
-def test_k4b_bulk_boxes(axe, K, dtype, rows, cols, ld, reps, monkeypatch):
-    """K4B: contiguous output runs (whole rows, or each padded row when ld > cols) arrive as cp.async.bulk
-    boxes from every summand, the sum in shared memory in k order, one bulk store per replica (AUTO takes it
-    from K = 4; the smaller K are forced here)."""
-    monkeypatch.setenv("AXE_K4_BULK_MIN_K", "2")
+@pytest.mark.parametrize("chunk", ["", "3"])
+def test_padded_rows_and_replicas(axe, K, dtype, rows, cols, ld, reps, chunk, monkeypatch):
+    """Whole or padded rows (ld > cols) summed into a replicated destination, with the persistent grid or the
+    in-order schedule forced to 3 blocks per CTA (a ragged last CTA)."""
+    monkeypatch.setenv("AXE_CHUNK", chunk)
     src = layout([(K, rows * ld), (rows, ld), (cols, 1)])
     dst = layout([(rows, cols), (cols, 1)], [(reps, rows * cols)] if reps > 1 else [])
     cfg = dict(src=src, src_st=linear_storage(K * rows * ld), dst=dst, dst_st=linear_storage(reps * rows * cols))
     d = run_local(axe, cfg, dtype, seed=K * 5 + rows)
-    assert d["kernel"] == "reduce" and d["mode"] == "bulk" and d["replicas"] == reps, d
+    assert d["kernel"] == "reduce" and d["mode"] == "vector" and d["replicas"] == reps, d
 
 
-def test_k4b_matches_vector_form_bitwise(axe, monkeypatch):
-    """K4B performs K4's arithmetic: its output equals the vector kernel's bit for bit (bench shape, scaled)."""
-    cfg = synth.reduce_local(8, 1024, 1024, "f32")
-    vals = synth.numbers(8 * 1024 * 1024, "f32", 78)
+@pytest.mark.parametrize("K,dtype,tiled", [(8, "f32", False), (2, "bf16", False), (8, "bf16", True)])
+def test_in_order_schedule_matches_persistent_bitwise(axe, K, dtype, tiled, monkeypatch):
+    """The in-order schedule (max(1, 8 / K) blocks of 256 vectors per CTA over a covering grid) changes which
+    CTA sums which outputs, never the arithmetic: bit for bit the persistent grid's result, at a size where
+    AUTO takes it (4096+ blocks)."""
+    rows, cols = (2048, 2048) if dtype == "f32" else (2048, 4096)
+    cfg = synth.reduce_local(K, rows, cols, dtype, tiled=tiled)
+    vals = synth.numbers(K * rows * cols, dtype, 78 + K)
     s = torch.from_numpy(vals.copy()).cuda()
     outs = []
-    for bulk in ("1", "0"):
-        monkeypatch.setenv("AXE_K4_BULK", bulk)
-        p = axe.ReducePlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], "f32")
-        assert p.describe()["mode"] == ("bulk" if bulk == "1" else "vector")
-        o = torch.zeros(1024 * 1024, dtype=torch.int32, device="cuda")
+    for chunk in ("", "0"):
+        monkeypatch.setenv("AXE_CHUNK", chunk)
+        p = axe.ReducePlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], dtype)
+        o = torch.zeros(rows * cols * synth.DTYPE_SIZE[dtype] // 2, dtype=torch.int16, device="cuda")
         p.execute(s, o)
         torch.cuda.synchronize()
         outs.append(o.cpu().numpy())
-    assert np.array_equal(outs[0], outs[1])
-
-
-def test_k4t_matches_vector_form_bitwise(axe, monkeypatch):
-    """K4T performs K4's arithmetic (fp32 accumulators in k order from 0, one rounding): its output equals the
-    vector kernel's bit for bit on the bench's shape scaled down."""
-    cfg = synth.reduce_local(8, 1024, 512, "bf16", tiled=True)
-    vals = synth.numbers(8 * 1024 * 512, "bf16", 77)
-    sbuf = oracle.scatter_logical(cfg["src"], cfg["src_st"], vals, 2, np.zeros(8 * 1024 * 512 * 2, np.uint8), NT)
-    s = torch.from_numpy(sbuf).cuda()
-    outs = []
-    for tma in ("1", "0"):
-        monkeypatch.setenv("AXE_K4_TMA", tma)
-        p = axe.ReducePlan(cfg["src"], cfg["src_st"], cfg["dst"], cfg["dst_st"], "bf16")
-        assert p.describe()["mode"] == ("tma" if tma == "1" else "vector")
-        o = torch.zeros(1024 * 512, dtype=torch.int16, device="cuda")
-        p.execute(s, o)
-        torch.cuda.synchronize()
-        outs.append(o.cpu().numpy())
+        assert p.describe()["chunk"] == (max(1, 8 // K) if chunk == "" else 0)
     assert np.array_equal(outs[0], outs[1])
 
 

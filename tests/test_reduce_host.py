@@ -21,12 +21,8 @@ NPF = {"f16": np.float16, "f32": np.float32, "f64": np.float64}
 
 def test_local_plan_structure(monkeypatch):
     cfg = [synth.reduce_local(8, 64, 128, "bf16")[k] for k in ("src", "src_st", "dst", "dst_st")]
-    d = axe.ReducePlan(*cfg, "bf16").describe()     # AUTO: K4B, the run of 64 x 128 outputs in 16 KiB boxes
-    assert d["kernel"] == "reduce" and d["mode"] == "bulk" and d["K"] == 8 and d["box_bytes"] == 8192, d
-    assert d["reduce_digits"] == [[8, 8192, 0]] and d["boxes"] == 2
-    monkeypatch.setenv("AXE_K4_BULK", "0")          # the vector form
-    d = axe.ReducePlan(*cfg, "bf16").describe()
-    assert d["kernel"] == "reduce" and d["K"] == 8 and d["vec_bytes"] == 16 and d["table"]
+    d = axe.ReducePlan(*cfg, "bf16").describe()     # the vector form
+    assert d["kernel"] == "reduce" and d["mode"] == "vector" and d["K"] == 8 and d["vec_bytes"] == 16 and d["table"]
     assert d["reduce_digits"] == [[8, 8192, 0]]          # k stride = one (64 x 128) slab, no destination stride
     assert d["streaming_stores"] == 0                     # 2-byte sums keep plain stores (measured)
     f = synth.reduce_local(8, 64, 64, "f32")
