@@ -182,7 +182,12 @@ __global__ void __launch_bounds__(32, 1) k_tma_region(const __grid_constant__ CU
   const uint32_t S = p.stages, slot = p.slot, box = p.box;
   // boxes of this CTA: box(k) = lo + k * bstep
   uint32_t lo, mine, bstep;
-  if (p.strided) {
+  if (p.chunk) {
+    const UnitRange R = unit_range(p.n, p.chunk);
+    lo = R.lo;
+    mine = R.end > lo ? R.end - lo : 0;
+    bstep = 1;
+  } else if (p.strided) {
     lo = blockIdx.x;
     bstep = gridDim.x;
     mine = lo < p.n ? (p.n - lo + bstep - 1) / bstep : 0;
@@ -442,13 +447,18 @@ cudaError_t launch_tma_region(const void *map128, TrParams p, int store, cudaStr
   }();
   const size_t ring = std::min(budget, ring_cap);
   p.stages = (uint32_t)std::min<size_t>(TR_STAGES, ring / p.slot);
-  if (p.stages < (uint32_t)TR_LAG + 1) return cudaErrorInvalidValue;
+  if (p.chunk && p.chunk <= TR_STAGES && (size_t)p.chunk * p.slot + 1024 + static_bytes <= (size_t)optin)
+    p.stages = p.chunk;  // in-order schedule: the CTA's boxes all in flight at once, no refill
+  else if (p.chunk)
+    p.chunk = 0;         // (boxes too large for a chunk-deep ring: the persistent grid)
+  if (!p.chunk && p.stages < (uint32_t)TR_LAG + 1) return cudaErrorInvalidValue;
   const size_t smem = (size_t)p.stages * p.slot + 1024;
   const cudaError_t attr_err = smem_attr(kern, optin - static_bytes);  // (the largest any launch asks for)
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap m;
   memcpy(&m, map128, sizeof(m));
-  const unsigned blocks = (unsigned)std::min<int64_t>(p.n, (int64_t)num_sms() * per_sm);
+  const unsigned blocks = p.chunk ? (p.n + p.chunk - 1) / p.chunk
+                                  : (unsigned)std::min<int64_t>(p.n, (int64_t)num_sms() * per_sm);
   static const int strided = [] {  // AXE_TMA_REGION_STRIDED: box order per CTA (A/B)
     const char *e = getenv("AXE_TMA_REGION_STRIDED");
     return (e && *e) ? atoi(e) : 1;

@@ -26,6 +26,7 @@ int encode_tensor_map(void *out128, void *gaddr, const uint64_t dims[5], const u
                       const uint32_t box[5], int swizzle_bytes);
 cudaError_t launch_tma_region(const void *map128, TrParams p, int store, cudaStream_t st);
 void stream_forget(cudaStream_t st);
+uint32_t unit_chunk(int64_t dflt);
 }  // namespace axe
 
 using namespace axe;
@@ -43,6 +44,7 @@ struct axe_tma_plan {
   std::vector<TmaAtom> host;  // per box: tensor-map coordinates (byte units on dim 0) + image offset
   int fuse = 1, fuse_dim = -1;  // atoms per box along the rows (box[fuse_dim] = fuse)
   TrProg prog{};              // the table as a mixed-radix program (prog.nd < 0: use the table)
+  uint32_t chunk = 0;         // boxes per CTA of the in-order schedule (0: the persistent ring grid)
   std::mutex mu;              // guards the caches below
   std::map<int, TmaAtom *> tables;  // device -> its copy of the table (prog.nd < 0 only)
   std::unordered_map<const void *, std::array<unsigned char, 128>> maps;  // region start -> CUtensorMap
@@ -169,6 +171,7 @@ static axe_status region_params(axe_tma_plan *plan, const void *s_image, cudaStr
   p->box = plan->box_bytes;
   p->slot = (plan->box_bytes + 1023) & ~1023u;
   p->dep = dep;
+  p->chunk = plan->chunk;
   p->reps.n = 1;
   if (p->prog.nd < 0) {
     int dev = 0;
@@ -315,6 +318,10 @@ axe_status axe_tma_plan_create(const axe_tma_desc *desc, const axe_layout *tiler
     }
   }
   p->prog = fit_program(p->host);
+  // beyond 64 MiB of boxes, the in-order schedule with 4 boxes per CTA (kernels.cuh unit_range;
+  // profiles/r02_sweep_front.log: config 2 at 16384^2 158.7 us vs 179.6, 8192^2 40.6 vs 45.0); the
+  // bench's 4096^2 keeps the persistent ring, which holds the whole copy in flight (10.0 us vs 11.0)
+  p->chunk = unit_chunk((int64_t)p->host.size() * p->box_bytes > (int64_t(64) << 20) ? 4 : 0);
   const char *force_table = getenv("AXE_TMA_REGION_TABLE");  // tests: run the table form
   if (force_table && *force_table == '1') p->prog.nd = -1;
   // a table the program does not reproduce is uploaded now when a device is current (so executes can
@@ -447,9 +454,9 @@ bool build_lowered(const std::vector<Joint> &J0, const Linear &ls, const Linear 
   char b[320];
   snprintf(b, sizeof b,
            "{\"kernel\":\"lowered\",\"mode\":\"%s\",\"atoms\":%lld,\"boxes\":%lld,\"box_bytes\":%u,\"swizzle\":%d,"
-           "\"replicas\":%d,\"box_program_digits\":%d,\"tensor_map\":{\"dims\":[",
+           "\"replicas\":%d,\"box_program_digits\":%d,\"chunk\":%u,\"tensor_map\":{\"dims\":[",
            store ? "bulk-load/tensor-store" : "tensor-load/bulk-store", (long long)(tp->host.size() * tp->fuse),
-           (long long)tp->host.size(), tp->box_bytes, sw, (int)reps.size(), tp->prog.nd);
+           (long long)tp->host.size(), tp->box_bytes, sw, (int)reps.size(), tp->prog.nd, tp->chunk);
   std::string s = b;
   for (int i = 0; i < d.rank; i++) s += (i ? "," : "") + std::to_string(d.dims[i]);
   s += "],\"strides\":[";

@@ -53,6 +53,8 @@ CONFIGS = {
     "config2": lambda: synth.config2(),
     "config2r": lambda: synth.config2(reverse=True),
     "config2_16k": lambda: synth.config2(16384),
+    "config2_8k": lambda: synth.config2(8192),
+    "config2r_16k": lambda: synth.config2(16384, reverse=True),
     "config3a": lambda: synth.config3(65536, "a"),
     "config3b": lambda: synth.config3(65536, "b"),
     "identity_4g": lambda: dict(name="identity_4g", es=2, src=synth.layout([(1 << 31, 1)]),
