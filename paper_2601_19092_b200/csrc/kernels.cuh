@@ -313,6 +313,10 @@ struct K7Params {
   int nrep;
   int64_t rep[K1_MAXREP];
   uint32_t chunk;                      // tiles per CTA (unit_range); 0: persistent grid
+  // ragged edges: tile digit ka (kb) steps the source columns (rows) by one tile; only elements below
+  // lim_a columns / lim_b rows exist (both whole 16-byte vectors).  -1: whole tiles on that side
+  int ka, kb;
+  uint32_t lim_a, lim_b;
   int dep;
 };
 

@@ -35,15 +35,18 @@ __device__ __forceinline__ uint4 ldg128(const uint8_t *p) {
 
 __device__ __forceinline__ uint32_t word(const uint4 &v, int m) { return m == 0 ? v.x : m == 1 ? v.y : m == 2 ? v.z : v.w; }
 
-template <int ES, int CW>
+template <int ES, int CW, bool RG>
 __device__ __forceinline__ void k7_gather(const K7Params &p, const uint8_t *sm, int64_t db, uint8_t *__restrict__ dst,
-                                          int lane, int warp) {
+                                          int lane, int warp, uint32_t ra, uint32_t rb) {
   constexpr int N = 16 / ES;
   constexpr int CH = 8 * CW;
+  // RG (ragged plans only): ra / rb = the source columns / rows of this tile that exist
+  if (RG && (uint32_t)(lane * N) >= rb) return;
   // gather: lane = row block, warp (+ 8 cw) = chunk column
 #pragma unroll
   for (int cw = 0; cw < CW; cw++) {
     const int cc = warp + 8 * cw;
+    if (RG && (uint32_t)(cc * N) >= ra) break;
     uint4 w[N];
 #pragma unroll
     for (int i = 0; i < N; i++) {
@@ -79,23 +82,33 @@ __device__ __forceinline__ void k7_gather(const K7Params &p, const uint8_t *sm, 
   }
 }
 
-__device__ __forceinline__ void tile_offsets(const K7Params &p, uint32_t i, int64_t &sb, int64_t &db) {
+// tile i's byte offsets, and the source columns (ra) / rows (rb) of it that exist: a ragged edge tile
+// (digit ka / kb at its last value) keeps lim - d * T of its T columns / rows
+template <bool RG>
+__device__ __forceinline__ void tile_offsets(const K7Params &p, uint32_t i, int64_t &sb, int64_t &db, uint32_t TC,
+                                             uint32_t TR, uint32_t &ra, uint32_t &rb) {
   sb = p.sbase;
   db = p.dbase;
+  ra = RG ? min(TC, p.lim_a) : TC;  // (a ragged side of less than one tile has no digit)
+  rb = RG ? min(TR, p.lim_b) : TR;
   for (int k = p.nd - 1; k >= 1; k--) {
     const uint32_t q = fdiv(p.fd[k], i);
     const uint32_t d = i - q * p.fd[k].d;
     i = q;
     sb += (int64_t)d * p.ss[k];
     db += (int64_t)d * p.ds[k];
+    if (RG && k == p.ka) ra = min(TC, p.lim_a - d * TC);
+    if (RG && k == p.kb) rb = min(TR, p.lim_b - d * TR);
   }
   if (p.nd > 0) {
     sb += (int64_t)i * p.ss[0];
     db += (int64_t)i * p.ds[0];
+    if (RG && p.ka == 0) ra = min(TC, p.lim_a - i * TC);
+    if (RG && p.kb == 0) rb = min(TR, p.lim_b - i * TR);
   }
 }
 
-template <int ES, int CW>
+template <int ES, int CW, bool RG>
 __global__ void __launch_bounds__(K7_THREADS) k7_transpose(const __grid_constant__ K7Params p,
                                                            const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
   constexpr int N = 16 / ES;          // elements per 16-byte vector
@@ -109,13 +122,15 @@ __global__ void __launch_bounds__(K7_THREADS) k7_transpose(const __grid_constant
   const UnitRange R = unit_range(p.ntiles, p.chunk);
   for (uint32_t tile = R.lo; tile < R.end; tile += R.step) {
     int64_t sb, db;
-    tile_offsets(p, tile, sb, db);
+    uint32_t ra, rb;
+    tile_offsets<RG>(p, tile, sb, db, 8 * N * CW, TR, ra, rb);
     // load: 8 consecutive threads read one 128-byte source row
     uint4 v[LOADS];
 #pragma unroll
     for (int u = 0; u < LOADS; u++) {
       const int idx = t + u * K7_THREADS, r = idx / CH, c = idx % CH;
-      v[u] = ldg128(src + sb + (int64_t)r * p.src_row + c * 16);
+      v[u] = !RG || ((uint32_t)r < rb && (uint32_t)(c * N) < ra) ? ldg128(src + sb + (int64_t)r * p.src_row + c * 16)
+                                                                 : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int u = 0; u < LOADS; u++) {
@@ -123,7 +138,7 @@ __global__ void __launch_bounds__(K7_THREADS) k7_transpose(const __grid_constant
       *reinterpret_cast<uint4 *>(sm + (r * CH + (c ^ ((r / N) & 7))) * 16) = v[u];  // XOR on the low 3 bits
     }
     __syncthreads();
-    k7_gather<ES, CW>(p, sm, db, dst, lane, warp);
+    k7_gather<ES, CW, RG>(p, sm, db, dst, lane, warp, ra, rb);
     __syncthreads();
   }
 }
@@ -135,7 +150,7 @@ __device__ __forceinline__ void cp_async16(uint8_t *s, const uint8_t *g) {
                : "memory");
 }
 
-template <int ES, int CW, int S>
+template <int ES, int CW, int S, bool RG>
 __global__ void __launch_bounds__(K7_THREADS) k7_transpose_async(const __grid_constant__ K7Params p,
                                                                  const uint8_t *__restrict__ src,
                                                                  uint8_t *__restrict__ dst) {
@@ -154,20 +169,24 @@ __global__ void __launch_bounds__(K7_THREADS) k7_transpose_async(const __grid_co
       const uint32_t tt = R.lo + (uint32_t)s * R.step;
       if (tt >= R.end) break;
       int64_t sb, db;
-      tile_offsets(p, tt, sb, db);
+      uint32_t ra, rb;
+      tile_offsets<RG>(p, tt, sb, db, 8 * N * CW, TR, ra, rb);
       for (int idx = t; idx < TR * (CH / 8); idx += K7_THREADS)
-        prefetch_l2(src + sb + (int64_t)(idx / (CH / 8)) * p.src_row + (idx % (CH / 8)) * 128);
+        if (!RG || ((uint32_t)(idx / (CH / 8)) < rb && (uint32_t)((idx % (CH / 8)) * 8 * N) < ra))
+          prefetch_l2(src + sb + (int64_t)(idx / (CH / 8)) * p.src_row + (idx % (CH / 8)) * 128);
     }
     pdl_wait();
   }
   pdl_launch_dependents();
   auto issue = [&](uint32_t tile, uint8_t *buf) {
     int64_t sb, db;
-    tile_offsets(p, tile, sb, db);
+    uint32_t ra, rb;
+    tile_offsets<RG>(p, tile, sb, db, 8 * N * CW, TR, ra, rb);
 #pragma unroll
     for (int u = 0; u < LOADS; u++) {
       const int idx = t + u * K7_THREADS, r = idx / CH, c = idx % CH;
-      cp_async16(buf + (r * CH + (c ^ ((r / N) & 7))) * 16, src + sb + (int64_t)r * p.src_row + c * 16);
+      if (!RG || ((uint32_t)r < rb && (uint32_t)(c * N) < ra))
+        cp_async16(buf + (r * CH + (c ^ ((r / N) & 7))) * 16, src + sb + (int64_t)r * p.src_row + c * 16);
     }
   };
   // S-stage ring: tiles it + 1 .. it + S - 1 are in flight while tile it is gathered and stored
@@ -185,32 +204,42 @@ __global__ void __launch_bounds__(K7_THREADS) k7_transpose_async(const __grid_co
     asm volatile("cp.async.wait_group %0;" ::"n"(S - 1) : "memory");  // this thread's vectors of `tile` landed
     __syncthreads();                                                    // ... and every other thread's
     int64_t sb, db;
-    tile_offsets(p, tile, sb, db);
-    k7_gather<ES, CW>(p, sm + (it % S) * TILE, db, dst, lane, warp);
+    uint32_t ra, rb;
+    tile_offsets<RG>(p, tile, sb, db, 8 * N * CW, TR, ra, rb);
+    k7_gather<ES, CW, RG>(p, sm + (it % S) * TILE, db, dst, lane, warp, ra, rb);
     __syncthreads();  // buffer it % S is refilled by a later iteration's issue
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-template <int ES, int CW, int S>
+template <int ES, int CW, int S, bool RG>
 cudaError_t go_async(const K7Params &p, unsigned blocks, size_t tile, const uint8_t *s, uint8_t *d, cudaStream_t st) {
-  const cudaError_t e = smem_attr((const void *)k7_transpose_async<ES, CW, S>, 200 * 1024);
+  const cudaError_t e = smem_attr((const void *)k7_transpose_async<ES, CW, S, RG>, 200 * 1024);
   if (e != cudaSuccess) return e;
-  return launch_ex(k7_transpose_async<ES, CW, S>, dim3(blocks), dim3(K7_THREADS), S * tile, st, p, s, d);
+  return launch_ex(k7_transpose_async<ES, CW, S, RG>, dim3(blocks), dim3(K7_THREADS), S * tile, st, p, s, d);
+}
+
+// RG: the ragged-edge variant (masked loads and stores); whole-tile plans run the unmasked one (the masks
+// cost the 1-CTA-per-SM bf16 form 17%: 8192^2 52.5 us vs 44.9)
+template <int ES, int CW, bool RG>
+cudaError_t go_rg(const K7Params &p, unsigned blocks, const uint8_t *s, uint8_t *d, cudaStream_t st) {
+  constexpr int N = 16 / ES;
+  const size_t tile = (size_t)32 * N * 8 * CW * 16;
+  if (p.async) {
+    if (p.async == 4) return go_async<ES, CW, 4, RG>(p, blocks, tile, s, d, st);
+    if (p.async == 3) return go_async<ES, CW, 3, RG>(p, blocks, tile, s, d, st);
+    return go_async<ES, CW, 2, RG>(p, blocks, tile, s, d, st);
+  }
+  const cudaError_t e = smem_attr((const void *)k7_transpose<ES, CW, RG>, 100 * 1024);
+  if (e != cudaSuccess) return e;
+  return launch_ex(k7_transpose<ES, CW, RG>, dim3(blocks), dim3(K7_THREADS), tile, st, p, s, d);
 }
 
 template <int ES, int CW>
 cudaError_t go(const K7Params &p, unsigned blocks, const uint8_t *s, uint8_t *d, cudaStream_t st) {
   constexpr int N = 16 / ES;
-  const size_t tile = (size_t)32 * N * 8 * CW * 16;
-  if (p.async) {
-    if (p.async == 4) return go_async<ES, CW, 4>(p, blocks, tile, s, d, st);
-    if (p.async == 3) return go_async<ES, CW, 3>(p, blocks, tile, s, d, st);
-    return go_async<ES, CW, 2>(p, blocks, tile, s, d, st);
-  }
-  const cudaError_t e = smem_attr((const void *)k7_transpose<ES, CW>, 100 * 1024);
-  if (e != cudaSuccess) return e;
-  return launch_ex(k7_transpose<ES, CW>, dim3(blocks), dim3(K7_THREADS), tile, st, p, s, d);
+  const bool ragged = p.ka >= 0 || p.kb >= 0 || p.lim_a < (uint32_t)(8 * N * CW) || p.lim_b < (uint32_t)(32 * N);
+  return ragged ? go_rg<ES, CW, true>(p, blocks, s, d, st) : go_rg<ES, CW, false>(p, blocks, s, d, st);
 }
 
 }  // namespace

@@ -954,7 +954,7 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
   }
   if (joint && (kernel == AXE_KERNEL_AUTO || kernel == AXE_KERNEL_TRANSPOSE) && env_int("AXE_K7", 1)) {
     std::string w7, w9;
-    if (build_k7(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &w7)) {
+    if (build_k7(J, ls, ld, *rq.sst, *rq.dstst, es, rq.max_align, &P, &w7, kernel == AXE_KERNEL_TRANSPOSE)) {
       P.kernel = KK_TRANSPOSE;
       *out = std::move(P);
       return AXE_OK;

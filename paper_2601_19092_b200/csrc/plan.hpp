@@ -82,7 +82,7 @@ bool build_k6(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
               const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why);
 cudaError_t launch_k6(const K6Params &p, unsigned blocks, const void *src, void *dst, cudaStream_t st);
 bool build_k7(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,
-              const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why);
+              const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why, bool forced = false);
 cudaError_t launch_k7(const K7Params &p, int es, unsigned blocks, const void *src, void *dst, cudaStream_t st);  // K3 as K1-TMA mode 2 + movmatrix in smem
 bool build_k9(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, const Storage &sst,
               const Storage &dstst, int es, CopyPlan *P, std::string *why);

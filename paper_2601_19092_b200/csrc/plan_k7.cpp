@@ -4,10 +4,11 @@
 // contiguous on the source (source stride 1: the columns of a source row) and
 // a digit b contiguous on the destination (destination stride 1: the rows of a
 // destination column) -- a 2-D transpose -- with 2-, 4- or 8-byte elements,
-// a multiple of 8 n columns and 32 n rows (n = 16 / es), and every other digit
-// (and both row / column pitches) moving whole 16-byte vectors.  The tiles are
-// (32 n rows) x (16 n or 8 n columns); the other digits and the outer parts of a
-// and b index tiles.  The paper's dispatch matches layouts against instruction
+// both extents whole 16-byte vectors (multiples of n = 16 / es elements), and every other
+// digit (and both row / column pitches) moving whole 16-byte vectors.  The tiles are
+// (32 n rows) x (8 n cw columns); the other digits and the outer parts of a and b index
+// tiles, and a last tile row / column only partly inside the extents is masked (ragged
+// edges: the rows / columns past the extent are neither read nor written).  The paper's dispatch matches layouts against instruction
 // atoms; this atom is LDS.128 + an n x n register transpose.
 #include <algorithm>
 #include <cstdlib>
@@ -19,8 +20,13 @@ namespace axe {
 
 int num_sms();
 
+static int env_i7(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return (e && *e) ? atoi(e) : dflt;
+}
+
 bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, const Storage &sst,
-              const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why) {
+              const Storage &dstst, int es, int max_align, CopyPlan *P, std::string *why, bool forced) {
   auto fail = [&](const char *m) {
     *why = m;
     return false;
@@ -55,7 +61,15 @@ bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   const Joint A = J[a], B = J[b];
   while (cw > 1 && A.e % (8 * n * cw)) cw /= 2;
   const int64_t TC = 8 * n * cw, TR = 32 * n;
-  if (A.e % TC || B.e % TR) return fail("transpose: extents are not whole tiles");
+  // ragged edges (a last tile column / row only partly inside): whole 16-byte vectors on both sides
+  if (A.e % n || B.e % n) return fail("transpose: extents are not whole 16-byte vectors");
+  const bool rag_a = A.e % TC != 0, rag_b = B.e % TR != 0;
+  if ((rag_a || rag_b) && !env_i7("AXE_K7_RAGGED", 1)) return fail("transpose: extents are not whole tiles");
+  // AUTO: ragged tiles only while at least half of every tile's area is inside (a skinny transpose is
+  // better served by K2 / K1); forced: any
+  if ((rag_a || rag_b) && !forced &&
+      2 * A.e * B.e < ((A.e + TC - 1) / TC * TC) * ((B.e + TR - 1) / TR * TR))
+    return fail("transpose: ragged tiles less than half inside");
   auto v16 = [&](int64_t s) { return (s * es) % 16 == 0; };
   if (!v16(A.ds) || !v16(B.ss) || A.ds < 0 || B.ss < 0) return fail("transpose: row / column pitch not 16-byte aligned");
   if (!v16(ls.base) || !v16(ld.base)) return fail("transpose: bases not 16-byte aligned");
@@ -65,10 +79,20 @@ bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
     if (!v16(J[i].ss) || !v16(J[i].ds)) return fail("transpose: a digit moves partial vectors");
     outer.push_back(J[i]);
   }
-  if (A.e / TC > 1) outer.push_back(Joint{A.e / TC, TC, TC * A.ds});
-  if (B.e / TR > 1) outer.push_back(Joint{B.e / TR, TR * B.ss, TR});
+  const int64_t nta = (A.e + TC - 1) / TC, ntb = (B.e + TR - 1) / TR;
+  const Joint TA{nta, TC, TC * A.ds}, TB{ntb, TR * B.ss, TR};
+  if (nta > 1) outer.push_back(TA);
+  if (ntb > 1) outer.push_back(TB);
   std::stable_sort(outer.begin(), outer.end(), [](const Joint &x, const Joint &y) { return std::llabs(x.ds) > std::llabs(y.ds); });
   sort_fuse_outer(outer);
+  // the ragged sides' tile digits, found again after the fusion (a fused one cannot be masked)
+  auto find = [&](const Joint &t) {
+    for (int i = 0; i < (int)outer.size(); i++)
+      if (outer[i].e == t.e && outer[i].ss == t.ss && outer[i].ds == t.ds) return i;
+    return -1;
+  };
+  // (a side of less than one tile has no digit: tile_offsets applies its limit to every tile)
+  const int ka = rag_a && nta > 1 ? find(TA) : -1, kb = rag_b && ntb > 1 ? find(TB) : -1;
   if ((int)outer.size() > K1_MAXD) return fail("transpose: too many tile digits");
   int64_t nt = 1;
   for (auto &o : outer) nt *= o.e;
@@ -86,9 +110,15 @@ bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   if ((int)reps.size() > K1_MAXREP) return fail("transpose: too many replicas");
   for (int64_t r : reps)
     if (!v16(r)) return fail("transpose: replica offsets not 16-byte aligned");
+  if ((rag_a && nta > 1 && ka < 0) || (rag_b && ntb > 1 && kb < 0))
+    return fail("transpose: a ragged tile digit fused with another");
   K7Params &k = P->k7;
   memset(&k, 0, sizeof(k));
   k.ntiles = (uint32_t)nt;
+  k.ka = ka;
+  k.kb = kb;
+  k.lim_a = (uint32_t)(rag_a ? A.e : TC);
+  k.lim_b = (uint32_t)(rag_b ? B.e : TR);
   k.nd = (int)outer.size();
   for (int i = 0; i < k.nd; i++) {
     k.fd[i] = make_fastdiv((uint32_t)outer[i].e);

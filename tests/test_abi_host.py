@@ -190,14 +190,16 @@ def test_nonnested_with_common_factor_plans_dual():
 
 def test_ragged_transposes_plan_k9():
     """Transposes K7 cannot take (rows not whole 16-byte vectors) and K2 cannot tile (4095 = 3^2.5.7.13,
-    4097 = 17.241) plan K9, the element-granular tile transpose; one whose extents factor stays on K2."""
+    4097 = 17.241) plan K9, the element-granular tile transpose; whole-vector extents stay on K7."""
     for R, C, es in [(4095, 4097, 2), (8191, 8193, 1), (333, 777, 4)]:
         d = axe.CopyPlan(layout([(R, C), (C, 1)]), linear_storage(R * C), layout([(R, 1), (C, R)]),
                          linear_storage(R * C), es).describe()
         assert d["kernel"] == "transpose" and d["mode"] == "ragged", (R, C, es, d)
+    # extents of whole 16-byte vectors that are not whole tiles: K7 with its ragged last tile row masked
     d = axe.CopyPlan(layout([(8000, 8000), (8000, 1)]), linear_storage(8000 * 8000), layout([(8000, 1), (8000, 8000)]),
                      linear_storage(8000 * 8000), 2).describe()
-    assert d["kernel"] == "tile", d
+    assert d["kernel"] == "transpose" and "mode" not in d and d["tile"] == [256, 64], d
+    assert d["tiles"] == 32 * 125, d     # ceil(8000 / 256) tile rows x 8000 / 64 tile columns
 
 
 def test_plan_errors():

@@ -118,10 +118,35 @@ def test_ragged_transposes(axe, R, Cn, es, pad_s, pad_d, B, reps, vec, monkeypat
     dst = layout([(B, Cn * ldd), (R, 1), (Cn, ldd)], [(reps, B * Cn * ldd)] if reps > 1 else [])
     cfg = dict(name=f"rag{R}x{Cn}x{es}", es=es, src=src, src_st=linear_storage(B * R * lds), dst=dst,
                dst_st=linear_storage(reps * B * Cn * ldd), seed=R * 7 + Cn + es)
-    check(axe, cfg)                      # AUTO: K2 where a legal tile exists, else K9
+    check(axe, cfg)                      # AUTO: K7 (ragged edges masked) / K2 where legal, else K9
     if R > 1 and Cn > 1:                 # (a single row is a plain copy)
-        d = check(axe, cfg, "transpose")  # forced transpose: K7 cannot run these, so K9
-        assert d["kernel"] == "transpose" and d.get("mode") == "ragged", d
+        d = check(axe, cfg, "transpose")  # forced transpose: K7 where the extents and pitches are whole
+        n = 16 // es                      # 16-byte vectors, else K9
+        k7 = es in (2, 4, 8) and R % n == 0 and Cn % n == 0 and lds * es % 16 == 0 and ldd * es % 16 == 0
+        assert d["kernel"] == "transpose" and d.get("mode") == (None if k7 else "ragged"), d
+
+
+@pytest.mark.parametrize("es", [2, 4, 8])
+@pytest.mark.parametrize("R,Cn,B,asyn,chunk", [(8000, 8000, 1, 2, ""), (136, 72, 3, 3, "3"), (40, 24, 2, 0, ""),
+                                                (264, 520, 1, 2, "1"), (8, 8, 1, 2, "")])
+def test_k7_ragged_edges(axe, monkeypatch, es, R, Cn, B, asyn, chunk):
+    """K7 with ragged edges: extents of whole 16-byte vectors that are not whole tiles (last tile row and / or
+    column partly outside, or a side shorter than one tile), batched, padded pitches, a destination replica;
+    register-staged and cp.async forms, persistent and in-order grids -- every byte against the oracle, the
+    cells past the extents untouched."""
+    n = 16 // es
+    R, Cn = R // n * n, Cn // n * n
+    monkeypatch.setenv("AXE_K7_ASYNC", str(asyn))
+    monkeypatch.setenv("AXE_CHUNK", chunk)
+    lds, ldd = Cn + n, R + 2 * n
+    src = layout([(B, R * lds), (R, lds), (Cn, 1)])
+    dst = layout([(B, Cn * ldd), (R, 1), (Cn, ldd)], [(2, B * Cn * ldd)])
+    cfg = dict(name=f"k7r{R}x{Cn}x{es}", es=es, src=src, src_st=linear_storage(B * R * lds), dst=dst,
+               dst_st=linear_storage(2 * B * Cn * ldd), seed=R + Cn + es)
+    d = check(axe, cfg, "transpose", "transpose")   # (AUTO takes K7 while half of each tile is inside)
+    assert "mode" not in d and d["replicas"] == 2, d
+    if R * Cn >= 1 << 20:
+        assert check(axe, cfg)["kernel"] == "transpose"
 
 
 @pytest.mark.parametrize("R,Cn,es", [(8192, 8192, 2), (8192, 8192, 4), (8192, 4096, 8)])
