@@ -353,7 +353,7 @@ def measure_extras(axe, torch):
         "config2_reverse_tiles_to_rowmajor": synth.config2(reverse=True),
         "config3a_mma_c_to_tcgen05_rows": synth.config3(65536, "a"),
         "config3b_mma_c_8x8_transposed": synth.config3(65536, "b"),
-        "transpose_8192sq_bf16_smem_staged": dict(es=2, src=synth.layout([(8192, 8192), (8192, 1)]),
+        "transpose_8192sq_bf16": dict(es=2, src=synth.layout([(8192, 8192), (8192, 1)]),
                                                  src_st=synth.linear_storage(8192 * 8192),
                                                  dst=synth.layout([(8192, 1), (8192, 8192)]),
                                                  dst_st=synth.linear_storage(8192 * 8192)),
@@ -365,6 +365,13 @@ def measure_extras(axe, torch):
                                         src_st=synth.linear_storage(8192 * 4096),
                                         dst=synth.layout([(8192, 1), (4096, 8192)]),
                                         dst_st=synth.linear_storage(8192 * 4096)),
+        # whole-vector extents that are not whole tiles: K7 with its ragged last tile row masked
+        "transpose_8000sq_bf16_ragged_edges": dict(es=2, src=synth.layout([(8000, 8000), (8000, 1)]),
+                                                   src_st=synth.linear_storage(8000 * 8000),
+                                                   dst=synth.layout([(8000, 1), (8000, 8000)]),
+                                                   dst_st=synth.linear_storage(8000 * 8000)),
+        # config 2 at 16384^2 (512 MiB a side): the lowered schedule on its in-order grid
+        "config2_16384sq_lowered": synth.config2(16384),
         # non-nested digit systems: (3*2^13, 2*2^13) padded -> (2*2^13, 3*2^13) padded, 768 MiB each side
         "nonnested_3x2_bf16_dual": dict(es=2, src=synth.layout([(3 << 13, (2 << 13) + 64), (2 << 13, 1)]),
                                         src_st=synth.linear_storage((3 << 13) * ((2 << 13) + 64)),
