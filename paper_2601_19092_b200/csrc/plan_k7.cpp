@@ -47,7 +47,9 @@ bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   if (async == 1) async = 2;  // (1 meant "double-buffered" before the ring depth was a knob)
   const char *cwe = getenv("AXE_K7_CW");
   const int cwmax = es == 2 ? 2 : 4;
-  const int cwdef = async ? (es == 8 ? 4 : 2) : (es == 4 ? 4 : 2);
+  // (bf16 with the in-order schedule, profiles/r02_sweep_front.log: cw 1 32 MiB 10.7 us vs 12.8 with cw 2,
+  // 128 MiB 43.4 vs 44.6, 256 MiB 85.9 vs 87.9 -- 32 KiB tiles fit 3 CTAs per SM)
+  const int cwdef = async ? (es == 8 ? 4 : es == 4 ? 2 : 1) : (es == 4 ? 4 : 2);
   int64_t cw = (cwe && *cwe) ? std::max(1, std::min(cwmax, atoi(cwe))) : cwdef;
   std::vector<Joint> J;
   for (auto &j : J0)
