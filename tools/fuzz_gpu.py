@@ -363,6 +363,9 @@ def main():
     while time.time() - t0 < a.seconds:
         case_seed = int(rng.integers(1 << 31)) if a.case is None else a.case
         crng = np.random.default_rng(case_seed)
+        # the in-order schedule: the planner's default, or 1..5 units per CTA forced on every kernel
+        chunk = str(crng.choice(["", "", "1", "2", "3", "5"]))
+        os.environ["AXE_CHUNK"] = chunk
         u = crng.random()
         if a.only:
             u = {"chain": 0.0, "redistribute": 0.1, "copy": 0.5, "reduce": 0.9, "tma_region": 0.99}[a.only]
@@ -374,7 +377,7 @@ def main():
             kinds["chain"] = kinds.get("chain", 0) + 1
             if err:
                 fails += 1
-                print(json.dumps({"case_seed": case_seed, "kind": "chain", "error": err}), flush=True)
+                print(json.dumps({"case_seed": case_seed, "kind": "chain", "chunk": chunk, "error": err}), flush=True)
         elif u < 0.15:
             cfg = redist_case(crng)
             err = run_redist(cfg, case_seed)
@@ -398,7 +401,7 @@ def main():
                 kinds[k] = kinds.get(k, 0) + 1
                 if err:
                     fails += 1
-                    print(json.dumps({"case_seed": case_seed, "kind": "copy", "kernel": k, "error": err,
+                    print(json.dumps({"case_seed": case_seed, "kind": "copy", "kernel": k, "chunk": chunk, "error": err,
                                       "cfg": {**cfg, "es": cfg["es"]}}, default=str), flush=True)
         elif u >= 0.96:
             err = run_tma_region(crng, case_seed)
@@ -418,7 +421,7 @@ def main():
             kinds["reduce"] = kinds.get("reduce", 0) + 1
             if err:
                 fails += 1
-                print(json.dumps({"case_seed": case_seed, "kind": "reduce", "error": err, "cfg": cfg}, default=str),
+                print(json.dumps({"case_seed": case_seed, "kind": "reduce", "chunk": chunk, "error": err, "cfg": cfg}, default=str),
                       flush=True)
         if a.case is not None:
             break
