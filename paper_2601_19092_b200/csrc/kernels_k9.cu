@@ -214,6 +214,51 @@ __global__ void __launch_bounds__(K9_THREADS) k9_vec(const __grid_constant__ K9P
       }
     }
     __syncthreads();
+    if constexpr (ES == 1) {
+      // 1-byte elements: each destination row segment (64 elements from b0) leaves as 4-byte words
+      // -- word w of the segment covers its bytes [4w - m, 4w - m + 4), m = the segment's start address mod
+      // 4 -- assembled from 4 / es row buffers; a word only partly inside the segment (its first and last)
+      // goes out element by element.  Consecutive lanes take consecutive words of a row.  (u8 8191 x 8193:
+      // 100.8 us vs 107.7 with byte stores; for bf16 the same form lost, 36.5 vs 31.2, so 2-byte
+      // elements keep the element stores below)
+      constexpr int EPW = 4 / ES;               // elements per word
+      constexpr int WPR = TB * ES / 4 + 1;      // words per row segment (one more when misaligned)
+      constexpr int TASKS = TA * WPR;
+      const int nbv = (int)(p.eb - b0 < TB ? p.eb - b0 : TB), nav = (int)(p.ea - a0 < TA ? p.ea - a0 : TA);
+      for (int task = t; task < TASKS; task += K9_THREADS) {
+        const int ia = task / WPR, w = task - ia * WPR;
+        if (ia >= nav) break;
+        const int64_t rowb = dbo + (a0 + ia) * p.d_a + b0 * ES;
+        for (int rr = 0; rr < p.nrep; rr++) {
+          const int64_t A = rowb + p.rep[rr];
+          const int m = (int)(((uintptr_t)dst + (uintptr_t)A) & 3u);
+          const int o0 = 4 * w - m;             // segment byte offset of the word's first byte
+          if (o0 >= TB * ES || o0 + 4 <= 0) continue;
+          const int j0 = o0 >= 0 ? o0 / ES : -((-o0 + ES - 1) / ES);
+          if (o0 >= 0 && j0 + EPW <= nbv) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int k = 0; k < EPW; k++) {
+              const int j = j0 + k;
+              const uint32_t x = *reinterpret_cast<const T *>(rows + j * K9V_ROW + moff[j] + ia * ES);
+              word |= x << (8 * ES * k);
+            }
+            const int64_t off = A + o0;
+            *reinterpret_cast<uint32_t *>(dst + (SWZ ? swz(p.dsw, off) : off)) = word;
+          } else {
+            for (int k = 0; k < EPW; k++) {
+              const int j = j0 + k;
+              if (j < 0 || j >= nbv) continue;
+              const T x = *reinterpret_cast<const T *>(rows + j * K9V_ROW + moff[j] + ia * ES);
+              const int64_t off = A + (int64_t)j * ES;
+              *reinterpret_cast<T *>(dst + (SWZ ? swz(p.dsw, off) : off)) = x;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      continue;
+    }
     // store: this thread's row jb_s of columns ia_s0 + u CS (consecutive lanes, consecutive b; element
     // stores -- assembling 16-byte destination chunks from 16 / es row buffers measured slower: 44.9 us vs
     // 31.1 on 4095 x 4097 bf16)
