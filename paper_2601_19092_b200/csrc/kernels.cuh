@@ -341,6 +341,7 @@ struct K9Params {
   // rounded up to 16) are not read
   int vec;
   int64_t src_limit;
+  uint32_t chunk;                      // tiles per CTA (unit_range); 0: persistent grid
   int dep;
 };
 

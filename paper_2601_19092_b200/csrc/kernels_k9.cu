@@ -106,20 +106,21 @@ __global__ void __launch_bounds__(K9_THREADS) k9_ragged(const __grid_constant__ 
         v[u] = *reinterpret_cast<const T *>(src + (SWZ ? swz(p.ssw, off) : off));
     }
   };
-  uint32_t tt = blockIdx.x;
+  const UnitRange R = unit_range(p.ntiles, p.chunk);
+  uint32_t tt = R.lo;
   Tile cur;
-  if (tt < p.ntiles) {
+  if (tt < R.end) {
     cur = tile_of(tt);
     load(cur);
   }
-  for (; tt < p.ntiles; tt += gridDim.x) {
+  for (; tt < R.end; tt += R.step) {
 #pragma unroll
     for (int u = 0; u < L; u++) tile[jb_l0 + u * RS][ia_l] = v[u];
     __syncthreads();
     // the next tile's loads go out before this tile's stores (register double buffering)
-    const uint32_t nt = tt + gridDim.x;
+    const uint32_t nt = tt + R.step;
     Tile nxt;
-    if (nt < p.ntiles) {
+    if (nt < R.end) {
       nxt = tile_of(nt);
       load(nxt);
     }
@@ -167,7 +168,8 @@ __global__ void __launch_bounds__(K9_THREADS) k9_vec(const __grid_constant__ K9P
   const int jb_s = t % TB, ia_s0 = t / TB;
   if (p.dep) pdl_wait();
   pdl_launch_dependents();
-  for (uint32_t tt = blockIdx.x; tt < p.ntiles; tt += gridDim.x) {
+  const UnitRange R = unit_range(p.ntiles, p.chunk);
+  for (uint32_t tt = R.lo; tt < R.end; tt += R.step) {
     uint32_t r = tt;
     uint32_t q = fdiv(p.fb, r);
     const uint32_t tb = r - q * p.fb.d;
@@ -287,12 +289,12 @@ cudaError_t go(const K9Params &p, const uint8_t *s, uint8_t *d, cudaStream_t st)
   const bool sw = p.ssw.mask || p.dsw.mask;
   if (p.vec && ES <= 8) {
     const void *kern = sw ? (const void *)k9_vec<ES, true> : (const void *)k9_vec<ES, false>;
-    const unsigned blocks = one_wave(kern, K9_THREADS, 0, std::max(1u, p.ntiles));
+    const unsigned blocks = p.chunk ? (p.ntiles + p.chunk - 1) / p.chunk : one_wave(kern, K9_THREADS, 0, std::max(1u, p.ntiles));
     return sw ? launch_ex(k9_vec<ES, true>, dim3(blocks), dim3(K9_THREADS), 0, st, p, s, d)
               : launch_ex(k9_vec<ES, false>, dim3(blocks), dim3(K9_THREADS), 0, st, p, s, d);
   }
   const void *kern = sw ? (const void *)k9_ragged<ES, true> : (const void *)k9_ragged<ES, false>;
-  const unsigned blocks = one_wave(kern, K9_THREADS, 0, std::max(1u, p.ntiles));
+  const unsigned blocks = p.chunk ? (p.ntiles + p.chunk - 1) / p.chunk : one_wave(kern, K9_THREADS, 0, std::max(1u, p.ntiles));
   return sw ? launch_ex(k9_ragged<ES, true>, dim3(blocks), dim3(K9_THREADS), 0, st, p, s, d)
             : launch_ex(k9_ragged<ES, false>, dim3(blocks), dim3(K9_THREADS), 0, st, p, s, d);
 }

@@ -80,6 +80,9 @@ bool build_k9(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   const char *ve = getenv("AXE_K9_VEC");
   k.vec = (es <= 8 && B.ss > 0 && !(ve && *ve == '0')) ? 1 : 0;
   k.src_limit = (sst.cells * es + 15) / 16 * 16;
+  // one tile per CTA over a covering grid once the tiles outnumber a wave (in-order schedule,
+  // profiles/r02_sweep_front.log: 4095 x 4097 bf16 29.3 us vs 31.1, u8 8191 x 8193 91.0 vs 100.8)
+  k.chunk = unit_chunk(nt > (int64_t)num_sms() * 8 ? 1 : 0);
   P->align = k.vec ? 16 : es;
   int64_t total = 1;
   for (auto &j : J0) total *= j.e;
@@ -87,8 +90,8 @@ bool build_k9(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   char buf[256];
   snprintf(buf, sizeof buf,
            "{\"kernel\":\"transpose\",\"mode\":\"ragged\",\"vector_loads\":%d,\"tile\":[%lld,%lld],\"tiles\":%lld,"
-           "\"replicas\":%d,\"joint\":",
-           k.vec, (long long)TB, (long long)TA, (long long)nt, k.nrep);
+           "\"chunk\":%u,\"replicas\":%d,\"joint\":",
+           k.vec, (long long)TB, (long long)TA, (long long)nt, k.chunk, k.nrep);
   P->desc = std::string(buf) + joint_json(J0) + "}";
   return true;
 }

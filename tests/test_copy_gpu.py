@@ -475,15 +475,18 @@ def _in_order_cases():
     ne = 3 * 65536 + 4096                     # identity, 16-byte vectors / 16 KiB bulk boxes and a short tail box
     ident = dict(name="ident_chunk", es=4, src=layout([(ne, 1)]), src_st=linear_storage(ne), dst=layout([(ne, 1)]),
                  dst_st=linear_storage(ne), seed=73)
+    k9 = dict(name="k9_chunk", es=2, src=layout([(2, 131 * 259), (131, 259), (257, 1)]),   # odd extents: K9
+              src_st=linear_storage(2 * 131 * 259), dst=layout([(2, 257 * 133), (131, 1), (257, 133)]),
+              dst_st=linear_storage(2 * 257 * 133), seed=74)
     lw = synth.config2(512)                   # the lowered schedule: 64 fused 8 KiB boxes
-    return [("lowered", lw, "lowered", "lowered"), ("lowered_r", synth.config2(512, reverse=True), "lowered", "lowered"),
+    return [("k9", k9, "transpose", "transpose"), ("lowered", lw, "lowered", "lowered"), ("lowered_r", synth.config2(512, reverse=True), "lowered", "lowered"),
             ("k7", k7, "transpose", "transpose"), ("vector", gat, "vector", "vector"), ("tma", gat, "tma", "tma"),
             ("bulk", ident, "tma", "tma"), ("shuffle", synth.config3(64, "a"), "shuffle", "shuffle"),
             ("k3tma", synth.config3(64, "b"), "auto", "tma"),
             ("dual", nonnested_pair(3, 2, 2048, 4, 64, 32, 2, name="dual_chunk"), "auto", "dual")]
 
 
-@pytest.mark.parametrize("case", range(9))
+@pytest.mark.parametrize("case", range(10))
 @pytest.mark.parametrize("chunk", ["1", "2", "3", "5"])
 def test_in_order_schedule_every_kernel(axe, monkeypatch, case, chunk):
     """The in-order schedule (kernels.cuh unit_range: `chunk` consecutive units per CTA over a covering grid)
