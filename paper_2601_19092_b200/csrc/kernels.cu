@@ -387,10 +387,12 @@ __global__ void __launch_bounds__(K1_THREADS) k8_odo(const __grid_constant__ K8P
   if (p.dep) pdl_wait();
   pdl_launch_dependents();
   const int lane = threadIdx.x & 31;
-  const uint32_t warps = gridDim.x * (K1_THREADS / 32);
   const FastDiv EA = p.afd[p.na - 1], EB = p.bfd[p.nb - 1];
   const int64_t sA = p.as[p.na - 1], sB = p.bs[p.nb - 1];
-  for (uint32_t c = blockIdx.x * (K1_THREADS / 32) + (threadIdx.x >> 5); c < p.nchunk; c += warps) {
+  // units of K1_THREADS / 32 consecutive chunks, warp w taking chunk w of each of its CTA's units
+  constexpr uint32_t WPB = K1_THREADS / 32;
+  const UnitRange R = unit_range((p.nchunk + WPB - 1) / WPB, p.chunk);
+  for (uint32_t c = R.lo * WPB + (threadIdx.x >> 5), ce = min(p.nchunk, R.end * WPB); c < ce; c += R.step * WPB) {
     uint32_t x = c * (uint32_t)(K8_ODO_J * 32) + lane;
     const uint32_t xend = min(p.total, (c + 1) * (uint32_t)(K8_ODO_J * 32));
     uint32_t qa = fdiv(EA, x), ra = x - qa * EA.d;
@@ -450,7 +452,8 @@ cudaError_t launch_k8(const K8Params &p, int vb, const void *src, void *dst, cud
   if (p.odo) {
     auto go = [&](auto kern) {
       const unsigned want = (p.nchunk + K1_THREADS / 32 - 1) / (K1_THREADS / 32);
-      const unsigned blocks = one_wave((const void *)kern, K1_THREADS, 0, std::max(1u, want));
+      const unsigned blocks =
+          p.chunk ? (want + p.chunk - 1) / p.chunk : one_wave((const void *)kern, K1_THREADS, 0, std::max(1u, want));
       return launch_ex(kern, dim3(blocks), dim3(K1_THREADS), 0, st, p, s, d);
     };
     switch (vb) {

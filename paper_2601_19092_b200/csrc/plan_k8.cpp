@@ -155,10 +155,14 @@ bool build_k8(const Linear &ls, const Linear &ld, const Storage &sst, const Stor
       k.nitems = (uint32_t)(nch * nout);
     }
   }
-  // bulk form: the in-order schedule, 2 boxes per CTA, once the boxes outnumber two waves of the
-  // persistent grid (nonnested 1 GiB: 236.9 us vs 262.8, profiles/r02_sweep_front.log); the chunked
-  // item form keeps its persistent grid unless AXE_CHUNK asks
-  k.chunk = k.bulk ? unit_chunk(k.nboxes > (uint32_t)(4 * num_sms()) ? 2 : 0) : k.chunked ? unit_chunk(0) : 0;
+  // the in-order schedule once the units outnumber the persistent grid (profiles/r02_sweep_front.log,
+  // nonnested 1.5 GiB): bulk form 2 boxes per CTA (236.9 us vs 262.8), chunked item form 1 item (234.0
+  // vs ~280), odometer 2 units of 8 warp chunks (947.5 vs ~985)
+  const int64_t wave = (int64_t)num_sms() * 8;
+  k.chunk = k.bulk      ? unit_chunk(k.nboxes > (uint32_t)(4 * num_sms()) ? 2 : 0)
+            : k.chunked ? unit_chunk((int64_t)k.nitems > wave ? 1 : 0)
+            : k.odo     ? unit_chunk((int64_t)k.nchunk / 8 > wave ? 2 : 0)
+                        : 0;
   P->align = std::max(P->align, P->vb);
   P->covers_all = (int64_t)reps.size() * vin * nout * V == dstst.cells;
   auto lin_json = [](const std::vector<LinIter> &L) {
