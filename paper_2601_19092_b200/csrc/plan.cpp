@@ -896,7 +896,16 @@ static axe_status plan_copy_core(const PlanRequest &rq, CopyPlan *out) {
     AXE_FAIL(AXE_ERR_UNSUPPORTED, "forced lowered schedule cannot run these layouts: %s",
              rq.max_align < 16 ? "needs 16-byte aligned buffers" : wl.c_str());
   }
-  if (joint && rq.max_align >= 16 && (kernel == AXE_KERNEL_AUTO || kernel == AXE_KERNEL_TMA)) {
+  // AUTO and unswizzled storage on both sides: K1-TMA only for a copy that is one contiguous run (a
+  // bulk copy: 32 MiB 10.9 us vs K1's 11.8); strided runs go to K1 (4 KiB runs 12.4 vs 14.0 at 32 MiB,
+  // 81.5 vs 85.1 at 256 MiB; 128-256-byte runs within 2%; profiles/r02_segment_probe.log)
+  bool tma_auto_ok = true;
+  if (kernel == AXE_KERNEL_AUTO && !rq.sst->swz_b && !rq.dstst->swz_b && env_int("AXE_TMA_STRIDED_AUTO", 0) == 0) {
+    int nz = 0;
+    for (auto &j : J) nz += j.e > 1;
+    tma_auto_ok = nz <= 1;
+  }
+  if (joint && rq.max_align >= 16 && (kernel == AXE_KERNEL_TMA || (kernel == AXE_KERNEL_AUTO && tma_auto_ok))) {
     std::string w0, w1, w2;
     // AUTO takes a TMA plan only with boxes of >= 4 KiB: 1 KiB boxes measured 35 us against K1's 21 us
     // on a 64 MiB copy of 1 KiB rows (tools/perf_configs.py rows_1k); forced TMA takes any box
