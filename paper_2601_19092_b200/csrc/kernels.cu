@@ -150,8 +150,9 @@ __global__ void __launch_bounds__(K1_THREADS) k1_vector(const __grid_constant__ 
   if (p.dep) pdl_wait();
   pdl_launch_dependents();
   const uint32_t total = p.total;
-  const uint32_t step = gridDim.x * (K1_THREADS * U);
-  for (uint32_t base = blockIdx.x * (K1_THREADS * U) + threadIdx.x; base < total; base += step) {
+  const UnitRange R = unit_range((total + K1_THREADS * U - 1) / (K1_THREADS * U), p.chunk);
+  for (uint32_t ut = R.lo; ut < R.end; ut += R.step) {
+    const uint32_t base = ut * (K1_THREADS * U) + threadIdx.x;
     T v[U];
     int64_t dof[U];
 #pragma unroll
@@ -333,8 +334,9 @@ __global__ void __launch_bounds__(K1_THREADS) k8_dual(const __grid_constant__ K8
   }
   pdl_launch_dependents();
   const uint32_t total = p.total;
-  const uint32_t step = gridDim.x * (K1_THREADS * U);
-  for (uint32_t base = blockIdx.x * (K1_THREADS * U) + threadIdx.x; base < total; base += step) {
+  const UnitRange R = unit_range((total + K1_THREADS * U - 1) / (K1_THREADS * U), p.chunk);
+  for (uint32_t ut = R.lo; ut < R.end; ut += R.step) {
+    const uint32_t base = ut * (K1_THREADS * U) + threadIdx.x;
     T v[U];
     int64_t dof[U];
 #pragma unroll
@@ -438,8 +440,7 @@ static cudaError_t k8_launch(const K8Params &p, const uint8_t *s, uint8_t *d, cu
   const void *kern = (const void *)k8_dual<VB, U>;
   const unsigned want = p.chunked ? p.nitems
                                   : (unsigned)((p.total + (uint64_t)K1_THREADS * U - 1) / ((uint64_t)K1_THREADS * U));
-  const unsigned blocks = p.chunked && p.chunk ? (p.nitems + p.chunk - 1) / p.chunk
-                                               : one_wave(kern, K1_THREADS, 0, std::max(1u, want));
+  const unsigned blocks = p.chunk ? (want + p.chunk - 1) / p.chunk : one_wave(kern, K1_THREADS, 0, std::max(1u, want));
   return launch_ex(k8_dual<VB, U>, dim3(blocks), dim3(K1_THREADS), 0, st, p, s, d);
 }
 

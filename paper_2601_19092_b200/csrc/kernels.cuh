@@ -244,6 +244,7 @@ struct K2Params {
   Swz ssw, dsw;                        // global swizzles of the storages
   int nrep;
   int64_t rep[K1_MAXREP];
+  uint32_t chunk;  // tiles per CTA (unit_range); 0: persistent grid
   int dep;
 };
 

@@ -77,7 +77,8 @@ __global__ void AXE_K2_BOUNDS k2_tile(const __grid_constant__ K2Params p, const 
                : "r"(p.A_l[t]), "r"(p.A_s[t]), "r"(p.A_d[t]));
   if (p.dep) pdl_wait();
   pdl_launch_dependents();
-  for (uint32_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+  const UnitRange R = unit_range(p.ntiles, p.chunk);
+  for (uint32_t tile = R.lo; tile < R.end; tile += R.step) {
     int64_t sb = p.sbase, db = p.dbase;
     {
       uint32_t i = tile;

@@ -462,6 +462,8 @@ static bool build_k1(const std::vector<Joint> &J0, const Linear &ls, const Linea
     int64_t blocks = (total + 256LL * u - 1) / (256LL * u);
     int64_t cap = grid_cap(8);
     P->blocks = (unsigned)std::max<int64_t>(1, std::min(blocks, cap));
+    k.chunk = unit_chunk(0);
+    P->blocks = chunk_grid(blocks, k.chunk, P->blocks);
     mode = "decode";
   }
   char b[320];

@@ -337,6 +337,8 @@ bool build_k2(const std::vector<Joint> &J, const Linear &ls, const Linear &ld, c
   int per_sm = std::max(1, std::min(8, (int)(200 * 1024 / (TE * es + 1024))));
   if (const char *ev = getenv("AXE_K2_PER_SM")) per_sm = std::max(1, atoi(ev));  // tuning knob
   P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(k.ntiles, grid_cap(per_sm)));
+  k.chunk = unit_chunk(0);
+  P->blocks = chunk_grid(k.ntiles, k.chunk, P->blocks);
   int64_t total = 1;
   for (auto &j : J) total *= j.e;
   P->covers_all = (int64_t)reps.size() * total == dstst.cells;

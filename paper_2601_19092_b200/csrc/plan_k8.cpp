@@ -162,7 +162,7 @@ bool build_k8(const Linear &ls, const Linear &ld, const Storage &sst, const Stor
   k.chunk = k.bulk      ? unit_chunk(k.nboxes > (uint32_t)(4 * num_sms()) ? 2 : 0)
             : k.chunked ? unit_chunk((int64_t)k.nitems > wave ? 1 : 0)
             : k.odo     ? unit_chunk((int64_t)k.nchunk / 8 > wave ? 2 : 0)
-                        : 0;
+                        : unit_chunk(0);
   P->align = std::max(P->align, P->vb);
   P->covers_all = (int64_t)reps.size() * vin * nout * V == dstst.cells;
   auto lin_json = [](const std::vector<LinIter> &L) {
