@@ -479,14 +479,15 @@ def _in_order_cases():
               src_st=linear_storage(2 * 131 * 259), dst=layout([(2, 257 * 133), (131, 1), (257, 133)]),
               dst_st=linear_storage(2 * 257 * 133), seed=74)
     lw = synth.config2(512)                   # the lowered schedule: 64 fused 8 KiB boxes
-    return [("k9", k9, "transpose", "transpose"), ("lowered", lw, "lowered", "lowered"), ("lowered_r", synth.config2(512, reverse=True), "lowered", "lowered"),
+    return [("tile", gat, "tile", "tile"), ("dual_pervec", nonnested_pair(3, 2, 16, 4, 8, 4, 2, name="dual_pv"), "dual", "dual"),
+            ("k9", k9, "transpose", "transpose"), ("lowered", lw, "lowered", "lowered"), ("lowered_r", synth.config2(512, reverse=True), "lowered", "lowered"),
             ("k7", k7, "transpose", "transpose"), ("vector", gat, "vector", "vector"), ("tma", gat, "tma", "tma"),
             ("bulk", ident, "tma", "tma"), ("shuffle", synth.config3(64, "a"), "shuffle", "shuffle"),
             ("k3tma", synth.config3(64, "b"), "auto", "tma"),
             ("dual", nonnested_pair(3, 2, 2048, 4, 64, 32, 2, name="dual_chunk"), "auto", "dual")]
 
 
-@pytest.mark.parametrize("case", range(10))
+@pytest.mark.parametrize("case", range(12))
 @pytest.mark.parametrize("chunk", ["1", "2", "3", "5"])
 def test_in_order_schedule_every_kernel(axe, monkeypatch, case, chunk):
     """The in-order schedule (kernels.cuh unit_range: `chunk` consecutive units per CTA over a covering grid)
@@ -495,6 +496,9 @@ def test_in_order_schedule_every_kernel(axe, monkeypatch, case, chunk):
     monkeypatch.setenv("AXE_CHUNK", chunk)
     monkeypatch.setenv("AXE_K7_ASYNC", "3")
     name, cfg, kernel, expect = _in_order_cases()[case]
+    if name == "dual_pervec":   # K8's per-vector form (neither bulk boxes nor chunked items)
+        monkeypatch.setenv("AXE_K8_BULK", "0")
+        monkeypatch.setenv("AXE_K8_CHUNKED", "0")
     desc = check(axe, cfg, kernel, expect)
     if "chunk" in desc:
         assert desc["chunk"] == int(chunk), desc
