@@ -462,6 +462,20 @@ def test_k7_batched_padded_transposes(axe, monkeypatch, es, cw, asyn):
     assert desc["tiles"] == B * 2 * 3 and desc["ctas"] == 4
 
 
+@pytest.mark.parametrize("chain", [0, 1, 2])
+@pytest.mark.parametrize("kernel", ["auto", "vector", "generic"])
+def test_storage_divisor_chains(axe, chain, kernel):
+    """Destination storages that split the m axis over several digits (the oracle's pin:
+    test_storage_divisor_chain_is_numpy_blocking) at a size the kernels tile: 4096 x 24 bf16."""
+    M, Nn = 4096, 24
+    st = [storage([("m", 16, 256), ("n", Nn), ("m", 256, 1)]),
+          storage([("m", 2, 2048), ("n", Nn), ("m", 8, 256), ("m", 256, 1)]),
+          storage([("m", 64, 64), ("m", 64, 1), ("n", Nn)])][chain]
+    cfg = dict(name=f"chain{chain}", es=2, src=layout([(M, Nn), (Nn, 1)]), src_st=linear_storage(M * Nn),
+               dst=layout([(M, 1, "m"), (Nn, 1, "n")]), dst_st=st, seed=80 + chain)
+    check(axe, cfg, kernel)
+
+
 def _in_order_cases():
     n8 = 16 // 8
     R, C = 2 * 32 * n8, 3 * 8 * n8 * 4

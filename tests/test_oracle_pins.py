@@ -420,6 +420,28 @@ def test_copy_errors():
     oracle.copy(layout([(4, 1)]), linear_storage(4), v[:16], dst, st, out2, 4)
 
 
+@pytest.mark.parametrize("es", [2, 4])
+def test_storage_divisor_chain_is_numpy_blocking(es):
+    """A storage axis split over two digits (S:O6: idx = sum_k ((c[a_k] / div_k) mod ext_k) prod_{j>k} ext_j):
+    m = 32 rows stored as (m / 8, n, m mod 8) -- the digit chain ("m", 4, 8), ("n", 3), ("m", 8, 1) -- is
+    numpy's blocking of a (32, 3) row-major array: reshape (4, 8, 3), transpose (0, 2, 1), flatten; a
+    three-digit chain ("m", 2, 16), ("n", 3), ("m", 4, 4), ("m", 4, 1) is the (2, 16) blocking; with both m
+    digits outside n, ("m", 4, 8), ("m", 8, 1), ("n", 3), the chain recomposes m: plain row-major."""
+    v = _vals(96, es, 5)
+    src = layout([(32, 3), (3, 1)])
+    dst = layout([(32, 1, "m"), (3, 1, "n")])
+    a = v.view(synth._DT[es]).reshape(32, 3)
+    out = np.zeros(96 * es, np.uint8)
+    oracle.copy(src, linear_storage(96), v, dst, storage([("m", 4, 8), ("n", 3), ("m", 8, 1)]), out, es)
+    assert np.array_equal(out.view(synth._DT[es]), np.ascontiguousarray(a.reshape(4, 8, 3).transpose(0, 2, 1)).reshape(-1))
+    out = np.zeros(96 * es, np.uint8)
+    oracle.copy(src, linear_storage(96), v, dst, storage([("m", 2, 16), ("n", 3), ("m", 4, 4), ("m", 4, 1)]), out, es)
+    assert np.array_equal(out.view(synth._DT[es]), np.ascontiguousarray(a.reshape(2, 16, 3).transpose(0, 2, 1)).reshape(-1))
+    out = np.zeros(96 * es, np.uint8)
+    oracle.copy(src, linear_storage(96), v, dst, storage([("m", 4, 8), ("m", 8, 1), ("n", 3)]), out, es)
+    assert np.array_equal(out, v)
+
+
 def test_storage_chain_validation():
     assert oracle.storage_check(storage([("reg", 16, 8), ("lane", 32), ("reg", 8)])) == 0
     assert oracle.storage_check(storage([("reg", 16, 4), ("lane", 32), ("reg", 8)])) != 0
