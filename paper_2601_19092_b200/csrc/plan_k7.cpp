@@ -87,6 +87,11 @@ bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   if (ntb > 1) outer.push_back(TB);
   std::stable_sort(outer.begin(), outer.end(), [](const Joint &x, const Joint &y) { return std::llabs(x.ds) > std::llabs(y.ds); });
   sort_fuse_outer(outer);
+  // tiles in source order: consecutive tiles (a CTA's chunk, neighbouring CTAs) continue the same source
+  // rows (bf16 8192^2 42.5 us vs 43.5 in destination order, 256 MiB 83.4 vs 85.9; fp32 1-2%;
+  // profiles/r02_sweep_front.log).  AXE_K7_ORDER=0: destination order
+  if (env_i7("AXE_K7_ORDER", 1) == 1)
+    std::stable_sort(outer.begin(), outer.end(), [](const Joint &x, const Joint &y) { return std::llabs(x.ss) > std::llabs(y.ss); });
   // the ragged sides' tile digits, found again after the fusion (a fused one cannot be masked)
   auto find = [&](const Joint &t) {
     for (int i = 0; i < (int)outer.size(); i++)
