@@ -216,6 +216,7 @@ struct TmaParams {
   int nrep;
   int64_t rep[K1_MAXREP];      // mode 0: byte offsets of the destination replicas
   uint32_t chunk;              // boxes per CTA (unit_range); 0: persistent grid
+  uint32_t prefetch;           // boxes per CTA pulled into L2 before griddepcontrol.wait (0: the ring)
   int dep;                     // 1: wait for the previous kernel in the stream (griddepcontrol.wait)
 };
 
