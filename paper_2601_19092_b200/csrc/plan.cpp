@@ -609,6 +609,7 @@ static bool build_tma(const std::vector<Joint> &J0, const Linear &ls, const Line
   // 12.8 us vs 14.5, 256 MiB 82.4 vs 96.1)
   k.chunk = unit_chunk(nboxes > (int64_t)P->blocks ? 2 : 0);
   P->blocks = chunk_grid(nboxes, k.chunk, P->blocks);
+  if (k.chunk && env_int("AXE_TMA_CHUNK_RING", 1)) k.stages = (int)std::min<int64_t>(k.stages, k.chunk);
   P->align = 16;
   P->covers_all = (int64_t)reps.size() * nboxes * box_bytes == dstst.cells * es;
   char b[320];
@@ -650,7 +651,7 @@ static bool build_bulk(const std::vector<Joint> &J0, const Linear &ls, const Lin
   for (int64_t d = 1; d * d <= run; d++)
     if (run % d == 0)
       for (int64_t c : {d, run / d})
-        if (c * es <= 16384 && (c * es) % 16 == 0 && c > be) be = c;
+        if (c * es <= env_int("AXE_TMA_BULK_BOX", 16384) && (c * es) % 16 == 0 && c > be) be = c;
   if (be * es < 1024) return fail("bulk: no box of 1-16 KiB divides the run");
   std::vector<int64_t> reps{0};
   for (auto &r : ld.R) {
@@ -713,6 +714,9 @@ static bool build_bulk(const std::vector<Joint> &J0, const Linear &ls, const Lin
   // up to 64 MiB the persistent ring keeps the whole copy in flight and wins: 11.1 us vs 14.3)
   k.chunk = unit_chunk(bytes > (int64_t(64) << 20) && nboxes > (int64_t)P->blocks ? 2 : 0);
   P->blocks = chunk_grid(nboxes, k.chunk, P->blocks);
+  // in-order schedule: a ring of the CTA's own boxes only (every box in flight at once, no refill), so the
+  // shared memory admits more CTAs per SM
+  if (k.chunk && env_int("AXE_TMA_CHUNK_RING", 1)) k.stages = (int)std::min<int64_t>(k.stages, k.chunk);
   P->align = 16;
   P->covers_all = (int64_t)reps.size() * nboxes * be == dstst.cells;
   char b[320];

@@ -180,6 +180,7 @@ bool build_k3_bulk(CopyPlan *P, std::string *why) {
   // 1223.5 us vs 1293.7, profiles/r02_sweep_front.log)
   t.chunk = unit_chunk(nboxes > (int64_t)P->blocks ? 1 : 0);
   P->blocks = chunk_grid(nboxes, t.chunk, P->blocks);
+  if (t.chunk) t.stages = (int)std::min<int64_t>(t.stages, std::max<uint32_t>(2, t.chunk));
   P->tm_swizzle = 0;
   P->tm_cache.reset();
   P->align = 16;
