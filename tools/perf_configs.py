@@ -132,7 +132,7 @@ REDUCE = {
     "reduce_bf16_k4": lambda: synth.reduce_local(4, 16384, 4096, "bf16"),
     "reduce_bf16_k3": lambda: synth.reduce_local(3, 16384, 8192, "bf16"),
     "reduce_bf16_k16": lambda: synth.reduce_local(16, 4096, 4096, "bf16"),
-    # smaller outputs (2 / 8 MiB): the persistent grid or the in-order schedule, K4B / K4T or the vector form
+    # smaller outputs (2 / 8 MiB): the persistent grid or the in-order schedule (K4B / K4T were compared here)
     "reduce_bf16_k8_2m": lambda: synth.reduce_local(8, 1024, 1024, "bf16"),
     "reduce_bf16_k8_2m_tiled": lambda: synth.reduce_local(8, 1024, 1024, "bf16", tiled=True),
     "reduce_bf16_k8_8m": lambda: synth.reduce_local(8, 2048, 2048, "bf16"),
