@@ -61,8 +61,8 @@ def test_reduce_scatter_plan(P):
         assert ex["send_elems"] == (P - 1) * 64 * 64 // P == ex["recv_elems"]
         assert ex["packs"] == 0 and ex["unpacks"] == 0  # partial rows and stage slabs are contiguous
         red = d["reduce"]
-        moved = red["boxes"] * red["box_bytes"] if red["mode"] == "bulk" else red["vectors"] * 16
-        assert red["K"] == P and moved == 64 * 64 // P * 2
+        assert red["mode"] == "vector"
+        assert red["K"] == P and red["vectors"] * 16 == 64 * 64 // P * 2
 
 
 @pytest.mark.parametrize("P", [2, 4, 8])
