@@ -193,7 +193,8 @@ struct TrParams {
   int dep;               // 1: griddepcontrol.wait before the first TMA
   int strided;           // 1: CTA c takes boxes c, c + grid, ... (0: a contiguous range per CTA)
   uint32_t prefetch;     // boxes per CTA pulled into L2 before griddepcontrol.wait
-  uint32_t chunk;        // > 0: the in-order schedule, `chunk` consecutive boxes per CTA over a covering grid
+  uint32_t chunk;        // > 0: the in-order schedule, `chunk` consecutive units per CTA over a covering grid
+  int pair;              // 1: units of 2 boxes whose image slots are contiguous (one image-side bulk copy)
   TmaReps reps;
 };
 

@@ -180,38 +180,45 @@ __global__ void __launch_bounds__(32, 1) k_tma_region(const __grid_constant__ CU
     return;
   }
   uint8_t *sm = (uint8_t *)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t S = p.stages, slot = p.slot, box = p.box;
-  // boxes of this CTA: box(k) = lo + k * bstep
+  // a unit = F consecutive boxes whose image slots are contiguous (p.pair: F = 2, one bulk copy of 2 boxes
+  // on the image side); a ring slot holds one unit
+  const uint32_t F = p.pair ? 2u : 1u;
+  const uint32_t S = p.stages, slot = p.slot, box = p.box, SL = F * slot, N = p.n / F;
+  // units of this CTA: unit(k) = lo + k * bstep
   uint32_t lo, mine, bstep;
   if (p.chunk) {
-    const UnitRange R = unit_range(p.n, p.chunk);
+    const UnitRange R = unit_range(N, p.chunk);
     lo = R.lo;
     mine = R.end > lo ? R.end - lo : 0;
     bstep = 1;
   } else if (p.strided) {
     lo = blockIdx.x;
     bstep = gridDim.x;
-    mine = lo < p.n ? (p.n - lo + bstep - 1) / bstep : 0;
+    mine = lo < N ? (N - lo + bstep - 1) / bstep : 0;
   } else {
-    lo = (uint32_t)((uint64_t)p.n * blockIdx.x / gridDim.x);
-    mine = (uint32_t)((uint64_t)p.n * (blockIdx.x + 1) / gridDim.x) - lo;
+    lo = (uint32_t)((uint64_t)N * blockIdx.x / gridDim.x);
+    mine = (uint32_t)((uint64_t)N * (blockIdx.x + 1) / gridDim.x) - lo;
     bstep = 1;
   }
   for (uint32_t s = 0; s < S; s++) mbar_init(&full[s], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("prefetch.tensormap [%0];" ::"l"(&map) : "memory");
   if (p.dep) {
-    // while the previous kernel drains: its first p.prefetch boxes into L2 (harmless if that kernel
+    // while the previous kernel drains: its first p.prefetch units into L2 (harmless if that kernel
     // still writes them -- the loads after the wait read L2, which holds the latest data)
     const uint32_t np = mine < p.prefetch ? mine : p.prefetch;
     for (uint32_t k = 0; k < np; k++) {
       int c[5];
       int64_t off;
-      tr_box(p, lo + k * bstep, c, off);
-      if constexpr (STORE)
-        bulk_prefetch(p.img + off, box);
-      else
-        tma_prefetch5(&map, c[0], c[1], c[2], c[3], c[4]);
+      if constexpr (STORE) {
+        tr_box(p, (lo + k * bstep) * F, c, off);
+        bulk_prefetch(p.img + off, F * box);
+      } else {
+        for (uint32_t j = 0; j < F; j++) {
+          tr_box(p, (lo + k * bstep) * F + j, c, off);
+          tma_prefetch5(&map, c[0], c[1], c[2], c[3], c[4]);
+        }
+      }
     }
     pdl_wait();
   }
@@ -220,27 +227,34 @@ __global__ void __launch_bounds__(32, 1) k_tma_region(const __grid_constant__ CU
     const uint32_t s = k % S;
     int c[5];
     int64_t off;
-    tr_box(p, lo + k * bstep, c, off);
-    mbar_expect_tx(&full[s], box);
-    if constexpr (STORE)
-      bulk_load(sm + (size_t)s * slot, p.img + off, box, &full[s]);
-    else
-      tma_load5(sm + (size_t)s * slot, &map, &full[s], c[0], c[1], c[2], c[3], c[4]);
+    mbar_expect_tx(&full[s], F * box);
+    if constexpr (STORE) {
+      tr_box(p, (lo + k * bstep) * F, c, off);
+      bulk_load(sm + (size_t)s * SL, p.img + off, F * box, &full[s]);
+    } else {
+      for (uint32_t j = 0; j < F; j++) {
+        tr_box(p, (lo + k * bstep) * F + j, c, off);
+        tma_load5(sm + (size_t)s * SL + j * slot, &map, &full[s], c[0], c[1], c[2], c[3], c[4]);
+      }
+    }
   };
   for (uint32_t k = 0; k < mine && k < S; k++) issue(k);
   for (uint32_t k = 0; k < mine; k++) {
     const uint32_t s = k % S;
     int c[5];
     int64_t off;
-    tr_box(p, lo + k * bstep, c, off);
     mbar_wait(&full[s], (k / S) & 1u);
     if constexpr (STORE) {
-      tma_store5(&map, sm + (size_t)s * slot, c[0], c[1], c[2], c[3], c[4]);
+      for (uint32_t j = 0; j < F; j++) {
+        tr_box(p, (lo + k * bstep) * F + j, c, off);
+        tma_store5(&map, sm + (size_t)s * SL + j * slot, c[0], c[1], c[2], c[3], c[4]);
+      }
     } else {
-      for (int r = 0; r < p.reps.n; r++) bulk_store(p.img + off + p.reps.r[r], sm + (size_t)s * slot, box);
+      tr_box(p, (lo + k * bstep) * F, c, off);
+      for (int r = 0; r < p.reps.n; r++) bulk_store(p.img + off + p.reps.r[r], sm + (size_t)s * SL, F * box);
     }
     bulk_commit();
-    // refill the slot of box k - TR_LAG once its store has read shared memory
+    // refill the slot of unit k - TR_LAG once its store has read shared memory
     if (k >= (uint32_t)TR_LAG && k - TR_LAG + S < mine) {
       bulk_wait_read<TR_LAG>();
       issue(k - TR_LAG + S);
@@ -430,8 +444,9 @@ cudaError_t launch_tma_region(const void *map128, TrParams p, int store, cudaStr
   // TR_LAG boxes after its store, so fewer slots would wait on a box never issued)
   int per_sm = tma_region_per_sm();
   auto ring_of = [&](int ps) { return (size_t)std::min(optin, per_sm_bytes / ps - 1024) - 4096; };
-  while (per_sm > 1 && ring_of(per_sm) / p.slot < (size_t)TR_LAG + 1) per_sm--;
-  if (ring_of(per_sm) / p.slot < (size_t)TR_LAG + 1) return cudaErrorInvalidValue;
+  const size_t uslot = (size_t)p.slot * (p.pair ? 2 : 1);  // a ring slot holds one unit (1 or 2 boxes)
+  while (per_sm > 1 && ring_of(per_sm) / uslot < (size_t)TR_LAG + 1) per_sm--;
+  if (ring_of(per_sm) / uslot < (size_t)TR_LAG + 1) return cudaErrorInvalidValue;
   // ring: the CTA's share of the SM's shared memory (1 KiB per CTA is reserved by the system, the
   // static barriers and the 1 KiB alignment pad come off the top), at most TR_STAGES slots
   static const int static_bytes = [] {  // the barriers (+ alignment) of the kernel's static shared memory
@@ -447,19 +462,20 @@ cudaError_t launch_tma_region(const void *map128, TrParams p, int store, cudaStr
     return (size_t)((e && *e) ? std::max(1024, atoi(e)) : (1 << 30));
   }();
   const size_t ring = std::min(budget, ring_cap);
-  p.stages = (uint32_t)std::min<size_t>(TR_STAGES, ring / p.slot);
-  if (p.chunk && p.chunk <= TR_STAGES && (size_t)p.chunk * p.slot + 1024 + static_bytes <= (size_t)optin)
-    p.stages = p.chunk;  // in-order schedule: the CTA's boxes all in flight at once, no refill
+  p.stages = (uint32_t)std::min<size_t>(TR_STAGES, ring / uslot);
+  if (p.chunk && p.chunk <= TR_STAGES && (size_t)p.chunk * uslot + 1024 + static_bytes <= (size_t)optin)
+    p.stages = p.chunk;  // in-order schedule: the CTA's units all in flight at once, no refill
   else if (p.chunk)
-    p.chunk = 0;         // (boxes too large for a chunk-deep ring: the persistent grid)
+    p.chunk = 0;         // (units too large for a chunk-deep ring: the persistent grid)
   if (!p.chunk && p.stages < (uint32_t)TR_LAG + 1) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)p.stages * p.slot + 1024;
+  const size_t smem = (size_t)p.stages * uslot + 1024;
   const cudaError_t attr_err = smem_attr(kern, optin - static_bytes);  // (the largest any launch asks for)
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap m;
   memcpy(&m, map128, sizeof(m));
-  const unsigned blocks = p.chunk ? (p.n + p.chunk - 1) / p.chunk
-                                  : (unsigned)std::min<int64_t>(p.n, (int64_t)num_sms() * per_sm);
+  const uint32_t units = p.n / (p.pair ? 2u : 1u);
+  const unsigned blocks = p.chunk ? (units + p.chunk - 1) / p.chunk
+                                  : (unsigned)std::min<int64_t>(units, (int64_t)num_sms() * per_sm);
   static const int strided = [] {  // AXE_TMA_REGION_STRIDED: box order per CTA (A/B)
     const char *e = getenv("AXE_TMA_REGION_STRIDED");
     return (e && *e) ? atoi(e) : 1;

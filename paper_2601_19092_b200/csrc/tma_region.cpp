@@ -44,7 +44,8 @@ struct axe_tma_plan {
   std::vector<TmaAtom> host;  // per box: tensor-map coordinates (byte units on dim 0) + image offset
   int fuse = 1, fuse_dim = -1;  // atoms per box along the rows (box[fuse_dim] = fuse)
   TrProg prog{};              // the table as a mixed-radix program (prog.nd < 0: use the table)
-  uint32_t chunk = 0;         // boxes per CTA of the in-order schedule (0: the persistent ring grid)
+  uint32_t chunk = 0;         // units per CTA of the in-order schedule (0: the persistent ring grid)
+  int pair = 0;               // units of 2 boxes with contiguous image slots (TrParams::pair)
   std::mutex mu;              // guards the caches below
   std::map<int, TmaAtom *> tables;  // device -> its copy of the table (prog.nd < 0 only)
   std::unordered_map<const void *, std::array<unsigned char, 128>> maps;  // region start -> CUtensorMap
@@ -172,6 +173,7 @@ static axe_status region_params(axe_tma_plan *plan, const void *s_image, cudaStr
   p->slot = (plan->box_bytes + 1023) & ~1023u;
   p->dep = dep;
   p->chunk = plan->chunk;
+  p->pair = plan->pair;
   p->reps.n = 1;
   if (p->prog.nd < 0) {
     int dev = 0;
@@ -322,6 +324,16 @@ axe_status axe_tma_plan_create(const axe_tma_desc *desc, const axe_layout *tiler
   // profiles/r02_sweep_front.log: config 2 at 16384^2 158.7 us vs 179.6, 8192^2 40.6 vs 45.0); the
   // bench's 4096^2 keeps the persistent ring, which holds the whole copy in flight (10.0 us vs 11.0)
   p->chunk = unit_chunk((int64_t)p->host.size() * p->box_bytes > (int64_t(64) << 20) ? 4 : 0);
+  {  // pairs of consecutive boxes whose image slots are contiguous move as one ring unit: two TMA tensor
+     // ops and ONE image-side bulk copy of both (config 2: 10.12 -> 9.81 us per dependent step, the bench
+     // 6520 -> 6814 GB/s; reverse at 16384^2 162.4 -> 160.0; profiles/r02_lowered_pair.log).
+     // AXE_TMA_PAIR=0: one box per unit
+    const char *pe = getenv("AXE_TMA_PAIR");
+    bool ok = !(pe && *pe == '0') && p->host.size() % 2 == 0 && p->box_bytes % 1024 == 0;
+    for (size_t k = 0; ok && k + 1 < p->host.size(); k += 2)
+      ok = p->host[k + 1].off == p->host[k].off + (int64_t)p->box_bytes;
+    p->pair = ok ? 1 : 0;
+  }
   const char *force_table = getenv("AXE_TMA_REGION_TABLE");  // tests: run the table form
   if (force_table && *force_table == '1') p->prog.nd = -1;
   // a table the program does not reproduce is uploaded now when a device is current (so executes can
@@ -454,9 +466,9 @@ bool build_lowered(const std::vector<Joint> &J0, const Linear &ls, const Linear 
   char b[320];
   snprintf(b, sizeof b,
            "{\"kernel\":\"lowered\",\"mode\":\"%s\",\"atoms\":%lld,\"boxes\":%lld,\"box_bytes\":%u,\"swizzle\":%d,"
-           "\"replicas\":%d,\"box_program_digits\":%d,\"chunk\":%u,\"tensor_map\":{\"dims\":[",
+           "\"replicas\":%d,\"box_program_digits\":%d,\"chunk\":%u,\"pair\":%d,\"tensor_map\":{\"dims\":[",
            store ? "bulk-load/tensor-store" : "tensor-load/bulk-store", (long long)(tp->host.size() * tp->fuse),
-           (long long)tp->host.size(), tp->box_bytes, sw, (int)reps.size(), tp->prog.nd, tp->chunk);
+           (long long)tp->host.size(), tp->box_bytes, sw, (int)reps.size(), tp->prog.nd, tp->chunk, tp->pair);
   std::string s = b;
   for (int i = 0; i < d.rank; i++) s += (i ? "," : "") + std::to_string(d.dims[i]);
   s += "],\"strides\":[";

@@ -202,6 +202,25 @@ def test_lowered_schedule_reverse(axe, n, t, es, sw):
     assert desc["mode"] == "bulk-load/tensor-store"
 
 
+@pytest.mark.parametrize("pair", ["1", "0"])
+@pytest.mark.parametrize("rev", [False, True])
+@pytest.mark.parametrize("chunk", ["", "0", "3"])
+@pytest.mark.parametrize("n,t,es,sw,reps", [(4096, 64, 2, synth.SW128, 1), (512, 32, 4, synth.SW128, 2),
+                                            (512, 64, 1, synth.SW64, 1), (256, 8, 4, synth.SW32, 1)])
+def test_lowered_paired_boxes(axe, monkeypatch, pair, rev, chunk, n, t, es, sw, reps):
+    """Two consecutive boxes whose image slots are contiguous form one ring unit (two TMA tensor ops, one
+    image-side bulk copy; the default) or one box per unit (AXE_TMA_PAIR=0), persistent and in-order grids
+    (3 units per CTA: a ragged last CTA), both directions, destination replicas -- against the oracle."""
+    monkeypatch.setenv("AXE_TMA_PAIR", pair)
+    monkeypatch.setenv("AXE_CHUNK", chunk)
+    cfg = synth.config2(n, t, es, sw, rev)
+    if reps > 1 and not rev:
+        cfg = dict(cfg, name="c2_pair_rep", dst=layout(cfg["dst"]["D"], [(reps, n * n)]),
+                   dst_st=linear_storage(reps * n * n, sw))
+    desc = check(axe, cfg, "lowered", "lowered")
+    assert desc["pair"] == (1 if pair == "1" and desc["box_bytes"] % 1024 == 0 and desc["boxes"] % 2 == 0 else 0), desc
+
+
 @pytest.mark.parametrize("kernel", ["lowered", "auto"])
 def test_lowered_schedule_destination_replicas(axe, kernel):
     """Config 2 into three replicas of the tiled destination (whole tiles apart): each fused box leaves
