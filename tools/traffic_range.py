@@ -3,7 +3,7 @@
 ONE profiler range, so ncu measures the range as a whole -- dirty lines of earlier copies are evicted
 during later ones, as in the bench -- instead of one cold, cache-flushed launch.
 
-  ncu --replay-mode app-range --profile-from-start off --cache-control none \
+  ncu --replay-mode app-range --cache-control none \
       --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
       python tools/traffic_range.py [config] [N]
   (bytes per launch = range sum / N; tools/perf_configs.py names the configs)"""
