@@ -194,7 +194,7 @@ struct TrParams {
   int strided;           // 1: CTA c takes boxes c, c + grid, ... (0: a contiguous range per CTA)
   uint32_t prefetch;     // boxes per CTA pulled into L2 before griddepcontrol.wait
   uint32_t chunk;        // > 0: the in-order schedule, `chunk` consecutive units per CTA over a covering grid
-  int pair;              // 1: units of 2 boxes whose image slots are contiguous (one image-side bulk copy)
+  int pair;              // > 1: units of `pair` boxes whose image slots are contiguous (one image-side bulk copy)
   TmaReps reps;
 };
 

@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(32, 1) k_tma_region(const __grid_constant__ CU
   uint8_t *sm = (uint8_t *)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
   // a unit = F consecutive boxes whose image slots are contiguous (p.pair: F = 2, one bulk copy of 2 boxes
   // on the image side); a ring slot holds one unit
-  const uint32_t F = p.pair ? 2u : 1u;
+  const uint32_t F = p.pair > 1 ? (uint32_t)p.pair : 1u;
   const uint32_t S = p.stages, slot = p.slot, box = p.box, SL = F * slot, N = p.n / F;
   // units of this CTA: unit(k) = lo + k * bstep
   uint32_t lo, mine, bstep;
@@ -444,7 +444,7 @@ cudaError_t launch_tma_region(const void *map128, TrParams p, int store, cudaStr
   // TR_LAG boxes after its store, so fewer slots would wait on a box never issued)
   int per_sm = tma_region_per_sm();
   auto ring_of = [&](int ps) { return (size_t)std::min(optin, per_sm_bytes / ps - 1024) - 4096; };
-  const size_t uslot = (size_t)p.slot * (p.pair ? 2 : 1);  // a ring slot holds one unit (1 or 2 boxes)
+  const size_t uslot = (size_t)p.slot * (p.pair > 1 ? p.pair : 1);  // a ring slot holds one unit (1, 2 or 4 boxes)
   while (per_sm > 1 && ring_of(per_sm) / uslot < (size_t)TR_LAG + 1) per_sm--;
   if (ring_of(per_sm) / uslot < (size_t)TR_LAG + 1) return cudaErrorInvalidValue;
   // ring: the CTA's share of the SM's shared memory (1 KiB per CTA is reserved by the system, the
@@ -473,7 +473,7 @@ cudaError_t launch_tma_region(const void *map128, TrParams p, int store, cudaStr
   if (attr_err != cudaSuccess) return attr_err;
   CUtensorMap m;
   memcpy(&m, map128, sizeof(m));
-  const uint32_t units = p.n / (p.pair ? 2u : 1u);
+  const uint32_t units = p.n / (p.pair > 1 ? (uint32_t)p.pair : 1u);
   const unsigned blocks = p.chunk ? (units + p.chunk - 1) / p.chunk
                                   : (unsigned)std::min<int64_t>(units, (int64_t)num_sms() * per_sm);
   static const int strided = [] {  // AXE_TMA_REGION_STRIDED: box order per CTA (A/B)

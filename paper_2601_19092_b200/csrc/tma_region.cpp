@@ -329,10 +329,15 @@ axe_status axe_tma_plan_create(const axe_tma_desc *desc, const axe_layout *tiler
      // 6520 -> 6814 GB/s; reverse at 16384^2 162.4 -> 160.0; profiles/r02_lowered_pair.log).
      // AXE_TMA_PAIR=0: one box per unit
     const char *pe = getenv("AXE_TMA_PAIR");
-    bool ok = !(pe && *pe == '0') && p->host.size() % 2 == 0 && p->box_bytes % 1024 == 0;
-    for (size_t k = 0; ok && k + 1 < p->host.size(); k += 2)
-      ok = p->host[k + 1].off == p->host[k].off + (int64_t)p->box_bytes;
-    p->pair = ok ? 1 : 0;
+    const int want = (pe && *pe) ? atoi(pe) : 2;  // boxes per unit (0 / 1: one)
+    int f = want >= 4 ? 4 : want >= 2 ? 2 : 1;
+    for (; f > 1; f /= 2) {
+      bool ok = p->host.size() % f == 0 && p->box_bytes % 1024 == 0;
+      for (size_t k = 0; ok && k < p->host.size(); k += f)
+        for (int j = 1; ok && j < f; j++) ok = p->host[k + j].off == p->host[k].off + (int64_t)j * p->box_bytes;
+      if (ok) break;
+    }
+    p->pair = f > 1 ? f : 0;
   }
   const char *force_table = getenv("AXE_TMA_REGION_TABLE");  // tests: run the table form
   if (force_table && *force_table == '1') p->prog.nd = -1;
