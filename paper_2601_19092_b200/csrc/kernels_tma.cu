@@ -168,7 +168,12 @@ __global__ void __launch_bounds__(32) k1_tma(const __grid_constant__ CUtensorMap
 // box run in the async proxy, so no proxy fence is needed.  Box coordinates come from the fitted
 // mixed-radix program (no dependent global load before a TMA issue); the table is the fallback.
 constexpr int TR_STAGES = 32;  // ring capacity (slots per CTA)
-constexpr int TR_LAG = 2;      // a slot is refilled once the store two boxes back has read it
+#ifndef AXE_TR_LAG
+#define AXE_TR_LAG 1
+#endif
+// a slot is refilled once the store TR_LAG units back has read it (with 16 KiB two-box units, lag 1:
+// config 2 9.69 us vs 9.83 with lag 2 and 9.98 with 3; profiles/r02_lowered_pair.log)
+constexpr int TR_LAG = AXE_TR_LAG;
 
 template <bool STORE>
 __global__ void __launch_bounds__(32, 1) k_tma_region(const __grid_constant__ CUtensorMap map,
