@@ -274,7 +274,9 @@ struct K3Params {
 // n threads load n consecutive source vectors, transpose the granules with warp shuffles, and each
 // stores one 16-byte destination vector -- no shared memory.
 #ifndef AXE_K6_U
-#define AXE_K6_U 8  // measured on config 3a: U = 4: 1402 us, 8: 1358 us, 16: 1884 us (147 registers)
+// measured on config 3a: persistent grid U = 4: 1402 us, 8: 1358 us, 16: 1884 us (147 registers); with the
+// in-order schedule U = 4 (4 tiles per CTA) 1277 us vs U = 8 (8 tiles) 1308 us
+#define AXE_K6_U 4
 #endif
 constexpr int K6_U = AXE_K6_U;  // groups per thread per tile
 struct K6Params {

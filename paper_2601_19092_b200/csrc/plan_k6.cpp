@@ -157,9 +157,9 @@ bool build_k6(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   k.dsw = make_swz(dstst);
   P->align = 16;
   P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(k.ntiles, grid_cap(8)));
-  // in-order schedule, 8 tiles per CTA, when the tiles outnumber the persistent grid (config 3a:
-  // 1308 us vs 1364, profiles/r02_sweep_front.log)
-  k.chunk = unit_chunk(k.ntiles > (int64_t)P->blocks ? 8 : 0);
+  // in-order schedule, 4 tiles (of 4 groups per thread) per CTA, when the tiles outnumber the persistent
+  // grid (config 3a: 1277 us vs 1364 persistent, profiles/r02_sweep_front.log)
+  k.chunk = unit_chunk(k.ntiles > (int64_t)P->blocks ? 4 : 0);
   P->blocks = chunk_grid(k.ntiles, k.chunk, P->blocks);
   int64_t total = ng * n * n;  // granules
   P->covers_all = (int64_t)reps.size() * total * run == dstst.cells;
