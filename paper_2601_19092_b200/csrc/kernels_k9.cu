@@ -267,16 +267,27 @@ __global__ void __launch_bounds__(K9_THREADS) k9_vec(const __grid_constant__ K9P
     if (b0 + jb_s < p.eb) {
       const uint8_t *rb = rows + jb_s * K9V_ROW + moff[jb_s];
       const int64_t dl = dbo + (a0 + ia_s0) * p.d_a + (b0 + jb_s) * ES, dstep = CS * p.d_a;
+      if (!SWZ && p.nrep == 1 && a0 + TA <= p.ea) {
+        // the common case -- unswizzled, one destination, a tile of whole columns: one shared load and
+        // one store per element, the address a running pointer
+        uint8_t *q = dst + dl + p.rep[0];
 #pragma unroll
-      for (int u = 0; u < L; u++) {
-        const int ia = ia_s0 + u * CS;
-        if (a0 + ia < p.ea) {
-          // (m_jb is a multiple of es -- elements are es-aligned in the 16-byte aligned buffer -- and so is
-          // the row stride, so this read is es-aligned)
-          const T x = *reinterpret_cast<const T *>(rb + ia * ES);
-          const int64_t off = dl + u * dstep;
-          for (int rr = 0; rr < p.nrep; rr++)
-            *reinterpret_cast<T *>(dst + (SWZ ? swz(p.dsw, off + p.rep[rr]) : off + p.rep[rr])) = x;
+        for (int u = 0; u < L; u++) {
+          *reinterpret_cast<T *>(q) = *reinterpret_cast<const T *>(rb + (ia_s0 + u * CS) * ES);
+          q += dstep;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < L; u++) {
+          const int ia = ia_s0 + u * CS;
+          if (a0 + ia < p.ea) {
+            // (m_jb is a multiple of es -- elements are es-aligned in the 16-byte aligned buffer -- and so
+            // is the row stride, so this read is es-aligned)
+            const T x = *reinterpret_cast<const T *>(rb + ia * ES);
+            const int64_t off = dl + u * dstep;
+            for (int rr = 0; rr < p.nrep; rr++)
+              *reinterpret_cast<T *>(dst + (SWZ ? swz(p.dsw, off + p.rep[rr]) : off + p.rep[rr])) = x;
+          }
         }
       }
     }
