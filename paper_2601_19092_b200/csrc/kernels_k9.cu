@@ -38,6 +38,10 @@ template <>
 struct ElemT<16> { using T = uint4; };
 
 constexpr int K9_THREADS = 256;
+#ifndef AXE_K9_MINB
+#define AXE_K9_MINB 6
+#endif
+
 constexpr int K9_TB = 64;
 
 template <int ES>
@@ -153,8 +157,8 @@ template <int ES>
 __host__ __device__ constexpr int k9v_row() { return ES == 8 ? 152 : 148; }
 
 template <int ES, bool SWZ>
-__global__ void __launch_bounds__(K9_THREADS) k9_vec(const __grid_constant__ K9Params p,
-                                                     const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
+__device__ __forceinline__ void k9_vec_body(const K9Params &p, const uint8_t *__restrict__ src,
+                                            uint8_t *__restrict__ dst) {
   using T = typename ElemT<ES>::T;
   constexpr int TA = 128 / ES, TB = K9_TB;
   constexpr int CS = K9_THREADS / TB;          // store phase: columns per pass
@@ -295,9 +299,30 @@ __global__ void __launch_bounds__(K9_THREADS) k9_vec(const __grid_constant__ K9P
   }
 }
 
+// register budget: 2-8-byte elements capped for 6 CTAs per SM (4095 x 4097 bf16 18.1 us vs 30.1 with the
+// compiler's choice under a 1-CTA bound; fp32 30.0 vs 53.6); the 1-byte word form keeps the compiler's
+// default (91.0 us; capped at 2-5 CTAs 99-117)
+template <int ES, bool SWZ>
+__global__ void __launch_bounds__(K9_THREADS, AXE_K9_MINB) k9_vec(const __grid_constant__ K9Params p,
+                                                                 const uint8_t *__restrict__ src,
+                                                                 uint8_t *__restrict__ dst) {
+  k9_vec_body<ES, SWZ>(p, src, dst);
+}
+template <bool SWZ>
+__global__ void __launch_bounds__(K9_THREADS) k9_vec_u8(const __grid_constant__ K9Params p,
+                                                        const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
+  k9_vec_body<1, SWZ>(p, src, dst);
+}
+
 template <int ES>
 cudaError_t go(const K9Params &p, const uint8_t *s, uint8_t *d, cudaStream_t st) {
   const bool sw = p.ssw.mask || p.dsw.mask;
+  if (p.vec && ES == 1) {
+    const void *kern = sw ? (const void *)k9_vec_u8<true> : (const void *)k9_vec_u8<false>;
+    const unsigned blocks = p.chunk ? (p.ntiles + p.chunk - 1) / p.chunk : one_wave(kern, K9_THREADS, 0, std::max(1u, p.ntiles));
+    return sw ? launch_ex(k9_vec_u8<true>, dim3(blocks), dim3(K9_THREADS), 0, st, p, s, d)
+              : launch_ex(k9_vec_u8<false>, dim3(blocks), dim3(K9_THREADS), 0, st, p, s, d);
+  }
   if (p.vec && ES <= 8) {
     const void *kern = sw ? (const void *)k9_vec<ES, true> : (const void *)k9_vec<ES, false>;
     const unsigned blocks = p.chunk ? (p.ntiles + p.chunk - 1) / p.chunk : one_wave(kern, K9_THREADS, 0, std::max(1u, p.ntiles));
