@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(K1_THREADS) k8_dual(const __grid_constant__ K8
 // (fast divisions) -- so consecutive lanes move consecutive x (coalesced wherever a side's innermost
 // digit is contiguous), and an element costs a compare and two adds per side instead of two full
 // decodings.  8 loads in flight per lane before their stores.
-template <int ES>
+template <int ES, bool SWZ>
 __global__ void __launch_bounds__(K1_THREADS) k8_odo(const __grid_constant__ K8Params p, const uint8_t *__restrict__ src,
                                                      uint8_t *__restrict__ dst) {
   using T = typename VecT<ES>::T;
@@ -407,7 +407,8 @@ __global__ void __launch_bounds__(K1_THREADS) k8_odo(const __grid_constant__ K8P
 #pragma unroll
       for (int u = 0; u < U; u++) {
         if (x < xend) {
-          v[u] = ld_stream<ES>(src + swz(p.ssw, oa + (int64_t)ra * sA));
+          const int64_t so = oa + (int64_t)ra * sA;
+          v[u] = ld_stream<ES>(src + (SWZ ? swz(p.ssw, so) : so));
           d[u] = ob + (int64_t)rb * sB;
         }
         x += 32;
@@ -424,11 +425,18 @@ __global__ void __launch_bounds__(K1_THREADS) k8_odo(const __grid_constant__ K8P
           ob = p.dbase + k8_digits<K8_MAXD>(p.nb - 1, p.bfd, p.bs, qb);
         }
       }
+      if (!SWZ && p.nrep == 1) {  // (the common case: no swizzle, one destination -- no replica loop)
+        const int64_t r0 = p.rep[0];
 #pragma unroll
-      for (int u = 0; u < U; u++) {
-        const uint32_t xu = x - (uint32_t)(U - u) * 32;
-        if (xu < xend)
-          for (int r = 0; r < p.nrep; r++) st_vec<ES>(dst + swz(p.dsw, d[u] + p.rep[r]), v[u]);
+        for (int u = 0; u < U; u++)
+          if (x - (uint32_t)(U - u) * 32 < xend) st_vec<ES>(dst + d[u] + r0, v[u]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const uint32_t xu = x - (uint32_t)(U - u) * 32;
+          if (xu < xend)
+            for (int r = 0; r < p.nrep; r++) st_vec<ES>(dst + (SWZ ? swz(p.dsw, d[u] + p.rep[r]) : d[u] + p.rep[r]), v[u]);
+        }
       }
     }
   }
@@ -457,12 +465,13 @@ cudaError_t launch_k8(const K8Params &p, int vb, const void *src, void *dst, cud
           p.chunk ? (want + p.chunk - 1) / p.chunk : one_wave((const void *)kern, K1_THREADS, 0, std::max(1u, want));
       return launch_ex(kern, dim3(blocks), dim3(K1_THREADS), 0, st, p, s, d);
     };
+    const bool sw = p.ssw.mask || p.dsw.mask;
     switch (vb) {
-      case 1: e = go(k8_odo<1>); break;
-      case 2: e = go(k8_odo<2>); break;
-      case 4: e = go(k8_odo<4>); break;
-      case 8: e = go(k8_odo<8>); break;
-      case 16: e = go(k8_odo<16>); break;
+      case 1: e = sw ? go(k8_odo<1, true>) : go(k8_odo<1, false>); break;
+      case 2: e = sw ? go(k8_odo<2, true>) : go(k8_odo<2, false>); break;
+      case 4: e = sw ? go(k8_odo<4, true>) : go(k8_odo<4, false>); break;
+      case 8: e = sw ? go(k8_odo<8, true>) : go(k8_odo<8, false>); break;
+      case 16: e = sw ? go(k8_odo<16, true>) : go(k8_odo<16, false>); break;
       default: return cudaErrorInvalidValue;
     }
     if (e != cudaSuccess) return e;
