@@ -289,9 +289,11 @@ __device__ __forceinline__ int64_t k8_digits(int n, const FastDiv *fd, const int
   return off;
 }
 
-template <int VB, int U>
+template <int VB, int U, bool SWZ>
 __global__ void __launch_bounds__(K1_THREADS) k8_dual(const __grid_constant__ K8Params p, const uint8_t *__restrict__ src,
                                                       uint8_t *__restrict__ dst) {
+  auto ssw = [&](int64_t b) { return SWZ ? swz(p.ssw, b) : b; };  // (SWZ = false: no swizzle on either side)
+  auto dsw = [&](int64_t b) { return SWZ ? swz(p.dsw, b) : b; };
   using T = typename VecT<VB>::T;
   if (p.dep && !p.chunked) pdl_wait();
   if (p.chunked) {
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(K1_THREADS) k8_dual(const __grid_constant__ K8
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const uint32_t w = c * CH + u * K1_THREADS + threadIdx.x;
-        if (w < vin && (w * VB) % 128 < VB) prefetch_l2(src + swz(p.ssw, so + (int64_t)w * p.iss[0]));
+        if (w < vin && (w * VB) % 128 < VB) prefetch_l2(src + ssw(so + (int64_t)w * p.iss[0]));
       }
     }
     if (p.dep) pdl_wait();
@@ -321,13 +323,13 @@ __global__ void __launch_bounds__(K1_THREADS) k8_dual(const __grid_constant__ K8
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const uint32_t w = c * CH + u * K1_THREADS + threadIdx.x;
-        if (w < vin) v[u] = ld_stream<VB>(src + swz(p.ssw, so + (int64_t)w * p.iss[0]));
+        if (w < vin) v[u] = ld_stream<VB>(src + ssw(so + (int64_t)w * p.iss[0]));
       }
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const uint32_t w = c * CH + u * K1_THREADS + threadIdx.x;
         if (w < vin)
-          for (int r = 0; r < p.nrep; r++) st_vec<VB>(dst + swz(p.dsw, d + (int64_t)w * p.ids[0] + p.rep[r]), v[u]);
+          for (int r = 0; r < p.nrep; r++) st_vec<VB>(dst + dsw(d + (int64_t)w * p.ids[0] + p.rep[r]), v[u]);
       }
     }
     return;
@@ -361,7 +363,7 @@ __global__ void __launch_bounds__(K1_THREADS) k8_dual(const __grid_constant__ K8
         }
         so += k8_digits<K8_MAXD>(p.na, p.afd, p.as, o);
         d += k8_digits<K8_MAXD>(p.nb, p.bfd, p.bs, o);
-        v[u] = ld_stream<VB>(src + swz(p.ssw, so));
+        v[u] = ld_stream<VB>(src + ssw(so));
         dof[u] = d;
       }
     }
@@ -369,7 +371,7 @@ __global__ void __launch_bounds__(K1_THREADS) k8_dual(const __grid_constant__ K8
     for (int u = 0; u < U; u++) {
       const uint32_t i = base + u * K1_THREADS;
       if (i < total)
-        for (int r = 0; r < p.nrep; r++) st_vec<VB>(dst + swz(p.dsw, dof[u] + p.rep[r]), v[u]);
+        for (int r = 0; r < p.nrep; r++) st_vec<VB>(dst + dsw(dof[u] + p.rep[r]), v[u]);
     }
   }
 }
@@ -445,11 +447,13 @@ __global__ void __launch_bounds__(K1_THREADS) k8_odo(const __grid_constant__ K8P
 template <int VB>
 static cudaError_t k8_launch(const K8Params &p, const uint8_t *s, uint8_t *d, cudaStream_t st) {
   constexpr int U = VB >= 8 ? 4 : 8;
-  const void *kern = (const void *)k8_dual<VB, U>;
+  const bool sw = p.ssw.mask || p.dsw.mask;
+  const void *kern = sw ? (const void *)k8_dual<VB, U, true> : (const void *)k8_dual<VB, U, false>;
   const unsigned want = p.chunked ? p.nitems
                                   : (unsigned)((p.total + (uint64_t)K1_THREADS * U - 1) / ((uint64_t)K1_THREADS * U));
   const unsigned blocks = p.chunk ? (want + p.chunk - 1) / p.chunk : one_wave(kern, K1_THREADS, 0, std::max(1u, want));
-  return launch_ex(k8_dual<VB, U>, dim3(blocks), dim3(K1_THREADS), 0, st, p, s, d);
+  return sw ? launch_ex(k8_dual<VB, U, true>, dim3(blocks), dim3(K1_THREADS), 0, st, p, s, d)
+            : launch_ex(k8_dual<VB, U, false>, dim3(blocks), dim3(K1_THREADS), 0, st, p, s, d);
 }
 
 int k8_chunk(int vb) { return K1_THREADS * (vb >= 8 ? 4 : 8); }
