@@ -150,14 +150,13 @@ bool build_k7(const std::vector<Joint> &J0, const Linear &ls, const Linear &ld, 
   const int64_t tile_bytes = TR * TC * es * (k.async ? k.async : 1);
   const int per_sm = (int)std::max<int64_t>(1, std::min<int64_t>(8, (220 * 1024) / (tile_bytes + 1024)));
   P->blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt, grid_cap(per_sm)));
-  // from 64 MiB a side (256 MiB with one CTA per SM), the in-order schedule: 2 tiles per CTA, 4 when one
+  // from 64 MiB a side (256 MiB with one CTA per SM), the in-order schedule: 1 tile per CTA, 4 when one
   // CTA fills the SM and its own ring is the only overlap (profiles/r02_sweep_front.log: 256 MiB fp32
-  // 82.0 us vs 92.4, bf16 88.0 vs 97.8; at 32 MiB the persistent grid wins, 10.5 vs 11.4, and so does
-  // bf16 at 128 MiB, 43.8 vs 48.1)
+  // 82.0 us vs 92.4 persistent with 2 tiles per CTA, 80.4 with 1 in source-major order; bf16 one CTA per
+  // SM 88.0 vs 97.8; at 32 MiB the persistent grid wins, 10.5 vs 11.4, and so does one-CTA bf16 at
+  // 128 MiB, 43.8 vs 48.1)
   const int64_t bytes = nt * TR * TC * es;
   const bool front = per_sm >= 2 ? bytes >= (int64_t(64) << 20) : bytes >= (int64_t(256) << 20);
-  // (1 tile per CTA with source-major tile order: 256 MiB fp32 80.4 us vs 81.0 with 2, fp64 84.1 vs 85.2,
-  // bf16 equal; profiles/r02_sweep_front.log)
   k.chunk = unit_chunk(front && nt > (int64_t)P->blocks ? (per_sm >= 2 ? 1 : 4) : 0);
   P->blocks = chunk_grid(nt, k.chunk, P->blocks);
   const char *mc = getenv("AXE_K7_MAX_CTAS");  // tests: several tiles per CTA on small inputs
