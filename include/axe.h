@@ -263,8 +263,9 @@ enum {
   AXE_KERNEL_TRANSPOSE = 8, /* K7: smem tile + n x n register-block transpose (2-D transposes)  */
   AXE_KERNEL_LOWERED = 9,   /* the paper's TMA lowering (axe_tma_lower) as a copy schedule: the
                                destination is a tiling of the swizzle atom over the joint digits,
-                               one TMA load + bulk store per (fused) atom box; AUTO takes it for
-                               copies into / out of TMA-swizzled storage (config 2)               */
+                               one TMA tensor op per (fused) atom box, one bulk copy per pair of
+                               boxes contiguous in the image; AUTO takes it for copies into / out
+                               of TMA-swizzled storage (config 2)                                 */
   AXE_KERNEL_DUAL = 10      /* K8: non-nested digit systems: the shared innermost run is
                                vectorised, the outer index decoded once per side                  */
 };
