@@ -94,7 +94,7 @@ __device__ __forceinline__ void k6_decode(int n, const FastDiv *fd, const int64_
   }
 }
 
-template <int N>
+template <int N, bool SWZ>
 __global__ void __launch_bounds__(K6_THREADS) k6_transpose(const __grid_constant__ K6Params p,
                                                            const uint8_t *__restrict__ src, uint8_t *__restrict__ dst) {
   const int j = threadIdx.x % N;
@@ -115,11 +115,16 @@ __global__ void __launch_bounds__(K6_THREADS) k6_transpose(const __grid_constant
     k6_decode(p.nout, p.ofd, p.oss, p.ods, t, sb, db);
     uint4 w[K6_U];
 #pragma unroll
-    for (int u = 0; u < K6_U; u++) w[u] = ldg128(src + swz(p.ssw, sb + so[u]));
+    for (int u = 0; u < K6_U; u++) w[u] = ldg128(src + (SWZ ? swz(p.ssw, sb + so[u]) : sb + so[u]));
 #pragma unroll
     for (int u = 0; u < K6_U; u++) {
       const uint4 v = N == 4 ? transpose4(w[u], j) : transpose2(w[u], j);
-      for (int r = 0; r < p.nrep; r++) *reinterpret_cast<uint4 *>(dst + swz(p.dsw, db + dof[u] + p.rep[r])) = v;
+      if (!SWZ && p.nrep == 1) {
+        *reinterpret_cast<uint4 *>(dst + db + dof[u] + p.rep[0]) = v;
+      } else {
+        for (int r = 0; r < p.nrep; r++)
+          *reinterpret_cast<uint4 *>(dst + (SWZ ? swz(p.dsw, db + dof[u] + p.rep[r]) : db + dof[u] + p.rep[r])) = v;
+      }
     }
   }
 }
@@ -129,8 +134,11 @@ __global__ void __launch_bounds__(K6_THREADS) k6_transpose(const __grid_constant
 cudaError_t launch_k6(const K6Params &p, unsigned blocks, const void *src, void *dst, cudaStream_t st) {
   const uint8_t *s = (const uint8_t *)src;
   uint8_t *d = (uint8_t *)dst;
-  cudaError_t e = p.n == 4 ? launch_ex(k6_transpose<4>, dim3(blocks), dim3(K6_THREADS), 0, st, p, s, d)
-                           : launch_ex(k6_transpose<2>, dim3(blocks), dim3(K6_THREADS), 0, st, p, s, d);
+  const bool sw = p.ssw.mask || p.dsw.mask;  // (unswizzled: no swizzle arithmetic per vector)
+  cudaError_t e = p.n == 4 ? (sw ? launch_ex(k6_transpose<4, true>, dim3(blocks), dim3(K6_THREADS), 0, st, p, s, d)
+                                 : launch_ex(k6_transpose<4, false>, dim3(blocks), dim3(K6_THREADS), 0, st, p, s, d))
+                           : (sw ? launch_ex(k6_transpose<2, true>, dim3(blocks), dim3(K6_THREADS), 0, st, p, s, d)
+                                 : launch_ex(k6_transpose<2, false>, dim3(blocks), dim3(K6_THREADS), 0, st, p, s, d));
   if (e != cudaSuccess) return e;
   g_launches++;
   return cudaGetLastError();
